@@ -1,0 +1,129 @@
+/*
+ * pcirc_b200.h — C ABI of the B200-native block-sparse probabilistic-circuit
+ * hot path (forward / backward / EM of arXiv 2406.00766, PyJuice).
+ *
+ * Plain pointers and sizes only; no torch types.  Every pointer named d_* is
+ * device memory on the current CUDA device; `stream` is a cudaStream_t cast to
+ * void* (0 = legacy default stream).  All launches are asynchronous on that
+ * stream; nothing allocates except pcb_plan_create.  Functions return a status:
+ *
+ *   PCB_OK 0, PCB_USAGE 1 (UsageError), PCB_FORMAT 2 (FormatError),
+ *   PCB_NUMERIC 3 (NumericError), PCB_CUDA 4 (launch / runtime failure)
+ *
+ * mapped by the Python shim onto the reference's exception classes
+ * (pcirc/errors.py:8-40).
+ *
+ * The reference has no native boundary: its hot path is Python/numpy
+ * (pcirc/runtime/engine.py, pcirc/runtime/em.py).  Each entry point below
+ * replaces the reference function cited beside it; a maintainer binds them
+ * with ctypes.
+ *
+ * Buffer layout (the reference's, pcirc/runtime/buffers.py:18-57): node-major,
+ * batch-contiguous fp32 matrices with row stride `ldb` (>= B, multiple of 32):
+ *   values, flows        [num_value_slots x ldb]
+ *   scratch, flow_scratch [scratch_size   x ldb]
+ *   prod_flows           [num_prod_rows   x ldb]
+ *   f_params             [f_params_size]        (theta_size prefix + replicas)
+ *   theta                [theta_size]
+ *   xT                   [num_vars x ldb] int32, category or -1 (missing)
+ * Sample columns b >= B are padding and never contribute to parameter flows.
+ */
+#ifndef PCIRC_B200_H
+#define PCIRC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCB_OK 0
+#define PCB_USAGE 1
+#define PCB_FORMAT 2
+#define PCB_NUMERIC 3
+#define PCB_CUDA 4
+
+#define PCB_ABI_VERSION 1
+
+typedef struct pcb_plan pcb_plan;
+
+/* ABI version of the loaded library. */
+int pcb_abi_version(void);
+
+/* Build an immutable execution plan.
+ *   prog/prog_len : host int64 program (layer / group records with offsets into
+ *                   d_blob), written by paper_2406_00766_b200/runtime/plan.py.
+ *   d_blob        : device int32 index tables (compiled layout narrowed to int32).
+ * Replaces: pcirc/compiler/ir.py:131-200 (CompiledCircuit consumed by engine.py). */
+int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob,
+                    int64_t blob_len, pcb_plan** out);
+int pcb_plan_destroy(pcb_plan* plan);
+
+/* Number of sum layers in the plan. */
+int pcb_plan_num_layers(const pcb_plan* plan);
+
+/* Validate a device batch (xT, [num_vars x ldb]) against the category counts:
+ * writes the number of bad entries to *d_bad (device int32).
+ * Replaces: pcirc/runtime/engine.py:36-52 (_validate_batch) for device batches. */
+int pcb_check_batch(const pcb_plan* plan, void* stream, int B, int ldb,
+                    const int32_t* d_xT, int32_t* d_bad);
+
+/* Transpose a row-major [B x num_vars] int64/int32 batch into xT [num_vars x ldb]. */
+int pcb_transpose_batch_i64(const pcb_plan* plan, void* stream, int B, int ldb,
+                            const int64_t* d_x, int32_t* d_xT);
+int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
+                            const int32_t* d_x, int32_t* d_xT);
+
+/* Full forward pass: values, scratch, lroot[B].
+ * Replaces: pcirc/runtime/engine.py:186-217 (forward). */
+int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb,
+                const int32_t* d_xT, const float* d_theta, float* d_values,
+                float* d_scratch, float* d_lroot);
+
+/* Full backward pass (flows, prod_flows, f_params incl. replica reduction).
+ * Replaces: pcirc/runtime/engine.py:220-259 (backward). */
+int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb,
+                 const int32_t* d_xT, const float* d_theta, const float* d_values,
+                 float* d_flows, float* d_scratch, float* d_flow_scratch,
+                 float* d_prod_flows, float* d_f_params);
+
+/* Per-layer operator API (the reference's private kernels that
+ * pcirc/bench.py:22-27 imports): product evaluation + sum forward of layer
+ * `layer` (engine.py:68-102), and its backward (engine.py:105-165 + :249-254). */
+int pcb_layer_forward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
+                      const float* d_theta, float* d_values, float* d_scratch);
+int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
+                       const float* d_theta, const float* d_values, float* d_flows,
+                       float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
+                       float* d_f_params);
+
+/* EM over the simplex groups, in place on d_theta:
+ *   theta[g] <- (1 - step) * theta[g] + step * (F[g] + k) / sum(F[g] + k)
+ * for every group whose total is > 0 (others keep theta).  step = 1 gives the
+ * full-batch renormalisation.  d_status (device int32[2]) receives
+ * [informative group count, non-finite result count].
+ * Replaces: pcirc/runtime/em.py:58-94 (em_step_full, em_step_mini, apply_theta). */
+int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params,
+                  float* d_theta, float pseudocount, float step_size, int32_t* d_status);
+
+/* f[i] += g[i] over n floats (EMAccumulator merge, pcirc/runtime/em.py:48-55). */
+int pcb_axpy_accumulate(void* stream, int64_t n, const float* d_src, float* d_dst);
+
+/* Non-finite count of a float vector into *d_count (device int32).
+ * Replaces the theta check of pcirc/runtime/engine.py:197-198. */
+int pcb_count_nonfinite(void* stream, int64_t n, const float* d_x, int32_t* d_count);
+
+/* Per-kernel-class launch counter (for the bench's gpu_launches claim). */
+int64_t pcb_launch_count(void);
+
+/* tcgen05 self-test: D[128 x n] = A[128 x k] . B[n x k]^T in bf16 with fp32
+ * accumulation on one CTA (n in {16..256, step 16}, k multiple of 16 <= 256).
+ * Used by tests to pin the UMMA descriptor encoding. */
+int pcb_tc_selftest(void* stream, int n, int k, const uint16_t* d_a, const uint16_t* d_b,
+                    float* d_d);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PCIRC_B200_H */

@@ -1,0 +1,370 @@
+// C ABI: plan parsing and the forward / backward / EM orchestration
+// (pcirc/runtime/engine.py:186-259, pcirc/runtime/em.py:58-94).
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+
+#include "pcb_internal.cuh"
+
+using namespace pcb;
+
+namespace {
+
+constexpr int64_t kMagic = 0x50434232;  // "PCB2"
+constexpr int64_t kVersion = 2;
+
+struct Reader {
+  const int64_t* p;
+  int64_t n, i = 0;
+  const int32_t* blob;
+  int64_t blob_len;
+  bool ok = true;
+  int64_t get() {
+    if (i >= n) {
+      ok = false;
+      return 0;
+    }
+    return p[i++];
+  }
+  const int32_t* ref(int64_t* count = nullptr) {
+    int64_t off = get(), cnt = get();
+    if (count) *count = cnt;
+    if (off < 0 || cnt < 0 || off + cnt > blob_len) {
+      ok = false;
+      return nullptr;
+    }
+    return blob + off;
+  }
+};
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int pcb_abi_version(void) { return PCB_ABI_VERSION; }
+
+int64_t pcb_launch_count(void) { return (int64_t)g_launches; }
+
+int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob,
+                    int64_t blob_len, pcb_plan** out) {
+  if (!prog || !out) return PCB_USAGE;
+  Reader r{prog, prog_len};
+  r.blob = d_blob;
+  r.blob_len = blob_len;
+  if (r.get() != kMagic || r.get() != kVersion) return PCB_USAGE;
+  pcb_plan* P = new (std::nothrow) pcb_plan();
+  if (!P) return PCB_USAGE;
+  P->num_vars = r.get();
+  P->num_value_slots = r.get();
+  P->scratch_size = r.get();
+  P->num_prod_rows = r.get();
+  P->theta_size = r.get();
+  P->f_params_size = r.get();
+  P->reserved = r.get();
+  P->root_slot = r.get();
+  P->root_row = r.get();
+  P->root_children = r.ref(&P->n_root_children);
+  P->var_ncat = r.ref();
+  P->use_tc = (int)r.get();
+  int64_t n_chunks = r.get();
+  for (int64_t c = 0; c < n_chunks && r.ok; ++c) {
+    InputChunk ch;
+    ch.ncat = r.get();
+    ch.n = r.get();
+    ch.slots = r.ref();
+    ch.vars = r.ref();
+    ch.pids = r.ref();
+    P->inputs.push_back(ch);
+  }
+  int64_t n_layers = r.get();
+  for (int64_t l = 0; l < n_layers && r.ok; ++l) {
+    Layer L;
+    L.k_m = r.get();
+    L.k_n = r.get();
+    L.window = r.get();
+    L.n_prod = r.get();
+    L.pad_rows = r.ref(&L.n_pad);
+    int64_t ne = r.get();
+    for (int64_t e = 0; e < ne && r.ok; ++e) {
+      Bucket b;
+      b.f = r.get();
+      b.n = r.get();
+      b.idx = r.ref();
+      b.children = r.ref();
+      L.evals.push_back(b);
+    }
+    int64_t nf = r.get();
+    for (int64_t g = 0; g < nf && r.ok; ++g) {
+      FwdGroup G;
+      G.rows = r.get();
+      G.cap = r.get();
+      G.sum_ids = r.ref();
+      G.prod_ids = r.ref();
+      G.param_ids = r.ref();
+      G.flow_ids = r.ref();
+      TcRows T;
+      T.count = r.get();
+      T.row_off = r.ref();
+      T.members = r.ref();
+      L.fwd.push_back(G);
+      L.fwd_tc.push_back(T);
+    }
+    int64_t nb = r.get();
+    for (int64_t g = 0; g < nb && r.ok; ++g) {
+      BwdGroup G;
+      G.rows = r.get();
+      G.cap = r.get();
+      G.ch_ids = r.ref();
+      G.par_ids = r.ref();
+      G.par_param_ids = r.ref();
+      TcRows T;
+      T.count = r.get();
+      T.row_off = r.ref();
+      T.members = r.ref();
+      L.bwd.push_back(G);
+      L.bwd_tc.push_back(T);
+    }
+    L.prod_slots = r.ref();
+    L.prod_rows = r.ref();
+    int64_t np = r.get();
+    for (int64_t e = 0; e < np && r.ok; ++e) {
+      Bucket b;
+      b.f = r.get();
+      b.n = r.get();
+      b.idx = r.ref();
+      b.children = r.ref();
+      L.pushes.push_back(b);
+    }
+    P->layers.push_back(std::move(L));
+  }
+  P->red_n = r.get();
+  P->red_dst = r.ref();
+  P->red_len = r.ref();
+  P->red_src_off = r.ref();
+  P->red_src = r.ref();
+  P->n_groups = r.get();
+  P->group_idx = r.ref();
+  P->group_off = r.ref();
+  if (!r.ok || r.get() != kMagic) {
+    delete P;
+    return PCB_USAGE;
+  }
+  *out = P;
+  return PCB_OK;
+}
+
+int pcb_plan_destroy(pcb_plan* plan) {
+  delete plan;
+  return PCB_OK;
+}
+
+int pcb_plan_num_layers(const pcb_plan* plan) { return plan ? (int)plan->layers.size() : -1; }
+
+}  // extern "C"
+
+namespace {
+
+__global__ void k_check_batch(int64_t nv, int B, int ldb, const int32_t* __restrict__ ncat,
+                              const int32_t* __restrict__ xT, int32_t* bad) {
+  int64_t total = nv * (int64_t)B;
+  int cnt = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = t / B;
+    int b = (int)(t - v * B);
+    int x = xT[v * ldb + b];
+    if (x < -1 || x >= ncat[v]) ++cnt;
+  }
+  if (cnt) atomicAdd(bad, cnt);
+}
+
+template <typename T>
+__global__ void k_transpose(int64_t nv, int B, int ldb, const T* __restrict__ x,
+                            int32_t* __restrict__ xT) {
+  __shared__ int32_t tile[32][33];
+  const int64_t v0 = (int64_t)blockIdx.x * 32;
+  const int b0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    int b = b0 + k;
+    int64_t v = v0 + threadIdx.x;
+    if (b < B && v < nv) tile[k][threadIdx.x] = (int32_t)x[(int64_t)b * nv + v];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    int64_t v = v0 + k;
+    int b = b0 + threadIdx.x;
+    if (b < B && v < nv) xT[v * ldb + b] = tile[threadIdx.x][k];
+  }
+}
+
+__global__ void k_axpy(int64_t n, const float* __restrict__ a, float* __restrict__ y) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    y[t] += a[t];
+}
+
+__global__ void k_nonfinite(int64_t n, const float* __restrict__ x, int32_t* cnt) {
+  int c = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    c += !isfinite(x[t]);
+  if (c) atomicAdd(cnt, c);
+}
+
+int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
+                  const float* theta, float* values, float* scratch) {
+  int st = launch_prod_eval(L, s, B, ldb, values, scratch);
+  if (st) return st;
+  for (size_t g = 0; g < L.fwd.size(); ++g) {
+    const TcRows& T = L.fwd_tc[g];
+    if (P->use_tc && T.count > 0 && tc_supported(L))
+      st = launch_sum_fwd_tc(L, L.fwd[g], T, s, B, ldb, theta, scratch, values);
+    else
+      st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, values);
+    if (st) return st;
+  }
+  return PCB_OK;
+}
+
+int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
+                   const float* theta, const float* values, float* flows, float* scratch,
+                   float* flow_scratch, float* prod_flows, float* f_params) {
+  int st = launch_prod_eval(L, s, B, ldb, values, scratch);  // recompute
+  if (st) return st;
+  for (auto& g : L.fwd) {
+    st = launch_param_flow_simt(L, g, s, B, ldb, theta, values, flows, scratch, f_params);
+    if (st) return st;
+  }
+  for (auto& g : L.bwd) {
+    st = launch_child_flow_simt(L, g, s, B, ldb, theta, values, flows, scratch, flow_scratch);
+    if (st) return st;
+  }
+  return launch_prod_accum_push(L, s, B, ldb, flow_scratch, prod_flows, flows);
+}
+
+bool bad_dims(const pcb_plan* p, int B, int ldb) {
+  return !p || B < 0 || ldb < B || (ldb % 4) != 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcb_check_batch(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
+                    int32_t* d_bad) {
+  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+  if (!B) return PCB_OK;
+  k_check_batch<<<grid_for(plan->num_vars * B, 256), 256, 0, as_stream(stream)>>>(
+      plan->num_vars, B, ldb, plan->var_ncat, d_xT, d_bad);
+  return check_launch();
+}
+
+int pcb_transpose_batch_i64(const pcb_plan* plan, void* stream, int B, int ldb,
+                            const int64_t* d_x, int32_t* d_xT) {
+  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+  if (!B) return PCB_OK;
+  dim3 grid((unsigned)((plan->num_vars + 31) / 32), (unsigned)((B + 31) / 32));
+  k_transpose<int64_t><<<grid, dim3(32, 8), 0, as_stream(stream)>>>(plan->num_vars, B, ldb, d_x,
+                                                                     d_xT);
+  return check_launch();
+}
+
+int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
+                            const int32_t* d_x, int32_t* d_xT) {
+  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+  if (!B) return PCB_OK;
+  dim3 grid((unsigned)((plan->num_vars + 31) / 32), (unsigned)((B + 31) / 32));
+  k_transpose<int32_t><<<grid, dim3(32, 8), 0, as_stream(stream)>>>(plan->num_vars, B, ldb, d_x,
+                                                                     d_xT);
+  return check_launch();
+}
+
+int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
+                const float* d_theta, float* d_values, float* d_scratch, float* d_lroot) {
+  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+  if (!B) return PCB_OK;
+  cudaStream_t s = as_stream(stream);
+  // values.fill(-inf) (engine.py:204): every input and sum-block row (padding
+  // rows included) is written below, so only the reserved constant rows need it.
+  int st = launch_fill_range(s, 0, plan->reserved, B, ldb, d_values, PCB_NEG_INF);
+  if (st) return st;
+  st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values);
+  if (st) return st;
+  for (auto& L : plan->layers) {
+    st = layer_forward(plan, L, s, B, ldb, d_theta, d_values, d_scratch);
+    if (st) return st;
+  }
+  return launch_root_fwd(plan, s, B, ldb, d_values, d_lroot);
+}
+
+int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
+                 const float* d_theta, const float* d_values, float* d_flows, float* d_scratch,
+                 float* d_flow_scratch, float* d_prod_flows, float* d_f_params) {
+  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * plan->f_params_size, s) != cudaSuccess)
+    return PCB_CUDA;
+  if (!B) return PCB_OK;
+  if (cudaMemsetAsync(d_flows, 0, sizeof(float) * plan->num_value_slots * ldb, s) != cudaSuccess)
+    return PCB_CUDA;
+  if (plan->num_prod_rows &&
+      cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * plan->num_prod_rows * ldb, s) !=
+          cudaSuccess)
+    return PCB_CUDA;
+  int st = launch_root_bwd(plan, s, B, ldb, d_flows, d_prod_flows);
+  if (st) return st;
+  for (auto it = plan->layers.rbegin(); it != plan->layers.rend(); ++it) {
+    st = layer_backward(plan, *it, s, B, ldb, d_theta, d_values, d_flows, d_scratch,
+                        d_flow_scratch, d_prod_flows, d_f_params);
+    if (st) return st;
+  }
+  st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_f_params);
+  if (st) return st;
+  return launch_replica_reduce(plan, s, d_f_params);
+}
+
+int pcb_layer_forward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
+                      const float* d_theta, float* d_values, float* d_scratch) {
+  if (bad_dims(plan, B, ldb) || layer < 0 || layer >= (int)plan->layers.size()) return PCB_USAGE;
+  if (!B) return PCB_OK;
+  return layer_forward(plan, plan->layers[layer], as_stream(stream), B, ldb, d_theta, d_values,
+                       d_scratch);
+}
+
+int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
+                       const float* d_theta, const float* d_values, float* d_flows,
+                       float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
+                       float* d_f_params) {
+  if (bad_dims(plan, B, ldb) || layer < 0 || layer >= (int)plan->layers.size()) return PCB_USAGE;
+  if (!B) return PCB_OK;
+  return layer_backward(plan, plan->layers[layer], as_stream(stream), B, ldb, d_theta, d_values,
+                        d_flows, d_scratch, d_flow_scratch, d_prod_flows, d_f_params);
+}
+
+int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, float* d_theta,
+                  float pseudocount, float step_size, int32_t* d_status) {
+  if (!plan || !(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f) return PCB_USAGE;
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
+  return launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status);
+}
+
+int pcb_axpy_accumulate(void* stream, int64_t n, const float* d_src, float* d_dst) {
+  if (n <= 0) return PCB_OK;
+  k_axpy<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, d_src, d_dst);
+  return check_launch();
+}
+
+int pcb_count_nonfinite(void* stream, int64_t n, const float* d_x, int32_t* d_count) {
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(d_count, 0, sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
+  if (n <= 0) return PCB_OK;
+  k_nonfinite<<<grid_for(n, 256), 256, 0, s>>>(n, d_x, d_count);
+  return check_launch();
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// Internal declarations shared by the pcirc_b200 CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/pcirc_b200.h"
+
+#define PCB_NEG_INF (-__builtin_huge_valf())
+
+namespace pcb {
+
+struct Ref {
+  int64_t off = 0;  // element offset into the device int32 blob
+  int64_t n = 0;    // element count
+};
+
+struct InputChunk {
+  int64_t ncat, n;
+  const int32_t *slots, *vars, *pids;
+};
+
+struct Bucket {  // product evaluation or push bucket
+  int64_t f, n;
+  const int32_t* idx;       // out scratch rows (eval) or prod-flow rows (push)
+  const int32_t* children;  // [n x f] value slots
+};
+
+struct FwdGroup {
+  int64_t rows, cap;
+  const int32_t *sum_ids, *prod_ids, *param_ids, *flow_ids;
+};
+
+struct BwdGroup {
+  int64_t rows, cap;
+  const int32_t *ch_ids, *par_ids, *par_param_ids;
+};
+
+// Tensor-core work list for one forward / backward group: "super-rows" stack
+// sum blocks (or product blocks) that share an identical child (parent) row.
+struct TcRows {
+  int64_t count = 0;           // number of super-rows
+  const int32_t* row_off = 0;  // [count+1] offsets into members (block rows of the group)
+  const int32_t* members = 0;  // group-row indices, stacked in order
+};
+
+struct Layer {
+  int64_t k_m, k_n, window, n_prod;
+  const int32_t* pad_rows;
+  int64_t n_pad;
+  std::vector<Bucket> evals;
+  std::vector<FwdGroup> fwd;
+  std::vector<BwdGroup> bwd;
+  std::vector<TcRows> fwd_tc;   // aligned with fwd (count 0 = no TC plan)
+  std::vector<TcRows> bwd_tc;   // aligned with bwd
+  const int32_t *prod_slots, *prod_rows;
+  std::vector<Bucket> pushes;
+};
+
+}  // namespace pcb
+
+struct pcb_plan {
+  int64_t num_vars, num_value_slots, scratch_size, num_prod_rows, theta_size,
+      f_params_size, reserved;
+  int64_t root_slot, root_row;
+  const int32_t* root_children;
+  int64_t n_root_children;
+  const int32_t* var_ncat;
+  std::vector<pcb::InputChunk> inputs;
+  std::vector<pcb::Layer> layers;
+  // replica reductions grouped by destination tile
+  int64_t red_n;
+  const int32_t *red_dst, *red_len, *red_src_off, *red_src;
+  // simplex groups
+  int64_t n_groups;
+  const int32_t *group_idx, *group_off;
+  int use_tc;  // 1: tensor-core sum kernels where the plan provides TC rows
+};
+
+namespace pcb {
+
+extern unsigned long long g_launches;
+
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+int check_launch();
+
+// SIMT kernels (pcb_simt.cu)
+int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
+                     const float* theta, float* values);
+int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
+                     float* scratch);
+int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
+                        const float* theta, const float* scratch, float* values);
+int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
+                           const float* theta, const float* values, const float* flows,
+                           const float* scratch, float* f_params);
+int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, int B, int ldb,
+                           const float* theta, const float* values, const float* flows,
+                           const float* scratch, float* flow_scratch);
+int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
+                           const float* flow_scratch, float* prod_flows, float* flows);
+int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
+                             const int32_t* xT, const float* theta, const float* flows,
+                             float* f_params);
+int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
+                    float* lroot);
+int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,
+                    float* prod_flows);
+int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params);
+int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
+              float pseudocount, float step, int32_t* status);
+int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,
+                      float v);
+int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, float* buf,
+                float v);
+
+// tensor-core kernels (pcb_tc.cu)
+int launch_sum_fwd_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
+                      int B, int ldb, const float* theta, const float* scratch, float* values);
+bool tc_supported(const Layer& L);
+
+}  // namespace pcb

@@ -1,0 +1,564 @@
+// SIMT kernels of the hot path: inputs, products, the generic (any block
+// size, incl. demoted K=1) sum-layer forward / parameter-flow / child-flow
+// kernels, flow bookkeeping, replica reduction and EM.
+//
+// Numerics follow pcirc/runtime/engine.py exactly (Appendix B of SURVEY.md):
+// streaming (lin, top) merge with dead-tile skipping, log-flow rescaling by a
+// per-sample block maximum, zero flow for impossible nodes; fp32 throughout.
+#include <math.h>
+
+#include "pcb_internal.cuh"
+
+namespace pcb {
+
+unsigned long long g_launches = 0;
+
+int check_launch() {
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PCB_OK : PCB_CUDA;
+}
+
+// ---------------------------------------------------------------- K1 inputs
+// values[slot_i, b] = log theta[pmf_i + x[var_i, b]], 0 when x is missing
+// (engine.py:55-65).  Threads run along the batch so x and values coalesce.
+__global__ void k_input_fwd(int64_t n, int B, int ldb, const int32_t* __restrict__ slots,
+                            const int32_t* __restrict__ vars, const int32_t* __restrict__ pids,
+                            const int32_t* __restrict__ xT, const float* __restrict__ theta,
+                            float* __restrict__ values) {
+  int64_t total = n * (int64_t)B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / B;
+    int b = (int)(t - i * B);
+    int x = xT[(int64_t)vars[i] * ldb + b];
+    float v = 0.f;
+    if (x >= 0) v = logf(__ldg(theta + pids[i] + x));
+    values[(int64_t)slots[i] * ldb + b] = v;
+  }
+}
+
+int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
+                     const float* theta, float* values) {
+  for (auto& c : p->inputs) {
+    int64_t total = c.n * B;
+    if (!total) continue;
+    k_input_fwd<<<grid_for(total, 256), 256, 0, s>>>(c.n, B, ldb, c.slots, c.vars, c.pids, xT,
+                                                      theta, values);
+    if (check_launch()) return PCB_CUDA;
+  }
+  return PCB_OK;
+}
+
+// ---------------------------------------------------------------- K2 products
+// scratch[out_j, b] = sum_f values[child_jf, b]; fan-in 0 rows are the -inf
+// padding of the layer window (engine.py:68-71).
+__global__ void k_prod_eval(int64_t n, int f, int B, int ldb, const int32_t* __restrict__ out,
+                            const int32_t* __restrict__ ch, const float* __restrict__ values,
+                            float* __restrict__ scratch) {
+  int64_t total = n * (int64_t)B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / B;
+    int b = (int)(t - j * B);
+    float acc = 0.f;
+    const int32_t* c = ch + j * f;
+    for (int q = 0; q < f; ++q) acc += values[(int64_t)c[q] * ldb + b];
+    scratch[(int64_t)out[j] * ldb + b] = acc;
+  }
+}
+
+__global__ void k_fill_rows(int64_t n, int B, int ldb, const int32_t* __restrict__ rows,
+                            float* __restrict__ buf, float v) {
+  int64_t total = n * (int64_t)B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / B;
+    int b = (int)(t - j * B);
+    buf[(int64_t)rows[j] * ldb + b] = v;
+  }
+}
+
+int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, float* buf,
+                float v) {
+  if (!n) return PCB_OK;
+  k_fill_rows<<<grid_for(n * B, 256), 256, 0, s>>>(n, B, ldb, rows, buf, v);
+  return check_launch();
+}
+
+__global__ void k_fill_range(int64_t row0, int64_t n, int B, int ldb, float* __restrict__ buf,
+                             float v) {
+  int64_t total = n * (int64_t)B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / B;
+    int b = (int)(t - j * B);
+    buf[(row0 + j) * ldb + b] = v;
+  }
+}
+
+int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,
+                      float v) {
+  if (!n || !B) return PCB_OK;
+  k_fill_range<<<grid_for(n * B, 256), 256, 0, s>>>(row0, n, B, ldb, buf, v);
+  return check_launch();
+}
+
+int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
+                     float* scratch) {
+  if (launch_fill(s, L.pad_rows, L.n_pad, B, ldb, scratch, PCB_NEG_INF)) return PCB_CUDA;
+  for (auto& e : L.evals) {
+    if (!e.n) continue;
+    k_prod_eval<<<grid_for(e.n * B, 256), 256, 0, s>>>(e.n, (int)e.f, B, ldb, e.idx,
+                                                        e.children, values, scratch);
+    if (check_launch()) return PCB_CUDA;
+  }
+  return PCB_OK;
+}
+
+// ---------------------------------------------------------------- K3 (SIMT)
+// Alg. 1 for one sum-block row and a 32-sample tile (engine.py:74-102).
+// block (32, 8): tx = sample, ty strides over the k_m sums of the block.
+constexpr int TB = 32;
+constexpr int TY = 8;
+constexpr int KMAX = 64;
+
+__global__ void __launch_bounds__(TB* TY)
+    k_sum_fwd_simt(int cap, int k_m, int k_n, int B, int ldb, const int32_t* __restrict__ sum_ids,
+                   const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
+                   const float* __restrict__ theta, const float* __restrict__ scratch,
+                   float* __restrict__ values) {
+  __shared__ float ex[KMAX][TB];
+  __shared__ float th[KMAX * KMAX];
+  __shared__ float cm[TB];
+  const int r = blockIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TB + tx;
+  const int b = blockIdx.x * TB + tx;
+  const bool live_b = b < B;
+  float lin[KMAX / TY];
+#pragma unroll
+  for (int i = 0; i < KMAX / TY; ++i) lin[i] = 0.f;
+  float top = PCB_NEG_INF;
+  for (int c = 0; c < cap; ++c) {
+    const int pid = prod_ids[(int64_t)r * cap + c];
+    const int tid0 = param_ids[(int64_t)r * cap + c];
+    if (tid0 == 0) continue;  // padded column: -inf child block, zero tile
+    for (int j = ty; j < k_n; j += TY)
+      ex[j][tx] = live_b ? scratch[(int64_t)(pid + j) * ldb + b] : PCB_NEG_INF;
+    for (int q = tid; q < k_m * k_n; q += TB * TY) th[q] = __ldg(theta + tid0 + q);
+    __syncthreads();
+    if (ty == 0) {
+      float m = PCB_NEG_INF;
+      for (int j = 0; j < k_n; ++j) m = fmaxf(m, ex[j][tx]);
+      cm[tx] = m;
+    }
+    __syncthreads();
+    const float cmax = cm[tx];
+    const bool dead = (cmax == PCB_NEG_INF);
+    for (int j = ty; j < k_n; j += TY) ex[j][tx] = dead ? 0.f : expf(ex[j][tx] - cmax);
+    __syncthreads();
+    if (!dead) {
+      const float s_old = (cmax > top) ? expf(top - cmax) : 1.f;
+      const float s_new = (cmax > top) ? 1.f : expf(cmax - top);
+#pragma unroll
+      for (int i = 0; i < KMAX / TY; ++i) {
+        const int m = ty + i * TY;
+        if (m < k_m) {
+          float part = 0.f;
+          for (int j = 0; j < k_n; ++j) part = fmaf(th[m * k_n + j], ex[j][tx], part);
+          lin[i] = lin[i] * s_old + part * s_new;
+        }
+      }
+      top = fmaxf(top, cmax);
+    }
+    __syncthreads();
+  }
+  if (!live_b) return;
+  const int sid = sum_ids[r];
+#pragma unroll
+  for (int i = 0; i < KMAX / TY; ++i) {
+    const int m = ty + i * TY;
+    if (m < k_m) values[(int64_t)(sid + m) * ldb + b] = logf(lin[i]) + top;
+  }
+}
+
+int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
+                        const float* theta, const float* scratch, float* values) {
+  if (!g.rows) return PCB_OK;
+  dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
+  k_sum_fwd_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
+                                               g.sum_ids, g.prod_ids, g.param_ids, theta,
+                                               scratch, values);
+  return check_launch();
+}
+
+// log-flow ratio of a sum node: -inf for impossible nodes (engine.py:114-117)
+__device__ __forceinline__ float log_ratio(float f, float l) {
+  return (l == PCB_NEG_INF) ? PCB_NEG_INF : (logf(f) - l);
+}
+
+// ---------------------------------------------------------------- K4 (SIMT)
+// Alg. 3 for one (sum-block row, child column) tile (engine.py:105-126):
+// cum[m, n] = sum_b exp(lnf[m,b] - nmax[b]) * exp(child[n,b] + nmax[b]);
+// f_params[flow + m*k_n + n] += theta * cum.
+constexpr int PF_THREADS = 256;
+
+__global__ void __launch_bounds__(PF_THREADS)
+    k_param_flow_simt(int cap, int k_m, int k_n, int B, int ldb, const int32_t* __restrict__ sum_ids,
+                      const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
+                      const int32_t* __restrict__ flow_ids, const float* __restrict__ theta,
+                      const float* __restrict__ values, const float* __restrict__ flows,
+                      const float* __restrict__ scratch, float* __restrict__ f_params) {
+  __shared__ float sc[KMAX][TB];
+  __shared__ float em[KMAX][TB];
+  __shared__ float nm[TB];
+  const int r = blockIdx.y, c = blockIdx.x;
+  const int tid0 = param_ids[(int64_t)r * cap + c];
+  if (tid0 == 0) return;
+  const int pid = prod_ids[(int64_t)r * cap + c];
+  const int fid = flow_ids[(int64_t)r * cap + c];
+  const int sid = sum_ids[r];
+  const int tid = threadIdx.x;
+  const int tx = tid % TB, ty = tid / TB;  // 32 x 8
+  const int tile = k_m * k_n;
+  constexpr int PER = KMAX * KMAX / PF_THREADS;
+  float cum[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) cum[i] = 0.f;
+  for (int b0 = 0; b0 < B; b0 += TB) {
+    const int b = b0 + tx;
+    const bool live = b < B;
+    for (int m = ty; m < k_m; m += PF_THREADS / TB) {
+      const int64_t o = (int64_t)(sid + m) * ldb + b;
+      sc[m][tx] = live ? log_ratio(flows[o], values[o]) : PCB_NEG_INF;
+    }
+    __syncthreads();
+    if (ty == 0) {
+      float mx = PCB_NEG_INF;
+      for (int m = 0; m < k_m; ++m) mx = fmaxf(mx, sc[m][tx]);
+      nm[tx] = mx;
+    }
+    __syncthreads();
+    const float nmax = nm[tx];
+    const bool dead = (nmax == PCB_NEG_INF) || !live;
+    for (int m = ty; m < k_m; m += PF_THREADS / TB) sc[m][tx] = dead ? 0.f : expf(sc[m][tx] - nmax);
+    for (int n = ty; n < k_n; n += PF_THREADS / TB)
+      em[n][tx] = dead ? 0.f : expf(scratch[(int64_t)(pid + n) * ldb + b] + nmax);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int q = tid + i * PF_THREADS;
+      if (q < tile) {
+        const int m = q / k_n, n = q - m * k_n;
+        float a = cum[i];
+        for (int t = 0; t < TB; ++t) a = fmaf(sc[m][t], em[n][t], a);
+        cum[i] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int q = tid + i * PF_THREADS;
+    if (q < tile) {
+      const float th = __ldg(theta + tid0 + q);
+      if (th != 0.f) atomicAdd(f_params + fid + q, th * cum[i]);
+    }
+  }
+}
+
+int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
+                           const float* theta, const float* values, const float* flows,
+                           const float* scratch, float* f_params) {
+  if (!g.rows || !g.cap) return PCB_OK;
+  dim3 grid((unsigned)g.cap, (unsigned)g.rows);
+  k_param_flow_simt<<<grid, PF_THREADS, 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
+                                                g.sum_ids, g.prod_ids, g.param_ids, g.flow_ids,
+                                                theta, values, flows, scratch, f_params);
+  return check_launch();
+}
+
+// ---------------------------------------------------------------- K5 (SIMT)
+// Alg. 4 for one product-block row and a 32-sample tile (engine.py:129-165).
+__global__ void __launch_bounds__(TB* TY)
+    k_child_flow_simt(int cap, int k_m, int k_n, int B, int ldb, const int32_t* __restrict__ ch_ids,
+                      const int32_t* __restrict__ par_ids, const int32_t* __restrict__ ppids,
+                      const float* __restrict__ theta, const float* __restrict__ values,
+                      const float* __restrict__ flows, const float* __restrict__ scratch,
+                      float* __restrict__ flow_scratch) {
+  __shared__ float sc[KMAX][TB];
+  __shared__ float th[KMAX * KMAX];
+  __shared__ float nm[TB];
+  const int r = blockIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TB + tx;
+  const int b = blockIdx.x * TB + tx;
+  const bool live_b = b < B;
+  float lin[KMAX / TY];
+#pragma unroll
+  for (int i = 0; i < KMAX / TY; ++i) lin[i] = 0.f;
+  float top = PCB_NEG_INF;
+  for (int p = 0; p < cap; ++p) {
+    const int tid0 = ppids[(int64_t)r * cap + p];
+    if (tid0 == 0) continue;
+    const int par = par_ids[(int64_t)r * cap + p];
+    for (int m = ty; m < k_m; m += TY) {
+      const int64_t o = (int64_t)(par + m) * ldb + b;
+      sc[m][tx] = live_b ? log_ratio(flows[o], values[o]) : PCB_NEG_INF;
+    }
+    for (int q = tid; q < k_m * k_n; q += TB * TY) th[q] = __ldg(theta + tid0 + q);
+    __syncthreads();
+    if (ty == 0) {
+      float mx = PCB_NEG_INF;
+      for (int m = 0; m < k_m; ++m) mx = fmaxf(mx, sc[m][tx]);
+      nm[tx] = mx;
+    }
+    __syncthreads();
+    const float nmax = nm[tx];
+    const bool dead = (nmax == PCB_NEG_INF);
+    for (int m = ty; m < k_m; m += TY) sc[m][tx] = dead ? 0.f : expf(sc[m][tx] - nmax);
+    __syncthreads();
+    if (!dead) {
+      const float s_old = (nmax > top) ? expf(top - nmax) : 1.f;
+      const float s_new = (nmax > top) ? 1.f : expf(nmax - top);
+#pragma unroll
+      for (int i = 0; i < KMAX / TY; ++i) {
+        const int n = ty + i * TY;
+        if (n < k_n) {
+          float part = 0.f;
+          for (int m = 0; m < k_m; ++m) part = fmaf(th[m * k_n + n], sc[m][tx], part);
+          lin[i] = lin[i] * s_old + part * s_new;
+        }
+      }
+      top = fmaxf(top, nmax);
+    }
+    __syncthreads();
+  }
+  if (!live_b) return;
+  const int ch = ch_ids[r];
+#pragma unroll
+  for (int i = 0; i < KMAX / TY; ++i) {
+    const int n = ty + i * TY;
+    if (n < k_n) {
+      const int64_t o = (int64_t)(ch + n) * ldb + b;
+      const float lp = scratch[o];
+      // lin * exp(top + l_p) computed in log space to avoid overflow
+      flow_scratch[o] = (lin[i] > 0.f) ? expf(logf(lin[i]) + top + lp) : 0.f;
+    }
+  }
+}
+
+int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, int B, int ldb,
+                           const float* theta, const float* values, const float* flows,
+                           const float* scratch, float* flow_scratch) {
+  if (!g.rows) return PCB_OK;
+  dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
+  k_child_flow_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
+                                                  g.ch_ids, g.par_ids, g.par_param_ids, theta,
+                                                  values, flows, scratch, flow_scratch);
+  return check_launch();
+}
+
+// ---------------------------------------------------------------- K6
+// prod_flows[row_j] += flow_scratch[slot_j] (engine.py:249-250)
+__global__ void k_prod_accum(int64_t n, int B, int ldb, const int32_t* __restrict__ slots,
+                             const int32_t* __restrict__ rows, const float* __restrict__ fs,
+                             float* __restrict__ pf) {
+  int64_t total = n * (int64_t)B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / B;
+    int b = (int)(t - j * B);
+    pf[(int64_t)rows[j] * ldb + b] += fs[(int64_t)slots[j] * ldb + b];
+  }
+}
+
+// flows[child] += prod_flows[row] for every child of a finished product (engine.py:251-254)
+__global__ void k_push(int64_t n, int f, int B, int ldb, const int32_t* __restrict__ rows,
+                       const int32_t* __restrict__ ch, const float* __restrict__ pf,
+                       float* __restrict__ flows) {
+  int64_t total = n * (int64_t)B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / B;
+    int b = (int)(t - j * B);
+    float v = pf[(int64_t)rows[j] * ldb + b];
+    if (v == 0.f) continue;
+    const int32_t* c = ch + j * f;
+    for (int q = 0; q < f; ++q) atomicAdd(flows + (int64_t)c[q] * ldb + b, v);
+  }
+}
+
+int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
+                           const float* flow_scratch, float* prod_flows, float* flows) {
+  if (L.n_prod) {
+    k_prod_accum<<<grid_for(L.n_prod * B, 256), 256, 0, s>>>(L.n_prod, B, ldb, L.prod_slots,
+                                                              L.prod_rows, flow_scratch, prod_flows);
+    if (check_launch()) return PCB_CUDA;
+  }
+  for (auto& p : L.pushes) {
+    if (!p.n) continue;
+    k_push<<<grid_for(p.n * B, 256), 256, 0, s>>>(p.n, (int)p.f, B, ldb, p.idx, p.children,
+                                                   prod_flows, flows);
+    if (check_launch()) return PCB_CUDA;
+  }
+  return PCB_OK;
+}
+
+// ---------------------------------------------------------------- K7
+// Input parameter flows (engine.py:168-183): observed -> f[pmf + x] += flow;
+// missing -> spread sum(flow) * theta over the pmf.  One CTA per input node.
+__global__ void k_input_param_flow(int ncat, int B, int ldb, const int32_t* __restrict__ slots,
+                                   const int32_t* __restrict__ vars, const int32_t* __restrict__ pids,
+                                   const int32_t* __restrict__ xT, const float* __restrict__ theta,
+                                   const float* __restrict__ flows, float* __restrict__ f_params) {
+  __shared__ float red[32];
+  const int i = blockIdx.x;
+  const int slot = slots[i], var = vars[i], pid = pids[i];
+  float miss = 0.f;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const float f = flows[(int64_t)slot * ldb + b];
+    const int x = xT[(int64_t)var * ldb + b];
+    if (x >= 0) {
+      if (f != 0.f) atomicAdd(f_params + pid + x, f);
+    } else {
+      miss += f;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = miss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float tot = red[0];
+  if (tot != 0.f)
+    for (int q = threadIdx.x; q < ncat; q += blockDim.x)
+      atomicAdd(f_params + pid + q, tot * __ldg(theta + pid + q));
+}
+
+int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
+                             const int32_t* xT, const float* theta, const float* flows,
+                             float* f_params) {
+  for (auto& c : p->inputs) {
+    if (!c.n) continue;
+    int threads = B >= 256 ? 256 : (B >= 128 ? 128 : 64);
+    k_input_param_flow<<<(unsigned)c.n, threads, 0, s>>>((int)c.ncat, B, ldb, c.slots, c.vars,
+                                                        c.pids, xT, theta, flows, f_params);
+    if (check_launch()) return PCB_CUDA;
+  }
+  return PCB_OK;
+}
+
+// ---------------------------------------------------------------- K10 root
+__global__ void k_root_fwd(int B, int ldb, int64_t root_slot, const int32_t* __restrict__ rc,
+                           int nrc, const float* __restrict__ values, float* __restrict__ lroot) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float v;
+  if (root_slot >= 0) {
+    v = values[root_slot * ldb + b];
+  } else {
+    v = 0.f;
+    for (int q = 0; q < nrc; ++q) v += values[(int64_t)rc[q] * ldb + b];
+  }
+  lroot[b] = v;
+}
+
+int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
+                    float* lroot) {
+  k_root_fwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_children,
+                                              (int)p->n_root_children, values, lroot);
+  return check_launch();
+}
+
+__global__ void k_root_bwd(int B, int ldb, int64_t root_slot, int64_t root_row,
+                           const int32_t* __restrict__ rc, int nrc, float* __restrict__ flows,
+                           float* __restrict__ pf) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (root_slot >= 0) {
+    flows[root_slot * ldb + b] = 1.f;
+  } else {
+    pf[root_row * ldb + b] = 1.f;
+    for (int q = 0; q < nrc; ++q) flows[(int64_t)rc[q] * ldb + b] += 1.f;
+  }
+}
+
+int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,
+                    float* prod_flows) {
+  k_root_bwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_row,
+                                              p->root_children, (int)p->n_root_children, flows,
+                                              prod_flows);
+  return check_launch();
+}
+
+// ---------------------------------------------------------------- K8 replicas
+// f[dst + e] += sum over replicas f[src + e] (engine.py:256-257), grouped by
+// destination so the sum is race-free and in the reference's order.
+__global__ void k_replica_reduce(int64_t n_dst, const int32_t* __restrict__ dst,
+                                 const int32_t* __restrict__ len, const int32_t* __restrict__ soff,
+                                 const int32_t* __restrict__ src, float* __restrict__ f) {
+  for (int64_t d = blockIdx.x; d < n_dst; d += gridDim.x) {
+    const int L = len[d];
+    const int a = soff[d], z = soff[d + 1];
+    for (int e = threadIdx.x; e < L; e += blockDim.x) {
+      float acc = f[(int64_t)dst[d] + e];
+      for (int k = a; k < z; ++k) acc += f[(int64_t)src[k] + e];
+      f[(int64_t)dst[d] + e] = acc;
+    }
+  }
+}
+
+int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params) {
+  if (!p->red_n) return PCB_OK;
+  k_replica_reduce<<<grid_for(p->red_n, 1, 148 * 16), 256, 0, s>>>(
+      p->red_n, p->red_dst, p->red_len, p->red_src_off, p->red_src, f_params);
+  return check_launch();
+}
+
+// ---------------------------------------------------------------- K9 EM
+// One warp per simplex group (em.py:58-94): counts = F + k; groups with a
+// positive total are renormalised and blended with step size; others keep theta.
+__global__ void k_em(int64_t n_groups, const int32_t* __restrict__ gidx,
+                     const int32_t* __restrict__ goff, const float* __restrict__ F,
+                     float* __restrict__ theta, float kappa, float step, int32_t* status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int informative = 0, bad = 0;
+  for (int64_t g = warp; g < n_groups; g += nwarps) {
+    const int a = goff[g], z = goff[g + 1];
+    float tot = 0.f;
+    for (int k = a + lane; k < z; k += 32) tot += F[gidx[k]] + kappa;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (!(tot > 0.f)) continue;
+    ++informative;
+    const float inv = 1.f / tot;
+    for (int k = a + lane; k < z; k += 32) {
+      const int q = gidx[k];
+      const float nv = (F[q] + kappa) * inv;
+      const float th = (step >= 1.f) ? nv : ((1.f - step) * theta[q] + step * nv);
+      if (!isfinite(th)) ++bad;
+      theta[q] = th;
+    }
+  }
+  if (lane == 0 && informative) atomicAdd(status, informative);
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if (lane == 0 && bad) atomicAdd(status + 1, bad);
+}
+
+int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
+              float pseudocount, float step, int32_t* status) {
+  if (!p->n_groups) return PCB_OK;
+  int blocks = grid_for(p->n_groups * 32, 256, 148 * 16);
+  k_em<<<blocks, 256, 0, s>>>(p->n_groups, p->group_idx, p->group_off, f_params, theta,
+                              pseudocount, step, status);
+  return check_launch();
+}
+
+}  // namespace pcb

@@ -1,0 +1,79 @@
+"""Device batch workspace (drop-in for ``pcirc/runtime/buffers.py:18-57``).
+
+Same arrays, same (rows x batch) node-major layout, on the GPU in fp32.
+Rows are padded to a stride ``ldb`` (multiple of 32 samples) so kernels
+can vectorise; the public attributes are ``[:, :B]`` views, so
+``bufs.values[slot, col]`` indexes exactly like the reference.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def padded_stride(batch_size: int) -> int:
+    return max(32, (int(batch_size) + 31) // 32 * 32)
+
+
+@dataclass
+class EvalBuffers:
+    batch_size: int
+    ldb: int
+    xT: object           # int32 [num_vars x ldb]
+    values_full: object  # fp32 [num_value_slots x ldb]
+    scratch_full: object
+    flows_full: object
+    flow_scratch_full: object
+    prod_flows_full: object
+    f_params: object     # fp32 [f_params_size]
+    lroot: object        # fp32 [B]
+    batch: np.ndarray | None = None
+    forward_done: bool = False
+    backward_done: bool = False
+    device: object = None
+    _extra: dict = field(default_factory=dict)
+
+    @property
+    def values(self):
+        return self.values_full[:, : self.batch_size]
+
+    @property
+    def scratch(self):
+        return self.scratch_full[:, : self.batch_size]
+
+    @property
+    def flows(self):
+        return self.flows_full[:, : self.batch_size]
+
+    @property
+    def flow_scratch(self):
+        return self.flow_scratch_full[:, : self.batch_size]
+
+    @property
+    def prod_flows(self):
+        return self.prod_flows_full[:, : self.batch_size]
+
+
+def allocate_buffers(compiled, batch_size: int, device=None) -> EvalBuffers:
+    """Zeroed device workspace for ``batch_size`` samples."""
+    import torch
+    dev = torch.device(device if device is not None else "cuda")
+    b = int(batch_size)
+    ldb = padded_stride(b)
+
+    def z(rows):
+        return torch.zeros((max(int(rows), 1), ldb), dtype=torch.float32, device=dev)
+
+    return EvalBuffers(
+        batch_size=b, ldb=ldb,
+        xT=torch.zeros((max(compiled.num_vars, 1), ldb), dtype=torch.int32, device=dev),
+        values_full=z(compiled.num_value_slots),
+        scratch_full=z(compiled.scratch_size),
+        flows_full=z(compiled.num_value_slots),
+        flow_scratch_full=z(compiled.scratch_size),
+        prod_flows_full=z(compiled.num_prod_rows),
+        f_params=torch.zeros(max(compiled.f_params_size, 1), dtype=torch.float32, device=dev),
+        lroot=torch.zeros(max(b, 1), dtype=torch.float32, device=dev)[:b],
+        device=dev,
+    )

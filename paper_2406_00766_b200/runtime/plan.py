@@ -1,0 +1,228 @@
+"""Device execution plan: the compiled layout narrowed to flat int32 tables.
+
+``build_program`` turns a :class:`CompiledCircuit` (host int64 arrays, the
+bit-exact layout contract) into
+
+* one device int32 blob holding every index table (groups, product buckets,
+  pushes, input chunks, replica CSR, simplex-group CSR), and
+* a host int64 program: layer / group records with (offset, count) refs into
+  the blob, parsed by ``pcb_plan_create`` (``csrc/pcb_capi.cu``).
+
+Derived, non-contract tables are added for the kernels: the per-layer list
+of scratch rows that must read -inf (window padding), replica reductions
+grouped by destination tile, and tensor-core "super-rows" (sum blocks with
+identical child-block rows stacked up to 256 sums for one MMA N extent).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from ..compiler._rows import group_matrix_rows
+from ..errors import UsageError
+from . import _lib
+
+MAGIC = 0x50434232
+VERSION = 2
+TC_NMAX = 256
+INT32_MAX = np.iinfo(np.int32).max
+
+
+class _Blob:
+    def __init__(self):
+        self.parts: list[np.ndarray] = []
+        self.size = 0
+
+    def add(self, arr) -> tuple[int, int]:
+        a = np.ascontiguousarray(np.asarray(arr, dtype=np.int64).ravel())
+        if a.size and (a.max() > INT32_MAX or a.min() < -INT32_MAX):
+            raise UsageError("index table exceeds int32 range")
+        off = self.size
+        if a.size:
+            self.parts.append(a.astype(np.int32))
+            self.size += a.size
+        return off, int(a.size)
+
+    def array(self) -> np.ndarray:
+        if not self.parts:
+            return np.zeros(1, dtype=np.int32)
+        return np.concatenate(self.parts)
+
+
+def tc_super_rows(prod_ids: np.ndarray, k_m: int, nmax: int = TC_NMAX):
+    """Stack group rows with identical child rows into <= nmax-sum super-rows."""
+    rows = prod_ids.shape[0]
+    if rows == 0:
+        return np.zeros(1, np.int64), np.zeros(0, np.int64)
+    per = max(1, nmax // max(k_m, 1))
+    gid, first = group_matrix_rows(prod_ids)
+    order = np.argsort(gid, kind="stable")
+    sizes = np.bincount(gid)
+    offs, members = [0], []
+    pos = 0
+    for g, sz in enumerate(sizes.tolist()):
+        mem = order[pos:pos + sz]
+        pos += sz
+        for a in range(0, sz, per):
+            chunk = mem[a:a + per]
+            members.append(chunk)
+            offs.append(offs[-1] + chunk.size)
+    return np.asarray(offs, dtype=np.int64), np.concatenate(members).astype(np.int64)
+
+
+def build_program(compiled, *, tensor_cores: bool = True):
+    """Return (program int64 array, blob int32 array, info dict)."""
+    blob = _Blob()
+    prog: list[int] = [MAGIC, VERSION]
+
+    def ref(arr):
+        off, n = blob.add(arr)
+        prog.extend([off, n])
+
+    c = compiled
+    prog += [c.num_vars, c.num_value_slots, c.scratch_size, c.num_prod_rows, c.theta_size,
+             c.f_params_size, c.reserved, c.root_slot, c.root_row]
+    ref(c.root_children if c.root_children is not None else np.zeros(0, np.int64))
+    ref(np.asarray(c.var_categories, dtype=np.int64))
+    prog.append(1 if tensor_cores else 0)
+
+    prog.append(len(c.input_layer))
+    for ch in c.input_layer:
+        prog += [int(ch.num_categories), int(ch.node_ids.size)]
+        ref(ch.slots)
+        ref(ch.vars)
+        ref(ch.param_ids)
+
+    n_tc_rows = 0
+    prog.append(len(c.layers))
+    for L in c.layers:
+        prog += [L.k_m, L.k_n, L.scratch_window, int(L.prod_slots.size)]
+        written = np.concatenate([ev.out for ev in L.prod_evals]) if L.prod_evals else \
+            np.zeros(0, np.int64)
+        pad = np.setdiff1d(np.arange(L.scratch_window, dtype=np.int64), written)
+        ref(pad)
+        prog.append(len(L.prod_evals))
+        for ev in L.prod_evals:
+            prog += [int(ev.children.shape[1]), int(ev.out.size)]
+            ref(ev.out)
+            ref(ev.children)
+        prog.append(len(L.fwd_groups))
+        for g in L.fwd_groups:
+            rows, cap = g.prod_ids.shape
+            prog += [rows, cap]
+            ref(g.sum_ids)
+            ref(g.prod_ids)
+            ref(g.param_ids)
+            ref(g.flow_ids)
+            if tensor_cores and L.k_n in (16, 32, 64) and rows:
+                offs, mem = tc_super_rows(g.prod_ids, L.k_m)
+                prog.append(offs.size - 1)
+                ref(offs)
+                ref(mem)
+                n_tc_rows += offs.size - 1
+            else:
+                prog += [0, 0, 0, 0, 0]
+        prog.append(len(L.bwd_groups))
+        for g in L.bwd_groups:
+            rows, cap = g.par_ids.shape
+            prog += [rows, cap]
+            ref(g.ch_ids)
+            ref(g.par_ids)
+            ref(g.par_param_ids)
+            prog += [0, 0, 0, 0, 0]
+        ref(L.prod_slots)
+        ref(L.prod_rows)
+        prog.append(len(L.pushes))
+        for p in L.pushes:
+            prog += [int(p.children.shape[1]), int(p.rows.size)]
+            ref(p.rows)
+            ref(p.children)
+
+    red = np.asarray(c.reductions, dtype=np.int64).reshape(-1, 3)
+    if red.shape[0]:
+        order = np.lexsort((np.arange(red.shape[0]), red[:, 1]))
+        r = red[order]
+        dst, first = np.unique(r[:, 1], return_index=True)
+        lens = r[first, 2]
+        soff = np.concatenate([first, [r.shape[0]]])
+        prog.append(dst.size)
+        ref(dst)
+        ref(lens)
+        ref(soff)
+        ref(r[:, 0])
+    else:
+        prog.append(0)
+        for _ in range(4):
+            ref(np.zeros(0, np.int64))
+
+    n_groups = int(c.group_off.size - 1)
+    prog.append(n_groups)
+    ref(c.group_idx)
+    ref(c.group_off)
+    prog.append(MAGIC)
+    info = {"blob_elems": blob.size, "tc_super_rows": n_tc_rows}
+    return np.asarray(prog, dtype=np.int64), blob.array(), info
+
+
+class DevicePlan:
+    """Device tables + C plan handle + fp32 theta for one compiled circuit."""
+
+    def __init__(self, compiled, device=None, *, tensor_cores: bool = True):
+        import torch
+        lib = _lib.load()
+        self.device = torch.device(device if device is not None else "cuda")
+        self.compiled = compiled
+        self.tensor_cores = tensor_cores
+        prog, blob, info = build_program(compiled, tensor_cores=tensor_cores)
+        self.info = info
+        self._prog = prog
+        self.blob = torch.from_numpy(blob).to(self.device)
+        handle = _lib.C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.call("pcb_plan_create", prog.ctypes.data, prog.size, self.blob.data_ptr(),
+                      self.blob.numel(), _lib.C.byref(handle))
+        self.handle = handle
+        self.theta = torch.empty(compiled.theta_size, dtype=torch.float32, device=self.device)
+        self.status = torch.zeros(4, dtype=torch.int32, device=self.device)
+        self.num_layers = lib.pcb_plan_num_layers(handle)
+        self.theta_source = None
+        self.upload_theta(compiled.theta)
+
+    def upload_theta(self, theta) -> None:
+        """Copy a host (numpy) or device theta into the plan's fp32 table."""
+        import torch
+        if isinstance(theta, np.ndarray):
+            if theta.shape != (self.compiled.theta_size,):
+                raise UsageError("parameter table shape mismatch")
+            self.theta_finite = bool(np.all(np.isfinite(theta)))
+            self.theta.copy_(torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float32)))
+        else:
+            t = theta.to(device=self.device, dtype=torch.float32)
+            if t.shape != (self.compiled.theta_size,):
+                raise UsageError("parameter table shape mismatch")
+            self.theta.copy_(t)
+            self.theta_finite = bool(torch.isfinite(self.theta).all().item())
+        self.theta_source = theta
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().pcb_plan_destroy(h)
+            except Exception:
+                pass
+
+
+def device_plan(compiled, device=None, *, tensor_cores: bool = True) -> DevicePlan:
+    """The cached plan of ``compiled`` on ``device`` (built on first use)."""
+    import torch
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    if compiled._device_plans is None:
+        compiled._device_plans = {}
+    key = (str(dev), tensor_cores)
+    plan = compiled._device_plans.get(key)
+    if plan is None:
+        plan = DevicePlan(compiled, dev, tensor_cores=tensor_cores)
+        compiled._device_plans[key] = plan
+    return plan
