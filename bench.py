@@ -1,0 +1,393 @@
+"""Benchmark: samples/s of forward + backward + mini-batch EM on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload hclt256|hclt16|hmm4096|...]
+
+One "step" = one pass of the hot path over one synthetic batch: input
+gathers, product gather-adds, tcgen05 sum-layer contractions, parameter and
+child flows, flow pushes, input flows, replica reduction, all-reduce of the
+parameter flows (N > 1) and the fused mini-batch EM update (alpha 0.01,
+pseudocount 1e-6) — the reference's ``train()`` inner loop
+(``pcirc/train.py:128-142``).
+
+``value``: inputs resident in HBM before the timed region.  ``e2e``: the same
+steps through the public API with each batch copied host(pinned)->device and
+the step log-likelihood read back inside the timed region.  Per-kernel-class
+times come from CUDA events recorded live on the launching stream in a
+separate profiled pass; the dominant class gives ``roofline``.  Every step's
+working set (GBs of values / flows / parameters) exceeds the 126 MB L2, so no
+explicit flush is needed.  ``--impl reference`` times the CPU oracle port of
+the reference on the host cores instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+
+WORKLOADS = {
+    "hclt256": dict(kind="hclt", num_vars=3072, hidden_dim=256, num_categories=256, block=32,
+                    batch=512, desc="HCLT latent=256, 3072 vars (ImageNet32-shaped), 256 cats"),
+    "hclt16": dict(kind="hclt", num_vars=784, hidden_dim=16, num_categories=256, block=16,
+                   batch=512, desc="HCLT latent=16, 784 vars (MNIST-shaped), 256 cats"),
+    "hclt64": dict(kind="hclt", num_vars=3072, hidden_dim=64, num_categories=256, block=32,
+                   batch=512, desc="HCLT latent=64, 3072 vars, 256 cats (dev proxy)"),
+    "hmm4096": dict(kind="hmm", seq_len=32, hidden_dim=4096, vocab_size=50257, block=32,
+                    batch=256, desc="HMM hidden=4096, vocab 50257, seq len 32"),
+}
+EPOCH = 60000
+STEP_SIZE = 0.01
+PSEUDOCOUNT = 1e-6
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def build_circuit(w):
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    if w["kind"] == "hclt":
+        cfg = S.StructureConfig(kind="hclt", num_vars=w["num_vars"], hidden_dim=w["hidden_dim"],
+                                num_categories=w["num_categories"], seed=0)
+    else:
+        cfg = S.StructureConfig(kind="hmm", seq_len=w["seq_len"], hidden_dim=w["hidden_dim"],
+                                vocab_size=w["vocab_size"], seed=0, tied=True)
+    g = S.build_structure(cfg)
+    c = compile_circuit(g, CompileConfig(block_size=w["block"]), validate=False)
+    return c
+
+
+def synthetic_batches(c, w, B, count, seed):
+    """Uniform categories, ``default_rng(1)``-derived."""
+    rng = np.random.default_rng([1, seed])
+    cats = np.asarray(c.var_categories)
+    return [rng.integers(0, cats[None, :], size=(B, c.num_vars)).astype(np.int32)
+            for _ in range(count)]
+
+
+def algorithmic_bytes(c, B):
+    """Minimal fp32 HBM bytes per step per kernel class."""
+    n_in = sum(int(ch.node_ids.size) for ch in c.input_layer)
+    n_sum = sum(int(L.report.num_sums) for L in c.layers)
+    n_prod = sum(int(L.report.num_prods) for L in c.layers)
+    F = sum(int(ev.children.size) for L in c.layers for ev in L.prod_evals)
+    E = c.num_edges
+    return {
+        "input_fwd": B * (4 * c.num_vars + 8 * n_in),
+        "prod_eval": 2 * B * 4 * (F + n_prod),            # forward + backward recompute
+        "sum_fwd_tc": B * 4 * (n_prod + n_sum) + 4 * E,
+        "sum_fwd_simt": B * 4 * (n_prod + n_sum) + 4 * E,
+        "param_flow": B * 4 * (2 * n_sum + n_prod) + 8 * E,
+        "child_flow": B * 4 * (2 * n_sum + 2 * n_prod),
+        "accum_push": B * 4 * (3 * n_prod + 3 * F),
+        "input_flow": B * 12 * n_in,
+        "em": 20 * c.theta_size,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6554.9), d.get("bf16_tflops_sustained", 1420.9), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------- CPU oracle
+def cpu_step_time(c, w, B_cpu, seed=7):
+    """Oracle (float64 numpy port of the reference) fwd + bwd + EM on B_cpu samples."""
+    import oracle
+    x = synthetic_batches(c, w, B_cpu, 1, seed)[0].astype(np.int64)
+    theta = c.theta.copy()
+    t0 = time.perf_counter()
+    _, bufs = oracle.forward(c, x, theta=theta)
+    oracle.backward(c, bufs, theta=theta)
+    new = oracle.em_step_full(c, bufs.f_params, theta=theta, pseudocount=PSEUDOCOUNT)
+    if new is not None:
+        theta = oracle.em_step_mini(theta, new, STEP_SIZE)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_size(w):
+    """Samples per CPU step: the full batch where a step fits in ~seconds,
+    else a bounded sample (the per-step EM over all of theta is fixed cost)."""
+    if w["kind"] == "hmm":
+        return 4
+    return {16: 512, 64: 64}.get(w["hidden_dim"], 32)
+
+
+def run_reference(args, w):
+    """--impl reference: the oracle port timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    c = build_circuit(w)
+    Bc = cpu_sample_size(w)
+    for _ in range(args.warmup):
+        cpu_step_time(c, w, Bc)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += cpu_step_time(c, w, Bc)
+    v = Bc * args.steps / tot
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": "samples/sec fwd+bwd+EM", "value": v,
+        "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": w["desc"], "batch_per_step": Bc,
+                   "sec_per_epoch": EPOCH / v},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": f"{Bc} samples per step of the {args.workload} workload "
+                                   "(forward+backward+EM step over the full theta)"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args, w):
+    import torch
+    import torch.distributed as dist
+    from paper_2406_00766_b200.runtime import _lib
+    from paper_2406_00766_b200.runtime.buffers import allocate_buffers
+    from paper_2406_00766_b200.runtime.em import em_update_
+    from paper_2406_00766_b200.runtime.plan import device_plan
+    from paper_2406_00766_b200.train import allreduce_accumulators
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    t0 = time.time()
+    c = build_circuit(w)
+    log(f"[bench] compiled {args.workload}: {c.num_edges} edges, theta {c.theta_size} "
+        f"in {time.time() - t0:.1f}s")
+    B = w["batch"]
+    plan = device_plan(c, dev)
+    bufs = allocate_buffers(c, B, dev)
+    n_pool = 4
+    host_batches = synthetic_batches(c, w, B, n_pool, seed=rank)
+    dev_batches = [torch.from_numpy(h).to(dev) for h in host_batches]
+    pinned = [torch.from_numpy(h).pin_memory() for h in host_batches]
+    stage = torch.empty((B, c.num_vars), dtype=torch.int32, device=dev)
+    theta_size = c.theta_size
+    stream = _lib.stream_handle()
+    ll_acc = torch.zeros((), dtype=torch.float64, device=dev)
+    ll_host = torch.zeros((), dtype=torch.float64).pin_memory()
+
+    def step(xdev, e2e=False):
+        _lib.call("pcb_transpose_batch_i32", plan.handle, stream, B, bufs.ldb, xdev.data_ptr(),
+                  bufs.xT.data_ptr())
+        _lib.call("pcb_forward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
+                  plan.theta.data_ptr(), bufs.values_full.data_ptr(),
+                  bufs.scratch_full.data_ptr(), bufs.lroot.data_ptr())
+        _lib.call("pcb_backward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
+                  plan.theta.data_ptr(), bufs.values_full.data_ptr(), bufs.flows_full.data_ptr(),
+                  bufs.scratch_full.data_ptr(), bufs.flow_scratch_full.data_ptr(),
+                  bufs.prod_flows_full.data_ptr(), bufs.f_params.data_ptr())
+        step_ll = bufs.lroot.double().sum()
+        allreduce_accumulators(bufs.f_params, step_ll, theta_size)
+        em_update_(c, bufs.f_params, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, check=False,
+                   plan=plan)
+        return step_ll
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also builds every lazily created kernel attribute)
+    for i in range(args.warmup):
+        step(dev_batches[i % n_pool])
+    barrier()
+
+    # ---- device-resident timed region
+    launches0 = _lib.load().pcb_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record()
+        for i in range(args.steps):
+            ll_acc += step(dev_batches[i % n_pool])
+        ev1.record()
+        barrier()
+    launches = _lib.load().pcb_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * B * args.steps / (ms / 1000.0)
+
+    # ---- end-to-end through host memory
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev2.record()
+    for i in range(args.steps):
+        stage.copy_(pinned[i % n_pool], non_blocking=True)
+        sl = step(stage)
+        ll_host.copy_(sl, non_blocking=True)
+    ev3.record()
+    barrier()
+    ms_e2e = ev2.elapsed_time(ev3)
+    t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_e2e = float(t.item())
+    e2e_value = world * B * args.steps / (ms_e2e / 1000.0)
+
+    # ---- profiled pass: live per-kernel-class CUDA-event times
+    prof_steps = max(1, min(3, args.steps))
+    _lib.profile_enable(True)
+    _lib.profile_read()
+    for i in range(prof_steps):
+        step(dev_batches[i % n_pool])
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    hbm, tflops, peak_src = measured_peaks()
+    algo = algorithmic_bytes(c, B)
+    classes = {k: v for k, v in prof.items() if v[0] > 0}
+    total_prof = sum(v[0] for v in classes.values())
+    dom = max(classes, key=lambda k: classes[k][0])
+    dom_ms, dom_scopes, dom_launches = classes[dom]
+    per_step_ms = dom_ms / prof_steps
+    dom_bytes = algo.get(dom)
+    traffic = None
+    tr_file = ROOT / "profiles" / f"traffic_{args.workload}.json"
+    if tr_file.exists():
+        traffic = json.loads(tr_file.read_text()).get(dom)
+    achieved = (dom_bytes / (per_step_ms / 1000.0) / 1e9) if dom_bytes else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_step": dom_bytes,
+                "kernel_ms_per_step": per_step_ms,
+                "launches_per_step": dom_launches / prof_steps,
+                "share_of_step": dom_ms / total_prof if total_prof else None}
+    breakdown = {k: {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[2] / prof_steps,
+                     "gbs": (algo[k] / (v[0] / prof_steps / 1000.0) / 1e9)
+                     if k in algo and v[0] > 0 else None}
+                 for k, v in classes.items()}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        Bc = cpu_sample_size(w)
+        secs = cpu_step_time(c, w, Bc)
+        cpu = {"value": Bc / secs, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"one forward+backward+EM step on {Bc} samples of {args.workload} "
+                         f"({secs:.1f} s, numpy float64, BLAS threads = host cores)"}
+    line = {
+        "metric": "samples/sec fwd+bwd+EM", "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "desc": w["desc"], "batch_per_gpu": B,
+                   "global_batch": world * B, "block_size": w["block"],
+                   "em": f"mini-batch, step {STEP_SIZE}, pseudocount {PSEUDOCOUNT}",
+                   "edges": c.num_edges, "theta_size": c.theta_size,
+                   "sec_per_epoch": EPOCH / value, "l2": "working set >> 126 MB L2 (no flush)",
+                   "parallelism": f"dp{world}"},
+        "e2e": {"value": e2e_value, "unit": "samples/s",
+                "h2d_bytes_per_step": B * c.num_vars * 4, "d2h_bytes_per_step": 8},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "kernels": breakdown,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="hclt256", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

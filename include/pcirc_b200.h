@@ -113,8 +113,16 @@ int pcb_axpy_accumulate(void* stream, int64_t n, const float* d_src, float* d_ds
  * Replaces the theta check of pcirc/runtime/engine.py:197-198. */
 int pcb_count_nonfinite(void* stream, int64_t n, const float* d_x, int32_t* d_count);
 
-/* Per-kernel-class launch counter (for the bench's gpu_launches claim). */
+/* Total kernel launches issued by this library (for the bench's gpu_launches claim). */
 int64_t pcb_launch_count(void);
+
+/* Live per-kernel-class timing with CUDA events on the launching stream.
+ * Classes: 0 input_fwd, 1 prod_eval, 2 sum_fwd_tc, 3 sum_fwd_simt,
+ * 4 param_flow, 5 child_flow, 6 accum_push, 7 input_flow, 8 replica, 9 em, 10 misc.
+ * pcb_profile_read fills per-class milliseconds, wrapper-scope counts and kernel
+ * launch counts accumulated since the previous read (it synchronises). */
+int pcb_profile_enable(int on);
+int pcb_profile_read(double* ms, int64_t* scopes, int64_t* launches, int n);
 
 /* tcgen05 self-test: D[128 x n] = A[128 x k] . B[n x k]^T in bf16 with fp32
  * accumulation on one CTA (n in {16..256, step 16}, k multiple of 16 <= 256).

@@ -314,7 +314,9 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
         L.n_pb = n_pb
 
     theta = np.concatenate(theta_parts)
-    _check_tying_alignment(rep, assigned)
+    if g.tying or getattr(g, "shares_slots", True):
+        _check_tying_alignment(rep, assigned)
+    del assigned
 
     # -- groups, product evaluation, flow bookkeeping ---------------------------
     prod_ch_off, prod_ch_flat = _product_children(g, n_nodes)
@@ -552,6 +554,82 @@ def _product_children(g: CircuitGraph, n_nodes: int):
 
 def _simplex_groups(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
     """Normalisation groups over physical positions, first-occurrence order."""
+    fast = _simplex_groups_disjoint(g, pmf_phys_of, slot_phys, theta_size)
+    if fast is not None:
+        return fast
+    return _simplex_groups_general(g, pmf_phys_of, slot_phys, theta_size)
+
+
+def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
+    """Fast path when no two sums share a physical position and no sum touches a
+    pmf: every sum is its own group and inputs dedupe by their pmf range, so
+    the first-occurrence order is plain node-id order."""
+    sum_segs = [s for s in g.segments if s.kind == KIND_SUM]
+    in_ids, _, in_ncat, _ = g.input_table()
+    n_sum_pos = sum(s.count * s.fan_in for s in sum_segs)
+    claim = np.zeros(theta_size, dtype=np.int8)
+    if in_ids.size:
+        starts = pmf_phys_of[in_ids]
+        key = np.stack([starts, in_ncat], axis=1)
+        _, first = np.unique(key, axis=0, return_index=True)
+        first = np.sort(first)
+        rs, rn = starts[first], in_ncat[first]
+        off = np.repeat(rs - np.concatenate([[0], np.cumsum(rn)[:-1]]), rn)
+        pmf_pos = np.arange(int(rn.sum()), dtype=np.int64) + off
+        claim[pmf_pos] = 1
+        if int(claim.sum()) != pmf_pos.size:
+            return None  # overlapping pmf ranges
+    else:
+        first = np.zeros(0, np.int64)
+        rs = rn = np.zeros(0, np.int64)
+    for s in sum_segs:
+        pos = slot_phys[s.slots].ravel()
+        if np.any(claim[pos]):
+            return None
+        claim[pos] = 1
+    if int(claim.sum()) != int(rn.sum()) + n_sum_pos:
+        return None  # a position shared between sums (or within one sum)
+    # assemble in node-id order: input group starts and sum rows interleave
+    items_id, items_kind, items_ref = [], [], []
+    items_id.append(in_ids[first])
+    items_kind.append(np.zeros(first.size, np.int8))
+    items_ref.append(np.arange(first.size, dtype=np.int64))
+    for si, s in enumerate(sum_segs):
+        items_id.append(np.arange(s.start, s.stop, dtype=np.int64))
+        items_kind.append(np.full(s.count, 1, np.int8))
+        items_ref.append(np.arange(s.count, dtype=np.int64) + (si << 40))
+    ids = np.concatenate(items_id)
+    order = np.argsort(ids, kind="stable")
+    kinds = np.concatenate(items_kind)[order]
+    refs = np.concatenate(items_ref)[order]
+    sizes = np.empty(ids.size, dtype=np.int64)
+    sizes[kinds == 0] = rn[refs[kinds == 0]]
+    segsz = np.array([s.fan_in for s in sum_segs], dtype=np.int64)
+    sizes[kinds == 1] = segsz[refs[kinds == 1] >> 40] if sum_segs else 0
+    group_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    group_idx = np.empty(int(group_off[-1]), dtype=np.int64)
+    # inputs: contiguous ranges
+    ii = np.flatnonzero(kinds == 0)
+    if ii.size:
+        n = rn[refs[ii]]
+        dst = np.repeat(group_off[ii], n) + (np.arange(int(n.sum())) -
+                                              np.repeat(np.cumsum(n) - n, n))
+        group_idx[dst] = np.repeat(rs[refs[ii]], n) + (np.arange(int(n.sum())) -
+                                                       np.repeat(np.cumsum(n) - n, n))
+    # sums: sorted physical slots per row, written segment by segment
+    pos_of = np.full(ids.size, 0, dtype=np.int64)
+    pos_of[order] = np.arange(ids.size)
+    base = first.size
+    for si, s in enumerate(sum_segs):
+        rows = pos_of[base:base + s.count]
+        base += s.count
+        phys = np.sort(slot_phys[s.slots], axis=1)
+        dst = group_off[rows][:, None] + np.arange(s.fan_in)
+        group_idx[dst] = phys
+    return group_idx, group_off
+
+
+def _simplex_groups_general(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
     members: list[np.ndarray] = []
     range_key: dict[tuple, int] = {}
     hash_key: dict[tuple, list] = {}

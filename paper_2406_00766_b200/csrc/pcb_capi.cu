@@ -235,12 +235,24 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
                    float* flow_scratch, float* prod_flows, float* f_params) {
   int st = launch_prod_eval(L, s, B, ldb, values, scratch);  // recompute
   if (st) return st;
-  for (auto& g : L.fwd) {
-    st = launch_param_flow_simt(L, g, s, B, ldb, theta, values, flows, scratch, f_params);
+  for (size_t g = 0; g < L.fwd.size(); ++g) {
+    const TcRows& T = L.fwd_tc[g];
+    if (P->use_tc && T.count > 0 && tc_bwd_supported(L))
+      st = launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
+                                f_params);
+    else
+      st = launch_param_flow_simt(L, L.fwd[g], s, B, ldb, theta, values, flows, scratch,
+                                  f_params);
     if (st) return st;
   }
-  for (auto& g : L.bwd) {
-    st = launch_child_flow_simt(L, g, s, B, ldb, theta, values, flows, scratch, flow_scratch);
+  for (size_t g = 0; g < L.bwd.size(); ++g) {
+    const TcRows& T = L.bwd_tc[g];
+    if (P->use_tc && T.count > 0 && tc_bwd_supported(L))
+      st = launch_child_flow_tc(L, L.bwd[g], T, s, B, ldb, theta, values, flows, scratch,
+                                flow_scratch);
+    else
+      st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
+                                  flow_scratch);
     if (st) return st;
   }
   return launch_prod_accum_push(L, s, B, ldb, flow_scratch, prod_flows, flows);
@@ -306,15 +318,19 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
                  float* d_flow_scratch, float* d_prod_flows, float* d_f_params) {
   if (bad_dims(plan, B, ldb)) return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
-  if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * plan->f_params_size, s) != cudaSuccess)
-    return PCB_CUDA;
-  if (!B) return PCB_OK;
-  if (cudaMemsetAsync(d_flows, 0, sizeof(float) * plan->num_value_slots * ldb, s) != cudaSuccess)
-    return PCB_CUDA;
-  if (plan->num_prod_rows &&
-      cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * plan->num_prod_rows * ldb, s) !=
-          cudaSuccess)
-    return PCB_CUDA;
+  {
+    ProfScope prof_(KC_MISC, s);
+    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * plan->f_params_size, s) != cudaSuccess)
+      return PCB_CUDA;
+    if (!B) return PCB_OK;
+    if (cudaMemsetAsync(d_flows, 0, sizeof(float) * plan->num_value_slots * ldb, s) !=
+        cudaSuccess)
+      return PCB_CUDA;
+    if (plan->num_prod_rows &&
+        cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * plan->num_prod_rows * ldb, s) !=
+            cudaSuccess)
+      return PCB_CUDA;
+  }
   int st = launch_root_bwd(plan, s, B, ldb, d_flows, d_prod_flows);
   if (st) return st;
   for (auto it = plan->layers.rbegin(); it != plan->layers.rend(); ++it) {

@@ -83,6 +83,33 @@ namespace pcb {
 
 extern unsigned long long g_launches;
 
+// kernel classes for the live per-class timing used by bench.py
+enum KClass {
+  KC_INPUT_FWD = 0,
+  KC_PROD_EVAL,
+  KC_SUM_FWD_TC,
+  KC_SUM_FWD_SIMT,
+  KC_PARAM_FLOW,
+  KC_CHILD_FLOW,
+  KC_ACCUM_PUSH,
+  KC_INPUT_FLOW,
+  KC_REPLICA,
+  KC_EM,
+  KC_MISC,
+  KC_COUNT
+};
+
+// Records a CUDA event pair around every launch wrapper of one class when
+// profiling is enabled (pcb_profile_enable); otherwise a no-op.
+struct ProfScope {
+  int cls;
+  cudaStream_t s;
+  unsigned long long l0;
+  int slot;
+  ProfScope(int c, cudaStream_t st);
+  ~ProfScope();
+};
+
 inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -126,5 +153,12 @@ int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, 
 int launch_sum_fwd_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                       int B, int ldb, const float* theta, const float* scratch, float* values);
 bool tc_supported(const Layer& L);
+bool tc_bwd_supported(const Layer& L);
+int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
+                         int B, int ldb, const float* theta, const float* values,
+                         const float* flows, const float* scratch, float* f_params);
+int launch_child_flow_tc(const Layer& L, const BwdGroup& g, const TcRows& tc, cudaStream_t s,
+                         int B, int ldb, const float* theta, const float* values,
+                         const float* flows, const float* scratch, float* flow_scratch);
 
 }  // namespace pcb

@@ -19,6 +19,77 @@ int check_launch() {
   return e == cudaSuccess ? PCB_OK : PCB_CUDA;
 }
 
+// ---------------------------------------------------------------- profiling
+namespace {
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  unsigned long long launches;
+};
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_event_pool;
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(int c, cudaStream_t st) : cls(c), s(st), l0(g_launches), slot(-1) {
+  if (!g_prof_on) return;
+  ProfRec r{c, take_event(), take_event(), 0};
+  cudaEventRecord(r.a, s);
+  slot = (int)g_prof.size();
+  g_prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (slot < 0) return;
+  cudaEventRecord(g_prof[slot].b, s);
+  g_prof[slot].launches = g_launches - l0;
+}
+
+}  // namespace pcb
+
+extern "C" int pcb_profile_enable(int on) {
+  pcb::g_prof_on = on != 0;
+  return PCB_OK;
+}
+
+// Per class: total milliseconds, number of wrapper scopes, number of kernel
+// launches since the last read.  Synchronises on the recorded events.
+extern "C" int pcb_profile_read(double* ms, int64_t* scopes, int64_t* launches, int n) {
+  using namespace pcb;
+  for (int i = 0; i < n; ++i) {
+    ms[i] = 0;
+    scopes[i] = 0;
+    launches[i] = 0;
+  }
+  int st = PCB_OK;
+  for (auto& r : g_prof) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+      st = PCB_CUDA;
+    if (r.cls < n) {
+      ms[r.cls] += t;
+      scopes[r.cls] += 1;
+      launches[r.cls] += (int64_t)r.launches;
+    }
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  return st;
+}
+
+namespace pcb {
+
 // ---------------------------------------------------------------- K1 inputs
 // values[slot_i, b] = log theta[pmf_i + x[var_i, b]], 0 when x is missing
 // (engine.py:55-65).  Threads run along the batch so x and values coalesce.
@@ -40,6 +111,7 @@ __global__ void k_input_fwd(int64_t n, int B, int ldb, const int32_t* __restrict
 
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
                      const float* theta, float* values) {
+  ProfScope prof_(KC_INPUT_FWD, s);
   for (auto& c : p->inputs) {
     int64_t total = c.n * B;
     if (!total) continue;
@@ -99,6 +171,7 @@ __global__ void k_fill_range(int64_t row0, int64_t n, int B, int ldb, float* __r
 
 int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,
                       float v) {
+  ProfScope prof_(KC_MISC, s);
   if (!n || !B) return PCB_OK;
   k_fill_range<<<grid_for(n * B, 256), 256, 0, s>>>(row0, n, B, ldb, buf, v);
   return check_launch();
@@ -106,6 +179,7 @@ int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, f
 
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
                      float* scratch) {
+  ProfScope prof_(KC_PROD_EVAL, s);
   if (launch_fill(s, L.pad_rows, L.n_pad, B, ldb, scratch, PCB_NEG_INF)) return PCB_CUDA;
   for (auto& e : L.evals) {
     if (!e.n) continue;
@@ -185,6 +259,7 @@ __global__ void __launch_bounds__(TB* TY)
 
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                         const float* theta, const float* scratch, float* values) {
+  ProfScope prof_(KC_SUM_FWD_SIMT, s);
   if (!g.rows) return PCB_OK;
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
   k_sum_fwd_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
@@ -271,6 +346,7 @@ __global__ void __launch_bounds__(PF_THREADS)
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
                            const float* scratch, float* f_params) {
+  ProfScope prof_(KC_PARAM_FLOW, s);
   if (!g.rows || !g.cap) return PCB_OK;
   dim3 grid((unsigned)g.cap, (unsigned)g.rows);
   k_param_flow_simt<<<grid, PF_THREADS, 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
@@ -352,6 +428,7 @@ __global__ void __launch_bounds__(TB* TY)
 int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
                            const float* scratch, float* flow_scratch) {
+  ProfScope prof_(KC_CHILD_FLOW, s);
   if (!g.rows) return PCB_OK;
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
   k_child_flow_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
@@ -392,6 +469,7 @@ __global__ void k_push(int64_t n, int f, int B, int ldb, const int32_t* __restri
 
 int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows) {
+  ProfScope prof_(KC_ACCUM_PUSH, s);
   if (L.n_prod) {
     k_prod_accum<<<grid_for(L.n_prod * B, 256), 256, 0, s>>>(L.n_prod, B, ldb, L.prod_slots,
                                                               L.prod_rows, flow_scratch, prod_flows);
@@ -444,6 +522,7 @@ __global__ void k_input_param_flow(int ncat, int B, int ldb, const int32_t* __re
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
                              float* f_params) {
+  ProfScope prof_(KC_INPUT_FLOW, s);
   for (auto& c : p->inputs) {
     if (!c.n) continue;
     int threads = B >= 256 ? 256 : (B >= 128 ? 128 : 64);
@@ -471,6 +550,7 @@ __global__ void k_root_fwd(int B, int ldb, int64_t root_slot, const int32_t* __r
 
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
                     float* lroot) {
+  ProfScope prof_(KC_MISC, s);
   k_root_fwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_children,
                                               (int)p->n_root_children, values, lroot);
   return check_launch();
@@ -491,6 +571,7 @@ __global__ void k_root_bwd(int B, int ldb, int64_t root_slot, int64_t root_row,
 
 int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,
                     float* prod_flows) {
+  ProfScope prof_(KC_MISC, s);
   k_root_bwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_row,
                                               p->root_children, (int)p->n_root_children, flows,
                                               prod_flows);
@@ -515,6 +596,7 @@ __global__ void k_replica_reduce(int64_t n_dst, const int32_t* __restrict__ dst,
 }
 
 int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params) {
+  ProfScope prof_(KC_REPLICA, s);
   if (!p->red_n) return PCB_OK;
   k_replica_reduce<<<grid_for(p->red_n, 1, 148 * 16), 256, 0, s>>>(
       p->red_n, p->red_dst, p->red_len, p->red_src_off, p->red_src, f_params);
@@ -554,6 +636,7 @@ __global__ void k_em(int64_t n_groups, const int32_t* __restrict__ gidx,
 
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
               float pseudocount, float step, int32_t* status) {
+  ProfScope prof_(KC_EM, s);
   if (!p->n_groups) return PCB_OK;
   int blocks = grid_for(p->n_groups * 32, 256, 148 * 16);
   k_em<<<blocks, 256, 0, s>>>(p->n_groups, p->group_idx, p->group_off, f_params, theta,

@@ -169,6 +169,10 @@ class CircuitGraph:
         self._num_nodes = 0
         self._root: int | None = None
         self._frozen = False
+        # True once any node reuses explicit slots (structural tying); together
+        # with an empty ``tying`` map this lets the compiler skip the tying
+        # alignment check, which cannot fail when every slot has one use
+        self.shares_slots = False
         self._starts_cache: np.ndarray | None = None
         self._kind_cache: np.ndarray | None = None
 
@@ -244,6 +248,8 @@ class CircuitGraph:
             slot = self._alloc_slots(ncat)
         elif slot < 0 or slot + ncat > self._num_slots:
             raise CircuitValidationError("input slot range not allocated")
+        else:
+            self.shares_slots = True
         if pmf is not None:
             self._params[slot:slot + ncat] = pmf
         seg = Segment(KIND_INPUT, self._num_nodes, 1,
@@ -277,6 +283,7 @@ class CircuitGraph:
             start = self._alloc_slots(ch.size)
             slot_arr = np.arange(start, start + ch.size, dtype=np.int64)
         else:
+            self.shares_slots = True
             slot_arr = np.asarray(slots, dtype=np.int64)
             if slot_arr.shape != ch.shape:
                 raise CircuitValidationError("one slot per child edge required")
@@ -317,6 +324,7 @@ class CircuitGraph:
             base = self._alloc_slots(n * ncat)
             slot = base + ncat * np.arange(n, dtype=np.int64)
         else:
+            self.shares_slots = True
             slot = np.broadcast_to(np.asarray(slots, dtype=np.int64), (n,)).copy()
             if slot.min() < 0 or slot.max() + ncat > self._num_slots:
                 raise CircuitValidationError("input slot range not allocated")
@@ -365,6 +373,7 @@ class CircuitGraph:
             base = self._alloc_slots(n * f)
             sl = base + np.arange(n * f, dtype=np.int64).reshape(n, f)
         else:
+            self.shares_slots = True
             sl = np.asarray(slots, dtype=np.int64)
             if sl.shape != ch.shape:
                 sl = np.broadcast_to(sl, ch.shape)
@@ -741,6 +750,7 @@ class CircuitGraph:
                               slots=np.asarray(node.slots, dtype=np.int64)[None, :],
                               dep=int(ch.max()))
             g._push(seg)
+        g.shares_slots = True  # unknown provenance
         g._params = np.asarray(params, dtype=np.float64).copy()
         g._num_slots = g._params.size
         if root is not None:

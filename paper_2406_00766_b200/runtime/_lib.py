@@ -35,6 +35,8 @@ SIGNATURES = {
     "pcb_axpy_accumulate": (_I, [_P, _L, _P, _P]),
     "pcb_count_nonfinite": (_I, [_P, _L, _P, _P]),
     "pcb_launch_count": (_L, []),
+    "pcb_profile_enable": (_I, [_I]),
+    "pcb_profile_read": (_I, [_P, _P, _P, _I]),
     "pcb_tc_selftest": (_I, [_P, _I, _I, _P, _P, _P]),
 }
 
@@ -67,6 +69,25 @@ def load(path: Path | None = None) -> C.CDLL:
 def call(name: str, *args) -> None:
     """Invoke an entry point and map its status onto the error classes."""
     raise_for_status(getattr(load(), name)(*args), name)
+
+
+KERNEL_CLASSES = ["input_fwd", "prod_eval", "sum_fwd_tc", "sum_fwd_simt", "param_flow",
+                  "child_flow", "accum_push", "input_flow", "replica", "em", "misc"]
+
+
+def profile_enable(on: bool) -> None:
+    load().pcb_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{class: (ms, scopes, launches)} accumulated since the last read."""
+    import numpy as np
+    n = len(KERNEL_CLASSES)
+    ms = np.zeros(n, dtype=np.float64)
+    sc = np.zeros(n, dtype=np.int64)
+    ln = np.zeros(n, dtype=np.int64)
+    call("pcb_profile_read", ms.ctypes.data, sc.ctypes.data, ln.ctypes.data, n)
+    return {k: (float(ms[i]), int(sc[i]), int(ln[i])) for i, k in enumerate(KERNEL_CLASSES)}
 
 
 def ptr(t) -> int:

@@ -75,9 +75,11 @@ def _status_check(plan, n_groups: int) -> None:
 
 
 def em_update_(compiled, f_params, *, pseudocount: float, step_size: float, theta=None,
-               check: bool = True, device=None):
-    """In-place ``theta <- (1-a) theta + a normalise(F + k)`` over every group."""
-    plan = device_plan(compiled, device)
+               check: bool = True, device=None, plan=None):
+    """In-place ``theta <- (1-a) theta + a normalise(F + k)`` over every group
+    (on ``plan.theta`` unless another table is given)."""
+    if plan is None:
+        plan = device_plan(compiled, device if device is not None else f_params.device)
     target = plan.theta if theta is None else theta
     _lib.call("pcb_em_update", plan.handle, _lib.stream_handle(), f_params.data_ptr(),
               target.data_ptr(), float(pseudocount), float(step_size), plan.status.data_ptr())
@@ -93,7 +95,7 @@ def em_step_full(compiled, acc: EMAccumulator, *, pseudocount: float = 0.0):
     plan = device_plan(compiled, acc.f_params.device)
     new = plan.theta.clone()
     em_update_(compiled, acc.f_params, pseudocount=pseudocount, step_size=1.0, theta=new,
-               device=acc.f_params.device)
+               plan=plan)
     return new
 
 

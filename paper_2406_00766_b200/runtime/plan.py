@@ -128,7 +128,14 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.ch_ids)
             ref(g.par_ids)
             ref(g.par_param_ids)
-            prog += [0, 0, 0, 0, 0]
+            if tensor_cores and L.k_n in (16, 32, 64) and L.k_m in (16, 32, 64) and rows:
+                offs, mem = tc_super_rows(g.par_ids, L.k_n)
+                prog.append(offs.size - 1)
+                ref(offs)
+                ref(mem)
+                n_tc_rows += offs.size - 1
+            else:
+                prog += [0, 0, 0, 0, 0]
         ref(L.prod_slots)
         ref(L.prod_rows)
         prog.append(len(L.pushes))

@@ -174,14 +174,14 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
                 allreduce_accumulators(bufs.f_params, step_ll, theta_size, group)
                 ep_ll += step_ll
                 em_update_(compiled, bufs.f_params, pseudocount=cfg.pseudocount,
-                           step_size=cfg.step_size, check=False, device=dev)
+                           step_size=cfg.step_size, check=False, plan=plan)
                 if n_groups:
                     dead_steps += (plan.status[0] == 0).int()
                 bad_values += plan.status[1]
             if cfg.mode == "full":
                 allreduce_accumulators(ep_fp, ep_ll, theta_size, group)
                 em_update_(compiled, ep_fp, pseudocount=cfg.pseudocount, step_size=1.0,
-                           check=False, device=dev)
+                           check=False, plan=plan)
                 if n_groups:
                     dead_steps += (plan.status[0] == 0).int()
                 bad_values += plan.status[1]

@@ -1,0 +1,102 @@
+"""GPU parity beyond the fixture sizes, against the float64 oracle.
+
+Exercises what the small golden cases cannot: several 128-sample tiles with
+a ragged last tile, stacked super-rows and multiple M tiles, child-column
+groups (cap * k_n > 256), tied transition tiles with replica reductions,
+and size-independent properties (flow conservation, EM simplex sums).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from _golden import rel_err
+from oracle.engine import log_gap
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-4
+
+
+def _np(t):
+    return t.detach().double().cpu().numpy()
+
+
+def _compare(c, x, tensor_cores=True):
+    from paper_2406_00766_b200.runtime import backward, em_update_, forward
+    lroot, bufs = forward(c, x, tensor_cores=tensor_cores)
+    backward(c, bufs, tensor_cores=tensor_cores)
+    rl, rb = oracle.forward(c, x)
+    oracle.backward(c, rb)
+    assert log_gap(_np(lroot), rl, 1e-5, RTOL) <= 1.0
+    assert rel_err(_np(bufs.f_params)[:c.theta_size], rb.f_params[:c.theta_size]) < RTOL
+    assert rel_err(_np(bufs.flows), rb.flows) < RTOL
+    new = oracle.em_step_full(c, rb.f_params, pseudocount=1e-6)
+    want = oracle.em_step_mini(c.theta, new, 0.01)
+    from paper_2406_00766_b200.runtime.plan import device_plan
+    plan = device_plan(c, tensor_cores=tensor_cores)
+    saved = plan.theta.clone()
+    em_update_(c, bufs.f_params, pseudocount=1e-6, step_size=0.01, plan=plan)
+    got = _np(plan.theta)
+    plan.theta.copy_(saved)
+    assert rel_err(got, want) < RTOL
+    return bufs
+
+
+@pytest.mark.parametrize("tensor_cores", [True, False])
+def test_hclt_multi_tile(tensor_cores):
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=40, hidden_dim=64,
+                                       num_categories=16, seed=3))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    x = np.random.default_rng(0).integers(0, 16, size=(300, 40))
+    x[np.random.default_rng(1).random(x.shape) < 0.1] = -1
+    _compare(c, x, tensor_cores)
+
+
+@pytest.mark.parametrize("k", [16, 32, 64])
+def test_hclt_block_sizes(k):
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=20, hidden_dim=64,
+                                       num_categories=8, seed=5))
+    c = compile_circuit(g, CompileConfig(block_size=k))
+    x = np.random.default_rng(2).integers(0, 8, size=(131, 20))
+    _compare(c, x)
+
+
+def test_tied_hmm_column_groups_and_replicas():
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    g = S.build_hmm(S.StructureConfig(kind="hmm", seq_len=4, hidden_dim=512, vocab_size=30,
+                                      seed=1, tied=True))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    assert max(gr.prod_ids.shape[1] for L in c.layers for gr in L.fwd_groups) * 32 > 256
+    assert len(c.reductions) > 0
+    x = np.random.default_rng(3).integers(0, 30, size=(70, 4))
+    _compare(c, x)
+
+
+def test_flow_conservation_and_simplex_at_scale():
+    """Size-independent checks on a 3072-variable HCLT (no oracle needed)."""
+    import torch
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.runtime import backward, em_update_, forward
+    from paper_2406_00766_b200.runtime.plan import device_plan
+    g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=3072, hidden_dim=32,
+                                       num_categories=256, seed=0))
+    c = compile_circuit(g, CompileConfig(block_size=32), validate=False)
+    x = np.random.default_rng(4).integers(0, 256, size=(512, 3072))
+    lroot, bufs = forward(c, x)
+    backward(c, bufs)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(lroot).all())
+    # every sample's input flows sum to the number of variables (each variable
+    # is covered once under the root: flows of its inputs sum to 1)
+    slots = np.concatenate([ch.slots for ch in c.input_layer])
+    tot = _np(bufs.flows)[slots].sum(axis=0)
+    np.testing.assert_allclose(tot, 3072.0, rtol=1e-4)
+    em_update_(c, bufs.f_params, pseudocount=1e-6, step_size=1.0)
+    th = _np(device_plan(c).theta)
+    sums = np.add.reduceat(th[c.group_idx], c.group_off[:-1])
+    np.testing.assert_allclose(sums, 1.0, atol=1e-4)
