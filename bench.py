@@ -230,7 +230,7 @@ def run_ours(args, w):
         f"in {time.time() - t0:.1f}s")
     B = w["batch"]
     plan = device_plan(c, dev)
-    bufs = allocate_buffers(c, B, dev)
+    bufs = allocate_buffers(c, B, dev, plan=plan)
     n_pool = 4
     host_batches = synthetic_batches(c, w, B, n_pool, seed=rank)
     dev_batches = [torch.from_numpy(h).to(dev) for h in host_batches]
@@ -246,11 +246,12 @@ def run_ours(args, w):
                   bufs.xT.data_ptr())
         _lib.call("pcb_forward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
                   plan.theta.data_ptr(), bufs.values_full.data_ptr(),
-                  bufs.scratch_full.data_ptr(), bufs.lroot.data_ptr())
+                  bufs.scratch_full.data_ptr(), bufs.lroot.data_ptr(), bufs.work.data_ptr())
         _lib.call("pcb_backward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
                   plan.theta.data_ptr(), bufs.values_full.data_ptr(), bufs.flows_full.data_ptr(),
                   bufs.scratch_full.data_ptr(), bufs.flow_scratch_full.data_ptr(),
-                  bufs.prod_flows_full.data_ptr(), bufs.f_params.data_ptr())
+                  bufs.prod_flows_full.data_ptr(), bufs.f_params.data_ptr(),
+                  bufs.work.data_ptr())
         step_ll = bufs.lroot.double().sum()
         allreduce_accumulators(bufs.f_params, step_ll, theta_size)
         em_update_(c, bufs.f_params, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, check=False,

@@ -43,7 +43,7 @@ extern "C" {
 #define PCB_NUMERIC 3
 #define PCB_CUDA 4
 
-#define PCB_ABI_VERSION 1
+#define PCB_ABI_VERSION 2
 
 typedef struct pcb_plan pcb_plan;
 
@@ -74,28 +74,33 @@ int pcb_transpose_batch_i64(const pcb_plan* plan, void* stream, int B, int ldb,
 int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
                             const int32_t* d_x, int32_t* d_xT);
 
+/* Floats of device workspace (d_work) the passes below need at row stride ldb:
+ * per-(product block, sample) child maxima and per-(sum block, sample) flow-ratio
+ * maxima.  Derived state, not part of the reference's buffers. */
+int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb);
+
 /* Full forward pass: values, scratch, lroot[B].
  * Replaces: pcirc/runtime/engine.py:186-217 (forward). */
 int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb,
                 const int32_t* d_xT, const float* d_theta, float* d_values,
-                float* d_scratch, float* d_lroot);
+                float* d_scratch, float* d_lroot, float* d_work);
 
 /* Full backward pass (flows, prod_flows, f_params incl. replica reduction).
  * Replaces: pcirc/runtime/engine.py:220-259 (backward). */
 int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb,
                  const int32_t* d_xT, const float* d_theta, const float* d_values,
                  float* d_flows, float* d_scratch, float* d_flow_scratch,
-                 float* d_prod_flows, float* d_f_params);
+                 float* d_prod_flows, float* d_f_params, float* d_work);
 
 /* Per-layer operator API (the reference's private kernels that
  * pcirc/bench.py:22-27 imports): product evaluation + sum forward of layer
  * `layer` (engine.py:68-102), and its backward (engine.py:105-165 + :249-254). */
 int pcb_layer_forward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
-                      const float* d_theta, float* d_values, float* d_scratch);
+                      const float* d_theta, float* d_values, float* d_scratch, float* d_work);
 int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
                        const float* d_theta, const float* d_values, float* d_flows,
                        float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
-                       float* d_f_params);
+                       float* d_f_params, float* d_work);
 
 /* EM over the simplex groups, in place on d_theta:
  *   theta[g] <- (1 - step) * theta[g] + step * (F[g] + k) / sum(F[g] + k)

@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 2;
+constexpr int64_t kVersion = 3;
 
 struct Reader {
   const int64_t* p;
@@ -139,6 +139,16 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       b.children = r.ref();
       L.pushes.push_back(b);
     }
+    L.prow_off = r.ref();
+    L.prow_ch = r.ref();
+    L.sb_base = r.get();
+    L.n_sb = r.get();
+    L.push_flag = r.ref();
+    L.push_off = r.ref();
+    L.push_ch = r.ref();
+    L.n_pb = L.window / L.k_n;  // including the -inf pad block 0
+    if (L.n_pb > P->max_pb) P->max_pb = L.n_pb;
+    if (L.n_sb > P->max_sb) P->max_sb = L.n_sb;
     P->layers.push_back(std::move(L));
   }
   P->red_n = r.get();
@@ -215,14 +225,21 @@ __global__ void k_nonfinite(int64_t n, const float* __restrict__ x, int32_t* cnt
   if (c) atomicAdd(cnt, c);
 }
 
+Work carve(const pcb_plan* P, int ldb, float* d_work) {
+  Work w;
+  w.bmax = d_work;
+  w.rmax = d_work + P->max_pb * (int64_t)ldb;
+  return w;
+}
+
 int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
-                  const float* theta, float* values, float* scratch) {
-  int st = launch_prod_eval(L, s, B, ldb, values, scratch);
+                  const float* theta, float* values, float* scratch, const Work& w) {
+  int st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);
   if (st) return st;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.fwd_tc[g];
     if (P->use_tc && T.count > 0 && tc_supported(L))
-      st = launch_sum_fwd_tc(L, L.fwd[g], T, s, B, ldb, theta, scratch, values);
+      st = launch_sum_fwd_tc(L, L.fwd[g], T, s, B, ldb, theta, scratch, w.bmax, values);
     else
       st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, values);
     if (st) return st;
@@ -232,14 +249,19 @@ int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int 
 
 int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
                    const float* theta, const float* values, float* flows, float* scratch,
-                   float* flow_scratch, float* prod_flows, float* f_params) {
-  int st = launch_prod_eval(L, s, B, ldb, values, scratch);  // recompute
+                   float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
+  int st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);  // recompute
   if (st) return st;
+  const bool tc = P->use_tc && tc_bwd_supported(L);
+  if (tc) {
+    st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax);
+    if (st) return st;
+  }
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.fwd_tc[g];
-    if (P->use_tc && T.count > 0 && tc_bwd_supported(L))
+    if (tc && T.count > 0)
       st = launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
-                                f_params);
+                                w.rmax, f_params);
     else
       st = launch_param_flow_simt(L, L.fwd[g], s, B, ldb, theta, values, flows, scratch,
                                   f_params);
@@ -247,9 +269,9 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   }
   for (size_t g = 0; g < L.bwd.size(); ++g) {
     const TcRows& T = L.bwd_tc[g];
-    if (P->use_tc && T.count > 0 && tc_bwd_supported(L))
+    if (tc && T.count > 0)
       st = launch_child_flow_tc(L, L.bwd[g], T, s, B, ldb, theta, values, flows, scratch,
-                                flow_scratch);
+                                w.rmax, flow_scratch);
     else
       st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
                                   flow_scratch);
@@ -259,7 +281,7 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
 }
 
 bool bad_dims(const pcb_plan* p, int B, int ldb) {
-  return !p || B < 0 || ldb < B || (ldb % 4) != 0;
+  return !p || B < 0 || ldb < B || (ldb % 32) != 0;
 }
 
 }  // namespace
@@ -295,11 +317,18 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
   return check_launch();
 }
 
+int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
+  if (!plan || ldb <= 0) return -1;
+  return (plan->max_pb + plan->max_sb) * (int64_t)ldb;
+}
+
 int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
-                const float* d_theta, float* d_values, float* d_scratch, float* d_lroot) {
-  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+                const float* d_theta, float* d_values, float* d_scratch, float* d_lroot,
+                float* d_work) {
+  if (bad_dims(plan, B, ldb) || !d_work) return PCB_USAGE;
   if (!B) return PCB_OK;
   cudaStream_t s = as_stream(stream);
+  const Work w = carve(plan, ldb, d_work);
   // values.fill(-inf) (engine.py:204): every input and sum-block row (padding
   // rows included) is written below, so only the reserved constant rows need it.
   int st = launch_fill_range(s, 0, plan->reserved, B, ldb, d_values, PCB_NEG_INF);
@@ -307,7 +336,7 @@ int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_
   st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values);
   if (st) return st;
   for (auto& L : plan->layers) {
-    st = layer_forward(plan, L, s, B, ldb, d_theta, d_values, d_scratch);
+    st = layer_forward(plan, L, s, B, ldb, d_theta, d_values, d_scratch, w);
     if (st) return st;
   }
   return launch_root_fwd(plan, s, B, ldb, d_values, d_lroot);
@@ -315,9 +344,10 @@ int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_
 
 int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
                  const float* d_theta, const float* d_values, float* d_flows, float* d_scratch,
-                 float* d_flow_scratch, float* d_prod_flows, float* d_f_params) {
-  if (bad_dims(plan, B, ldb)) return PCB_USAGE;
+                 float* d_flow_scratch, float* d_prod_flows, float* d_f_params, float* d_work) {
+  if (bad_dims(plan, B, ldb) || !d_work) return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
+  const Work w = carve(plan, ldb, d_work);
   {
     ProfScope prof_(KC_MISC, s);
     if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * plan->f_params_size, s) != cudaSuccess)
@@ -335,7 +365,7 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
   if (st) return st;
   for (auto it = plan->layers.rbegin(); it != plan->layers.rend(); ++it) {
     st = layer_backward(plan, *it, s, B, ldb, d_theta, d_values, d_flows, d_scratch,
-                        d_flow_scratch, d_prod_flows, d_f_params);
+                        d_flow_scratch, d_prod_flows, d_f_params, w);
     if (st) return st;
   }
   st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_f_params);
@@ -344,21 +374,24 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
 }
 
 int pcb_layer_forward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
-                      const float* d_theta, float* d_values, float* d_scratch) {
-  if (bad_dims(plan, B, ldb) || layer < 0 || layer >= (int)plan->layers.size()) return PCB_USAGE;
+                      const float* d_theta, float* d_values, float* d_scratch, float* d_work) {
+  if (bad_dims(plan, B, ldb) || !d_work || layer < 0 || layer >= (int)plan->layers.size())
+    return PCB_USAGE;
   if (!B) return PCB_OK;
   return layer_forward(plan, plan->layers[layer], as_stream(stream), B, ldb, d_theta, d_values,
-                       d_scratch);
+                       d_scratch, carve(plan, ldb, d_work));
 }
 
 int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
                        const float* d_theta, const float* d_values, float* d_flows,
                        float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
-                       float* d_f_params) {
-  if (bad_dims(plan, B, ldb) || layer < 0 || layer >= (int)plan->layers.size()) return PCB_USAGE;
+                       float* d_f_params, float* d_work) {
+  if (bad_dims(plan, B, ldb) || !d_work || layer < 0 || layer >= (int)plan->layers.size())
+    return PCB_USAGE;
   if (!B) return PCB_OK;
   return layer_backward(plan, plan->layers[layer], as_stream(stream), B, ldb, d_theta, d_values,
-                        d_flows, d_scratch, d_flow_scratch, d_prod_flows, d_f_params);
+                        d_flows, d_scratch, d_flow_scratch, d_prod_flows, d_f_params,
+                        carve(plan, ldb, d_work));
 }
 
 int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, float* d_theta,

@@ -57,6 +57,19 @@ struct Layer {
   std::vector<TcRows> bwd_tc;   // aligned with bwd
   const int32_t *prod_slots, *prod_rows;
   std::vector<Bucket> pushes;
+  // derived tables (plan v3)
+  const int32_t *prow_off, *prow_ch;  // per scratch row: product children CSR
+  int64_t sb_base, n_sb;              // sum blocks of the layer: slots [sb_base, +n_sb*k_m)
+  int64_t n_pb;                       // product blocks in the window incl. pad block 0
+  const int32_t *push_flag, *push_off, *push_ch;  // fused accumulate + push, product order
+};
+
+// Workspace carved from the caller's d_work buffer (pcb_plan_workspace_floats):
+//   bmax [max_pb x ldb]  per product block and sample: max child log value
+//   rmax [max_sb x ldb]  per sum block and sample: max log(flow) - log(value)
+struct Work {
+  float* bmax;
+  float* rmax;
 };
 
 }  // namespace pcb
@@ -77,6 +90,7 @@ struct pcb_plan {
   int64_t n_groups;
   const int32_t *group_idx, *group_off;
   int use_tc;  // 1: tensor-core sum kernels where the plan provides TC rows
+  int64_t max_pb = 1, max_sb = 1;
 };
 
 namespace pcb {
@@ -123,7 +137,9 @@ int check_launch();
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
                      const float* theta, float* values);
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
-                     float* scratch);
+                     float* scratch, float* bmax);
+int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
+                     const float* flows, float* rmax);
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                         const float* theta, const float* scratch, float* values);
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
@@ -151,14 +167,17 @@ int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, 
 
 // tensor-core kernels (pcb_tc.cu)
 int launch_sum_fwd_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
-                      int B, int ldb, const float* theta, const float* scratch, float* values);
+                      int B, int ldb, const float* theta, const float* scratch,
+                      const float* bmax, float* values);
 bool tc_supported(const Layer& L);
 bool tc_bwd_supported(const Layer& L);
 int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* values,
-                         const float* flows, const float* scratch, float* f_params);
+                         const float* flows, const float* scratch, const float* rmax,
+                         float* f_params);
 int launch_child_flow_tc(const Layer& L, const BwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* values,
-                         const float* flows, const float* scratch, float* flow_scratch);
+                         const float* flows, const float* scratch, const float* rmax,
+                         float* flow_scratch);
 
 }  // namespace pcb

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(128, 1)
                  const int32_t* __restrict__ members, const int32_t* __restrict__ sum_ids,
                  const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
                  const float* __restrict__ theta, const float* __restrict__ scratch,
-                 float* __restrict__ values) {
+                 const float* __restrict__ bmax, float* __restrict__ values) {
   using SM = FwdSmem<KN>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[2];
@@ -113,14 +113,13 @@ __global__ void __launch_bounds__(128, 1)
   const int32_t* prow = prod_ids + (int64_t)r0 * cap;
   const int32_t* trow = param_ids + (int64_t)r0 * cap;
 
-  // per-sample maximum over every child of the super-row
+  // per-sample maximum over every child of the super-row, from the product
+  // kernel's per-block maxima (scratch block index = scratch row / k_n)
   float gm = PCB_NEG_INF;
   if (live)
     for (int c = 0; c < cap; ++c) {
       if (trow[c] == 0) continue;
-      const float* src = scratch + (int64_t)prow[c] * ldb + b;
-#pragma unroll 8
-      for (int j = 0; j < KN; ++j) gm = fmaxf(gm, src[(int64_t)j * ldb]);
+      gm = fmaxf(gm, bmax[(int64_t)(prow[c] / KN) * ldb + b]);
     }
   const bool dead = (gm == PCB_NEG_INF);
 
@@ -262,11 +261,11 @@ __global__ void __launch_bounds__(128, 1)
                     const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
                     const int32_t* __restrict__ flow_ids, const float* __restrict__ theta,
                     const float* __restrict__ values, const float* __restrict__ flows,
-                    const float* __restrict__ scratch, float* __restrict__ f_params) {
+                    const float* __restrict__ scratch, const float* __restrict__ rmax,
+                    int64_t sb_base, float* __restrict__ f_params) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
-  __shared__ float red[4][PF_KC];
   __shared__ float cb[PF_KC];
   __shared__ int cols[TC_NMAX / 16];
   __shared__ int ncols_s;
@@ -337,16 +336,21 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int q = 0; q < PF_KC; ++q)
       if (b0 + q >= B) ln[q] = PCB_NEG_INF;
-    // per-sample max over the 128 rows of the tile: warp max then 4-way
-#pragma unroll
-    for (int q = 0; q < PF_KC; ++q) {
-      float v = ln[q];
-      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == q) red[warp][q] = v;
-    }
     if (it >= 2) mbar_wait(smem_u32(&mbar[stage]), ((it - 2) >> 1) & 1);
-    __syncthreads();
-    if (tid < PF_KC) cb[tid] = fmaxf(fmaxf(red[0][tid], red[1][tid]), fmaxf(red[2][tid], red[3][tid]));
+    __syncthreads();  // previous chunk's readers of cb are done
+    // per-sample shift: max of the ratio-max rows of the tile's sum blocks
+    if (tid < PF_KC) {
+      float v = PCB_NEG_INF;
+      if (b0 + tid < B) {
+        const int s_lo = (mt * TC_M) / k_m;
+        const int s_hi = (min(mt * TC_M + TC_M, Nsum) - 1) / k_m;
+        for (int s = s_lo; s <= s_hi; ++s) {
+          const int64_t blk = (sum_ids[members[m0 + s]] - sb_base) / k_m;
+          v = fmaxf(v, rmax[blk * ldb + b0 + tid]);
+        }
+      }
+      cb[tid] = v;
+    }
     __syncthreads();
     uint8_t* sAh = smem + stage * PfSmem::kStage;
     uint8_t* sAl = sAh + PfSmem::kA;
@@ -467,6 +471,7 @@ __global__ void __launch_bounds__(128, 1)
                     const int32_t* __restrict__ par_ids, const int32_t* __restrict__ ppids,
                     const float* __restrict__ theta, const float* __restrict__ values,
                     const float* __restrict__ flows, const float* __restrict__ scratch,
+                    const float* __restrict__ rmax, int64_t sb_base,
                     float* __restrict__ flow_scratch) {
   using SM = CfSmem<KM>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -484,14 +489,12 @@ __global__ void __launch_bounds__(128, 1)
   const int32_t* parow = par_ids + (int64_t)r0 * cap;
   const int32_t* pprow = ppids + (int64_t)r0 * cap;
 
+  // per-sample max of lnf over every parent sum, from the ratio-max pass
   float gm = PCB_NEG_INF;
   if (live)
     for (int p = 0; p < cap; ++p) {
       if (pprow[p] == 0) continue;
-      const int64_t base = (int64_t)parow[p] * ldb + b;
-#pragma unroll 8
-      for (int k = 0; k < KM; ++k)
-        gm = fmaxf(gm, lnf_of(flows[base + (int64_t)k * ldb], values[base + (int64_t)k * ldb]));
+      gm = fmaxf(gm, rmax[((int64_t)parow[p] - sb_base) / KM * ldb + b]);
     }
   const bool dead = (gm == PCB_NEG_INF);
 
@@ -617,7 +620,8 @@ bool tc_bwd_supported(const Layer& L) {
 template <int KN>
 static int launch_pf_kn(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                         int B, int ldb, const float* theta, const float* values,
-                        const float* flows, const float* scratch, float* f_params) {
+                        const float* flows, const float* scratch, const float* rmax,
+                        float* f_params) {
   static bool attr_set = false;
   const int bytes = PfSmem::kBytes;
   if (!attr_set) {
@@ -632,19 +636,20 @@ static int launch_pf_kn(const Layer& L, const FwdGroup& g, const TcRows& tc, cud
   dim3 grid((unsigned)tc.count, (unsigned)mtiles, (unsigned)cgroups);
   k_param_flow_tc<KN><<<grid, TC_M, bytes, s>>>(
       (int)g.cap, (int)L.k_m, B, ldb, tc.row_off, tc.members, g.sum_ids, g.prod_ids,
-      g.param_ids, g.flow_ids, theta, values, flows, scratch, f_params);
+      g.param_ids, g.flow_ids, theta, values, flows, scratch, rmax, L.sb_base, f_params);
   return check_launch();
 }
 
 int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* values,
-                         const float* flows, const float* scratch, float* f_params) {
+                         const float* flows, const float* scratch, const float* rmax,
+                         float* f_params) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   switch (L.k_n) {
-    case 16: return launch_pf_kn<16>(L, g, tc, s, B, ldb, theta, values, flows, scratch, f_params);
-    case 32: return launch_pf_kn<32>(L, g, tc, s, B, ldb, theta, values, flows, scratch, f_params);
-    case 64: return launch_pf_kn<64>(L, g, tc, s, B, ldb, theta, values, flows, scratch, f_params);
+    case 16: return launch_pf_kn<16>(L, g, tc, s, B, ldb, theta, values, flows, scratch, rmax, f_params);
+    case 32: return launch_pf_kn<32>(L, g, tc, s, B, ldb, theta, values, flows, scratch, rmax, f_params);
+    case 64: return launch_pf_kn<64>(L, g, tc, s, B, ldb, theta, values, flows, scratch, rmax, f_params);
     default: return PCB_USAGE;
   }
 }
@@ -652,7 +657,8 @@ int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
 template <int KM>
 static int launch_cf_km(const Layer& L, const BwdGroup& g, const TcRows& tc, cudaStream_t s,
                         int B, int ldb, const float* theta, const float* values,
-                        const float* flows, const float* scratch, float* flow_scratch) {
+                        const float* flows, const float* scratch, const float* rmax,
+                        float* flow_scratch) {
   static bool attr_set = false;
   const int bytes = CfSmem<KM>::kBytes;
   if (!attr_set) {
@@ -665,19 +671,20 @@ static int launch_cf_km(const Layer& L, const BwdGroup& g, const TcRows& tc, cud
   k_child_flow_tc<KM><<<grid, TC_M, bytes, s>>>((int)g.cap, (int)L.k_n, B, ldb, tc.row_off,
                                                  tc.members, g.ch_ids, g.par_ids,
                                                  g.par_param_ids, theta, values, flows, scratch,
-                                                 flow_scratch);
+                                                 rmax, L.sb_base, flow_scratch);
   return check_launch();
 }
 
 int launch_child_flow_tc(const Layer& L, const BwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* values,
-                         const float* flows, const float* scratch, float* flow_scratch) {
+                         const float* flows, const float* scratch, const float* rmax,
+                         float* flow_scratch) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   switch (L.k_m) {
-    case 16: return launch_cf_km<16>(L, g, tc, s, B, ldb, theta, values, flows, scratch, flow_scratch);
-    case 32: return launch_cf_km<32>(L, g, tc, s, B, ldb, theta, values, flows, scratch, flow_scratch);
-    case 64: return launch_cf_km<64>(L, g, tc, s, B, ldb, theta, values, flows, scratch, flow_scratch);
+    case 16: return launch_cf_km<16>(L, g, tc, s, B, ldb, theta, values, flows, scratch, rmax, flow_scratch);
+    case 32: return launch_cf_km<32>(L, g, tc, s, B, ldb, theta, values, flows, scratch, rmax, flow_scratch);
+    case 64: return launch_cf_km<64>(L, g, tc, s, B, ldb, theta, values, flows, scratch, rmax, flow_scratch);
     default: return PCB_USAGE;
   }
 }
@@ -685,7 +692,7 @@ int launch_child_flow_tc(const Layer& L, const BwdGroup& g, const TcRows& tc, cu
 template <int KN>
 static int launch_fwd_kn(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* scratch,
-                         float* values) {
+                         const float* bmax, float* values) {
   static bool attr_set = false;
   const int bytes = FwdSmem<KN>::kBytes;
   if (!attr_set) {
@@ -697,18 +704,19 @@ static int launch_fwd_kn(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   dim3 grid((unsigned)tc.count, (unsigned)((B + TC_M - 1) / TC_M));
   k_sum_fwd_tc<KN><<<grid, TC_M, bytes, s>>>((int)g.cap, (int)L.k_m, B, ldb, tc.row_off,
                                               tc.members, g.sum_ids, g.prod_ids, g.param_ids,
-                                              theta, scratch, values);
+                                              theta, scratch, bmax, values);
   return check_launch();
 }
 
 int launch_sum_fwd_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
-                      int B, int ldb, const float* theta, const float* scratch, float* values) {
+                      int B, int ldb, const float* theta, const float* scratch,
+                      const float* bmax, float* values) {
   ProfScope prof_(KC_SUM_FWD_TC, s);
   if (!tc.count || !B) return PCB_OK;
   switch (L.k_n) {
-    case 16: return launch_fwd_kn<16>(L, g, tc, s, B, ldb, theta, scratch, values);
-    case 32: return launch_fwd_kn<32>(L, g, tc, s, B, ldb, theta, scratch, values);
-    case 64: return launch_fwd_kn<64>(L, g, tc, s, B, ldb, theta, scratch, values);
+    case 16: return launch_fwd_kn<16>(L, g, tc, s, B, ldb, theta, scratch, bmax, values);
+    case 32: return launch_fwd_kn<32>(L, g, tc, s, B, ldb, theta, scratch, bmax, values);
+    case 64: return launch_fwd_kn<64>(L, g, tc, s, B, ldb, theta, scratch, bmax, values);
     default: return PCB_USAGE;
   }
 }

@@ -27,10 +27,11 @@ SIGNATURES = {
     "pcb_check_batch": (_I, [_P, _P, _I, _I, _P, _P]),
     "pcb_transpose_batch_i64": (_I, [_P, _P, _I, _I, _P, _P]),
     "pcb_transpose_batch_i32": (_I, [_P, _P, _I, _I, _P, _P]),
-    "pcb_forward": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P]),
-    "pcb_backward": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "pcb_layer_forward": (_I, [_P, _I, _P, _I, _I, _P, _P, _P]),
-    "pcb_layer_backward": (_I, [_P, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "pcb_plan_workspace_floats": (_L, [_P, _I]),
+    "pcb_forward": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "pcb_backward": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "pcb_layer_forward": (_I, [_P, _I, _P, _I, _I, _P, _P, _P, _P]),
+    "pcb_layer_backward": (_I, [_P, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pcb_em_update": (_I, [_P, _P, _P, _P, _F, _F, _P]),
     "pcb_axpy_accumulate": (_I, [_P, _L, _P, _P]),
     "pcb_count_nonfinite": (_I, [_P, _L, _P, _P]),
@@ -40,7 +41,7 @@ SIGNATURES = {
     "pcb_tc_selftest": (_I, [_P, _I, _I, _P, _P, _P]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 

@@ -28,6 +28,7 @@ class EvalBuffers:
     prod_flows_full: object
     f_params: object     # fp32 [f_params_size]
     lroot: object        # fp32 [B]
+    work: object = None  # fp32 kernel workspace (block maxima), pcb_plan_workspace_floats
     batch: np.ndarray | None = None
     forward_done: bool = False
     backward_done: bool = False
@@ -55,12 +56,17 @@ class EvalBuffers:
         return self.prod_flows_full[:, : self.batch_size]
 
 
-def allocate_buffers(compiled, batch_size: int, device=None) -> EvalBuffers:
+def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None) -> EvalBuffers:
     """Zeroed device workspace for ``batch_size`` samples."""
     import torch
-    dev = torch.device(device if device is not None else "cuda")
+    from . import _lib
+    from .plan import device_plan
+    if plan is None:
+        plan = device_plan(compiled, device)
+    dev = plan.device
     b = int(batch_size)
     ldb = padded_stride(b)
+    n_work = int(_lib.load().pcb_plan_workspace_floats(plan.handle, ldb))
 
     def z(rows):
         return torch.zeros((max(int(rows), 1), ldb), dtype=torch.float32, device=dev)
@@ -75,5 +81,6 @@ def allocate_buffers(compiled, batch_size: int, device=None) -> EvalBuffers:
         prod_flows_full=z(compiled.num_prod_rows),
         f_params=torch.zeros(max(compiled.f_params_size, 1), dtype=torch.float32, device=dev),
         lroot=torch.zeros(max(b, 1), dtype=torch.float32, device=dev)[:b],
+        work=torch.zeros(max(n_work, 1), dtype=torch.float32, device=dev),
         device=dev,
     )

@@ -100,12 +100,13 @@ def forward(compiled, batch, *, batch_tile: int = 64, bufs: EvalBuffers | None =
         raise NumericError("parameter table contains non-finite values")
     B = _batch_rows(compiled, batch)
     if bufs is None or bufs.batch_size != B:
-        bufs = allocate_buffers(compiled, B, plan.device)
+        bufs = allocate_buffers(compiled, B, plan.device, plan=plan)
     with torch.cuda.device(plan.device):
         stage_batch(compiled, plan, batch, bufs, validate=validate)
         _lib.call("pcb_forward", plan.handle, _lib.stream_handle(), B, bufs.ldb,
                   bufs.xT.data_ptr(), plan.theta.data_ptr(), bufs.values_full.data_ptr(),
-                  bufs.scratch_full.data_ptr(), _lib.ptr(bufs.lroot) if B else 0)
+                  bufs.scratch_full.data_ptr(), _lib.ptr(bufs.lroot) if B else 0,
+                  bufs.work.data_ptr())
     bufs.forward_done = True
     bufs.backward_done = False
     return bufs.lroot, bufs
@@ -124,7 +125,7 @@ def backward(compiled, bufs: EvalBuffers, *, batch_tile: int = 64, device=None,
                   bufs.xT.data_ptr(), plan.theta.data_ptr(), bufs.values_full.data_ptr(),
                   bufs.flows_full.data_ptr(), bufs.scratch_full.data_ptr(),
                   bufs.flow_scratch_full.data_ptr(), bufs.prod_flows_full.data_ptr(),
-                  bufs.f_params.data_ptr())
+                  bufs.f_params.data_ptr(), bufs.work.data_ptr())
     bufs.backward_done = True
     return bufs
 
@@ -135,7 +136,7 @@ def layer_forward(compiled, layer: int, bufs: EvalBuffers, *, tensor_cores: bool
     plan = device_plan(compiled, bufs.device, tensor_cores=tensor_cores)
     _lib.call("pcb_layer_forward", plan.handle, layer, _lib.stream_handle(), bufs.batch_size,
               bufs.ldb, plan.theta.data_ptr(), bufs.values_full.data_ptr(),
-              bufs.scratch_full.data_ptr())
+              bufs.scratch_full.data_ptr(), bufs.work.data_ptr())
 
 
 def layer_backward(compiled, layer: int, bufs: EvalBuffers, *, tensor_cores: bool = True):
@@ -145,4 +146,4 @@ def layer_backward(compiled, layer: int, bufs: EvalBuffers, *, tensor_cores: boo
               bufs.ldb, plan.theta.data_ptr(), bufs.values_full.data_ptr(),
               bufs.flows_full.data_ptr(), bufs.scratch_full.data_ptr(),
               bufs.flow_scratch_full.data_ptr(), bufs.prod_flows_full.data_ptr(),
-              bufs.f_params.data_ptr())
+              bufs.f_params.data_ptr(), bufs.work.data_ptr())

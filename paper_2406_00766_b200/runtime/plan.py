@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 2
+VERSION = 3
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -143,6 +143,35 @@ def build_program(compiled, *, tensor_cores: bool = True):
             prog += [int(p.children.shape[1]), int(p.rows.size)]
             ref(p.rows)
             ref(p.children)
+        # derived: per-scratch-row product CSR (pad rows have no children)
+        fan = np.zeros(L.scratch_window, dtype=np.int64)
+        for ev in L.prod_evals:
+            fan[ev.out] = ev.children.shape[1]
+        row_off = np.concatenate([[0], np.cumsum(fan)]).astype(np.int64)
+        ch_flat = np.zeros(int(row_off[-1]), dtype=np.int64)
+        for ev in L.prod_evals:
+            f = ev.children.shape[1]
+            ch_flat[(row_off[ev.out][:, None] + np.arange(f)).ravel()] = ev.children.ravel()
+        ref(row_off)
+        ref(ch_flat)
+        # derived: sum-block range of the layer (contiguous value slots)
+        sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
+            np.zeros(0, np.int64)
+        prog += [int(sids.min()) if sids.size else 0, int(sids.size)]
+        # derived: fused accumulate + push table in product order
+        push_of = {}
+        for p in L.pushes:
+            for r, ch in zip(p.rows.tolist(), p.children):
+                push_of[r] = ch
+        flags = np.array([1 if r in push_of else 0 for r in L.prod_rows.tolist()], np.int64)
+        pfan = np.array([push_of[r].size if r in push_of else 0
+                         for r in L.prod_rows.tolist()], np.int64)
+        poff = np.concatenate([[0], np.cumsum(pfan)]).astype(np.int64)
+        pch = (np.concatenate([push_of[r] for r in L.prod_rows.tolist() if r in push_of])
+               if pfan.sum() else np.zeros(0, np.int64))
+        ref(flags)
+        ref(poff)
+        ref(pch)
 
     red = np.asarray(c.reductions, dtype=np.int64).reshape(-1, 3)
     if red.shape[0]:

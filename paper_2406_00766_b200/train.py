@@ -148,7 +148,7 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
                 B = hi - lo
                 bufs = bufs_cache.get(B)
                 if bufs is None:
-                    bufs = bufs_cache[B] = allocate_buffers(compiled, B, dev)
+                    bufs = bufs_cache[B] = allocate_buffers(compiled, B, dev, plan=plan)
                 idx = order_dev[a + lo:a + hi]
                 xb = data_dev.index_select(0, idx)
                 step_ll = torch.zeros((), dtype=torch.float64, device=dev)
@@ -158,13 +158,13 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
                     _lib.call("pcb_forward", plan.handle, stream, B, bufs.ldb,
                               bufs.xT.data_ptr(), plan.theta.data_ptr(),
                               bufs.values_full.data_ptr(), bufs.scratch_full.data_ptr(),
-                              bufs.lroot.data_ptr())
+                              bufs.lroot.data_ptr(), bufs.work.data_ptr())
                     step_ll += bufs.lroot.double().sum()
                 _lib.call("pcb_backward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
                           plan.theta.data_ptr(), bufs.values_full.data_ptr(),
                           bufs.flows_full.data_ptr(), bufs.scratch_full.data_ptr(),
                           bufs.flow_scratch_full.data_ptr(), bufs.prod_flows_full.data_ptr(),
-                          bufs.f_params.data_ptr())
+                          bufs.f_params.data_ptr(), bufs.work.data_ptr())
                 samples += b_all
                 if cfg.mode == "full":
                     _lib.call("pcb_axpy_accumulate", stream, ep_fp.numel(),
