@@ -62,6 +62,17 @@ int pcb_plan_destroy(pcb_plan* plan);
 /* Number of sum layers in the plan. */
 int pcb_plan_num_layers(const pcb_plan* plan);
 
+/* Rows of the all-layer product scratch (sum of layer windows): every layer's
+ * products stay resident between forward and backward. */
+int64_t pcb_plan_scratch_rows(const pcb_plan* plan);
+
+/* Bind the device buffer (>= the plan's MMA-tile element count, bf16) that holds
+ * the tensor-core copies of theta, and (re)derive them from d_theta: every
+ * tile of a tensor-core layer as bf16 hi + lo planes in UMMA core-matrix
+ * order.  Call pcb_theta_refresh after every change of theta. */
+int pcb_plan_set_mma(pcb_plan* plan, void* d_mma, int64_t elems);
+int pcb_theta_refresh(const pcb_plan* plan, void* stream, const float* d_theta);
+
 /* Validate a device batch (xT, [num_vars x ldb]) against the category counts:
  * writes the number of bad entries to *d_bad (device int32).
  * Replaces: pcirc/runtime/engine.py:36-52 (_validate_batch) for device batches. */
@@ -134,6 +145,11 @@ int pcb_profile_read(double* ms, int64_t* scopes, int64_t* launches, int n);
  * Used by tests to pin the UMMA descriptor encoding. */
 int pcb_tc_selftest(void* stream, int n, int k, const uint16_t* d_a, const uint16_t* d_b,
                     float* d_d);
+
+/* Same with B given as [k x n] row-major and read through an MN-major UMMA
+ * descriptor from the theta-tile layout (variant selects the LBO/SBO roles). */
+int pcb_tc_selftest_mn(void* stream, int n, int k, int variant, const uint16_t* d_a,
+                       const uint16_t* d_b, float* d_d);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 3;
+constexpr int64_t kVersion = 5;
 
 struct Reader {
   const int64_t* p;
@@ -70,6 +70,13 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->root_children = r.ref(&P->n_root_children);
   P->var_ncat = r.ref();
   P->use_tc = (int)r.get();
+  P->n_mma_tiles = r.get();
+  P->mma_elems = r.get();
+  P->mma_theta = r.ref();
+  P->mma_slab = r.ref();
+  P->mma_km = r.ref();
+  P->mma_kn = r.ref();
+  P->scratch_rows = r.get();
   int64_t n_chunks = r.get();
   for (int64_t c = 0; c < n_chunks && r.ok; ++c) {
     InputChunk ch;
@@ -80,6 +87,14 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     ch.pids = r.ref();
     P->inputs.push_back(ch);
   }
+  P->in_blocks.n = r.get();
+  P->in_blocks.var = r.ref();
+  P->in_blocks.ncat = r.ref();
+  P->in_blocks.slot0 = r.ref();
+  P->in_blocks.count = r.ref();
+  P->in_blocks.pid_off = r.ref();
+  P->in_blocks.pids = r.ref();
+  P->in_blocks.max_elems = r.get();
   int64_t n_layers = r.get();
   for (int64_t l = 0; l < n_layers && r.ok; ++l) {
     Layer L;
@@ -87,6 +102,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.k_n = r.get();
     L.window = r.get();
     L.n_prod = r.get();
+    L.scratch_off = r.get();
     L.pad_rows = r.ref(&L.n_pad);
     int64_t ne = r.get();
     for (int64_t e = 0; e < ne && r.ok; ++e) {
@@ -106,6 +122,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.prod_ids = r.ref();
       G.param_ids = r.ref();
       G.flow_ids = r.ref();
+      G.param_slab = r.ref();
       TcRows T;
       T.count = r.get();
       T.row_off = r.ref();
@@ -121,6 +138,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.ch_ids = r.ref();
       G.par_ids = r.ref();
       G.par_param_ids = r.ref();
+      G.par_slab = r.ref();
       TcRows T;
       T.count = r.get();
       T.row_off = r.ref();
@@ -173,6 +191,19 @@ int pcb_plan_destroy(pcb_plan* plan) {
 }
 
 int pcb_plan_num_layers(const pcb_plan* plan) { return plan ? (int)plan->layers.size() : -1; }
+
+int pcb_plan_set_mma(pcb_plan* plan, void* d_mma, int64_t elems) {
+  if (!plan || elems < plan->mma_elems) return PCB_USAGE;
+  plan->mma = reinterpret_cast<__nv_bfloat16*>(d_mma);
+  return PCB_OK;
+}
+
+int pcb_theta_refresh(const pcb_plan* plan, void* stream, const float* d_theta) {
+  if (!plan) return PCB_USAGE;
+  return launch_theta_to_mma(plan, as_stream(stream), d_theta);
+}
+
+int64_t pcb_plan_scratch_rows(const pcb_plan* plan) { return plan ? plan->scratch_rows : -1; }
 
 }  // extern "C"
 
@@ -232,14 +263,18 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   return w;
 }
 
+// Products of every layer stay resident in their own window of the
+// all-layer scratch, so the backward pass reads them instead of recomputing
+// (the reference recomputes into one shared window, engine.py:242).
 int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
-                  const float* theta, float* values, float* scratch, const Work& w) {
+                  const float* theta, float* values, float* scratch_all, const Work& w) {
+  float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
   int st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);
   if (st) return st;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.fwd_tc[g];
     if (P->use_tc && T.count > 0 && tc_supported(L))
-      st = launch_sum_fwd_tc(L, L.fwd[g], T, s, B, ldb, theta, scratch, w.bmax, values);
+      st = launch_sum_fwd_tc(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values);
     else
       st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, values);
     if (st) return st;
@@ -248,10 +283,10 @@ int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int 
 }
 
 int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
-                   const float* theta, const float* values, float* flows, float* scratch,
+                   const float* theta, const float* values, float* flows, float* scratch_all,
                    float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
-  int st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);  // recompute
-  if (st) return st;
+  float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
+  int st = PCB_OK;
   const bool tc = P->use_tc && tc_bwd_supported(L);
   if (tc) {
     st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax);
@@ -270,8 +305,8 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   for (size_t g = 0; g < L.bwd.size(); ++g) {
     const TcRows& T = L.bwd_tc[g];
     if (tc && T.count > 0)
-      st = launch_child_flow_tc(L, L.bwd[g], T, s, B, ldb, theta, values, flows, scratch,
-                                w.rmax, flow_scratch);
+      st = launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch, w.rmax,
+                                flow_scratch);
     else
       st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
                                   flow_scratch);

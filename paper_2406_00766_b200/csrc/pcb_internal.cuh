@@ -1,6 +1,7 @@
 // Internal declarations shared by the pcirc_b200 CUDA translation units.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -22,6 +23,15 @@ struct InputChunk {
   const int32_t *slots, *vars, *pids;
 };
 
+// Inputs staged per variable in shared memory: block b covers `count`
+// consecutive value slots from slot0 on variable var, each with an exclusive
+// pmf of ncat entries starting at pids[pid_off + i].
+struct InBlocks {
+  int64_t n = 0, max_elems = 0;
+  const int32_t *var = nullptr, *ncat = nullptr, *slot0 = nullptr, *count = nullptr,
+                *pid_off = nullptr, *pids = nullptr;
+};
+
 struct Bucket {  // product evaluation or push bucket
   int64_t f, n;
   const int32_t* idx;       // out scratch rows (eval) or prod-flow rows (push)
@@ -31,11 +41,13 @@ struct Bucket {  // product evaluation or push bucket
 struct FwdGroup {
   int64_t rows, cap;
   const int32_t *sum_ids, *prod_ids, *param_ids, *flow_ids;
+  const int32_t* param_slab;  // bf16 MMA-tile offset per (row, col), -1 for padding
 };
 
 struct BwdGroup {
   int64_t rows, cap;
   const int32_t *ch_ids, *par_ids, *par_param_ids;
+  const int32_t* par_slab;
 };
 
 // Tensor-core work list for one forward / backward group: "super-rows" stack
@@ -48,6 +60,7 @@ struct TcRows {
 
 struct Layer {
   int64_t k_m, k_n, window, n_prod;
+  int64_t scratch_off;  // first row of this layer's window in the all-layer scratch
   const int32_t* pad_rows;
   int64_t n_pad;
   std::vector<Bucket> evals;
@@ -81,7 +94,8 @@ struct pcb_plan {
   const int32_t* root_children;
   int64_t n_root_children;
   const int32_t* var_ncat;
-  std::vector<pcb::InputChunk> inputs;
+  std::vector<pcb::InputChunk> inputs;  // generic (gather / atomic) inputs
+  pcb::InBlocks in_blocks;              // shared-memory staged inputs
   std::vector<pcb::Layer> layers;
   // replica reductions grouped by destination tile
   int64_t red_n;
@@ -91,6 +105,11 @@ struct pcb_plan {
   const int32_t *group_idx, *group_off;
   int use_tc;  // 1: tensor-core sum kernels where the plan provides TC rows
   int64_t max_pb = 1, max_sb = 1;
+  // bf16 tensor-core copies of theta tiles (plan v4)
+  int64_t n_mma_tiles = 0, mma_elems = 0;
+  const int32_t *mma_theta = nullptr, *mma_slab = nullptr, *mma_km = nullptr, *mma_kn = nullptr;
+  __nv_bfloat16* mma = nullptr;  // bound by pcb_plan_set_mma
+  int64_t scratch_rows = 1;      // all-layer scratch rows (sum of layer windows)
 };
 
 namespace pcb {
@@ -166,18 +185,18 @@ int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, 
                 float v);
 
 // tensor-core kernels (pcb_tc.cu)
-int launch_sum_fwd_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
-                      int B, int ldb, const float* theta, const float* scratch,
-                      const float* bmax, float* values);
+int launch_sum_fwd_tc(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
+                      cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
+                      float* values);
 bool tc_supported(const Layer& L);
 bool tc_bwd_supported(const Layer& L);
+int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta);
 int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* values,
                          const float* flows, const float* scratch, const float* rmax,
                          float* f_params);
-int launch_child_flow_tc(const Layer& L, const BwdGroup& g, const TcRows& tc, cudaStream_t s,
-                         int B, int ldb, const float* theta, const float* values,
-                         const float* flows, const float* scratch, const float* rmax,
-                         float* flow_scratch);
+int launch_child_flow_tc(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
+                         cudaStream_t s, int B, int ldb, const float* values, const float* flows,
+                         const float* scratch, const float* rmax, float* flow_scratch);
 
 }  // namespace pcb

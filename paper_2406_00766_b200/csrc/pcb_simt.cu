@@ -109,9 +109,57 @@ __global__ void k_input_fwd(int64_t n, int B, int ldb, const int32_t* __restrict
   }
 }
 
+// Staged inputs (one CTA per block of <= 128 inputs on one variable): the
+// block's pmfs are read once, coalesced, as log-pmfs into shared memory; every
+// sample then reads its category's log-probability from smem and the values
+// rows are written coalesced along the batch.  Replaces 4-byte gathers that
+// each pull a 32-byte sector of a pmf table far larger than L2.
+constexpr int IN_THREADS = 512;
+
+__global__ void __launch_bounds__(IN_THREADS)
+    k_input_fwd_block(int B, int ldb, const int32_t* __restrict__ bvar,
+                      const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
+                      const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
+                      const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
+                      const float* __restrict__ theta, float* __restrict__ values) {
+  extern __shared__ float tbl[];
+  const int blk = blockIdx.x;
+  const int ncat = bncat[blk], cnt = bcount[blk], var = bvar[blk];
+  const int64_t slot0 = bslot0[blk];
+  const int32_t* pid = pids + bpoff[blk];
+  for (int i = 0; i < cnt; ++i) {
+    const float* src = theta + pid[i];
+    for (int q = threadIdx.x; q < ncat; q += IN_THREADS) tbl[i * ncat + q] = __logf(src[q]);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += IN_THREADS) {
+    const int x = xT[(int64_t)var * ldb + b];
+    float* dst = values + slot0 * ldb + b;
+    if (x < 0) {
+      for (int i = 0; i < cnt; ++i) dst[(int64_t)i * ldb] = 0.f;
+    } else {
+      for (int i = 0; i < cnt; ++i) dst[(int64_t)i * ldb] = tbl[i * ncat + x];
+    }
+  }
+}
+
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
                      const float* theta, float* values) {
   ProfScope prof_(KC_INPUT_FWD, s);
+  const InBlocks& ib = p->in_blocks;
+  if (ib.n) {
+    const int bytes = (int)ib.max_elems * 4;
+    static int attr = 0;
+    if (bytes > attr) {
+      if (cudaFuncSetAttribute(k_input_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               bytes) != cudaSuccess)
+        return PCB_CUDA;
+      attr = bytes;
+    }
+    k_input_fwd_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
+        B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, values);
+    if (check_launch()) return PCB_CUDA;
+  }
   for (auto& c : p->inputs) {
     int64_t total = c.n * B;
     if (!total) continue;
@@ -627,10 +675,72 @@ __global__ void k_input_param_flow(int ncat, int B, int ldb, const int32_t* __re
       atomicAdd(f_params + pid + q, tot * __ldg(theta + pid + q));
 }
 
+// Staged input flows: a shared-memory histogram [inputs x categories] of the
+// block's observed flows (smem atomics), plus the per-input missing-sample
+// flow spread over its pmf; the block owns its pmf ranges exclusively, so the
+// result is added to f_params with plain coalesced read-modify-writes.
+__global__ void __launch_bounds__(IN_THREADS)
+    k_input_flow_block(int B, int ldb, const int32_t* __restrict__ bvar,
+                       const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
+                       const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
+                       const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
+                       const float* __restrict__ theta, const float* __restrict__ flows,
+                       float* __restrict__ f_params) {
+  extern __shared__ float hist[];
+  __shared__ float miss[128];
+  const int blk = blockIdx.x;
+  const int ncat = bncat[blk], cnt = bcount[blk], var = bvar[blk];
+  const int64_t slot0 = bslot0[blk];
+  const int32_t* pid = pids + bpoff[blk];
+  for (int q = threadIdx.x; q < cnt * ncat; q += IN_THREADS) hist[q] = 0.f;
+  for (int q = threadIdx.x; q < cnt; q += IN_THREADS) miss[q] = 0.f;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += IN_THREADS) {
+    const int x = xT[(int64_t)var * ldb + b];
+    const float* src = flows + slot0 * ldb + b;
+    if (x < 0) {
+      for (int i = 0; i < cnt; ++i) {
+        const float f = src[(int64_t)i * ldb];
+        if (f != 0.f) atomicAdd(&miss[i], f);
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i) {
+        const float f = src[(int64_t)i * ldb];
+        if (f != 0.f) atomicAdd(&hist[i * ncat + x], f);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = 0; i < cnt; ++i) {
+    float* dst = f_params + pid[i];
+    const float* th = theta + pid[i];
+    const float m = miss[i];
+    for (int q = threadIdx.x; q < ncat; q += IN_THREADS) {
+      const float add = hist[i * ncat + q] + (m != 0.f ? m * th[q] : 0.f);
+      if (add != 0.f) dst[q] += add;
+    }
+  }
+}
+
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
                              float* f_params) {
   ProfScope prof_(KC_INPUT_FLOW, s);
+  const InBlocks& ib = p->in_blocks;
+  if (ib.n) {
+    const int bytes = (int)ib.max_elems * 4;
+    static int attr = 0;
+    if (bytes > attr) {
+      if (cudaFuncSetAttribute(k_input_flow_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               bytes) != cudaSuccess)
+        return PCB_CUDA;
+      attr = bytes;
+    }
+    k_input_flow_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
+        B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
+        f_params);
+    if (check_launch()) return PCB_CUDA;
+  }
   for (auto& c : p->inputs) {
     if (!c.n) continue;
     int threads = B >= 256 ? 256 : (B >= 128 ? 128 : 64);

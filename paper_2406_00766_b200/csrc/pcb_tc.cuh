@@ -34,6 +34,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);   // M / 16
 }
 
+// Same with B MN-major (bit 16): B's N dimension contiguous inside a core matrix.
+__host__ __device__ constexpr uint32_t idesc_bf16_bmn(int M, int N) {
+  return idesc_bf16(M, N) | (1u << 16);
+}
+
+// cp.async 16-byte global -> shared (L2 only), and group wait
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -121,6 +134,12 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int n) {
 // extent is kc elements of 2 bytes (core matrix = 8 rows x 8 elements)
 __device__ __forceinline__ uint32_t kmajor_off(int row, int k, int kc) {
   return (uint32_t)((((row >> 3) * (kc >> 3) + (k >> 3)) << 7) + ((row & 7) << 4) + ((k & 7) << 1));
+}
+
+// element offset of (row, col) inside a pre-split theta tile of `cols`
+// columns: 8x8 core matrices, cores ordered row-group-major
+__host__ __device__ __forceinline__ int tile_off(int row, int col, int cols) {
+  return ((row >> 3) * (cols >> 3) + (col >> 3)) * 64 + (row & 7) * 8 + (col & 7);
 }
 
 // split fp32 x into bf16 hi + bf16 lo with x ~= hi + lo (rel. error ~2^-17)

@@ -75,7 +75,7 @@ def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None) -> Ev
         batch_size=b, ldb=ldb,
         xT=torch.zeros((max(compiled.num_vars, 1), ldb), dtype=torch.int32, device=dev),
         values_full=z(compiled.num_value_slots),
-        scratch_full=z(compiled.scratch_size),
+        scratch_full=z(plan.info["scratch_rows"]),  # every layer's window stays resident
         flows_full=z(compiled.num_value_slots),
         flow_scratch_full=z(compiled.scratch_size),
         prod_flows_full=z(compiled.num_prod_rows),

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 3
+VERSION = 5
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -69,6 +69,105 @@ def tc_super_rows(prod_ids: np.ndarray, k_m: int, nmax: int = TC_NMAX):
     return np.asarray(offs, dtype=np.int64), np.concatenate(members).astype(np.int64)
 
 
+TC_K = (16, 32, 64)
+
+
+def tc_layer(L) -> bool:
+    """Layers whose sum contractions run on tcgen05 (block sizes 16 / 32 / 64)."""
+    return L.k_m in TC_K and L.k_n in TC_K
+
+
+def mma_tiles(compiled, tensor_cores: bool = True):
+    """Unique parameter tiles of tensor-core layers and their bf16 slab offsets.
+
+    Returns (theta starts sorted, slab offsets, k_m, k_n, total bf16 elements);
+    each tile occupies 2 * k_m * k_n bf16 (hi plane, lo plane)."""
+    starts, kms, kns = [], [], []
+    if tensor_cores:
+        for L in compiled.layers:
+            if not tc_layer(L):
+                continue
+            ids = np.unique(np.concatenate([g.param_ids[g.param_ids != 0]
+                                            for g in L.fwd_groups]))
+            starts.append(ids)
+            kms.append(np.full(ids.size, L.k_m, np.int64))
+            kns.append(np.full(ids.size, L.k_n, np.int64))
+    if not starts:
+        z = np.zeros(0, np.int64)
+        return z, z, z, z, 0
+    s = np.concatenate(starts)
+    km = np.concatenate(kms)
+    kn = np.concatenate(kns)
+    s, first = np.unique(s, return_index=True)  # a tied tile may recur across layers
+    km, kn = km[first], kn[first]
+    size = 2 * km * kn
+    slab = np.concatenate([[0], np.cumsum(size)[:-1]]).astype(np.int64)
+    return s, slab, km, kn, int(size.sum())
+
+
+IN_BLOCK_ELEMS = 32768   # pmf entries staged in shared memory per input block (128 KB)
+
+
+def input_blocks(compiled):
+    """Split the input layer into shared-memory blocks and generic leftovers.
+
+    A block is a run of inputs on one variable with consecutive value slots
+    and exclusively owned pmfs (no other input shares the pmf range), at most
+    ``IN_BLOCK_ELEMS // ncat`` inputs.  Returns (blocks, leftover chunks):
+    blocks = dict of arrays var, ncat, slot0, count, pid_off + flat pids;
+    leftovers = list of (ncat, slots, vars, pids).
+    """
+    all_pids = np.concatenate([ch.param_ids for ch in compiled.input_layer]) \
+        if compiled.input_layer else np.zeros(0, np.int64)
+    uniq, counts = np.unique(all_pids, return_counts=True)
+    blk = {k: [] for k in ("var", "ncat", "slot0", "count", "pid_off")}
+    pid_flat: list[np.ndarray] = []
+    n_pid = 0
+    leftovers = []
+    for ch in compiled.input_layer:
+        ncat = int(ch.num_categories)
+        per = IN_BLOCK_ELEMS // ncat if ncat <= IN_BLOCK_ELEMS // 8 else 0
+        per = min(per, 128)
+        excl = counts[np.searchsorted(uniq, ch.param_ids)] == 1
+        n = ch.slots.size
+        take = np.zeros(n, dtype=bool)
+        if per >= 8 and n:
+            # maximal runs: same var, consecutive slots, exclusive pmf
+            brk = np.ones(n, dtype=bool)
+            brk[1:] = (ch.vars[1:] != ch.vars[:-1]) | (ch.slots[1:] != ch.slots[:-1] + 1) | \
+                ~excl[1:] | ~excl[:-1]
+            starts = np.flatnonzero(brk)
+            ends = np.concatenate([starts[1:], [n]])
+            for a, z in zip(starts.tolist(), ends.tolist()):
+                if not excl[a] or z - a < 8:
+                    continue
+                for s0 in range(a, z, per):
+                    s1 = min(z, s0 + per)
+                    blk["var"].append(int(ch.vars[s0]))
+                    blk["ncat"].append(ncat)
+                    blk["slot0"].append(int(ch.slots[s0]))
+                    blk["count"].append(s1 - s0)
+                    blk["pid_off"].append(n_pid)
+                    pid_flat.append(ch.param_ids[s0:s1])
+                    n_pid += s1 - s0
+                take[a:z] = True
+        rest = ~take
+        if rest.any():
+            leftovers.append((ncat, ch.slots[rest], ch.vars[rest], ch.param_ids[rest]))
+    arrays = {k: np.asarray(v, dtype=np.int64) for k, v in blk.items()}
+    arrays["pids"] = np.concatenate(pid_flat) if pid_flat else np.zeros(0, np.int64)
+    return arrays, leftovers
+
+
+def _slab_of(ids, starts, slab):
+    """Slab offset per parameter-tile id (-1 for the zero tile / padding)."""
+    out = np.full(ids.shape, -1, dtype=np.int64)
+    nz = ids != 0
+    if nz.any():
+        out[nz] = slab[np.searchsorted(starts, ids[nz])]
+    return out
+
+
 def build_program(compiled, *, tensor_cores: bool = True):
     """Return (program int64 array, blob int32 array, info dict)."""
     blob = _Blob()
@@ -84,18 +183,35 @@ def build_program(compiled, *, tensor_cores: bool = True):
     ref(c.root_children if c.root_children is not None else np.zeros(0, np.int64))
     ref(np.asarray(c.var_categories, dtype=np.int64))
     prog.append(1 if tensor_cores else 0)
+    t_start, t_slab, t_km, t_kn, mma_elems = mma_tiles(c, tensor_cores)
+    prog += [int(t_start.size), mma_elems]
+    ref(t_start)
+    ref(t_slab)
+    ref(t_km)
+    ref(t_kn)
+    scratch_total = int(sum(L.scratch_window for L in c.layers)) or 1
+    prog.append(scratch_total)
 
-    prog.append(len(c.input_layer))
-    for ch in c.input_layer:
-        prog += [int(ch.num_categories), int(ch.node_ids.size)]
-        ref(ch.slots)
-        ref(ch.vars)
-        ref(ch.param_ids)
+    blocks, leftovers = input_blocks(c)
+    prog.append(len(leftovers))
+    for ncat, slots, vars_, pids in leftovers:
+        prog += [ncat, int(slots.size)]
+        ref(slots)
+        ref(vars_)
+        ref(pids)
+    nb = int(blocks["var"].size)
+    prog.append(nb)
+    for key in ("var", "ncat", "slot0", "count", "pid_off", "pids"):
+        ref(blocks[key])
+    prog.append(int((blocks["ncat"] * blocks["count"]).max()) if nb else 0)
 
     n_tc_rows = 0
+    scratch_off = 0
     prog.append(len(c.layers))
     for L in c.layers:
-        prog += [L.k_m, L.k_n, L.scratch_window, int(L.prod_slots.size)]
+        prog += [L.k_m, L.k_n, L.scratch_window, int(L.prod_slots.size), scratch_off]
+        scratch_off += L.scratch_window
+        use_tc = tensor_cores and tc_layer(L)
         written = np.concatenate([ev.out for ev in L.prod_evals]) if L.prod_evals else \
             np.zeros(0, np.int64)
         pad = np.setdiff1d(np.arange(L.scratch_window, dtype=np.int64), written)
@@ -113,7 +229,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.prod_ids)
             ref(g.param_ids)
             ref(g.flow_ids)
-            if tensor_cores and L.k_n in (16, 32, 64) and rows:
+            ref(_slab_of(g.param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
+            if use_tc and rows:
                 offs, mem = tc_super_rows(g.prod_ids, L.k_m)
                 prog.append(offs.size - 1)
                 ref(offs)
@@ -128,7 +245,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.ch_ids)
             ref(g.par_ids)
             ref(g.par_param_ids)
-            if tensor_cores and L.k_n in (16, 32, 64) and L.k_m in (16, 32, 64) and rows:
+            ref(_slab_of(g.par_param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
+            if use_tc and rows:
                 offs, mem = tc_super_rows(g.par_ids, L.k_n)
                 prog.append(offs.size - 1)
                 ref(offs)
@@ -195,7 +313,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
     ref(c.group_idx)
     ref(c.group_off)
     prog.append(MAGIC)
-    info = {"blob_elems": blob.size, "tc_super_rows": n_tc_rows}
+    info = {"blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+            "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
 
 
@@ -218,10 +337,17 @@ class DevicePlan:
                       self.blob.numel(), _lib.C.byref(handle))
         self.handle = handle
         self.theta = torch.empty(compiled.theta_size, dtype=torch.float32, device=self.device)
+        # bf16 hi/lo tensor-core copies of theta (derived; refreshed after every update)
+        self.mma = torch.zeros(max(info["mma_elems"], 8), dtype=torch.bfloat16, device=self.device)
+        _lib.call("pcb_plan_set_mma", handle, self.mma.data_ptr(), info["mma_elems"])
         self.status = torch.zeros(4, dtype=torch.int32, device=self.device)
         self.num_layers = lib.pcb_plan_num_layers(handle)
         self.theta_source = None
         self.upload_theta(compiled.theta)
+
+    def refresh_mma(self) -> None:
+        """Re-derive the bf16 tensor-core tiles from ``self.theta`` (after any change)."""
+        _lib.call("pcb_theta_refresh", self.handle, _lib.stream_handle(), self.theta.data_ptr())
 
     def upload_theta(self, theta) -> None:
         """Copy a host (numpy) or device theta into the plan's fp32 table."""
@@ -238,6 +364,8 @@ class DevicePlan:
             self.theta.copy_(t)
             self.theta_finite = bool(torch.isfinite(self.theta).all().item())
         self.theta_source = theta
+        with torch.cuda.device(self.device):
+            self.refresh_mma()
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -67,7 +67,8 @@ def test_hclt_block_sizes(k):
 def test_tied_hmm_column_groups_and_replicas():
     from paper_2406_00766_b200 import structures as S
     from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
-    g = S.build_hmm(S.StructureConfig(kind="hmm", seq_len=4, hidden_dim=512, vocab_size=30,
+    # 6 positions -> 5 tied transition layers > contention threshold 4 -> replicas
+    g = S.build_hmm(S.StructureConfig(kind="hmm", seq_len=6, hidden_dim=512, vocab_size=30,
                                       seed=1, tied=True))
     c = compile_circuit(g, CompileConfig(block_size=32))
     assert max(gr.prod_ids.shape[1] for L in c.layers for gr in L.fwd_groups) * 32 > 256
