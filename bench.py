@@ -55,6 +55,25 @@ def log(*a):
 
 
 def build_circuit(w):
+    """Generate + compile the workload circuit.  ``PCB_CIRCUIT_CACHE=<dir>``
+    pickles the compiled IR so repeated runs on one box skip the compile."""
+    cache = os.environ.get("PCB_CIRCUIT_CACHE")
+    if cache:
+        import pickle
+        key = "_".join(f"{k}{v}" for k, v in sorted(w.items()) if k != "desc")
+        path = Path(cache) / f"{key}.pkl"
+        if path.exists():
+            with open(path, "rb") as f:
+                return pickle.load(f)
+        c = _build_circuit(w)
+        path.parent.mkdir(parents=True, exist_ok=True)
+        with open(path, "wb") as f:
+            pickle.dump(c, f, protocol=5)
+        return c
+    return _build_circuit(w)
+
+
+def _build_circuit(w):
     from paper_2406_00766_b200 import structures as S
     from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
     if w["kind"] == "hclt":

@@ -127,9 +127,20 @@ __global__ void __launch_bounds__(IN_THREADS)
   const int ncat = bncat[blk], cnt = bcount[blk], var = bvar[blk];
   const int64_t slot0 = bslot0[blk];
   const int32_t* pid = pids + bpoff[blk];
-  for (int i = 0; i < cnt; ++i) {
-    const float* src = theta + pid[i];
-    for (int q = threadIdx.x; q < ncat; q += IN_THREADS) tbl[i * ncat + q] = __logf(src[q]);
+  const int total = cnt * ncat;
+  // stage log-pmfs: 4 independent loads in flight per thread
+  for (int q0 = threadIdx.x; q0 < total; q0 += 4 * IN_THREADS) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * IN_THREADS;
+      v[u] = (q < total) ? __ldg(theta + pid[q / ncat] + (q % ncat)) : 1.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * IN_THREADS;
+      if (q < total) tbl[q] = __logf(v[u]);
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < B; b += IN_THREADS) {
@@ -138,6 +149,7 @@ __global__ void __launch_bounds__(IN_THREADS)
     if (x < 0) {
       for (int i = 0; i < cnt; ++i) dst[(int64_t)i * ldb] = 0.f;
     } else {
+#pragma unroll 8
       for (int i = 0; i < cnt; ++i) dst[(int64_t)i * ldb] = tbl[i * ncat + x];
     }
   }
@@ -698,27 +710,24 @@ __global__ void __launch_bounds__(IN_THREADS)
   for (int b = threadIdx.x; b < B; b += IN_THREADS) {
     const int x = xT[(int64_t)var * ldb + b];
     const float* src = flows + slot0 * ldb + b;
-    if (x < 0) {
-      for (int i = 0; i < cnt; ++i) {
-        const float f = src[(int64_t)i * ldb];
-        if (f != 0.f) atomicAdd(&miss[i], f);
-      }
-    } else {
-      for (int i = 0; i < cnt; ++i) {
-        const float f = src[(int64_t)i * ldb];
-        if (f != 0.f) atomicAdd(&hist[i * ncat + x], f);
-      }
+    float* row = (x < 0) ? miss : hist + x;
+    const int step = (x < 0) ? 1 : ncat;
+    for (int i0 = 0; i0 < cnt; i0 += 8) {
+      float f[8];  // 8 independent loads in flight before the smem atomics
+#pragma unroll
+      for (int u = 0; u < 8; ++u) f[u] = (i0 + u < cnt) ? src[(int64_t)(i0 + u) * ldb] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (f[u] != 0.f) atomicAdd(row + (i0 + u) * step, f[u]);
     }
   }
   __syncthreads();
-  for (int i = 0; i < cnt; ++i) {
-    float* dst = f_params + pid[i];
-    const float* th = theta + pid[i];
+  const int total = cnt * ncat;
+  for (int q = threadIdx.x; q < total; q += IN_THREADS) {
+    const int i = q / ncat, c = q - i * ncat;
     const float m = miss[i];
-    for (int q = threadIdx.x; q < ncat; q += IN_THREADS) {
-      const float add = hist[i * ncat + q] + (m != 0.f ? m * th[q] : 0.f);
-      if (add != 0.f) dst[q] += add;
-    }
+    const float add = hist[q] + (m != 0.f ? m * __ldg(theta + pid[i] + c) : 0.f);
+    if (add != 0.f) f_params[pid[i] + c] += add;
   }
 }
 

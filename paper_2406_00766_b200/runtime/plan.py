@@ -105,7 +105,7 @@ def mma_tiles(compiled, tensor_cores: bool = True):
     return s, slab, km, kn, int(size.sum())
 
 
-IN_BLOCK_ELEMS = 32768   # pmf entries staged in shared memory per input block (128 KB)
+IN_BLOCK_ELEMS = 16384   # pmf entries staged in shared memory per input block (64 KB)
 
 
 def input_blocks(compiled):
