@@ -252,10 +252,19 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
         theta_size += int(first_ncat.sum())
         starts = gstart[gid]
         pmf_phys_of[in_ids] = starts
-        rng_slots = np.repeat(in_slot, in_ncat)
-        rng_off = np.arange(rng_slots.size) - np.repeat(np.cumsum(in_ncat) - in_ncat, in_ncat)
-        rng_phys = np.repeat(starts, in_ncat) + rng_off
-        rng_slots = rng_slots + rng_off
+        # expand each distinct (slot range, pmf) pairing once: inputs that share
+        # slots (tied HMM emissions) would otherwise repeat identical writes
+        _, ufirst = np.unique(np.stack([in_slot, in_ncat, starts], axis=1), axis=0,
+                              return_index=True)
+        ufirst = np.sort(ufirst)
+        o = np.argsort(in_slot[ufirst], kind="stable")
+        s_sorted, n_sorted = in_slot[ufirst][o], in_ncat[ufirst][o]
+        if np.any(s_sorted[1:] < s_sorted[:-1] + n_sorted[:-1]):
+            ufirst = np.arange(in_ids.size)  # overlapping ranges: keep write order exact
+        u_slot, u_ncat, u_start = in_slot[ufirst], in_ncat[ufirst], starts[ufirst]
+        rng_off = np.arange(int(u_ncat.sum())) - np.repeat(np.cumsum(u_ncat) - u_ncat, u_ncat)
+        rng_phys = np.repeat(u_start, u_ncat) + rng_off
+        rng_slots = np.repeat(u_slot, u_ncat) + rng_off
         slot_phys[rng_slots] = rng_phys
         assigned.append((rng_slots, rng_phys))
 
@@ -630,40 +639,56 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
 
 
 def _simplex_groups_general(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
-    members: list[np.ndarray] = []
-    range_key: dict[tuple, int] = {}
-    hash_key: dict[tuple, list] = {}
-
-    def add_range(start: int, n: int):
-        k = (start, n)
-        if k not in range_key:
-            range_key[k] = len(members)
-            members.append(np.arange(start, start + n, dtype=np.int64))
-
+    """Exact dedupe of every node's sorted physical positions, numbered by the
+    first node (in id order) that has them.  Contiguous position sets are keyed
+    as (start, n) ranges (inputs' pmfs and contiguous sums share that space);
+    other sum rows are grouped per fan-in with hashed row grouping."""
+    cand_id, cand_kind, cand_ref = [], [], []   # kind 0: range, 1: row of fan-in table
+    r_start, r_n = [], []
+    rows_by_f: dict[int, list] = {}
+    in_ids, _, in_ncat, _ = g.input_table()
+    if in_ids.size:
+        r_start.append(pmf_phys_of[in_ids])
+        r_n.append(in_ncat)
+        cand_id.append(in_ids)
     for s in g.segments:
-        if s.kind == KIND_INPUT:
-            starts = pmf_phys_of[s.start:s.stop]
-            for st, n in zip(starts.tolist(), s.ncat.tolist()):
-                add_range(st, n)
-        elif s.kind == KIND_SUM:
-            phys = np.sort(slot_phys[s.slots], axis=1)
-            n, f = phys.shape
-            contig = (phys[:, -1] - phys[:, 0] == f - 1)
-            if f > 1:
-                contig &= np.all(np.diff(phys, axis=1) == 1, axis=1)
-            lgid, lfirst = group_matrix_rows(phys)
-            hs = row_hashes(phys[lfirst])
-            for j, r in enumerate(lfirst.tolist()):
-                if contig[r]:
-                    add_range(int(phys[r, 0]), f)
-                    continue
-                key = (f, int(hs[j]))
-                lst = hash_key.setdefault(key, [])
-                if not any(np.array_equal(members[gi], phys[r]) for gi in lst):
-                    lst.append(len(members))
-                    members.append(phys[r].copy())
-    if not members:
+        if s.kind != KIND_SUM:
+            continue
+        phys = np.sort(slot_phys[s.slots], axis=1)
+        f = phys.shape[1]
+        contig = (phys[:, -1] - phys[:, 0] == f - 1)
+        if f > 1:
+            contig &= np.all(np.diff(phys, axis=1) == 1, axis=1)
+        ids = np.arange(s.start, s.stop, dtype=np.int64)
+        if contig.any():
+            r_start.append(phys[contig, 0])
+            r_n.append(np.full(int(contig.sum()), f, np.int64))
+            cand_id.append(ids[contig])
+        if (~contig).any():
+            rows_by_f.setdefault(f, []).append((ids[~contig], phys[~contig]))
+    groups = []  # (first node id, member array)
+    if r_start:
+        rs = np.concatenate(r_start)
+        rn = np.concatenate(r_n)
+        rid = np.concatenate(cand_id)
+        order = np.argsort(rid, kind="stable")
+        key = np.stack([rs[order], rn[order]], axis=1)
+        _, first = np.unique(key, axis=0, return_index=True)
+        for fi in first.tolist():
+            st, n = int(key[fi, 0]), int(key[fi, 1])
+            groups.append((int(rid[order][fi]), np.arange(st, st + n, dtype=np.int64)))
+    for f, parts in rows_by_f.items():
+        ids = np.concatenate([p[0] for p in parts])
+        mat = np.concatenate([p[1] for p in parts])
+        order = np.argsort(ids, kind="stable")
+        ids, mat = ids[order], mat[order]
+        _, first = group_matrix_rows(mat)
+        for fi in first.tolist():
+            groups.append((int(ids[fi]), mat[fi]))
+    if not groups:
         return np.zeros(0, dtype=np.int64), np.zeros(1, dtype=np.int64)
+    groups.sort(key=lambda t: t[0])
+    members = [m for _, m in groups]
     sizes = np.array([m.size for m in members], dtype=np.int64)
     group_idx = np.concatenate(members)
     group_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
