@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 5;
+constexpr int64_t kVersion = 6;
 
 struct Reader {
   const int64_t* p;
@@ -123,12 +123,16 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.param_ids = r.ref();
       G.flow_ids = r.ref();
       G.param_slab = r.ref();
-      TcRows T;
+      TcRows T, Tp;
       T.count = r.get();
       T.row_off = r.ref();
       T.members = r.ref();
+      Tp.count = r.get();
+      Tp.row_off = r.ref();
+      Tp.members = r.ref();
       L.fwd.push_back(G);
       L.fwd_tc.push_back(T);
+      L.pf_tc.push_back(Tp);
     }
     int64_t nb = r.get();
     for (int64_t g = 0; g < nb && r.ok; ++g) {
@@ -293,7 +297,7 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     if (st) return st;
   }
   for (size_t g = 0; g < L.fwd.size(); ++g) {
-    const TcRows& T = L.fwd_tc[g];
+    const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
       st = launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
                                 w.rmax, f_params);

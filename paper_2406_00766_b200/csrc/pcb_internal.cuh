@@ -67,6 +67,7 @@ struct Layer {
   std::vector<FwdGroup> fwd;
   std::vector<BwdGroup> bwd;
   std::vector<TcRows> fwd_tc;   // aligned with fwd (count 0 = no TC plan)
+  std::vector<TcRows> pf_tc;    // aligned with fwd: full stacks for the param-flow kernel
   std::vector<TcRows> bwd_tc;   // aligned with bwd
   const int32_t *prod_slots, *prod_rows;
   std::vector<Bucket> pushes;

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 5
+VERSION = 6
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -48,12 +48,22 @@ class _Blob:
         return np.concatenate(self.parts)
 
 
-def tc_super_rows(prod_ids: np.ndarray, k_m: int, nmax: int = TC_NMAX):
-    """Stack group rows with identical child rows into <= nmax-sum super-rows."""
+SMS = 148  # B200 streaming multiprocessors
+
+
+def tc_super_rows(prod_ids: np.ndarray, k_m: int, nmax: int = TC_NMAX, min_count: int = 0):
+    """Stack group rows with identical child rows into <= nmax-sum super-rows.
+
+    ``min_count`` caps the stack so the layer still yields about that many
+    super-rows (CTAs): stacking shares one operand conversion across up to
+    ``nmax / k_m`` blocks, but a layer of a few identical rows (HMM: 128 rows)
+    must not collapse into a handful of CTAs on a 148-SM part."""
     rows = prod_ids.shape[0]
     if rows == 0:
         return np.zeros(1, np.int64), np.zeros(0, np.int64)
     per = max(1, nmax // max(k_m, 1))
+    if min_count:
+        per = max(1, min(per, rows // min_count))
     gid, first = group_matrix_rows(prod_ids)
     order = np.argsort(gid, kind="stable")
     sizes = np.bincount(gid)
@@ -231,13 +241,16 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.flow_ids)
             ref(_slab_of(g.param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
             if use_tc and rows:
-                offs, mem = tc_super_rows(g.prod_ids, L.k_m)
-                prog.append(offs.size - 1)
-                ref(offs)
-                ref(mem)
-                n_tc_rows += offs.size - 1
+                # forward: enough super-rows to fill the SMs; param flows: full
+                # stacks (their grid also spans column groups)
+                for mc in (SMS, 0):
+                    offs, mem = tc_super_rows(g.prod_ids, L.k_m, min_count=mc)
+                    prog.append(offs.size - 1)
+                    ref(offs)
+                    ref(mem)
+                    n_tc_rows += offs.size - 1
             else:
-                prog += [0, 0, 0, 0, 0]
+                prog += [0, 0, 0, 0, 0] * 2
         prog.append(len(L.bwd_groups))
         for g in L.bwd_groups:
             rows, cap = g.par_ids.shape
@@ -247,7 +260,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.par_param_ids)
             ref(_slab_of(g.par_param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
             if use_tc and rows:
-                offs, mem = tc_super_rows(g.par_ids, L.k_n)
+                offs, mem = tc_super_rows(g.par_ids, L.k_n, min_count=SMS)
                 prog.append(offs.size - 1)
                 ref(offs)
                 ref(mem)

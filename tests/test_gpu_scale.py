@@ -73,7 +73,7 @@ def test_tied_hmm_column_groups_and_replicas():
     c = compile_circuit(g, CompileConfig(block_size=32))
     assert max(gr.prod_ids.shape[1] for L in c.layers for gr in L.fwd_groups) * 32 > 256
     assert len(c.reductions) > 0
-    x = np.random.default_rng(3).integers(0, 30, size=(70, 4))
+    x = np.random.default_rng(3).integers(0, 30, size=(70, 6))
     _compare(c, x)
 
 
