@@ -237,46 +237,60 @@ int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, f
   return check_launch();
 }
 
-// One CTA per (product block, 512-sample slab): every scratch row of the block
-// is the sum of its children's log values (-inf for window padding), written
-// with float4 along the batch; the per-sample block maximum goes to bmax so
-// the sum contraction needs no max pre-pass.
-constexpr int VB = 4;             // samples per thread (float4)
-constexpr int SLAB = 128 * VB;    // samples per CTA
+// One CTA per (product block, 128-sample slab): 8 warps stride over the
+// block's scratch rows, lane = 4 consecutive samples (float4).  Every row is
+// the sum of its children's log values (-inf for window padding); the
+// per-sample block maximum goes to bmax (reduced across warps in shared
+// memory) so the sum contraction needs no max pre-pass.
+constexpr int VB = 4;              // samples per lane (float4)
+constexpr int SLAB = 32 * VB;      // samples per CTA
+constexpr int RW = 8;              // warps per CTA (rows in flight)
 
 __device__ __forceinline__ float4 f4max(float4 a, float4 b) {
   return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), fmaxf(a.w, b.w));
 }
 
-__global__ void __launch_bounds__(128)
+// max over the RW warps' float4 partials; warp 0 writes the result
+__device__ __forceinline__ void block_max_store(float4 mx, float* __restrict__ dst, bool live) {
+  __shared__ float4 red[RW][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  red[warp][lane] = mx;
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int w = 1; w < RW; ++w) mx = f4max(mx, red[w][lane]);
+    if (live) *reinterpret_cast<float4*>(dst) = mx;
+  }
+}
+
+__global__ void __launch_bounds__(RW * 32)
     k_prod_block(int k_n, int B, int ldb, const int32_t* __restrict__ row_off,
                  const int32_t* __restrict__ ch, const float* __restrict__ values,
                  float* __restrict__ scratch, float* __restrict__ bmax) {
   const int blk = blockIdx.x;
-  const int b = blockIdx.y * SLAB + threadIdx.x * VB;
-  if (b >= B) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.y * SLAB + lane * VB;
+  const bool live = b < B;
   const float ninf = PCB_NEG_INF;
   float4 mx = make_float4(ninf, ninf, ninf, ninf);
-  for (int j = 0; j < k_n; ++j) {
+  for (int j = warp; j < k_n; j += RW) {
     const int r = blk * k_n + j;
-    const int a = row_off[r], z = row_off[r + 1];
-    float4 acc;
-    if (a == z) {
-      acc = make_float4(ninf, ninf, ninf, ninf);
-    } else {
-      acc = *reinterpret_cast<const float4*>(values + (int64_t)ch[a] * ldb + b);
+    const int a = __ldg(row_off + r), z = __ldg(row_off + r + 1);
+    float4 acc = make_float4(ninf, ninf, ninf, ninf);
+    if (a < z && live) {
+      acc = *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + a) * ldb + b);
       for (int q = a + 1; q < z; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(values + (int64_t)ch[q] * ldb + b);
+        const float4 v = *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + q) * ldb + b);
         acc.x += v.x;
         acc.y += v.y;
         acc.z += v.z;
         acc.w += v.w;
       }
     }
-    *reinterpret_cast<float4*>(scratch + (int64_t)r * ldb + b) = acc;
+    if (live) *reinterpret_cast<float4*>(scratch + (int64_t)r * ldb + b) = acc;
     mx = f4max(mx, acc);
   }
-  *reinterpret_cast<float4*>(bmax + (int64_t)blk * ldb + b) = mx;
+  block_max_store(mx, bmax + (int64_t)blk * ldb + b, live);
 }
 
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
@@ -284,31 +298,33 @@ int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float
   ProfScope prof_(KC_PROD_EVAL, s);
   if (!B || !L.n_pb) return PCB_OK;
   dim3 grid((unsigned)L.n_pb, (unsigned)((B + SLAB - 1) / SLAB));
-  k_prod_block<<<grid, 128, 0, s>>>((int)L.k_n, B, ldb, L.prow_off, L.prow_ch, values, scratch,
-                                    bmax);
+  k_prod_block<<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off, L.prow_ch, values,
+                                        scratch, bmax);
   return check_launch();
 }
 
 // rmax[sb, b] = max over the block's sums of log(flow) - log(value) (-inf for
 // impossible sums): the per-sample shift for the flow contractions.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(RW * 32)
     k_ratio_max(int k_m, int B, int ldb, int64_t sb_base, const float* __restrict__ values,
                 const float* __restrict__ flows, float* __restrict__ rmax) {
   const int blk = blockIdx.x;
-  const int b = blockIdx.y * SLAB + threadIdx.x * VB;
-  if (b >= B) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.y * SLAB + lane * VB;
+  const bool live = b < B;
   const float ninf = PCB_NEG_INF;
   float4 mx = make_float4(ninf, ninf, ninf, ninf);
-  for (int m = 0; m < k_m; ++m) {
-    const int64_t o = (sb_base + (int64_t)blk * k_m + m) * ldb + b;
-    const float4 f = *reinterpret_cast<const float4*>(flows + o);
-    const float4 l = *reinterpret_cast<const float4*>(values + o);
-    mx.x = fmaxf(mx.x, (l.x == ninf) ? ninf : __logf(f.x) - l.x);
-    mx.y = fmaxf(mx.y, (l.y == ninf) ? ninf : __logf(f.y) - l.y);
-    mx.z = fmaxf(mx.z, (l.z == ninf) ? ninf : __logf(f.z) - l.z);
-    mx.w = fmaxf(mx.w, (l.w == ninf) ? ninf : __logf(f.w) - l.w);
-  }
-  *reinterpret_cast<float4*>(rmax + (int64_t)blk * ldb + b) = mx;
+  if (live)
+    for (int m = warp; m < k_m; m += RW) {
+      const int64_t o = (sb_base + (int64_t)blk * k_m + m) * ldb + b;
+      const float4 f = *reinterpret_cast<const float4*>(flows + o);
+      const float4 l = *reinterpret_cast<const float4*>(values + o);
+      mx.x = fmaxf(mx.x, (l.x == ninf) ? ninf : __logf(f.x) - l.x);
+      mx.y = fmaxf(mx.y, (l.y == ninf) ? ninf : __logf(f.y) - l.y);
+      mx.z = fmaxf(mx.z, (l.z == ninf) ? ninf : __logf(f.z) - l.z);
+      mx.w = fmaxf(mx.w, (l.w == ninf) ? ninf : __logf(f.w) - l.w);
+    }
+  block_max_store(mx, rmax + (int64_t)blk * ldb + b, live);
 }
 
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
@@ -316,7 +332,7 @@ int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!B || !L.n_sb) return PCB_OK;
   dim3 grid((unsigned)L.n_sb, (unsigned)((B + SLAB - 1) / SLAB));
-  k_ratio_max<<<grid, 128, 0, s>>>((int)L.k_m, B, ldb, L.sb_base, values, flows, rmax);
+  k_ratio_max<<<grid, RW * 32, 0, s>>>((int)L.k_m, B, ldb, L.sb_base, values, flows, rmax);
   return check_launch();
 }
 
@@ -599,27 +615,29 @@ __global__ void k_push(int64_t n, int f, int B, int ldb, const int32_t* __restri
 
 // Fused (engine.py:249-254): for every product evaluated in the layer,
 // prod_flows[row] += flow_scratch[slot]; if the layer is its pushing layer,
-// add the finished row to each child's flow.
-__global__ void __launch_bounds__(128)
-    k_flow_push(int B, int ldb, const int32_t* __restrict__ slots,
+// add the finished row to each child's flow.  One warp per product row,
+// lane = 4 consecutive samples; a CTA covers RW rows x 128 samples.
+__global__ void __launch_bounds__(RW * 32)
+    k_flow_push(int64_t n, int B, int ldb, const int32_t* __restrict__ slots,
                 const int32_t* __restrict__ rows, const int32_t* __restrict__ flag,
                 const int32_t* __restrict__ poff, const int32_t* __restrict__ pch,
                 const float* __restrict__ fs, float* __restrict__ pf, float* __restrict__ flows) {
-  const int j = blockIdx.x;
-  const int b = blockIdx.y * SLAB + threadIdx.x * VB;
-  if (b >= B) return;
-  const int64_t ro = (int64_t)rows[j] * ldb + b;
+  const int64_t j = (int64_t)blockIdx.x * RW + (threadIdx.x >> 5);
+  const int b = blockIdx.y * SLAB + (threadIdx.x & 31) * VB;
+  if (j >= n || b >= B) return;
+  const int64_t ro = (int64_t)__ldg(rows + j) * ldb + b;
   float4 p = *reinterpret_cast<const float4*>(pf + ro);
-  const float4 a = *reinterpret_cast<const float4*>(fs + (int64_t)slots[j] * ldb + b);
+  const float4 a = *reinterpret_cast<const float4*>(fs + (int64_t)__ldg(slots + j) * ldb + b);
   p.x += a.x;
   p.y += a.y;
   p.z += a.z;
   p.w += a.w;
   *reinterpret_cast<float4*>(pf + ro) = p;
-  if (!flag[j]) return;
+  if (!__ldg(flag + j)) return;
   const float pv[4] = {p.x, p.y, p.z, p.w};
-  for (int q = poff[j]; q < poff[j + 1]; ++q) {
-    float* dst = flows + (int64_t)pch[q] * ldb + b;
+  const int q1 = __ldg(poff + j + 1);
+  for (int q = __ldg(poff + j); q < q1; ++q) {
+    float* dst = flows + (int64_t)__ldg(pch + q) * ldb + b;
 #pragma unroll
     for (int e = 0; e < VB; ++e)
       if (b + e < B && pv[e] != 0.f) atomicAdd(dst + e, pv[e]);
@@ -630,9 +648,9 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows) {
   ProfScope prof_(KC_ACCUM_PUSH, s);
   if (!B || !L.n_prod) return PCB_OK;
-  dim3 grid((unsigned)L.n_prod, (unsigned)((B + SLAB - 1) / SLAB));
-  k_flow_push<<<grid, 128, 0, s>>>(B, ldb, L.prod_slots, L.prod_rows, L.push_flag, L.push_off,
-                                   L.push_ch, flow_scratch, prod_flows, flows);
+  dim3 grid((unsigned)((L.n_prod + RW - 1) / RW), (unsigned)((B + SLAB - 1) / SLAB));
+  k_flow_push<<<grid, RW * 32, 0, s>>>(L.n_prod, B, ldb, L.prod_slots, L.prod_rows, L.push_flag,
+                                       L.push_off, L.push_ch, flow_scratch, prod_flows, flows);
   return check_launch();
 }
 

@@ -90,8 +90,11 @@ __global__ void __launch_bounds__(TC_THREADS, (KN <= 32) ? 2 : 1)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int row = tid & (TC_M - 1);  // sample within the tile
   const int half = tid >> 7;         // which half of the K chunk this thread converts
-  const int sr = blockIdx.x;
-  const int b = blockIdx.y * TC_M + row;
+  // 1-D grid, batch tiles of one super-row adjacent so its theta tiles are
+  // fetched from HBM once and re-read from L2
+  const int ntiles = (B + TC_M - 1) / TC_M;
+  const int sr = blockIdx.x / ntiles;
+  const int b = (blockIdx.x - sr * ntiles) * TC_M + row;
   const bool live = b < B;
   const int m0 = row_off[sr];
   const int S = row_off[sr + 1] - m0;
@@ -228,8 +231,11 @@ __global__ void __launch_bounds__(TC_THREADS, (KM <= 32) ? 2 : 1)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int row = tid & (TC_M - 1);
   const int half = tid >> 7;
-  const int sr = blockIdx.x;
-  const int b = blockIdx.y * TC_M + row;
+  // 1-D grid, batch tiles of one super-row adjacent so its theta tiles are
+  // fetched from HBM once and re-read from L2
+  const int ntiles = (B + TC_M - 1) / TC_M;
+  const int sr = blockIdx.x / ntiles;
+  const int b = (blockIdx.x - sr * ntiles) * TC_M + row;
   const bool live = b < B;
   const int m0 = row_off[sr];
   const int S = row_off[sr + 1] - m0;
@@ -344,12 +350,16 @@ __global__ void __launch_bounds__(TC_THREADS, (KM <= 32) ? 2 : 1)
 }
 
 // --------------------------------------------------------------- param flows
-// One CTA = one 128-sum M tile of a super-row (blockIdx.z) x up to 256
-// product columns; K = samples streamed 32 at a time.  Two threads per sum
-// row (16 samples each).  c_b = per-sample max of rmax over the tile's sum
-// blocks.  The next chunk's flows / values / child values are loaded into
-// registers before the current chunk is converted.
+// One CTA = one 128-sum M tile of a super-row x up to 256 product columns x
+// one slice of the batch (blockIdx.z = mtile + mtiles * kslice; slices
+// split the contraction so small layers still fill the machine — the
+// epilogue's red.add into f_params sums them).  K = samples streamed 32 at a
+// time, two threads per sum row (16 samples each).  c_b = per-sample max of
+// rmax over the tile's sum blocks.  Every address is resolved once per CTA
+// (shared-memory tables / registers); each chunk's flows, values, child
+// values and shifts are loaded into registers one chunk ahead.
 constexpr int PF_KC = 32;
+constexpr int PF_MAXSB = TC_M / 16 + 1;  // sum blocks a 128-row tile can touch (k_m >= 16)
 
 struct PfSmem {
   static constexpr int kA = TC_M * PF_KC * 2;
@@ -360,13 +370,13 @@ struct PfSmem {
 
 template <int KN>
 __global__ void __launch_bounds__(TC_THREADS, 2)
-    k_param_flow_tc(int cap, int k_m, int B, int ldb, const int32_t* __restrict__ row_off,
-                    const int32_t* __restrict__ members, const int32_t* __restrict__ sum_ids,
-                    const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
-                    const int32_t* __restrict__ flow_ids, const float* __restrict__ theta,
-                    const float* __restrict__ values, const float* __restrict__ flows,
-                    const float* __restrict__ scratch, const float* __restrict__ rmax,
-                    int64_t sb_base, float* __restrict__ f_params) {
+    k_param_flow_tc(int cap, int k_m, int B, int ldb, int mtiles, int kslices,
+                    const int32_t* __restrict__ row_off, const int32_t* __restrict__ members,
+                    const int32_t* __restrict__ sum_ids, const int32_t* __restrict__ prod_ids,
+                    const int32_t* __restrict__ param_ids, const int32_t* __restrict__ flow_ids,
+                    const float* __restrict__ theta, const float* __restrict__ values,
+                    const float* __restrict__ flows, const float* __restrict__ scratch,
+                    const float* __restrict__ rmax, int64_t sb_base, float* __restrict__ f_params) {
   constexpr int HS = PF_KC / 2;               // samples per thread per chunk (A side)
   constexpr int BQ = TC_NMAX * (PF_KC / 8) / TC_THREADS;  // B items per thread (max)
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -374,18 +384,27 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   __shared__ uint32_t tmem_base;
   __shared__ float cb[2][PF_KC];
   __shared__ int cols[TC_NMAX / 16];
-  __shared__ int ncols_s;
+  __shared__ int64_t rblk[PF_MAXSB];
+  __shared__ int ncols_s, nrblk_s;
   constexpr int CPG = TC_NMAX / KN;  // child columns per CTA
   const int tid = threadIdx.x, warp = tid >> 5;
   const int sr = blockIdx.x;
   const int cg = blockIdx.y;
-  const int mt = blockIdx.z;
+  const int mt = blockIdx.z % mtiles;
+  const int ks = blockIdx.z / mtiles;
   const int m0 = row_off[sr];
   const int S = row_off[sr + 1] - m0;
   const int Nsum = S * k_m;
   if (mt * TC_M >= Nsum) return;
+  // this CTA's batch slice, in whole chunks
+  const int nchunks = (B + PF_KC - 1) / PF_KC;
+  const int per = (nchunks + kslices - 1) / kslices;
+  const int kc0 = ks * per, kc1 = min(nchunks, kc0 + per);
+  if (kc0 >= kc1) return;
   const int r0 = members[m0];
   const int32_t* trow = param_ids + (int64_t)r0 * cap;
+  const int s_lo = (mt * TC_M) / k_m;
+  const int s_hi = (min(mt * TC_M + TC_M, Nsum) - 1) / k_m;
   if (tid == 0) {
     int seen = 0, n = 0;
     for (int c = 0; c < cap; ++c) {
@@ -394,6 +413,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       ++seen;
     }
     ncols_s = n;
+    for (int s = s_lo; s <= s_hi; ++s)
+      rblk[s - s_lo] = (int64_t)(sum_ids[members[m0 + s]] - sb_base) / k_m * ldb;
+    nrblk_s = s_hi - s_lo + 1;
   }
   __syncthreads();
   const int ncol = ncols_s;
@@ -405,8 +427,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const bool row_live = ms < Nsum;
   int sum_slot = 0;
   if (row_live) sum_slot = sum_ids[members[m0 + ms / k_m]] + (ms % k_m);
-  const int s_lo = (mt * TC_M) / k_m;
-  const int s_hi = (min(mt * TC_M + TC_M, Nsum) - 1) / k_m;
+  const int nrb = nrblk_s;
 
   const uint32_t ncols_t = tmem_cols_for(Npad);
   if (tid == 0) {
@@ -424,54 +445,56 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int32_t* prow = prod_ids + (int64_t)r0 * cap;
   const int nitems = Npad * (PF_KC / 8);
 
-  auto load_a = [&](int b0, float* fr, float* lr) {
+  // per-thread B items: the scratch row (constant over chunks) and smem slot
+  const float* bsrc[BQ];
+  int bn[BQ], bk[BQ];
+#pragma unroll
+  for (int u = 0; u < BQ; ++u) {
+    const int q = tid + u * TC_THREADS;
+    const int n = q / (PF_KC / 8), kq = q - n * (PF_KC / 8);
+    bn[u] = n;
+    bk[u] = kq;
+    bsrc[u] = (q < nitems) ? scratch + (int64_t)(prow[cols[n / KN]] + n % KN) * ldb + kq * 8
+                           : nullptr;
+  }
+  const float* fsrc = flows + (int64_t)sum_slot * ldb + ahalf * HS;
+  const float* vsrc = values + (int64_t)sum_slot * ldb + ahalf * HS;
+
+  float fn[HS], ln[HS], ev[BQ][8], cbn = PCB_NEG_INF;
+  auto load_chunk = [&](int b0) {
     if (row_live) {
-      const float4* fp =
-          reinterpret_cast<const float4*>(flows + (int64_t)sum_slot * ldb + b0 + ahalf * HS);
-      const float4* vp =
-          reinterpret_cast<const float4*>(values + (int64_t)sum_slot * ldb + b0 + ahalf * HS);
+      const float4* fp = reinterpret_cast<const float4*>(fsrc + b0);
+      const float4* vp = reinterpret_cast<const float4*>(vsrc + b0);
 #pragma unroll
       for (int q = 0; q < HS / 4; ++q) {
         const float4 f = fp[q], v = vp[q];
-        fr[4 * q] = f.x, fr[4 * q + 1] = f.y, fr[4 * q + 2] = f.z, fr[4 * q + 3] = f.w;
-        lr[4 * q] = v.x, lr[4 * q + 1] = v.y, lr[4 * q + 2] = v.z, lr[4 * q + 3] = v.w;
+        fn[4 * q] = f.x, fn[4 * q + 1] = f.y, fn[4 * q + 2] = f.z, fn[4 * q + 3] = f.w;
+        ln[4 * q] = v.x, ln[4 * q + 1] = v.y, ln[4 * q + 2] = v.z, ln[4 * q + 3] = v.w;
       }
     }
-  };
-  float fn[HS], ln[HS];
-  load_a(0, fn, ln);
-  int it = 0;
-  for (int b0 = 0; b0 < B; b0 += PF_KC, ++it) {
-    const int stage = it & 1;
-    // child values of this chunk: issued first, consumed after the A conversion
-    float ev[BQ][8];
 #pragma unroll
     for (int u = 0; u < BQ; ++u) {
-      const int q = tid + u * TC_THREADS;
-      if (q < nitems) {
-        const int n = q / (PF_KC / 8), kq = q - n * (PF_KC / 8);
-        const int c = cols[n / KN], j = n % KN;
-        const float* src = scratch + (int64_t)(prow[c] + j) * ldb + b0 + kq * 8;
-        const float4 x0 = *reinterpret_cast<const float4*>(src);
-        const float4 x1 = *reinterpret_cast<const float4*>(src + 4);
+      if (bsrc[u]) {
+        const float4 x0 = *reinterpret_cast<const float4*>(bsrc[u] + b0);
+        const float4 x1 = *reinterpret_cast<const float4*>(bsrc[u] + b0 + 4);
         ev[u][0] = x0.x, ev[u][1] = x0.y, ev[u][2] = x0.z, ev[u][3] = x0.w;
         ev[u][4] = x1.x, ev[u][5] = x1.y, ev[u][6] = x1.z, ev[u][7] = x1.w;
       }
     }
-    float f[HS], l[HS];
-#pragma unroll
-    for (int e = 0; e < HS; ++e) f[e] = fn[e], l[e] = ln[e];
-    if (b0 + PF_KC < B) load_a(b0 + PF_KC, fn, ln);  // prefetch the next chunk's A side
-    if (tid < PF_KC) {  // per-sample shift of this chunk (double-buffered)
+    if (tid < PF_KC) {  // per-sample shift of this chunk
       float v = PCB_NEG_INF;
       if (b0 + tid < B)
-        for (int s = s_lo; s <= s_hi; ++s) {
-          const int64_t blk = (sum_ids[members[m0 + s]] - sb_base) / k_m;
-          v = fmaxf(v, rmax[blk * ldb + b0 + tid]);
-        }
-      cb[stage][tid] = v;
+        for (int i = 0; i < nrb; ++i) v = fmaxf(v, rmax[rblk[i] + b0 + tid]);
+      cbn = v;
     }
+  };
+  load_chunk(kc0 * PF_KC);
+  int it = 0;
+  for (int kc = kc0; kc < kc1; ++kc, ++it) {
+    const int b0 = kc * PF_KC;
+    const int stage = it & 1;
     if (it >= 2) mbar_wait(smem_u32(&done[stage]), ((it - 2) >> 1) & 1);
+    if (tid < PF_KC) cb[stage][tid] = cbn;
     __syncthreads();
     uint8_t* sAh = smem + stage * PfSmem::kStage;
     uint8_t* sAl = sAh + PfSmem::kA;
@@ -486,7 +509,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         const float c = cbs[q];
         x[e] = (!row_live || c == PCB_NEG_INF || b0 + q >= B)
                    ? 0.f
-                   : scaled_ratio(f[e], l[e], c * kL2E);
+                   : scaled_ratio(fn[e], ln[e], c * kL2E);
       }
 #pragma unroll
       for (int kq = 0; kq < HS / 8; ++kq)
@@ -494,18 +517,17 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
 #pragma unroll
     for (int u = 0; u < BQ; ++u) {
-      const int q = tid + u * TC_THREADS;
-      if (q < nitems) {
-        const int n = q / (PF_KC / 8), kq = q - n * (PF_KC / 8);
+      if (bsrc[u]) {
         float x[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float c = cbs[kq * 8 + e];
+          const float c = cbs[bk[u] * 8 + e];
           x[e] = (c == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(ev[u][e], kL2E, c * kL2E)), 1e37f);
         }
-        store_split8(sBh, sBl, kmajor_off(n, kq * 8, PF_KC), x);
+        store_split8(sBh, sBl, kmajor_off(bn[u], bk[u] * 8, PF_KC), x);
       }
     }
+    if (kc + 1 < kc1) load_chunk(b0 + PF_KC);  // next chunk's operands, in flight during the MMA
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -513,10 +535,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       const uint32_t aH = smem_u32(sAh), aL = smem_u32(sAl);
       const uint32_t bH = smem_u32(sBh), bL = smem_u32(sBl);
 #pragma unroll
-      for (int ks = 0; ks < PF_KC / 16; ++ks) {
-        const uint32_t o = ks * 256;
+      for (int kk = 0; kk < PF_KC / 16; ++kk) {
+        const uint32_t o = kk * 256;
         mma_bf16(tmem, make_desc(aH + o, 128, SBO), make_desc(bH + o, 128, SBO), idesc,
-                 (it > 0 || ks > 0) ? 1u : 0u);
+                 (it > 0 || kk > 0) ? 1u : 0u);
         mma_bf16(tmem, make_desc(aH + o, 128, SBO), make_desc(bL + o, 128, SBO), idesc, 1u);
         mma_bf16(tmem, make_desc(aL + o, 128, SBO), make_desc(bH + o, 128, SBO), idesc, 1u);
       }
@@ -578,7 +600,7 @@ static int fwd_kn(const pcb_plan* P, const Layer& L, const FwdGroup& g, const Tc
                   float* values) {
   static bool done = false;
   if (set_smem(k_sum_fwd_tc<KN>, FwdSmem<KN>::kBytes, done)) return PCB_CUDA;
-  dim3 grid((unsigned)tc.count, (unsigned)((B + TC_M - 1) / TC_M));
+  const unsigned grid = (unsigned)(tc.count * ((B + TC_M - 1) / TC_M));
   k_sum_fwd_tc<KN><<<grid, TC_THREADS, FwdSmem<KN>::kBytes, s>>>(
       (int)g.cap, (int)L.k_m, B, ldb, tc.row_off, tc.members, g.sum_ids, g.prod_ids,
       g.param_ids, g.param_slab, P->mma, scratch, bmax, values);
@@ -604,7 +626,7 @@ static int cf_km(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcR
                  const float* scratch, const float* rmax, float* flow_scratch) {
   static bool done = false;
   if (set_smem(k_child_flow_tc<KM>, CfSmem<KM>::kBytes, done)) return PCB_CUDA;
-  dim3 grid((unsigned)tc.count, (unsigned)((B + TC_M - 1) / TC_M));
+  const unsigned grid = (unsigned)(tc.count * ((B + TC_M - 1) / TC_M));
   k_child_flow_tc<KM><<<grid, TC_THREADS, CfSmem<KM>::kBytes, s>>>(
       (int)g.cap, (int)L.k_n, B, ldb, tc.row_off, tc.members, g.ch_ids, g.par_ids,
       g.par_param_ids, g.par_slab, P->mma, values, flows, scratch, rmax, L.sb_base,
@@ -633,10 +655,17 @@ static int pf_kn(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream
   if (set_smem(k_param_flow_tc<KN>, PfSmem::kBytes, done)) return PCB_CUDA;
   const int cgroups = (int)((g.cap * KN + TC_NMAX - 1) / TC_NMAX);
   const int mtiles = (int)((TC_NMAX + TC_M - 1) / TC_M);  // super-rows hold <= 256 sums
-  dim3 grid((unsigned)tc.count, (unsigned)cgroups, (unsigned)mtiles);
+  // split the batch so a layer launches >= ~2 waves of 2 CTAs/SM; each slice
+  // keeps >= 2 chunks so the register prefetch still has something to hide
+  const int64_t base = (int64_t)tc.count * cgroups * mtiles;
+  const int nchunks = (B + PF_KC - 1) / PF_KC;
+  int kslices = (int)((4 * 148 + base - 1) / base);
+  kslices = max(1, min(kslices, nchunks / 2));
+  dim3 grid((unsigned)tc.count, (unsigned)cgroups, (unsigned)(mtiles * kslices));
   k_param_flow_tc<KN><<<grid, TC_THREADS, PfSmem::kBytes, s>>>(
-      (int)g.cap, (int)L.k_m, B, ldb, tc.row_off, tc.members, g.sum_ids, g.prod_ids,
-      g.param_ids, g.flow_ids, theta, values, flows, scratch, rmax, L.sb_base, f_params);
+      (int)g.cap, (int)L.k_m, B, ldb, mtiles, kslices, tc.row_off, tc.members, g.sum_ids,
+      g.prod_ids, g.param_ids, g.flow_ids, theta, values, flows, scratch, rmax, L.sb_base,
+      f_params);
   return check_launch();
 }
 
