@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 6;
+constexpr int64_t kVersion = 7;
 
 struct Reader {
   const int64_t* p;
@@ -70,6 +70,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->root_children = r.ref(&P->n_root_children);
   P->var_ncat = r.ref();
   P->use_tc = (int)r.get();
+  // PCB_TC_LEGACY=1: per-launch (non-persistent) tensor-core kernels, for A/B runs
+  if (P->use_tc && getenv("PCB_TC_LEGACY")) P->use_tc = 2;
   P->n_mma_tiles = r.get();
   P->mma_elems = r.get();
   P->mma_theta = r.ref();
@@ -95,6 +97,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->in_blocks.pid_off = r.ref();
   P->in_blocks.pids = r.ref();
   P->in_blocks.max_elems = r.get();
+  P->prod_rows_written = (int)r.get();
   int64_t n_layers = r.get();
   for (int64_t l = 0; l < n_layers && r.ok; ++l) {
     Layer L;
@@ -278,7 +281,9 @@ int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int 
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.fwd_tc[g];
     if (P->use_tc && T.count > 0 && tc_supported(L))
-      st = launch_sum_fwd_tc(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values);
+      st = (P->use_tc == 1 && ws_supported((int)L.k_n, (int)L.k_m))
+               ? launch_sum_fwd_ws(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values)
+               : launch_sum_fwd_tc(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values);
     else
       st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, values);
     if (st) return st;
@@ -309,8 +314,11 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   for (size_t g = 0; g < L.bwd.size(); ++g) {
     const TcRows& T = L.bwd_tc[g];
     if (tc && T.count > 0)
-      st = launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch, w.rmax,
-                                flow_scratch);
+      st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
+               ? launch_child_flow_ws(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
+                                      w.rmax, flow_scratch)
+               : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
+                                      w.rmax, flow_scratch);
     else
       st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
                                   flow_scratch);
@@ -395,7 +403,8 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
     if (cudaMemsetAsync(d_flows, 0, sizeof(float) * plan->num_value_slots * ldb, s) !=
         cudaSuccess)
       return PCB_CUDA;
-    if (plan->num_prod_rows &&
+    // every product row's first accumulation stores (plan flag): no zeroing
+    if (plan->num_prod_rows && !plan->prod_rows_written &&
         cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * plan->num_prod_rows * ldb, s) !=
             cudaSuccess)
       return PCB_CUDA;

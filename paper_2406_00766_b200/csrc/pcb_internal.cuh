@@ -75,7 +75,9 @@ struct Layer {
   const int32_t *prow_off, *prow_ch;  // per scratch row: product children CSR
   int64_t sb_base, n_sb;              // sum blocks of the layer: slots [sb_base, +n_sb*k_m)
   int64_t n_pb;                       // product blocks in the window incl. pad block 0
-  const int32_t *push_flag, *push_off, *push_ch;  // fused accumulate + push, product order
+  // fused accumulate + push, product order: flag bit0 push, bit1 first
+  // accumulation (store); push_ch = slot * 2 + (single push into the slot)
+  const int32_t *push_flag, *push_off, *push_ch;
 };
 
 // Workspace carved from the caller's d_work buffer (pcb_plan_workspace_floats):
@@ -104,13 +106,14 @@ struct pcb_plan {
   // simplex groups
   int64_t n_groups;
   const int32_t *group_idx, *group_off;
-  int use_tc;  // 1: tensor-core sum kernels where the plan provides TC rows
+  int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported); 2: legacy TC
   int64_t max_pb = 1, max_sb = 1;
   // bf16 tensor-core copies of theta tiles (plan v4)
   int64_t n_mma_tiles = 0, mma_elems = 0;
   const int32_t *mma_theta = nullptr, *mma_slab = nullptr, *mma_km = nullptr, *mma_kn = nullptr;
   __nv_bfloat16* mma = nullptr;  // bound by pcb_plan_set_mma
   int64_t scratch_rows = 1;      // all-layer scratch rows (sum of layer windows)
+  int prod_rows_written = 0;     // every prod-flow row is stored by its first accumulation
 };
 
 namespace pcb {
@@ -196,6 +199,14 @@ int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
                          int B, int ldb, const float* theta, const float* values,
                          const float* flows, const float* scratch, const float* rmax,
                          float* f_params);
+// warp-specialised persistent variants (pcb_tc_ws.cu), K block 16 / 32
+bool ws_supported(int kc, int nb);
+int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
+                      cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
+                      float* values);
+int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
+                         cudaStream_t s, int B, int ldb, const float* values, const float* flows,
+                         const float* scratch, const float* rmax, float* flow_scratch);
 int launch_child_flow_tc(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* values, const float* flows,
                          const float* scratch, const float* rmax, float* flow_scratch);

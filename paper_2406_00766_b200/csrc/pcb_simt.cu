@@ -614,9 +614,11 @@ __global__ void k_push(int64_t n, int f, int B, int ldb, const int32_t* __restri
 }
 
 // Fused (engine.py:249-254): for every product evaluated in the layer,
-// prod_flows[row] += flow_scratch[slot]; if the layer is its pushing layer,
-// add the finished row to each child's flow.  One warp per product row,
-// lane = 4 consecutive samples; a CTA covers RW rows x 128 samples.
+// prod_flows[row] += flow_scratch[slot] (a store for the row's first
+// accumulation in the pass); if the layer is its pushing layer, add the
+// finished row to each child's flow — a plain store for children with a
+// single push in the whole pass, else a vector (float4) atomic.  One warp per
+// product row, lane = 4 consecutive samples; a CTA covers RW rows x 128 samples.
 __global__ void __launch_bounds__(RW * 32)
     k_flow_push(int64_t n, int B, int ldb, const int32_t* __restrict__ slots,
                 const int32_t* __restrict__ rows, const int32_t* __restrict__ flag,
@@ -625,22 +627,33 @@ __global__ void __launch_bounds__(RW * 32)
   const int64_t j = (int64_t)blockIdx.x * RW + (threadIdx.x >> 5);
   const int b = blockIdx.y * SLAB + (threadIdx.x & 31) * VB;
   if (j >= n || b >= B) return;
+  const int fl = __ldg(flag + j);
   const int64_t ro = (int64_t)__ldg(rows + j) * ldb + b;
-  float4 p = *reinterpret_cast<const float4*>(pf + ro);
-  const float4 a = *reinterpret_cast<const float4*>(fs + (int64_t)__ldg(slots + j) * ldb + b);
-  p.x += a.x;
-  p.y += a.y;
-  p.z += a.z;
-  p.w += a.w;
+  float4 p = *reinterpret_cast<const float4*>(fs + (int64_t)__ldg(slots + j) * ldb + b);
+  if (!(fl & 2)) {
+    const float4 o = *reinterpret_cast<const float4*>(pf + ro);
+    p.x += o.x;
+    p.y += o.y;
+    p.z += o.z;
+    p.w += o.w;
+  }
   *reinterpret_cast<float4*>(pf + ro) = p;
-  if (!__ldg(flag + j)) return;
-  const float pv[4] = {p.x, p.y, p.z, p.w};
+  if (!(fl & 1)) return;
+  const bool full = b + VB <= B;
   const int q1 = __ldg(poff + j + 1);
   for (int q = __ldg(poff + j); q < q1; ++q) {
-    float* dst = flows + (int64_t)__ldg(pch + q) * ldb + b;
+    const int code = __ldg(pch + q);
+    float* dst = flows + (int64_t)(code >> 1) * ldb + b;
+    if (code & 1) {
+      *reinterpret_cast<float4*>(dst) = p;
+    } else if (full) {
+      atomicAdd(reinterpret_cast<float4*>(dst), p);
+    } else {
+      const float pv[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
-    for (int e = 0; e < VB; ++e)
-      if (b + e < B && pv[e] != 0.f) atomicAdd(dst + e, pv[e]);
+      for (int e = 0; e < VB; ++e)
+        if (b + e < B) atomicAdd(dst + e, pv[e]);
+    }
   }
 }
 

@@ -125,36 +125,97 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 // ------------------------------------------------- theta -> bf16 MMA tiles
-// Every tensor-core tile (k_m x k_n, row-major in theta) is re-laid as two
-// bf16 planes (hi, lo with theta ~= hi + lo) in core-matrix order
-// (tile_off): the same bytes are a K-major B operand for the sum forward
-// (N = sums, K = products) and an MN-major B operand for the child flows
-// (N = products, K = sums).  Refreshed after every theta update.
-__global__ void k_theta_to_mma(int64_t n_tiles, const int32_t* __restrict__ t_theta,
-                               const int32_t* __restrict__ t_slab, const int32_t* __restrict__ t_km,
-                               const int32_t* __restrict__ t_kn, const float* __restrict__ theta,
-                               __nv_bfloat16* __restrict__ mma) {
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const int km = t_km[t], kn = t_kn[t];
-    const int sz = km * kn;
-    const float* src = theta + t_theta[t];
-    __nv_bfloat16* hi = mma + (int64_t)t_slab[t];
-    __nv_bfloat16* lo = hi + sz;
-    for (int q = threadIdx.x; q < sz; q += blockDim.x) {
-      const int m = q / kn, j = q - m * kn;
-      const int o = tile_off(m, j, kn);
-      __nv_bfloat16 h, l;
-      split_bf16(src[q], h, l);
-      hi[o] = h;
-      lo[o] = l;
+// Every tensor-core tile (k_m x k_n, row-major in theta) is re-laid as four
+// bf16 planes in core-matrix order (tile_off), theta ~= hi + lo:
+//   [0, sz)     hi, sum-major      K-major B of the sum forward (N = sums,
+//   [sz, 2sz)   lo, sum-major      K = products); also the MN-major B of the
+//                                  per-launch child-flow kernel
+//   [2sz, 3sz)  hi, product-major  K-major B of the child flows (N = products,
+//   [3sz, 4sz)  lo, product-major  K = sums)
+// Hi planes of consecutive tiles stack along N with a uniform core stride,
+// so a super-row's stacked tiles form one MMA operand.  One CTA per tile:
+// the tile is staged in shared memory, then every thread packs one 8-wide
+// core row per plane pair (16-byte stores).  Refreshed after every theta update.
+constexpr int TM_MAX = 64;
+constexpr int TM_THREADS = 256;
+constexpr int TM_V4 = TM_MAX * TM_MAX / 4 / TM_THREADS;  // float4 loads per thread (max)
+__global__ void __launch_bounds__(TM_THREADS)
+    k_theta_to_mma(int64_t n_tiles, const int32_t* __restrict__ t_theta,
+                   const int32_t* __restrict__ t_slab, const int32_t* __restrict__ t_km,
+                   const int32_t* __restrict__ t_kn, const float* __restrict__ theta,
+                   __nv_bfloat16* __restrict__ mma) {
+  __shared__ float tile[TM_MAX * (TM_MAX + 1)];
+  // the next tile's elements are loaded (float4, row-major) while this one is packed
+  float4 nx[TM_V4];
+  auto load = [&](int64_t t) {
+    const int sz = __ldg(t_km + t) * __ldg(t_kn + t);
+    const int64_t start = __ldg(t_theta + t);
+    const float* src = theta + start;
+    if ((start & 3) == 0) {  // tiles after odd-sized input pmfs may be unaligned
+#pragma unroll
+      for (int u = 0; u < TM_V4; ++u) {
+        const int q = (threadIdx.x + u * TM_THREADS) * 4;
+        if (q < sz) nx[u] = __ldg(reinterpret_cast<const float4*>(src + q));
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < TM_V4; ++u) {
+        const int q = (threadIdx.x + u * TM_THREADS) * 4;
+        if (q < sz)
+          nx[u] = make_float4(__ldg(src + q), __ldg(src + q + 1), __ldg(src + q + 2),
+                              __ldg(src + q + 3));
+      }
     }
+  };
+  int64_t t = blockIdx.x;
+  if (t < n_tiles) load(t);
+  for (; t < n_tiles; t += gridDim.x) {
+    const int km = __ldg(t_km + t), kn = __ldg(t_kn + t);
+    const int sz = km * kn, ld = kn + 1;
+#pragma unroll
+    for (int u = 0; u < TM_V4; ++u) {
+      const int q = (threadIdx.x + u * TM_THREADS) * 4;
+      if (q < sz) {
+        const int m = q / kn, j = q - m * kn;
+        float* d = tile + m * ld + j;
+        d[0] = nx[u].x, d[1] = nx[u].y, d[2] = nx[u].z, d[3] = nx[u].w;
+      }
+    }
+    __syncthreads();
+    if (t + gridDim.x < n_tiles) load(t + gridDim.x);
+    uint8_t* base = reinterpret_cast<uint8_t*>(mma + (int64_t)__ldg(t_slab + t));
+    const int n8 = sz / 8;
+    for (int q = threadIdx.x; q < 2 * n8; q += TM_THREADS) {
+      float v[8];
+      uint32_t off;
+      int plane;
+      if (q < n8) {  // sum-major: core row (m, j..j+7)
+        const int m = q / (kn / 8), j = (q - m * (kn / 8)) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = tile[m * ld + j + e];
+        off = (uint32_t)tile_off(m, j, kn) * 2u;
+        plane = 0;
+      } else {       // product-major: core row (j, m..m+7)
+        const int r = q - n8;
+        const int j = r / (km / 8), m = (r - j * (km / 8)) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = tile[(m + e) * ld + j];
+        off = (uint32_t)tile_off(j, m, km) * 2u;
+        plane = 2;
+      }
+      uint4 hi, lo;
+      split_pack8(v, hi, lo);
+      *reinterpret_cast<uint4*>(base + (plane * sz) * 2 + off) = hi;
+      *reinterpret_cast<uint4*>(base + ((plane + 1) * sz) * 2 + off) = lo;
+    }
+    __syncthreads();
   }
 }
 
 int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta) {
   ProfScope prof_(KC_EM, s);
   if (!p->n_mma_tiles || !p->mma) return PCB_OK;
-  k_theta_to_mma<<<grid_for(p->n_mma_tiles, 1, 148 * 8), 256, 0, s>>>(
+  k_theta_to_mma<<<grid_for(p->n_mma_tiles, 1, 148 * 8), TM_THREADS, 0, s>>>(
       p->n_mma_tiles, p->mma_theta, p->mma_slab, p->mma_km, p->mma_kn, theta, p->mma);
   return check_launch();
 }

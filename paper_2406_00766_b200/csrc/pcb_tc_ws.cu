@@ -1,0 +1,511 @@
+// Warp-specialised, persistent tcgen05 sum-layer kernels for sm_100a:
+// the sum forward (engine.py:74-102) and the child flows (engine.py:129-165).
+//
+// Both are "transform + GEMM" over node-major fp32 rows:
+//   forward     D[b, n] = sum_j e^{child[j,b] - g_b} theta[n, j]      (A = children)
+//   child flow  D[b, j] = sum_m e^{lnf[m,b] - g_b} theta[m, j]         (A = parent ratios)
+// with M = 128 samples per work item, N = a stacked super-row (<= 256) and K
+// streamed one child (parent) block at a time.  A work item is one
+// (super-row, 128-sample tile); CTAs are persistent (one per SM, TMEM
+// 2 x 256 columns double-buffers the accumulator) and take items round-robin
+// so the batch tiles of one super-row run side by side and share its theta
+// tiles through L2.
+//
+// Warp roles (14 warps):
+//   warp 0      producer: 1-D TMA bulk copies (cp.async.bulk) of the raw fp32
+//               rows of each K block (one row segment of 128 samples per lane)
+//               into the raw ring, and of the pre-split bf16 theta tiles into
+//               the operand ring;
+//   warp 1      MMA issuer: three kind::f16 MMAs per 16-wide K step
+//               (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM), commits
+//               free operand stages and publish finished accumulators;
+//   warps 2-5   converters: thread = sample; raw row values -> shifted
+//               exponential (MUFU ex2, shift folded into one FFMA) -> packed
+//               bf16 hi/lo planes in the K-major core-matrix layout;
+//   warps 6-13  shift + epilogue: per-sample shift g_b of the next item (max
+//               of the side maxima bmax / rmax over its K blocks), then TMEM ->
+//               registers -> log-domain result -> coalesced fp32 row stores
+//               (two warps per TMEM lane quarter, alternate 16-column chunks).
+// Every hand-off is an mbarrier: raw full/empty, operand full/empty,
+// accumulator full/empty, shift full/empty.
+#include <math.h>
+
+#include "pcb_internal.cuh"
+#include "pcb_tc.cuh"
+
+namespace pcb {
+
+using namespace tc;
+
+namespace {
+
+constexpr int WS_M = 128;           // samples per item
+constexpr int WS_NMAX = 256;        // stacked N per item
+constexpr int WS_THREADS = 448;     // 14 warps
+constexpr int WS_PRODUCER = 0, WS_MMA = 1, WS_CONV0 = 2, WS_EPI0 = 6;
+
+enum { MODE_FWD = 0, MODE_CF = 1 };
+
+struct WsArgs {
+  int cap;        // K blocks per group row
+  int nb;         // N of one stacked tile (k_m forward, k_n child flow)
+  int B, ldb;
+  int n_items, ntiles;
+  int64_t sb_base;                 // shift-row base (child flow: first sum-block slot)
+  const int32_t* row_off;          // super-row -> members
+  const int32_t* members;          // group rows
+  const int32_t* out_ids;          // sum_ids (fwd) / ch_ids (cf): first output row per member
+  const int32_t* src_ids;          // prod_ids (fwd) / par_ids (cf): first source row per column
+  const int32_t* real_ids;         // param_ids (fwd) / par_param_ids (cf): 0 = padding column
+  const int32_t* slab;             // bf16 tile offset per (member, column)
+  const __nv_bfloat16* mma;
+  const float* src0;               // scratch (fwd) / flows (cf)
+  const float* src1;               // - / values (cf)
+  const float* shift;              // bmax (fwd) / rmax (cf)
+  const float* aux;                // - / scratch (cf epilogue: child log values)
+  float* out;                      // values (fwd) / flow_scratch (cf)
+};
+
+template <int MODE, int KC>
+struct WsCfg {
+  static constexpr int kSrc = MODE == MODE_CF ? 2 : 1;        // raw arrays per K block
+  static constexpr int kRows = KC * kSrc;                     // raw rows per stage
+  static constexpr int kRaw = kRows * WS_M * 4;               // raw stage bytes
+  static constexpr int kA = WS_M * KC * 2;                    // one bf16 A plane
+  static constexpr int kBPlane = WS_NMAX * KC * 2;            // stacked theta hi (or lo) plane
+  static constexpr int kB = 2 * kBPlane;
+  static constexpr int kOp = 2 * kA + kB;
+  static constexpr int kBudget = 210 * 1024;
+  static constexpr int kOS = (KC <= 16) ? 4 : (MODE == MODE_CF ? 2 : 3);
+  static constexpr int kRSmax = (kBudget - kOS * kOp) / kRaw;
+  static constexpr int kRS = kRSmax > 6 ? 6 : kRSmax;
+  static constexpr int kBytes = kRS * kRaw + kOS * kOp;
+  static_assert(kRS >= 2, "raw ring too small");
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// ring position: slot and wait parities of use u of a ring with S stages
+struct Ring {
+  int S, u = 0;
+  __device__ explicit Ring(int s) : S(s) {}
+  __device__ int slot() const { return u % S; }
+  __device__ uint32_t full_par() const { return (uint32_t)((u / S) & 1); }
+  __device__ uint32_t empty_par() const { return full_par() ^ 1u; }
+  __device__ void next() { ++u; }
+};
+
+__device__ __forceinline__ int next_real(const int32_t* __restrict__ ids, int cap, int c) {
+  while (c < cap && __ldg(ids + c) == 0) ++c;
+  return c;
+}
+
+}  // namespace
+
+template <int MODE, int KC>
+__global__ void __launch_bounds__(WS_THREADS, 1) k_sum_ws(const WsArgs a) {
+  using C = WsCfg<MODE, KC>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS];
+  __shared__ uint64_t op_full[C::kOS], op_empty[C::kOS];
+  __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
+  __shared__ float g_s[2][WS_M];
+  __shared__ uint32_t tmem_base;
+  uint8_t* raw = smem;
+  uint8_t* ops = smem + C::kRS * C::kRaw;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < C::kRS; ++i) {
+      mbar_init(smem_u32(&raw_full[i]), 1);
+      mbar_init(smem_u32(&raw_empty[i]), 4);
+    }
+    for (int i = 0; i < C::kOS; ++i) {
+      mbar_init(smem_u32(&op_full[i]), 4 + 1);  // 4 converter warps + theta tx
+      mbar_init(smem_u32(&op_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 8);
+      mbar_init(smem_u32(&g_full[i]), 4);
+      mbar_init(smem_u32(&g_empty[i]), 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == WS_MMA) tmem_alloc(smem_u32(&tmem_base), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int plane_elems = a.nb * KC;        // one bf16 plane of one theta tile
+  const int plane_bytes = plane_elems * 2;
+  const int plane0 = (MODE == MODE_FWD) ? 0 : 2;  // sum-major / product-major planes
+
+  if (warp == WS_PRODUCER) {
+    // ------------------------------------------------------------ producer
+    Ring rr(C::kRS), orr(C::kOS);
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      const int sr = item / a.ntiles;
+      const int b0 = (item - sr * a.ntiles) * WS_M;
+      const int m0 = a.row_off[sr];
+      const int S = a.row_off[sr + 1] - m0;
+      const int r0 = a.members[m0];
+      const int32_t* src = a.src_ids + (int64_t)r0 * a.cap;
+      const int32_t* real = a.real_ids + (int64_t)r0 * a.cap;
+      const uint32_t seg = (uint32_t)min(WS_M, a.ldb - b0) * 4u;  // bytes per row segment
+      for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+        const int64_t row0 = __ldg(src + c);
+        // raw rows of this K block
+        mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
+        const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
+        if (lane == 0) mbar_arrive_expect_tx(rf, (uint32_t)C::kRows * seg);
+        __syncwarp();
+        uint8_t* dst = raw + rr.slot() * C::kRaw;
+        for (int r = lane; r < C::kRows; r += 32) {
+          const float* base = (MODE == MODE_CF && r >= KC) ? a.src1 : a.src0;
+          const int rr_ = (MODE == MODE_CF && r >= KC) ? r - KC : r;
+          bulk_g2s(smem_u32(dst + r * (WS_M * 4)), base + (row0 + rr_) * a.ldb + b0, seg, rf);
+        }
+        rr.next();
+        // stacked theta tiles of this K block: hi planes back to back, then lo
+        // planes, so the S tiles form one N = S * nb operand per plane
+        mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
+        const uint32_t of = smem_u32(&op_full[orr.slot()]);
+        uint8_t* bdst = ops + orr.slot() * C::kOp + 2 * C::kA;
+        if (lane == 0) mbar_arrive_expect_tx(of, (uint32_t)(2 * S * plane_bytes));
+        __syncwarp();
+        for (int q = lane; q < 2 * S; q += 32) {
+          const int s = q >> 1, lo = q & 1;
+          const int64_t slab = __ldg(a.slab + (int64_t)__ldg(a.members + m0 + s) * a.cap + c);
+          bulk_g2s(smem_u32(bdst + lo * C::kBPlane + s * plane_bytes),
+                   a.mma + slab + (int64_t)(plane0 + lo) * plane_elems, (uint32_t)plane_bytes, of);
+        }
+        orr.next();
+      }
+    }
+  } else if (warp == WS_MMA) {
+    // ------------------------------------------------------------ MMA issuer
+    Ring orr(C::kOS);
+    int acc_u = 0;
+    constexpr uint32_t SBO = (KC / 8) * 128;  // A and B both K-major, no swizzle
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      const int sr = item / a.ntiles;
+      const int m0 = a.row_off[sr];
+      const int S = a.row_off[sr + 1] - m0;
+      const int32_t* real = a.real_ids + (int64_t)a.members[m0] * a.cap;
+      const int as = acc_u & 1;
+      mbar_wait(smem_u32(&acc_empty[as]), (uint32_t)(((acc_u >> 1) & 1) ^ 1));
+      tc_fence_after();
+      const uint32_t d0 = tmem + (uint32_t)(as * WS_NMAX);
+      bool first = true;
+      for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+        mbar_wait(smem_u32(&op_full[orr.slot()]), orr.full_par());
+        tc_fence_after();
+        if (lane == 0) {
+          uint8_t* st = ops + orr.slot() * C::kOp;
+          const uint32_t aH = smem_u32(st), aL = aH + C::kA;
+          const uint32_t bH = aH + 2 * C::kA, bL = bH + C::kBPlane;
+          const uint32_t idesc = idesc_bf16(WS_M, S * a.nb);
+#pragma unroll
+          for (int ks = 0; ks < KC / 16; ++ks) {
+            const uint64_t ah = make_desc(aH + ks * 256, 128, SBO);
+            const uint64_t al = make_desc(aL + ks * 256, 128, SBO);
+            const uint64_t bh = make_desc(bH + ks * 256, 128, SBO);
+            const uint64_t bl = make_desc(bL + ks * 256, 128, SBO);
+            mma_bf16(d0, ah, bh, idesc, (first && ks == 0) ? 0u : 1u);
+            mma_bf16(d0, ah, bl, idesc, 1u);
+            mma_bf16(d0, al, bh, idesc, 1u);
+          }
+          mma_commit(smem_u32(&op_empty[orr.slot()]));
+        }
+        __syncwarp();
+        first = false;
+        orr.next();
+      }
+      if (lane == 0) {
+        if (first)
+          mbar_arrive(smem_u32(&acc_full[as]));  // no K block: nothing to wait for
+        else
+          mma_commit(smem_u32(&acc_full[as]));
+      }
+      __syncwarp();
+      ++acc_u;
+    }
+  } else if (warp < WS_EPI0) {
+    // ------------------------------------------------------------ converters
+    const int t = tid - WS_CONV0 * 32;  // sample within the item
+    Ring rr(C::kRS), orr(C::kOS);
+    int g_u = 0;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      const int sr = item / a.ntiles;
+      const int b = (item - sr * a.ntiles) * WS_M + t;
+      const bool live = b < a.B;
+      const int m0 = a.row_off[sr];
+      const int32_t* real = a.real_ids + (int64_t)a.members[m0] * a.cap;
+      const int gs = g_u & 1;
+      mbar_wait(smem_u32(&g_full[gs]), (uint32_t)((g_u >> 1) & 1));
+      const float g = g_s[gs][t];
+      const bool dead = !live || g == PCB_NEG_INF;
+      const float gl2 = dead ? 0.f : g * kL2E;
+      for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+        mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
+        const float* rs = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
+        float x[KC];
+        if (MODE == MODE_FWD) {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) x[j] = rs[j * WS_M + t];
+        } else {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) {
+            const float f = rs[j * WS_M + t], l = rs[(KC + j) * WS_M + t];
+            x[j] = (l == PCB_NEG_INF || !(f > 0.f)) ? PCB_NEG_INF : lg2(f) - fmaf(l, kL2E, gl2);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&raw_empty[rr.slot()]));
+        rr.next();
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+          if (MODE == MODE_FWD)
+            x[j] = dead ? 0.f : ex2(fmaf(x[j], kL2E, -gl2));
+          else
+            x[j] = dead ? 0.f : ex2(x[j]);  // ex2(-inf) = 0: impossible sums, zero flow
+        }
+        mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
+        uint8_t* sAh = ops + orr.slot() * C::kOp;
+        uint8_t* sAl = sAh + C::kA;
+#pragma unroll
+        for (int q = 0; q < KC / 8; ++q) {
+          float v8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v8[e] = x[q * 8 + e];
+          uint4 hi, lo;
+          split_pack8(v8, hi, lo);
+          const uint32_t off = kmajor_off(t, q * 8, KC);
+          *reinterpret_cast<uint4*>(sAh + off) = hi;
+          *reinterpret_cast<uint4*>(sAl + off) = lo;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&op_full[orr.slot()]));
+        orr.next();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&g_empty[gs]));
+      ++g_u;
+    }
+  } else {
+    // ------------------------------------------------------------ shift + epilogue
+    // warps 6..13: lane quarter q4 = warp % 4 (TMEM lanes 32*q4..), column
+    // half h; warps 6-9 (h = 0) also publish the converters' shift.
+    const int q4 = warp & 3;
+    const int h = (warp - WS_EPI0) >> 2;
+    const int t = q4 * 32 + lane;          // sample within the item
+    auto shift_of = [&](int item, int& nk) {
+      const int sr = item / a.ntiles;
+      const int b = (item - sr * a.ntiles) * WS_M + t;
+      const int m0 = a.row_off[sr];
+      const int64_t r0 = a.members[m0];
+      const int32_t* src = a.src_ids + r0 * a.cap;
+      const int32_t* real = a.real_ids + r0 * a.cap;
+      float g = PCB_NEG_INF;
+      nk = 0;
+      for (int c = 0; c < a.cap; ++c) {
+        if (__ldg(real + c) == 0) continue;
+        ++nk;
+        if (b < a.B) g = fmaxf(g, a.shift[(int64_t)(__ldg(src + c) - a.sb_base) / KC * a.ldb + b]);
+      }
+      return g;
+    };
+    int g_u = 0, acc_u = 0;
+    int item = blockIdx.x;
+    int nk = 0, nk_next = 0;
+    float g = 0.f;
+    if (item < a.n_items) {
+      g = shift_of(item, nk);
+      if (h == 0) {
+        g_s[0][t] = g;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&g_full[0]));
+      }
+    }
+    for (; item < a.n_items; item += gridDim.x) {
+      // the next item's shift, computed (and for h = 0 published) before
+      // draining this one
+      const int nxt = item + gridDim.x;
+      float g_next = 0.f;
+      if (nxt < a.n_items) {
+        const int gs = (g_u + 1) & 1;
+        if (h == 0) mbar_wait(smem_u32(&g_empty[gs]), (uint32_t)((((g_u + 1) >> 1) & 1) ^ 1));
+        g_next = shift_of(nxt, nk_next);
+        if (h == 0) {
+          g_s[gs][t] = g_next;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&g_full[gs]));
+        }
+      }
+      const int sr = item / a.ntiles;
+      const int b = (item - sr * a.ntiles) * WS_M + t;
+      const bool live = b < a.B;
+      const int m0 = a.row_off[sr];
+      const int S = a.row_off[sr + 1] - m0;
+      const int N = S * a.nb;
+      const int as = acc_u & 1;
+      const bool dead = g == PCB_NEG_INF || nk == 0;
+      auto out_row = [&](int c0) {  // first output row of the 16 columns at c0
+        const int s = c0 / a.nb, j0 = c0 - s * a.nb;  // nb is a multiple of 16
+        return (int64_t)__ldg(a.out_ids + __ldg(a.members + m0 + s)) + j0;
+      };
+      // child flow: the epilogue also reads the children's log values; the
+      // next chunk's are loaded before this chunk's TMEM load
+      float l[16], ln[16];
+      if (MODE == MODE_CF && live && h * 16 < N) {
+        const float* lp = a.aux + out_row(h * 16) * a.ldb + b;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ln[i] = lp[(int64_t)i * a.ldb];
+      }
+      mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t)(as * WS_NMAX) + ((uint32_t)(q4 * 32) << 16);
+      for (int c0 = h * 16; c0 < N; c0 += 32) {
+        if (MODE == MODE_CF) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) l[i] = ln[i];
+          if (live && c0 + 32 < N) {
+            const float* lp = a.aux + out_row(c0 + 32) * a.ldb + b;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ln[i] = lp[(int64_t)i * a.ldb];
+          }
+        }
+        float v[16];
+        tmem_ld16(tbase + c0, v);
+        if (!live) continue;
+        float* o = a.out + out_row(c0) * a.ldb + b;
+        if (MODE == MODE_FWD) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float d = nk ? v[i] : 0.f;
+            o[(int64_t)i * a.ldb] = (dead || !(d > 0.f)) ? PCB_NEG_INF : fmaf(lg2(d), kLN2, g);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float d = nk ? v[i] : 0.f;
+            // flow = D * exp(g + l_child), evaluated as 2^(log2 D + (g + l) log2 e)
+            o[(int64_t)i * a.ldb] = (dead || !(d > 0.f)) ? 0.f : ex2(lg2(d) + (g + l[i]) * kL2E);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
+      ++acc_u;
+      ++g_u;
+      g = g_next;
+      nk = nk_next;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WS_MMA) tmem_free(tmem, 512);
+}
+
+namespace {
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+template <int MODE, int KC>
+int launch_ws(const WsArgs& a, cudaStream_t s) {
+  using C = WsCfg<MODE, KC>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_sum_ws<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kBytes) != cudaSuccess)
+      return PCB_CUDA;
+    attr = true;
+  }
+  const int grid = min(a.n_items, sm_count());
+  k_sum_ws<MODE, KC><<<grid, WS_THREADS, C::kBytes, s>>>(a);
+  return check_launch();
+}
+
+}  // namespace
+
+bool ws_supported(int kc, int nb) { return (kc == 16 || kc == 32) && (nb == 16 || nb == 32 || nb == 64); }
+
+int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
+                      cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
+                      float* values) {
+  ProfScope prof_(KC_SUM_FWD_TC, s);
+  if (!tc.count || !B) return PCB_OK;
+  WsArgs a{};
+  a.cap = (int)g.cap;
+  a.nb = (int)L.k_m;
+  a.B = B;
+  a.ldb = ldb;
+  a.ntiles = (B + WS_M - 1) / WS_M;
+  a.n_items = (int)tc.count * a.ntiles;
+  a.sb_base = 0;
+  a.row_off = tc.row_off;
+  a.members = tc.members;
+  a.out_ids = g.sum_ids;
+  a.src_ids = g.prod_ids;
+  a.real_ids = g.param_ids;
+  a.slab = g.param_slab;
+  a.mma = P->mma;
+  a.src0 = scratch;
+  a.src1 = nullptr;
+  a.shift = bmax;
+  a.aux = nullptr;
+  a.out = values;
+  switch (L.k_n) {
+    case 16: return launch_ws<MODE_FWD, 16>(a, s);
+    case 32: return launch_ws<MODE_FWD, 32>(a, s);
+    default: return PCB_USAGE;
+  }
+}
+
+int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
+                         cudaStream_t s, int B, int ldb, const float* values, const float* flows,
+                         const float* scratch, const float* rmax, float* flow_scratch) {
+  ProfScope prof_(KC_CHILD_FLOW, s);
+  if (!tc.count || !B) return PCB_OK;
+  WsArgs a{};
+  a.cap = (int)g.cap;
+  a.nb = (int)L.k_n;
+  a.B = B;
+  a.ldb = ldb;
+  a.ntiles = (B + WS_M - 1) / WS_M;
+  a.n_items = (int)tc.count * a.ntiles;
+  a.sb_base = L.sb_base;
+  a.row_off = tc.row_off;
+  a.members = tc.members;
+  a.out_ids = g.ch_ids;
+  a.src_ids = g.par_ids;
+  a.real_ids = g.par_param_ids;
+  a.slab = g.par_slab;
+  a.mma = P->mma;
+  a.src0 = flows;
+  a.src1 = values;
+  a.shift = rmax;
+  a.aux = scratch;
+  a.out = flow_scratch;
+  switch (L.k_m) {
+    case 16: return launch_ws<MODE_CF, 16>(a, s);
+    case 32: return launch_ws<MODE_CF, 32>(a, s);
+    default: return PCB_USAGE;
+  }
+}
+
+}  // namespace pcb

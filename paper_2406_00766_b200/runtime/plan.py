@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 6
+VERSION = 7
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -91,7 +91,9 @@ def mma_tiles(compiled, tensor_cores: bool = True):
     """Unique parameter tiles of tensor-core layers and their bf16 slab offsets.
 
     Returns (theta starts sorted, slab offsets, k_m, k_n, total bf16 elements);
-    each tile occupies 2 * k_m * k_n bf16 (hi plane, lo plane)."""
+    each tile occupies 4 * k_m * k_n bf16: hi and lo planes of the tile in
+    sum-major core order (the K-major B operand of the sum forward), then hi
+    and lo planes of its transpose (the K-major B operand of the child flows)."""
     starts, kms, kns = [], [], []
     if tensor_cores:
         for L in compiled.layers:
@@ -110,7 +112,7 @@ def mma_tiles(compiled, tensor_cores: bool = True):
     kn = np.concatenate(kns)
     s, first = np.unique(s, return_index=True)  # a tied tile may recur across layers
     km, kn = km[first], kn[first]
-    size = 2 * km * kn
+    size = 4 * km * kn
     slab = np.concatenate([[0], np.cumsum(size)[:-1]]).astype(np.int64)
     return s, slab, km, kn, int(size.sum())
 
@@ -215,10 +217,29 @@ def build_program(compiled, *, tensor_cores: bool = True):
         ref(blocks[key])
     prog.append(int((blocks["ncat"] * blocks["count"]).max()) if nb else 0)
 
+    # pushes per value slot over the whole backward pass (root pushes included):
+    # a slot with exactly one push takes a plain store instead of an atomic add
+    push_count = np.zeros(c.num_value_slots, dtype=np.int64)
+    for L in c.layers:
+        for p in L.pushes:
+            np.add.at(push_count, p.children.ravel(), 1)
+    if c.root_children is not None and c.root_row >= 0:
+        np.add.at(push_count, np.asarray(c.root_children, dtype=np.int64), 1)
+    # the last layer (in backward order: the highest) accumulating each product row
+    # writes it instead of adding; every row written => no prod_flows memset
+    last_layer = np.full(max(c.num_prod_rows, 1), -1, dtype=np.int64)
+    for li, L in enumerate(c.layers):
+        last_layer[np.asarray(L.prod_rows, dtype=np.int64)] = li
+    covered = np.ones(last_layer.size, dtype=bool)
+    covered[last_layer < 0] = False
+    if c.root_row >= 0:
+        covered[c.root_row] = True
+    prog.append(1 if bool(covered.all()) else 0)
+
     n_tc_rows = 0
     scratch_off = 0
     prog.append(len(c.layers))
-    for L in c.layers:
+    for li, L in enumerate(c.layers):
         prog += [L.k_m, L.k_n, L.scratch_window, int(L.prod_slots.size), scratch_off]
         scratch_off += L.scratch_window
         use_tc = tensor_cores and tc_layer(L)
@@ -289,17 +310,27 @@ def build_program(compiled, *, tensor_cores: bool = True):
         sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
             np.zeros(0, np.int64)
         prog += [int(sids.min()) if sids.size else 0, int(sids.size)]
-        # derived: fused accumulate + push table in product order
-        push_of = {}
+        # derived: fused accumulate + push table in product order.  flag bit 0:
+        # push the finished row; bit 1: first accumulation of the row in the
+        # backward pass (store, not add).  Children are encoded slot * 2 +
+        # (1 if the slot has a single push in the whole pass: plain store).
+        prow_arr = np.asarray(L.prod_rows, dtype=np.int64)
+        n_pr = prow_arr.size
+        pfan = np.zeros(n_pr, dtype=np.int64)
+        pos_of_row = {}
+        if L.pushes:
+            pos_of_row = {r: i for i, r in enumerate(prow_arr.tolist())}
+        parts = [None] * n_pr
         for p in L.pushes:
-            for r, ch in zip(p.rows.tolist(), p.children):
-                push_of[r] = ch
-        flags = np.array([1 if r in push_of else 0 for r in L.prod_rows.tolist()], np.int64)
-        pfan = np.array([push_of[r].size if r in push_of else 0
-                         for r in L.prod_rows.tolist()], np.int64)
+            idx = np.fromiter((pos_of_row[r] for r in p.rows.tolist()), np.int64, p.rows.size)
+            pfan[idx] = p.children.shape[1]
+            for i, ch in zip(idx.tolist(), p.children):
+                parts[i] = ch
+        flags = (pfan > 0).astype(np.int64) | (2 * (last_layer[prow_arr] == li)).astype(np.int64)
         poff = np.concatenate([[0], np.cumsum(pfan)]).astype(np.int64)
-        pch = (np.concatenate([push_of[r] for r in L.prod_rows.tolist() if r in push_of])
+        pch = (np.concatenate([q for q in parts if q is not None]).astype(np.int64)
                if pfan.sum() else np.zeros(0, np.int64))
+        pch = pch * 2 + (push_count[pch] == 1)
         ref(flags)
         ref(poff)
         ref(pch)
