@@ -11,11 +11,12 @@
 // so the batch tiles of one super-row run side by side and share its theta
 // tiles through L2.
 //
-// Warp roles (14 warps):
-//   warp 0      producer: 1-D TMA bulk copies (cp.async.bulk) of the raw fp32
-//               rows of each K block (one row segment of 128 samples per lane)
-//               into the raw ring, and of the pre-split bf16 theta tiles into
-//               the operand ring;
+// Warp roles (15 warps):
+//   warp 0      raw producer: one 2-D TMA box (cp.async.bulk.tensor) of the
+//               K block's fp32 rows x 128 samples per source array into the
+//               raw ring;
+//   warp 14     theta producer: 1-D bulk copies of the stacked pre-split bf16
+//               theta planes into the operand ring;
 //   warp 1      MMA issuer: three kind::f16 MMAs per 16-wide K step
 //               (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM), commits
 //               free operand stages and publish finished accumulators;
@@ -28,6 +29,8 @@
 //               (two warps per TMEM lane quarter, alternate 16-column chunks).
 // Every hand-off is an mbarrier: raw full/empty, operand full/empty,
 // accumulator full/empty, shift full/empty.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 
 #include "pcb_internal.cuh"
@@ -41,8 +44,8 @@ namespace {
 
 constexpr int WS_M = 128;           // samples per item
 constexpr int WS_NMAX = 256;        // stacked N per item
-constexpr int WS_THREADS = 448;     // 14 warps
-constexpr int WS_PRODUCER = 0, WS_MMA = 1, WS_CONV0 = 2, WS_EPI0 = 6;
+constexpr int WS_THREADS = 480;     // 15 warps
+constexpr int WS_PRODUCER = 0, WS_MMA = 1, WS_CONV0 = 2, WS_EPI0 = 6, WS_THETA = 14;
 
 enum { MODE_FWD = 0, MODE_CF = 1 };
 
@@ -76,9 +79,9 @@ struct WsCfg {
   static constexpr int kB = 2 * kBPlane;
   static constexpr int kOp = 2 * kA + kB;
   static constexpr int kBudget = 210 * 1024;
-  static constexpr int kOS = (KC <= 16) ? 4 : (MODE == MODE_CF ? 2 : 3);
+  static constexpr int kOS = (KC <= 16) ? 4 : 2;
   static constexpr int kRSmax = (kBudget - kOS * kOp) / kRaw;
-  static constexpr int kRS = kRSmax > 6 ? 6 : kRSmax;
+  static constexpr int kRS = kRSmax > 8 ? 8 : kRSmax;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static_assert(kRS >= 2, "raw ring too small");
 };
@@ -105,7 +108,9 @@ __device__ __forceinline__ int next_real(const int32_t* __restrict__ ids, int ca
 }  // namespace
 
 template <int MODE, int KC>
-__global__ void __launch_bounds__(WS_THREADS, 1) k_sum_ws(const WsArgs a) {
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    k_sum_ws(const WsArgs a, const __grid_constant__ CUtensorMap tm0,
+             const __grid_constant__ CUtensorMap tm1) {
   using C = WsCfg<MODE, KC>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS];
@@ -144,33 +149,42 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_sum_ws(const WsArgs a) {
   const int plane0 = (MODE == MODE_FWD) ? 0 : 2;  // sum-major / product-major planes
 
   if (warp == WS_PRODUCER) {
-    // ------------------------------------------------------------ producer
-    Ring rr(C::kRS), orr(C::kOS);
+    // ------------------------------------------------------------ raw producer
+    // one 2-D TMA box [KC rows x 128 samples] per source array and K block;
+    // samples past ldb are zero-filled by the TMA unit
+    if (lane == 0) {
+      prefetch_tmap(&tm0);
+      if (MODE == MODE_CF) prefetch_tmap(&tm1);
+      Ring rr(C::kRS);
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        const int sr = item / a.ntiles;
+        const int b0 = (item - sr * a.ntiles) * WS_M;
+        const int r0 = a.members[a.row_off[sr]];
+        const int32_t* src = a.src_ids + (int64_t)r0 * a.cap;
+        const int32_t* real = a.real_ids + (int64_t)r0 * a.cap;
+        for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+          const int row0 = __ldg(src + c);
+          mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
+          const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
+          mbar_arrive_expect_tx(rf, (uint32_t)C::kRaw);
+          const uint32_t dst = smem_u32(raw + rr.slot() * C::kRaw);
+          tma_load_2d(dst, &tm0, b0, row0, rf);
+          if (MODE == MODE_CF) tma_load_2d(dst + KC * WS_M * 4, &tm1, b0, row0, rf);
+          rr.next();
+        }
+      }
+    }
+  } else if (warp == WS_THETA) {
+    // ------------------------------------------------------------ theta producer
+    // stacked theta tiles of each K block: hi planes back to back, then lo
+    // planes, so the S tiles form one N = S * nb operand per plane
+    Ring orr(C::kOS);
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const int sr = item / a.ntiles;
-      const int b0 = (item - sr * a.ntiles) * WS_M;
       const int m0 = a.row_off[sr];
       const int S = a.row_off[sr + 1] - m0;
-      const int r0 = a.members[m0];
-      const int32_t* src = a.src_ids + (int64_t)r0 * a.cap;
-      const int32_t* real = a.real_ids + (int64_t)r0 * a.cap;
-      const uint32_t seg = (uint32_t)min(WS_M, a.ldb - b0) * 4u;  // bytes per row segment
+      const int32_t* real = a.real_ids + (int64_t)a.members[m0] * a.cap;
       for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
-        const int64_t row0 = __ldg(src + c);
-        // raw rows of this K block
-        mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
-        const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
-        if (lane == 0) mbar_arrive_expect_tx(rf, (uint32_t)C::kRows * seg);
-        __syncwarp();
-        uint8_t* dst = raw + rr.slot() * C::kRaw;
-        for (int r = lane; r < C::kRows; r += 32) {
-          const float* base = (MODE == MODE_CF && r >= KC) ? a.src1 : a.src0;
-          const int rr_ = (MODE == MODE_CF && r >= KC) ? r - KC : r;
-          bulk_g2s(smem_u32(dst + r * (WS_M * 4)), base + (row0 + rr_) * a.ldb + b0, seg, rf);
-        }
-        rr.next();
-        // stacked theta tiles of this K block: hi planes back to back, then lo
-        // planes, so the S tiles form one N = S * nb operand per plane
         mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
         const uint32_t of = smem_u32(&op_full[orr.slot()]);
         uint8_t* bdst = ops + orr.slot() * C::kOp + 2 * C::kA;
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_sum_ws(const WsArgs a) {
       if (lane == 0) mbar_arrive(smem_u32(&g_empty[gs]));
       ++g_u;
     }
-  } else {
+  } else if (warp >= WS_EPI0) {
     // ------------------------------------------------------------ shift + epilogue
     // warps 6..13: lane quarter q4 = warp % 4 (TMEM lanes 32*q4..), column
     // half h; warps 6-9 (h = 0) also publish the converters' shift.
@@ -425,8 +439,35 @@ int sm_count() {
   return n;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 map over a node-major buffer [rows x ldb], box [box_rows x 128 samples]
+int make_rows_map(CUtensorMap* m, const float* base, int64_t rows, int ldb, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return PCB_CUDA;
+  const cuuint64_t dims[2] = {(cuuint64_t)ldb, (cuuint64_t)(rows > 0 ? rows : 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldb * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)WS_M, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PCB_OK : PCB_CUDA;
+}
+
 template <int MODE, int KC>
-int launch_ws(const WsArgs& a, cudaStream_t s) {
+int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   using C = WsCfg<MODE, KC>;
   static bool attr = false;
   if (!attr) {
@@ -435,8 +476,12 @@ int launch_ws(const WsArgs& a, cudaStream_t s) {
       return PCB_CUDA;
     attr = true;
   }
+  CUtensorMap tm0, tm1;
+  if (make_rows_map(&tm0, a.src0, rows0, a.ldb, KC)) return PCB_CUDA;
+  if (make_rows_map(&tm1, a.src1 ? a.src1 : a.src0, a.src1 ? rows1 : rows0, a.ldb, KC))
+    return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_sum_ws<MODE, KC><<<grid, WS_THREADS, C::kBytes, s>>>(a);
+  k_sum_ws<MODE, KC><<<grid, WS_THREADS, C::kBytes, s>>>(a, tm0, tm1);
   return check_launch();
 }
 
@@ -470,8 +515,8 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.aux = nullptr;
   a.out = values;
   switch (L.k_n) {
-    case 16: return launch_ws<MODE_FWD, 16>(a, s);
-    case 32: return launch_ws<MODE_FWD, 32>(a, s);
+    case 16: return launch_ws<MODE_FWD, 16>(a, L.window, 0, s);
+    case 32: return launch_ws<MODE_FWD, 32>(a, L.window, 0, s);
     default: return PCB_USAGE;
   }
 }
@@ -502,8 +547,8 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.aux = scratch;
   a.out = flow_scratch;
   switch (L.k_m) {
-    case 16: return launch_ws<MODE_CF, 16>(a, s);
-    case 32: return launch_ws<MODE_CF, 32>(a, s);
+    case 16: return launch_ws<MODE_CF, 16>(a, P->num_value_slots, P->num_value_slots, s);
+    case 32: return launch_ws<MODE_CF, 32>(a, P->num_value_slots, P->num_value_slots, s);
     default: return PCB_USAGE;
   }
 }
