@@ -86,8 +86,9 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
                             const int32_t* d_x, int32_t* d_xT);
 
 /* Floats of device workspace (d_work) the passes below need at row stride ldb:
- * per-(product block, sample) child maxima and per-(sum block, sample) flow-ratio
- * maxima.  Derived state, not part of the reference's buffers. */
+ * per-(product block, sample) child maxima, per-(sum block, sample) flow-ratio
+ * maxima and per-(sum, sample) shifted log2 flow ratios of one layer.  Derived
+ * state, not part of the reference's buffers. */
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb);
 
 /* Full forward pass: values, scratch, lroot[B].

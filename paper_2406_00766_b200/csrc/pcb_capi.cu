@@ -174,6 +174,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.n_pb = L.window / L.k_n;  // including the -inf pad block 0
     if (L.n_pb > P->max_pb) P->max_pb = L.n_pb;
     if (L.n_sb > P->max_sb) P->max_sb = L.n_sb;
+    if (L.n_sb * L.k_m > P->max_sum_rows) P->max_sum_rows = L.n_sb * L.k_m;
     P->layers.push_back(std::move(L));
   }
   P->red_n = r.get();
@@ -267,6 +268,7 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   Work w;
   w.bmax = d_work;
   w.rmax = d_work + P->max_pb * (int64_t)ldb;
+  w.ratio = w.rmax + P->max_sb * (int64_t)ldb;
   return w;
 }
 
@@ -298,14 +300,17 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   int st = PCB_OK;
   const bool tc = P->use_tc && tc_bwd_supported(L);
   if (tc) {
-    st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax);
+    st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax, w.ratio);
     if (st) return st;
   }
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
-      st = launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
-                                w.rmax, f_params);
+      st = (P->use_tc == 1 && pf_ws_supported(L))
+               ? launch_param_flow_ws(L, L.fwd[g], T, s, B, ldb, theta, w.ratio, w.rmax, scratch,
+                                      f_params)
+               : launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
+                                      w.rmax, f_params);
     else
       st = launch_param_flow_simt(L, L.fwd[g], s, B, ldb, theta, values, flows, scratch,
                                   f_params);
@@ -315,8 +320,8 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     const TcRows& T = L.bwd_tc[g];
     if (tc && T.count > 0)
       st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
-               ? launch_child_flow_ws(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
-                                      w.rmax, flow_scratch)
+               ? launch_child_flow_ws(P, L, L.bwd[g], T, s, B, ldb, w.ratio, scratch, w.rmax,
+                                      flow_scratch)
                : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
                                       w.rmax, flow_scratch);
     else
@@ -366,7 +371,7 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
 
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
-  return (plan->max_pb + plan->max_sb) * (int64_t)ldb;
+  return (plan->max_pb + plan->max_sb + plan->max_sum_rows) * (int64_t)ldb;
 }
 
 int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,

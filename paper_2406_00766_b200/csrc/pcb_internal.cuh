@@ -82,10 +82,13 @@ struct Layer {
 
 // Workspace carved from the caller's d_work buffer (pcb_plan_workspace_floats):
 //   bmax [max_pb x ldb]  per product block and sample: max child log value
-//   rmax [max_sb x ldb]  per sum block and sample: max log(flow) - log(value)
+//   rmax [max_sb x ldb]  per sum block and sample: max lg2(flow) - value*log2(e)
+//   ratio [max_sum_rows x ldb] per sum row of the layer: log2 flow ratio minus
+//                               its block's rmax (k_ratio)
 struct Work {
   float* bmax;
   float* rmax;
+  float* ratio;
 };
 
 }  // namespace pcb
@@ -107,7 +110,7 @@ struct pcb_plan {
   int64_t n_groups;
   const int32_t *group_idx, *group_off;
   int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported); 2: legacy TC
-  int64_t max_pb = 1, max_sb = 1;
+  int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1;
   // bf16 tensor-core copies of theta tiles (plan v4)
   int64_t n_mma_tiles = 0, mma_elems = 0;
   const int32_t *mma_theta = nullptr, *mma_slab = nullptr, *mma_km = nullptr, *mma_kn = nullptr;
@@ -162,7 +165,7 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
                      float* scratch, float* bmax);
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
-                     const float* flows, float* rmax);
+                     const float* flows, float* rmax, float* ratio);
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                         const float* theta, const float* scratch, float* values);
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
@@ -205,8 +208,12 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
                       float* values);
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
-                         cudaStream_t s, int B, int ldb, const float* values, const float* flows,
-                         const float* scratch, const float* rmax, float* flow_scratch);
+                         cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
+                         const float* rmax, float* flow_scratch);
+bool pf_ws_supported(const Layer& L);
+int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
+                         int B, int ldb, const float* theta, const float* ratio, const float* rmax,
+                         const float* scratch, float* f_params);
 int launch_child_flow_tc(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* values, const float* flows,
                          const float* scratch, const float* rmax, float* flow_scratch);

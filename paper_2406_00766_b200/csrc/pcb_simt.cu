@@ -245,6 +245,7 @@ int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, f
 constexpr int VB = 4;              // samples per lane (float4)
 constexpr int SLAB = 32 * VB;      // samples per CTA
 constexpr int RW = 8;              // warps per CTA (rows in flight)
+constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ float4 f4max(float4 a, float4 b) {
   return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), fmaxf(a.w, b.w));
@@ -303,36 +304,76 @@ int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float
   return check_launch();
 }
 
-// rmax[sb, b] = max over the block's sums of log(flow) - log(value) (-inf for
-// impossible sums): the per-sample shift for the flow contractions.
+// Flow ratios of one sum block (engine.py:114-117), in log2 units:
+//   R[sb, b]  = max over the block's sums of lg2(flow) - value * log2(e)
+//               (-inf when every sum is impossible or flowless): the shift;
+//   r[m, b]   = lg2(flow_m) - fma(value_m, log2 e, R)  (<= 0; -inf for
+//               impossible / zero-flow sums), r rows indexed from sb_base.
+// The shift only has to be applied consistently: every product of a large
+// log value with log2(e) is fused with the subtraction of R, so r keeps full
+// precision even at |log p| ~ 1e4.  The tensor-core flow kernels read r (one
+// row per sum instead of flows + values) and R.
+constexpr int KM_MAX = 64;
 __global__ void __launch_bounds__(RW * 32)
-    k_ratio_max(int k_m, int B, int ldb, int64_t sb_base, const float* __restrict__ values,
-                const float* __restrict__ flows, float* __restrict__ rmax) {
+    k_ratio(int k_m, int B, int ldb, int64_t sb_base, const float* __restrict__ values,
+            const float* __restrict__ flows, float* __restrict__ rmax, float* __restrict__ ratio) {
+  constexpr int PER = KM_MAX / RW;
   const int blk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.y * SLAB + lane * VB;
   const bool live = b < B;
   const float ninf = PCB_NEG_INF;
+  float4 t[PER];
   float4 mx = make_float4(ninf, ninf, ninf, ninf);
-  if (live)
-    for (int m = warp; m < k_m; m += RW) {
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int m = warp + u * RW;
+    t[u] = make_float4(ninf, ninf, ninf, ninf);
+    if (live && m < k_m) {
       const int64_t o = (sb_base + (int64_t)blk * k_m + m) * ldb + b;
       const float4 f = *reinterpret_cast<const float4*>(flows + o);
       const float4 l = *reinterpret_cast<const float4*>(values + o);
-      mx.x = fmaxf(mx.x, (l.x == ninf) ? ninf : __logf(f.x) - l.x);
-      mx.y = fmaxf(mx.y, (l.y == ninf) ? ninf : __logf(f.y) - l.y);
-      mx.z = fmaxf(mx.z, (l.z == ninf) ? ninf : __logf(f.z) - l.z);
-      mx.w = fmaxf(mx.w, (l.w == ninf) ? ninf : __logf(f.w) - l.w);
+      // t = lg2 f, with l folded in only for the (imprecise) max
+      t[u].x = (l.x == ninf || !(f.x > 0.f)) ? ninf : __log2f(f.x);
+      t[u].y = (l.y == ninf || !(f.y > 0.f)) ? ninf : __log2f(f.y);
+      t[u].z = (l.z == ninf || !(f.z > 0.f)) ? ninf : __log2f(f.z);
+      t[u].w = (l.w == ninf || !(f.w > 0.f)) ? ninf : __log2f(f.w);
+      if (t[u].x != ninf) mx.x = fmaxf(mx.x, t[u].x - l.x * kLog2e);
+      if (t[u].y != ninf) mx.y = fmaxf(mx.y, t[u].y - l.y * kLog2e);
+      if (t[u].z != ninf) mx.z = fmaxf(mx.z, t[u].z - l.z * kLog2e);
+      if (t[u].w != ninf) mx.w = fmaxf(mx.w, t[u].w - l.w * kLog2e);
     }
-  block_max_store(mx, rmax + (int64_t)blk * ldb + b, live);
+  }
+  __shared__ float4 red[RW][32];
+  red[warp][lane] = mx;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < RW; ++w) mx = f4max(mx, red[w][lane]);
+  if (!live) return;
+  if (warp == 0) *reinterpret_cast<float4*>(rmax + (int64_t)blk * ldb + b) = mx;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int m = warp + u * RW;
+    if (m < k_m) {
+      const int64_t row = (int64_t)blk * k_m + m;
+      const float4 l = *reinterpret_cast<const float4*>(values + (sb_base + row) * ldb + b);
+      float4 r;
+      r.x = (t[u].x == ninf) ? ninf : t[u].x - fmaf(l.x, kLog2e, mx.x);
+      r.y = (t[u].y == ninf) ? ninf : t[u].y - fmaf(l.y, kLog2e, mx.y);
+      r.z = (t[u].z == ninf) ? ninf : t[u].z - fmaf(l.z, kLog2e, mx.z);
+      r.w = (t[u].w == ninf) ? ninf : t[u].w - fmaf(l.w, kLog2e, mx.w);
+      *reinterpret_cast<float4*>(ratio + row * ldb + b) = r;
+    }
+  }
 }
 
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
-                     const float* flows, float* rmax) {
+                     const float* flows, float* rmax, float* ratio) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!B || !L.n_sb) return PCB_OK;
+  if (L.k_m > KM_MAX) return PCB_USAGE;
   dim3 grid((unsigned)L.n_sb, (unsigned)((B + SLAB - 1) / SLAB));
-  k_ratio_max<<<grid, RW * 32, 0, s>>>((int)L.k_m, B, ldb, L.sb_base, values, flows, rmax);
+  k_ratio<<<grid, RW * 32, 0, s>>>((int)L.k_m, B, ldb, L.sb_base, values, flows, rmax, ratio);
   return check_launch();
 }
 

@@ -1,0 +1,425 @@
+// Warp-specialised, persistent tcgen05 parameter-flow kernel for sm_100a
+// (Alg. 3, engine.py:105-126):
+//
+//   cum[m, j] = sum_b e^{lnf[m,b] - c_b} e^{child[j,b] + c_b}
+//   f_params[flow(m, j)] += theta[m, j] * cum[m, j]
+//
+// a contraction over the batch.  A work item is one (super-row, column
+// group, 128-sum M tile, batch slice): M = the tile's sums, N = up to 256
+// child columns, K = samples streamed 32 at a time.  The shift c_b is the
+// per-sample max over the tile's sum blocks of the ratio shift R (k_ratio,
+// log2 units) and cancels between the two operands:
+//   A[m, b] = 2^{r[m,b] + R_blk(m)[b] - c_b},   E[j, b] = 2^{child[j,b] log2e + c_b}
+// (r = the shifted log2 ratio rows of k_ratio).  Both operands are split
+// into bf16 hi + lo and contracted as hi*hi + hi*lo + lo*hi (fp32 TMEM).
+//
+// Warp roles (14 warps):
+//   warp 0       producer: per 32-sample chunk, 2-D TMA boxes (128-byte
+//                swizzled) of the tile's r rows, its R rows and the child
+//                log-value rows into the raw ring;
+//   warp 1       MMA issuer (double-buffered TMEM accumulators, 2 x 256 cols);
+//   warps 2-9    converters: the chunk's shifts c_b, then raw -> exponentials
+//                -> packed bf16 planes in the K-major core-matrix layout;
+//   warps 10-13  epilogue: TMEM -> theta (.) cum -> red.add into f_params.
+#include <math.h>
+
+#include "pcb_internal.cuh"
+#include "pcb_tc.cuh"
+#include "pcb_ws.cuh"
+
+namespace pcb {
+
+using namespace tc;
+using namespace ws;
+
+namespace {
+
+constexpr int PF_M = 128;          // sums per tile
+constexpr int PF_N = 256;          // child columns per item
+constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzle row)
+constexpr int PF_THREADS = 448;    // 14 warps
+constexpr int PF_CONV0 = 2, PF_NCONV = 8, PF_EPI0 = 10;
+constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
+
+struct PfArgs {
+  int cap, k_m, B, ldb;
+  int n_items, mtiles, kslices, cgroups, nchunks;
+  int64_t sb_base;
+  const int32_t *row_off, *members, *sum_ids, *prod_ids, *param_ids, *flow_ids;
+  const float* theta;
+  float* f_params;
+};
+
+template <int KN>
+struct PfCfg {
+  static constexpr int kA = PF_M * PF_KS * 4;          // raw r rows of the tile
+  static constexpr int kE = PF_N * PF_KS * 4;          // raw child rows
+  static constexpr int kR = PF_MAXMEM * PF_KS * 4;     // raw R rows (one per sum block)
+  static constexpr int kRaw = kA + kE + kR;
+  static constexpr int kOpA = PF_M * PF_KS * 2;        // one bf16 A plane
+  static constexpr int kOpB = PF_N * PF_KS * 2;        // one bf16 B plane
+  static constexpr int kOp = 2 * kOpA + 2 * kOpB;
+  static constexpr int kRS = 2, kOS = 2;
+  static constexpr int kBytes = kRS * kRaw + kOS * kOp;
+  static constexpr int kCPG = PF_N / KN;                // child columns per item
+  static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need 1024-byte alignment");
+};
+
+struct PfItem {
+  int sr, cg, mt, ks;
+  int m0, S, r0;       // super-row members
+  int s_lo, nmem;      // member blocks of the tile
+  int rows;            // live sum rows of the tile
+  int kc0, kc1;        // chunk range
+};
+
+__device__ __forceinline__ PfItem pf_item(const PfArgs& a, int item) {
+  PfItem it;
+  it.mt = item % a.mtiles;
+  int q = item / a.mtiles;
+  it.ks = q % a.kslices;
+  q /= a.kslices;
+  it.cg = q % a.cgroups;
+  it.sr = q / a.cgroups;
+  it.m0 = a.row_off[it.sr];
+  it.S = a.row_off[it.sr + 1] - it.m0;
+  it.r0 = a.members[it.m0];
+  const int nsum = it.S * a.k_m;
+  it.rows = min(PF_M, nsum - it.mt * PF_M);
+  it.s_lo = it.mt * PF_M / a.k_m;
+  it.nmem = it.rows > 0 ? (it.rows + a.k_m - 1) / a.k_m : 0;
+  const int per = (a.nchunks + a.kslices - 1) / a.kslices;
+  it.kc0 = it.ks * per;
+  it.kc1 = min(a.nchunks, it.kc0 + per);
+  return it;
+}
+
+// the item's real child columns (at most kCPG): writes cols[], returns count
+__device__ __forceinline__ int pf_cols(const PfArgs& a, const PfItem& it, int cpg, int* cols) {
+  const int32_t* trow = a.param_ids + (int64_t)it.r0 * a.cap;
+  int seen = 0, n = 0;
+  for (int c = 0; c < a.cap && n < cpg; ++c) {
+    if (__ldg(trow + c) == 0) continue;
+    if (seen >= it.cg * cpg) cols[n++] = c;
+    ++seen;
+  }
+  return n;
+}
+
+__device__ __forceinline__ bool pf_active(const PfItem& it) { return it.rows > 0 && it.kc0 < it.kc1; }
+
+// element (row, k) of a 128-byte-swizzled fp32 box with 32-float rows
+__device__ __forceinline__ float swz(const float* box, int row, int k) {
+  return box[row * 32 + ((((k >> 2) ^ (row & 7)) << 2) | (k & 3))];
+}
+
+}  // namespace
+
+template <int KN>
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    k_param_flow_ws(const PfArgs a, const __grid_constant__ CUtensorMap tm_r,
+                    const __grid_constant__ CUtensorMap tm_R, const __grid_constant__ CUtensorMap tm_e) {
+  using C = PfCfg<KN>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOS], op_empty[C::kOS];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
+  __shared__ float cs[C::kRS][PF_KS];
+  __shared__ int cols_p[C::kCPG];
+  __shared__ uint32_t tmem_base;
+  uint8_t* raw = smem;
+  uint8_t* ops = smem + C::kRS * C::kRaw;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < C::kRS; ++i) {
+      mbar_init(smem_u32(&raw_full[i]), 1);
+      mbar_init(smem_u32(&raw_empty[i]), PF_NCONV);
+    }
+    for (int i = 0; i < C::kOS; ++i) {
+      mbar_init(smem_u32(&op_full[i]), PF_NCONV);
+      mbar_init(smem_u32(&op_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(smem_u32(&tmem_base), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      prefetch_tmap(&tm_r);
+      prefetch_tmap(&tm_R);
+      prefetch_tmap(&tm_e);
+      Ring rr(C::kRS);
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        const PfItem it = pf_item(a, item);
+        if (!pf_active(it)) continue;
+        const int ncol = pf_cols(a, it, C::kCPG, cols_p);
+        if (!ncol) continue;
+        const int32_t* prow = a.prod_ids + (int64_t)it.r0 * a.cap;
+        const uint32_t bytes = (uint32_t)(it.nmem * a.k_m + it.nmem + ncol * KN) * PF_KS * 4;
+        for (int kc = it.kc0; kc < it.kc1; ++kc) {
+          const int b0 = kc * PF_KS;
+          mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
+          const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
+          mbar_arrive_expect_tx(rf, bytes);
+          const uint32_t st = smem_u32(raw + rr.slot() * C::kRaw);
+          for (int s = 0; s < it.nmem; ++s) {
+            const int row = __ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo + s)) - (int)a.sb_base;
+            tma_load_2d(st + s * a.k_m * PF_KS * 4, &tm_r, b0, row, rf);
+            tma_load_2d(st + C::kA + C::kE + s * PF_KS * 4, &tm_R, b0, row / a.k_m, rf);
+          }
+          for (int ci = 0; ci < ncol; ++ci)
+            tma_load_2d(st + C::kA + ci * KN * PF_KS * 4, &tm_e, b0, __ldg(prow + cols_p[ci]), rf);
+          rr.next();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    Ring orr(C::kOS);
+    int acc_u = 0;
+    constexpr uint32_t SBO = (PF_KS / 8) * 128;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      const PfItem it = pf_item(a, item);
+      if (!pf_active(it)) continue;
+      int cbuf[C::kCPG];
+      const int ncol = pf_cols(a, it, C::kCPG, cbuf);
+      if (!ncol) continue;
+      const uint32_t idesc = idesc_bf16(PF_M, ncol * KN);
+      const int as = acc_u & 1;
+      mbar_wait(smem_u32(&acc_empty[as]), (uint32_t)(((acc_u >> 1) & 1) ^ 1));
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(as * PF_N);
+      for (int kc = it.kc0; kc < it.kc1; ++kc) {
+        mbar_wait(smem_u32(&op_full[orr.slot()]), orr.full_par());
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t aH = smem_u32(ops + orr.slot() * C::kOp), aL = aH + C::kOpA;
+          const uint32_t bH = aL + C::kOpA, bL = bH + C::kOpB;
+#pragma unroll
+          for (int k = 0; k < PF_KS / 16; ++k) {
+            const uint64_t ah = make_desc(aH + k * 256, 128, SBO);
+            const uint64_t al = make_desc(aL + k * 256, 128, SBO);
+            const uint64_t bh = make_desc(bH + k * 256, 128, SBO);
+            const uint64_t bl = make_desc(bL + k * 256, 128, SBO);
+            mma_bf16(d, ah, bh, idesc, (kc > it.kc0 || k > 0) ? 1u : 0u);
+            mma_bf16(d, ah, bl, idesc, 1u);
+            mma_bf16(d, al, bh, idesc, 1u);
+          }
+          mma_commit(smem_u32(&op_empty[orr.slot()]));
+        }
+        __syncwarp();
+        orr.next();
+      }
+      if (lane == 0) mma_commit(smem_u32(&acc_full[as]));
+      __syncwarp();
+      ++acc_u;
+    }
+  } else if (warp < PF_EPI0) {
+    // ------------------------------------------------------------ converters
+    const int t = tid - PF_CONV0 * 32;  // 0..255
+    Ring rr(C::kRS), orr(C::kOS);
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      const PfItem it = pf_item(a, item);
+      if (!pf_active(it)) continue;
+      int cbuf[C::kCPG];
+      const int ncol = pf_cols(a, it, C::kCPG, cbuf);
+      if (!ncol) continue;
+      const int npad = ncol * KN;
+      for (int kc = it.kc0; kc < it.kc1; ++kc) {
+        const int b0 = kc * PF_KS;
+        mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
+        const float* rA = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
+        const float* rE = rA + C::kA / 4;
+        const float* rR = rE + C::kE / 4;
+        float* c_s = cs[rr.slot()];
+        if (t < PF_KS) {  // the chunk's per-sample shift: max of R over the tile's blocks
+          float v = PCB_NEG_INF;
+          if (b0 + t < a.B)
+            for (int s = 0; s < it.nmem; ++s) v = fmaxf(v, rR[s * PF_KS + t]);
+          c_s[t] = v;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(PF_NCONV * 32) : "memory");
+        mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
+        uint8_t* oAh = ops + orr.slot() * C::kOp;
+        uint8_t* oAl = oAh + C::kOpA;
+        uint8_t* oBh = oAl + C::kOpA;
+        uint8_t* oBl = oBh + C::kOpB;
+        // A: 128 rows x 4 octets; thread -> (row = q % 128, octet = q / 128)
+        for (int q = t; q < PF_M * (PF_KS / 8); q += PF_NCONV * 32) {
+          const int m = q & (PF_M - 1), o = q >> 7;
+          float v[8];
+          if (m < it.rows) {
+            const int blk = m / a.k_m;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int k = o * 8 + e;
+              const float c = c_s[k];
+              v[e] = (c == PCB_NEG_INF) ? 0.f : ex2(swz(rA, m, k) + (rR[blk * PF_KS + k] - c));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = 0.f;
+          }
+          uint4 hi, lo;
+          split_pack8(v, hi, lo);
+          const uint32_t off = kmajor_off(m, o * 8, PF_KS);
+          *reinterpret_cast<uint4*>(oAh + off) = hi;
+          *reinterpret_cast<uint4*>(oAl + off) = lo;
+        }
+        // E: npad rows x 4 octets
+        for (int q = t; q < npad * (PF_KS / 8); q += PF_NCONV * 32) {
+          const int n = q % npad, o = q / npad;
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int k = o * 8 + e;
+            const float c = c_s[k];
+            v[e] = (c == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(swz(rE, n, k), kL2E, c)), 1e37f);
+          }
+          uint4 hi, lo;
+          split_pack8(v, hi, lo);
+          const uint32_t off = kmajor_off(n, o * 8, PF_KS);
+          *reinterpret_cast<uint4*>(oBh + off) = hi;
+          *reinterpret_cast<uint4*>(oBl + off) = lo;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(smem_u32(&raw_empty[rr.slot()]));
+          mbar_arrive(smem_u32(&op_full[orr.slot()]));
+        }
+        rr.next();
+        orr.next();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q4 = warp & 3;
+    const int er = q4 * 32 + lane;  // sum row within the tile (TMEM lane)
+    int acc_u = 0;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      const PfItem it = pf_item(a, item);
+      if (!pf_active(it)) continue;
+      int cbuf[C::kCPG];
+      const int ncol = pf_cols(a, it, C::kCPG, cbuf);
+      if (!ncol) continue;
+      const bool live = er < it.rows;
+      const int s = it.s_lo + (live ? er / a.k_m : 0);
+      const int mm = er % a.k_m;
+      const int64_t rowbase = (int64_t)__ldg(a.members + it.m0 + s) * a.cap;
+      const int as = acc_u & 1;
+      mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t)(as * PF_N) + ((uint32_t)(q4 * 32) << 16);
+      for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + c0, v);
+        if (!live) continue;
+        const int c = cbuf[c0 / KN];
+        const int j0 = c0 % KN;
+        const int64_t tile = __ldg(a.param_ids + rowbase + c) + mm * KN + j0;
+        const int64_t flow = __ldg(a.flow_ids + rowbase + c) + mm * KN + j0;
+        const float* th = a.theta + tile;
+        float* dst = a.f_params + flow;
+        float w[16];  // zero-theta terms skipped (an overflowed cum must not make inf * 0)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float tv = __ldg(th + i);
+          w[i] = (tv != 0.f) ? tv * v[i] : 0.f;
+        }
+        if (((tile | flow) & 3) == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            atomicAdd(reinterpret_cast<float4*>(dst + i), make_float4(w[i], w[i + 1], w[i + 2], w[i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (w[i] != 0.f) atomicAdd(dst + i, w[i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
+      ++acc_u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, 512);
+}
+
+namespace {
+
+template <int KN>
+int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float* rmax,
+              const float* scratch, cudaStream_t s) {
+  using C = PfCfg<KN>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_param_flow_ws<KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kBytes) != cudaSuccess)
+      return PCB_CUDA;
+    attr = true;
+  }
+  PfArgs a = a0;
+  a.cgroups = (int)((a.cap * KN + PF_N - 1) / PF_N);
+  a.mtiles = 2;  // super-rows hold <= 256 sums
+  a.nchunks = (a.B + PF_KS - 1) / PF_KS;
+  // batch slices so small layers still cover the SMs; >= 2 chunks per slice
+  const int base = a.n_items * a.cgroups * a.mtiles;  // n_items holds the super-row count here
+  int ks = (2 * sm_count() + base - 1) / base;
+  a.kslices = max(1, min(ks, a.nchunks / 2));
+  a.n_items = base * a.kslices;
+  CUtensorMap tr, tR, te;
+  if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, true) ||
+      make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, PF_KS, false) ||
+      make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, true))
+    return PCB_CUDA;
+  const int grid = min(a.n_items, sm_count());
+  k_param_flow_ws<KN><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te);
+  return check_launch();
+}
+
+}  // namespace
+
+bool pf_ws_supported(const Layer& L) {
+  return (L.k_n == 16 || L.k_n == 32 || L.k_n == 64) && (L.k_m == 16 || L.k_m == 32 || L.k_m == 64);
+}
+
+int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
+                         int B, int ldb, const float* theta, const float* ratio, const float* rmax,
+                         const float* scratch, float* f_params) {
+  ProfScope prof_(KC_PARAM_FLOW, s);
+  if (!tc.count || !B) return PCB_OK;
+  PfArgs a{};
+  a.cap = (int)g.cap;
+  a.k_m = (int)L.k_m;
+  a.B = B;
+  a.ldb = ldb;
+  a.n_items = (int)tc.count;
+  a.sb_base = L.sb_base;
+  a.row_off = tc.row_off;
+  a.members = tc.members;
+  a.sum_ids = g.sum_ids;
+  a.prod_ids = g.prod_ids;
+  a.param_ids = g.param_ids;
+  a.flow_ids = g.flow_ids;
+  a.theta = theta;
+  a.f_params = f_params;
+  switch (L.k_n) {
+    case 16: return launch_pf<16>(a, L, ratio, rmax, scratch, s);
+    case 32: return launch_pf<32>(a, L, ratio, rmax, scratch, s);
+    case 64: return launch_pf<64>(a, L, ratio, rmax, scratch, s);
+    default: return PCB_USAGE;
+  }
+}
+
+}  // namespace pcb

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(TC_THREADS, (KM <= 32) ? 2 : 1)
     for (int p = 0; p < cap; ++p)
       if (pprow[p] != 0) gm = fmaxf(gm, rmax[((int64_t)parow[p] - sb_base) / KM * ldb + b]);
   const bool dead = (gm == PCB_NEG_INF);
-  const float gl2 = dead ? 0.f : gm * kL2E;
+  const float gl2 = dead ? 0.f : gm;  // rmax is in log2 units
 
   const uint32_t ncols = tmem_cols_for(N);
   if (tid == 0) {
@@ -339,9 +339,9 @@ __global__ void __launch_bounds__(TC_THREADS, (KM <= 32) ? 2 : 1)
       const int s = n / k_n, j = n - s * k_n;
       const int64_t o = (int64_t)(ch_ids[members[m0 + s]] + j) * ldb + b;
       const float d = (it > 0) ? v[i] : 0.f;
-      // flow = D * exp(g + l_child), evaluated as 2^(log2 D + (g + l) log2 e)
+      // flow = D * 2^g * exp(l_child), evaluated as 2^(log2 D + l log2 e + g)
       flow_scratch[o] = (dead || !(d > 0.f)) ? 0.f
-                                              : ex2(lg2(d) + (gm + scratch[o]) * kL2E);
+                                              : ex2(lg2(d) + fmaf(scratch[o], kL2E, gm));
     }
   }
   tc_fence_before();
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         const float c = cbs[q];
         x[e] = (!row_live || c == PCB_NEG_INF || b0 + q >= B)
                    ? 0.f
-                   : scaled_ratio(fn[e], ln[e], c * kL2E);
+                   : scaled_ratio(fn[e], ln[e], c);
       }
 #pragma unroll
       for (int kq = 0; kq < HS / 8; ++kq)
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float c = cbs[bk[u] * 8 + e];
-          x[e] = (c == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(ev[u][e], kL2E, c * kL2E)), 1e37f);
+          x[e] = (c == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(ev[u][e], kL2E, c)), 1e37f);
         }
         store_split8(sBh, sBl, kmajor_off(bn[u], bk[u] * 8, PF_KC), x);
       }

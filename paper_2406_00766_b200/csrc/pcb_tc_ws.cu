@@ -29,16 +29,16 @@
 //               (two warps per TMEM lane quarter, alternate 16-column chunks).
 // Every hand-off is an mbarrier: raw full/empty, operand full/empty,
 // accumulator full/empty, shift full/empty.
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <math.h>
 
 #include "pcb_internal.cuh"
 #include "pcb_tc.cuh"
+#include "pcb_ws.cuh"
 
 namespace pcb {
 
 using namespace tc;
+using namespace ws;
 
 namespace {
 
@@ -62,17 +62,17 @@ struct WsArgs {
   const int32_t* real_ids;         // param_ids (fwd) / par_param_ids (cf): 0 = padding column
   const int32_t* slab;             // bf16 tile offset per (member, column)
   const __nv_bfloat16* mma;
-  const float* src0;               // scratch (fwd) / flows (cf)
-  const float* src1;               // - / values (cf)
-  const float* shift;              // bmax (fwd) / rmax (cf)
+  const float* src0;               // scratch (fwd) / ratio rows r (cf, from sb_base)
+  const float* shift;              // bmax (fwd) / rmax R (cf)
   const float* aux;                // - / scratch (cf epilogue: child log values)
   float* out;                      // values (fwd) / flow_scratch (cf)
 };
 
 template <int MODE, int KC>
 struct WsCfg {
-  static constexpr int kSrc = MODE == MODE_CF ? 2 : 1;        // raw arrays per K block
-  static constexpr int kRows = KC * kSrc;                     // raw rows per stage
+  // raw rows per stage: the K block's rows (forward: child log values; child
+  // flow: shifted log2 flow ratios r) + (child flow) the block's shift row R
+  static constexpr int kRows = KC + (MODE == MODE_CF ? 1 : 0);
   static constexpr int kRaw = kRows * WS_M * 4;               // raw stage bytes
   static constexpr int kA = WS_M * KC * 2;                    // one bf16 A plane
   static constexpr int kBPlane = WS_NMAX * KC * 2;            // stacked theta hi (or lo) plane
@@ -85,25 +85,6 @@ struct WsCfg {
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static_assert(kRS >= 2, "raw ring too small");
 };
-
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-// ring position: slot and wait parities of use u of a ring with S stages
-struct Ring {
-  int S, u = 0;
-  __device__ explicit Ring(int s) : S(s) {}
-  __device__ int slot() const { return u % S; }
-  __device__ uint32_t full_par() const { return (uint32_t)((u / S) & 1); }
-  __device__ uint32_t empty_par() const { return full_par() ^ 1u; }
-  __device__ void next() { ++u; }
-};
-
-__device__ __forceinline__ int next_real(const int32_t* __restrict__ ids, int cap, int c) {
-  while (c < cap && __ldg(ids + c) == 0) ++c;
-  return c;
-}
 
 }  // namespace
 
@@ -163,13 +144,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const int32_t* src = a.src_ids + (int64_t)r0 * a.cap;
         const int32_t* real = a.real_ids + (int64_t)r0 * a.cap;
         for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
-          const int row0 = __ldg(src + c);
+          const int row0 = __ldg(src + c) - (int)a.sb_base;
           mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
           const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
           mbar_arrive_expect_tx(rf, (uint32_t)C::kRaw);
           const uint32_t dst = smem_u32(raw + rr.slot() * C::kRaw);
           tma_load_2d(dst, &tm0, b0, row0, rf);
-          if (MODE == MODE_CF) tma_load_2d(dst + KC * WS_M * 4, &tm1, b0, row0, rf);
+          if (MODE == MODE_CF) tma_load_2d(dst + KC * WS_M * 4, &tm1, b0, row0 / KC, rf);
           rr.next();
         }
       }
@@ -262,7 +243,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       mbar_wait(smem_u32(&g_full[gs]), (uint32_t)((g_u >> 1) & 1));
       const float g = g_s[gs][t];
       const bool dead = !live || g == PCB_NEG_INF;
-      const float gl2 = dead ? 0.f : g * kL2E;
+      // forward: g is a natural-log max (folded into one FFMA per element);
+      // child flow: g is already in log2 units
+      const float gl2 = dead ? 0.f : (MODE == MODE_FWD ? g * kL2E : g);
       for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
         const float* rs = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
@@ -271,11 +254,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < KC; ++j) x[j] = rs[j * WS_M + t];
         } else {
+          // r + (R_block - g): both shifts are fp32 log2 values, their
+          // difference is small and (near-)exact
+          const float d = rs[KC * WS_M + t] - gl2;
 #pragma unroll
-          for (int j = 0; j < KC; ++j) {
-            const float f = rs[j * WS_M + t], l = rs[(KC + j) * WS_M + t];
-            x[j] = (l == PCB_NEG_INF || !(f > 0.f)) ? PCB_NEG_INF : lg2(f) - fmaf(l, kL2E, gl2);
-          }
+          for (int j = 0; j < KC; ++j) x[j] = rs[j * WS_M + t] + d;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&raw_empty[rr.slot()]));
@@ -407,8 +390,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float d = nk ? v[i] : 0.f;
-            // flow = D * exp(g + l_child), evaluated as 2^(log2 D + (g + l) log2 e)
-            o[(int64_t)i * a.ldb] = (dead || !(d > 0.f)) ? 0.f : ex2(lg2(d) + (g + l[i]) * kL2E);
+            // flow = D * 2^g * exp(l_child) = 2^(log2 D + fma(l, log2 e, g))
+            o[(int64_t)i * a.ldb] = (dead || !(d > 0.f)) ? 0.f : ex2(lg2(d) + fmaf(l[i], kL2E, g));
           }
         }
       }
@@ -428,44 +411,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 
 namespace {
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-      n = 148;
-  }
-  return n;
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// 2-D fp32 map over a node-major buffer [rows x ldb], box [box_rows x 128 samples]
-int make_rows_map(CUtensorMap* m, const float* base, int64_t rows, int ldb, int box_rows) {
-  auto fn = encode_fn();
-  if (!fn) return PCB_CUDA;
-  const cuuint64_t dims[2] = {(cuuint64_t)ldb, (cuuint64_t)(rows > 0 ? rows : 1)};
-  const cuuint64_t strides[1] = {(cuuint64_t)ldb * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)WS_M, (cuuint32_t)box_rows};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? PCB_OK : PCB_CUDA;
-}
-
 template <int MODE, int KC>
 int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   using C = WsCfg<MODE, KC>;
@@ -478,7 +423,9 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   }
   CUtensorMap tm0, tm1;
   if (make_rows_map(&tm0, a.src0, rows0, a.ldb, KC)) return PCB_CUDA;
-  if (make_rows_map(&tm1, a.src1 ? a.src1 : a.src0, a.src1 ? rows1 : rows0, a.ldb, KC))
+  // child flow: the per-block shift rows R, one row per box
+  if (make_rows_map(&tm1, MODE == MODE_CF ? a.shift : a.src0, MODE == MODE_CF ? rows1 : rows0,
+                    a.ldb, MODE == MODE_CF ? 1 : KC))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
   k_sum_ws<MODE, KC><<<grid, WS_THREADS, C::kBytes, s>>>(a, tm0, tm1);
@@ -510,7 +457,6 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.slab = g.param_slab;
   a.mma = P->mma;
   a.src0 = scratch;
-  a.src1 = nullptr;
   a.shift = bmax;
   a.aux = nullptr;
   a.out = values;
@@ -522,8 +468,8 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
 }
 
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
-                         cudaStream_t s, int B, int ldb, const float* values, const float* flows,
-                         const float* scratch, const float* rmax, float* flow_scratch) {
+                         cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
+                         const float* rmax, float* flow_scratch) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -541,14 +487,13 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.real_ids = g.par_param_ids;
   a.slab = g.par_slab;
   a.mma = P->mma;
-  a.src0 = flows;
-  a.src1 = values;
+  a.src0 = ratio;
   a.shift = rmax;
   a.aux = scratch;
   a.out = flow_scratch;
   switch (L.k_m) {
-    case 16: return launch_ws<MODE_CF, 16>(a, P->num_value_slots, P->num_value_slots, s);
-    case 32: return launch_ws<MODE_CF, 32>(a, P->num_value_slots, P->num_value_slots, s);
+    case 16: return launch_ws<MODE_CF, 16>(a, L.n_sb * L.k_m, L.n_sb, s);
+    case 32: return launch_ws<MODE_CF, 32>(a, L.n_sb * L.k_m, L.n_sb, s);
     default: return PCB_USAGE;
   }
 }
