@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 7;
+constexpr int64_t kVersion = 10;
 
 struct Reader {
   const int64_t* p;
@@ -97,6 +97,10 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->in_blocks.pid_off = r.ref();
   P->in_blocks.pids = r.ref();
   P->in_blocks.max_elems = r.get();
+  P->in_blocks.max_ncat = r.get();
+  P->n_zero = r.get();
+  P->zero_start = r.ref();
+  P->zero_len = r.ref();
   P->prod_rows_written = (int)r.get();
   int64_t n_layers = r.get();
   for (int64_t l = 0; l < n_layers && r.ok; ++l) {
@@ -126,6 +130,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.param_ids = r.ref();
       G.flow_ids = r.ref();
       G.param_slab = r.ref();
+      G.exclusive = (int)r.get();
       TcRows T, Tp;
       T.count = r.get();
       T.row_off = r.ref();
@@ -405,8 +410,9 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
     if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * plan->f_params_size, s) != cudaSuccess)
       return PCB_CUDA;
     if (!B) return PCB_OK;
-    if (cudaMemsetAsync(d_flows, 0, sizeof(float) * plan->num_value_slots * ldb, s) !=
-        cudaSuccess)
+    // only rows that accumulate (several pushes) or receive none need zeros;
+    // single-push rows are stored by their push
+    if (launch_zero_ranges(s, plan->n_zero, plan->zero_start, plan->zero_len, ldb, d_flows))
       return PCB_CUDA;
     // every product row's first accumulation stores (plan flag): no zeroing
     if (plan->num_prod_rows && !plan->prod_rows_written &&

@@ -27,7 +27,7 @@ struct InputChunk {
 // consecutive value slots from slot0 on variable var, each with an exclusive
 // pmf of ncat entries starting at pids[pid_off + i].
 struct InBlocks {
-  int64_t n = 0, max_elems = 0;
+  int64_t n = 0, max_elems = 0, max_ncat = 0;
   const int32_t *var = nullptr, *ncat = nullptr, *slot0 = nullptr, *count = nullptr,
                 *pid_off = nullptr, *pids = nullptr;
 };
@@ -42,6 +42,7 @@ struct FwdGroup {
   int64_t rows, cap;
   const int32_t *sum_ids, *prod_ids, *param_ids, *flow_ids;
   const int32_t* param_slab;  // bf16 MMA-tile offset per (row, col), -1 for padding
+  int exclusive = 0;          // every flow tile of the group has no other writer in the pass
 };
 
 struct BwdGroup {
@@ -117,6 +118,8 @@ struct pcb_plan {
   __nv_bfloat16* mma = nullptr;  // bound by pcb_plan_set_mma
   int64_t scratch_rows = 1;      // all-layer scratch rows (sum of layer windows)
   int prod_rows_written = 0;     // every prod-flow row is stored by its first accumulation
+  int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
+  const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
 
 namespace pcb {
@@ -190,6 +193,8 @@ int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, f
                       float v);
 int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, float* buf,
                 float v);
+int launch_zero_ranges(cudaStream_t s, int64_t n, const int32_t* start, const int32_t* len,
+                       int ldb, float* buf);
 
 // tensor-core kernels (pcb_tc.cu)
 int launch_sum_fwd_tc(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,

@@ -6,6 +6,7 @@
 // streaming (lin, top) merge with dead-tile skipping, log-flow rescaling by a
 // per-sample block maximum, zero flow for impossible nodes; fp32 throughout.
 #include <math.h>
+#include <stdlib.h>
 
 #include "pcb_internal.cuh"
 
@@ -227,6 +228,24 @@ __global__ void k_fill_range(int64_t row0, int64_t n, int B, int ldb, float* __r
     int b = (int)(t - j * B);
     buf[(row0 + j) * ldb + b] = v;
   }
+}
+
+// zero rows [start_r, start_r + len_r) of a [rows x ldb] buffer for every range r
+__global__ void k_zero_ranges(int64_t n, const int32_t* __restrict__ start,
+                              const int32_t* __restrict__ len, int ldb, float* __restrict__ buf) {
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+    float4* p = reinterpret_cast<float4*>(buf + (int64_t)__ldg(start + r) * ldb);
+    const int64_t total = (int64_t)__ldg(len + r) * ldb / 4;
+    for (int64_t q = threadIdx.x; q < total; q += blockDim.x) p[q] = z;
+  }
+}
+
+int launch_zero_ranges(cudaStream_t s, int64_t n, const int32_t* start, const int32_t* len,
+                       int ldb, float* buf) {
+  if (!n) return PCB_OK;
+  k_zero_ranges<<<grid_for(n, 1, 148 * 16), 256, 0, s>>>(n, start, len, ldb, buf);
+  return check_launch();
 }
 
 int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,
@@ -762,7 +781,7 @@ __global__ void k_input_param_flow(int ncat, int B, int ldb, const int32_t* __re
 // Staged input flows: a shared-memory histogram [inputs x categories] of the
 // block's observed flows (smem atomics), plus the per-input missing-sample
 // flow spread over its pmf; the block owns its pmf ranges exclusively, so the
-// result is added to f_params with plain coalesced read-modify-writes.
+// result is stored to f_params (coalesced, no read-modify-write).
 __global__ void __launch_bounds__(IN_THREADS)
     k_input_flow_block(int B, int ldb, const int32_t* __restrict__ bvar,
                        const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
@@ -798,8 +817,8 @@ __global__ void __launch_bounds__(IN_THREADS)
   for (int q = threadIdx.x; q < total; q += IN_THREADS) {
     const int i = q / ncat, c = q - i * ncat;
     const float m = miss[i];
-    const float add = hist[q] + (m != 0.f ? m * __ldg(theta + pid[i] + c) : 0.f);
-    if (add != 0.f) f_params[pid[i] + c] += add;
+    // exclusive pmf range (plan.input_blocks): a store, no read-modify-write
+    f_params[pid[i] + c] = hist[q] + (m != 0.f ? m * __ldg(theta + pid[i] + c) : 0.f);
   }
 }
 
@@ -808,6 +827,7 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              float* f_params) {
   ProfScope prof_(KC_INPUT_FLOW, s);
   const InBlocks& ib = p->in_blocks;
+  // bucketed kernel when the sort arrays and >= 1 flow row fit in shared memory
   if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
     static int attr = 0;

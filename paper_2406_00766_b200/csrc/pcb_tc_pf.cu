@@ -20,7 +20,9 @@
 //   warp 1       MMA issuer (double-buffered TMEM accumulators, 2 x 256 cols);
 //   warps 2-9    converters: the chunk's shifts c_b, then raw -> exponentials
 //                -> packed bf16 planes in the K-major core-matrix layout;
-//   warps 10-13  epilogue: TMEM -> theta (.) cum -> red.add into f_params.
+//   warps 10-13  epilogue: TMEM -> theta (.) cum -> f_params (plain stores when
+//                the group's flow tiles have a single writer and the batch
+//                is not sliced; else vector red.add).
 #include <math.h>
 
 #include "pcb_internal.cuh"
@@ -43,6 +45,7 @@ constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
 
 struct PfArgs {
   int cap, k_m, B, ldb;
+  int store;  // 1: each flow entry has exactly one writer in the pass (plain stores)
   int n_items, mtiles, kslices, cgroups, nchunks;
   int64_t sb_base;
   const int32_t *row_off, *members, *sum_ids, *prod_ids, *param_ids, *flow_ids;
@@ -106,6 +109,14 @@ __device__ __forceinline__ int pf_cols(const PfArgs& a, const PfItem& it, int cp
   return n;
 }
 
+// number of real child columns of the item
+__device__ __forceinline__ int pf_ncols(const PfArgs& a, const PfItem& it, int cpg) {
+  const int32_t* trow = a.param_ids + (int64_t)it.r0 * a.cap;
+  int seen = 0;
+  for (int c = 0; c < a.cap; ++c) seen += __ldg(trow + c) != 0;
+  return max(0, min(cpg, seen - it.cg * cpg));
+}
+
 __device__ __forceinline__ bool pf_active(const PfItem& it) { return it.rows > 0 && it.kc0 < it.kc1; }
 
 // element (row, k) of a 128-byte-swizzled fp32 box with 32-float rows
@@ -123,8 +134,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOS], op_empty[C::kOS];
   __shared__ uint64_t acc_full[2], acc_empty[2];
-  __shared__ float cs[C::kRS][PF_KS];
+  __shared__ __align__(16) float cs[C::kRS][PF_KS];
   __shared__ int cols_p[C::kCPG];
+  __shared__ int cols_w[4][C::kCPG];  // epilogue warps' column lists
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
   uint8_t* ops = smem + C::kRS * C::kRaw;
@@ -189,8 +201,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const PfItem it = pf_item(a, item);
       if (!pf_active(it)) continue;
-      int cbuf[C::kCPG];
-      const int ncol = pf_cols(a, it, C::kCPG, cbuf);
+      const int ncol = pf_ncols(a, it, C::kCPG);
       if (!ncol) continue;
       const uint32_t idesc = idesc_bf16(PF_M, ncol * KN);
       const int as = acc_u & 1;
@@ -229,8 +240,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const PfItem it = pf_item(a, item);
       if (!pf_active(it)) continue;
-      int cbuf[C::kCPG];
-      const int ncol = pf_cols(a, it, C::kCPG, cbuf);
+      const int ncol = pf_ncols(a, it, C::kCPG);
       if (!ncol) continue;
       const int npad = ncol * KN;
       for (int kc = it.kc0; kc < it.kc1; ++kc) {
@@ -252,18 +262,27 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         uint8_t* oAl = oAh + C::kOpA;
         uint8_t* oBh = oAl + C::kOpA;
         uint8_t* oBl = oBh + C::kOpB;
+        // raw boxes are 128-byte swizzled: the 16-byte chunk h of row m sits at
+        // chunk h ^ (m % 8), so 8 consecutive rows read conflict-free float4s
+        const float4* rA4 = reinterpret_cast<const float4*>(rA);
+        const float4* rE4 = reinterpret_cast<const float4*>(rE);
+        const float4* rR4 = reinterpret_cast<const float4*>(rR);
+        const float4* c4 = reinterpret_cast<const float4*>(c_s);
         // A: 128 rows x 4 octets; thread -> (row = q % 128, octet = q / 128)
         for (int q = t; q < PF_M * (PF_KS / 8); q += PF_NCONV * 32) {
           const int m = q & (PF_M - 1), o = q >> 7;
           float v[8];
           if (m < it.rows) {
-            const int blk = m / a.k_m;
+            const int blk = m / a.k_m, sw = m & 7;
+            const float4 x0 = rA4[m * 8 + ((2 * o) ^ sw)], x1 = rA4[m * 8 + ((2 * o + 1) ^ sw)];
+            const float4 R0 = rR4[blk * 8 + 2 * o], R1 = rR4[blk * 8 + 2 * o + 1];
+            const float4 c0 = c4[2 * o], c1 = c4[2 * o + 1];
+            const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            const float Rs[8] = {R0.x, R0.y, R0.z, R0.w, R1.x, R1.y, R1.z, R1.w};
+            const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int k = o * 8 + e;
-              const float c = c_s[k];
-              v[e] = (c == PCB_NEG_INF) ? 0.f : ex2(swz(rA, m, k) + (rR[blk * PF_KS + k] - c));
-            }
+            for (int e = 0; e < 8; ++e)
+              v[e] = (cc[e] == PCB_NEG_INF) ? 0.f : ex2(xs[e] + (Rs[e] - cc[e]));
           } else {
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = 0.f;
@@ -276,14 +295,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         }
         // E: npad rows x 4 octets
         for (int q = t; q < npad * (PF_KS / 8); q += PF_NCONV * 32) {
-          const int n = q % npad, o = q / npad;
+          const int n = q % npad, o = q / npad, sw = n & 7;
+          const float4 x0 = rE4[n * 8 + ((2 * o) ^ sw)], x1 = rE4[n * 8 + ((2 * o + 1) ^ sw)];
+          const float4 c0 = c4[2 * o], c1 = c4[2 * o + 1];
+          const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
           float v[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int k = o * 8 + e;
-            const float c = c_s[k];
-            v[e] = (c == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(swz(rE, n, k), kL2E, c)), 1e37f);
-          }
+          for (int e = 0; e < 8; ++e)
+            v[e] = (cc[e] == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(xs[e], kL2E, cc[e])), 1e37f);
           uint4 hi, lo;
           split_pack8(v, hi, lo);
           const uint32_t off = kmajor_off(n, o * 8, PF_KS);
@@ -304,38 +324,68 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int q4 = warp & 3;
     const int er = q4 * 32 + lane;  // sum row within the tile (TMEM lane)
+    int* cols = cols_w[warp - PF_EPI0];
     int acc_u = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const PfItem it = pf_item(a, item);
       if (!pf_active(it)) continue;
-      int cbuf[C::kCPG];
-      const int ncol = pf_cols(a, it, C::kCPG, cbuf);
+      int ncol = 0;
+      if (lane == 0) ncol = pf_cols(a, it, C::kCPG, cols);
+      ncol = __shfl_sync(0xffffffffu, ncol, 0);
+      __syncwarp();
       if (!ncol) continue;
       const bool live = er < it.rows;
       const int s = it.s_lo + (live ? er / a.k_m : 0);
       const int mm = er % a.k_m;
       const int64_t rowbase = (int64_t)__ldg(a.members + it.m0 + s) * a.cap;
       const int as = acc_u & 1;
+      // theta of the next 16 columns (one row segment: 4 float4) is loaded
+      // before this chunk's TMEM read
+      auto tile_of = [&](int c0) {
+        return (int64_t)__ldg(a.param_ids + rowbase + cols[c0 / KN]) + mm * KN + (c0 % KN);
+      };
+      auto load_th = [&](int64_t tile, float* th) {
+        const float* tp = a.theta + tile;
+        if ((tile & 3) == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(tp + i));
+            th[i] = q.x, th[i + 1] = q.y, th[i + 2] = q.z, th[i + 3] = q.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) th[i] = __ldg(tp + i);
+        }
+      };
+      float th[16], thn[16];
+      if (live) load_th(tile_of(0), thn);
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(as * PF_N) + ((uint32_t)(q4 * 32) << 16);
       for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) th[i] = thn[i];
+        if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
         float v[16];
         tmem_ld16(tbase + c0, v);
         if (!live) continue;
-        const int c = cbuf[c0 / KN];
+        const int c = cols[c0 / KN];
         const int j0 = c0 % KN;
         const int64_t tile = __ldg(a.param_ids + rowbase + c) + mm * KN + j0;
         const int64_t flow = __ldg(a.flow_ids + rowbase + c) + mm * KN + j0;
-        const float* th = a.theta + tile;
         float* dst = a.f_params + flow;
         float w[16];  // zero-theta terms skipped (an overflowed cum must not make inf * 0)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float tv = __ldg(th + i);
-          w[i] = (tv != 0.f) ? tv * v[i] : 0.f;
-        }
-        if (((tile | flow) & 3) == 0) {
+        for (int i = 0; i < 16; ++i) w[i] = (th[i] != 0.f) ? th[i] * v[i] : 0.f;
+        const bool vec = ((tile | flow) & 3) == 0;
+        if (a.store && vec) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+        } else if (a.store) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) dst[i] = w[i];
+        } else if (vec) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
             atomicAdd(reinterpret_cast<float4*>(dst + i), make_float4(w[i], w[i + 1], w[i + 2], w[i + 3]));
@@ -378,6 +428,7 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   int ks = (2 * sm_count() + base - 1) / base;
   a.kslices = max(1, min(ks, a.nchunks / 2));
   a.n_items = base * a.kslices;
+  a.store = a.store && a.kslices == 1;  // batch slices add partial sums
   CUtensorMap tr, tR, te;
   if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, true) ||
       make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, PF_KS, false) ||
@@ -414,6 +465,7 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   a.flow_ids = g.flow_ids;
   a.theta = theta;
   a.f_params = f_params;
+  a.store = g.exclusive;
   switch (L.k_n) {
     case 16: return launch_pf<16>(a, L, ratio, rmax, scratch, s);
     case 32: return launch_pf<32>(a, L, ratio, rmax, scratch, s);

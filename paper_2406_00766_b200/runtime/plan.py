@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 7
+VERSION = 10
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -216,6 +216,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
     for key in ("var", "ncat", "slot0", "count", "pid_off", "pids"):
         ref(blocks[key])
     prog.append(int((blocks["ncat"] * blocks["count"]).max()) if nb else 0)
+    prog.append(int(blocks["ncat"].max()) if nb else 0)
 
     # pushes per value slot over the whole backward pass (root pushes included):
     # a slot with exactly one push takes a plain store instead of an atomic add
@@ -224,7 +225,24 @@ def build_program(compiled, *, tensor_cores: bool = True):
         for p in L.pushes:
             np.add.at(push_count, p.children.ravel(), 1)
     if c.root_children is not None and c.root_row >= 0:
-        np.add.at(push_count, np.asarray(c.root_children, dtype=np.int64), 1)
+        # the root pass adds into these rows: never a single plain store
+        np.add.at(push_count, np.asarray(c.root_children, dtype=np.int64), 2)
+    # flow rows the backward pass must zero first: all but the single-store rows
+    need = push_count != 1
+    if c.num_value_slots:
+        edges = np.flatnonzero(np.diff(np.concatenate([[0], need.astype(np.int8), [0]])))
+        z_start, z_end = edges[0::2], edges[1::2]
+        # pieces of <= 64 rows: one CTA each
+        pieces = [np.arange(a, e, 64) for a, e in zip(z_start.tolist(), z_end.tolist())]
+        if pieces:
+            ps = np.concatenate(pieces)
+            pe = np.minimum(ps + 64, np.repeat(z_end, [p.size for p in pieces]))
+            z_start, z_end = ps, pe
+    else:
+        z_start = z_end = np.zeros(0, np.int64)
+    prog.append(int(z_start.size))
+    ref(z_start)
+    ref(z_end - z_start)
     # the last layer (in backward order: the highest) accumulating each product row
     # writes it instead of adding; every row written => no prod_flows memset
     last_layer = np.full(max(c.num_prod_rows, 1), -1, dtype=np.int64)
@@ -235,6 +253,18 @@ def build_program(compiled, *, tensor_cores: bool = True):
     if c.root_row >= 0:
         covered[c.root_row] = True
     prog.append(1 if bool(covered.all()) else 0)
+
+    # flow tiles written by exactly one (layer, group, row, column) in the pass:
+    # a group whose tiles are all exclusive may store its parameter flows
+    flow_starts = [g.flow_ids[g.param_ids != 0] for L in c.layers for g in L.fwd_groups]
+    if flow_starts:
+        fu, fcnt = np.unique(np.concatenate(flow_starts), return_counts=True)
+    else:
+        fu, fcnt = np.zeros(0, np.int64), np.zeros(0, np.int64)
+
+    def exclusive(g) -> int:
+        f = g.flow_ids[g.param_ids != 0]
+        return int(bool(np.all(fcnt[np.searchsorted(fu, f)] == 1))) if f.size else 1
 
     n_tc_rows = 0
     scratch_off = 0
@@ -261,6 +291,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.param_ids)
             ref(g.flow_ids)
             ref(_slab_of(g.param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
+            prog.append(exclusive(g))
             if use_tc and rows:
                 # forward: enough super-rows to fill the SMs; param flows: full
                 # stacks (their grid also spans column groups)
