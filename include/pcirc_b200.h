@@ -73,6 +73,10 @@ int64_t pcb_plan_scratch_rows(const pcb_plan* plan);
 int pcb_plan_set_mma(pcb_plan* plan, void* d_mma, int64_t elems);
 int pcb_theta_refresh(const pcb_plan* plan, void* stream, const float* d_theta);
 
+/* Bind the plan's own theta table: pcb_em_update on exactly this table also
+ * rewrites the bf16 tensor-core planes (no separate pcb_theta_refresh). */
+int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta);
+
 /* Validate a device batch (xT, [num_vars x ldb]) against the category counts:
  * writes the number of bad entries to *d_bad (device int32).
  * Replaces: pcirc/runtime/engine.py:36-52 (_validate_batch) for device batches. */
@@ -118,7 +122,8 @@ int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int
  *   theta[g] <- (1 - step) * theta[g] + step * (F[g] + k) / sum(F[g] + k)
  * for every group whose total is > 0 (others keep theta).  step = 1 gives the
  * full-batch renormalisation.  d_status (device int32[2]) receives
- * [informative group count, non-finite result count].
+ * [informative group count, non-finite result count].  On the table bound by
+ * pcb_plan_set_theta the tensor-core planes are refreshed in the same pass.
  * Replaces: pcirc/runtime/em.py:58-94 (em_step_full, em_step_mini, apply_theta). */
 int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params,
                   float* d_theta, float pseudocount, float step_size, int32_t* d_status);

@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 10;
+constexpr int64_t kVersion = 11;
 
 struct Reader {
   const int64_t* p;
@@ -190,6 +190,17 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->n_groups = r.get();
   P->group_idx = r.ref();
   P->group_off = r.ref();
+  P->n_em_blk = r.get();
+  P->n_em_tiles = r.get();
+  P->em_km = r.ref();
+  P->em_kn = r.ref();
+  P->em_tile_off = r.ref();
+  P->em_goff = r.ref();
+  P->em_tile_start = r.ref();
+  P->em_tile_slab = r.ref();
+  P->n_em_rest = r.get();
+  P->em_rest = r.ref();
+  P->em_rest_start = r.ref();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -208,6 +219,12 @@ int pcb_plan_num_layers(const pcb_plan* plan) { return plan ? (int)plan->layers.
 int pcb_plan_set_mma(pcb_plan* plan, void* d_mma, int64_t elems) {
   if (!plan || elems < plan->mma_elems) return PCB_USAGE;
   plan->mma = reinterpret_cast<__nv_bfloat16*>(d_mma);
+  return PCB_OK;
+}
+
+int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta) {
+  if (!plan) return PCB_USAGE;
+  plan->theta_bound = d_theta;
   return PCB_OK;
 }
 
@@ -458,7 +475,15 @@ int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, f
   if (!plan || !(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f) return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
   if (cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
-  return launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status);
+  // the plan's own table: the tile-block pass also rewrites the bf16 MMA
+  // planes; tensor-core tiles outside tile blocks get the separate refresh
+  const bool own = d_theta == plan->theta_bound && plan->mma;
+  int st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own);
+  if (st) return st;
+  st = launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status);
+  if (st) return st;
+  if (own && plan->n_em_tiles < plan->n_mma_tiles) return launch_theta_to_mma(plan, s, d_theta);
+  return PCB_OK;
 }
 
 int pcb_axpy_accumulate(void* stream, int64_t n, const float* d_src, float* d_dst) {

@@ -110,6 +110,14 @@ struct pcb_plan {
   // simplex groups
   int64_t n_groups;
   const int32_t *group_idx, *group_off;
+  // EM tile blocks: k_m groups that exactly tile k_m x k_n tensor-core tiles
+  // (updated tile by tile, bf16 planes written in the same pass); the other
+  // groups (em_rest) take the generic per-group pass
+  int64_t n_em_blk = 0, n_em_tiles = 0, n_em_rest = 0;
+  const int32_t *em_km = nullptr, *em_kn = nullptr, *em_tile_off = nullptr, *em_goff = nullptr,
+                *em_tile_start = nullptr, *em_tile_slab = nullptr, *em_rest = nullptr,
+                *em_rest_start = nullptr;  // first theta index of a contiguous rest group, else -1
+  const float* theta_bound = nullptr;  // the plan's own theta (pcb_plan_set_theta)
   int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported); 2: legacy TC
   int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1;
   // bf16 tensor-core copies of theta tiles (plan v4)
@@ -189,6 +197,8 @@ int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* fl
 int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params);
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
               float pseudocount, float step, int32_t* status);
+int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
+                    float pseudocount, float step, int32_t* status, bool planes);
 int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,
                       float v);
 int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, float* buf,

@@ -924,24 +924,29 @@ int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params) {
 
 // ---------------------------------------------------------------- K9 EM
 // One warp per simplex group (em.py:58-94): counts = F + k; groups with a
-// positive total are renormalised and blended with step size; others keep theta.
-__global__ void k_em(int64_t n_groups, const int32_t* __restrict__ gidx,
+// positive total are renormalised and blended with step size; others keep
+// theta.  Runs over the groups outside tensor-core tile blocks (k_em_tiles).
+__global__ void k_em(int64_t n_list, const int32_t* __restrict__ glist,
+                     const int32_t* __restrict__ gstart, const int32_t* __restrict__ gidx,
                      const int32_t* __restrict__ goff, const float* __restrict__ F,
                      float* __restrict__ theta, float kappa, float step, int32_t* status) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int informative = 0, bad = 0;
-  for (int64_t g = warp; g < n_groups; g += nwarps) {
+  for (int64_t gi = warp; gi < n_list; gi += nwarps) {
+    const int64_t g = __ldg(glist + gi);
     const int a = goff[g], z = goff[g + 1];
+    // contiguous groups index theta directly (no index-table reads)
+    const int c0 = __ldg(gstart + gi), shift = c0 - a;
     float tot = 0.f;
-    for (int k = a + lane; k < z; k += 32) tot += F[gidx[k]] + kappa;
+    for (int k = a + lane; k < z; k += 32) tot += F[c0 >= 0 ? k + shift : gidx[k]] + kappa;
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     if (!(tot > 0.f)) continue;
     ++informative;
     const float inv = 1.f / tot;
     for (int k = a + lane; k < z; k += 32) {
-      const int q = gidx[k];
+      const int q = c0 >= 0 ? k + shift : gidx[k];
       const float nv = (F[q] + kappa) * inv;
       const float th = (step >= 1.f) ? nv : ((1.f - step) * theta[q] + step * nv);
       if (!isfinite(th)) ++bad;
@@ -956,10 +961,10 @@ __global__ void k_em(int64_t n_groups, const int32_t* __restrict__ gidx,
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
               float pseudocount, float step, int32_t* status) {
   ProfScope prof_(KC_EM, s);
-  if (!p->n_groups) return PCB_OK;
-  int blocks = grid_for(p->n_groups * 32, 256, 148 * 16);
-  k_em<<<blocks, 256, 0, s>>>(p->n_groups, p->group_idx, p->group_off, f_params, theta,
-                              pseudocount, step, status);
+  if (!p->n_em_rest) return PCB_OK;
+  int blocks = grid_for(p->n_em_rest * 32, 256, 148 * 16);
+  k_em<<<blocks, 256, 0, s>>>(p->n_em_rest, p->em_rest, p->em_rest_start, p->group_idx,
+                              p->group_off, f_params, theta, pseudocount, step, status);
   return check_launch();
 }
 

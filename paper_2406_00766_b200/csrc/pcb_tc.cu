@@ -212,6 +212,145 @@ __global__ void __launch_bounds__(TM_THREADS)
   }
 }
 
+// ------------------------------------------------- EM over tile blocks
+// One CTA per tile block (em.py:58-94 for k_m groups that exactly tile a set
+// of k_m x k_n tensor-core tiles, group i = row i of every tile): pass 1 sums
+// F + k per row over the block's tiles (threads = row x 4-column quads,
+// float4 loads, quad-group shuffles); pass 2 renormalises, blends and stores
+// theta tile by tile and, for the plan's own table, packs the updated tile
+// into its four bf16 MMA planes (k_theta_to_mma layout) from shared memory.
+// 4 consecutive floats: one vector load when 16-byte aligned (tiles after
+// odd-sized input pmfs may not be)
+__device__ __forceinline__ float4 ld4(const float* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) return *reinterpret_cast<const float4*>(p);
+  return make_float4(p[0], p[1], p[2], p[3]);
+}
+
+constexpr int EM_THREADS = 256;
+constexpr int EM_NP = 4;  // row passes per thread (k_m x k_n <= 64 x 64)
+__global__ void __launch_bounds__(EM_THREADS)
+    k_em_tiles(int64_t n_blk, const int32_t* __restrict__ bkm, const int32_t* __restrict__ bkn,
+               const int32_t* __restrict__ toff, const int32_t* __restrict__ tstart,
+               const int32_t* __restrict__ tslab, const float* __restrict__ F,
+               float* __restrict__ theta, __nv_bfloat16* __restrict__ mma, float kappa,
+               float step, int planes, int32_t* status) {
+  __shared__ float tile[TM_MAX * (TM_MAX + 1)];
+  const int tid = threadIdx.x;
+  int informative = 0, bad = 0;
+  for (int64_t b = blockIdx.x; b < n_blk; b += gridDim.x) {
+    const int km = __ldg(bkm + b), kn = __ldg(bkn + b);
+    const int t0 = __ldg(toff + b), t1 = __ldg(toff + b + 1);
+    const int tpr = kn / 4, rp = EM_THREADS / tpr;  // threads per row, rows per pass
+    const int c4 = (tid % tpr) * 4, r_in = tid / tpr;
+    float acc[EM_NP];
+#pragma unroll
+    for (int p = 0; p < EM_NP; ++p) acc[p] = 0.f;
+    for (int t = t0; t < t1; ++t) {
+      const float* f = F + __ldg(tstart + t);
+#pragma unroll
+      for (int p = 0; p < EM_NP; ++p) {
+        const int row = p * rp + r_in;
+        if (row < km) {
+          const float4 v = ld4(f + row * kn + c4);
+          acc[p] += (v.x + kappa) + (v.y + kappa) + (v.z + kappa) + (v.w + kappa);
+        }
+      }
+    }
+    // row totals: reduce over the tpr (power of two) threads of each row
+#pragma unroll
+    for (int p = 0; p < EM_NP; ++p)
+      for (int o = tpr / 2; o > 0; o >>= 1) acc[p] += __shfl_xor_sync(0xffffffffu, acc[p], o);
+    float inv[EM_NP];
+#pragma unroll
+    for (int p = 0; p < EM_NP; ++p) {
+      const int row = p * rp + r_in;
+      const bool live = row < km && acc[p] > 0.f;
+      inv[p] = live ? 1.f / acc[p] : 0.f;
+      if (live && tid % tpr == 0) ++informative;
+    }
+    const int ld = kn + 1;
+    for (int t = t0; t < t1; ++t) {
+      const int64_t ts = __ldg(tstart + t);
+      const float* f = F + ts;
+      float* th = theta + ts;
+#pragma unroll
+      for (int p = 0; p < EM_NP; ++p) {
+        const int row = p * rp + r_in;
+        if (row >= km) continue;
+        const float4 fv = ld4(f + row * kn + c4);
+        float4 o = ld4(th + row * kn + c4);
+        if (inv[p] > 0.f) {
+          const float w = inv[p];
+          const float n[4] = {(fv.x + kappa) * w, (fv.y + kappa) * w, (fv.z + kappa) * w,
+                              (fv.w + kappa) * w};
+          float* op = &o.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            op[e] = (step >= 1.f) ? n[e] : ((1.f - step) * op[e] + step * n[e]);
+            if (!isfinite(op[e])) ++bad;
+          }
+          float* tp = th + row * kn + c4;
+          if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
+            *reinterpret_cast<float4*>(tp) = o;
+          } else {
+            tp[0] = o.x, tp[1] = o.y, tp[2] = o.z, tp[3] = o.w;
+          }
+        }
+        if (planes) {
+          float* d = tile + row * ld + c4;
+          d[0] = o.x, d[1] = o.y, d[2] = o.z, d[3] = o.w;
+        }
+      }
+      if (!planes) continue;
+      __syncthreads();
+      uint8_t* base = reinterpret_cast<uint8_t*>(mma + (int64_t)__ldg(tslab + t));
+      const int sz = km * kn, n8 = sz / 8;
+      for (int q = tid; q < 2 * n8; q += EM_THREADS) {
+        float v[8];
+        uint32_t off;
+        int plane;
+        if (q < n8) {  // sum-major core row (m, j..j+7)
+          const int m = q / (kn / 8), j = (q - m * (kn / 8)) * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = tile[m * ld + j + e];
+          off = (uint32_t)tile_off(m, j, kn) * 2u;
+          plane = 0;
+        } else {       // product-major core row (j, m..m+7)
+          const int r = q - n8;
+          const int j = r / (km / 8), m = (r - j * (km / 8)) * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = tile[(m + e) * ld + j];
+          off = (uint32_t)tile_off(j, m, km) * 2u;
+          plane = 2;
+        }
+        uint4 hi, lo;
+        split_pack8(v, hi, lo);
+        *reinterpret_cast<uint4*>(base + (plane * sz) * 2 + off) = hi;
+        *reinterpret_cast<uint4*>(base + ((plane + 1) * sz) * 2 + off) = lo;
+      }
+      __syncthreads();
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    informative += __shfl_xor_sync(0xffffffffu, informative, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((tid & 31) == 0) {
+    if (informative) atomicAdd(status, informative);
+    if (bad) atomicAdd(status + 1, bad);
+  }
+}
+
+int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
+                    float pseudocount, float step, int32_t* status, bool planes) {
+  ProfScope prof_(KC_EM, s);
+  if (!p->n_em_blk) return PCB_OK;
+  k_em_tiles<<<grid_for(p->n_em_blk, 1, 148 * 8), EM_THREADS, 0, s>>>(
+      p->n_em_blk, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab,
+      f_params, theta, p->mma, pseudocount, step, planes ? 1 : 0, status);
+  return check_launch();
+}
+
 int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta) {
   ProfScope prof_(KC_EM, s);
   if (!p->n_mma_tiles || !p->mma) return PCB_OK;

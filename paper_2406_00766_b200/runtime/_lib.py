@@ -27,6 +27,7 @@ SIGNATURES = {
     "pcb_plan_scratch_rows": (_L, [_P]),
     "pcb_plan_set_mma": (_I, [_P, _P, _L]),
     "pcb_theta_refresh": (_I, [_P, _P, _P]),
+    "pcb_plan_set_theta": (_I, [_P, _P]),
     "pcb_tc_selftest_mn": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "pcb_check_batch": (_I, [_P, _P, _I, _I, _P, _P]),
     "pcb_transpose_batch_i64": (_I, [_P, _P, _I, _I, _P, _P]),

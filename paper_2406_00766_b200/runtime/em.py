@@ -83,8 +83,7 @@ def em_update_(compiled, f_params, *, pseudocount: float, step_size: float, thet
     target = plan.theta if theta is None else theta
     _lib.call("pcb_em_update", plan.handle, _lib.stream_handle(), f_params.data_ptr(),
               target.data_ptr(), float(pseudocount), float(step_size), plan.status.data_ptr())
-    if target is plan.theta:
-        plan.refresh_mma()
+    # on plan.theta the EM pass rewrites the tensor-core planes itself
     if check:
         _status_check(plan, int(compiled.group_off.size - 1))
     return target

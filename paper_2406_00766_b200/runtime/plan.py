@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 10
+VERSION = 11
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -169,6 +169,86 @@ def input_blocks(compiled):
     arrays = {k: np.asarray(v, dtype=np.int64) for k, v in blk.items()}
     arrays["pids"] = np.concatenate(pid_flat) if pid_flat else np.zeros(0, np.int64)
     return arrays, leftovers
+
+
+def group_runs(group_idx, group_off):
+    """Run-length encode the simplex-group index table: maximal runs of
+    consecutive theta indices inside each group.  Returns (per-group run
+    offsets [n_groups + 1], run starts, run lengths)."""
+    gi = np.asarray(group_idx, dtype=np.int64)
+    go = np.asarray(group_off, dtype=np.int64)
+    n = gi.size
+    if n == 0:
+        return np.zeros(go.size, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64)
+    brk = np.ones(n, dtype=bool)
+    brk[1:] = gi[1:] != gi[:-1] + 1
+    brk[go[:-1][go[:-1] < n]] = True          # every group starts a run
+    starts = np.flatnonzero(brk)
+    lens = np.diff(np.concatenate([starts, [n]]))
+    run_off = np.searchsorted(starts, go)       # group start positions are run starts
+    return run_off.astype(np.int64), gi[starts], lens.astype(np.int64)
+
+
+def em_tile_blocks(compiled, t_start, t_slab, t_km, t_kn):
+    """Simplex groups that exactly tile tensor-core parameter tiles.
+
+    A block is k_m groups (the sums of one sum block) whose parameters are the
+    k_m rows of a set of k_m x k_n tiles, row i of every tile belonging to the
+    block's i-th group.  The EM pass runs such blocks tile by tile (coalesced
+    whole-tile traffic) and writes the bf16 MMA planes of the updated tiles in
+    the same pass.  Returns dict(blk_km, blk_kn, blk_tile_off [n+1],
+    blk_groups (flat, k_m per block), tile_start, tile_slab) and the sorted ids
+    of the groups left to the generic per-group pass.
+    """
+    gi = np.asarray(compiled.group_idx, dtype=np.int64)
+    go = np.asarray(compiled.group_off, dtype=np.int64)
+    n_groups = go.size - 1
+    empty = dict(blk_km=np.zeros(0, np.int64), blk_kn=np.zeros(0, np.int64),
+                 blk_tile_off=np.zeros(1, np.int64), blk_groups=np.zeros(0, np.int64),
+                 tile_start=np.zeros(0, np.int64), tile_slab=np.zeros(0, np.int64))
+    if n_groups <= 0 or t_start.size == 0:
+        return empty, np.arange(max(n_groups, 0), dtype=np.int64)
+    run_off, rs, rl = group_runs(gi, go)
+    run_grp = np.repeat(np.arange(n_groups, dtype=np.int64), np.diff(run_off))
+    order = np.argsort(rs, kind="stable")
+    rs_s, rl_s, rg_s = rs[order], rl[order], run_grp[order]
+    n_runs_of = np.diff(run_off)
+    covered = np.zeros(n_groups, dtype=bool)
+    blocks = []  # (km, kn, groups tuple, tile indices)
+    for km, kn in sorted(set(zip(t_km.tolist(), t_kn.tolist()))):
+        sel = np.flatnonzero((t_km == km) & (t_kn == kn))
+        rows = t_start[sel][:, None] + np.arange(km, dtype=np.int64)[None, :] * kn
+        pos = np.searchsorted(rs_s, rows)
+        pos_c = np.minimum(pos, rs_s.size - 1)
+        ok = (rs_s[pos_c] == rows) & (rl_s[pos_c] == kn)
+        good = ok.all(axis=1)
+        if not good.any():
+            continue
+        own = rg_s[pos_c[good]]                    # [tiles x km] owner group per row
+        tiles = sel[good]
+        key, inv = np.unique(own, axis=0, return_inverse=True)
+        inv = inv.ravel()
+        cnt = np.bincount(inv, minlength=key.shape[0])
+        torder = np.argsort(inv, kind="stable")
+        offs = np.concatenate([[0], np.cumsum(cnt)])
+        for b in range(key.shape[0]):
+            grp = key[b]
+            # every group of the block lives exactly in these tiles (and is distinct)
+            if np.unique(grp).size != km or np.any(n_runs_of[grp] != cnt[b]) or covered[grp].any():
+                continue
+            blocks.append((km, kn, grp, tiles[torder[offs[b]:offs[b + 1]]]))
+            covered[grp] = True
+    if not blocks:
+        return empty, np.arange(n_groups, dtype=np.int64)
+    tl = [np.sort(b[3]) for b in blocks]
+    out = dict(
+        blk_km=np.array([b[0] for b in blocks], np.int64),
+        blk_kn=np.array([b[1] for b in blocks], np.int64),
+        blk_tile_off=np.concatenate([[0], np.cumsum([t.size for t in tl])]).astype(np.int64),
+        blk_groups=np.concatenate([b[2] for b in blocks]).astype(np.int64),
+        tile_start=np.concatenate([t_start[t] for t in tl]).astype(np.int64),
+        tile_slab=np.concatenate([t_slab[t] for t in tl]).astype(np.int64))
+    return out, np.flatnonzero(~covered).astype(np.int64)
 
 
 def _slab_of(ids, starts, slab):
@@ -387,8 +467,26 @@ def build_program(compiled, *, tensor_cores: bool = True):
     prog.append(n_groups)
     ref(c.group_idx)
     ref(c.group_off)
+    # EM tile blocks (groups that exactly tile tensor-core tiles) + the rest
+    tb, rest = em_tile_blocks(c, t_start, t_slab, t_km, t_kn)
+    prog.append(int(tb["blk_km"].size))
+    prog.append(int(tb["tile_start"].size))
+    tb["blk_goff"] = np.concatenate([[0], np.cumsum(tb["blk_km"])]).astype(np.int64)
+    for key in ("blk_km", "blk_kn", "blk_tile_off", "blk_goff", "tile_start", "tile_slab"):
+        ref(tb[key])
+    prog.append(int(rest.size))
+    ref(rest)
+    # contiguous rest groups (an input pmf is one run): first theta index, else -1
+    gi = np.asarray(c.group_idx, dtype=np.int64)
+    go = np.asarray(c.group_off, dtype=np.int64)
+    run_off, _, _ = group_runs(gi, go)
+    one = (np.diff(run_off) == 1) & (np.diff(go) > 0)
+    contig = np.full(max(n_groups, 0), -1, dtype=np.int64)
+    contig[one] = gi[np.minimum(go[:-1][one], max(gi.size - 1, 0))]
+    ref(contig[rest] if rest.size else np.zeros(0, np.int64))
     prog.append(MAGIC)
     info = {"blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+            "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
 
@@ -412,6 +510,7 @@ class DevicePlan:
                       self.blob.numel(), _lib.C.byref(handle))
         self.handle = handle
         self.theta = torch.empty(compiled.theta_size, dtype=torch.float32, device=self.device)
+        _lib.call("pcb_plan_set_theta", handle, self.theta.data_ptr())
         # bf16 hi/lo tensor-core copies of theta (derived; refreshed after every update)
         self.mma = torch.zeros(max(info["mma_elems"], 8), dtype=torch.bfloat16, device=self.device)
         _lib.call("pcb_plan_set_mma", handle, self.mma.data_ptr(), info["mma_elems"])
