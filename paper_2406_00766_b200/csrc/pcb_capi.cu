@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 11;
+constexpr int64_t kVersion = 12;
 
 struct Reader {
   const int64_t* p;
@@ -141,6 +141,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       L.fwd.push_back(G);
       L.fwd_tc.push_back(T);
       L.pf_tc.push_back(Tp);
+      if (Tp.count > P->max_tc_rows) P->max_tc_rows = Tp.count;
     }
     int64_t nb = r.get();
     for (int64_t g = 0; g < nb && r.ok; ++g) {
@@ -151,12 +152,17 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.par_ids = r.ref();
       G.par_param_ids = r.ref();
       G.par_slab = r.ref();
-      TcRows T;
+      TcRows T, Tf;
       T.count = r.get();
       T.row_off = r.ref();
       T.members = r.ref();
+      Tf.count = r.get();
+      Tf.row_off = r.ref();
+      Tf.members = r.ref();
       L.bwd.push_back(G);
       L.bwd_tc.push_back(T);
+      L.bwd_tc_full.push_back(Tf);
+      if (Tf.count > P->max_tc_rows) P->max_tc_rows = Tf.count;
     }
     L.prod_slots = r.ref();
     L.prod_rows = r.ref();
@@ -291,6 +297,7 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.bmax = d_work;
   w.rmax = d_work + P->max_pb * (int64_t)ldb;
   w.ratio = w.rmax + P->max_sb * (int64_t)ldb;
+  w.counters = reinterpret_cast<int32_t*>(w.ratio + P->max_sum_rows * (int64_t)ldb);
   return w;
 }
 
@@ -306,7 +313,9 @@ int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int 
     const TcRows& T = L.fwd_tc[g];
     if (P->use_tc && T.count > 0 && tc_supported(L))
       st = (P->use_tc == 1 && ws_supported((int)L.k_n, (int)L.k_m))
-               ? launch_sum_fwd_ws(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values)
+               ? launch_sum_fwd_ws(P, L, L.fwd[g], ws_long_k(L.fwd[g].cap) ? L.pf_tc[g] : T, s,
+                                   B, ldb, scratch, w.bmax, values, w.counters,
+                                   L.fwd.size() == 1)
                : launch_sum_fwd_tc(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values);
     else
       st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, values);
@@ -342,8 +351,10 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     const TcRows& T = L.bwd_tc[g];
     if (tc && T.count > 0)
       st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
-               ? launch_child_flow_ws(P, L, L.bwd[g], T, s, B, ldb, w.ratio, scratch, w.rmax,
-                                      flow_scratch)
+               ? launch_child_flow_ws(P, L, L.bwd[g],
+                                      ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T, s, B, ldb,
+                                      w.ratio, scratch, w.rmax, flow_scratch, w.counters,
+                                      L.bwd.size() == 1)
                : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
                                       w.rmax, flow_scratch);
     else
@@ -393,7 +404,9 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
 
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
-  return (plan->max_pb + plan->max_sb + plan->max_sum_rows) * (int64_t)ldb;
+  // + one split-K arrival counter per (super-row, 128-sample tile)
+  return (plan->max_pb + plan->max_sb + plan->max_sum_rows) * (int64_t)ldb +
+         plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }
 
 int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,

@@ -70,6 +70,7 @@ struct Layer {
   std::vector<TcRows> fwd_tc;   // aligned with fwd (count 0 = no TC plan)
   std::vector<TcRows> pf_tc;    // aligned with fwd: full stacks for the param-flow kernel
   std::vector<TcRows> bwd_tc;   // aligned with bwd
+  std::vector<TcRows> bwd_tc_full;  // aligned with bwd: full stacks (persistent kernels)
   const int32_t *prod_slots, *prod_rows;
   std::vector<Bucket> pushes;
   // derived tables (plan v3)
@@ -86,10 +87,12 @@ struct Layer {
 //   rmax [max_sb x ldb]  per sum block and sample: max lg2(flow) - value*log2(e)
 //   ratio [max_sum_rows x ldb] per sum row of the layer: log2 flow ratio minus
 //                               its block's rmax (k_ratio)
+//   counters [max_tc_rows x ldb/128] split-K arrivals (self-resetting, zeroed at allocation)
 struct Work {
   float* bmax;
   float* rmax;
   float* ratio;
+  int32_t* counters;
 };
 
 }  // namespace pcb
@@ -119,7 +122,7 @@ struct pcb_plan {
                 *em_rest_start = nullptr;  // first theta index of a contiguous rest group, else -1
   const float* theta_bound = nullptr;  // the plan's own theta (pcb_plan_set_theta)
   int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported); 2: legacy TC
-  int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1;
+  int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1, max_tc_rows = 1;
   // bf16 tensor-core copies of theta tiles (plan v4)
   int64_t n_mma_tiles = 0, mma_elems = 0;
   const int32_t *mma_theta = nullptr, *mma_slab = nullptr, *mma_km = nullptr, *mma_kn = nullptr;
@@ -219,12 +222,19 @@ int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
                          float* f_params);
 // warp-specialised persistent variants (pcb_tc_ws.cu), K block 16 / 32
 bool ws_supported(int kc, int nb);
+// long contractions (>= 32 K blocks, e.g. HMM's 4096-wide layers) use full
+// 256-wide stacks and split K across CTAs; short ones keep more, narrower
+// super-rows and no split
+inline bool ws_long_k(int64_t cap) { return cap >= 32; }
+// split_ok: the group owns its layer's output rows, so K may be split
+// across CTAs (partial sums reduced in place, finished by the last arrival)
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values);
+                      float* values, int32_t* counters, bool split_ok);
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
-                         const float* rmax, float* flow_scratch);
+                         const float* rmax, float* flow_scratch, int32_t* counters,
+                         bool split_ok);
 bool pf_ws_supported(const Layer& L);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,

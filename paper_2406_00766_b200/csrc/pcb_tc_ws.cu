@@ -54,6 +54,7 @@ struct WsArgs {
   int nb;         // N of one stacked tile (k_m forward, k_n child flow)
   int B, ldb;
   int n_items, ntiles;
+  int kslices, kper;               // K split: slice ks covers real columns [ks * kper, +kper)
   int64_t sb_base;                 // shift-row base (child flow: first sum-block slot)
   const int32_t* row_off;          // super-row -> members
   const int32_t* members;          // group rows
@@ -66,7 +67,34 @@ struct WsArgs {
   const float* shift;              // bmax (fwd) / rmax R (cf)
   const float* aux;                // - / scratch (cf epilogue: child log values)
   float* out;                      // values (fwd) / flow_scratch (cf)
+  int32_t* counters;               // split-K arrivals per (super-row, tile)
 };
+
+struct WsItem {
+  int sr, tile, ks, b0, m0, S, r0;
+};
+
+// item = tile + ntiles * (slice + kslices * super-row): the tiles and slices of
+// one super-row run side by side (theta tiles shared through L2)
+__device__ __forceinline__ WsItem ws_item(const WsArgs& a, int item) {
+  WsItem it;
+  it.tile = item % a.ntiles;
+  const int q = item / a.ntiles;
+  it.ks = q % a.kslices;
+  it.sr = q / a.kslices;
+  it.b0 = it.tile * WS_M;
+  it.m0 = a.row_off[it.sr];
+  it.S = a.row_off[it.sr + 1] - it.m0;
+  it.r0 = a.members[it.m0];
+  return it;
+}
+
+// the first real column of the item's K slice
+__device__ __forceinline__ int slice_first(const int32_t* __restrict__ real, int cap, int skip) {
+  int c = next_real(real, cap, 0);
+  for (int k = 0; k < skip && c < cap; ++k) c = next_real(real, cap, c + 1);
+  return c;
+}
 
 template <int MODE, int KC>
 struct WsCfg {
@@ -98,6 +126,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   __shared__ uint64_t op_full[C::kOS], op_empty[C::kOS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
   __shared__ float g_s[2][WS_M];
+  __shared__ bool g_last;
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
   uint8_t* ops = smem + C::kRS * C::kRaw;
@@ -138,12 +167,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       if (MODE == MODE_CF) prefetch_tmap(&tm1);
       Ring rr(C::kRS);
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-        const int sr = item / a.ntiles;
-        const int b0 = (item - sr * a.ntiles) * WS_M;
-        const int r0 = a.members[a.row_off[sr]];
-        const int32_t* src = a.src_ids + (int64_t)r0 * a.cap;
-        const int32_t* real = a.real_ids + (int64_t)r0 * a.cap;
-        for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+        const WsItem it = ws_item(a, item);
+        const int b0 = it.b0;
+        const int32_t* src = a.src_ids + (int64_t)it.r0 * a.cap;
+        const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
+        int c = slice_first(real, a.cap, it.ks * a.kper);
+        for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
           const int row0 = __ldg(src + c) - (int)a.sb_base;
           mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
           const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
@@ -161,11 +190,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     // planes, so the S tiles form one N = S * nb operand per plane
     Ring orr(C::kOS);
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-      const int sr = item / a.ntiles;
-      const int m0 = a.row_off[sr];
-      const int S = a.row_off[sr + 1] - m0;
-      const int32_t* real = a.real_ids + (int64_t)a.members[m0] * a.cap;
-      for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+      const WsItem it = ws_item(a, item);
+      const int m0 = it.m0, S = it.S;
+      const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
+      int c = slice_first(real, a.cap, it.ks * a.kper);
+      for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
         const uint32_t of = smem_u32(&op_full[orr.slot()]);
         uint8_t* bdst = ops + orr.slot() * C::kOp + 2 * C::kA;
@@ -186,16 +215,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     int acc_u = 0;
     constexpr uint32_t SBO = (KC / 8) * 128;  // A and B both K-major, no swizzle
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-      const int sr = item / a.ntiles;
-      const int m0 = a.row_off[sr];
-      const int S = a.row_off[sr + 1] - m0;
-      const int32_t* real = a.real_ids + (int64_t)a.members[m0] * a.cap;
+      const WsItem it = ws_item(a, item);
+      const int S = it.S;
+      const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
       const int as = acc_u & 1;
       mbar_wait(smem_u32(&acc_empty[as]), (uint32_t)(((acc_u >> 1) & 1) ^ 1));
       tc_fence_after();
       const uint32_t d0 = tmem + (uint32_t)(as * WS_NMAX);
       bool first = true;
-      for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+      int c = slice_first(real, a.cap, it.ks * a.kper);
+      for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&op_full[orr.slot()]), orr.full_par());
         tc_fence_after();
         if (lane == 0) {
@@ -234,11 +263,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     Ring rr(C::kRS), orr(C::kOS);
     int g_u = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-      const int sr = item / a.ntiles;
-      const int b = (item - sr * a.ntiles) * WS_M + t;
+      const WsItem it = ws_item(a, item);
+      const int b = it.b0 + t;
       const bool live = b < a.B;
-      const int m0 = a.row_off[sr];
-      const int32_t* real = a.real_ids + (int64_t)a.members[m0] * a.cap;
+      const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
       const int gs = g_u & 1;
       mbar_wait(smem_u32(&g_full[gs]), (uint32_t)((g_u >> 1) & 1));
       const float g = g_s[gs][t];
@@ -246,7 +274,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       // forward: g is a natural-log max (folded into one FFMA per element);
       // child flow: g is already in log2 units
       const float gl2 = dead ? 0.f : (MODE == MODE_FWD ? g * kL2E : g);
-      for (int c = next_real(real, a.cap, 0); c < a.cap; c = next_real(real, a.cap, c + 1)) {
+      int c = slice_first(real, a.cap, it.ks * a.kper);
+      for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
         const float* rs = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
         float x[KC];
@@ -301,10 +330,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     const int h = (warp - WS_EPI0) >> 2;
     const int t = q4 * 32 + lane;          // sample within the item
     auto shift_of = [&](int item, int& nk) {
-      const int sr = item / a.ntiles;
-      const int b = (item - sr * a.ntiles) * WS_M + t;
-      const int m0 = a.row_off[sr];
-      const int64_t r0 = a.members[m0];
+      const WsItem it = ws_item(a, item);
+      const int b = it.b0 + t;
+      const int64_t r0 = it.r0;
       const int32_t* src = a.src_ids + r0 * a.cap;
       const int32_t* real = a.real_ids + r0 * a.cap;
       float g = PCB_NEG_INF;
@@ -343,61 +371,99 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
           if (lane == 0) mbar_arrive(smem_u32(&g_full[gs]));
         }
       }
-      const int sr = item / a.ntiles;
-      const int b = (item - sr * a.ntiles) * WS_M + t;
+      const WsItem it = ws_item(a, item);
+      const int b = it.b0 + t;
       const bool live = b < a.B;
-      const int m0 = a.row_off[sr];
-      const int S = a.row_off[sr + 1] - m0;
-      const int N = S * a.nb;
+      const int m0 = it.m0;
+      const int N = it.S * a.nb;
       const int as = acc_u & 1;
       const bool dead = g == PCB_NEG_INF || nk == 0;
       auto out_row = [&](int c0) {  // first output row of the 16 columns at c0
         const int s = c0 / a.nb, j0 = c0 - s * a.nb;  // nb is a multiple of 16
         return (int64_t)__ldg(a.out_ids + __ldg(a.members + m0 + s)) + j0;
       };
-      // child flow: the epilogue also reads the children's log values; the
-      // next chunk's are loaded before this chunk's TMEM load
-      float l[16], ln[16];
-      if (MODE == MODE_CF && live && h * 16 < N) {
-        const float* lp = a.aux + out_row(h * 16) * a.ldb + b;
+      // finished result of 16 columns from their fp32 sums d (TMEM or reduced)
+      auto finish = [&](float* o, const float* d, const float* l) {
+        if (MODE == MODE_FWD) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) ln[i] = lp[(int64_t)i * a.ldb];
-      }
+          for (int i = 0; i < 16; ++i)
+            o[(int64_t)i * a.ldb] = (dead || !(d[i] > 0.f)) ? PCB_NEG_INF : fmaf(lg2(d[i]), kLN2, g);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)  // flow = D * 2^g * exp(l) = 2^(log2 D + fma(l, log2 e, g))
+            o[(int64_t)i * a.ldb] = (dead || !(d[i] > 0.f)) ? 0.f : ex2(lg2(d[i]) + fmaf(l[i], kL2E, g));
+        }
+      };
+      auto load_l = [&](int c0, float* l) {
+        const float* lp = a.aux + out_row(c0) * a.ldb + b;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) l[i] = lp[(int64_t)i * a.ldb];
+      };
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(as * WS_NMAX) + ((uint32_t)(q4 * 32) << 16);
-      for (int c0 = h * 16; c0 < N; c0 += 32) {
-        if (MODE == MODE_CF) {
+      if (a.kslices == 1) {
+        // child flow: the epilogue also reads the children's log values; the
+        // next chunk's are loaded before this chunk's TMEM load
+        float l[16], ln[16];
+        if (MODE == MODE_CF && live && h * 16 < N) load_l(h * 16, ln);
+        for (int c0 = h * 16; c0 < N; c0 += 32) {
+          if (MODE == MODE_CF) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) l[i] = ln[i];
-          if (live && c0 + 32 < N) {
-            const float* lp = a.aux + out_row(c0 + 32) * a.ldb + b;
+            for (int i = 0; i < 16; ++i) l[i] = ln[i];
+            if (live && c0 + 32 < N) load_l(c0 + 32, ln);
+          }
+          float v[16];
+          tmem_ld16(tbase + c0, v);
+          if (!live) continue;
+          if (!nk) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) ln[i] = lp[(int64_t)i * a.ldb];
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          }
+          finish(a.out + out_row(c0) * a.ldb + b, v, l);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
+      } else {
+        // split K: add this slice's partial sums into the (zeroed) output rows;
+        // the last slice to arrive finishes the item from the reduced sums
+        const int nks = min(a.kper, max(0, nk - it.ks * a.kper));
+        for (int c0 = h * 16; c0 < N; c0 += 32) {
+          float v[16];
+          tmem_ld16(tbase + c0, v);
+          if (!live || !nks) continue;
+          float* o = a.out + out_row(c0) * a.ldb + b;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) atomicAdd(o + (int64_t)i * a.ldb, v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
+        __threadfence();
+        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
+        if (warp == WS_EPI0 && lane == 0) {
+          int32_t* cnt = a.counters + it.sr * a.ntiles + it.tile;
+          const int old = atomicAdd(cnt, 1);
+          const bool last = old == a.kslices - 1;
+          if (last) *cnt = 0;  // self-resetting for the next launch
+          g_last = last;
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
+        if (g_last) {
+          __threadfence();
+          for (int c0 = h * 16; c0 < N; c0 += 32) {
+            if (!live) continue;
+            float* o = a.out + out_row(c0) * a.ldb + b;
+            float d[16], l[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d[i] = __ldcg(o + (int64_t)i * a.ldb);
+            if (MODE == MODE_CF) load_l(c0, l);
+            finish(o, d, l);
           }
         }
-        float v[16];
-        tmem_ld16(tbase + c0, v);
-        if (!live) continue;
-        float* o = a.out + out_row(c0) * a.ldb + b;
-        if (MODE == MODE_FWD) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float d = nk ? v[i] : 0.f;
-            o[(int64_t)i * a.ldb] = (dead || !(d > 0.f)) ? PCB_NEG_INF : fmaf(lg2(d), kLN2, g);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float d = nk ? v[i] : 0.f;
-            // flow = D * 2^g * exp(l_child) = 2^(log2 D + fma(l, log2 e, g))
-            o[(int64_t)i * a.ldb] = (dead || !(d > 0.f)) ? 0.f : ex2(lg2(d) + fmaf(l[i], kL2E, g));
-          }
-        }
+        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // g_last reuse
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
       ++acc_u;
       ++g_u;
       g = g_next;
@@ -432,13 +498,28 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   return check_launch();
 }
 
+// K split so a layer with few (super-row, tile) items still covers the SMs:
+// >= 2 K blocks per slice; only when the group owns all output rows it zeroes
+void plan_split(WsArgs& a, int64_t count, bool split_ok) {
+  const int64_t base = count * a.ntiles;
+  int ks = 1;
+  if (split_ok && ws_long_k(a.cap) && base < 2 * sm_count()) {
+    const int64_t want = (2 * sm_count() + base - 1) / base;
+    ks = (int)(want < a.cap / 2 ? want : a.cap / 2);
+  }
+  a.kslices = max(1, ks);
+  a.kper = (a.cap + a.kslices - 1) / a.kslices;
+  a.kslices = (a.cap + a.kper - 1) / a.kper;
+  a.n_items = (int)(base * a.kslices);
+}
+
 }  // namespace
 
 bool ws_supported(int kc, int nb) { return (kc == 16 || kc == 32) && (nb == 16 || nb == 32 || nb == 64); }
 
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values) {
+                      float* values, int32_t* counters, bool split_ok) {
   ProfScope prof_(KC_SUM_FWD_TC, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -460,6 +541,13 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.shift = bmax;
   a.aux = nullptr;
   a.out = values;
+  a.counters = counters;
+  plan_split(a, tc.count, split_ok);
+  // split K reduces partial sums in place: zero the layer's sum rows first
+  if (a.kslices > 1 &&
+      cudaMemsetAsync(values + L.sb_base * (int64_t)ldb, 0,
+                      sizeof(float) * L.n_sb * L.k_m * (int64_t)ldb, s) != cudaSuccess)
+    return PCB_CUDA;
   switch (L.k_n) {
     case 16: return launch_ws<MODE_FWD, 16>(a, L.window, 0, s);
     case 32: return launch_ws<MODE_FWD, 32>(a, L.window, 0, s);
@@ -469,7 +557,8 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
 
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
-                         const float* rmax, float* flow_scratch) {
+                         const float* rmax, float* flow_scratch, int32_t* counters,
+                         bool split_ok) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -491,6 +580,11 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.shift = rmax;
   a.aux = scratch;
   a.out = flow_scratch;
+  a.counters = counters;
+  plan_split(a, tc.count, split_ok);
+  if (a.kslices > 1 &&
+      cudaMemsetAsync(flow_scratch, 0, sizeof(float) * L.window * (int64_t)ldb, s) != cudaSuccess)
+    return PCB_CUDA;
   switch (L.k_m) {
     case 16: return launch_ws<MODE_CF, 16>(a, L.n_sb * L.k_m, L.n_sb, s);
     case 32: return launch_ws<MODE_CF, 32>(a, L.n_sb * L.k_m, L.n_sb, s);

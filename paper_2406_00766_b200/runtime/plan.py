@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 11
+VERSION = 12
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 
@@ -392,13 +392,16 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.par_param_ids)
             ref(_slab_of(g.par_param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
             if use_tc and rows:
-                offs, mem = tc_super_rows(g.par_ids, L.k_n, min_count=SMS)
-                prog.append(offs.size - 1)
-                ref(offs)
-                ref(mem)
-                n_tc_rows += offs.size - 1
+                # per-launch kernels: enough super-rows to fill the SMs; the
+                # persistent kernels: full stacks (they split K instead)
+                for mc in (SMS, 0):
+                    offs, mem = tc_super_rows(g.par_ids, L.k_n, min_count=mc)
+                    prog.append(offs.size - 1)
+                    ref(offs)
+                    ref(mem)
+                    n_tc_rows += offs.size - 1
             else:
-                prog += [0, 0, 0, 0, 0]
+                prog += [0, 0, 0, 0, 0] * 2
         ref(L.prod_slots)
         ref(L.prod_rows)
         prog.append(len(L.pushes))

@@ -37,6 +37,7 @@ def _compare(c, x, tensor_cores=True):
     em_update_(c, bufs.f_params, pseudocount=1e-6, step_size=0.01, plan=plan)
     got = _np(plan.theta)
     plan.theta.copy_(saved)
+    plan.refresh_mma()  # the EM pass rewrote the tensor-core planes of plan.theta
     assert rel_err(got, want) < RTOL
     return bufs
 
@@ -74,6 +75,22 @@ def test_tied_hmm_column_groups_and_replicas():
     assert max(gr.prod_ids.shape[1] for L in c.layers for gr in L.fwd_groups) * 32 > 256
     assert len(c.reductions) > 0
     x = np.random.default_rng(3).integers(0, 30, size=(70, 6))
+    _compare(c, x)
+
+
+@pytest.mark.parametrize("batch", [70, 300])
+def test_hmm_long_k_split(batch):
+    """1024 hidden states: 32 child blocks per sum row, so the persistent
+    forward / child-flow kernels run with 256-wide stacks and split K across
+    CTAs (partial sums reduced in place, finished by the last slice)."""
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    g = S.build_hmm(S.StructureConfig(kind="hmm", seq_len=4, hidden_dim=1024, vocab_size=20,
+                                      seed=2, tied=True))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    assert max(gr.prod_ids.shape[1] for L in c.layers for gr in L.fwd_groups) >= 32
+    x = np.random.default_rng(5).integers(0, 20, size=(batch, 4))
+    x[::9, 1] = -1
     _compare(c, x)
 
 
