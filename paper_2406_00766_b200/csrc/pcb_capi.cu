@@ -297,7 +297,8 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.bmax = d_work;
   w.rmax = d_work + P->max_pb * (int64_t)ldb;
   w.ratio = w.rmax + P->max_sb * (int64_t)ldb;
-  w.counters = reinterpret_cast<int32_t*>(w.ratio + P->max_sum_rows * (int64_t)ldb);
+  w.gshift = w.ratio + P->max_sum_rows * (int64_t)ldb;
+  w.counters = reinterpret_cast<int32_t*>(w.gshift + P->max_tc_rows * (int64_t)ldb);
   return w;
 }
 
@@ -314,7 +315,7 @@ int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int 
     if (P->use_tc && T.count > 0 && tc_supported(L))
       st = (P->use_tc == 1 && ws_supported((int)L.k_n, (int)L.k_m))
                ? launch_sum_fwd_ws(P, L, L.fwd[g], ws_long_k(L.fwd[g].cap) ? L.pf_tc[g] : T, s,
-                                   B, ldb, scratch, w.bmax, values, w.counters,
+                                   B, ldb, scratch, w.bmax, values, w.gshift, w.counters,
                                    L.fwd.size() == 1)
                : launch_sum_fwd_tc(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values);
     else
@@ -353,8 +354,8 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
       st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
                ? launch_child_flow_ws(P, L, L.bwd[g],
                                       ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T, s, B, ldb,
-                                      w.ratio, scratch, w.rmax, flow_scratch, w.counters,
-                                      L.bwd.size() == 1)
+                                      w.ratio, scratch, w.rmax, flow_scratch, w.gshift,
+                                      w.counters, L.bwd.size() == 1)
                : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
                                       w.rmax, flow_scratch);
     else
@@ -405,7 +406,7 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
   // + one split-K arrival counter per (super-row, 128-sample tile)
-  return (plan->max_pb + plan->max_sb + plan->max_sum_rows) * (int64_t)ldb +
+  return (plan->max_pb + plan->max_sb + plan->max_sum_rows + plan->max_tc_rows) * (int64_t)ldb +
          plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }
 

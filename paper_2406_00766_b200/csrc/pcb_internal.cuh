@@ -88,10 +88,12 @@ struct Layer {
 //   ratio [max_sum_rows x ldb] per sum row of the layer: log2 flow ratio minus
 //                               its block's rmax (k_ratio)
 //   counters [max_tc_rows x ldb/128] split-K arrivals (self-resetting, zeroed at allocation)
+//   gshift [max_tc_rows x ldb] per-(super-row, sample) shift of long-K layers
 struct Work {
   float* bmax;
   float* rmax;
   float* ratio;
+  float* gshift;
   int32_t* counters;
 };
 
@@ -230,11 +232,11 @@ inline bool ws_long_k(int64_t cap) { return cap >= 32; }
 // across CTAs (partial sums reduced in place, finished by the last arrival)
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values, int32_t* counters, bool split_ok);
+                      float* values, float* gshift, int32_t* counters, bool split_ok);
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
-                         const float* rmax, float* flow_scratch, int32_t* counters,
-                         bool split_ok);
+                         const float* rmax, float* flow_scratch, float* gshift,
+                         int32_t* counters, bool split_ok);
 bool pf_ws_supported(const Layer& L);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,

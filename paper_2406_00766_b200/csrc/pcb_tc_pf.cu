@@ -38,7 +38,9 @@ namespace {
 
 constexpr int PF_M = 128;          // sums per tile
 constexpr int PF_N = 256;          // child columns per item
-constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzle row)
+constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzled box row)
+constexpr int PF_CH = PF_KS / 4;   // 16-byte chunks per box row
+constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
 constexpr int PF_THREADS = 448;    // 14 warps
 constexpr int PF_CONV0 = 2, PF_NCONV = 8, PF_EPI0 = 10;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
@@ -57,15 +59,16 @@ template <int KN>
 struct PfCfg {
   static constexpr int kA = PF_M * PF_KS * 4;          // raw r rows of the tile
   static constexpr int kE = PF_N * PF_KS * 4;          // raw child rows
-  static constexpr int kR = PF_MAXMEM * PF_KS * 4;     // raw R rows (one per sum block)
-  static constexpr int kRaw = kA + kE + kR;
+  static constexpr int kRP = 128;                      // R row pitch (TMA destinations are 128-B aligned)
+  static constexpr int kR = PF_MAXMEM * kRP;            // raw R rows (one per sum block)
+  static constexpr int kRaw = (kA + kE + kR + 1023) / 1024 * 1024;  // swizzle-atom aligned stages
   static constexpr int kOpA = PF_M * PF_KS * 2;        // one bf16 A plane
   static constexpr int kOpB = PF_N * PF_KS * 2;        // one bf16 B plane
   static constexpr int kOp = 2 * kOpA + 2 * kOpB;
-  static constexpr int kRS = 2, kOS = 2;
+  static constexpr int kRS = (PF_KS == 16) ? 5 : 2, kOS = (PF_KS == 16) ? 3 : 2;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static constexpr int kCPG = PF_N / KN;                // child columns per item
-  static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need 1024-byte alignment");
+  static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need aligned bases");
 };
 
 struct PfItem {
@@ -119,9 +122,11 @@ __device__ __forceinline__ int pf_ncols(const PfArgs& a, const PfItem& it, int c
 
 __device__ __forceinline__ bool pf_active(const PfItem& it) { return it.rows > 0 && it.kc0 < it.kc1; }
 
-// element (row, k) of a 128-byte-swizzled fp32 box with 32-float rows
-__device__ __forceinline__ float swz(const float* box, int row, int k) {
-  return box[row * 32 + ((((k >> 2) ^ (row & 7)) << 2) | (k & 3))];
+// physical 16-byte chunk of logical chunk c of box row `row` under the TMA
+// swizzle (128 B: chunk ^ row % 8; 64 B: chunk ^ (row / 2) % 4): 8
+// consecutive rows read conflict-free float4s
+__device__ __forceinline__ int swz_chunk(int row, int c) {
+  return PF_KS == 32 ? (c ^ (row & 7)) : (c ^ ((row >> 1) & 3));
 }
 
 }  // namespace
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           for (int s = 0; s < it.nmem; ++s) {
             const int row = __ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo + s)) - (int)a.sb_base;
             tma_load_2d(st + s * a.k_m * PF_KS * 4, &tm_r, b0, row, rf);
-            tma_load_2d(st + C::kA + C::kE + s * PF_KS * 4, &tm_R, b0, row / a.k_m, rf);
+            tma_load_2d(st + C::kA + C::kE + s * C::kRP, &tm_R, b0, row / a.k_m, rf);
           }
           for (int ci = 0; ci < ncol; ++ci)
             tma_load_2d(st + C::kA + ci * KN * PF_KS * 4, &tm_e, b0, __ldg(prow + cols_p[ci]), rf);
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         if (t < PF_KS) {  // the chunk's per-sample shift: max of R over the tile's blocks
           float v = PCB_NEG_INF;
           if (b0 + t < a.B)
-            for (int s = 0; s < it.nmem; ++s) v = fmaxf(v, rR[s * PF_KS + t]);
+            for (int s = 0; s < it.nmem; ++s) v = fmaxf(v, rR[s * (C::kRP / 4) + t]);
           c_s[t] = v;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(PF_NCONV * 32) : "memory");
@@ -262,8 +267,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         uint8_t* oAl = oAh + C::kOpA;
         uint8_t* oBh = oAl + C::kOpA;
         uint8_t* oBl = oBh + C::kOpB;
-        // raw boxes are 128-byte swizzled: the 16-byte chunk h of row m sits at
-        // chunk h ^ (m % 8), so 8 consecutive rows read conflict-free float4s
+        // raw boxes are swizzled (swz_chunk)
         const float4* rA4 = reinterpret_cast<const float4*>(rA);
         const float4* rE4 = reinterpret_cast<const float4*>(rE);
         const float4* rR4 = reinterpret_cast<const float4*>(rR);
@@ -273,9 +277,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           const int m = q & (PF_M - 1), o = q >> 7;
           float v[8];
           if (m < it.rows) {
-            const int blk = m / a.k_m, sw = m & 7;
-            const float4 x0 = rA4[m * 8 + ((2 * o) ^ sw)], x1 = rA4[m * 8 + ((2 * o + 1) ^ sw)];
-            const float4 R0 = rR4[blk * 8 + 2 * o], R1 = rR4[blk * 8 + 2 * o + 1];
+            const int blk = m / a.k_m;
+            const float4 x0 = rA4[m * PF_CH + swz_chunk(m, 2 * o)];
+            const float4 x1 = rA4[m * PF_CH + swz_chunk(m, 2 * o + 1)];
+            const float4 R0 = rR4[blk * (C::kRP / 16) + 2 * o];
+            const float4 R1 = rR4[blk * (C::kRP / 16) + 2 * o + 1];
             const float4 c0 = c4[2 * o], c1 = c4[2 * o + 1];
             const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
             const float Rs[8] = {R0.x, R0.y, R0.z, R0.w, R1.x, R1.y, R1.z, R1.w};
@@ -295,8 +301,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         }
         // E: npad rows x 4 octets
         for (int q = t; q < npad * (PF_KS / 8); q += PF_NCONV * 32) {
-          const int n = q % npad, o = q / npad, sw = n & 7;
-          const float4 x0 = rE4[n * 8 + ((2 * o) ^ sw)], x1 = rE4[n * 8 + ((2 * o + 1) ^ sw)];
+          const int n = q % npad, o = q / npad;
+          const float4 x0 = rE4[n * PF_CH + swz_chunk(n, 2 * o)];
+          const float4 x1 = rE4[n * PF_CH + swz_chunk(n, 2 * o + 1)];
           const float4 c0 = c4[2 * o], c1 = c4[2 * o + 1];
           const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
           const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -430,9 +437,9 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   a.n_items = base * a.kslices;
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
   CUtensorMap tr, tR, te;
-  if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, true) ||
-      make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, PF_KS, false) ||
-      make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, true))
+  if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, PF_SWZ) ||
+      make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, PF_KS, 0) ||
+      make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, PF_SWZ))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
   k_param_flow_ws<KN><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te);

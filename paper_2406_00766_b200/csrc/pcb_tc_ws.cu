@@ -68,6 +68,7 @@ struct WsArgs {
   const float* aux;                // - / scratch (cf epilogue: child log values)
   float* out;                      // values (fwd) / flow_scratch (cf)
   int32_t* counters;               // split-K arrivals per (super-row, tile)
+  const float* gshift;             // precomputed per-(super-row, sample) shifts, or null
 };
 
 struct WsItem {
@@ -337,6 +338,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       const int32_t* real = a.real_ids + r0 * a.cap;
       float g = PCB_NEG_INF;
       nk = 0;
+      if (a.gshift) {  // long K: shifts precomputed by k_group_shift
+        for (int c = 0; c < a.cap; ++c) nk += __ldg(real + c) != 0;
+        if (b < a.B) g = __ldg(a.gshift + (int64_t)it.sr * a.ldb + b);
+        return g;
+      }
       for (int c = 0; c < a.cap; ++c) {
         if (__ldg(real + c) == 0) continue;
         ++nk;
@@ -498,6 +504,51 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   return check_launch();
 }
 
+// per-(super-row, sample) shift of a long-K group: max over the super-row's
+// real K blocks of the side maxima (bmax / R).  CTA = super-row x 32
+// samples; its 8 warps split the K blocks (lane = sample), combined in smem.
+__global__ void __launch_bounds__(256)
+    k_group_shift(int cap, int kc, int B, int ldb, int64_t sb_base,
+                  const int32_t* __restrict__ row_off, const int32_t* __restrict__ members,
+                  const int32_t* __restrict__ src_ids, const int32_t* __restrict__ real_ids,
+                  const float* __restrict__ shift, float* __restrict__ gout) {
+  __shared__ float part[8][32];
+  const int sr = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.y * 32 + lane;
+  const int64_t r0 = __ldg(members + __ldg(row_off + sr));
+  const int32_t* src = src_ids + r0 * cap;
+  const int32_t* real = real_ids + r0 * cap;
+  float g = PCB_NEG_INF;
+  if (b < B)
+    for (int c0 = warp; c0 < cap; c0 += 8 * 4) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 8 * u;
+        v[u] = (c < cap && __ldg(real + c) != 0)
+                   ? __ldg(shift + (int64_t)(__ldg(src + c) - sb_base) / kc * ldb + b)
+                   : PCB_NEG_INF;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) g = fmaxf(g, v[u]);
+    }
+  part[warp][lane] = g;
+  __syncthreads();
+  if (warp == 0 && b < B) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) g = fmaxf(g, part[w][lane]);
+    gout[(int64_t)sr * ldb + b] = g;
+  }
+}
+
+int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, cudaStream_t s) {
+  dim3 grid((unsigned)count, (unsigned)((a.B + 31) / 32));
+  k_group_shift<<<grid, 256, 0, s>>>(a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off, a.members,
+                                     a.src_ids, a.real_ids, a.shift, gout);
+  return check_launch();
+}
+
 // K split so a layer with few (super-row, tile) items still covers the SMs:
 // >= 2 K blocks per slice; only when the group owns all output rows it zeroes
 void plan_split(WsArgs& a, int64_t count, bool split_ok) {
@@ -519,7 +570,7 @@ bool ws_supported(int kc, int nb) { return (kc == 16 || kc == 32) && (nb == 16 |
 
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values, int32_t* counters, bool split_ok) {
+                      float* values, float* gshift, int32_t* counters, bool split_ok) {
   ProfScope prof_(KC_SUM_FWD_TC, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -543,6 +594,10 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.out = values;
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
+  if (ws_long_k(a.cap)) {
+    if (launch_group_shift(a, (int)L.k_n, tc.count, gshift, s)) return PCB_CUDA;
+    a.gshift = gshift;
+  }
   // split K reduces partial sums in place: zero the layer's sum rows first
   if (a.kslices > 1 &&
       cudaMemsetAsync(values + L.sb_base * (int64_t)ldb, 0,
@@ -557,8 +612,8 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
 
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
-                         const float* rmax, float* flow_scratch, int32_t* counters,
-                         bool split_ok) {
+                         const float* rmax, float* flow_scratch, float* gshift,
+                         int32_t* counters, bool split_ok) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -582,6 +637,10 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.out = flow_scratch;
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
+  if (ws_long_k(a.cap)) {
+    if (launch_group_shift(a, (int)L.k_m, tc.count, gshift, s)) return PCB_CUDA;
+    a.gshift = gshift;
+  }
   if (a.kslices > 1 &&
       cudaMemsetAsync(flow_scratch, 0, sizeof(float) * L.window * (int64_t)ldb, s) != cudaSuccess)
     return PCB_CUDA;

@@ -57,10 +57,10 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D fp32 map over a node-major buffer [rows x ldb], box [box_rows x box_cols
-// samples]; swizzle128 permutes the 16-byte chunks of each 128-byte box row by
-// (row % 8) so row-parallel shared-memory reads are bank-conflict free
+// samples]; swizzle_bytes (64 / 128) permutes the 16-byte chunks of each box
+// row so row-parallel shared-memory reads are bank-conflict free
 inline int make_rows_map(CUtensorMap* m, const float* base, int64_t rows, int ldb, int box_rows,
-                         int box_cols = 128, bool swizzle128 = false) {
+                         int box_cols = 128, int swizzle_bytes = 0) {
   auto fn = encode_fn();
   if (!fn) return PCB_CUDA;
   const cuuint64_t dims[2] = {(cuuint64_t)ldb, (cuuint64_t)(rows > 0 ? rows : 1)};
@@ -69,7 +69,9 @@ inline int make_rows_map(CUtensorMap* m, const float* base, int64_t rows, int ld
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                        : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? PCB_OK : PCB_CUDA;
 }
