@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 12;
+constexpr int64_t kVersion = 13;
 
 struct Reader {
   const int64_t* p;
@@ -205,6 +205,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->em_tile_start = r.ref();
   P->em_tile_slab = r.ref();
   P->n_em_rest = r.get();
+  P->n_em_small = r.get();
   P->em_rest = r.ref();
   P->em_rest_start = r.ref();
   if (!r.ok || r.get() != kMagic) {

@@ -118,7 +118,7 @@ struct pcb_plan {
   // EM tile blocks: k_m groups that exactly tile k_m x k_n tensor-core tiles
   // (updated tile by tile, bf16 planes written in the same pass); the other
   // groups (em_rest) take the generic per-group pass
-  int64_t n_em_blk = 0, n_em_tiles = 0, n_em_rest = 0;
+  int64_t n_em_blk = 0, n_em_tiles = 0, n_em_rest = 0, n_em_small = 0;  // rest: small first
   const int32_t *em_km = nullptr, *em_kn = nullptr, *em_tile_off = nullptr, *em_goff = nullptr,
                 *em_tile_start = nullptr, *em_tile_slab = nullptr, *em_rest = nullptr,
                 *em_rest_start = nullptr;  // first theta index of a contiguous rest group, else -1

@@ -746,36 +746,30 @@ int launch_prod_accum_push_buckets(const Layer& L, cudaStream_t s, int B, int ld
 // ---------------------------------------------------------------- K7
 // Input parameter flows (engine.py:168-183): observed -> f[pmf + x] += flow;
 // missing -> spread sum(flow) * theta over the pmf.  One CTA per input node.
-__global__ void k_input_param_flow(int ncat, int B, int ldb, const int32_t* __restrict__ slots,
+__global__ void k_input_param_flow(int64_t n, int ncat, int B, int ldb,
+                                   const int32_t* __restrict__ slots,
                                    const int32_t* __restrict__ vars, const int32_t* __restrict__ pids,
                                    const int32_t* __restrict__ xT, const float* __restrict__ theta,
                                    const float* __restrict__ flows, float* __restrict__ f_params) {
-  __shared__ float red[32];
-  const int i = blockIdx.x;
-  const int slot = slots[i], var = vars[i], pid = pids[i];
-  float miss = 0.f;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    const float f = flows[(int64_t)slot * ldb + b];
-    const int x = xT[(int64_t)var * ldb + b];
-    if (x >= 0) {
-      if (f != 0.f) atomicAdd(f_params + pid + x, f);
-    } else {
-      miss += f;
+  // one warp per input node: lanes run along the batch (coalesced flows / x)
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const int64_t slot = __ldg(slots + i), var = __ldg(vars + i), pid = __ldg(pids + i);
+    float miss = 0.f;
+    for (int b = lane; b < B; b += 32) {
+      const float f = flows[slot * ldb + b];
+      const int x = __ldg(xT + var * ldb + b);
+      if (x >= 0) {
+        if (f != 0.f) atomicAdd(f_params + pid + x, f);
+      } else {
+        miss += f;
+      }
     }
+    for (int o = 16; o > 0; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
+    if (miss != 0.f)
+      for (int q = lane; q < ncat; q += 32) atomicAdd(f_params + pid + q, miss * __ldg(theta + pid + q));
   }
-  for (int o = 16; o > 0; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = miss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const float tot = red[0];
-  if (tot != 0.f)
-    for (int q = threadIdx.x; q < ncat; q += blockDim.x)
-      atomicAdd(f_params + pid + q, tot * __ldg(theta + pid + q));
 }
 
 // Staged input flows: a shared-memory histogram [inputs x categories] of the
@@ -844,9 +838,9 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
   }
   for (auto& c : p->inputs) {
     if (!c.n) continue;
-    int threads = B >= 256 ? 256 : (B >= 128 ? 128 : 64);
-    k_input_param_flow<<<(unsigned)c.n, threads, 0, s>>>((int)c.ncat, B, ldb, c.slots, c.vars,
-                                                        c.pids, xT, theta, flows, f_params);
+    k_input_param_flow<<<grid_for(c.n * 32, 256), 256, 0, s>>>(c.n, (int)c.ncat, B, ldb, c.slots,
+                                                               c.vars, c.pids, xT, theta, flows,
+                                                               f_params);
     if (check_launch()) return PCB_CUDA;
   }
   return PCB_OK;
@@ -958,14 +952,65 @@ __global__ void k_em(int64_t n_list, const int32_t* __restrict__ glist,
   if (lane == 0 && bad) atomicAdd(status + 1, bad);
 }
 
+// Big groups (>= EM_BIG entries): one CTA per group, block-reduced total.
+__global__ void __launch_bounds__(256)
+    k_em_big(int64_t n_list, const int32_t* __restrict__ glist,
+             const int32_t* __restrict__ gstart, const int32_t* __restrict__ gidx,
+             const int32_t* __restrict__ goff, const float* __restrict__ F,
+             float* __restrict__ theta, float kappa, float step, int32_t* status) {
+  __shared__ float red[8];
+  __shared__ float tot_s;
+  int informative = 0, bad = 0;
+  for (int64_t gi = blockIdx.x; gi < n_list; gi += gridDim.x) {
+    const int64_t g = __ldg(glist + gi);
+    const int a = goff[g], z = goff[g + 1];
+    const int c0 = __ldg(gstart + gi), shift = c0 - a;
+    float tot = 0.f;
+    for (int k = a + threadIdx.x; k < z; k += 256) tot += F[c0 >= 0 ? k + shift : gidx[k]] + kappa;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = tot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      tot_s = t;
+    }
+    __syncthreads();
+    tot = tot_s;
+    __syncthreads();  // red / tot_s are reused by the next group
+    if (!(tot > 0.f)) continue;
+    if (threadIdx.x == 0) ++informative;
+    const float inv = 1.f / tot;
+    for (int k = a + threadIdx.x; k < z; k += 256) {
+      const int q = c0 >= 0 ? k + shift : gidx[k];
+      const float nv = (F[q] + kappa) * inv;
+      const float th = (step >= 1.f) ? nv : ((1.f - step) * theta[q] + step * nv);
+      if (!isfinite(th)) ++bad;
+      theta[q] = th;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if (threadIdx.x == 0 && informative) atomicAdd(status, informative);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(status + 1, bad);
+}
+
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
               float pseudocount, float step, int32_t* status) {
   ProfScope prof_(KC_EM, s);
-  if (!p->n_em_rest) return PCB_OK;
-  int blocks = grid_for(p->n_em_rest * 32, 256, 148 * 16);
-  k_em<<<blocks, 256, 0, s>>>(p->n_em_rest, p->em_rest, p->em_rest_start, p->group_idx,
-                              p->group_off, f_params, theta, pseudocount, step, status);
-  return check_launch();
+  const int64_t ns = p->n_em_small, nb = p->n_em_rest - p->n_em_small;
+  if (ns) {
+    int blocks = grid_for(ns * 32, 256, 148 * 16);
+    k_em<<<blocks, 256, 0, s>>>(ns, p->em_rest, p->em_rest_start, p->group_idx, p->group_off,
+                                f_params, theta, pseudocount, step, status);
+    if (check_launch()) return PCB_CUDA;
+  }
+  if (nb) {
+    k_em_big<<<grid_for(nb, 1, 148 * 8), 256, 0, s>>>(nb, p->em_rest + ns, p->em_rest_start + ns,
+                                                      p->group_idx, p->group_off, f_params,
+                                                      theta, pseudocount, step, status);
+    if (check_launch()) return PCB_CUDA;
+  }
+  return PCB_OK;
 }
 
 }  // namespace pcb

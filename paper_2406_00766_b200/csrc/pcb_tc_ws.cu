@@ -343,10 +343,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         if (b < a.B) g = __ldg(a.gshift + (int64_t)it.sr * a.ldb + b);
         return g;
       }
-      for (int c = 0; c < a.cap; ++c) {
-        if (__ldg(real + c) == 0) continue;
-        ++nk;
-        if (b < a.B) g = fmaxf(g, a.shift[(int64_t)(__ldg(src + c) - a.sb_base) / KC * a.ldb + b]);
+      // 8 K blocks per round: their ids, then their side maxima, in flight together
+      for (int c0 = 0; c0 < a.cap; c0 += 8) {
+        int sc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          sc[u] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
+        }
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          nk += sc[u] >= 0;
+          v[u] = (sc[u] >= 0 && b < a.B)
+                     ? __ldg(a.shift + (int64_t)(sc[u] - a.sb_base) / KC * a.ldb + b)
+                     : PCB_NEG_INF;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g = fmaxf(g, v[u]);
       }
       return g;
     };
@@ -551,15 +565,23 @@ int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, cuda
 
 // K split so a layer with few (super-row, tile) items still covers the SMs:
 // >= 2 K blocks per slice; only when the group owns all output rows it zeroes
+// The slice count minimises a wave model: waves(items) x (K blocks per item +
+// per-item pipeline fill / epilogue overhead, ~3 K blocks), with >= 2 blocks
+// per slice.
 void plan_split(WsArgs& a, int64_t count, bool split_ok) {
   const int64_t base = count * a.ntiles;
-  int ks = 1;
-  if (split_ok && ws_long_k(a.cap) && base < 2 * sm_count()) {
-    const int64_t want = (2 * sm_count() + base - 1) / base;
-    ks = (int)(want < a.cap / 2 ? want : a.cap / 2);
+  const int64_t sms = sm_count();
+  int best = 1;
+  if (split_ok && ws_long_k(a.cap)) {
+    int64_t best_cost = -1;
+    for (int ks = 1; ks <= a.cap / 2; ++ks) {
+      const int64_t per = (a.cap + ks - 1) / ks;
+      const int64_t waves = (base * ks + sms - 1) / sms;
+      const int64_t cost = waves * (per + 3);
+      if (best_cost < 0 || cost < best_cost) best_cost = cost, best = ks;
+    }
   }
-  a.kslices = max(1, ks);
-  a.kper = (a.cap + a.kslices - 1) / a.kslices;
+  a.kper = (a.cap + best - 1) / best;
   a.kslices = (a.cap + a.kper - 1) / a.kper;
   a.n_items = (int)(base * a.kslices);
 }

@@ -22,9 +22,10 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 12
+VERSION = 13
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
+EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
 
 
 class _Blob:
@@ -477,11 +478,16 @@ def build_program(compiled, *, tensor_cores: bool = True):
     tb["blk_goff"] = np.concatenate([[0], np.cumsum(tb["blk_km"])]).astype(np.int64)
     for key in ("blk_km", "blk_kn", "blk_tile_off", "blk_goff", "tile_start", "tile_slab"):
         ref(tb[key])
-    prog.append(int(rest.size))
-    ref(rest)
-    # contiguous rest groups (an input pmf is one run): first theta index, else -1
+    # remaining groups: small ones (one warp each) first, then big ones (one
+    # CTA each, >= EM_BIG entries, e.g. HMM emission pmfs over the vocabulary)
     gi = np.asarray(c.group_idx, dtype=np.int64)
     go = np.asarray(c.group_off, dtype=np.int64)
+    gsize = np.diff(go)[rest] if rest.size else np.zeros(0, np.int64)
+    rest = np.concatenate([rest[gsize < EM_BIG], rest[gsize >= EM_BIG]]).astype(np.int64)
+    prog.append(int(rest.size))
+    prog.append(int((gsize < EM_BIG).sum()))
+    ref(rest)
+    # contiguous rest groups (an input pmf is one run): first theta index, else -1
     run_off, _, _ = group_runs(gi, go)
     one = (np.diff(run_off) == 1) & (np.diff(go) > 0)
     contig = np.full(max(n_groups, 0), -1, dtype=np.int64)
