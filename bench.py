@@ -202,7 +202,8 @@ def run_reference(args, w):
     if rank != 0:
         return
     c = build_circuit(w)
-    Bc = cpu_sample_size(w)
+    # a quarter of the baseline sample per step keeps K + W steps within minutes
+    Bc = max(1, cpu_sample_size(w) // 4)
     for _ in range(args.warmup):
         cpu_step_time(c, w, Bc)
     tot = 0.0
@@ -231,9 +232,7 @@ def run_ours(args, w):
     import torch
     import torch.distributed as dist
     from paper_2406_00766_b200.runtime import _lib
-    from paper_2406_00766_b200.runtime.buffers import allocate_buffers
-    from paper_2406_00766_b200.runtime.em import em_update_
-    from paper_2406_00766_b200.runtime.plan import device_plan
+    from paper_2406_00766_b200.runtime.step import TrainStep
     from paper_2406_00766_b200.train import allreduce_accumulators
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -248,34 +247,23 @@ def run_ours(args, w):
     log(f"[bench] compiled {args.workload}: {c.num_edges} edges, theta {c.theta_size} "
         f"in {time.time() - t0:.1f}s")
     B = w["batch"]
-    plan = device_plan(c, dev)
-    bufs = allocate_buffers(c, B, dev, plan=plan)
     n_pool = 4
     host_batches = synthetic_batches(c, w, B, n_pool, seed=rank)
     dev_batches = [torch.from_numpy(h).to(dev) for h in host_batches]
     pinned = [torch.from_numpy(h).pin_memory() for h in host_batches]
-    stage = torch.empty((B, c.num_vars), dtype=torch.int32, device=dev)
     theta_size = c.theta_size
     ll_acc = torch.zeros((), dtype=torch.float64, device=dev)
     ll_host = torch.zeros((), dtype=torch.float64).pin_memory()
-
-    def step(xdev, e2e=False):
-        stream = _lib.stream_handle()  # the capture stream while a CUDA graph records
-        _lib.call("pcb_transpose_batch_i32", plan.handle, stream, B, bufs.ldb, xdev.data_ptr(),
-                  bufs.xT.data_ptr())
-        _lib.call("pcb_forward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
-                  plan.theta.data_ptr(), bufs.values_full.data_ptr(),
-                  bufs.scratch_full.data_ptr(), bufs.lroot.data_ptr(), bufs.work.data_ptr())
-        _lib.call("pcb_backward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
-                  plan.theta.data_ptr(), bufs.values_full.data_ptr(), bufs.flows_full.data_ptr(),
-                  bufs.scratch_full.data_ptr(), bufs.flow_scratch_full.data_ptr(),
-                  bufs.prod_flows_full.data_ptr(), bufs.f_params.data_ptr(),
-                  bufs.work.data_ptr())
-        step_ll = bufs.lroot.double().sum()
-        allreduce_accumulators(bufs.f_params, step_ll, theta_size)
-        em_update_(c, bufs.f_params, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, check=False,
-                   plan=plan)
-        return step_ll
+    # the training step as a CUDA graph on one GPU (the batch is copied into a
+    # static input buffer, every kernel replays without host launches); eager
+    # launches with the NCCL all-reduce on N > 1
+    graphed = world == 1 and not args.no_graph
+    ts = TrainStep(c, B, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, device=dev,
+                   graph=graphed,
+                   allreduce=None if world == 1 else
+                   (lambda fp, ll: allreduce_accumulators(fp, ll, theta_size)))
+    plan = ts.plan
+    run = ts.run
 
     def barrier():
         if world > 1:
@@ -284,34 +272,8 @@ def run_ours(args, w):
 
     # warm-up (also builds every lazily created kernel attribute)
     for i in range(args.warmup):
-        step(dev_batches[i % n_pool])
+        run(dev_batches[i % n_pool])
     barrier()
-
-    # one step as a CUDA graph (single GPU): the batch is copied into a static
-    # input buffer, then every kernel of the step replays without host launches
-    run = step
-    graphed = world == 1 and not args.no_graph
-    if graphed:
-        x_static = torch.empty_like(dev_batches[0])
-        x_static.copy_(dev_batches[0])
-        graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):
-            step(x_static)
-            torch.cuda.synchronize()
-            cap0 = _lib.load().pcb_launch_count()
-            with torch.cuda.graph(graph, stream=side):
-                ll_static = step(x_static)
-            graph_launches = _lib.load().pcb_launch_count() - cap0
-        torch.cuda.current_stream(dev).wait_stream(side)
-        barrier()
-
-        def run(xdev, e2e=False):
-            if xdev is not x_static:
-                x_static.copy_(xdev, non_blocking=True)
-            graph.replay()
-            return ll_static
 
     # ---- device-resident timed region
     launches0 = _lib.load().pcb_launch_count()
@@ -325,7 +287,7 @@ def run_ours(args, w):
         barrier()
     launches = _lib.load().pcb_launch_count() - launches0
     if graphed:  # replays launch the captured kernels without host calls
-        launches = graph_launches * args.steps
+        launches = ts.launches_per_step * args.steps
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -339,9 +301,8 @@ def run_ours(args, w):
     barrier()
     ev2.record()
     for i in range(args.steps):
-        dst = x_static if graphed else stage
-        dst.copy_(pinned[i % n_pool], non_blocking=True)
-        sl = run(dst)
+        ts.x.copy_(pinned[i % n_pool], non_blocking=True)
+        sl = run(ts.x)
         ll_host.copy_(sl, non_blocking=True)
     ev3.record()
     barrier()
@@ -356,8 +317,8 @@ def run_ours(args, w):
     prof_steps = max(1, min(3, args.steps))
     _lib.profile_enable(True)
     _lib.profile_read()
-    for i in range(prof_steps):
-        step(dev_batches[i % n_pool])
+    for i in range(prof_steps):  # eager: the class timers are host-side event pairs
+        ts._eager(dev_batches[i % n_pool])
     torch.cuda.synchronize()
     prof = _lib.profile_read()
     _lib.profile_enable(False)

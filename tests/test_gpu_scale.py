@@ -150,3 +150,28 @@ def test_flow_conservation_and_simplex_at_scale():
     th = _np(plan.theta)
     sums = np.add.reduceat(th[c.group_idx], c.group_off[:-1])
     np.testing.assert_allclose(sums, 1.0, atol=1e-4)
+
+
+def test_ratspn_repetitions():
+    """RAT-SPN with repetitions (BASELINE configs[4] shape family): mostly
+    demoted K = 1 layers (SIMT paths) under a wide root mixture."""
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    g = S.build_ratspn(S.StructureConfig(kind="ratspn", num_vars=16, depth=3, hidden_dim=4,
+                                         num_categories=8, num_repetitions=6, seed=3))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    x = np.random.default_rng(6).integers(0, 8, size=(200, 16))
+    x[np.random.default_rng(7).random(x.shape) < 0.15] = -1
+    _compare(c, x)
+
+
+def test_pd_small():
+    """Poon-Domingos region decomposition (configs[3] family, all-pairs cuts)."""
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    g = S.build_pd(S.StructureConfig(kind="pd", shape=(3, 4), hidden_dim=3, num_categories=5,
+                                     seed=4))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    x = np.random.default_rng(8).integers(0, 5, size=(150, 12))
+    x[::11, 2] = -1
+    _compare(c, x)
