@@ -816,13 +816,107 @@ __global__ void __launch_bounds__(IN_THREADS)
   }
 }
 
+// Staged input flows without floating-point atomics (shared-memory float
+// atomics are CAS loops on sm_100): the block's samples are counting-sorted
+// by category once (native int atomics; missing = bucket ncat), then each warp
+// takes input rows: it stages the row's flows in its shared-memory slot
+// (coalesced float4) and every lane sums the sorted segments of its
+// categories, adding the missing-flow spread, with one coalesced store per
+// pmf entry (the block owns its pmf ranges exclusively).
+constexpr int IS_THREADS = 256, IS_WARPS = IS_THREADS / 32;
+__global__ void __launch_bounds__(IS_THREADS)
+    k_input_flow_sorted(int B, int ldb, const int32_t* __restrict__ bvar,
+                        const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
+                        const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
+                        const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
+                        const float* __restrict__ theta, const float* __restrict__ flows,
+                        float* __restrict__ f_params) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  const int blk = blockIdx.x;
+  const int ncat = __ldg(bncat + blk), cnt = __ldg(bcount + blk), var = __ldg(bvar + blk);
+  const int64_t slot0 = __ldg(bslot0 + blk);
+  const int32_t* pid = pids + __ldg(bpoff + blk);
+  const int nb = ncat + 1;                      // buckets incl. missing
+  float* rowbuf = reinterpret_cast<float*>(sm_raw);              // [IS_WARPS][ldb]
+  int* start = reinterpret_cast<int*>(rowbuf + IS_WARPS * ldb);  // [nb + 1]
+  int* fill = start + nb + 1;                   // [nb]
+  int* order = fill + nb;                       // [B]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = tid; c < nb; c += IS_THREADS) fill[c] = 0;
+  __syncthreads();
+  const int32_t* xrow = xT + (int64_t)var * ldb;
+  for (int b = tid; b < B; b += IS_THREADS) {
+    const int x = __ldg(xrow + b);
+    atomicAdd(fill + (x < 0 ? ncat : x), 1);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the bucket sizes
+    int run = 0;
+    for (int c0 = 0; c0 < nb; c0 += 32) {
+      const int c = c0 + lane;
+      const int v = c < nb ? fill[c] : 0;
+      int inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (c < nb) start[c] = run + inc - v;
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) start[nb] = run;
+  }
+  __syncthreads();
+  for (int c = tid; c < nb; c += IS_THREADS) fill[c] = 0;
+  __syncthreads();
+  for (int b = tid; b < B; b += IS_THREADS) {
+    const int x = __ldg(xrow + b);
+    const int k = x < 0 ? ncat : x;
+    order[start[k] + atomicAdd(fill + k, 1)] = b;
+  }
+  __syncthreads();
+  float* row = rowbuf + warp * ldb;
+  const int m0 = start[ncat], m1 = start[nb];
+  for (int i = warp; i < cnt; i += IS_WARPS) {
+    const float4* src = reinterpret_cast<const float4*>(flows + (slot0 + i) * ldb);
+    for (int q = lane; q < ldb / 4; q += 32) reinterpret_cast<float4*>(row)[q] = src[q];
+    __syncwarp();
+    float miss = 0.f;
+    for (int p = m0 + lane; p < m1; p += 32) miss += row[order[p]];
+    for (int o = 16; o > 0; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
+    const int64_t base = __ldg(pid + i);
+    for (int c = lane; c < ncat; c += 32) {
+      float h = 0.f;
+      const int p1 = start[c + 1];
+      for (int p = start[c]; p < p1; ++p) h += row[order[p]];
+      f_params[base + c] = h + (miss != 0.f ? miss * __ldg(theta + base + c) : 0.f);
+    }
+    __syncwarp();
+  }
+}
+
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
                              float* f_params) {
   ProfScope prof_(KC_INPUT_FLOW, s);
   const InBlocks& ib = p->in_blocks;
-  // bucketed kernel when the sort arrays and >= 1 flow row fit in shared memory
-  if (ib.n) {
+  // sorted (atomic-free) kernel when its shared-memory slots fit, else the
+  // shared-memory histogram
+  const int64_t sorted_bytes = ((int64_t)IS_WARPS * ldb + 2 * (ib.max_ncat + 1) + 1 + B) * 4;
+  static const bool hist_only = getenv("PCB_INFLOW_HIST") != nullptr;
+  if (ib.n && !hist_only && sorted_bytes <= 160 * 1024) {
+    static int attr_s = 0;
+    if (sorted_bytes > attr_s) {
+      if (cudaFuncSetAttribute(k_input_flow_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sorted_bytes) != cudaSuccess)
+        return PCB_CUDA;
+      attr_s = (int)sorted_bytes;
+    }
+    k_input_flow_sorted<<<(unsigned)ib.n, IS_THREADS, (size_t)sorted_bytes, s>>>(
+        B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
+        f_params);
+    if (check_launch()) return PCB_CUDA;
+  } else if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
     static int attr = 0;
     if (bytes > attr) {
