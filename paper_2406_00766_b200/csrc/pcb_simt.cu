@@ -684,35 +684,53 @@ __global__ void __launch_bounds__(RW * 32)
                 const int32_t* __restrict__ rows, const int32_t* __restrict__ flag,
                 const int32_t* __restrict__ poff, const int32_t* __restrict__ pch,
                 const float* __restrict__ fs, float* __restrict__ pf, float* __restrict__ flows) {
-  const int64_t j = (int64_t)blockIdx.x * RW + (threadIdx.x >> 5);
+  // each warp takes PU consecutive product rows; their index loads, then
+  // their flow loads, are issued together before any store
+  constexpr int PU = 4;
+  const int64_t j0 = ((int64_t)blockIdx.x * RW + (threadIdx.x >> 5)) * PU;
   const int b = blockIdx.y * SLAB + (threadIdx.x & 31) * VB;
-  if (j >= n || b >= B) return;
-  const int fl = __ldg(flag + j);
-  const int64_t ro = (int64_t)__ldg(rows + j) * ldb + b;
-  float4 p = *reinterpret_cast<const float4*>(fs + (int64_t)__ldg(slots + j) * ldb + b);
-  if (!(fl & 2)) {
-    const float4 o = *reinterpret_cast<const float4*>(pf + ro);
-    p.x += o.x;
-    p.y += o.y;
-    p.z += o.z;
-    p.w += o.w;
-  }
-  *reinterpret_cast<float4*>(pf + ro) = p;
-  if (!(fl & 1)) return;
-  const bool full = b + VB <= B;
-  const int q1 = __ldg(poff + j + 1);
-  for (int q = __ldg(poff + j); q < q1; ++q) {
-    const int code = __ldg(pch + q);
-    float* dst = flows + (int64_t)(code >> 1) * ldb + b;
-    if (code & 1) {
-      *reinterpret_cast<float4*>(dst) = p;
-    } else if (full) {
-      atomicAdd(reinterpret_cast<float4*>(dst), p);
-    } else {
-      const float pv[4] = {p.x, p.y, p.z, p.w};
+  if (j0 >= n || b >= B) return;
+  int fl[PU], rw[PU], sl[PU];
 #pragma unroll
-      for (int e = 0; e < VB; ++e)
-        if (b + e < B) atomicAdd(dst + e, pv[e]);
+  for (int u = 0; u < PU; ++u) {
+    const bool ok = j0 + u < n;
+    fl[u] = ok ? __ldg(flag + j0 + u) : 0;
+    rw[u] = ok ? __ldg(rows + j0 + u) : 0;
+    sl[u] = ok ? __ldg(slots + j0 + u) : -1;
+  }
+  float4 p[PU];
+#pragma unroll
+  for (int u = 0; u < PU; ++u) {
+    p[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sl[u] >= 0) p[u] = *reinterpret_cast<const float4*>(fs + (int64_t)sl[u] * ldb + b);
+    if (sl[u] >= 0 && !(fl[u] & 2)) {
+      const float4 o = *reinterpret_cast<const float4*>(pf + (int64_t)rw[u] * ldb + b);
+      p[u].x += o.x;
+      p[u].y += o.y;
+      p[u].z += o.z;
+      p[u].w += o.w;
+    }
+  }
+  const bool full = b + VB <= B;
+#pragma unroll
+  for (int u = 0; u < PU; ++u) {
+    if (sl[u] < 0) continue;
+    *reinterpret_cast<float4*>(pf + (int64_t)rw[u] * ldb + b) = p[u];
+    if (!(fl[u] & 1)) continue;
+    const int q1 = __ldg(poff + j0 + u + 1);
+    for (int q = __ldg(poff + j0 + u); q < q1; ++q) {
+      const int code = __ldg(pch + q);
+      float* dst = flows + (int64_t)(code >> 1) * ldb + b;
+      if (code & 1) {
+        *reinterpret_cast<float4*>(dst) = p[u];
+      } else if (full) {
+        atomicAdd(reinterpret_cast<float4*>(dst), p[u]);
+      } else {
+        const float pv[4] = {p[u].x, p[u].y, p[u].z, p[u].w};
+#pragma unroll
+        for (int e = 0; e < VB; ++e)
+          if (b + e < B) atomicAdd(dst + e, pv[e]);
+      }
     }
   }
 }
@@ -721,7 +739,7 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows) {
   ProfScope prof_(KC_ACCUM_PUSH, s);
   if (!B || !L.n_prod) return PCB_OK;
-  dim3 grid((unsigned)((L.n_prod + RW - 1) / RW), (unsigned)((B + SLAB - 1) / SLAB));
+  dim3 grid((unsigned)((L.n_prod + RW * 4 - 1) / (RW * 4)), (unsigned)((B + SLAB - 1) / SLAB));
   k_flow_push<<<grid, RW * 32, 0, s>>>(L.n_prod, B, ldb, L.prod_slots, L.prod_rows, L.push_flag,
                                        L.push_off, L.push_ch, flow_scratch, prod_flows, flows);
   return check_launch();
