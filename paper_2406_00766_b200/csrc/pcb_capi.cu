@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 13;
+constexpr int64_t kVersion = 14;
 
 struct Reader {
   const int64_t* p;
@@ -138,6 +138,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       Tp.count = r.get();
       Tp.row_off = r.ref();
       Tp.members = r.ref();
+      Tp.flags = r.ref();
       L.fwd.push_back(G);
       L.fwd_tc.push_back(T);
       L.pf_tc.push_back(Tp);

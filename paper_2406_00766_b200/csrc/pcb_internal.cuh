@@ -57,6 +57,7 @@ struct TcRows {
   int64_t count = 0;           // number of super-rows
   const int32_t* row_off = 0;  // [count+1] offsets into members (block rows of the group)
   const int32_t* members = 0;  // group-row indices, stacked in order
+  const int32_t* flags = 0;    // (param-flow stacks) bit 0: contiguous sum rows, bit 1: contiguous children
 };
 
 struct Layer {

@@ -51,6 +51,7 @@ struct PfArgs {
   int n_items, mtiles, kslices, cgroups, nchunks;
   int64_t sb_base;
   const int32_t *row_off, *members, *sum_ids, *prod_ids, *param_ids, *flow_ids;
+  const int32_t* flags;  // per super-row: bit 0 contiguous sum rows, bit 1 contiguous children
   const float* theta;
   float* f_params;
 };
@@ -134,7 +135,10 @@ __device__ __forceinline__ int swz_chunk(int row, int c) {
 template <int KN>
 __global__ void __launch_bounds__(PF_THREADS, 1)
     k_param_flow_ws(const PfArgs a, const __grid_constant__ CUtensorMap tm_r,
-                    const __grid_constant__ CUtensorMap tm_R, const __grid_constant__ CUtensorMap tm_e) {
+                    const __grid_constant__ CUtensorMap tm_R, const __grid_constant__ CUtensorMap tm_e,
+                    const __grid_constant__ CUtensorMap tm_r128,
+                    const __grid_constant__ CUtensorMap tm_Rt,
+                    const __grid_constant__ CUtensorMap tm_e256) {
   using C = PfCfg<KN>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOS], op_empty[C::kOS];
@@ -180,20 +184,35 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const int ncol = pf_cols(a, it, C::kCPG, cols_p);
         if (!ncol) continue;
         const int32_t* prow = a.prod_ids + (int64_t)it.r0 * a.cap;
-        const uint32_t bytes = (uint32_t)(it.nmem * a.k_m + it.nmem + ncol * KN) * PF_KS * 4;
+        // contiguous sum rows / children: one box each (the boxes may cover
+        // rows past the tile, which the converters ignore)
+        const int fl = __ldg(a.flags + it.sr);
+        const int a_rows = (fl & 1) ? PF_M + PF_M / a.k_m : it.nmem * a.k_m + it.nmem;
+        const int e_rows = (fl & 2) ? PF_N : ncol * KN;
+        const uint32_t bytes = (uint32_t)(a_rows + e_rows) * PF_KS * 4;
         for (int kc = it.kc0; kc < it.kc1; ++kc) {
           const int b0 = kc * PF_KS;
           mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
           const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
           mbar_arrive_expect_tx(rf, bytes);
           const uint32_t st = smem_u32(raw + rr.slot() * C::kRaw);
-          for (int s = 0; s < it.nmem; ++s) {
-            const int row = __ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo + s)) - (int)a.sb_base;
-            tma_load_2d(st + s * a.k_m * PF_KS * 4, &tm_r, b0, row, rf);
-            tma_load_2d(st + C::kA + C::kE + s * C::kRP, &tm_R, b0, row / a.k_m, rf);
+          if (fl & 1) {
+            const int row = __ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo)) - (int)a.sb_base;
+            tma_load_2d(st, &tm_r128, b0, row, rf);
+            tma_load_2d(st + C::kA + C::kE, &tm_Rt, b0, row / a.k_m, rf);
+          } else {
+            for (int s = 0; s < it.nmem; ++s) {
+              const int row = __ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo + s)) - (int)a.sb_base;
+              tma_load_2d(st + s * a.k_m * PF_KS * 4, &tm_r, b0, row, rf);
+              tma_load_2d(st + C::kA + C::kE + s * C::kRP, &tm_R, b0, row / a.k_m, rf);
+            }
           }
-          for (int ci = 0; ci < ncol; ++ci)
-            tma_load_2d(st + C::kA + ci * KN * PF_KS * 4, &tm_e, b0, __ldg(prow + cols_p[ci]), rf);
+          if (fl & 2) {
+            tma_load_2d(st + C::kA, &tm_e256, b0, __ldg(prow + cols_p[0]), rf);
+          } else {
+            for (int ci = 0; ci < ncol; ++ci)
+              tma_load_2d(st + C::kA + ci * KN * PF_KS * 4, &tm_e, b0, __ldg(prow + cols_p[ci]), rf);
+          }
           rr.next();
         }
       }
@@ -436,13 +455,16 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   a.kslices = max(1, min(ks, a.nchunks / 2));
   a.n_items = base * a.kslices;
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
-  CUtensorMap tr, tR, te;
+  CUtensorMap tr, tR, te, tr128, tRt, te256;
   if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, PF_SWZ) ||
       make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, PF_KS, 0) ||
-      make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, PF_SWZ))
+      make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, PF_SWZ) ||
+      make_rows_map(&tr128, ratio, L.n_sb * L.k_m, a.ldb, PF_M, PF_KS, PF_SWZ) ||
+      make_rows_map(&tRt, rmax, L.n_sb, a.ldb, PF_M / (int)L.k_m, PF_KS, 0) ||
+      make_rows_map(&te256, scratch, L.window, a.ldb, PF_N, PF_KS, PF_SWZ))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_param_flow_ws<KN><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te);
+  k_param_flow_ws<KN><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te, tr128, tRt, te256);
   return check_launch();
 }
 
@@ -470,6 +492,7 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   a.prod_ids = g.prod_ids;
   a.param_ids = g.param_ids;
   a.flow_ids = g.flow_ids;
+  a.flags = tc.flags;
   a.theta = theta;
   a.f_params = f_params;
   a.store = g.exclusive;

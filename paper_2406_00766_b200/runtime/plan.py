@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 13
+VERSION = 14
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -252,6 +252,25 @@ def em_tile_blocks(compiled, t_start, t_slab, t_km, t_kn):
     return out, np.flatnonzero(~covered).astype(np.int64)
 
 
+def pf_contig_flags(g, offs, mem, k_m: int, k_n: int) -> np.ndarray:
+    """Per (full-stack) super-row: bit 0 = its member sum blocks are
+    consecutive sum rows, bit 1 = its real child blocks are consecutive
+    scratch rows — the parameter-flow kernel then moves each with one TMA box
+    per chunk instead of one per block."""
+    n = offs.size - 1
+    flags = np.zeros(n, dtype=np.int64)
+    for r in range(n):
+        m = mem[offs[r]:offs[r + 1]]
+        sid = g.sum_ids[m]
+        a_ok = bool(np.all(np.diff(sid) == k_m)) if sid.size > 1 else True
+        row = int(m[0])
+        real = g.param_ids[row] != 0
+        p = g.prod_ids[row][real]
+        e_ok = bool(np.all(np.diff(p) == k_n)) if p.size > 1 else True
+        flags[r] = int(a_ok) | (int(e_ok) << 1)
+    return flags
+
+
 def _slab_of(ids, starts, slab):
     """Slab offset per parameter-tile id (-1 for the zero tile / padding)."""
     out = np.full(ids.shape, -1, dtype=np.int64)
@@ -382,8 +401,9 @@ def build_program(compiled, *, tensor_cores: bool = True):
                     ref(offs)
                     ref(mem)
                     n_tc_rows += offs.size - 1
+                ref(pf_contig_flags(g, offs, mem, L.k_m, L.k_n))
             else:
-                prog += [0, 0, 0, 0, 0] * 2
+                prog += [0, 0, 0, 0, 0] * 2 + [0, 0]
         prog.append(len(L.bwd_groups))
         for g in L.bwd_groups:
             rows, cap = g.par_ids.shape
