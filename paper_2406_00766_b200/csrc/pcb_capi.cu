@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 14;
+constexpr int64_t kVersion = 15;
 
 struct Reader {
   const int64_t* p;
@@ -70,12 +70,12 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->root_children = r.ref(&P->n_root_children);
   P->var_ncat = r.ref();
   P->use_tc = (int)r.get();
-  // PCB_TC_LEGACY=1: per-launch (non-persistent) tensor-core kernels, for A/B runs
-  if (P->use_tc && getenv("PCB_TC_LEGACY")) P->use_tc = 2;
   P->n_mma_tiles = r.get();
   P->mma_elems = r.get();
+  P->mma_plane = r.get();
   P->mma_theta = r.ref();
-  P->mma_slab = r.ref();
+  P->mma_slab_f = r.ref();
+  P->mma_slab_c = r.ref();
   P->mma_km = r.ref();
   P->mma_kn = r.ref();
   P->scratch_rows = r.get();
@@ -135,6 +135,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       T.count = r.get();
       T.row_off = r.ref();
       T.members = r.ref();
+      T.flags = r.ref();
       Tp.count = r.get();
       Tp.row_off = r.ref();
       Tp.members = r.ref();
@@ -157,9 +158,11 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       T.count = r.get();
       T.row_off = r.ref();
       T.members = r.ref();
+      T.flags = r.ref();
       Tf.count = r.get();
       Tf.row_off = r.ref();
       Tf.members = r.ref();
+      Tf.flags = r.ref();
       L.bwd.push_back(G);
       L.bwd_tc.push_back(T);
       L.bwd_tc_full.push_back(Tf);
@@ -204,7 +207,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->em_tile_off = r.ref();
   P->em_goff = r.ref();
   P->em_tile_start = r.ref();
-  P->em_tile_slab = r.ref();
+  P->em_tile_slab_f = r.ref();
+  P->em_tile_slab_c = r.ref();
   P->n_em_rest = r.get();
   P->n_em_small = r.get();
   P->em_rest = r.ref();

@@ -57,7 +57,9 @@ struct TcRows {
   int64_t count = 0;           // number of super-rows
   const int32_t* row_off = 0;  // [count+1] offsets into members (block rows of the group)
   const int32_t* members = 0;  // group-row indices, stacked in order
-  const int32_t* flags = 0;    // (param-flow stacks) bit 0: contiguous sum rows, bit 1: contiguous children
+  // bit 0: contiguous sum rows, bit 1: contiguous children (param-flow stacks);
+  // bit 2: the stacked theta tiles of every column are one run per plane
+  const int32_t* flags = 0;
 };
 
 struct Layer {
@@ -121,14 +123,19 @@ struct pcb_plan {
   // groups (em_rest) take the generic per-group pass
   int64_t n_em_blk = 0, n_em_tiles = 0, n_em_rest = 0, n_em_small = 0;  // rest: small first
   const int32_t *em_km = nullptr, *em_kn = nullptr, *em_tile_off = nullptr, *em_goff = nullptr,
-                *em_tile_start = nullptr, *em_tile_slab = nullptr, *em_rest = nullptr,
+                *em_tile_start = nullptr, *em_tile_slab_f = nullptr, *em_tile_slab_c = nullptr,
+                *em_rest = nullptr,
                 *em_rest_start = nullptr;  // first theta index of a contiguous rest group, else -1
   const float* theta_bound = nullptr;  // the plan's own theta (pcb_plan_set_theta)
-  int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported); 2: legacy TC
+  int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported)
   int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1, max_tc_rows = 1;
   // bf16 tensor-core copies of theta tiles (plan v4)
-  int64_t n_mma_tiles = 0, mma_elems = 0;
-  const int32_t *mma_theta = nullptr, *mma_slab = nullptr, *mma_km = nullptr, *mma_kn = nullptr;
+  // bf16 planes: regions of mma_plane elements: [F hi][F lo][C hi][C lo];
+  // tile t's sum-major planes at slab_f[t] (+ plane), its product-major
+  // planes at 2 * plane + slab_c[t] (+ plane)
+  int64_t n_mma_tiles = 0, mma_elems = 0, mma_plane = 0;
+  const int32_t *mma_theta = nullptr, *mma_slab_f = nullptr, *mma_slab_c = nullptr,
+                *mma_km = nullptr, *mma_kn = nullptr;
   __nv_bfloat16* mma = nullptr;  // bound by pcb_plan_set_mma
   int64_t scratch_rows = 1;      // all-layer scratch rows (sum of layer windows)
   int prod_rows_written = 0;     // every prod-flow row is stored by its first accumulation

@@ -126,14 +126,16 @@ __global__ void __launch_bounds__(128, 1)
 
 // ------------------------------------------------- theta -> bf16 MMA tiles
 // Every tensor-core tile (k_m x k_n, row-major in theta) is re-laid as four
-// bf16 planes in core-matrix order (tile_off), theta ~= hi + lo:
-//   [0, sz)     hi, sum-major      K-major B of the sum forward (N = sums,
-//   [sz, 2sz)   lo, sum-major      K = products); also the MN-major B of the
-//                                  per-launch child-flow kernel
-//   [2sz, 3sz)  hi, product-major  K-major B of the child flows (N = products,
-//   [3sz, 4sz)  lo, product-major  K = sums)
+// bf16 planes in core-matrix order (tile_off), theta ~= hi + lo, in four
+// regions of `plane` elements (runtime/plan.py mma_tiles):
+//   slab_f             hi, sum-major      K-major B of the sum forward (N =
+//   plane + slab_f     lo, sum-major      sums, K = products); also the MN-major
+//                                         B of the per-launch child-flow kernel
+//   2 plane + slab_c   hi, product-major  K-major B of the child flows (N =
+//   3 plane + slab_c   lo, product-major  products, K = sums)
 // Hi planes of consecutive tiles stack along N with a uniform core stride,
-// so a super-row's stacked tiles form one MMA operand.  One CTA per tile:
+// and slab_f / slab_c follow the stacking orders, so a super-row's stacked
+// tiles of one column are one contiguous run per plane.  One CTA per tile:
 // the tile is staged in shared memory, then every thread packs one 8-wide
 // core row per plane pair (16-byte stores).  Refreshed after every theta update.
 constexpr int TM_MAX = 64;
@@ -141,9 +143,10 @@ constexpr int TM_THREADS = 256;
 constexpr int TM_V4 = TM_MAX * TM_MAX / 4 / TM_THREADS;  // float4 loads per thread (max)
 __global__ void __launch_bounds__(TM_THREADS)
     k_theta_to_mma(int64_t n_tiles, const int32_t* __restrict__ t_theta,
-                   const int32_t* __restrict__ t_slab, const int32_t* __restrict__ t_km,
-                   const int32_t* __restrict__ t_kn, const float* __restrict__ theta,
-                   __nv_bfloat16* __restrict__ mma) {
+                   const int32_t* __restrict__ t_slab_f, const int32_t* __restrict__ t_slab_c,
+                   const int32_t* __restrict__ t_km, const int32_t* __restrict__ t_kn,
+                   const float* __restrict__ theta, __nv_bfloat16* __restrict__ mma,
+                   int64_t plane) {
   __shared__ float tile[TM_MAX * (TM_MAX + 1)];
   // the next tile's elements are loaded (float4, row-major) while this one is packed
   float4 nx[TM_V4];
@@ -183,30 +186,32 @@ __global__ void __launch_bounds__(TM_THREADS)
     }
     __syncthreads();
     if (t + gridDim.x < n_tiles) load(t + gridDim.x);
-    uint8_t* base = reinterpret_cast<uint8_t*>(mma + (int64_t)__ldg(t_slab + t));
+    __nv_bfloat16* fh = mma + __ldg(t_slab_f + t);
+    __nv_bfloat16* ch = mma + 2 * plane + __ldg(t_slab_c + t);
     const int n8 = sz / 8;
     for (int q = threadIdx.x; q < 2 * n8; q += TM_THREADS) {
       float v[8];
       uint32_t off;
-      int plane;
+      int pl;
       if (q < n8) {  // sum-major: core row (m, j..j+7)
         const int m = q / (kn / 8), j = (q - m * (kn / 8)) * 8;
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = tile[m * ld + j + e];
         off = (uint32_t)tile_off(m, j, kn) * 2u;
-        plane = 0;
+        pl = 0;
       } else {       // product-major: core row (j, m..m+7)
         const int r = q - n8;
         const int j = r / (km / 8), m = (r - j * (km / 8)) * 8;
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = tile[(m + e) * ld + j];
         off = (uint32_t)tile_off(j, m, km) * 2u;
-        plane = 2;
+        pl = 2;
       }
       uint4 hi, lo;
       split_pack8(v, hi, lo);
-      *reinterpret_cast<uint4*>(base + (plane * sz) * 2 + off) = hi;
-      *reinterpret_cast<uint4*>(base + ((plane + 1) * sz) * 2 + off) = lo;
+      uint8_t* dst = reinterpret_cast<uint8_t*>(pl == 0 ? fh : ch) + off;
+      *reinterpret_cast<uint4*>(dst) = hi;
+      *reinterpret_cast<uint4*>(dst + plane * 2) = lo;
     }
     __syncthreads();
   }
@@ -231,9 +236,10 @@ constexpr int EM_NP = 4;  // row passes per thread (k_m x k_n <= 64 x 64)
 __global__ void __launch_bounds__(EM_THREADS)
     k_em_tiles(int64_t n_blk, const int32_t* __restrict__ bkm, const int32_t* __restrict__ bkn,
                const int32_t* __restrict__ toff, const int32_t* __restrict__ tstart,
-               const int32_t* __restrict__ tslab, const float* __restrict__ F,
-               float* __restrict__ theta, __nv_bfloat16* __restrict__ mma, float kappa,
-               float step, int planes, int32_t* status) {
+               const int32_t* __restrict__ tslab_f, const int32_t* __restrict__ tslab_c,
+               const float* __restrict__ F, float* __restrict__ theta,
+               __nv_bfloat16* __restrict__ mma, int64_t plane_n, float kappa, float step,
+               int planes, int32_t* status) {
   __shared__ float tile[TM_MAX * (TM_MAX + 1)];
   const int tid = threadIdx.x;
   int informative = 0, bad = 0;
@@ -303,30 +309,32 @@ __global__ void __launch_bounds__(EM_THREADS)
       }
       if (!planes) continue;
       __syncthreads();
-      uint8_t* base = reinterpret_cast<uint8_t*>(mma + (int64_t)__ldg(tslab + t));
+      __nv_bfloat16* fh = mma + __ldg(tslab_f + t);
+      __nv_bfloat16* ch = mma + 2 * plane_n + __ldg(tslab_c + t);
       const int sz = km * kn, n8 = sz / 8;
       for (int q = tid; q < 2 * n8; q += EM_THREADS) {
         float v[8];
         uint32_t off;
-        int plane;
+        int pl;
         if (q < n8) {  // sum-major core row (m, j..j+7)
           const int m = q / (kn / 8), j = (q - m * (kn / 8)) * 8;
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = tile[m * ld + j + e];
           off = (uint32_t)tile_off(m, j, kn) * 2u;
-          plane = 0;
+          pl = 0;
         } else {       // product-major core row (j, m..m+7)
           const int r = q - n8;
           const int j = r / (km / 8), m = (r - j * (km / 8)) * 8;
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = tile[(m + e) * ld + j];
           off = (uint32_t)tile_off(j, m, km) * 2u;
-          plane = 2;
+          pl = 2;
         }
         uint4 hi, lo;
         split_pack8(v, hi, lo);
-        *reinterpret_cast<uint4*>(base + (plane * sz) * 2 + off) = hi;
-        *reinterpret_cast<uint4*>(base + ((plane + 1) * sz) * 2 + off) = lo;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(pl == 0 ? fh : ch) + off;
+        *reinterpret_cast<uint4*>(dst) = hi;
+        *reinterpret_cast<uint4*>(dst + plane_n * 2) = lo;
       }
       __syncthreads();
     }
@@ -346,8 +354,9 @@ int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, fl
   ProfScope prof_(KC_EM, s);
   if (!p->n_em_blk) return PCB_OK;
   k_em_tiles<<<grid_for(p->n_em_blk, 1, 148 * 8), EM_THREADS, 0, s>>>(
-      p->n_em_blk, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab,
-      f_params, theta, p->mma, pseudocount, step, planes ? 1 : 0, status);
+      p->n_em_blk, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab_f,
+      p->em_tile_slab_c, f_params, theta, p->mma, p->mma_plane, pseudocount, step,
+      planes ? 1 : 0, status);
   return check_launch();
 }
 
@@ -355,7 +364,8 @@ int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta) {
   ProfScope prof_(KC_EM, s);
   if (!p->n_mma_tiles || !p->mma) return PCB_OK;
   k_theta_to_mma<<<grid_for(p->n_mma_tiles, 1, 148 * 8), TM_THREADS, 0, s>>>(
-      p->n_mma_tiles, p->mma_theta, p->mma_slab, p->mma_km, p->mma_kn, theta, p->mma);
+      p->n_mma_tiles, p->mma_theta, p->mma_slab_f, p->mma_slab_c, p->mma_km, p->mma_kn, theta,
+      p->mma, p->mma_plane);
   return check_launch();
 }
 

@@ -43,15 +43,18 @@ __device__ __forceinline__ void store_split8(uint8_t* sh, uint8_t* sl, uint32_t 
 }
 
 // one thread: TMA-bulk-copy the S stacked bf16 tiles of one stage (each
-// `tile_bytes`, hi plane then lo plane) into dst, completing on `full`
+// `tile_bytes`: hi plane at slab, lo plane one plane region later) into dst
+// as [hi | lo] per tile, completing on `full`
 __device__ __forceinline__ void issue_tiles(uint8_t* dst, const __nv_bfloat16* __restrict__ mma,
-                                            const int32_t* __restrict__ slab_rows, int64_t stride,
-                                            const int32_t* __restrict__ members, int m0, int S,
-                                            int col, int tile_bytes, uint32_t full) {
+                                            int64_t plane, const int32_t* __restrict__ slab_rows,
+                                            int64_t stride, const int32_t* __restrict__ members,
+                                            int m0, int S, int col, int tile_bytes, uint32_t full) {
   mbar_arrive_expect_tx(full, (uint32_t)(S * tile_bytes));
   for (int s = 0; s < S; ++s) {
-    const int slab = slab_rows[(int64_t)members[m0 + s] * stride + col];
-    bulk_g2s(smem_u32(dst + s * tile_bytes), mma + slab, (uint32_t)tile_bytes, full);
+    const int64_t slab = slab_rows[(int64_t)members[m0 + s] * stride + col];
+    const uint32_t d = smem_u32(dst + s * tile_bytes);
+    bulk_g2s(d, mma + slab, (uint32_t)tile_bytes / 2, full);
+    bulk_g2s(d + tile_bytes / 2, mma + slab + plane, (uint32_t)tile_bytes / 2, full);
   }
 }
 
@@ -80,6 +83,7 @@ __global__ void __launch_bounds__(TC_THREADS, (KN <= 32) ? 2 : 1)
                  const int32_t* __restrict__ members, const int32_t* __restrict__ sum_ids,
                  const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
                  const int32_t* __restrict__ param_slab, const __nv_bfloat16* __restrict__ mma,
+                 int64_t plane,
                  const float* __restrict__ scratch, const float* __restrict__ bmax,
                  float* __restrict__ values) {
   using SM = FwdSmem<KN>;
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(TC_THREADS, (KN <= 32) ? 2 : 1)
     uint8_t* sAl = sAh + SM::kA;
     uint8_t* sB = sAl + SM::kA;
     if (tid == 0)
-      issue_tiles(sB, mma, param_slab, cap, members, m0, S, c, tile_bytes,
+      issue_tiles(sB, mma, plane, param_slab, cap, members, m0, S, c, tile_bytes,
                   smem_u32(&full[stage]));
 #pragma unroll
     for (int e = 0; e < HALF; ++e) x[e] = dead ? 0.f : ex2(fmaf(x[e], kL2E, -gml));
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(TC_THREADS, (KM <= 32) ? 2 : 1)
                     const int32_t* __restrict__ members, const int32_t* __restrict__ ch_ids,
                     const int32_t* __restrict__ par_ids, const int32_t* __restrict__ ppids,
                     const int32_t* __restrict__ par_slab, const __nv_bfloat16* __restrict__ mma,
+                    int64_t plane,
                     const float* __restrict__ values, const float* __restrict__ flows,
                     const float* __restrict__ scratch, const float* __restrict__ rmax,
                     int64_t sb_base, float* __restrict__ flow_scratch) {
@@ -295,7 +300,8 @@ __global__ void __launch_bounds__(TC_THREADS, (KM <= 32) ? 2 : 1)
     uint8_t* sAl = sAh + SM::kA;
     uint8_t* sB = sAl + SM::kA;
     if (tid == 0)
-      issue_tiles(sB, mma, par_slab, cap, members, m0, S, p, tile_bytes, smem_u32(&full[stage]));
+      issue_tiles(sB, mma, plane, par_slab, cap, members, m0, S, p, tile_bytes,
+                  smem_u32(&full[stage]));
 #pragma unroll
     for (int q = 0; q < HALF / 8; ++q)
       store_split8(sAh, sAl, kmajor_off(row, half * HALF + q * 8, KM), x + q * 8);
@@ -603,7 +609,7 @@ static int fwd_kn(const pcb_plan* P, const Layer& L, const FwdGroup& g, const Tc
   const unsigned grid = (unsigned)(tc.count * ((B + TC_M - 1) / TC_M));
   k_sum_fwd_tc<KN><<<grid, TC_THREADS, FwdSmem<KN>::kBytes, s>>>(
       (int)g.cap, (int)L.k_m, B, ldb, tc.row_off, tc.members, g.sum_ids, g.prod_ids,
-      g.param_ids, g.param_slab, P->mma, scratch, bmax, values);
+      g.param_ids, g.param_slab, P->mma, P->mma_plane, scratch, bmax, values);
   return check_launch();
 }
 
@@ -629,7 +635,7 @@ static int cf_km(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcR
   const unsigned grid = (unsigned)(tc.count * ((B + TC_M - 1) / TC_M));
   k_child_flow_tc<KM><<<grid, TC_THREADS, CfSmem<KM>::kBytes, s>>>(
       (int)g.cap, (int)L.k_n, B, ldb, tc.row_off, tc.members, g.ch_ids, g.par_ids,
-      g.par_param_ids, g.par_slab, P->mma, values, flows, scratch, rmax, L.sb_base,
+      g.par_param_ids, g.par_slab, P->mma, P->mma_plane, values, flows, scratch, rmax, L.sb_base,
       flow_scratch);
   return check_launch();
 }

@@ -61,7 +61,9 @@ struct WsArgs {
   const int32_t* out_ids;          // sum_ids (fwd) / ch_ids (cf): first output row per member
   const int32_t* src_ids;          // prod_ids (fwd) / par_ids (cf): first source row per column
   const int32_t* real_ids;         // param_ids (fwd) / par_param_ids (cf): 0 = padding column
-  const int32_t* slab;             // bf16 tile offset per (member, column)
+  const int32_t* slab;             // bf16 hi-plane offset per (member, column); lo = + plane
+  const int32_t* flags;            // per super-row: bit 2 = stacked tiles contiguous
+  int64_t plane;                   // elements per plane region of the bf16 theta copy
   const __nv_bfloat16* mma;
   const float* src0;               // scratch (fwd) / ratio rows r (cf, from sb_base)
   const float* shift;              // bmax (fwd) / rmax R (cf)
@@ -155,9 +157,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
-  const int plane_elems = a.nb * KC;        // one bf16 plane of one theta tile
-  const int plane_bytes = plane_elems * 2;
-  const int plane0 = (MODE == MODE_FWD) ? 0 : 2;  // sum-major / product-major planes
+  const int plane_bytes = a.nb * KC * 2;  // one bf16 plane of one theta tile
 
   if (warp == WS_PRODUCER) {
     // ------------------------------------------------------------ raw producer
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       const WsItem it = ws_item(a, item);
       const int m0 = it.m0, S = it.S;
       const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
+      const bool contig = a.flags && (__ldg(a.flags + it.sr) & 4);
       int c = slice_first(real, a.cap, it.ks * a.kper);
       for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
@@ -201,11 +202,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         uint8_t* bdst = ops + orr.slot() * C::kOp + 2 * C::kA;
         if (lane == 0) mbar_arrive_expect_tx(of, (uint32_t)(2 * S * plane_bytes));
         __syncwarp();
-        for (int q = lane; q < 2 * S; q += 32) {
-          const int s = q >> 1, lo = q & 1;
-          const int64_t slab = __ldg(a.slab + (int64_t)__ldg(a.members + m0 + s) * a.cap + c);
-          bulk_g2s(smem_u32(bdst + lo * C::kBPlane + s * plane_bytes),
-                   a.mma + slab + (int64_t)(plane0 + lo) * plane_elems, (uint32_t)plane_bytes, of);
+        if (contig) {  // the S tiles of this column are one run per plane
+          if (lane < 2) {
+            const int64_t slab = __ldg(a.slab + (int64_t)__ldg(a.members + m0) * a.cap + c);
+            bulk_g2s(smem_u32(bdst + lane * C::kBPlane), a.mma + slab + lane * a.plane,
+                     (uint32_t)(S * plane_bytes), of);
+          }
+        } else {
+          for (int q = lane; q < 2 * S; q += 32) {
+            const int s = q >> 1, lo = q & 1;
+            const int64_t slab = __ldg(a.slab + (int64_t)__ldg(a.members + m0 + s) * a.cap + c);
+            bulk_g2s(smem_u32(bdst + lo * C::kBPlane + s * plane_bytes), a.mma + slab + lo * a.plane,
+                     (uint32_t)plane_bytes, of);
+          }
         }
         orr.next();
       }
@@ -609,6 +618,8 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.src_ids = g.prod_ids;
   a.real_ids = g.param_ids;
   a.slab = g.param_slab;
+  a.flags = tc.flags;
+  a.plane = P->mma_plane;
   a.mma = P->mma;
   a.src0 = scratch;
   a.shift = bmax;
@@ -652,6 +663,8 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.src_ids = g.par_ids;
   a.real_ids = g.par_param_ids;
   a.slab = g.par_slab;
+  a.flags = tc.flags;
+  a.plane = P->mma_plane;
   a.mma = P->mma;
   a.src0 = ratio;
   a.shift = rmax;

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 14
+VERSION = 15
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -88,14 +88,42 @@ def tc_layer(L) -> bool:
     return L.k_m in TC_K and L.k_n in TC_K
 
 
-def mma_tiles(compiled, tensor_cores: bool = True):
-    """Unique parameter tiles of tensor-core layers and their bf16 slab offsets.
+def _stack_order(mats, tiles_of):
+    """Tile ids in stacking order: for every group of identical rows of each
+    matrix (child-block rows of the forward groups / parent-block rows of the
+    backward groups), column by column, the group's rows in order — so any
+    run of stacked rows of one column has consecutive plane offsets."""
+    order = []
+    for mat, tmat in zip(mats, tiles_of):
+        if mat.shape[0] == 0:
+            continue
+        gid, _ = group_matrix_rows(mat)
+        rows = np.argsort(gid, kind="stable")          # rows grouped, in order
+        g_sorted = gid[rows]
+        cols = np.arange(mat.shape[1])
+        # (group, column, row) order
+        key_g = np.repeat(g_sorted, cols.size)
+        key_c = np.tile(cols, rows.size)
+        key_r = np.repeat(np.arange(rows.size), cols.size)
+        o = np.lexsort((key_r, key_c, key_g))
+        t = tmat[rows][:, cols].ravel()[o]
+        order.append(t[t != 0])
+    return np.concatenate(order) if order else np.zeros(0, np.int64)
 
-    Returns (theta starts sorted, slab offsets, k_m, k_n, total bf16 elements);
-    each tile occupies 4 * k_m * k_n bf16: hi and lo planes of the tile in
-    sum-major core order (the K-major B operand of the sum forward), then hi
-    and lo planes of its transpose (the K-major B operand of the child flows)."""
+
+def mma_tiles(compiled, tensor_cores: bool = True):
+    """Unique parameter tiles of tensor-core layers and their bf16 plane offsets.
+
+    The bf16 copy of theta is four regions of T elements each: hi and lo of
+    every tile in sum-major core order (the K-major B operand of the sum
+    forward) at ``slab_f`` / ``slab_f + T``, and hi and lo of its transpose
+    (the K-major B operand of the child flows) at ``2T + slab_c`` / ``3T +
+    slab_c``.  ``slab_f`` follows the forward stacking order and ``slab_c``
+    the child-flow stacking order, so a super-row's stacked tiles of one
+    column are one contiguous run per plane.
+    Returns (theta starts sorted, slab_f, slab_c, k_m, k_n, T)."""
     starts, kms, kns = [], [], []
+    fm, ft, bm, bt = [], [], [], []
     if tensor_cores:
         for L in compiled.layers:
             if not tc_layer(L):
@@ -105,17 +133,53 @@ def mma_tiles(compiled, tensor_cores: bool = True):
             starts.append(ids)
             kms.append(np.full(ids.size, L.k_m, np.int64))
             kns.append(np.full(ids.size, L.k_n, np.int64))
+            for g in L.fwd_groups:
+                fm.append(g.prod_ids)
+                ft.append(g.param_ids)
+            for g in L.bwd_groups:
+                bm.append(g.par_ids)
+                bt.append(g.par_param_ids)
     if not starts:
         z = np.zeros(0, np.int64)
-        return z, z, z, z, 0
+        return z, z, z, z, z, 0
     s = np.concatenate(starts)
     km = np.concatenate(kms)
     kn = np.concatenate(kns)
     s, first = np.unique(s, return_index=True)  # a tied tile may recur across layers
     km, kn = km[first], kn[first]
-    size = 4 * km * kn
-    slab = np.concatenate([[0], np.cumsum(size)[:-1]]).astype(np.int64)
-    return s, slab, km, kn, int(size.sum())
+    size = km * kn
+
+    def offsets(order):
+        # first appearance in `order`, then any tile never stacked
+        idx = np.searchsorted(s, order)
+        seen = np.zeros(s.size, dtype=bool)
+        uniq = []
+        if idx.size:
+            _, f = np.unique(idx, return_index=True)
+            uniq = idx[np.sort(f)]
+            seen[uniq] = True
+        seq = np.concatenate([np.asarray(uniq, dtype=np.int64), np.flatnonzero(~seen)])
+        off = np.empty(s.size, dtype=np.int64)
+        off[seq] = np.concatenate([[0], np.cumsum(size[seq])[:-1]])
+        return off
+
+    slab_f = offsets(_stack_order(fm, ft))
+    slab_c = offsets(_stack_order(bm, bt))
+    return s, slab_f, slab_c, km, kn, int(size.sum())
+
+
+def theta_contig_flags(slab_ids, offs, mem, plane: int) -> np.ndarray:
+    """Per super-row: 4 if, for every column, its stacked tiles' plane
+    offsets are consecutive (one bulk copy per plane), else 0."""
+    n = offs.size - 1
+    flags = np.zeros(n, dtype=np.int64)
+    for r in range(n):
+        m = mem[offs[r]:offs[r + 1]]
+        sl = slab_ids[m]                       # [S, cap]
+        ok = np.all((sl[1:] - sl[:-1] == plane) | (sl[1:] < 0) & (sl[:-1] < 0)) \
+            if m.size > 1 else True
+        flags[r] = 4 if ok else 0
+    return flags
 
 
 IN_BLOCK_ELEMS = 16384   # pmf entries staged in shared memory per input block (64 KB)
@@ -190,7 +254,7 @@ def group_runs(group_idx, group_off):
     return run_off.astype(np.int64), gi[starts], lens.astype(np.int64)
 
 
-def em_tile_blocks(compiled, t_start, t_slab, t_km, t_kn):
+def em_tile_blocks(compiled, t_start, t_slab_f, t_slab_c, t_km, t_kn):
     """Simplex groups that exactly tile tensor-core parameter tiles.
 
     A block is k_m groups (the sums of one sum block) whose parameters are the
@@ -206,7 +270,8 @@ def em_tile_blocks(compiled, t_start, t_slab, t_km, t_kn):
     n_groups = go.size - 1
     empty = dict(blk_km=np.zeros(0, np.int64), blk_kn=np.zeros(0, np.int64),
                  blk_tile_off=np.zeros(1, np.int64), blk_groups=np.zeros(0, np.int64),
-                 tile_start=np.zeros(0, np.int64), tile_slab=np.zeros(0, np.int64))
+                 tile_start=np.zeros(0, np.int64), tile_slab_f=np.zeros(0, np.int64),
+                 tile_slab_c=np.zeros(0, np.int64))
     if n_groups <= 0 or t_start.size == 0:
         return empty, np.arange(max(n_groups, 0), dtype=np.int64)
     run_off, rs, rl = group_runs(gi, go)
@@ -248,7 +313,8 @@ def em_tile_blocks(compiled, t_start, t_slab, t_km, t_kn):
         blk_tile_off=np.concatenate([[0], np.cumsum([t.size for t in tl])]).astype(np.int64),
         blk_groups=np.concatenate([b[2] for b in blocks]).astype(np.int64),
         tile_start=np.concatenate([t_start[t] for t in tl]).astype(np.int64),
-        tile_slab=np.concatenate([t_slab[t] for t in tl]).astype(np.int64))
+        tile_slab_f=np.concatenate([t_slab_f[t] for t in tl]).astype(np.int64),
+        tile_slab_c=np.concatenate([t_slab_c[t] for t in tl]).astype(np.int64))
     return out, np.flatnonzero(~covered).astype(np.int64)
 
 
@@ -295,10 +361,12 @@ def build_program(compiled, *, tensor_cores: bool = True):
     ref(c.root_children if c.root_children is not None else np.zeros(0, np.int64))
     ref(np.asarray(c.var_categories, dtype=np.int64))
     prog.append(1 if tensor_cores else 0)
-    t_start, t_slab, t_km, t_kn, mma_elems = mma_tiles(c, tensor_cores)
-    prog += [int(t_start.size), mma_elems]
+    t_start, t_slab_f, t_slab_c, t_km, t_kn, plane_t = mma_tiles(c, tensor_cores)
+    mma_elems = 4 * plane_t
+    prog += [int(t_start.size), mma_elems, plane_t]
     ref(t_start)
-    ref(t_slab)
+    ref(t_slab_f)
+    ref(t_slab_c)
     ref(t_km)
     ref(t_kn)
     scratch_total = int(sum(L.scratch_window for L in c.layers)) or 1
@@ -390,7 +458,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.prod_ids)
             ref(g.param_ids)
             ref(g.flow_ids)
-            ref(_slab_of(g.param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
+            fslab = _slab_of(g.param_ids, t_start, t_slab_f) if use_tc else np.zeros(0, np.int64)
+            ref(fslab)
             prog.append(exclusive(g))
             if use_tc and rows:
                 # forward: enough super-rows to fill the SMs; param flows: full
@@ -400,10 +469,12 @@ def build_program(compiled, *, tensor_cores: bool = True):
                     prog.append(offs.size - 1)
                     ref(offs)
                     ref(mem)
+                    ref(theta_contig_flags(fslab.reshape(g.param_ids.shape), offs, mem,
+                                           L.k_m * L.k_n)
+                        | (pf_contig_flags(g, offs, mem, L.k_m, L.k_n) if mc == 0 else 0))
                     n_tc_rows += offs.size - 1
-                ref(pf_contig_flags(g, offs, mem, L.k_m, L.k_n))
             else:
-                prog += [0, 0, 0, 0, 0] * 2 + [0, 0]
+                prog += [0, 0, 0, 0, 0, 0, 0] * 2
         prog.append(len(L.bwd_groups))
         for g in L.bwd_groups:
             rows, cap = g.par_ids.shape
@@ -411,7 +482,17 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.ch_ids)
             ref(g.par_ids)
             ref(g.par_param_ids)
-            ref(_slab_of(g.par_param_ids, t_start, t_slab) if use_tc else np.zeros(0, np.int64))
+            # the persistent child-flow kernel reads the product-major planes
+            # (region 2 + slab_c); the per-launch one (block size 64) the
+            # sum-major planes through an MN-major descriptor
+            ws_cf = L.k_m in (16, 32)
+            if use_tc:
+                bslab = (2 * plane_t + _slab_of(g.par_param_ids, t_start, t_slab_c)) if ws_cf \
+                    else _slab_of(g.par_param_ids, t_start, t_slab_f)
+                bslab[g.par_param_ids == 0] = -1
+            else:
+                bslab = np.zeros(0, np.int64)
+            ref(bslab)
             if use_tc and rows:
                 # per-launch kernels: enough super-rows to fill the SMs; the
                 # persistent kernels: full stacks (they split K instead)
@@ -420,9 +501,11 @@ def build_program(compiled, *, tensor_cores: bool = True):
                     prog.append(offs.size - 1)
                     ref(offs)
                     ref(mem)
+                    ref(theta_contig_flags(bslab.reshape(g.par_param_ids.shape), offs, mem,
+                                           L.k_m * L.k_n))
                     n_tc_rows += offs.size - 1
             else:
-                prog += [0, 0, 0, 0, 0] * 2
+                prog += [0, 0, 0, 0, 0, 0, 0] * 2
         ref(L.prod_slots)
         ref(L.prod_rows)
         prog.append(len(L.pushes))
@@ -492,11 +575,12 @@ def build_program(compiled, *, tensor_cores: bool = True):
     ref(c.group_idx)
     ref(c.group_off)
     # EM tile blocks (groups that exactly tile tensor-core tiles) + the rest
-    tb, rest = em_tile_blocks(c, t_start, t_slab, t_km, t_kn)
+    tb, rest = em_tile_blocks(c, t_start, t_slab_f, t_slab_c, t_km, t_kn)
     prog.append(int(tb["blk_km"].size))
     prog.append(int(tb["tile_start"].size))
     tb["blk_goff"] = np.concatenate([[0], np.cumsum(tb["blk_km"])]).astype(np.int64)
-    for key in ("blk_km", "blk_kn", "blk_tile_off", "blk_goff", "tile_start", "tile_slab"):
+    for key in ("blk_km", "blk_kn", "blk_tile_off", "blk_goff", "tile_start", "tile_slab_f",
+                "tile_slab_c"):
         ref(tb[key])
     # remaining groups: small ones (one warp each) first, then big ones (one
     # CTA each, >= EM_BIG entries, e.g. HMM emission pmfs over the vocabulary)
