@@ -102,6 +102,8 @@ int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb,
                 float* d_scratch, float* d_lroot, float* d_work);
 
 /* Full backward pass (flows, prod_flows, f_params incl. replica reduction).
+ * d_prod_flows may be NULL when every product row is accumulated and pushed
+ * in a single layer (then nothing reads it; PCB_USAGE otherwise).
  * Replaces: pcirc/runtime/engine.py:220-259 (backward). */
 int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb,
                  const int32_t* d_xT, const float* d_theta, const float* d_values,

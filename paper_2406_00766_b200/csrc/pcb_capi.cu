@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 15;
+constexpr int64_t kVersion = 16;
 
 struct Reader {
   const int64_t* p;
@@ -213,6 +213,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->n_em_small = r.get();
   P->em_rest = r.ref();
   P->em_rest_start = r.ref();
+  P->prod_flows_optional = (int)r.get();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -440,6 +441,8 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
                  const float* d_theta, const float* d_values, float* d_flows, float* d_scratch,
                  float* d_flow_scratch, float* d_prod_flows, float* d_f_params, float* d_work) {
   if (bad_dims(plan, B, ldb) || !d_work) return PCB_USAGE;
+  // prod_flows may be skipped only when no product row accumulates across layers
+  if (!d_prod_flows && plan->num_prod_rows && !plan->prod_flows_optional) return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
   const Work w = carve(plan, ldb, d_work);
   {
@@ -452,7 +455,7 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
     if (launch_zero_ranges(s, plan->n_zero, plan->zero_start, plan->zero_len, ldb, d_flows))
       return PCB_CUDA;
     // every product row's first accumulation stores (plan flag): no zeroing
-    if (plan->num_prod_rows && !plan->prod_rows_written &&
+    if (d_prod_flows && plan->num_prod_rows && !plan->prod_rows_written &&
         cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * plan->num_prod_rows * ldb, s) !=
             cudaSuccess)
       return PCB_CUDA;

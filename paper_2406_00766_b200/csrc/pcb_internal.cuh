@@ -139,6 +139,7 @@ struct pcb_plan {
   __nv_bfloat16* mma = nullptr;  // bound by pcb_plan_set_mma
   int64_t scratch_rows = 1;      // all-layer scratch rows (sum of layer windows)
   int prod_rows_written = 0;     // every prod-flow row is stored by its first accumulation
+  int prod_flows_optional = 0;   // every product row is accumulated + pushed in one layer
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };

@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(RW * 32)
   for (int u = 0; u < PU; ++u) {
     p[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sl[u] >= 0) p[u] = *reinterpret_cast<const float4*>(fs + (int64_t)sl[u] * ldb + b);
-    if (sl[u] >= 0 && !(fl[u] & 2)) {
+    if (sl[u] >= 0 && pf && !(fl[u] & 2)) {
       const float4 o = *reinterpret_cast<const float4*>(pf + (int64_t)rw[u] * ldb + b);
       p[u].x += o.x;
       p[u].y += o.y;
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(RW * 32)
 #pragma unroll
   for (int u = 0; u < PU; ++u) {
     if (sl[u] < 0) continue;
-    *reinterpret_cast<float4*>(pf + (int64_t)rw[u] * ldb + b) = p[u];
+    if (pf) *reinterpret_cast<float4*>(pf + (int64_t)rw[u] * ldb + b) = p[u];
     if (!(fl[u] & 1)) continue;
     const int q1 = __ldg(poff + j0 + u + 1);
     for (int q = __ldg(poff + j0 + u); q < q1; ++q) {
@@ -989,7 +989,7 @@ __global__ void k_root_bwd(int B, int ldb, int64_t root_slot, int64_t root_row,
   if (root_slot >= 0) {
     flows[root_slot * ldb + b] = 1.f;
   } else {
-    pf[root_row * ldb + b] = 1.f;
+    if (pf) pf[root_row * ldb + b] = 1.f;
     for (int q = 0; q < nrc; ++q) flows[(int64_t)rc[q] * ldb + b] += 1.f;
   }
 }

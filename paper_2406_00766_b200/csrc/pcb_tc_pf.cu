@@ -41,6 +41,9 @@ constexpr int PF_N = 256;          // child columns per item
 constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzled box row)
 constexpr int PF_CH = PF_KS / 4;   // 16-byte chunks per box row
 constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
+#ifndef PF_RS
+#define PF_RS 2                    // raw stages (operand stages = 4 - PF_RS at 32-sample chunks)
+#endif
 constexpr int PF_THREADS = 448;    // 14 warps
 constexpr int PF_CONV0 = 2, PF_NCONV = 8, PF_EPI0 = 10;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
@@ -66,7 +69,7 @@ struct PfCfg {
   static constexpr int kOpA = PF_M * PF_KS * 2;        // one bf16 A plane
   static constexpr int kOpB = PF_N * PF_KS * 2;        // one bf16 B plane
   static constexpr int kOp = 2 * kOpA + 2 * kOpB;
-  static constexpr int kRS = (PF_KS == 16) ? 5 : 2, kOS = (PF_KS == 16) ? 3 : 2;
+  static constexpr int kRS = (PF_KS == 16) ? 5 : PF_RS, kOS = (PF_KS == 16) ? 3 : 4 - PF_RS;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static constexpr int kCPG = PF_N / KN;                // child columns per item
   static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need aligned bases");

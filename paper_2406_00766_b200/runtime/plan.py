@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 15
+VERSION = 16
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -421,6 +421,9 @@ def build_program(compiled, *, tensor_cores: bool = True):
     if c.root_row >= 0:
         covered[c.root_row] = True
     prog.append(1 if bool(covered.all()) else 0)
+    # every product row is accumulated and pushed in one layer: the backward
+    # pass may skip materialising prod_flows (d_prod_flows = NULL)
+    pf_optional = True
 
     # flow tiles written by exactly one (layer, group, row, column) in the pass:
     # a group whose tiles are all exclusive may store its parameter flows
@@ -545,6 +548,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             for i, ch in zip(idx.tolist(), p.children):
                 parts[i] = ch
         flags = (pfan > 0).astype(np.int64) | (2 * (last_layer[prow_arr] == li)).astype(np.int64)
+        pf_optional = pf_optional and bool(np.all(flags == 3))
         poff = np.concatenate([[0], np.cumsum(pfan)]).astype(np.int64)
         pch = (np.concatenate([q for q in parts if q is not None]).astype(np.int64)
                if pfan.sum() else np.zeros(0, np.int64))
@@ -597,8 +601,9 @@ def build_program(compiled, *, tensor_cores: bool = True):
     contig = np.full(max(n_groups, 0), -1, dtype=np.int64)
     contig[one] = gi[np.minimum(go[:-1][one], max(gi.size - 1, 0))]
     ref(contig[rest] if rest.size else np.zeros(0, np.int64))
+    prog.append(int(pf_optional))
     prog.append(MAGIC)
-    info = {"blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+    info = {"prod_flows_optional": pf_optional, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info

@@ -36,6 +36,9 @@ class TrainStep:
         self.bufs = allocate_buffers(compiled, self.B, self.dev, plan=self.plan)
         self.x = torch.zeros((self.B, compiled.num_vars), dtype=torch.int32, device=self.dev)
         self.allreduce = allreduce
+        # the step never reads prod_flows: skip writing it when the layout allows
+        self._pf_ptr = (0 if self.plan.info.get("prod_flows_optional")
+                        else self.bufs.prod_flows_full.data_ptr())
         self.graph = None
         self.ll = None
         self.launches_per_step = None
@@ -53,7 +56,7 @@ class TrainStep:
         _lib.call("pcb_backward", p.handle, s, self.B, b.ldb, b.xT.data_ptr(),
                   p.theta.data_ptr(), b.values_full.data_ptr(), b.flows_full.data_ptr(),
                   b.scratch_full.data_ptr(), b.flow_scratch_full.data_ptr(),
-                  b.prod_flows_full.data_ptr(), b.f_params.data_ptr(), b.work.data_ptr())
+                  self._pf_ptr, b.f_params.data_ptr(), b.work.data_ptr())
         ll = b.lroot.double().sum()
         if self.allreduce is not None:
             self.allreduce(b.f_params, ll)
