@@ -41,9 +41,6 @@ constexpr int PF_N = 256;          // child columns per item
 constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzled box row)
 constexpr int PF_CH = PF_KS / 4;   // 16-byte chunks per box row
 constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
-#ifndef PF_RS
-#define PF_RS 2                    // raw stages (operand stages = 4 - PF_RS at 32-sample chunks)
-#endif
 constexpr int PF_THREADS = 448;    // 14 warps
 constexpr int PF_CONV0 = 2, PF_NCONV = 8, PF_EPI0 = 10;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
@@ -59,7 +56,9 @@ struct PfArgs {
   float* f_params;
 };
 
-template <int KN>
+// RS raw stages and 4 - RS operand stages (32-sample chunks): 2 / 2 for
+// HBM-streaming layers, 3 / 1 for dense layers whose operands sit in L2
+template <int KN, int RS>
 struct PfCfg {
   static constexpr int kA = PF_M * PF_KS * 4;          // raw r rows of the tile
   static constexpr int kE = PF_N * PF_KS * 4;          // raw child rows
@@ -69,7 +68,7 @@ struct PfCfg {
   static constexpr int kOpA = PF_M * PF_KS * 2;        // one bf16 A plane
   static constexpr int kOpB = PF_N * PF_KS * 2;        // one bf16 B plane
   static constexpr int kOp = 2 * kOpA + 2 * kOpB;
-  static constexpr int kRS = (PF_KS == 16) ? 5 : PF_RS, kOS = (PF_KS == 16) ? 3 : 4 - PF_RS;
+  static constexpr int kRS = (PF_KS == 16) ? 5 : RS, kOS = (PF_KS == 16) ? 3 : 4 - RS;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static constexpr int kCPG = PF_N / KN;                // child columns per item
   static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need aligned bases");
@@ -135,14 +134,14 @@ __device__ __forceinline__ int swz_chunk(int row, int c) {
 
 }  // namespace
 
-template <int KN>
+template <int KN, int RS>
 __global__ void __launch_bounds__(PF_THREADS, 1)
     k_param_flow_ws(const PfArgs a, const __grid_constant__ CUtensorMap tm_r,
                     const __grid_constant__ CUtensorMap tm_R, const __grid_constant__ CUtensorMap tm_e,
                     const __grid_constant__ CUtensorMap tm_r128,
                     const __grid_constant__ CUtensorMap tm_Rt,
                     const __grid_constant__ CUtensorMap tm_e256) {
-  using C = PfCfg<KN>;
+  using C = PfCfg<KN, RS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOS], op_empty[C::kOS];
   __shared__ uint64_t acc_full[2], acc_empty[2];
@@ -437,13 +436,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 
 namespace {
 
-template <int KN>
+template <int KN, int RS>
 int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float* rmax,
               const float* scratch, cudaStream_t s) {
-  using C = PfCfg<KN>;
+  using C = PfCfg<KN, RS>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(k_param_flow_ws<KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k_param_flow_ws<KN, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kBytes) != cudaSuccess)
       return PCB_CUDA;
     attr = true;
@@ -467,7 +466,7 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
       make_rows_map(&te256, scratch, L.window, a.ldb, PF_N, PF_KS, PF_SWZ))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_param_flow_ws<KN><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te, tr128, tRt, te256);
+  k_param_flow_ws<KN, RS><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te, tr128, tRt, te256);
   return check_launch();
 }
 
@@ -499,10 +498,16 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   a.theta = theta;
   a.f_params = f_params;
   a.store = g.exclusive;
+  // dense layers (several 256-child column groups) re-read operands from L2:
+  // a deeper raw ring pays there
+  const bool dense = g.cap * L.k_n > PF_N;
   switch (L.k_n) {
-    case 16: return launch_pf<16>(a, L, ratio, rmax, scratch, s);
-    case 32: return launch_pf<32>(a, L, ratio, rmax, scratch, s);
-    case 64: return launch_pf<64>(a, L, ratio, rmax, scratch, s);
+    case 16: return dense ? launch_pf<16, 3>(a, L, ratio, rmax, scratch, s)
+                          : launch_pf<16, 2>(a, L, ratio, rmax, scratch, s);
+    case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, s)
+                          : launch_pf<32, 2>(a, L, ratio, rmax, scratch, s);
+    case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, s)
+                          : launch_pf<64, 2>(a, L, ratio, rmax, scratch, s);
     default: return PCB_USAGE;
   }
 }
