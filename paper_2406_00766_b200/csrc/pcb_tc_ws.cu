@@ -11,19 +11,19 @@
 // so the batch tiles of one super-row run side by side and share its theta
 // tiles through L2.
 //
-// Warp roles (15 warps):
+// Warp roles (19 warps):
 //   warp 0      raw producer: one 2-D TMA box (cp.async.bulk.tensor) of the
 //               K block's fp32 rows x 128 samples per source array into the
 //               raw ring;
-//   warp 14     theta producer: 1-D bulk copies of the stacked pre-split bf16
+//   warp 18     theta producer: 1-D bulk copies of the stacked pre-split bf16
 //               theta planes into the operand ring;
 //   warp 1      MMA issuer: three kind::f16 MMAs per 16-wide K step
 //               (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM), commits
 //               free operand stages and publish finished accumulators;
-//   warps 2-5   converters: thread = sample; raw row values -> shifted
+//   warps 2-9   converters: thread = (sample, K half); raw row values -> shifted
 //               exponential (MUFU ex2, shift folded into one FFMA) -> packed
 //               bf16 hi/lo planes in the K-major core-matrix layout;
-//   warps 6-13  shift + epilogue: per-sample shift g_b of the next item (max
+//   warps 10-17 shift + epilogue: per-sample shift g_b of the next item (max
 //               of the side maxima bmax / rmax over its K blocks), then TMEM ->
 //               registers -> log-domain result -> coalesced fp32 row stores
 //               (two warps per TMEM lane quarter, alternate 16-column chunks).
@@ -44,8 +44,19 @@ namespace {
 
 constexpr int WS_M = 128;           // samples per item
 constexpr int WS_NMAX = 256;        // stacked N per item
-constexpr int WS_THREADS = 480;     // 15 warps
-constexpr int WS_PRODUCER = 0, WS_MMA = 1, WS_CONV0 = 2, WS_EPI0 = 6, WS_THETA = 14;
+constexpr int WS_PRODUCER = 0, WS_MMA = 1, WS_CONV0 = 2;
+
+// warp layout: producer, MMA, NCONV converter warps (128 / 256 threads: one
+// or two per sample, splitting each K block), 8 epilogue warps, the theta
+// producer and the shift warp
+template <int NCONV>
+struct WsWarps {
+  static constexpr int kConv = NCONV;
+  static constexpr int kEpi0 = WS_CONV0 + NCONV;
+  static constexpr int kTheta = kEpi0 + 8;
+  static constexpr int kShift = kTheta + 1;
+  static constexpr int kThreads = (kShift + 1) * 32;
+};
 
 enum { MODE_FWD = 0, MODE_CF = 1 };
 
@@ -115,20 +126,26 @@ struct WsCfg {
   static constexpr int kRS = kRSmax > 8 ? 8 : kRSmax;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static_assert(kRS >= 2, "raw ring too small");
+  // converter warps: the child-flow conversion (two inputs per element) gets
+  // two threads per sample, the forward one
+  static constexpr int kNConv = MODE == MODE_CF ? 8 : 4;
 };
 
 }  // namespace
 
 template <int MODE, int KC>
-__global__ void __launch_bounds__(WS_THREADS, 1)
+__global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     k_sum_ws(const WsArgs a, const __grid_constant__ CUtensorMap tm0,
              const __grid_constant__ CUtensorMap tm1) {
   using C = WsCfg<MODE, KC>;
+  using W = WsWarps<C::kNConv>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS];
   __shared__ uint64_t op_full[C::kOS], op_empty[C::kOS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
   __shared__ float g_s[2][WS_M];
+  __shared__ int g_nk[2];                // real K blocks of the item (0: dead)
+  __shared__ int g_orow[2][WS_NMAX / 16];  // first output row of every 16 columns
   __shared__ bool g_last;
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
@@ -138,17 +155,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   if (tid == 0) {
     for (int i = 0; i < C::kRS; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
-      mbar_init(smem_u32(&raw_empty[i]), 4);
+      mbar_init(smem_u32(&raw_empty[i]), W::kConv);
     }
     for (int i = 0; i < C::kOS; ++i) {
-      mbar_init(smem_u32(&op_full[i]), 4 + 1);  // 4 converter warps + theta tx
+      mbar_init(smem_u32(&op_full[i]), W::kConv + 1);  // converter warps + theta tx
       mbar_init(smem_u32(&op_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 8);
-      mbar_init(smem_u32(&g_full[i]), 4);
-      mbar_init(smem_u32(&g_empty[i]), 4);
+      mbar_init(smem_u32(&g_full[i]), 1);               // the shift warp
+      mbar_init(smem_u32(&g_empty[i]), W::kConv + 8);   // converters + epilogue warps
     }
     fence_mbar_init();
   }
@@ -185,7 +202,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
       }
     }
-  } else if (warp == WS_THETA) {
+  } else if (warp == W::kTheta) {
     // ------------------------------------------------------------ theta producer
     // stacked theta tiles of each K block: hi planes back to back, then lo
     // planes, so the S tiles form one N = S * nb operand per plane
@@ -267,9 +284,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       __syncwarp();
       ++acc_u;
     }
-  } else if (warp < WS_EPI0) {
+  } else if (warp < W::kEpi0) {
     // ------------------------------------------------------------ converters
-    const int t = tid - WS_CONV0 * 32;  // sample within the item
+    const int t = (tid - WS_CONV0 * 32) & (WS_M - 1);  // sample within the item
+    const int kh = (tid - WS_CONV0 * 32) / WS_M;        // which part of each K block
+    constexpr int KH = KC * 4 / W::kConv;                // K columns per converter thread
     Ring rr(C::kRS), orr(C::kOS);
     int g_u = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -288,22 +307,23 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
         const float* rs = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
-        float x[KC];
+        float x[KH];
+        const float* rh = rs + kh * KH * WS_M;
         if (MODE == MODE_FWD) {
 #pragma unroll
-          for (int j = 0; j < KC; ++j) x[j] = rs[j * WS_M + t];
+          for (int j = 0; j < KH; ++j) x[j] = rh[j * WS_M + t];
         } else {
           // r + (R_block - g): both shifts are fp32 log2 values, their
           // difference is small and (near-)exact
           const float d = rs[KC * WS_M + t] - gl2;
 #pragma unroll
-          for (int j = 0; j < KC; ++j) x[j] = rs[j * WS_M + t] + d;
+          for (int j = 0; j < KH; ++j) x[j] = rh[j * WS_M + t] + d;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&raw_empty[rr.slot()]));
         rr.next();
 #pragma unroll
-        for (int j = 0; j < KC; ++j) {
+        for (int j = 0; j < KH; ++j) {
           if (MODE == MODE_FWD)
             x[j] = dead ? 0.f : ex2(fmaf(x[j], kL2E, -gl2));
           else
@@ -313,13 +333,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         uint8_t* sAh = ops + orr.slot() * C::kOp;
         uint8_t* sAl = sAh + C::kA;
 #pragma unroll
-        for (int q = 0; q < KC / 8; ++q) {
+        for (int q = 0; q < KH / 8; ++q) {
           float v8[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) v8[e] = x[q * 8 + e];
           uint4 hi, lo;
           split_pack8(v8, hi, lo);
-          const uint32_t off = kmajor_off(t, q * 8, KC);
+          const uint32_t off = kmajor_off(t, kh * KH + q * 8, KC);
           *reinterpret_cast<uint4*>(sAh + off) = hi;
           *reinterpret_cast<uint4*>(sAl + off) = lo;
         }
@@ -332,85 +352,96 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       if (lane == 0) mbar_arrive(smem_u32(&g_empty[gs]));
       ++g_u;
     }
-  } else if (warp >= WS_EPI0) {
-    // ------------------------------------------------------------ shift + epilogue
-    // warps 6..13: lane quarter q4 = warp % 4 (TMEM lanes 32*q4..), column
-    // half h; warps 6-9 (h = 0) also publish the converters' shift.
-    const int q4 = warp & 3;
-    const int h = (warp - WS_EPI0) >> 2;
-    const int t = q4 * 32 + lane;          // sample within the item
-    auto shift_of = [&](int item, int& nk) {
-      const WsItem it = ws_item(a, item);
-      const int b = it.b0 + t;
+  } else if (warp == W::kShift) {
+    // ------------------------------------------------------------ shift warp
+    // per item, ahead of the converters and the epilogue: the per-sample
+    // shift g_b (max of the side maxima bmax / R over the item's K blocks;
+    // lane = 4 samples), the number of real K blocks, and the output rows
+    // shifts of the lane's 4 samples: the K blocks' ids once (warp-uniform),
+    // then the 4 x 8 side maxima of each round in flight together
+    constexpr int SPL = WS_M / 32;  // samples per lane
+    auto shifts = [&](const WsItem& it, float* g, int& nk) {
       const int64_t r0 = it.r0;
       const int32_t* src = a.src_ids + r0 * a.cap;
       const int32_t* real = a.real_ids + r0 * a.cap;
-      float g = PCB_NEG_INF;
+#pragma unroll
+      for (int u = 0; u < SPL; ++u) g[u] = PCB_NEG_INF;
       nk = 0;
       if (a.gshift) {  // long K: shifts precomputed by k_group_shift
         for (int c = 0; c < a.cap; ++c) nk += __ldg(real + c) != 0;
-        if (b < a.B) g = __ldg(a.gshift + (int64_t)it.sr * a.ldb + b);
-        return g;
+#pragma unroll
+        for (int u = 0; u < SPL; ++u) {
+          const int b = it.b0 + lane + 32 * u;
+          if (b < a.B) g[u] = __ldg(a.gshift + (int64_t)it.sr * a.ldb + b);
+        }
+        return;
       }
-      // 8 K blocks per round: their ids, then their side maxima, in flight together
       for (int c0 = 0; c0 < a.cap; c0 += 8) {
         int sc[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = c0 + u;
-          sc[u] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
+        for (int e = 0; e < 8; ++e) {
+          const int c = c0 + e;
+          sc[e] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
+          nk += sc[e] >= 0;
         }
-        float v[8];
+        float v[SPL][8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          nk += sc[u] >= 0;
-          v[u] = (sc[u] >= 0 && b < a.B)
-                     ? __ldg(a.shift + (int64_t)(sc[u] - a.sb_base) / KC * a.ldb + b)
-                     : PCB_NEG_INF;
+        for (int u = 0; u < SPL; ++u) {
+          const int b = it.b0 + lane + 32 * u;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            v[u][e] = (sc[e] >= 0 && b < a.B)
+                          ? __ldg(a.shift + (int64_t)(sc[e] - a.sb_base) / KC * a.ldb + b)
+                          : PCB_NEG_INF;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) g = fmaxf(g, v[u]);
+        for (int u = 0; u < SPL; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) g[u] = fmaxf(g[u], v[u][e]);
       }
-      return g;
     };
-    int g_u = 0, acc_u = 0;
-    int item = blockIdx.x;
-    int nk = 0, nk_next = 0;
-    float g = 0.f;
-    if (item < a.n_items) {
-      g = shift_of(item, nk);
-      if (h == 0) {
-        g_s[0][t] = g;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&g_full[0]));
+    int g_u = 0;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++g_u) {
+      const WsItem it = ws_item(a, item);
+      const int gs = g_u & 1;
+      mbar_wait(smem_u32(&g_empty[gs]), (uint32_t)(((g_u >> 1) & 1) ^ 1));
+      int nk = 0;
+      float gv[SPL];
+      shifts(it, gv, nk);
+#pragma unroll
+      for (int u = 0; u < SPL; ++u) g_s[gs][lane + 32 * u] = gv[u];
+      const int N = it.S * a.nb;
+      if (lane < N / 16) {
+        const int c0 = lane * 16, sm = c0 / a.nb;
+        g_orow[gs][lane] = __ldg(a.out_ids + __ldg(a.members + it.m0 + sm)) + (c0 - sm * a.nb);
       }
+      if (lane == 0) g_nk[gs] = nk;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&g_full[gs]));
     }
-    for (; item < a.n_items; item += gridDim.x) {
-      // the next item's shift, computed (and for h = 0 published) before
-      // draining this one
-      const int nxt = item + gridDim.x;
-      float g_next = 0.f;
-      if (nxt < a.n_items) {
-        const int gs = (g_u + 1) & 1;
-        if (h == 0) mbar_wait(smem_u32(&g_empty[gs]), (uint32_t)((((g_u + 1) >> 1) & 1) ^ 1));
-        g_next = shift_of(nxt, nk_next);
-        if (h == 0) {
-          g_s[gs][t] = g_next;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&g_full[gs]));
-        }
-      }
+  } else if (warp >= W::kEpi0) {
+    // ------------------------------------------------------------ epilogue
+    // warps 10..17: lane quarter q4 = warp % 4 (TMEM lanes 32*q4..), column
+    // half h (alternate 16-column chunks)
+    const int q4 = warp & 3;
+    const int h = (warp - W::kEpi0) >> 2;
+    const int t = q4 * 32 + lane;          // sample within the item
+    int g_u = 0, acc_u = 0;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++g_u) {
       const WsItem it = ws_item(a, item);
       const int b = it.b0 + t;
       const bool live = b < a.B;
-      const int m0 = it.m0;
       const int N = it.S * a.nb;
       const int as = acc_u & 1;
+      const int gs = g_u & 1;
+      mbar_wait(smem_u32(&g_full[gs]), (uint32_t)((g_u >> 1) & 1));
+      // the slot is released at the end of the item (the shift warp runs
+      // at most two items ahead, like the TMEM double buffer)
+      const float g = g_s[gs][t];
+      const int nk = g_nk[gs];
       const bool dead = g == PCB_NEG_INF || nk == 0;
-      auto out_row = [&](int c0) {  // first output row of the 16 columns at c0
-        const int s = c0 / a.nb, j0 = c0 - s * a.nb;  // nb is a multiple of 16
-        return (int64_t)__ldg(a.out_ids + __ldg(a.members + m0 + s)) + j0;
-      };
+      const int* orow_s = g_orow[gs];
+      auto out_row = [&](int c0) -> int64_t { return orow_s[c0 >> 4]; };
       // finished result of 16 columns from their fp32 sums d (TMEM or reduced)
       auto finish = [&](float* o, const float* d, const float* l) {
         if (MODE == MODE_FWD) {
@@ -471,7 +502,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
         __threadfence();
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
-        if (warp == WS_EPI0 && lane == 0) {
+        if (warp == W::kEpi0 && lane == 0) {
           int32_t* cnt = a.counters + it.sr * a.ntiles + it.tile;
           const int old = atomicAdd(cnt, 1);
           const bool last = old == a.kslices - 1;
@@ -493,10 +524,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // g_last reuse
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&g_empty[gs]));
       ++acc_u;
-      ++g_u;
-      g = g_next;
-      nk = nk_next;
     }
   }
   tc_fence_before();
@@ -523,7 +553,7 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
                     a.ldb, MODE == MODE_CF ? 1 : KC))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_sum_ws<MODE, KC><<<grid, WS_THREADS, C::kBytes, s>>>(a, tm0, tm1);
+  k_sum_ws<MODE, KC><<<grid, WsWarps<C::kNConv>::kThreads, C::kBytes, s>>>(a, tm0, tm1);
   return check_launch();
 }
 
