@@ -129,18 +129,43 @@ __global__ void __launch_bounds__(IN_THREADS)
   const int64_t slot0 = bslot0[blk];
   const int32_t* pid = pids + bpoff[blk];
   const int total = cnt * ncat;
-  // stage log-pmfs: 4 independent loads in flight per thread
-  for (int q0 = threadIdx.x; q0 < total; q0 += 4 * IN_THREADS) {
-    float v[4];
+  // stage log-pmfs: a warp per input row, float4 loads when the pmf is
+  // 16-byte aligned (4 rows in flight per warp), else scalar loads
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = IN_THREADS / 32;
+  if ((ncat & 3) == 0) {
+    for (int i0 = warp; i0 < cnt; i0 += NW * 4) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = q0 + u * IN_THREADS;
-      v[u] = (q < total) ? __ldg(theta + pid[q / ncat] + (q % ncat)) : 1.f;
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * NW;
+        if (i >= cnt) continue;
+        const float* src = theta + __ldg(pid + i);
+        float* dst = tbl + i * ncat;
+        const bool al = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+        for (int c = lane * 4; c < ncat; c += 128) {
+          float4 v = al ? __ldg(reinterpret_cast<const float4*>(src + c))
+                        : make_float4(__ldg(src + c), __ldg(src + c + 1), __ldg(src + c + 2),
+                                      __ldg(src + c + 3));
+          dst[c] = __logf(v.x);
+          dst[c + 1] = __logf(v.y);
+          dst[c + 2] = __logf(v.z);
+          dst[c + 3] = __logf(v.w);
+        }
+      }
     }
+  } else {
+    for (int q0 = threadIdx.x; q0 < total; q0 += 4 * IN_THREADS) {
+      float v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = q0 + u * IN_THREADS;
-      if (q < total) tbl[q] = __logf(v[u]);
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * IN_THREADS;
+        v[u] = (q < total) ? __ldg(theta + pid[q / ncat] + (q % ncat)) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * IN_THREADS;
+        if (q < total) tbl[q] = __logf(v[u]);
+      }
     }
   }
   __syncthreads();
@@ -1045,6 +1070,38 @@ __global__ void k_em(int64_t n_list, const int32_t* __restrict__ glist,
     const int a = goff[g], z = goff[g + 1];
     // contiguous groups index theta directly (no index-table reads)
     const int c0 = __ldg(gstart + gi), shift = c0 - a;
+    if (c0 >= 0 && z - a <= 256) {
+      // small contiguous group (an input pmf): every flow, then every old
+      // theta, in flight together; one reduction; stores
+      float v[8], o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * u;
+        v[u] = k < z - a ? __ldg(F + c0 + k) + kappa : 0.f;
+      }
+      float tot = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tot += v[u];
+      for (int o2 = 16; o2 > 0; o2 >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o2);
+      if (!(tot > 0.f)) continue;
+      ++informative;
+      const float inv = 1.f / tot;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * u;
+        o[u] = (k < z - a && step < 1.f) ? theta[c0 + k] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * u;
+        if (k >= z - a) continue;
+        const float nv = v[u] * inv;
+        const float th = (step >= 1.f) ? nv : ((1.f - step) * o[u] + step * nv);
+        if (!isfinite(th)) ++bad;
+        theta[c0 + k] = th;
+      }
+      continue;
+    }
     float tot = 0.f;
     for (int k = a + lane; k < z; k += 32) tot += F[c0 >= 0 ? k + shift : gidx[k]] + kappa;
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);

@@ -126,9 +126,7 @@ struct WsCfg {
   static constexpr int kRS = kRSmax > 8 ? 8 : kRSmax;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
   static_assert(kRS >= 2, "raw ring too small");
-  // converter warps: the child-flow conversion (two inputs per element) gets
-  // two threads per sample, the forward one
-  static constexpr int kNConv = MODE == MODE_CF ? 8 : 4;
+  static constexpr int kNConv = 8;  // converter warps: two threads per sample
 };
 
 }  // namespace
