@@ -358,7 +358,7 @@ int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float
 // precision even at |log p| ~ 1e4.  The tensor-core flow kernels read r (one
 // row per sum instead of flows + values) and R.
 constexpr int KM_MAX = 64;
-__global__ void __launch_bounds__(RW * 32)
+__global__ void __launch_bounds__(RW * 32, 5)
     k_ratio(int k_m, int B, int ldb, int64_t sb_base, const float* __restrict__ values,
             const float* __restrict__ flows, float* __restrict__ rmax, float* __restrict__ ratio) {
   constexpr int PER = KM_MAX / RW;
@@ -922,7 +922,15 @@ __global__ void __launch_bounds__(IS_THREADS)
   const int m0 = start[ncat], m1 = start[nb];
   for (int i = warp; i < cnt; i += IS_WARPS) {
     const float4* src = reinterpret_cast<const float4*>(flows + (slot0 + i) * ldb);
-    for (int q = lane; q < ldb / 4; q += 32) reinterpret_cast<float4*>(row)[q] = src[q];
+    for (int q0 = lane; q0 < ldb / 4; q0 += 128) {  // 4 loads in flight per lane
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + 32 * u < ldb / 4) v[u] = src[q0 + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + 32 * u < ldb / 4) reinterpret_cast<float4*>(row)[q0 + 32 * u] = v[u];
+    }
     __syncwarp();
     float miss = 0.f;
     for (int p = m0 + lane; p < m1; p += 32) miss += row[order[p]];

@@ -251,14 +251,29 @@ __global__ void __launch_bounds__(EM_THREADS)
     float acc[EM_NP];
 #pragma unroll
     for (int p = 0; p < EM_NP; ++p) acc[p] = 0.f;
-    for (int t = t0; t < t1; ++t) {
-      const float* f = F + __ldg(tstart + t);
+    const bool one_pass = rp >= km;  // every thread owns one row quad of each tile
+    if (one_pass) {
+      // 4 tiles' flows in flight per round
+      for (int t = t0; t < t1; t += 4) {
+        float4 v[4];
 #pragma unroll
-      for (int p = 0; p < EM_NP; ++p) {
-        const int row = p * rp + r_in;
-        if (row < km) {
-          const float4 v = ld4(f + row * kn + c4);
-          acc[p] += (v.x + kappa) + (v.y + kappa) + (v.z + kappa) + (v.w + kappa);
+        for (int u = 0; u < 4; ++u)
+          v[u] = (t + u < t1 && r_in < km) ? ld4(F + __ldg(tstart + t + u) + r_in * kn + c4)
+                                           : make_float4(-kappa, -kappa, -kappa, -kappa);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          acc[0] += (v[u].x + kappa) + (v[u].y + kappa) + (v[u].z + kappa) + (v[u].w + kappa);
+      }
+    } else {
+      for (int t = t0; t < t1; ++t) {
+        const float* f = F + __ldg(tstart + t);
+#pragma unroll
+        for (int p = 0; p < EM_NP; ++p) {
+          const int row = p * rp + r_in;
+          if (row < km) {
+            const float4 v = ld4(f + row * kn + c4);
+            acc[p] += (v.x + kappa) + (v.y + kappa) + (v.z + kappa) + (v.w + kappa);
+          }
         }
       }
     }
@@ -275,16 +290,30 @@ __global__ void __launch_bounds__(EM_THREADS)
       if (live && tid % tpr == 0) ++informative;
     }
     const int ld = kn + 1;
+    // one-pass blocks: the next tile's flows and theta are loaded before this
+    // tile's plane packing (two barriers) runs
+    float4 fn = make_float4(0.f, 0.f, 0.f, 0.f), on = fn;
+    if (one_pass && r_in < km) {
+      const int64_t ts = __ldg(tstart + t0);
+      fn = ld4(F + ts + r_in * kn + c4);
+      on = ld4(theta + ts + r_in * kn + c4);
+    }
     for (int t = t0; t < t1; ++t) {
       const int64_t ts = __ldg(tstart + t);
       const float* f = F + ts;
       float* th = theta + ts;
+      const float4 fc = fn, oc = on;
+      if (one_pass && t + 1 < t1 && r_in < km) {
+        const int64_t tn = __ldg(tstart + t + 1);
+        fn = ld4(F + tn + r_in * kn + c4);
+        on = ld4(theta + tn + r_in * kn + c4);
+      }
 #pragma unroll
       for (int p = 0; p < EM_NP; ++p) {
         const int row = p * rp + r_in;
-        if (row >= km) continue;
-        const float4 fv = ld4(f + row * kn + c4);
-        float4 o = ld4(th + row * kn + c4);
+        if (row >= km || (one_pass && p > 0)) continue;
+        const float4 fv = one_pass ? fc : ld4(f + row * kn + c4);
+        float4 o = one_pass ? oc : ld4(th + row * kn + c4);
         if (inv[p] > 0.f) {
           const float w = inv[p];
           const float n[4] = {(fv.x + kappa) * w, (fv.y + kappa) * w, (fv.z + kappa) * w,
