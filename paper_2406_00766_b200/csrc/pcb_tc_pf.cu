@@ -189,9 +189,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         // contiguous sum rows / children: one box each (the boxes may cover
         // rows past the tile, which the converters ignore)
         const int fl = __ldg(a.flags + it.sr);
-        const int a_rows = (fl & 1) ? PF_M + PF_M / a.k_m : it.nmem * a.k_m + it.nmem;
+        // R rows are 32-sample (128-byte) boxes whatever the chunk width
+        const int a_rows = (fl & 1) ? PF_M : it.nmem * a.k_m;
+        const int r_rows = (fl & 1) ? PF_M / a.k_m : it.nmem;
         const int e_rows = (fl & 2) ? PF_N : ncol * KN;
-        const uint32_t bytes = (uint32_t)(a_rows + e_rows) * PF_KS * 4;
+        const uint32_t bytes = (uint32_t)(a_rows + e_rows) * PF_KS * 4 + (uint32_t)r_rows * C::kRP;
         for (int kc = it.kc0; kc < it.kc1; ++kc) {
           const int b0 = kc * PF_KS;
           mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
@@ -459,10 +461,10 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
   CUtensorMap tr, tR, te, tr128, tRt, te256;
   if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, PF_SWZ) ||
-      make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, PF_KS, 0) ||
+      make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, C::kRP / 4, 0) ||
       make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, PF_SWZ) ||
       make_rows_map(&tr128, ratio, L.n_sb * L.k_m, a.ldb, PF_M, PF_KS, PF_SWZ) ||
-      make_rows_map(&tRt, rmax, L.n_sb, a.ldb, PF_M / (int)L.k_m, PF_KS, 0) ||
+      make_rows_map(&tRt, rmax, L.n_sb, a.ldb, PF_M / (int)L.k_m, C::kRP / 4, 0) ||
       make_rows_map(&te256, scratch, L.window, a.ldb, PF_N, PF_KS, PF_SWZ))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
