@@ -238,10 +238,17 @@ def run_ours(args, w):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; PCB_DIST_BACKEND=gloo (with ranks sharing a GPU)
+    # exercises the multi-rank path where fewer GPUs than ranks exist
+    backend = os.environ.get("PCB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     t0 = time.time()
     c = build_circuit(w)
     log(f"[bench] compiled {args.workload}: {c.num_edges} edges, theta {c.theta_size} "
