@@ -425,16 +425,34 @@ def build_program(compiled, *, tensor_cores: bool = True):
     # pass may skip materialising prod_flows (d_prod_flows = NULL)
     pf_optional = True
 
+    # replica flow ranges (compiler/build.py:516-533) are folded onto their
+    # master tiles: on the GPU every parameter-flow kernel accumulates with
+    # red.add (stores only for single-writer tiles), so the contention the
+    # replicas avoid on the CPU costs nothing, and the replica reduction pass
+    # and its 31 x 16.8 M-float traffic at HMM-4096 disappear.  The replica
+    # ranges of f_params stay zero.
+    red = np.asarray(c.reductions, dtype=np.int64).reshape(-1, 3)
+    rep_src, rep_dst = red[:, 0], red[:, 1]
+    rep_order = np.argsort(rep_src)
+    rep_src, rep_dst = rep_src[rep_order], rep_dst[rep_order]
+
+    def folded(ids):
+        if rep_src.size == 0:
+            return ids
+        pos = np.minimum(np.searchsorted(rep_src, ids), rep_src.size - 1)
+        hit = rep_src[pos] == ids
+        return np.where(hit, rep_dst[pos], ids)
+
     # flow tiles written by exactly one (layer, group, row, column) in the pass:
     # a group whose tiles are all exclusive may store its parameter flows
-    flow_starts = [g.flow_ids[g.param_ids != 0] for L in c.layers for g in L.fwd_groups]
+    flow_starts = [folded(g.flow_ids)[g.param_ids != 0] for L in c.layers for g in L.fwd_groups]
     if flow_starts:
         fu, fcnt = np.unique(np.concatenate(flow_starts), return_counts=True)
     else:
         fu, fcnt = np.zeros(0, np.int64), np.zeros(0, np.int64)
 
     def exclusive(g) -> int:
-        f = g.flow_ids[g.param_ids != 0]
+        f = folded(g.flow_ids)[g.param_ids != 0]
         return int(bool(np.all(fcnt[np.searchsorted(fu, f)] == 1))) if f.size else 1
 
     n_tc_rows = 0
@@ -460,7 +478,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(g.sum_ids)
             ref(g.prod_ids)
             ref(g.param_ids)
-            ref(g.flow_ids)
+            ref(folded(g.flow_ids))
             fslab = _slab_of(g.param_ids, t_start, t_slab_f) if use_tc else np.zeros(0, np.int64)
             ref(fslab)
             prog.append(exclusive(g))
@@ -557,7 +575,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
         ref(poff)
         ref(pch)
 
-    red = np.asarray(c.reductions, dtype=np.int64).reshape(-1, 3)
+    red = red[:0]  # folded above: no replica reduction pass
     if red.shape[0]:
         order = np.lexsort((np.arange(red.shape[0]), red[:, 1]))
         r = red[order]
