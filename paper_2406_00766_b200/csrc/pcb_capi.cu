@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 16;
+constexpr int64_t kVersion = 17;
 
 struct Reader {
   const int64_t* p;
@@ -131,6 +131,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.flow_ids = r.ref();
       G.param_slab = r.ref();
       G.exclusive = (int)r.get();
+      G.uniform = (int)r.get();
       TcRows T, Tp;
       T.count = r.get();
       T.row_off = r.ref();
@@ -154,6 +155,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.par_ids = r.ref();
       G.par_param_ids = r.ref();
       G.par_slab = r.ref();
+      G.uniform = (int)r.get();
       TcRows T, Tf;
       T.count = r.get();
       T.row_off = r.ref();

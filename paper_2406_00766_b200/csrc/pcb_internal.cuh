@@ -43,12 +43,14 @@ struct FwdGroup {
   const int32_t *sum_ids, *prod_ids, *param_ids, *flow_ids;
   const int32_t* param_slab;  // bf16 MMA-tile offset per (row, col), -1 for padding
   int exclusive = 0;          // every flow tile of the group has no other writer in the pass
+  int uniform = 0;            // every row has the same child blocks (dense layer)
 };
 
 struct BwdGroup {
   int64_t rows, cap;
   const int32_t *ch_ids, *par_ids, *par_param_ids;
   const int32_t* par_slab;
+  int uniform = 0;  // every row has the same parent blocks (dense layer)
 };
 
 // Tensor-core work list for one forward / backward group: "super-rows" stack

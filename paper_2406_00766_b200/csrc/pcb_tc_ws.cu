@@ -82,6 +82,7 @@ struct WsArgs {
   float* out;                      // values (fwd) / flow_scratch (cf)
   int32_t* counters;               // split-K arrivals per (super-row, tile)
   const float* gshift;             // precomputed per-(super-row, sample) shifts, or null
+  int64_t gshift_stride;           // ldb, or 0 when every super-row shares one shift row
 };
 
 struct WsItem {
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
 #pragma unroll
         for (int u = 0; u < SPL; ++u) {
           const int b = it.b0 + lane + 32 * u;
-          if (b < a.B) g[u] = __ldg(a.gshift + (int64_t)it.sr * a.ldb + b);
+          if (b < a.B) g[u] = __ldg(a.gshift + (int64_t)it.sr * a.gshift_stride + b);
         }
         return;
       }
@@ -656,8 +657,9 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
   if (ws_long_k(a.cap)) {
-    if (launch_group_shift(a, (int)L.k_n, tc.count, gshift, s)) return PCB_CUDA;
+    if (launch_group_shift(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, s)) return PCB_CUDA;
     a.gshift = gshift;
+    a.gshift_stride = g.uniform ? 0 : ldb;
   }
   // split K reduces partial sums in place: zero the layer's sum rows first
   if (a.kslices > 1 &&
@@ -701,8 +703,9 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
   if (ws_long_k(a.cap)) {
-    if (launch_group_shift(a, (int)L.k_m, tc.count, gshift, s)) return PCB_CUDA;
+    if (launch_group_shift(a, (int)L.k_m, g.uniform ? 1 : tc.count, gshift, s)) return PCB_CUDA;
     a.gshift = gshift;
+    a.gshift_stride = g.uniform ? 0 : ldb;
   }
   if (a.kslices > 1 &&
       cudaMemsetAsync(flow_scratch, 0, sizeof(float) * L.window * (int64_t)ldb, s) != cudaSuccess)

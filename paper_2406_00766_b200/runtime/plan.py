@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 16
+VERSION = 17
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -482,6 +482,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             fslab = _slab_of(g.param_ids, t_start, t_slab_f) if use_tc else np.zeros(0, np.int64)
             ref(fslab)
             prog.append(exclusive(g))
+            # every row has the same child blocks: one shift row serves them all
+            prog.append(int(rows > 0 and group_matrix_rows(g.prod_ids)[1].size == 1))
             if use_tc and rows:
                 # forward: enough super-rows to fill the SMs; param flows: full
                 # stacks (their grid also spans column groups)
@@ -514,6 +516,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             else:
                 bslab = np.zeros(0, np.int64)
             ref(bslab)
+            prog.append(int(rows > 0 and group_matrix_rows(g.par_ids)[1].size == 1))
             if use_tc and rows:
                 # per-launch kernels: enough super-rows to fill the SMs; the
                 # persistent kernels: full stacks (they split K instead)
