@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 17;
+constexpr int64_t kVersion = 18;
 
 struct Reader {
   const int64_t* p;
@@ -110,6 +110,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.window = r.get();
     L.n_prod = r.get();
     L.scratch_off = r.get();
+    L.flow_lo = r.get();
+    L.flow_hi = r.get();
     L.pad_rows = r.ref(&L.n_pad);
     int64_t ne = r.get();
     for (int64_t e = 0; e < ne && r.ok; ++e) {
@@ -216,6 +218,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->em_rest = r.ref();
   P->em_rest_start = r.ref();
   P->prod_flows_optional = (int)r.get();
+  P->fp_cover = (int)r.get();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -334,6 +337,13 @@ int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int 
   return PCB_OK;
 }
 
+// f_params[0, zero_tile) collects the padding edges' flows (param id 0)
+int64_t zero_tile(const pcb_plan* P) {
+  int64_t z = 0;
+  for (const Layer& L : P->layers) z = std::max(z, L.k_m * L.k_n);
+  return z;
+}
+
 int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
                    const float* theta, const float* values, float* flows, float* scratch_all,
                    float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
@@ -344,6 +354,12 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax, w.ratio);
     if (st) return st;
   }
+  // accumulating layers zero their own flow range first (fp_cover plans skip
+  // the whole-buffer memset)
+  if (P->fp_cover && L.flow_hi > L.flow_lo && !(tc && B > 0 && pf_layer_stores(P, L, B)) &&
+      cudaMemsetAsync(f_params + L.flow_lo, 0, sizeof(float) * (L.flow_hi - L.flow_lo), s) !=
+          cudaSuccess)
+    return PCB_CUDA;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
@@ -449,7 +465,9 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
   const Work w = carve(plan, ldb, d_work);
   {
     ProfScope prof_(KC_MISC, s);
-    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * plan->f_params_size, s) != cudaSuccess)
+    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * (plan->fp_cover ? zero_tile(plan)
+                                                                       : plan->f_params_size),
+                        s) != cudaSuccess)
       return PCB_CUDA;
     if (!B) return PCB_OK;
     // only rows that accumulate (several pushes) or receive none need zeros;

@@ -66,6 +66,7 @@ struct TcRows {
 
 struct Layer {
   int64_t k_m, k_n, window, n_prod;
+  int64_t flow_lo = 0, flow_hi = 0;  // the layer's f_params flow range (disjoint when fp_cover)
   int64_t scratch_off;  // first row of this layer's window in the all-layer scratch
   const int32_t* pad_rows;
   int64_t n_pad;
@@ -142,6 +143,10 @@ struct pcb_plan {
   int64_t scratch_rows = 1;      // all-layer scratch rows (sum of layer windows)
   int prod_rows_written = 0;     // every prod-flow row is stored by its first accumulation
   int prod_flows_optional = 0;   // every product row is accumulated + pushed in one layer
+  // f_params[:theta_size] is the zero tile, the stored pmf ranges of the
+  // staged inputs and disjoint per-layer flow ranges: the backward pass zeroes
+  // only the ranges of layers that accumulate (no whole-buffer memset)
+  int fp_cover = 0;
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
@@ -249,6 +254,7 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
                          const float* rmax, float* flow_scratch, float* gshift,
                          int32_t* counters, bool split_ok);
 bool pf_ws_supported(const Layer& L);
+bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
                          const float* scratch, float* f_params);

@@ -436,6 +436,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   if (warp == 1) tmem_free(tmem, 512);
 }
 
+// batch slices so small layers still cover the SMs; >= 2 chunks per slice
+int pf_kslices(int64_t count, int64_t cap, int kn, int B) {
+  const int64_t base = count * ((cap * kn + PF_N - 1) / PF_N) * 2;
+  const int nchunks = (B + PF_KS - 1) / PF_KS;
+  const int ks = (int)((2 * sm_count() + base - 1) / base);
+  return max(1, min(ks, nchunks / 2));
+}
+
 namespace {
 
 template <int KN, int RS>
@@ -453,10 +461,8 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   a.cgroups = (int)((a.cap * KN + PF_N - 1) / PF_N);
   a.mtiles = 2;  // super-rows hold <= 256 sums
   a.nchunks = (a.B + PF_KS - 1) / PF_KS;
-  // batch slices so small layers still cover the SMs; >= 2 chunks per slice
-  const int base = a.n_items * a.cgroups * a.mtiles;  // n_items holds the super-row count here
-  int ks = (2 * sm_count() + base - 1) / base;
-  a.kslices = max(1, min(ks, a.nchunks / 2));
+  a.kslices = pf_kslices(a.n_items, a.cap, KN, a.B);  // n_items holds the super-row count here
+  const int base = a.n_items * a.cgroups * a.mtiles;
   a.n_items = base * a.kslices;
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
   CUtensorMap tr, tR, te, tr128, tRt, te256;
@@ -477,6 +483,19 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
 bool pf_ws_supported(const Layer& L) {
   return (L.k_n == 16 || L.k_n == 32 || L.k_n == 64) && (L.k_m == 16 || L.k_m == 32 || L.k_m == 64);
 }
+
+// the layer's parameter flows are all plain stores at batch size B (so its
+// f_params range needs no zeroing)
+bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B) {
+  if (P->use_tc != 1 || !pf_ws_supported(L)) return false;
+  for (size_t g = 0; g < L.fwd.size(); ++g) {
+    const TcRows& T = L.pf_tc[g];
+    if (!T.count || !L.fwd[g].exclusive) return false;
+    if (pf_kslices(T.count, L.fwd[g].cap, (int)L.k_n, B) != 1) return false;
+  }
+  return true;
+}
+
 
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 17
+VERSION = 18
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -455,11 +455,49 @@ def build_program(compiled, *, tensor_cores: bool = True):
         f = folded(g.flow_ids)[g.param_ids != 0]
         return int(bool(np.all(fcnt[np.searchsorted(fu, f)] == 1))) if f.size else 1
 
+    # per-layer flow ranges and whether f_params[:theta_size] is covered by
+    # them, the staged (stored) input pmfs and the zero tile, all disjoint
+    layer_range, fp_cover = [], True
+    spans = []
+    for L in c.layers:
+        starts, sizes = [], []
+        for g in L.fwd_groups:
+            f = folded(g.flow_ids)[g.param_ids != 0]
+            starts.append(np.unique(f))
+        u = np.unique(np.concatenate(starts)) if starts else np.zeros(0, np.int64)
+        tsz = int(L.k_m * L.k_n)
+        if u.size:
+            lo, hi = int(u.min()), int(u.max()) + tsz
+            layer_range.append((lo, hi))
+            fp_cover = fp_cover and (hi - lo == u.size * tsz)  # tiles exactly tile it
+            spans.append((lo, hi))
+        else:
+            layer_range.append((0, 0))
+    if leftovers:
+        fp_cover = False
+    if nb:
+        # staged inputs store their whole pmf ranges
+        pid_sorted = np.sort(blocks["pids"])
+        ncat_of = np.repeat(blocks["ncat"], blocks["count"])
+        order = np.argsort(blocks["pids"], kind="stable")
+        for a0, n0 in zip(pid_sorted.tolist(), ncat_of[order].tolist()):
+            spans.append((int(a0), int(a0) + int(n0)))
+    zt = int(np.max([L.k_m * L.k_n for L in c.layers])) if c.layers else 0
+    spans.append((0, zt))
+    spans.sort()
+    pos = 0
+    for a0, b0 in spans:
+        if a0 != pos:
+            fp_cover = False
+            break
+        pos = b0
+    fp_cover = fp_cover and pos == c.theta_size
     n_tc_rows = 0
     scratch_off = 0
     prog.append(len(c.layers))
     for li, L in enumerate(c.layers):
-        prog += [L.k_m, L.k_n, L.scratch_window, int(L.prod_slots.size), scratch_off]
+        prog += [L.k_m, L.k_n, L.scratch_window, int(L.prod_slots.size), scratch_off,
+                 int(layer_range[li][0]), int(layer_range[li][1])]
         scratch_off += L.scratch_window
         use_tc = tensor_cores and tc_layer(L)
         written = np.concatenate([ev.out for ev in L.prod_evals]) if L.prod_evals else \
@@ -623,8 +661,9 @@ def build_program(compiled, *, tensor_cores: bool = True):
     contig[one] = gi[np.minimum(go[:-1][one], max(gi.size - 1, 0))]
     ref(contig[rest] if rest.size else np.zeros(0, np.int64))
     prog.append(int(pf_optional))
+    prog.append(int(fp_cover))
     prog.append(MAGIC)
-    info = {"prod_flows_optional": pf_optional, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+    info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
