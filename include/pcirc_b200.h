@@ -77,6 +77,17 @@ int pcb_theta_refresh(const pcb_plan* plan, void* stream, const float* d_theta);
  * rewrites the bf16 tensor-core planes (no separate pcb_theta_refresh). */
 int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta);
 
+/* Lean step mode (training steps that only consume the log-likelihood and
+ * f_params): when the first layer's products are single-child aliases of
+ * exclusively owned staged inputs (plan-detected), forward writes those
+ * inputs' log values straight into the product rows of the scratch and
+ * backward reads their flows straight from the product-flow rows, skipping
+ * that layer's product evaluation and flow push.  The aliased inputs' rows of
+ * d_values / d_flows and the aliased products' d_prod_flows rows are then not
+ * written.  Host-side setting read at launch time (also while a CUDA graph
+ * records); default 0. */
+int pcb_plan_set_lean(pcb_plan* plan, int lean);
+
 /* Validate a device batch (xT, [num_vars x ldb]) against the category counts:
  * writes the number of bad entries to *d_bad (device int32).
  * Replaces: pcirc/runtime/engine.py:36-52 (_validate_batch) for device batches. */

@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 18;
+constexpr int64_t kVersion = 19;
 
 struct Reader {
   const int64_t* p;
@@ -98,6 +98,11 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->in_blocks.pids = r.ref();
   P->in_blocks.max_elems = r.get();
   P->in_blocks.max_ncat = r.get();
+  P->in_blocks.max_count = r.get();
+  P->in_blocks.alias_row = r.ref();
+  P->in_blocks.alias_dir = r.ref();
+  P->leaf_alias = (int)r.get();
+  P->alias_pad = r.ref(&P->n_alias_pad);
   P->n_zero = r.get();
   P->zero_start = r.ref();
   P->zero_len = r.ref();
@@ -246,6 +251,12 @@ int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta) {
   return PCB_OK;
 }
 
+int pcb_plan_set_lean(pcb_plan* plan, int lean) {
+  if (!plan) return PCB_USAGE;
+  plan->lean = lean ? 1 : 0;
+  return PCB_OK;
+}
+
 int pcb_theta_refresh(const pcb_plan* plan, void* stream, const float* d_theta) {
   if (!plan) return PCB_USAGE;
   return launch_theta_to_mma(plan, as_stream(stream), d_theta);
@@ -314,13 +325,26 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   return w;
 }
 
+// the layer's products alias their inputs in this (lean) step
+bool lean_alias(const pcb_plan* P, const Layer& L) {
+  return P->lean && P->leaf_alias && &L == &P->layers[0];
+}
+
 // Products of every layer stay resident in their own window of the
 // all-layer scratch, so the backward pass reads them instead of recomputing
 // (the reference recomputes into one shared window, engine.py:242).
 int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
                   const float* theta, float* values, float* scratch_all, const Work& w) {
   float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
-  int st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);
+  int st;
+  if (lean_alias(P, L)) {
+    // the input pass wrote the product rows and block maxima: only the
+    // window's padding rows / blocks need -inf
+    st = launch_fill(s, L.pad_rows, L.n_pad, B, ldb, scratch, PCB_NEG_INF);
+    if (!st) st = launch_fill(s, P->alias_pad, P->n_alias_pad, B, ldb, w.bmax, PCB_NEG_INF);
+  } else {
+    st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);
+  }
   if (st) return st;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.fwd_tc[g];
@@ -388,6 +412,8 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
                                   flow_scratch);
     if (st) return st;
   }
+  // aliased leaf products: the input pass reads their flow rows directly
+  if (lean_alias(P, L)) return PCB_OK;
   return launch_prod_accum_push(L, s, B, ldb, flow_scratch, prod_flows, flows);
 }
 
@@ -446,7 +472,7 @@ int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_
   // rows included) is written below, so only the reserved constant rows need it.
   int st = launch_fill_range(s, 0, plan->reserved, B, ldb, d_values, PCB_NEG_INF);
   if (st) return st;
-  st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values);
+  st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values, d_scratch, w.bmax);
   if (st) return st;
   for (auto& L : plan->layers) {
     st = layer_forward(plan, L, s, B, ldb, d_theta, d_values, d_scratch, w);
@@ -487,7 +513,8 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
                         d_flow_scratch, d_prod_flows, d_f_params, w);
     if (st) return st;
   }
-  st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_f_params);
+  st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch,
+                                d_f_params);
   if (st) return st;
   return launch_replica_reduce(plan, s, d_f_params);
 }

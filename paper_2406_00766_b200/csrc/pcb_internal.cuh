@@ -27,9 +27,12 @@ struct InputChunk {
 // consecutive value slots from slot0 on variable var, each with an exclusive
 // pmf of ncat entries starting at pids[pid_off + i].
 struct InBlocks {
-  int64_t n = 0, max_elems = 0, max_ncat = 0;
+  int64_t n = 0, max_elems = 0, max_ncat = 0, max_count = 0;
   const int32_t *var = nullptr, *ncat = nullptr, *slot0 = nullptr, *count = nullptr,
                 *pid_off = nullptr, *pids = nullptr;
+  // leaf aliases (plan.leaf_alias): first product row of the block's inputs
+  // in the first layer's window (-1: not aliased) and the row step (+1 / -1)
+  const int32_t *alias_row = nullptr, *alias_dir = nullptr;
 };
 
 struct Bucket {  // product evaluation or push bucket
@@ -147,6 +150,11 @@ struct pcb_plan {
   // staged inputs and disjoint per-layer flow ranges: the backward pass zeroes
   // only the ranges of layers that accumulate (no whole-buffer memset)
   int fp_cover = 0;
+  // the first layer's products alias their staged inputs (pcb_plan_set_lean)
+  int leaf_alias = 0;
+  int64_t n_alias_pad = 0;
+  const int32_t* alias_pad = nullptr;  // pad blocks of the first layer's window
+  int lean = 0;
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
@@ -193,7 +201,7 @@ int check_launch();
 
 // SIMT kernels (pcb_simt.cu)
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
-                     const float* theta, float* values);
+                     const float* theta, float* values, float* scratch_all, float* bmax);
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
                      float* scratch, float* bmax);
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
@@ -210,7 +218,7 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows);
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
-                             float* f_params);
+                             const float* flow_scratch, float* f_params);
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
                     float* lroot);
 int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,

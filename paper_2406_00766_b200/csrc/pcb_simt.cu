@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(IN_THREADS)
                       const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
                       const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
                       const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
-                      const float* __restrict__ theta, float* __restrict__ values) {
+                      const float* __restrict__ theta, float* __restrict__ values,
+                      const int32_t* __restrict__ arow, const int32_t* __restrict__ adir,
+                      float* __restrict__ ascratch, float* __restrict__ abmax, int kn) {
   extern __shared__ float tbl[];
   const int blk = blockIdx.x;
   const int ncat = bncat[blk], cnt = bcount[blk], var = bvar[blk];
@@ -169,6 +171,29 @@ __global__ void __launch_bounds__(IN_THREADS)
     }
   }
   __syncthreads();
+  const int r0 = arow ? __ldg(arow + blk) : -1;
+  if (r0 >= 0) {
+    // leaf alias (lean step): the inputs' log values are the product rows of
+    // the first layer's window (row r0 + dir * i); whole product blocks, so
+    // the block maxima the sum kernels shift by are formed here
+    const int64_t step = (int64_t)__ldg(adir + blk) * ldb;
+    for (int b = threadIdx.x; b < B; b += IN_THREADS) {
+      const int x = xT[(int64_t)var * ldb + b];
+      const float* t = tbl + (x < 0 ? 0 : x);
+      float* dst = ascratch + (int64_t)r0 * ldb + b;
+      for (int i0 = 0; i0 < cnt; i0 += kn) {
+        float mx = PCB_NEG_INF;
+#pragma unroll 8
+        for (int i = i0; i < i0 + kn; ++i) {
+          const float v = x < 0 ? 0.f : t[i * ncat];
+          dst[i * step] = v;
+          mx = fmaxf(mx, v);
+        }
+        abmax[(int64_t)((r0 + (step > 0 ? i0 : -i0)) / kn) * ldb + b] = mx;
+      }
+    }
+    return;
+  }
   for (int b = threadIdx.x; b < B; b += IN_THREADS) {
     const int x = xT[(int64_t)var * ldb + b];
     float* dst = values + slot0 * ldb + b;
@@ -182,7 +207,7 @@ __global__ void __launch_bounds__(IN_THREADS)
 }
 
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
-                     const float* theta, float* values) {
+                     const float* theta, float* values, float* scratch_all, float* bmax) {
   ProfScope prof_(KC_INPUT_FWD, s);
   const InBlocks& ib = p->in_blocks;
   if (ib.n) {
@@ -194,8 +219,13 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
         return PCB_CUDA;
       attr = bytes;
     }
+    const bool alias = p->lean && p->leaf_alias;
+    const Layer* L0 = alias ? &p->layers[0] : nullptr;
     k_input_fwd_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
-        B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, values);
+        B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, values,
+        alias ? ib.alias_row : nullptr, ib.alias_dir,
+        alias ? scratch_all + L0->scratch_off * (int64_t)ldb : nullptr, bmax,
+        alias ? (int)L0->k_n : 1);
     if (check_launch()) return PCB_CUDA;
   }
   for (auto& c : p->inputs) {
@@ -825,7 +855,8 @@ __global__ void __launch_bounds__(IN_THREADS)
                        const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
                        const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
                        const float* __restrict__ theta, const float* __restrict__ flows,
-                       float* __restrict__ f_params) {
+                       const int32_t* __restrict__ arow, const int32_t* __restrict__ adir,
+                       const float* __restrict__ aflows, float* __restrict__ f_params) {
   extern __shared__ float hist[];
   __shared__ float miss[128];
   const int blk = blockIdx.x;
@@ -835,15 +866,19 @@ __global__ void __launch_bounds__(IN_THREADS)
   for (int q = threadIdx.x; q < cnt * ncat; q += IN_THREADS) hist[q] = 0.f;
   for (int q = threadIdx.x; q < cnt; q += IN_THREADS) miss[q] = 0.f;
   __syncthreads();
+  // input i's flow row: flows[slot0 + i], or the aliased product-flow row
+  const int r0 = arow ? __ldg(arow + blk) : -1;
+  const float* fbase = r0 >= 0 ? aflows + (int64_t)r0 * ldb : flows + slot0 * ldb;
+  const int64_t fstep = r0 >= 0 ? (int64_t)__ldg(adir + blk) * ldb : (int64_t)ldb;
   for (int b = threadIdx.x; b < B; b += IN_THREADS) {
     const int x = xT[(int64_t)var * ldb + b];
-    const float* src = flows + slot0 * ldb + b;
+    const float* src = fbase + b;
     float* row = (x < 0) ? miss : hist + x;
     const int step = (x < 0) ? 1 : ncat;
     for (int i0 = 0; i0 < cnt; i0 += 8) {
       float f[8];  // 8 independent loads in flight before the smem atomics
 #pragma unroll
-      for (int u = 0; u < 8; ++u) f[u] = (i0 + u < cnt) ? src[(int64_t)(i0 + u) * ldb] : 0.f;
+      for (int u = 0; u < 8; ++u) f[u] = (i0 + u < cnt) ? src[(i0 + u) * fstep] : 0.f;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         if (f[u] != 0.f) atomicAdd(row + (i0 + u) * step, f[u]);
@@ -873,7 +908,8 @@ __global__ void __launch_bounds__(IS_THREADS)
                         const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
                         const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
                         const float* __restrict__ theta, const float* __restrict__ flows,
-                        float* __restrict__ f_params) {
+                        const int32_t* __restrict__ arow, const int32_t* __restrict__ adir,
+                        const float* __restrict__ aflows, float* __restrict__ f_params) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
   const int blk = blockIdx.x;
   const int ncat = __ldg(bncat + blk), cnt = __ldg(bcount + blk), var = __ldg(bvar + blk);
@@ -920,8 +956,12 @@ __global__ void __launch_bounds__(IS_THREADS)
   __syncthreads();
   float* row = rowbuf + warp * ldb;
   const int m0 = start[ncat], m1 = start[nb];
+  // input i's flow row: flows[slot0 + i], or the aliased product-flow row
+  const int r0 = arow ? __ldg(arow + blk) : -1;
+  const float* fbase = r0 >= 0 ? aflows + (int64_t)r0 * ldb : flows + slot0 * ldb;
+  const int64_t fstep = r0 >= 0 ? (int64_t)__ldg(adir + blk) * ldb : (int64_t)ldb;
   for (int i = warp; i < cnt; i += IS_WARPS) {
-    const float4* src = reinterpret_cast<const float4*>(flows + (slot0 + i) * ldb);
+    const float4* src = reinterpret_cast<const float4*>(fbase + i * fstep);
     for (int q0 = lane; q0 < ldb / 4; q0 += 128) {  // 4 loads in flight per lane
       float4 v[4];
 #pragma unroll
@@ -948,9 +988,10 @@ __global__ void __launch_bounds__(IS_THREADS)
 
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
-                             float* f_params) {
+                             const float* flow_scratch, float* f_params) {
   ProfScope prof_(KC_INPUT_FLOW, s);
   const InBlocks& ib = p->in_blocks;
+  const int32_t* arow = (p->lean && p->leaf_alias) ? ib.alias_row : nullptr;
   // sorted (atomic-free) kernel when its shared-memory slots fit, else the
   // shared-memory histogram
   const int64_t sorted_bytes = ((int64_t)IS_WARPS * ldb + 2 * (ib.max_ncat + 1) + 1 + B) * 4;
@@ -965,7 +1006,7 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
     }
     k_input_flow_sorted<<<(unsigned)ib.n, IS_THREADS, (size_t)sorted_bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
-        f_params);
+        arow, ib.alias_dir, flow_scratch, f_params);
     if (check_launch()) return PCB_CUDA;
   } else if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
@@ -978,7 +1019,7 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
     }
     k_input_flow_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
-        f_params);
+        arow, ib.alias_dir, flow_scratch, f_params);
     if (check_launch()) return PCB_CUDA;
   }
   for (auto& c : p->inputs) {

@@ -41,8 +41,12 @@ constexpr int PF_N = 256;          // child columns per item
 constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzled box row)
 constexpr int PF_CH = PF_KS / 4;   // 16-byte chunks per box row
 constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
-constexpr int PF_THREADS = 448;    // 14 warps
-constexpr int PF_CONV0 = 2, PF_NCONV = 8, PF_EPI0 = 10;
+#ifndef PCB_PF_NCONV
+#define PCB_PF_NCONV 8
+#endif
+// warps: producer, MMA, converters, 4 epilogue
+constexpr int PF_CONV0 = 2, PF_NCONV = PCB_PF_NCONV, PF_EPI0 = PF_CONV0 + PF_NCONV;
+constexpr int PF_THREADS = (PF_EPI0 + 4) * 32;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
 
 struct PfArgs {
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
   } else if (warp < PF_EPI0) {
     // ------------------------------------------------------------ converters
-    const int t = tid - PF_CONV0 * 32;  // 0..255
+    const int t = tid - PF_CONV0 * 32;  // 0..PF_NCONV*32-1
     Ring rr(C::kRS), orr(C::kOS);
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const PfItem it = pf_item(a, item);

@@ -7,6 +7,7 @@ runtime entry point raises.  ``build()`` in ``__graft_entry__`` (or
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from ..errors import PcircError, raise_for_status
@@ -28,6 +29,7 @@ SIGNATURES = {
     "pcb_plan_set_mma": (_I, [_P, _P, _L]),
     "pcb_theta_refresh": (_I, [_P, _P, _P]),
     "pcb_plan_set_theta": (_I, [_P, _P]),
+    "pcb_plan_set_lean": (_I, [_P, _I]),
     "pcb_tc_selftest_mn": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "pcb_check_batch": (_I, [_P, _P, _I, _I, _P, _P]),
     "pcb_transpose_batch_i64": (_I, [_P, _P, _I, _I, _P, _P]),
@@ -56,7 +58,8 @@ def load(path: Path | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # PCB_LIB: an alternative build of the same library (kernel A/B experiments)
+    p = Path(path) if path else Path(os.environ.get("PCB_LIB") or LIB_PATH)
     if not p.exists():
         raise PcircError(
             f"CUDA library {p} is not built; run __graft_entry__.build() "

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 18
+VERSION = 19
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -236,6 +236,57 @@ def input_blocks(compiled):
     return arrays, leftovers
 
 
+def leaf_alias(compiled, blocks, push_count):
+    """Leaf products that are aliases of their one input child.
+
+    When every product of the first layer has a single child, that child is a
+    staged input whose only parent is the product, and each staged input block
+    maps onto whole product blocks of the layer window as one ascending or
+    descending run, a lean step (``pcb_plan_set_lean``) writes the inputs' log
+    values straight into the product rows (plus the block maxima the sum
+    kernels shift by) and reads the inputs' flows straight from the product
+    flow rows: the product evaluation and the flow push of that layer vanish.
+    Returns (per-block first product row or -1, per-block row step,
+    window pad blocks or None when the layer does not qualify).
+    """
+    nb = int(blocks["var"].size)
+    arow = np.full(nb, -1, dtype=np.int64)
+    adir = np.ones(nb, dtype=np.int64)
+    none = (np.full(nb, -1, dtype=np.int64), adir, None)
+    if not compiled.layers or nb == 0:
+        return none
+    L = compiled.layers[0]
+    if not L.prod_evals or any(ev.children.shape[1] != 1 for ev in L.prod_evals):
+        return none
+    out = np.concatenate([ev.out for ev in L.prod_evals]).astype(np.int64)
+    ch = np.concatenate([ev.children[:, 0] for ev in L.prod_evals]).astype(np.int64)
+    if np.unique(ch).size != ch.size or np.any(push_count[ch] != 1):
+        return none
+    row_of = np.full(compiled.num_value_slots, -1, dtype=np.int64)
+    row_of[ch] = out
+    kn = int(L.k_n)
+    covered = 0
+    for b in range(nb):
+        s0, n = int(blocks["slot0"][b]), int(blocks["count"][b])
+        r = row_of[s0:s0 + n]
+        if np.all(r < 0):
+            continue
+        if np.any(r < 0) or n % kn:
+            return none
+        d = int(r[1] - r[0]) if n > 1 else 1
+        if d not in (1, -1) or np.any(np.diff(r) != d) or int(r.min()) % kn:
+            return none
+        arow[b], adir[b] = int(r[0]), d
+        covered += n
+    if covered != out.size:
+        return none
+    pad = np.setdiff1d(np.arange(L.scratch_window, dtype=np.int64), out)
+    pad_blk = np.unique(pad // kn)
+    if pad.size != pad_blk.size * kn:
+        return none
+    return arow, adir, pad_blk
+
+
 def group_runs(group_idx, group_off):
     """Run-length encode the simplex-group index table: maximal runs of
     consecutive theta indices inside each group.  Returns (per-group run
@@ -372,7 +423,18 @@ def build_program(compiled, *, tensor_cores: bool = True):
     scratch_total = int(sum(L.scratch_window for L in c.layers)) or 1
     prog.append(scratch_total)
 
+    # pushes per value slot over the whole backward pass (root pushes included):
+    # a slot with exactly one push takes a plain store instead of an atomic add
+    push_count = np.zeros(c.num_value_slots, dtype=np.int64)
+    for L in c.layers:
+        for p in L.pushes:
+            np.add.at(push_count, p.children.ravel(), 1)
+    if c.root_children is not None and c.root_row >= 0:
+        # the root pass adds into these rows: never a single plain store
+        np.add.at(push_count, np.asarray(c.root_children, dtype=np.int64), 2)
+
     blocks, leftovers = input_blocks(c)
+    alias_row, alias_dir, alias_pad = leaf_alias(c, blocks, push_count)
     prog.append(len(leftovers))
     for ncat, slots, vars_, pids in leftovers:
         prog += [ncat, int(slots.size)]
@@ -385,16 +447,11 @@ def build_program(compiled, *, tensor_cores: bool = True):
         ref(blocks[key])
     prog.append(int((blocks["ncat"] * blocks["count"]).max()) if nb else 0)
     prog.append(int(blocks["ncat"].max()) if nb else 0)
-
-    # pushes per value slot over the whole backward pass (root pushes included):
-    # a slot with exactly one push takes a plain store instead of an atomic add
-    push_count = np.zeros(c.num_value_slots, dtype=np.int64)
-    for L in c.layers:
-        for p in L.pushes:
-            np.add.at(push_count, p.children.ravel(), 1)
-    if c.root_children is not None and c.root_row >= 0:
-        # the root pass adds into these rows: never a single plain store
-        np.add.at(push_count, np.asarray(c.root_children, dtype=np.int64), 2)
+    prog.append(int(blocks["count"].max()) if nb else 0)
+    ref(alias_row)
+    ref(alias_dir)
+    prog.append(1 if alias_pad is not None else 0)
+    ref(alias_pad if alias_pad is not None else np.zeros(0, np.int64))
     # flow rows the backward pass must zero first: all but the single-store rows
     need = push_count != 1
     if c.num_value_slots:
@@ -663,7 +720,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
     prog.append(int(pf_optional))
     prog.append(int(fp_cover))
     prog.append(MAGIC)
-    info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+    info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
+            "leaf_alias": alias_pad is not None, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info

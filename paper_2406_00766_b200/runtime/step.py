@@ -50,13 +50,19 @@ class TrainStep:
         s = _lib.stream_handle()  # the capture stream while a graph records
         _lib.call("pcb_transpose_batch_i32", p.handle, s, self.B, b.ldb, x.data_ptr(),
                   b.xT.data_ptr())
-        _lib.call("pcb_forward", p.handle, s, self.B, b.ldb, b.xT.data_ptr(),
-                  p.theta.data_ptr(), b.values_full.data_ptr(), b.scratch_full.data_ptr(),
-                  b.lroot.data_ptr(), b.work.data_ptr())
-        _lib.call("pcb_backward", p.handle, s, self.B, b.ldb, b.xT.data_ptr(),
-                  p.theta.data_ptr(), b.values_full.data_ptr(), b.flows_full.data_ptr(),
-                  b.scratch_full.data_ptr(), b.flow_scratch_full.data_ptr(),
-                  self._pf_ptr, b.f_params.data_ptr(), b.work.data_ptr())
+        # lean launches: the step never reads node values / flows, so aliased
+        # leaf products skip their evaluation and push (pcb_plan_set_lean)
+        _lib.call("pcb_plan_set_lean", p.handle, 1)
+        try:
+            _lib.call("pcb_forward", p.handle, s, self.B, b.ldb, b.xT.data_ptr(),
+                      p.theta.data_ptr(), b.values_full.data_ptr(), b.scratch_full.data_ptr(),
+                      b.lroot.data_ptr(), b.work.data_ptr())
+            _lib.call("pcb_backward", p.handle, s, self.B, b.ldb, b.xT.data_ptr(),
+                      p.theta.data_ptr(), b.values_full.data_ptr(), b.flows_full.data_ptr(),
+                      b.scratch_full.data_ptr(), b.flow_scratch_full.data_ptr(),
+                      self._pf_ptr, b.f_params.data_ptr(), b.work.data_ptr())
+        finally:
+            _lib.call("pcb_plan_set_lean", p.handle, 0)
         ll = b.lroot.double().sum()
         if self.allreduce is not None:
             self.allreduce(b.f_params, ll)

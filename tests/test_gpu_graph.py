@@ -46,3 +46,38 @@ def test_graph_step_matches_eager_and_oracle():
         assert abs(ll_g[i] - lr.sum()) <= 1e-4 * abs(lr.sum())
     nz = np.abs(theta) > 1e-6
     assert np.max(np.abs(th_g[nz] - theta[nz]) / np.abs(theta[nz])) < 1e-4
+
+
+@pytest.mark.parametrize("tensor_cores", [True, False])
+@pytest.mark.parametrize("k", [16, 32])
+def test_lean_step_matches_full(tensor_cores, k):
+    """Lean launches (leaf products aliased onto their inputs: no leaf product
+    pass, no leaf push) give bit-identical log-likelihoods and the same
+    parameter flows, missing values included (flows agree to float rounding:
+    product flows with several parent blocks are accumulated atomically, so
+    their summation order varies from run to run in either mode)."""
+    import torch
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.runtime import _lib, backward, forward
+    from paper_2406_00766_b200.runtime.plan import device_plan
+    g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=30, hidden_dim=2 * k,
+                                       num_categories=8, seed=5))
+    c = compile_circuit(g, CompileConfig(block_size=k))
+    plan = device_plan(c, tensor_cores=tensor_cores)
+    assert plan.info["leaf_alias"]
+    x = np.random.default_rng(3).integers(0, 8, size=(200, 30))
+    x[np.random.default_rng(4).random(x.shape) < 0.15] = -1
+    lr0, b0 = forward(c, x, tensor_cores=tensor_cores)
+    backward(c, b0, tensor_cores=tensor_cores)
+    want_ll, want_f = lr0.clone(), b0.f_params.clone()
+    _lib.call("pcb_plan_set_lean", plan.handle, 1)
+    try:
+        lr1, b1 = forward(c, x, tensor_cores=tensor_cores)
+        backward(c, b1, tensor_cores=tensor_cores)
+        torch.cuda.synchronize()
+    finally:
+        _lib.call("pcb_plan_set_lean", plan.handle, 0)
+    assert torch.equal(lr1, want_ll)
+    got, ref = b1.f_params.double(), want_f.double()
+    assert torch.max(torch.abs(got - ref) / torch.clamp(ref.abs(), min=1e-30)).item() < 2e-6

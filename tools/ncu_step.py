@@ -23,6 +23,8 @@ def main():
     bufs = allocate_buffers(c, B, plan=plan)
     x = torch.from_numpy(bench.synthetic_batches(c, w, B, 1, 0)[0]).cuda()
     s = _lib.stream_handle()
+    pf = 0 if plan.info.get("prod_flows_optional") else bufs.prod_flows_full.data_ptr()
+    _lib.call("pcb_plan_set_lean", plan.handle, 1)  # as runtime.step.TrainStep
     for _ in range(steps):
         _lib.call("pcb_transpose_batch_i32", plan.handle, s, B, bufs.ldb, x.data_ptr(),
                   bufs.xT.data_ptr())
@@ -32,7 +34,7 @@ def main():
         _lib.call("pcb_backward", plan.handle, s, B, bufs.ldb, bufs.xT.data_ptr(),
                   plan.theta.data_ptr(), bufs.values_full.data_ptr(), bufs.flows_full.data_ptr(),
                   bufs.scratch_full.data_ptr(), bufs.flow_scratch_full.data_ptr(),
-                  bufs.prod_flows_full.data_ptr(), bufs.f_params.data_ptr(),
+                  pf, bufs.f_params.data_ptr(),
                   bufs.work.data_ptr())
         em_update_(c, bufs.f_params, pseudocount=1e-6, step_size=0.01, check=False, plan=plan)
     torch.cuda.synchronize()
