@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 19;
+constexpr int64_t kVersion = 20;
 
 struct Reader {
   const int64_t* p;
@@ -195,6 +195,16 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.push_flag = r.ref();
     L.push_off = r.ref();
     L.push_ch = r.ref();
+    L.n_pblk = r.get();
+    L.pb_row = r.ref();
+    L.pb_f = r.ref();
+    L.pb_qoff = r.ref();
+    L.q_blk = r.ref(&L.n_pq);
+    L.q_base = r.ref();
+    L.q_kind = r.ref();
+    L.q_rrow = r.ref();
+    L.pre_ratio = (int)r.get();
+    L.rmax_off = r.get();
     L.n_pb = L.window / L.k_n;  // including the -inf pad block 0
     if (L.n_pb > P->max_pb) P->max_pb = L.n_pb;
     if (L.n_sb > P->max_sb) P->max_sb = L.n_sb;
@@ -224,9 +234,22 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->em_rest_start = r.ref();
   P->prod_flows_optional = (int)r.get();
   P->fp_cover = (int)r.get();
+  P->n_rmax = r.get();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
+  }
+  // the fused push may pre-compute a layer's flow ratios only if that layer's
+  // flow kernels are the persistent tensor-core ones (they read ratio rows,
+  // never flows)
+  P->push_ratio_ok = P->use_tc == 1 && P->n_rmax > 0;
+  for (const Layer& L : P->layers) {
+    if (!L.pre_ratio) continue;
+    bool ok = tc_bwd_supported(L) && ws_supported((int)L.k_m, (int)L.k_n) && pf_ws_supported(L) &&
+              L.k_m <= 64 && (L.k_n == 16 || L.k_n == 32 || L.k_n == 64);
+    for (size_t g = 0; g < L.pf_tc.size(); ++g) ok = ok && L.pf_tc[g].count > 0;
+    for (size_t g = 0; g < L.bwd_tc.size(); ++g) ok = ok && L.bwd_tc[g].count > 0;
+    if (!ok) P->push_ratio_ok = 0;
   }
   *out = P;
   return PCB_OK;
@@ -321,7 +344,8 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.rmax = d_work + P->max_pb * (int64_t)ldb;
   w.ratio = w.rmax + P->max_sb * (int64_t)ldb;
   w.gshift = w.ratio + P->max_sum_rows * (int64_t)ldb;
-  w.counters = reinterpret_cast<int32_t*>(w.gshift + P->max_tc_rows * (int64_t)ldb);
+  w.rmax_all = w.gshift + P->max_tc_rows * (int64_t)ldb;
+  w.counters = reinterpret_cast<int32_t*>(w.rmax_all + P->n_rmax * (int64_t)ldb);
   return w;
 }
 
@@ -374,7 +398,14 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
   int st = PCB_OK;
   const bool tc = P->use_tc && tc_bwd_supported(L);
-  if (tc) {
+  const bool fused = P->lean && P->push_ratio_ok;
+  // pre-ratioed layers (fused push): the flow rows already hold the ratios
+  const float* ratio = w.ratio;
+  const float* rmax = w.rmax;
+  if (fused && L.pre_ratio) {
+    ratio = flows + L.sb_base * (int64_t)ldb;
+    rmax = w.rmax_all + L.rmax_off * (int64_t)ldb;
+  } else if (tc) {
     st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax, w.ratio);
     if (st) return st;
   }
@@ -388,7 +419,7 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
       st = (P->use_tc == 1 && pf_ws_supported(L))
-               ? launch_param_flow_ws(L, L.fwd[g], T, s, B, ldb, theta, w.ratio, w.rmax, scratch,
+               ? launch_param_flow_ws(L, L.fwd[g], T, s, B, ldb, theta, ratio, rmax, scratch,
                                       f_params)
                : launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
                                       w.rmax, f_params);
@@ -403,7 +434,7 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
       st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
                ? launch_child_flow_ws(P, L, L.bwd[g],
                                       ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T, s, B, ldb,
-                                      w.ratio, scratch, w.rmax, flow_scratch, w.gshift,
+                                      ratio, scratch, rmax, flow_scratch, w.gshift,
                                       w.counters, L.bwd.size() == 1)
                : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
                                       w.rmax, flow_scratch);
@@ -414,6 +445,8 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   }
   // aliased leaf products: the input pass reads their flow rows directly
   if (lean_alias(P, L)) return PCB_OK;
+  if (fused && L.n_pblk)
+    return launch_push_ratio(L, s, B, ldb, flow_scratch, values, flows, w.rmax_all);
   return launch_prod_accum_push(L, s, B, ldb, flow_scratch, prod_flows, flows);
 }
 
@@ -457,7 +490,8 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
   // + one split-K arrival counter per (super-row, 128-sample tile)
-  return (plan->max_pb + plan->max_sb + plan->max_sum_rows + plan->max_tc_rows) * (int64_t)ldb +
+  return (plan->max_pb + plan->max_sb + plan->max_sum_rows + plan->max_tc_rows + plan->n_rmax) *
+             (int64_t)ldb +
          plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }
 

@@ -89,6 +89,15 @@ struct Layer {
   // fused accumulate + push, product order: flag bit0 push, bit1 first
   // accumulation (store); push_ch = slot * 2 + (single push into the slot)
   const int32_t *push_flag, *push_off, *push_ch;
+  // fused push + flow ratio (lean steps, plan.push_ratio_tables): blocks of
+  // k products (flow-scratch rows pb_row..+k, fan-in pb_f); per fan-in slot q
+  // (pb_qoff..): child base slot, kind (0: flow store, 1: ratio of a
+  // pre-ratioed sum block, its R row at q_rrow)
+  int64_t n_pblk = 0, n_pq = 0;  // push blocks, fan-in slots
+  const int32_t *pb_row = nullptr, *pb_f = nullptr, *pb_qoff = nullptr, *q_blk = nullptr,
+                *q_base = nullptr, *q_kind = nullptr, *q_rrow = nullptr;
+  int pre_ratio = 0;     // every sum block's ratio comes from a fused push
+  int64_t rmax_off = -1;  // its R rows in the all-layer rmax region
 };
 
 // Workspace carved from the caller's d_work buffer (pcb_plan_workspace_floats):
@@ -103,6 +112,7 @@ struct Work {
   float* rmax;
   float* ratio;
   float* gshift;
+  float* rmax_all;  // [n_rmax x ldb] R rows of the pre-ratioed layers
   int32_t* counters;
 };
 
@@ -152,6 +162,10 @@ struct pcb_plan {
   int fp_cover = 0;
   // the first layer's products alias their staged inputs (pcb_plan_set_lean)
   int leaf_alias = 0;
+  // fused push + ratio usable (every pre-ratioed layer runs the persistent
+  // tensor-core flow kernels, which read ratio rows only)
+  int push_ratio_ok = 0;
+  int64_t n_rmax = 0;
   int64_t n_alias_pad = 0;
   const int32_t* alias_pad = nullptr;  // pad blocks of the first layer's window
   int lean = 0;
@@ -206,6 +220,8 @@ int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float
                      float* scratch, float* bmax);
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
                      const float* flows, float* rmax, float* ratio);
+int launch_push_ratio(const Layer& L, cudaStream_t s, int B, int ldb, const float* flow_scratch,
+                      const float* values, float* flows, float* rmax_all);
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                         const float* theta, const float* scratch, float* values);
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,

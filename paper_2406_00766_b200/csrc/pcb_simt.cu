@@ -451,6 +451,99 @@ int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float
   return check_launch();
 }
 
+// Fused flow push + flow ratio (lean steps): one CTA per (fan-in slot of a
+// push block of K products, 128-sample slab).  The slot's K children are
+// consecutive single-push slots: either plain flow stores of the block's K
+// product flows, or one whole sum block of a pre-ratioed layer, whose ratio
+// rows r (k_ratio's arithmetic, bit for bit) overwrite the flow rows and
+// whose shift R goes to its rmax_all row.  Replaces the push's flow stores
+// plus the ratio pass's re-read of flows and values.  The block's product
+// flows are read once per slot (the slots of a block are adjacent CTAs: L2).
+template <int K>
+__global__ void __launch_bounds__(RW * 32)
+    k_push_ratio(int B, int ldb, const int32_t* __restrict__ qblk,
+                 const int32_t* __restrict__ prow, const int32_t* __restrict__ qbase,
+                 const int32_t* __restrict__ qkind, const int32_t* __restrict__ qrrow,
+                 const float* __restrict__ fs, const float* __restrict__ values,
+                 float* __restrict__ flows, float* __restrict__ rmax_all) {
+  constexpr int PER = (K + RW - 1) / RW;
+  const int q = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.y * SLAB + lane * VB;
+  const bool live = b < B;
+  const float ninf = PCB_NEG_INF;
+  const int64_t r0 = __ldg(prow + __ldg(qblk + q)), cb = __ldg(qbase + q);
+  const bool ratio = __ldg(qkind + q) != 0;
+  float4 p[PER], l[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int m = warp + u * RW;
+    p[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    l[u] = make_float4(ninf, ninf, ninf, ninf);
+    if (live && m < K) {
+      p[u] = *reinterpret_cast<const float4*>(fs + (r0 + m) * ldb + b);
+      if (ratio) l[u] = *reinterpret_cast<const float4*>(values + (cb + m) * ldb + b);
+    }
+  }
+  if (!ratio) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int m = warp + u * RW;
+      if (live && m < K) *reinterpret_cast<float4*>(flows + (cb + m) * ldb + b) = p[u];
+    }
+    return;
+  }
+  float4 mx = make_float4(ninf, ninf, ninf, ninf);
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {  // p <- lg2 f (k_ratio's t)
+    p[u].x = (l[u].x == ninf || !(p[u].x > 0.f)) ? ninf : __log2f(p[u].x);
+    p[u].y = (l[u].y == ninf || !(p[u].y > 0.f)) ? ninf : __log2f(p[u].y);
+    p[u].z = (l[u].z == ninf || !(p[u].z > 0.f)) ? ninf : __log2f(p[u].z);
+    p[u].w = (l[u].w == ninf || !(p[u].w > 0.f)) ? ninf : __log2f(p[u].w);
+    if (p[u].x != ninf) mx.x = fmaxf(mx.x, p[u].x - l[u].x * kLog2e);
+    if (p[u].y != ninf) mx.y = fmaxf(mx.y, p[u].y - l[u].y * kLog2e);
+    if (p[u].z != ninf) mx.z = fmaxf(mx.z, p[u].z - l[u].z * kLog2e);
+    if (p[u].w != ninf) mx.w = fmaxf(mx.w, p[u].w - l[u].w * kLog2e);
+  }
+  __shared__ float4 red[RW][32];
+  red[warp][lane] = mx;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < RW; ++w) mx = f4max(mx, red[w][lane]);
+  if (!live) return;
+  if (warp == 0) *reinterpret_cast<float4*>(rmax_all + (int64_t)__ldg(qrrow + q) * ldb + b) = mx;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int m = warp + u * RW;
+    if (m < K) {
+      float4 r;
+      r.x = (p[u].x == ninf) ? ninf : p[u].x - fmaf(l[u].x, kLog2e, mx.x);
+      r.y = (p[u].y == ninf) ? ninf : p[u].y - fmaf(l[u].y, kLog2e, mx.y);
+      r.z = (p[u].z == ninf) ? ninf : p[u].z - fmaf(l[u].z, kLog2e, mx.z);
+      r.w = (p[u].w == ninf) ? ninf : p[u].w - fmaf(l[u].w, kLog2e, mx.w);
+      *reinterpret_cast<float4*>(flows + (cb + m) * ldb + b) = r;
+    }
+  }
+}
+
+int launch_push_ratio(const Layer& L, cudaStream_t s, int B, int ldb, const float* flow_scratch,
+                      const float* values, float* flows, float* rmax_all) {
+  ProfScope prof_(KC_ACCUM_PUSH, s);
+  if (!B || !L.n_pq) return PCB_OK;
+  dim3 grid((unsigned)L.n_pq, (unsigned)((B + SLAB - 1) / SLAB));
+#define PCB_PR(K)                                                                              \
+  k_push_ratio<K><<<grid, RW * 32, 0, s>>>(B, ldb, L.q_blk, L.pb_row, L.q_base, L.q_kind,      \
+                                           L.q_rrow, flow_scratch, values, flows, rmax_all)
+  switch (L.k_n) {
+    case 16: PCB_PR(16); break;
+    case 32: PCB_PR(32); break;
+    case 64: PCB_PR(64); break;
+    default: return PCB_USAGE;
+  }
+#undef PCB_PR
+  return check_launch();
+}
+
 // ---------------------------------------------------------------- K3 (SIMT)
 // Alg. 1 for one sum-block row and a 32-sample tile (engine.py:74-102).
 // block (32, 8): tx = sample, ty strides over the k_m sums of the block.

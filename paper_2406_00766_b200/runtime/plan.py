@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 19
+VERSION = 20
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -287,6 +287,122 @@ def leaf_alias(compiled, blocks, push_count):
     return arow, adir, pad_blk
 
 
+def push_tables(L, li, last_layer, push_count):
+    """Fused accumulate + push table of layer li in product order.  flag bit 0:
+    push the finished row; bit 1: first accumulation of the row in the
+    backward pass (store, not add).  Children are encoded slot * 2 + (1 if the
+    slot has a single push in the whole pass: plain store)."""
+    prow_arr = np.asarray(L.prod_rows, dtype=np.int64)
+    n_pr = prow_arr.size
+    pfan = np.zeros(n_pr, dtype=np.int64)
+    pos_of_row = {}
+    if L.pushes:
+        pos_of_row = {r: i for i, r in enumerate(prow_arr.tolist())}
+    parts = [None] * n_pr
+    for p in L.pushes:
+        idx = np.fromiter((pos_of_row[r] for r in p.rows.tolist()), np.int64, p.rows.size)
+        pfan[idx] = p.children.shape[1]
+        for i, ch in zip(idx.tolist(), p.children):
+            parts[i] = ch
+    flags = (pfan > 0).astype(np.int64) | (2 * (last_layer[prow_arr] == li)).astype(np.int64)
+    poff = np.concatenate([[0], np.cumsum(pfan)]).astype(np.int64)
+    pch = (np.concatenate([q for q in parts if q is not None]).astype(np.int64)
+           if pfan.sum() else np.zeros(0, np.int64))
+    pch = pch * 2 + (push_count[pch] == 1)
+    return flags, poff, pch
+
+
+def push_ratio_tables(compiled, push_tabs):
+    """Fused push + flow-ratio plan for lean steps.
+
+    A push block is k (= the layer's product block size) consecutive products
+    (consecutive flow-scratch slots, one fan-in f, pushed and first-stored in
+    this layer) whose i-th children, for every fan-in slot, are k consecutive
+    value slots with a single push each.  The fused kernel copies the block's
+    flows into those slots — or, when the slots are exactly one sum block of a
+    "pre-ratioed" layer, writes that block's flow ratios (k_ratio's r, in
+    place of the flows) and its per-sample shift R instead.  A layer is
+    pre-ratioed when every one of its sum blocks is such a target; its
+    backward pass then skips the ratio pass (its R rows live at rmax_off).
+    Returns (per-layer block tables, pre_ratio flags, rmax offsets, rows).
+    """
+    layers = compiled.layers
+    nl = len(layers)
+    # sum blocks of every layer: first slot -> (layer, block)
+    sb_of = {}
+    sb_info = []
+    for li, L in enumerate(layers):
+        sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
+            np.zeros(0, np.int64)
+        base = int(sids.min()) if sids.size else 0
+        sb_info.append((base, int(sids.size), int(L.k_m)))
+        for blk in range(int(sids.size)):
+            sb_of[base + blk * int(L.k_m)] = (li, blk)
+    cand = []  # per layer: list of (slot0, f, [child bases]) or None
+    for li, L in enumerate(layers):
+        flags, poff, pch = push_tabs[li]
+        slots = np.asarray(L.prod_slots, dtype=np.int64)
+        k = int(L.k_n)
+        n = slots.size
+        ok = n > 0 and n % k == 0 and bool(np.all(flags == 3)) and \
+            bool(np.all(pch & 1)) if n else False
+        blocks = []
+        if ok:
+            fan = np.diff(poff)
+            ch = pch >> 1
+            for j0 in range(0, n, k):
+                f = int(fan[j0])
+                if np.any(fan[j0:j0 + k] != f) or f == 0 or \
+                        np.any(np.diff(slots[j0:j0 + k]) != 1):
+                    ok = False
+                    break
+                kids = ch[poff[j0]:poff[j0 + k]].reshape(k, f)
+                if np.any(np.diff(kids, axis=0) != 1):
+                    ok = False
+                    break
+                blocks.append((int(slots[j0]), f, kids[0].tolist()))
+        cand.append(blocks if ok else None)
+    # pre-ratioed layers: every sum block is the target of one fused slot
+    hits = [0] * nl
+    for li in range(nl):
+        if cand[li] is None:
+            continue
+        for _, _, bases in cand[li]:
+            for cb in bases:
+                t = sb_of.get(cb)
+                if t is not None and sb_info[t[0]][2] == int(layers[li].k_n):
+                    hits[t[0]] += 1
+    pre = [bool(sb_info[li][1] > 0 and hits[li] == sb_info[li][1]) for li in range(nl)]
+    rmax_off, n_rmax = [], 0
+    for li in range(nl):
+        rmax_off.append(n_rmax if pre[li] else -1)
+        n_rmax += sb_info[li][1] if pre[li] else 0
+    tabs = []
+    empty = np.zeros(0, np.int64)
+    for li in range(nl):
+        if cand[li] is None:
+            tabs.append({k: empty for k in ("row", "f", "qoff", "qblk", "qbase", "qkind",
+                                            "qrrow")})
+            continue
+        row, fs, qoff, qbl, qb, qk, qr = [], [], [0], [], [], [], []
+        for bi, (slot0, f, bases) in enumerate(cand[li]):
+            row.append(slot0)
+            fs.append(f)
+            for cb in bases:
+                qbl.append(bi)
+                t = sb_of.get(cb)
+                ratio = t is not None and pre[t[0]] and sb_info[t[0]][2] == int(layers[li].k_n)
+                qb.append(cb)
+                qk.append(1 if ratio else 0)
+                qr.append(rmax_off[t[0]] + t[1] if ratio else -1)
+            qoff.append(len(qb))
+        tabs.append({"row": np.asarray(row, np.int64), "f": np.asarray(fs, np.int64),
+                     "qoff": np.asarray(qoff, np.int64), "qblk": np.asarray(qbl, np.int64),
+                     "qbase": np.asarray(qb, np.int64),
+                     "qkind": np.asarray(qk, np.int64), "qrrow": np.asarray(qr, np.int64)})
+    return tabs, pre, rmax_off, n_rmax
+
+
 def group_runs(group_idx, group_off):
     """Run-length encode the simplex-group index table: maximal runs of
     consecutive theta indices inside each group.  Returns (per-group run
@@ -549,6 +665,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             break
         pos = b0
     fp_cover = fp_cover and pos == c.theta_size
+    push_tabs = [push_tables(L, li, last_layer, push_count) for li, L in enumerate(c.layers)]
+    push_ratio, pre_ratio, rmax_off, n_rmax = push_ratio_tables(c, push_tabs)
     n_tc_rows = 0
     scratch_off = 0
     prog.append(len(c.layers))
@@ -647,31 +765,18 @@ def build_program(compiled, *, tensor_cores: bool = True):
         sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
             np.zeros(0, np.int64)
         prog += [int(sids.min()) if sids.size else 0, int(sids.size)]
-        # derived: fused accumulate + push table in product order.  flag bit 0:
-        # push the finished row; bit 1: first accumulation of the row in the
-        # backward pass (store, not add).  Children are encoded slot * 2 +
-        # (1 if the slot has a single push in the whole pass: plain store).
-        prow_arr = np.asarray(L.prod_rows, dtype=np.int64)
-        n_pr = prow_arr.size
-        pfan = np.zeros(n_pr, dtype=np.int64)
-        pos_of_row = {}
-        if L.pushes:
-            pos_of_row = {r: i for i, r in enumerate(prow_arr.tolist())}
-        parts = [None] * n_pr
-        for p in L.pushes:
-            idx = np.fromiter((pos_of_row[r] for r in p.rows.tolist()), np.int64, p.rows.size)
-            pfan[idx] = p.children.shape[1]
-            for i, ch in zip(idx.tolist(), p.children):
-                parts[i] = ch
-        flags = (pfan > 0).astype(np.int64) | (2 * (last_layer[prow_arr] == li)).astype(np.int64)
+        flags, poff, pch = push_tabs[li]
         pf_optional = pf_optional and bool(np.all(flags == 3))
-        poff = np.concatenate([[0], np.cumsum(pfan)]).astype(np.int64)
-        pch = (np.concatenate([q for q in parts if q is not None]).astype(np.int64)
-               if pfan.sum() else np.zeros(0, np.int64))
-        pch = pch * 2 + (push_count[pch] == 1)
         ref(flags)
         ref(poff)
         ref(pch)
+        # fused push + flow ratio (lean steps): blocks of k product rows whose
+        # children form, per fan-in slot, k consecutive single-push slots
+        pr = push_ratio[li]
+        prog.append(int(pr["row"].size))
+        for key in ("row", "f", "qoff", "qblk", "qbase", "qkind", "qrrow"):
+            ref(pr[key])
+        prog += [int(pre_ratio[li]), int(rmax_off[li])]
 
     red = red[:0]  # folded above: no replica reduction pass
     if red.shape[0]:
@@ -719,9 +824,11 @@ def build_program(compiled, *, tensor_cores: bool = True):
     ref(contig[rest] if rest.size else np.zeros(0, np.int64))
     prog.append(int(pf_optional))
     prog.append(int(fp_cover))
+    prog.append(int(n_rmax))
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
-            "leaf_alias": alias_pad is not None, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+            "leaf_alias": alias_pad is not None,
+            "pre_ratio_layers": int(sum(pre_ratio)), "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info

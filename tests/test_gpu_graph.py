@@ -49,24 +49,32 @@ def test_graph_step_matches_eager_and_oracle():
 
 
 @pytest.mark.parametrize("tensor_cores", [True, False])
-@pytest.mark.parametrize("k", [16, 32])
-def test_lean_step_matches_full(tensor_cores, k):
-    """Lean launches (leaf products aliased onto their inputs: no leaf product
-    pass, no leaf push) give bit-identical log-likelihoods and the same
-    parameter flows, missing values included (flows agree to float rounding:
-    product flows with several parent blocks are accumulated atomically, so
-    their summation order varies from run to run in either mode)."""
+@pytest.mark.parametrize("kind,k", [("hclt", 16), ("hclt", 32), ("hmm", 32)])
+def test_lean_step_matches_full(tensor_cores, kind, k):
+    """Lean launches give bit-identical log-likelihoods and the same parameter
+    flows, missing values included: leaf products aliased onto their inputs
+    (no leaf product pass, no leaf push) and flow ratios formed by the fused
+    push (no ratio pass).  Flows agree to float rounding: product flows with
+    several parent blocks are accumulated atomically, so their summation order
+    varies from run to run in either mode."""
     import torch
     from paper_2406_00766_b200 import structures as S
     from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
     from paper_2406_00766_b200.runtime import _lib, backward, forward
     from paper_2406_00766_b200.runtime.plan import device_plan
-    g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=30, hidden_dim=2 * k,
-                                       num_categories=8, seed=5))
+    if kind == "hclt":
+        g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=30, hidden_dim=2 * k,
+                                           num_categories=8, seed=5))
+        nv, ncat = 30, 8
+    else:
+        g = S.build_structure(S.StructureConfig(kind="hmm", seq_len=8, hidden_dim=128,
+                                                vocab_size=40, seed=2, tied=True))
+        nv, ncat = 8, 40
     c = compile_circuit(g, CompileConfig(block_size=k))
     plan = device_plan(c, tensor_cores=tensor_cores)
-    assert plan.info["leaf_alias"]
-    x = np.random.default_rng(3).integers(0, 8, size=(200, 30))
+    assert plan.info["leaf_alias"] == (kind == "hclt")
+    assert plan.info["pre_ratio_layers"] > 0
+    x = np.random.default_rng(3).integers(0, ncat, size=(200, nv))
     x[np.random.default_rng(4).random(x.shape) < 0.15] = -1
     lr0, b0 = forward(c, x, tensor_cores=tensor_cores)
     backward(c, b0, tensor_cores=tensor_cores)
