@@ -255,6 +255,12 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   return PCB_OK;
 }
 
+pcb_plan::~pcb_plan() {
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (side) cudaStreamDestroy(side);
+}
+
 int pcb_plan_destroy(pcb_plan* plan) {
   delete plan;
   return PCB_OK;
@@ -409,22 +415,32 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     st = launch_ratio_max(L, s, B, ldb, values, flows, w.rmax, w.ratio);
     if (st) return st;
   }
+  // parameter flows: on the side stream when their inputs (ratio rows in the
+  // flows buffer, per-layer R rows, the layer's scratch window) stay valid
+  // for the rest of the pass, i.e. for pre-ratioed layers of a lean step
+  cudaStream_t sp = s;
+  if (fused && L.pre_ratio && P->side) {
+    if (cudaEventRecord(P->ev_fork, s) != cudaSuccess ||
+        cudaStreamWaitEvent(P->side, P->ev_fork, 0) != cudaSuccess)
+      return PCB_CUDA;
+    sp = P->side;
+  }
   // accumulating layers zero their own flow range first (fp_cover plans skip
   // the whole-buffer memset)
   if (P->fp_cover && L.flow_hi > L.flow_lo && !(tc && B > 0 && pf_layer_stores(P, L, B)) &&
-      cudaMemsetAsync(f_params + L.flow_lo, 0, sizeof(float) * (L.flow_hi - L.flow_lo), s) !=
+      cudaMemsetAsync(f_params + L.flow_lo, 0, sizeof(float) * (L.flow_hi - L.flow_lo), sp) !=
           cudaSuccess)
     return PCB_CUDA;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
       st = (P->use_tc == 1 && pf_ws_supported(L))
-               ? launch_param_flow_ws(L, L.fwd[g], T, s, B, ldb, theta, ratio, rmax, scratch,
+               ? launch_param_flow_ws(L, L.fwd[g], T, sp, B, ldb, theta, ratio, rmax, scratch,
                                       f_params)
-               : launch_param_flow_tc(L, L.fwd[g], T, s, B, ldb, theta, values, flows, scratch,
+               : launch_param_flow_tc(L, L.fwd[g], T, sp, B, ldb, theta, values, flows, scratch,
                                       w.rmax, f_params);
     else
-      st = launch_param_flow_simt(L, L.fwd[g], s, B, ldb, theta, values, flows, scratch,
+      st = launch_param_flow_simt(L, L.fwd[g], sp, B, ldb, theta, values, flows, scratch,
                                   f_params);
     if (st) return st;
   }
@@ -540,6 +556,12 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
             cudaSuccess)
       return PCB_CUDA;
   }
+  const bool side = plan->lean && plan->push_ratio_ok;
+  if (side && !plan->side &&
+      (cudaStreamCreateWithFlags(&plan->side, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming) != cudaSuccess))
+    return PCB_CUDA;
   int st = launch_root_bwd(plan, s, B, ldb, d_flows, d_prod_flows);
   if (st) return st;
   for (auto it = plan->layers.rbegin(); it != plan->layers.rend(); ++it) {
@@ -550,6 +572,9 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
   st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch,
                                 d_f_params);
   if (st) return st;
+  if (side && (cudaEventRecord(plan->ev_join, plan->side) != cudaSuccess ||
+               cudaStreamWaitEvent(s, plan->ev_join, 0) != cudaSuccess))
+    return PCB_CUDA;
   return launch_replica_reduce(plan, s, d_f_params);
 }
 

@@ -119,6 +119,7 @@ struct Work {
 }  // namespace pcb
 
 struct pcb_plan {
+  ~pcb_plan();
   int64_t num_vars, num_value_slots, scratch_size, num_prod_rows, theta_size,
       f_params_size, reserved;
   int64_t root_slot, root_row;
@@ -169,6 +170,11 @@ struct pcb_plan {
   int64_t n_alias_pad = 0;
   const int32_t* alias_pad = nullptr;  // pad blocks of the first layer's window
   int lean = 0;
+  // lean steps: parameter flows of pre-ratioed layers run on a side stream
+  // (forked per layer, joined at the end of the backward pass), overlapping
+  // the child-flow / push chain; created on first use
+  mutable cudaStream_t side = nullptr;
+  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
