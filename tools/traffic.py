@@ -18,7 +18,7 @@ CLASSES = [
     ("k_sum_ws<0", "sum_fwd_tc"), ("k_sum_fwd_tc", "sum_fwd_tc"), ("k_sum_fwd_simt", "sum_fwd_simt"),
     ("k_param_flow", "param_flow"), ("k_ratio", "param_flow"),
     ("k_sum_ws<1", "child_flow"), ("k_child_flow", "child_flow"),
-    ("k_flow_push", "accum_push"), ("k_input_flow", "input_flow"), ("k_input_param_flow", "input_flow"),
+    ("k_flow_push", "accum_push"), ("k_push_ratio", "accum_push"), ("k_input_flow", "input_flow"), ("k_input_param_flow", "input_flow"),
     ("k_replica", "replica"), ("k_em", "em"), ("k_theta_to_mma", "em"),
 ]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
