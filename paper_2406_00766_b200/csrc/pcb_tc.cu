@@ -233,6 +233,12 @@ __device__ __forceinline__ float4 ld4(const float* p) {
 
 constexpr int EM_THREADS = 256;
 constexpr int EM_NP = 4;  // row passes per thread (k_m x k_n <= 64 x 64)
+// register path: blocks of <= EM_RT tiles of exactly EM_THREADS float4s
+// (32 x 32): every thread loads its quad of every tile's flows and theta at
+// once (2 x EM_RT vector loads in flight), and all tiles are staged in shared
+// memory for one plane-packing pass
+constexpr int EM_RT = 8;
+constexpr int EM_SMEM = (8 * 32 * 33 > TM_MAX * (TM_MAX + 1)) ? 8 * 32 * 33 : TM_MAX * (TM_MAX + 1);
 __global__ void __launch_bounds__(EM_THREADS)
     k_em_tiles(int64_t n_blk, const int32_t* __restrict__ bkm, const int32_t* __restrict__ bkn,
                const int32_t* __restrict__ toff, const int32_t* __restrict__ tstart,
@@ -240,12 +246,94 @@ __global__ void __launch_bounds__(EM_THREADS)
                const float* __restrict__ F, float* __restrict__ theta,
                __nv_bfloat16* __restrict__ mma, int64_t plane_n, float kappa, float step,
                int planes, int32_t* status) {
-  __shared__ float tile[TM_MAX * (TM_MAX + 1)];
+  __shared__ float tile[EM_SMEM];
   const int tid = threadIdx.x;
   int informative = 0, bad = 0;
   for (int64_t b = blockIdx.x; b < n_blk; b += gridDim.x) {
     const int km = __ldg(bkm + b), kn = __ldg(bkn + b);
     const int t0 = __ldg(toff + b), t1 = __ldg(toff + b + 1);
+    if (km * kn == 4 * EM_THREADS && km == 32 && t1 - t0 <= EM_RT) {
+      const int r = tid >> 3, c4 = (tid & 7) * 4;  // row, column quad (k_n = 32)
+      float4 fv[EM_RT], ov[EM_RT];
+#pragma unroll
+      for (int u = 0; u < EM_RT; ++u) {
+        if (t0 + u < t1) {
+          const int64_t o = __ldg(tstart + t0 + u) + r * 32 + c4;
+          fv[u] = ld4(F + o);
+          ov[u] = ld4(theta + o);
+        }
+      }
+      float acc = 0.f;
+#pragma unroll
+      for (int u = 0; u < EM_RT; ++u)
+        if (t0 + u < t1)
+          acc += (fv[u].x + kappa) + (fv[u].y + kappa) + (fv[u].z + kappa) + (fv[u].w + kappa);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const float inv = acc > 0.f ? 1.f / acc : 0.f;
+      if (acc > 0.f && (tid & 7) == 0) ++informative;
+#pragma unroll
+      for (int u = 0; u < EM_RT; ++u) {
+        if (t0 + u >= t1) continue;
+        float4 o = ov[u];
+        if (inv > 0.f) {
+          const float4 f = fv[u];
+          const float n[4] = {(f.x + kappa) * inv, (f.y + kappa) * inv, (f.z + kappa) * inv,
+                              (f.w + kappa) * inv};
+          float* op = &o.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            op[e] = (step >= 1.f) ? n[e] : ((1.f - step) * op[e] + step * n[e]);
+            if (!isfinite(op[e])) ++bad;
+          }
+          float* tp = theta + __ldg(tstart + t0 + u) + r * 32 + c4;
+          if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
+            *reinterpret_cast<float4*>(tp) = o;
+          } else {
+            tp[0] = o.x, tp[1] = o.y, tp[2] = o.z, tp[3] = o.w;
+          }
+        }
+        if (planes) {
+          float* d = tile + u * (32 * 33) + r * 33 + c4;
+          d[0] = o.x, d[1] = o.y, d[2] = o.z, d[3] = o.w;
+        }
+      }
+      if (!planes) continue;
+      __syncthreads();
+      const int nt = t1 - t0, n8 = 32 * 32 / 8;
+      for (int q = tid; q < nt * 2 * n8; q += EM_THREADS) {
+        const int u = q / (2 * n8), qq = q - u * 2 * n8;
+        const float* tl = tile + u * (32 * 33);
+        float v[8];
+        uint32_t off;
+        int pl;
+        if (qq < n8) {  // sum-major core row (m, j..j+7)
+          const int m = qq >> 2, j = (qq & 3) * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = tl[m * 33 + j + e];
+          off = (uint32_t)tile_off(m, j, 32) * 2u;
+          pl = 0;
+        } else {  // product-major core row (j, m..m+7)
+          const int rr = qq - n8;
+          const int j = rr >> 2, m = (rr & 3) * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = tl[(m + e) * 33 + j];
+          off = (uint32_t)tile_off(j, m, 32) * 2u;
+          pl = 2;
+        }
+        uint4 hi, lo;
+        split_pack8(v, hi, lo);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(
+                           pl == 0 ? mma + __ldg(tslab_f + t0 + u)
+                                   : mma + 2 * plane_n + __ldg(tslab_c + t0 + u)) +
+                       off;
+        *reinterpret_cast<uint4*>(dst) = hi;
+        *reinterpret_cast<uint4*>(dst + plane_n * 2) = lo;
+      }
+      __syncthreads();
+      continue;
+    }
+
     const int tpr = kn / 4, rp = EM_THREADS / tpr;  // threads per row, rows per pass
     const int c4 = (tid % tpr) * 4, r_in = tid / tpr;
     float acc[EM_NP];
