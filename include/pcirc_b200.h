@@ -88,6 +88,16 @@ int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta);
  * records); default 0. */
 int pcb_plan_set_lean(pcb_plan* plan, int lean);
 
+/* Inline input EM for single-process lean steps (no flow all-reduce between
+ * the backward pass and EM): while enabled, a lean pcb_backward on the plan's
+ * own bound table applies the mini-batch EM update (pseudocount, step_size)
+ * to every staged input's pmf in the input-flow pass itself (its flows are
+ * then not written to d_f_params), zeroing and accumulating d_status; the
+ * next pcb_em_update with the same parameters and d_status updates only the
+ * remaining groups.  Same arithmetic as the separate pass. */
+int pcb_plan_set_inline_em(pcb_plan* plan, int enable, float pseudocount, float step_size,
+                           int32_t* d_status);
+
 /* Validate a device batch (xT, [num_vars x ldb]) against the category counts:
  * writes the number of bad entries to *d_bad (device int32).
  * Replaces: pcirc/runtime/engine.py:36-52 (_validate_batch) for device batches. */

@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 20;
+constexpr int64_t kVersion = 21;
 
 struct Reader {
   const int64_t* p;
@@ -235,6 +235,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->prod_flows_optional = (int)r.get();
   P->fp_cover = (int)r.get();
   P->n_rmax = r.get();
+  P->n_em_small_noninl = r.get();
+  P->in_inline_ok = (int)r.get();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -277,6 +279,18 @@ int pcb_plan_set_mma(pcb_plan* plan, void* d_mma, int64_t elems) {
 int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta) {
   if (!plan) return PCB_USAGE;
   plan->theta_bound = d_theta;
+  return PCB_OK;
+}
+
+int pcb_plan_set_inline_em(pcb_plan* plan, int enable, float pseudocount, float step_size,
+                           int32_t* d_status) {
+  if (!plan || (enable && (!(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f ||
+                           !d_status)))
+    return PCB_USAGE;
+  plan->inline_em = enable ? 1 : 0;
+  plan->inline_kappa = pseudocount;
+  plan->inline_step = step_size;
+  plan->inline_status = d_status;
   return PCB_OK;
 }
 
@@ -353,6 +367,12 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.rmax_all = w.gshift + P->max_tc_rows * (int64_t)ldb;
   w.counters = reinterpret_cast<int32_t*>(w.rmax_all + P->n_rmax * (int64_t)ldb);
   return w;
+}
+
+// the input-flow pass applies EM to the staged inputs' pmfs (lean step, the
+// plan's own table, single process)
+bool inline_em_active(const pcb_plan* P, const float* theta) {
+  return P->inline_em && P->lean && P->in_inline_ok && theta == P->theta_bound;
 }
 
 // the layer's products alias their inputs in this (lean) step
@@ -562,6 +582,10 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
        cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
        cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming) != cudaSuccess))
     return PCB_CUDA;
+  const bool inl = inline_em_active(plan, d_theta);
+  plan->inline_done = 0;
+  if (inl && cudaMemsetAsync(plan->inline_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
+    return PCB_CUDA;
   int st = launch_root_bwd(plan, s, B, ldb, d_flows, d_prod_flows);
   if (st) return st;
   for (auto it = plan->layers.rbegin(); it != plan->layers.rend(); ++it) {
@@ -569,9 +593,11 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
                         d_flow_scratch, d_prod_flows, d_f_params, w);
     if (st) return st;
   }
+  bool done = false;
   st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch,
-                                d_f_params);
+                                d_f_params, inl, &done);
   if (st) return st;
+  plan->inline_done = done ? 1 : 0;
   if (side && (cudaEventRecord(plan->ev_join, plan->side) != cudaSuccess ||
                cudaStreamWaitEvent(s, plan->ev_join, 0) != cudaSuccess))
     return PCB_CUDA;
@@ -603,13 +629,20 @@ int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, f
                   float pseudocount, float step_size, int32_t* d_status) {
   if (!plan || !(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f) return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
-  if (cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
+  // inline input EM already updated the staged inputs' pmfs in the backward
+  // pass (same parameters; its counts are already in d_status)
+  const bool inl = inline_em_active(plan, d_theta) && plan->inline_done &&
+                   d_status == plan->inline_status && pseudocount == plan->inline_kappa &&
+                   step_size == plan->inline_step;
+  plan->inline_done = 0;
+  if (!inl && cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
+    return PCB_CUDA;
   // the plan's own table: the tile-block pass also rewrites the bf16 MMA
   // planes; tensor-core tiles outside tile blocks get the separate refresh
   const bool own = d_theta == plan->theta_bound && plan->mma;
   int st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own);
   if (st) return st;
-  st = launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status);
+  st = launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, inl);
   if (st) return st;
   if (own && plan->n_em_tiles < plan->n_mma_tiles) return launch_theta_to_mma(plan, s, d_theta);
   return PCB_OK;

@@ -175,6 +175,15 @@ struct pcb_plan {
   // the child-flow / push chain; created on first use
   mutable cudaStream_t side = nullptr;
   mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // inline input EM (pcb_plan_set_inline_em): the input-flow pass of a lean
+  // backward applies the EM update to the staged inputs' pmf groups (the
+  // last small rest groups, [n_em_small_noninl, n_em_small)) directly
+  int64_t n_em_small_noninl = 0;
+  int in_inline_ok = 0;  // every staged input pmf is such a group (ncat <= 256)
+  int inline_em = 0;
+  float inline_kappa = 0.f, inline_step = 1.f;
+  int32_t* inline_status = nullptr;
+  mutable int inline_done = 0;  // the last backward pass applied it
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
@@ -240,14 +249,15 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows);
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
-                             const float* flow_scratch, float* f_params);
+                             const float* flow_scratch, float* f_params, bool inline_em,
+                             bool* inline_done);
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
                     float* lroot);
 int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,
                     float* prod_flows);
 int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params);
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
-              float pseudocount, float step, int32_t* status);
+              float pseudocount, float step, int32_t* status, bool skip_inline);
 int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
                     float pseudocount, float step, int32_t* status, bool planes);
 int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,

@@ -1002,9 +1002,12 @@ __global__ void __launch_bounds__(IS_THREADS)
                         const int32_t* __restrict__ pids, const int32_t* __restrict__ xT,
                         const float* __restrict__ theta, const float* __restrict__ flows,
                         const int32_t* __restrict__ arow, const int32_t* __restrict__ adir,
-                        const float* __restrict__ aflows, float* __restrict__ f_params) {
+                        const float* __restrict__ aflows, float* __restrict__ f_params,
+                        float* __restrict__ em_theta, float kappa, float step,
+                        int32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
   const int blk = blockIdx.x;
+  int informative = 0, bad = 0;
   const int ncat = __ldg(bncat + blk), cnt = __ldg(bcount + blk), var = __ldg(bvar + blk);
   const int64_t slot0 = __ldg(bslot0 + blk);
   const int32_t* pid = pids + __ldg(bpoff + blk);
@@ -1069,6 +1072,45 @@ __global__ void __launch_bounds__(IS_THREADS)
     for (int p = m0 + lane; p < m1; p += 32) miss += row[order[p]];
     for (int o = 16; o > 0; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
     const int64_t base = __ldg(pid + i);
+    if (em_theta) {
+      // inline EM of the input's pmf (one simplex group, ncat <= 256):
+      // k_em's arithmetic on the flows just formed, theta updated in place
+      float v[8], o[8], tot = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // old theta first: its loads overlap the sums
+        const int c = lane + 32 * u;
+        o[u] = c < ncat ? em_theta[base + c] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = lane + 32 * u;
+        v[u] = 0.f;
+        if (c < ncat) {
+          float h = 0.f;
+          const int p1 = start[c + 1];
+          for (int p = start[c]; p < p1; ++p) h += row[order[p]];
+          v[u] = h + (miss != 0.f ? miss * o[u] : 0.f) + kappa;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tot += v[u];
+      for (int o2 = 16; o2 > 0; o2 >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o2);
+      if (tot > 0.f) {
+        ++informative;
+        const float inv = 1.f / tot;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = lane + 32 * u;
+          if (c >= ncat) continue;
+          const float nv = v[u] * inv;
+          const float th = (step >= 1.f) ? nv : ((1.f - step) * o[u] + step * nv);
+          if (!isfinite(th)) ++bad;
+          em_theta[base + c] = th;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     for (int c = lane; c < ncat; c += 32) {
       float h = 0.f;
       const int p1 = start[c + 1];
@@ -1077,12 +1119,19 @@ __global__ void __launch_bounds__(IS_THREADS)
     }
     __syncwarp();
   }
+  if (em_theta) {
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if (lane == 0 && informative) atomicAdd(status, informative);
+    if (lane == 0 && bad) atomicAdd(status + 1, bad);
+  }
 }
 
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
-                             const float* flow_scratch, float* f_params) {
+                             const float* flow_scratch, float* f_params, bool inline_em,
+                             bool* inline_done) {
   ProfScope prof_(KC_INPUT_FLOW, s);
+  *inline_done = false;
   const InBlocks& ib = p->in_blocks;
   const int32_t* arow = (p->lean && p->leaf_alias) ? ib.alias_row : nullptr;
   // sorted (atomic-free) kernel when its shared-memory slots fit, else the
@@ -1099,8 +1148,11 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
     }
     k_input_flow_sorted<<<(unsigned)ib.n, IS_THREADS, (size_t)sorted_bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
-        arow, ib.alias_dir, flow_scratch, f_params);
+        arow, ib.alias_dir, flow_scratch, f_params,
+        inline_em ? const_cast<float*>(theta) : nullptr, p->inline_kappa, p->inline_step,
+        p->inline_status);
     if (check_launch()) return PCB_CUDA;
+    *inline_done = inline_em;
   } else if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
     static int attr = 0;
@@ -1306,9 +1358,12 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
-              float pseudocount, float step, int32_t* status) {
+              float pseudocount, float step, int32_t* status, bool skip_inline) {
   ProfScope prof_(KC_EM, s);
-  const int64_t ns = p->n_em_small, nb = p->n_em_rest - p->n_em_small;
+  const int64_t nb = p->n_em_rest - p->n_em_small;
+  // the staged inputs' pmf groups (last among the small ones) were updated
+  // by the input-flow pass (inline EM)
+  const int64_t ns = skip_inline ? p->n_em_small_noninl : p->n_em_small;
   if (ns) {
     int blocks = grid_for(ns * 32, 256, 148 * 16);
     k_em<<<blocks, 256, 0, s>>>(ns, p->em_rest, p->em_rest_start, p->group_idx, p->group_off,
@@ -1316,7 +1371,8 @@ int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* t
     if (check_launch()) return PCB_CUDA;
   }
   if (nb) {
-    k_em_big<<<grid_for(nb, 1, 148 * 8), 256, 0, s>>>(nb, p->em_rest + ns, p->em_rest_start + ns,
+    const int64_t s0 = p->n_em_small;
+    k_em_big<<<grid_for(nb, 1, 148 * 8), 256, 0, s>>>(nb, p->em_rest + s0, p->em_rest_start + s0,
                                                       p->group_idx, p->group_off, f_params,
                                                       theta, pseudocount, step, status);
     if (check_launch()) return PCB_CUDA;

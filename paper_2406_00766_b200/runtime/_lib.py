@@ -30,6 +30,7 @@ SIGNATURES = {
     "pcb_theta_refresh": (_I, [_P, _P, _P]),
     "pcb_plan_set_theta": (_I, [_P, _P]),
     "pcb_plan_set_lean": (_I, [_P, _I]),
+    "pcb_plan_set_inline_em": (_I, [_P, _I, _F, _F, _P]),
     "pcb_tc_selftest_mn": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "pcb_check_batch": (_I, [_P, _P, _I, _I, _P, _P]),
     "pcb_transpose_batch_i64": (_I, [_P, _P, _I, _I, _P, _P]),

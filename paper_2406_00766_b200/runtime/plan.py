@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 20
+VERSION = 21
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -812,23 +812,37 @@ def build_program(compiled, *, tensor_cores: bool = True):
     gi = np.asarray(c.group_idx, dtype=np.int64)
     go = np.asarray(c.group_off, dtype=np.int64)
     gsize = np.diff(go)[rest] if rest.size else np.zeros(0, np.int64)
-    rest = np.concatenate([rest[gsize < EM_BIG], rest[gsize >= EM_BIG]]).astype(np.int64)
-    prog.append(int(rest.size))
-    prog.append(int((gsize < EM_BIG).sum()))
-    ref(rest)
     # contiguous rest groups (an input pmf is one run): first theta index, else -1
     run_off, _, _ = group_runs(gi, go)
     one = (np.diff(run_off) == 1) & (np.diff(go) > 0)
     contig = np.full(max(n_groups, 0), -1, dtype=np.int64)
     contig[one] = gi[np.minimum(go[:-1][one], max(gi.size - 1, 0))]
+    # small groups that are exactly a staged input's pmf (ncat <= 256) go
+    # last among the small ones: the inline input EM updates them
+    in_pmf = {}
+    if nb:
+        ncat_of = np.repeat(blocks["ncat"], blocks["count"])
+        in_pmf = dict(zip(blocks["pids"].tolist(), ncat_of.tolist()))
+    inl = np.array([bool(contig[g] >= 0 and in_pmf.get(int(contig[g])) == int(sz) and sz <= 256)
+                    for g, sz in zip(rest.tolist(), gsize.tolist())], dtype=bool)
+    small = gsize < EM_BIG
+    rest_o = np.concatenate([rest[small & ~inl], rest[small & inl], rest[~small]]).astype(np.int64)
+    n_small_noninl = int((small & ~inl).sum())
+    in_inline_ok = bool(nb) and int((small & inl).sum()) == int(blocks["pids"].size)
+    rest = rest_o
+    prog.append(int(rest.size))
+    prog.append(int(small.sum()))
+    ref(rest)
     ref(contig[rest] if rest.size else np.zeros(0, np.int64))
     prog.append(int(pf_optional))
     prog.append(int(fp_cover))
     prog.append(int(n_rmax))
+    prog.append(n_small_noninl)
+    prog.append(int(in_inline_ok))
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,
-            "pre_ratio_layers": int(sum(pre_ratio)), "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+            "pre_ratio_layers": int(sum(pre_ratio)), "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info

@@ -39,6 +39,9 @@ class TrainStep:
         # the step never reads prod_flows: skip writing it when the layout allows
         self._pf_ptr = (0 if self.plan.info.get("prod_flows_optional")
                         else self.bufs.prod_flows_full.data_ptr())
+        # one process: no flow all-reduce between backward and EM, so the
+        # input-flow pass may apply EM to the inputs' pmfs (pcb_plan_set_inline_em)
+        self._inline_em = allreduce is None
         self.graph = None
         self.ll = None
         self.launches_per_step = None
@@ -53,6 +56,9 @@ class TrainStep:
         # lean launches: the step never reads node values / flows, so aliased
         # leaf products skip their evaluation and push (pcb_plan_set_lean)
         _lib.call("pcb_plan_set_lean", p.handle, 1)
+        if self._inline_em:
+            _lib.call("pcb_plan_set_inline_em", p.handle, 1, self.pseudocount, self.step_size,
+                      p.status.data_ptr())
         try:
             _lib.call("pcb_forward", p.handle, s, self.B, b.ldb, b.xT.data_ptr(),
                       p.theta.data_ptr(), b.values_full.data_ptr(), b.scratch_full.data_ptr(),
@@ -61,13 +67,15 @@ class TrainStep:
                       p.theta.data_ptr(), b.values_full.data_ptr(), b.flows_full.data_ptr(),
                       b.scratch_full.data_ptr(), b.flow_scratch_full.data_ptr(),
                       self._pf_ptr, b.f_params.data_ptr(), b.work.data_ptr())
+            ll = b.lroot.double().sum()
+            if self.allreduce is not None:
+                self.allreduce(b.f_params, ll)
+            em_update_(self.c, b.f_params, pseudocount=self.pseudocount,
+                       step_size=self.step_size, check=False, plan=p)
         finally:
             _lib.call("pcb_plan_set_lean", p.handle, 0)
-        ll = b.lroot.double().sum()
-        if self.allreduce is not None:
-            self.allreduce(b.f_params, ll)
-        em_update_(self.c, b.f_params, pseudocount=self.pseudocount,
-                   step_size=self.step_size, check=False, plan=p)
+            if self._inline_em:
+                _lib.call("pcb_plan_set_inline_em", p.handle, 0, 0.0, 1.0, 0)
         return ll
 
     def _capture(self):

@@ -89,3 +89,37 @@ def test_lean_step_matches_full(tensor_cores, kind, k):
     assert torch.equal(lr1, want_ll)
     got, ref = b1.f_params.double(), want_f.double()
     assert torch.max(torch.abs(got - ref) / torch.clamp(ref.abs(), min=1e-30)).item() < 2e-6
+
+
+def test_inline_input_em_matches_separate_pass():
+    """A one-process TrainStep (lean launches; the input-flow pass applies EM
+    to the staged inputs' pmfs) updates theta and the EM status counters like
+    the plain forward / backward / pcb_em_update sequence."""
+    import torch
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.runtime import backward, forward
+    from paper_2406_00766_b200.runtime.em import apply_theta, em_update_
+    from paper_2406_00766_b200.runtime.plan import device_plan
+    from paper_2406_00766_b200.runtime.step import TrainStep
+    g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=30, hidden_dim=64,
+                                       num_categories=8, seed=7))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    assert device_plan(c).info["input_inline_em"]
+    x = np.random.default_rng(9).integers(0, 8, size=(192, 30))
+    x[np.random.default_rng(10).random(x.shape) < 0.1] = -1
+    apply_theta(c, c.theta)
+    ts = TrainStep(c, 192, pseudocount=1e-3, step_size=0.1, graph=False)
+    ll = float(ts.run(torch.from_numpy(x.astype(np.int32)).cuda()).item())
+    th_inline = ts.plan.theta.double().cpu().numpy()
+    st_inline = ts.plan.status[:2].cpu().numpy().copy()
+    apply_theta(c, c.theta)
+    plan = device_plan(c)
+    lr, bufs = forward(c, x)
+    backward(c, bufs)
+    em_update_(c, bufs.f_params, pseudocount=1e-3, step_size=0.1, check=False, plan=plan)
+    th_ref = plan.theta.double().cpu().numpy()
+    st_ref = plan.status[:2].cpu().numpy()
+    assert abs(ll - float(lr.double().sum())) <= 1e-6 * abs(ll)
+    np.testing.assert_array_equal(st_inline, st_ref)
+    np.testing.assert_allclose(th_inline, th_ref, rtol=2e-6, atol=1e-12)
