@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 21;
+constexpr int64_t kVersion = 22;
 
 struct Reader {
   const int64_t* p;
@@ -137,6 +137,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.param_ids = r.ref();
       G.flow_ids = r.ref();
       G.param_slab = r.ref();
+      G.param_slab_c = r.ref();
       G.exclusive = (int)r.get();
       G.uniform = (int)r.get();
       TcRows T, Tp;
@@ -237,6 +238,12 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->n_rmax = r.get();
   P->n_em_small_noninl = r.get();
   P->in_inline_ok = (int)r.get();
+  P->n_em_pre = r.get();
+  for (auto& L : P->layers) {
+    L.em_lo = r.get();
+    L.em_hi = r.get();
+    L.em_fusable = (int)r.get();
+  }
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -372,7 +379,7 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
 // the input-flow pass applies EM to the staged inputs' pmfs (lean step, the
 // plan's own table, single process)
 bool inline_em_active(const pcb_plan* P, const float* theta) {
-  return P->inline_em && P->lean && P->in_inline_ok && theta == P->theta_bound;
+  return P->inline_em && P->lean && theta == P->theta_bound;
 }
 
 // the layer's products alias their inputs in this (lean) step
@@ -418,6 +425,29 @@ int64_t zero_tile(const pcb_plan* P) {
   return z;
 }
 
+int child_flows(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
+                const float* theta, const float* values, const float* flows, float* scratch,
+                float* flow_scratch, const float* ratio, const float* rmax, bool tc,
+                const Work& w) {
+  for (size_t g = 0; g < L.bwd.size(); ++g) {
+    const TcRows& T = L.bwd_tc[g];
+    int st;
+    if (tc && T.count > 0)
+      st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
+               ? launch_child_flow_ws(P, L, L.bwd[g],
+                                      ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T, s, B, ldb,
+                                      ratio, scratch, rmax, flow_scratch, w.gshift,
+                                      w.counters, L.bwd.size() == 1)
+               : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
+                                      w.rmax, flow_scratch);
+    else
+      st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
+                                  flow_scratch);
+    if (st) return st;
+  }
+  return PCB_OK;
+}
+
 int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
                    const float* theta, const float* values, float* flows, float* scratch_all,
                    float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
@@ -438,6 +468,18 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   // parameter flows: on the side stream when their inputs (ratio rows in the
   // flows buffer, per-layer R rows, the layer's scratch window) stay valid
   // for the rest of the pass, i.e. for pre-ratioed layers of a lean step
+  // EM fused into the parameter-flow epilogue (one-process lean step): the
+  // layer's θ tiles and planes are rewritten there, so its parameter flows
+  // run after its child flows (which read the planes)
+  L.em_done = 0;
+  const bool em_fuse = inline_em_active(P, theta) && L.em_fusable && fused && L.pre_ratio &&
+                       P->side && P->mma && tc && P->use_tc == 1 && pf_ws_supported(L) &&
+                       pf_layer_stores(P, L, B);
+  if (em_fuse) {
+    st = child_flows(P, L, s, B, ldb, theta, values, flows, scratch, flow_scratch, ratio, rmax,
+                     tc, w);
+    if (st) return st;
+  }
   cudaStream_t sp = s;
   if (fused && L.pre_ratio && P->side) {
     if (cudaEventRecord(P->ev_fork, s) != cudaSuccess ||
@@ -445,6 +487,8 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
       return PCB_CUDA;
     sp = P->side;
   }
+  PfEm em{P->inline_kappa, P->inline_step, P->inline_status, P->mma, P->mma_plane,
+          const_cast<float*>(theta)};
   // accumulating layers zero their own flow range first (fp_cover plans skip
   // the whole-buffer memset)
   if (P->fp_cover && L.flow_hi > L.flow_lo && !(tc && B > 0 && pf_layer_stores(P, L, B)) &&
@@ -456,7 +500,7 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     if (tc && T.count > 0)
       st = (P->use_tc == 1 && pf_ws_supported(L))
                ? launch_param_flow_ws(L, L.fwd[g], T, sp, B, ldb, theta, ratio, rmax, scratch,
-                                      f_params)
+                                      f_params, em_fuse ? &em : nullptr)
                : launch_param_flow_tc(L, L.fwd[g], T, sp, B, ldb, theta, values, flows, scratch,
                                       w.rmax, f_params);
     else
@@ -464,19 +508,11 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
                                   f_params);
     if (st) return st;
   }
-  for (size_t g = 0; g < L.bwd.size(); ++g) {
-    const TcRows& T = L.bwd_tc[g];
-    if (tc && T.count > 0)
-      st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
-               ? launch_child_flow_ws(P, L, L.bwd[g],
-                                      ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T, s, B, ldb,
-                                      ratio, scratch, rmax, flow_scratch, w.gshift,
-                                      w.counters, L.bwd.size() == 1)
-               : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
-                                      w.rmax, flow_scratch);
-    else
-      st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
-                                  flow_scratch);
+  if (em_fuse) {
+    L.em_done = 1;
+  } else {
+    st = child_flows(P, L, s, B, ldb, theta, values, flows, scratch, flow_scratch, ratio, rmax,
+                     tc, w);
     if (st) return st;
   }
   // aliased leaf products: the input pass reads their flow rows directly
@@ -583,7 +619,8 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
        cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming) != cudaSuccess))
     return PCB_CUDA;
   const bool inl = inline_em_active(plan, d_theta);
-  plan->inline_done = 0;
+  plan->inline_done = inl ? 1 : 0;  // d_status zeroed here; inline updates may follow
+  plan->inline_inputs_done = 0;
   if (inl && cudaMemsetAsync(plan->inline_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
     return PCB_CUDA;
   int st = launch_root_bwd(plan, s, B, ldb, d_flows, d_prod_flows);
@@ -595,9 +632,9 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
   }
   bool done = false;
   st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch,
-                                d_f_params, inl, &done);
+                                d_f_params, inl && plan->in_inline_ok, &done);
   if (st) return st;
-  plan->inline_done = done ? 1 : 0;
+  plan->inline_inputs_done = done ? 1 : 0;
   if (side && (cudaEventRecord(plan->ev_join, plan->side) != cudaSuccess ||
                cudaStreamWaitEvent(s, plan->ev_join, 0) != cudaSuccess))
     return PCB_CUDA;
@@ -634,15 +671,41 @@ int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, f
   const bool inl = inline_em_active(plan, d_theta) && plan->inline_done &&
                    d_status == plan->inline_status && pseudocount == plan->inline_kappa &&
                    step_size == plan->inline_step;
+  const bool inl_inputs = inl && plan->inline_inputs_done;
   plan->inline_done = 0;
+  plan->inline_inputs_done = 0;
   if (!inl && cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
     return PCB_CUDA;
   // the plan's own table: the tile-block pass also rewrites the bf16 MMA
   // planes; tensor-core tiles outside tile blocks get the separate refresh
   const bool own = d_theta == plan->theta_bound && plan->mma;
-  int st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own);
+  int st = PCB_OK;
+  if (inl) {
+    // tile blocks of layers whose EM ran in their parameter-flow epilogue are
+    // skipped (blocks are ordered: other layers first, then layer by layer)
+    int64_t lo = 0, hi = plan->n_em_pre;
+    for (const Layer& L : plan->layers) {
+      if (!L.em_fusable || L.em_hi <= L.em_lo) continue;
+      if (!L.em_done && L.em_lo == hi) {
+        hi = L.em_hi;
+        continue;
+      }
+      if (!L.em_done) {
+        st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own,
+                             lo, hi);
+        if (st) return st;
+        lo = L.em_lo;
+        hi = L.em_hi;
+      }
+    }
+    st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own, lo,
+                         hi);
+    for (const Layer& L : plan->layers) L.em_done = 0;
+  } else {
+    st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own);
+  }
   if (st) return st;
-  st = launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, inl);
+  st = launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, inl_inputs);
   if (st) return st;
   if (own && plan->n_em_tiles < plan->n_mma_tiles) return launch_theta_to_mma(plan, s, d_theta);
   return PCB_OK;

@@ -45,6 +45,7 @@ struct FwdGroup {
   int64_t rows, cap;
   const int32_t *sum_ids, *prod_ids, *param_ids, *flow_ids;
   const int32_t* param_slab;  // bf16 MMA-tile offset per (row, col), -1 for padding
+  const int32_t* param_slab_c;  // product-major plane offset per (row, col) (fused EM)
   int exclusive = 0;          // every flow tile of the group has no other writer in the pass
   int uniform = 0;            // every row has the same child blocks (dense layer)
 };
@@ -97,6 +98,11 @@ struct Layer {
   const int32_t *pb_row = nullptr, *pb_f = nullptr, *pb_qoff = nullptr, *q_blk = nullptr,
                 *q_base = nullptr, *q_kind = nullptr, *q_rrow = nullptr;
   int pre_ratio = 0;     // every sum block's ratio comes from a fused push
+  // EM fused into this layer's parameter-flow epilogue (plan.em_fused_order):
+  // its tile blocks are [em_lo, em_hi); em_done: the last backward pass did it
+  int em_fusable = 0;
+  int64_t em_lo = 0, em_hi = 0;
+  mutable int em_done = 0;
   int64_t rmax_off = -1;  // its R rows in the all-layer rmax region
 };
 
@@ -183,7 +189,9 @@ struct pcb_plan {
   int inline_em = 0;
   float inline_kappa = 0.f, inline_step = 1.f;
   int32_t* inline_status = nullptr;
-  mutable int inline_done = 0;  // the last backward pass applied it
+  mutable int inline_done = 0;         // the last backward pass zeroed d_status for inline EM
+  mutable int inline_inputs_done = 0;  // ... and updated the staged inputs' pmfs
+  int64_t n_em_pre = 0;  // tile blocks of layers without fused EM (first in order)
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
@@ -259,7 +267,16 @@ int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params);
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
               float pseudocount, float step, int32_t* status, bool skip_inline);
 int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
-                    float pseudocount, float step, int32_t* status, bool planes);
+                    float pseudocount, float step, int32_t* status, bool planes,
+                    int64_t blk0 = 0, int64_t blk1 = -1);
+// EM fused into the parameter-flow epilogue (one-process lean steps)
+struct PfEm {
+  float kappa, step;
+  int32_t* status;
+  __nv_bfloat16* mma;
+  int64_t plane;
+  float* theta;  // updated in place
+};
 int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, float* buf,
                       float v);
 int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, float* buf,
@@ -297,7 +314,7 @@ bool pf_ws_supported(const Layer& L);
 bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
-                         const float* scratch, float* f_params);
+                         const float* scratch, float* f_params, const PfEm* em = nullptr);
 int launch_child_flow_tc(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* values, const float* flows,
                          const float* scratch, const float* rmax, float* flow_scratch);

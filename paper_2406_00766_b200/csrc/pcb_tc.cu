@@ -240,7 +240,8 @@ constexpr int EM_NP = 4;  // row passes per thread (k_m x k_n <= 64 x 64)
 constexpr int EM_RT = 8;
 constexpr int EM_SMEM = (8 * 32 * 33 > TM_MAX * (TM_MAX + 1)) ? 8 * 32 * 33 : TM_MAX * (TM_MAX + 1);
 __global__ void __launch_bounds__(EM_THREADS)
-    k_em_tiles(int64_t n_blk, const int32_t* __restrict__ bkm, const int32_t* __restrict__ bkn,
+    k_em_tiles(int64_t blk0, int64_t n_blk, const int32_t* __restrict__ bkm,
+               const int32_t* __restrict__ bkn,
                const int32_t* __restrict__ toff, const int32_t* __restrict__ tstart,
                const int32_t* __restrict__ tslab_f, const int32_t* __restrict__ tslab_c,
                const float* __restrict__ F, float* __restrict__ theta,
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(EM_THREADS)
   __shared__ float tile[EM_SMEM];
   const int tid = threadIdx.x;
   int informative = 0, bad = 0;
-  for (int64_t b = blockIdx.x; b < n_blk; b += gridDim.x) {
+  for (int64_t b = blk0 + blockIdx.x; b < n_blk; b += gridDim.x) {
     const int km = __ldg(bkm + b), kn = __ldg(bkn + b);
     const int t0 = __ldg(toff + b), t1 = __ldg(toff + b + 1);
     if (km * kn == 4 * EM_THREADS && km == 32 && t1 - t0 <= EM_RT) {
@@ -467,11 +468,13 @@ __global__ void __launch_bounds__(EM_THREADS)
 }
 
 int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
-                    float pseudocount, float step, int32_t* status, bool planes) {
+                    float pseudocount, float step, int32_t* status, bool planes, int64_t blk0,
+                    int64_t blk1) {
   ProfScope prof_(KC_EM, s);
-  if (!p->n_em_blk) return PCB_OK;
-  k_em_tiles<<<grid_for(p->n_em_blk, 1, 148 * 8), EM_THREADS, 0, s>>>(
-      p->n_em_blk, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab_f,
+  if (blk1 < 0) blk1 = p->n_em_blk;
+  if (blk1 <= blk0) return PCB_OK;
+  k_em_tiles<<<grid_for(blk1 - blk0, 1, 148 * 8), EM_THREADS, 0, s>>>(
+      blk0, blk1, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab_f,
       p->em_tile_slab_c, f_params, theta, p->mma, p->mma_plane, pseudocount, step,
       planes ? 1 : 0, status);
   return check_launch();

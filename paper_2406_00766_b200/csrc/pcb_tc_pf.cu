@@ -58,6 +58,15 @@ struct PfArgs {
   const int32_t* flags;  // per super-row: bit 0 contiguous sum rows, bit 1 contiguous children
   const float* theta;
   float* f_params;
+  // fused EM (em != 0): each epilogue thread holds its sum row's whole group;
+  // theta and the four bf16 planes of its tiles are rewritten, f_params not
+  int em;
+  float kappa, step;
+  int32_t* status;
+  __nv_bfloat16* mma;
+  int64_t plane;
+  const int32_t *slab_f, *slab_c;
+  float* theta_out;
 };
 
 // RS raw stages and 4 - RS operand stages (32-sample chunks): 2 / 2 for
@@ -152,6 +161,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __shared__ __align__(16) float cs[C::kRS][PF_KS];
   __shared__ int cols_p[C::kCPG];
   __shared__ int cols_w[4][C::kCPG];  // epilogue warps' column lists
+  __shared__ float em_wt[4][32 * 33];  // fused EM: a warp's updated 32 x 32 tile
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
   uint8_t* ops = smem + C::kRS * C::kRaw;
@@ -360,6 +370,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int er = q4 * 32 + lane;  // sum row within the tile (TMEM lane)
     int* cols = cols_w[warp - PF_EPI0];
     int acc_u = 0;
+    int em_inf = 0, em_bad = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const PfItem it = pf_item(a, item);
       if (!pf_active(it)) continue;
@@ -396,6 +407,98 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(as * PF_N) + ((uint32_t)(q4 * 32) << 16);
+      if constexpr (KN == 32) {
+        if (a.em) {
+          // pass 1: the row's group total sum(F + k) over all its columns
+          float tot = 0.f;
+          for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) th[i] = thn[i];
+            if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
+            float v[16];
+            tmem_ld16(tbase + c0, v);
+            if (!live) continue;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) tot += ((th[i] != 0.f) ? th[i] * v[i] : 0.f) + a.kappa;
+          }
+          const bool inf_row = live && tot > 0.f;
+          const float inv = inf_row ? 1.f / tot : 0.f;
+          em_inf += inf_row;
+          // pass 2: blend, store theta, pack the sum-major planes; stage the
+          // tile for the product-major planes
+          if (live) load_th(tile_of(0), thn);
+          float* wt = em_wt[warp - PF_EPI0];
+          for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) th[i] = thn[i];
+            if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
+            float v[16];
+            tmem_ld16(tbase + c0, v);
+            const int c = cols[c0 / KN];
+            const int j0 = c0 % KN;
+            if (live) {
+              float nt[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float f = (th[i] != 0.f) ? th[i] * v[i] : 0.f;
+                const float n = (f + a.kappa) * inv;
+                nt[i] = inf_row ? ((a.step >= 1.f) ? n : ((1.f - a.step) * th[i] + a.step * n))
+                                : th[i];
+                if (inf_row && !isfinite(nt[i])) ++em_bad;
+              }
+              const int64_t tile = __ldg(a.param_ids + rowbase + c);
+              float* tp = a.theta_out + tile + mm * KN + j0;
+              if ((tile & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                  *reinterpret_cast<float4*>(tp + i) = make_float4(nt[i], nt[i + 1], nt[i + 2], nt[i + 3]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) tp[i] = nt[i];
+              }
+              __nv_bfloat16* fpl = a.mma + __ldg(a.slab_f + rowbase + c);
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                float e8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) e8[e] = nt[8 * h2 + e];
+                uint4 hi, lo;
+                split_pack8(e8, hi, lo);
+                uint8_t* dst = reinterpret_cast<uint8_t*>(fpl) +
+                               (uint32_t)tile_off(mm, j0 + 8 * h2, KN) * 2u;
+                *reinterpret_cast<uint4*>(dst) = hi;
+                *reinterpret_cast<uint4*>(dst + a.plane * 2) = lo;
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) wt[lane * 33 + j0 + i] = nt[i];
+            }
+            if (j0 + 16 == KN) {  // the warp's 32 x 32 tile is complete
+              __syncwarp();
+              if (live) {
+                __nv_bfloat16* cpl = a.mma + 2 * a.plane + __ldg(a.slab_c + rowbase + c);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int q = lane + 32 * k, j = q >> 2, g8 = (q & 3) * 8;
+                  float e8[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) e8[e] = wt[(g8 + e) * 33 + j];
+                  uint4 hi, lo;
+                  split_pack8(e8, hi, lo);
+                  uint8_t* dst = reinterpret_cast<uint8_t*>(cpl) + (uint32_t)tile_off(j, g8, KN) * 2u;
+                  *reinterpret_cast<uint4*>(dst) = hi;
+                  *reinterpret_cast<uint4*>(dst + a.plane * 2) = lo;
+                }
+              }
+              __syncwarp();
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
+          ++acc_u;
+          continue;
+        }
+      }
       for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) th[i] = thn[i];
@@ -434,6 +537,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
       ++acc_u;
     }
+    if (a.em) {
+      for (int o = 16; o > 0; o >>= 1) {
+        em_inf += __shfl_xor_sync(0xffffffffu, em_inf, o);
+        em_bad += __shfl_xor_sync(0xffffffffu, em_bad, o);
+      }
+      if (lane == 0 && em_inf) atomicAdd(a.status, em_inf);
+      if (lane == 0 && em_bad) atomicAdd(a.status + 1, em_bad);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -469,6 +580,7 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   const int base = a.n_items * a.cgroups * a.mtiles;
   a.n_items = base * a.kslices;
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
+  if (a.em && (a.kslices != 1 || a.cgroups != 1)) return PCB_USAGE;  // needs whole rows
   CUtensorMap tr, tR, te, tr128, tRt, te256;
   if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, PF_SWZ) ||
       make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, C::kRP / 4, 0) ||
@@ -503,7 +615,7 @@ bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B) {
 
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
-                         const float* scratch, float* f_params) {
+                         const float* scratch, float* f_params, const PfEm* em) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   PfArgs a{};
@@ -523,6 +635,17 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   a.theta = theta;
   a.f_params = f_params;
   a.store = g.exclusive;
+  if (em) {
+    a.em = 1;
+    a.kappa = em->kappa;
+    a.step = em->step;
+    a.status = em->status;
+    a.mma = em->mma;
+    a.plane = em->plane;
+    a.slab_f = g.param_slab;
+    a.slab_c = g.param_slab_c;
+    a.theta_out = em->theta;
+  }
   // dense layers (several 256-child column groups) re-read operands from L2:
   // a deeper raw ring pays there
   const bool dense = g.cap * L.k_n > PF_N;

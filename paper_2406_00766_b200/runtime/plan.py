@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 21
+VERSION = 22
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -485,6 +485,82 @@ def em_tile_blocks(compiled, t_start, t_slab_f, t_slab_c, t_km, t_kn):
     return out, np.flatnonzero(~covered).astype(np.int64)
 
 
+def em_fused_order(compiled, tb, tensor_cores: bool):
+    """EM fused into the parameter-flow epilogue (one-process lean steps).
+
+    A layer qualifies when its blocks are 32 x 32, every sum row's children
+    fit one 256-column item (cap * k_n <= 256), its flow tiles have a single
+    writer, and each of its sum blocks is exactly one EM tile block (group i =
+    row i of the block's tiles, no tile shared with another sum block): the
+    epilogue thread of a sum row then holds the row's whole group.  The tile
+    blocks are reordered: blocks of other layers first (n_pre of them), then
+    each qualifying layer's blocks contiguously.  Returns (tb, n_pre,
+    per-layer [lo, hi) ranges, per-layer flags)."""
+    nl = len(compiled.layers)
+    nb = int(tb["blk_km"].size)
+    none = (tb, nb, [(0, 0)] * nl, [False] * nl)
+    if nb == 0 or not tensor_cores:
+        return none
+    off = tb["blk_tile_off"]
+    by_tiles = {}
+    for b in range(nb):
+        if int(tb["blk_km"][b]) == 32 and int(tb["blk_kn"][b]) == 32:
+            by_tiles[frozenset(tb["tile_start"][off[b]:off[b + 1]].tolist())] = b
+    # tiles used by more than one (layer, sum block): their flows have several
+    # producers, so no single epilogue sees a whole group
+    uses = {}
+    for L in compiled.layers:
+        for g in L.fwd_groups:
+            for t in np.asarray(g.param_ids, dtype=np.int64).ravel().tolist():
+                if t:
+                    uses[t] = uses.get(t, 0) + 1
+    owner = np.full(nb, -1, dtype=np.int64)
+    fus = [False] * nl
+    for li, L in enumerate(compiled.layers):
+        if not tc_layer(L) or int(L.k_m) != 32 or int(L.k_n) != 32 or not L.fwd_groups:
+            continue
+        ok, mine = True, []
+        for g in L.fwd_groups:
+            pid = np.asarray(g.param_ids, dtype=np.int64)
+            if g.prod_ids.shape[1] * 32 > 256:
+                ok = False
+                break
+            for row in pid:
+                t = row[row != 0]
+                b = by_tiles.get(frozenset(t.tolist()))
+                if b is None or t.size != np.unique(t).size or owner[b] >= 0 or \
+                        off[b + 1] - off[b] != t.size or any(uses[x] != 1 for x in t.tolist()):
+                    ok = False
+                    break
+                mine.append(b)
+            if not ok:
+                break
+        if ok and mine:
+            owner[np.asarray(mine)] = li
+            fus[li] = True
+    key = np.where(owner >= 0, owner, -1)
+    order = np.argsort(key, kind="stable")
+    n_pre = int((owner < 0).sum())
+    sizes = np.diff(off)[order]
+    tidx = np.repeat(off[:-1][order] - np.concatenate([[0], np.cumsum(sizes)[:-1]]), sizes) + \
+        np.arange(int(sizes.sum()), dtype=np.int64)
+    goff = np.concatenate([[0], np.cumsum(tb["blk_km"])])
+    gsz = tb["blk_km"][order]
+    gidx = np.repeat(goff[:-1][order] - np.concatenate([[0], np.cumsum(gsz)[:-1]]), gsz) + \
+        np.arange(int(gsz.sum()), dtype=np.int64)
+    out = dict(blk_km=tb["blk_km"][order], blk_kn=tb["blk_kn"][order],
+               blk_tile_off=np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64),
+               blk_groups=tb["blk_groups"][gidx],
+               tile_start=tb["tile_start"][tidx], tile_slab_f=tb["tile_slab_f"][tidx],
+               tile_slab_c=tb["tile_slab_c"][tidx])
+    ks = key[order]
+    ranges = []
+    for li in range(nl):
+        idx = np.flatnonzero(ks == li)
+        ranges.append((int(idx[0]), int(idx[-1]) + 1) if idx.size else (0, 0))
+    return out, n_pre, ranges, fus
+
+
 def pf_contig_flags(g, offs, mem, k_m: int, k_n: int) -> np.ndarray:
     """Per (full-stack) super-row: bit 0 = its member sum blocks are
     consecutive sum rows, bit 1 = its real child blocks are consecutive
@@ -694,6 +770,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(folded(g.flow_ids))
             fslab = _slab_of(g.param_ids, t_start, t_slab_f) if use_tc else np.zeros(0, np.int64)
             ref(fslab)
+            # product-major plane offsets (EM fused into the parameter flows)
+            ref(_slab_of(g.param_ids, t_start, t_slab_c) if use_tc else np.zeros(0, np.int64))
             prog.append(exclusive(g))
             # every row has the same child blocks: one shift row serves them all
             prog.append(int(rows > 0 and group_matrix_rows(g.prod_ids)[1].size == 1))
@@ -801,6 +879,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
     ref(c.group_off)
     # EM tile blocks (groups that exactly tile tensor-core tiles) + the rest
     tb, rest = em_tile_blocks(c, t_start, t_slab_f, t_slab_c, t_km, t_kn)
+    tb, n_em_pre, em_ranges, em_fusable = em_fused_order(c, tb, tensor_cores)
     prog.append(int(tb["blk_km"].size))
     prog.append(int(tb["tile_start"].size))
     tb["blk_goff"] = np.concatenate([[0], np.cumsum(tb["blk_km"])]).astype(np.int64)
@@ -839,10 +918,13 @@ def build_program(compiled, *, tensor_cores: bool = True):
     prog.append(int(n_rmax))
     prog.append(n_small_noninl)
     prog.append(int(in_inline_ok))
+    prog.append(int(n_em_pre))
+    for (lo, hi), fz in zip(em_ranges, em_fusable):
+        prog += [int(lo), int(hi), int(fz)]
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,
-            "pre_ratio_layers": int(sum(pre_ratio)), "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+            "pre_ratio_layers": int(sum(pre_ratio)), "em_fused_layers": int(sum(em_fusable)), "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
