@@ -95,22 +95,56 @@ def synthetic_batches(c, w, B, count, seed):
             for _ in range(count)]
 
 
-def algorithmic_bytes(c, B):
-    """Minimal fp32 HBM bytes per step per kernel class."""
+def fused_em_bytes(c, info, B, sms=148):
+    """(edges of the layers whose EM runs in the parameter-flow epilogue at
+    batch B, staged input pmf entries updated in the input-flow pass): the
+    plan's em-fusable layers whose parameter flows are unsplit (the C side's
+    pf_kslices == 1 for every group)."""
+    from paper_2406_00766_b200.runtime.plan import tc_super_rows
+    e_f = 0
+    for li in info.get("em_fused_layer_ids", []):
+        L = c.layers[li]
+        ok, e = True, 0
+        for g in L.fwd_groups:
+            offs, _ = tc_super_rows(g.prod_ids, L.k_m, min_count=0)
+            cg = -(-int(g.prod_ids.shape[1]) * int(L.k_n) // 256)
+            base = (offs.size - 1) * cg * 2
+            ks = max(1, min(-(-2 * sms // max(base, 1)), (-(-B // 32)) // 2))
+            ok = ok and ks == 1
+            e += int((np.asarray(g.param_ids) != 0).sum()) * int(L.k_m) * int(L.k_n)
+        e_f += e if ok else 0
+    n_pmf = 0
+    if info.get("input_inline_em"):
+        n_pmf = sum(int(ch.param_ids.size) * int(ch.num_categories) for ch in c.input_layer)
+    return e_f, n_pmf
+
+
+def algorithmic_bytes(c, B, info=None):
+    """Minimal fp32 HBM bytes per step per kernel class for
+    the lean training step: products stay resident (evaluated once), the
+    first layer's products alias their inputs when the plan allows it, and
+    the fused push moves each pushed product flow to its children once."""
+    info = info or {}
     n_in = sum(int(ch.node_ids.size) for ch in c.input_layer)
     n_sum = sum(int(L.report.num_sums) for L in c.layers)
-    n_prod = sum(int(L.report.num_prods) for L in c.layers)
-    F = sum(int(ev.children.size) for L in c.layers for ev in L.prod_evals)
+    skip = 1 if info.get("leaf_alias") else 0  # aliased first layer: no product pass / push
+    n_prod = sum(int(L.report.num_prods) for L in c.layers[skip:])
+    F = sum(int(ev.children.size) for L in c.layers[skip:] for ev in L.prod_evals)
     E = c.num_edges
+    n_pmf = sum(int(ch.param_ids.size) * int(ch.num_categories) for ch in c.input_layer)
     return {
-        "input_fwd": B * (4 * c.num_vars + 8 * n_in),
-        "prod_eval": 2 * B * 4 * (F + n_prod),            # forward + backward recompute
+        # batch + value rows + each pmf once
+        "input_fwd": B * 4 * (c.num_vars + n_in) + 4 * n_pmf,
+        "prod_eval": B * 4 * (F + n_prod),
         "sum_fwd_tc": B * 4 * (n_prod + n_sum) + 4 * E,
         "sum_fwd_simt": B * 4 * (n_prod + n_sum) + 4 * E,
-        "param_flow": B * 4 * (2 * n_sum + n_prod) + 8 * E,
-        "child_flow": B * 4 * (2 * n_sum + 2 * n_prod),
-        "accum_push": B * 4 * (3 * n_prod + 3 * F),
-        "input_flow": B * 12 * n_in,
+        # ratio rows + product values; theta read + flow write per edge
+        "param_flow": B * 4 * (n_sum + n_prod) + 8 * E,
+        # ratio rows + product values + product-flow rows; bf16 hi/lo planes
+        "child_flow": B * 4 * (n_sum + 2 * n_prod) + 4 * E,
+        "accum_push": B * 4 * (n_prod + F + n_sum),  # product flows, child rows, sum values
+        # flow rows + batch + pmf read (missing-value spread) and flow write
+        "input_flow": B * 4 * (n_in + c.num_vars) + 8 * n_pmf,
         "em": 20 * c.theta_size,
     }
 
@@ -324,9 +358,13 @@ def run_ours(args, w):
     prof_steps = max(1, min(3, args.steps))
     _lib.profile_enable(True)
     _lib.profile_read()
-    for i in range(prof_steps):  # eager: the class timers are host-side event pairs
+    # eager: the class timers are host-side event pairs; the side-stream
+    # overlap is switched off so each class is timed on its own
+    ts.lean_mode = 2
+    for i in range(prof_steps):
         ts._eager(dev_batches[i % n_pool])
     torch.cuda.synchronize()
+    ts.lean_mode = 1
     prof = _lib.profile_read()
     _lib.profile_enable(False)
 
@@ -335,7 +373,20 @@ def run_ours(args, w):
             dist.destroy_process_group()
         return
     hbm, tflops, peak_src = measured_peaks()
-    algo = algorithmic_bytes(c, B)
+    algo = algorithmic_bytes(c, B, ts.plan.info)
+    # one-process steps fold EM into the input-flow and parameter-flow passes
+    # (DESIGN §3a): the EM class then covers only the small layers' groups, and
+    # the per-class minimal bytes above (unfused) no longer describe it
+    inline_em = bool(getattr(ts, "_inline_em", False))
+    if inline_em:
+        algo.pop("em", None)
+        # the fused EM's extra minimal bytes: theta write + four bf16 planes
+        # instead of the flow write per edge of the layers whose parameter
+        # flows run unsplit, theta read + write instead of the flow write per
+        # staged input pmf entry
+        e_f, n_pmf = fused_em_bytes(c, ts.plan.info, B)
+        algo["param_flow"] += 8 * e_f
+        algo["input_flow"] += 4 * n_pmf
     classes = {k: v for k, v in prof.items() if v[0] > 0}
     total_prof = sum(v[0] for v in classes.values())
     dom = max(classes, key=lambda k: classes[k][0])
@@ -354,12 +405,6 @@ def run_ours(args, w):
                 "kernel_ms_per_step": per_step_ms,
                 "launches_per_step": dom_launches / prof_steps,
                 "share_of_step": dom_ms / total_prof if total_prof else None}
-    # one-process steps fold EM into the input-flow and parameter-flow passes
-    # (DESIGN §3a): the EM class then covers only the small layers' groups, and
-    # the per-class minimal bytes above (unfused) no longer describe it
-    inline_em = bool(getattr(ts, "_inline_em", False))
-    if inline_em:
-        algo.pop("em", None)
     breakdown = {k: {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[2] / prof_steps,
                      "gbs": (algo[k] / (v[0] / prof_steps / 1000.0) / 1e9)
                      if k in algo and v[0] > 0 else None}

@@ -86,7 +86,7 @@ int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta);
  * d_values / d_flows and the aliased products' d_prod_flows rows are then not
  * written.  Host-side setting read at launch time (also while a CUDA graph
  * records); default 0. */
-int pcb_plan_set_lean(pcb_plan* plan, int lean);
+int pcb_plan_set_lean(pcb_plan* plan, int lean);  /* 2: lean, side stream serialised (profiling) */
 
 /* Inline input EM for single-process lean steps (no flow all-reduce between
  * the backward pass and EM): while enabled, a lean pcb_backward on the plan's

@@ -303,7 +303,7 @@ int pcb_plan_set_inline_em(pcb_plan* plan, int enable, float pseudocount, float 
 
 int pcb_plan_set_lean(pcb_plan* plan, int lean) {
   if (!plan) return PCB_USAGE;
-  plan->lean = lean ? 1 : 0;
+  plan->lean = lean == 2 ? 2 : (lean ? 1 : 0);
   return PCB_OK;
 }
 
@@ -481,7 +481,7 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     if (st) return st;
   }
   cudaStream_t sp = s;
-  if (fused && L.pre_ratio && P->side) {
+  if (fused && L.pre_ratio && P->side && P->lean != 2) {
     if (cudaEventRecord(P->ev_fork, s) != cudaSuccess ||
         cudaStreamWaitEvent(P->side, P->ev_fork, 0) != cudaSuccess)
       return PCB_CUDA;

@@ -924,7 +924,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,
-            "pre_ratio_layers": int(sum(pre_ratio)), "em_fused_layers": int(sum(em_fusable)), "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
+            "pre_ratio_layers": int(sum(pre_ratio)), "em_fused_layers": int(sum(em_fusable)),
+            "em_fused_layer_ids": [li for li, f in enumerate(em_fusable) if f], "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total}
     return np.asarray(prog, dtype=np.int64), blob.array(), info

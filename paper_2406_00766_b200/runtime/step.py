@@ -42,6 +42,7 @@ class TrainStep:
         # one process: no flow all-reduce between backward and EM, so the
         # input-flow pass may apply EM to the inputs' pmfs (pcb_plan_set_inline_em)
         self._inline_em = allreduce is None
+        self.lean_mode = 1  # 2: no side-stream overlap (per-kernel profiling)
         self.graph = None
         self.ll = None
         self.launches_per_step = None
@@ -55,7 +56,7 @@ class TrainStep:
                   b.xT.data_ptr())
         # lean launches: the step never reads node values / flows, so aliased
         # leaf products skip their evaluation and push (pcb_plan_set_lean)
-        _lib.call("pcb_plan_set_lean", p.handle, 1)
+        _lib.call("pcb_plan_set_lean", p.handle, self.lean_mode)
         if self._inline_em:
             _lib.call("pcb_plan_set_inline_em", p.handle, 1, self.pseudocount, self.step_size,
                       p.status.data_ptr())
