@@ -597,10 +597,13 @@ int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32
   const Work w = carve(plan, ldb, d_work);
   {
     ProfScope prof_(KC_MISC, s);
-    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * (plan->fp_cover ? zero_tile(plan)
-                                                                       : plan->f_params_size),
-                        s) != cudaSuccess)
-      return PCB_CUDA;
+    // replica ranges (past theta_size) are folded onto their master tiles and
+    // never written: a lean step, whose EM reads only [0, theta_size), leaves
+    // them alone
+    const int64_t fp_n = plan->fp_cover ? zero_tile(plan)
+                         : plan->lean  ? plan->theta_size
+                                       : plan->f_params_size;
+    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * fp_n, s) != cudaSuccess) return PCB_CUDA;
     if (!B) return PCB_OK;
     // only rows that accumulate (several pushes) or receive none need zeros;
     // single-push rows are stored by their push
