@@ -132,3 +132,58 @@ def test_inline_em_matches_separate_pass(batch):
         np.testing.assert_array_equal(sts[i], plan.status[:2].cpu().numpy())
         np.testing.assert_allclose(ths[i], plan.theta.double().cpu().numpy(), rtol=1e-5,
                                    atol=1e-12)
+
+
+def _lean_step_vs_oracle(c, x, pseudocount=1e-4, step=0.2):
+    """One one-process TrainStep (lean launches, inline EM where the plan
+    allows it, CUDA graph) against the float64 oracle's forward / backward /
+    mini-batch EM on the same batch."""
+    import torch
+    from paper_2406_00766_b200.runtime.em import apply_theta
+    from paper_2406_00766_b200.runtime.step import TrainStep
+    theta0 = c.theta.copy()
+    apply_theta(c, c.theta)
+    ts = TrainStep(c, x.shape[0], pseudocount=pseudocount, step_size=step, graph=True)
+    ll = float(ts.run(torch.from_numpy(x.astype(np.int32)).cuda()).item())
+    got = ts.plan.theta.double().cpu().numpy()
+    lr, rb = oracle.forward(c, x, theta=theta0)
+    oracle.backward(c, rb, theta=theta0)
+    new = oracle.em_step_full(c, rb.f_params, theta=theta0, pseudocount=pseudocount)
+    want = oracle.em_step_mini(theta0, new, step)
+    assert abs(ll - lr.sum()) <= 1e-4 * abs(lr.sum())
+    nz = np.abs(want) > 1e-6
+    assert np.max(np.abs(got[nz] - want[nz]) / np.abs(want[nz])) < 1e-4
+    apply_theta(c, theta0)
+
+
+@pytest.mark.parametrize("kind", ["pd", "ratspn", "hmm_untied", "hclt16"])
+def test_lean_train_step_other_structures(kind):
+    """The lean / inline-EM training step on every generator family: each
+    restructuring (leaf alias, fused push + ratio, side-stream parameter
+    flows, inline input EM, fused tile EM) applies only where the plan proves
+    it, and the step still matches the oracle elsewhere."""
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    rng = np.random.default_rng(21)
+    if kind == "pd":
+        g = S.build_pd(S.StructureConfig(kind="pd", shape=(3, 4), hidden_dim=3,
+                                         num_categories=5, seed=4))
+        c = compile_circuit(g, CompileConfig(block_size=32))
+        x = rng.integers(0, 5, size=(150, 12))
+    elif kind == "ratspn":
+        g = S.build_ratspn(S.StructureConfig(kind="ratspn", num_vars=16, depth=3, hidden_dim=4,
+                                             num_categories=8, num_repetitions=6, seed=3))
+        c = compile_circuit(g, CompileConfig(block_size=32))
+        x = rng.integers(0, 8, size=(200, 16))
+    elif kind == "hmm_untied":
+        g = S.build_structure(S.StructureConfig(kind="hmm", seq_len=6, hidden_dim=64,
+                                                vocab_size=30, seed=5, tied=False))
+        c = compile_circuit(g, CompileConfig(block_size=32))
+        x = rng.integers(0, 30, size=(64, 6))  # unsplit parameter flows: fused tile EM
+    else:
+        g = S.build_hclt(S.StructureConfig(kind="hclt", num_vars=40, hidden_dim=32,
+                                           num_categories=16, seed=6))
+        c = compile_circuit(g, CompileConfig(block_size=16))
+        x = rng.integers(0, 16, size=(96, 40))
+    x[rng.random(x.shape) < 0.1] = -1
+    _lean_step_vs_oracle(c, x)
