@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libpcirc_b200.so"
-SOURCES = ["pcb_simt.cu", "pcb_tc.cu", "pcb_tc_sum.cu", "pcb_tc_ws.cu", "pcb_tc_pf.cu", "pcb_capi.cu"]
+SOURCES = ["pcb_simt.cu", "pcb_tc.cu", "pcb_tc_ws.cu", "pcb_tc_pf.cu", "pcb_capi.cu"]
 HEADERS = ["pcb_internal.cuh", "pcb_tc.cuh", "pcb_ws.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

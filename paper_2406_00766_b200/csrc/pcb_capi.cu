@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 22;
+constexpr int64_t kVersion = 23;
 
 struct Reader {
   const int64_t* p;
@@ -68,6 +68,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   P->root_slot = r.get();
   P->root_row = r.get();
   P->root_children = r.ref(&P->n_root_children);
+  P->root_cb = r.ref();
+  P->root_vb = r.get();
   P->var_ncat = r.ref();
   P->use_tc = (int)r.get();
   P->n_mma_tiles = r.get();
@@ -191,6 +193,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     }
     L.prow_off = r.ref();
     L.prow_ch = r.ref();
+    L.prow_cb = r.ref();
     L.sb_base = r.get();
     L.n_sb = r.get();
     L.push_flag = r.ref();
@@ -207,6 +210,10 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.pre_ratio = (int)r.get();
     L.rmax_off = r.get();
     L.n_pb = L.window / L.k_n;  // including the -inf pad block 0
+    L.pb_off = P->n_pb_tot;
+    L.vb_off = P->n_sb_tot;
+    P->n_pb_tot += L.n_pb;
+    P->n_sb_tot += L.n_sb;
     if (L.n_pb > P->max_pb) P->max_pb = L.n_pb;
     if (L.n_sb > P->max_sb) P->max_sb = L.n_sb;
     if (L.n_sb * L.k_m > P->max_sum_rows) P->max_sum_rows = L.n_sb * L.k_m;
@@ -367,11 +374,12 @@ __global__ void k_nonfinite(int64_t n, const float* __restrict__ x, int32_t* cnt
 
 Work carve(const pcb_plan* P, int ldb, float* d_work) {
   Work w;
-  w.bmax = d_work;
-  w.rmax = d_work + P->max_pb * (int64_t)ldb;
+  w.vbase = d_work;
+  w.pbase = w.vbase + P->n_sb_tot * (int64_t)ldb;
+  w.rmax = w.pbase + P->n_pb_tot * (int64_t)ldb;
   w.ratio = w.rmax + P->max_sb * (int64_t)ldb;
   w.gshift = w.ratio + P->max_sum_rows * (int64_t)ldb;
-  w.rmax_all = w.gshift + P->max_tc_rows * (int64_t)ldb;
+  w.rmax_all = w.gshift + 2 * P->max_tc_rows * (int64_t)ldb;
   w.counters = reinterpret_cast<int32_t*>(w.rmax_all + P->n_rmax * (int64_t)ldb);
   return w;
 }
@@ -393,26 +401,26 @@ bool lean_alias(const pcb_plan* P, const Layer& L) {
 int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
                   const float* theta, float* values, float* scratch_all, const Work& w) {
   float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
+  float* pbase = w.pbase + L.pb_off * (int64_t)ldb;
+  float* vbase = w.vbase + L.vb_off * (int64_t)ldb;
   int st;
   if (lean_alias(P, L)) {
-    // the input pass wrote the product rows and block maxima: only the
+    // the input pass wrote the product rows and block bases: only the
     // window's padding rows / blocks need -inf
     st = launch_fill(s, L.pad_rows, L.n_pad, B, ldb, scratch, PCB_NEG_INF);
-    if (!st) st = launch_fill(s, P->alias_pad, P->n_alias_pad, B, ldb, w.bmax, PCB_NEG_INF);
+    if (!st) st = launch_fill(s, P->alias_pad, P->n_alias_pad, B, ldb, pbase, PCB_NEG_INF);
   } else {
-    st = launch_prod_eval(L, s, B, ldb, values, scratch, w.bmax);
+    st = launch_prod_eval(L, s, B, ldb, values, w.vbase, scratch, pbase);
   }
   if (st) return st;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.fwd_tc[g];
-    if (P->use_tc && T.count > 0 && tc_supported(L))
-      st = (P->use_tc == 1 && ws_supported((int)L.k_n, (int)L.k_m))
-               ? launch_sum_fwd_ws(P, L, L.fwd[g], ws_long_k(L.fwd[g].cap) ? L.pf_tc[g] : T, s,
-                                   B, ldb, scratch, w.bmax, values, w.gshift, w.counters,
-                                   L.fwd.size() == 1)
-               : launch_sum_fwd_tc(P, L, L.fwd[g], T, s, B, ldb, scratch, w.bmax, values);
+    if (P->use_tc && T.count > 0 && tc_supported(L) && ws_supported((int)L.k_n, (int)L.k_m))
+      st = launch_sum_fwd_ws(P, L, L.fwd[g], ws_long_k(L.fwd[g].cap) ? L.pf_tc[g] : T, s, B, ldb,
+                             scratch, pbase, values, vbase, w.gshift, w.counters,
+                             L.fwd.size() == 1);
     else
-      st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, values);
+      st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, pbase, values, vbase);
     if (st) return st;
   }
   return PCB_OK;
@@ -429,20 +437,18 @@ int child_flows(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ld
                 const float* theta, const float* values, const float* flows, float* scratch,
                 float* flow_scratch, const float* ratio, const float* rmax, bool tc,
                 const Work& w) {
+  const float* pbase = w.pbase + L.pb_off * (int64_t)ldb;
+  const float* vbase = w.vbase + L.vb_off * (int64_t)ldb;
   for (size_t g = 0; g < L.bwd.size(); ++g) {
     const TcRows& T = L.bwd_tc[g];
     int st;
-    if (tc && T.count > 0)
-      st = (P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
-               ? launch_child_flow_ws(P, L, L.bwd[g],
-                                      ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T, s, B, ldb,
-                                      ratio, scratch, rmax, flow_scratch, w.gshift,
-                                      w.counters, L.bwd.size() == 1)
-               : launch_child_flow_tc(P, L, L.bwd[g], T, s, B, ldb, values, flows, scratch,
-                                      w.rmax, flow_scratch);
+    if (tc && T.count > 0 && P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
+      st = launch_child_flow_ws(P, L, L.bwd[g], ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T,
+                                s, B, ldb, ratio, scratch, rmax, vbase, pbase, flow_scratch,
+                                w.gshift, w.counters, L.bwd.size() == 1);
     else
-      st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch,
-                                  flow_scratch);
+      st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch, pbase,
+                                  vbase, flow_scratch);
     if (st) return st;
   }
   return PCB_OK;
@@ -453,7 +459,10 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
                    float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
   float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
   int st = PCB_OK;
-  const bool tc = P->use_tc && tc_bwd_supported(L);
+  // tensor-core flows: the persistent kernels (K blocks 16 / 32); other
+  // block sizes take the SIMT kernels
+  const bool tc = P->use_tc == 1 && tc_bwd_supported(L) && ws_supported((int)L.k_m, (int)L.k_n) &&
+                  pf_ws_supported(L);
   const bool fused = P->lean && P->push_ratio_ok;
   // pre-ratioed layers (fused push): the flow rows already hold the ratios
   const float* ratio = w.ratio;
@@ -495,17 +504,16 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
       cudaMemsetAsync(f_params + L.flow_lo, 0, sizeof(float) * (L.flow_hi - L.flow_lo), sp) !=
           cudaSuccess)
     return PCB_CUDA;
+  const float* pbase = w.pbase + L.pb_off * (int64_t)ldb;
+  const float* vbase = w.vbase + L.vb_off * (int64_t)ldb;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
-      st = (P->use_tc == 1 && pf_ws_supported(L))
-               ? launch_param_flow_ws(L, L.fwd[g], T, sp, B, ldb, theta, ratio, rmax, scratch,
-                                      f_params, em_fuse ? &em : nullptr)
-               : launch_param_flow_tc(L, L.fwd[g], T, sp, B, ldb, theta, values, flows, scratch,
-                                      w.rmax, f_params);
+      st = launch_param_flow_ws(L, L.fwd[g], T, sp, B, ldb, theta, ratio, rmax, scratch, vbase,
+                                pbase, f_params, em_fuse ? &em : nullptr);
     else
-      st = launch_param_flow_simt(L, L.fwd[g], sp, B, ldb, theta, values, flows, scratch,
-                                  f_params);
+      st = launch_param_flow_simt(L, L.fwd[g], sp, B, ldb, theta, values, flows, scratch, pbase,
+                                  vbase, f_params);
     if (st) return st;
   }
   if (em_fuse) {
@@ -562,7 +570,8 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
   // + one split-K arrival counter per (super-row, 128-sample tile)
-  return (plan->max_pb + plan->max_sb + plan->max_sum_rows + plan->max_tc_rows + plan->n_rmax) *
+  return (plan->n_sb_tot + plan->n_pb_tot + plan->max_sb + plan->max_sum_rows +
+          2 * plan->max_tc_rows + plan->n_rmax) *
              (int64_t)ldb +
          plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }
@@ -578,13 +587,13 @@ int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_
   // rows included) is written below, so only the reserved constant rows need it.
   int st = launch_fill_range(s, 0, plan->reserved, B, ldb, d_values, PCB_NEG_INF);
   if (st) return st;
-  st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values, d_scratch, w.bmax);
+  st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values, d_scratch, w.pbase);
   if (st) return st;
   for (auto& L : plan->layers) {
     st = layer_forward(plan, L, s, B, ldb, d_theta, d_values, d_scratch, w);
     if (st) return st;
   }
-  return launch_root_fwd(plan, s, B, ldb, d_values, d_lroot);
+  return launch_root_fwd(plan, s, B, ldb, d_values, w.vbase, d_lroot);
 }
 
 int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,

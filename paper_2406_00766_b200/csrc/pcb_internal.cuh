@@ -85,8 +85,10 @@ struct Layer {
   std::vector<Bucket> pushes;
   // derived tables (plan v3)
   const int32_t *prow_off, *prow_ch;  // per scratch row: product children CSR
+  const int32_t* prow_cb;             // per CSR child: its value block's vbase row, -1 = base 0
   int64_t sb_base, n_sb;              // sum blocks of the layer: slots [sb_base, +n_sb*k_m)
   int64_t n_pb;                       // product blocks in the window incl. pad block 0
+  int64_t pb_off = 0, vb_off = 0;     // first pbase / vbase row of the layer
   // fused accumulate + push, product order: flag bit0 push, bit1 first
   // accumulation (store); push_ch = slot * 2 + (single push into the slot)
   const int32_t *push_flag, *push_off, *push_ch;
@@ -106,15 +108,30 @@ struct Layer {
   int64_t rmax_off = -1;  // its R rows in the all-layer rmax region
 };
 
+// Log values are stored as (integer base, fp32 offset) pairs: every value
+// row of a block holds l - base, the base is one integer-valued fp32 per
+// (block, sample).  Bases add exactly (|base| < 2^24), so differences of
+// log values of any magnitude (|log p| ~ 1.7e4 at 3072 variables, where the
+// fp32 spacing is 2^-9) are formed from small offsets and exact integer
+// base differences: flows keep full fp32 relative precision.
+//   inputs                      base 0 (log-pmf rows)
+//   sum block (vbase row)       G = max of its child blocks' bases (the
+//                               sum kernels' shift), offsets ln D
+//   product block (pbase row)   floor(max_j (sum of its children's bases +
+//                               offsets)), -inf for an all -inf block
 // Workspace carved from the caller's d_work buffer (pcb_plan_workspace_floats):
-//   bmax [max_pb x ldb]  per product block and sample: max child log value
-//   rmax [max_sb x ldb]  per sum block and sample: max lg2(flow) - value*log2(e)
+//   vbase [n_sb_tot x ldb]  per sum block (all layers) and sample
+//   pbase [n_pb_tot x ldb]  per product block (all layers' windows, pad
+//                           block 0 included) and sample
+//   rmax [max_sb x ldb]  per sum block and sample: max lg2(flow) - offset*log2(e)
 //   ratio [max_sum_rows x ldb] per sum row of the layer: log2 flow ratio minus
 //                               its block's rmax (k_ratio)
+//   gshift [2 max_tc_rows x ldb] per-(super-row, sample) shifts of long-K
+//                               layers (child flows: g rows, then base rows)
 //   counters [max_tc_rows x ldb/128] split-K arrivals (self-resetting, zeroed at allocation)
-//   gshift [max_tc_rows x ldb] per-(super-row, sample) shift of long-K layers
 struct Work {
-  float* bmax;
+  float* vbase;
+  float* pbase;
   float* rmax;
   float* ratio;
   float* gshift;
@@ -130,7 +147,9 @@ struct pcb_plan {
       f_params_size, reserved;
   int64_t root_slot, root_row;
   const int32_t* root_children;
+  const int32_t* root_cb;  // vbase row per root child (-1: base 0)
   int64_t n_root_children;
+  int64_t root_vb = -1;    // vbase row of a sum root's block
   const int32_t* var_ncat;
   std::vector<pcb::InputChunk> inputs;  // generic (gather / atomic) inputs
   pcb::InBlocks in_blocks;              // shared-memory staged inputs
@@ -152,6 +171,7 @@ struct pcb_plan {
   const float* theta_bound = nullptr;  // the plan's own theta (pcb_plan_set_theta)
   int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported)
   int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1, max_tc_rows = 1;
+  int64_t n_pb_tot = 0, n_sb_tot = 0;  // all layers' product / sum blocks (base rows)
   // bf16 tensor-core copies of theta tiles (plan v4)
   // bf16 planes: regions of mma_plane elements: [F hi][F lo][C hi][C lo];
   // tile t's sum-major planes at slab_f[t] (+ plane), its product-major
@@ -236,31 +256,37 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
 
 int check_launch();
 
-// SIMT kernels (pcb_simt.cu)
+// SIMT kernels (pcb_simt.cu).  Base rows: `pbase` / `vbase` point at the
+// layer's first product / sum block row (Layer::pb_off / vb_off), except
+// where noted.
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
-                     const float* theta, float* values, float* scratch_all, float* bmax);
+                     const float* theta, float* values, float* scratch_all, float* pbase_all);
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
-                     float* scratch, float* bmax);
+                     const float* vbase_all, float* scratch, float* pbase);
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
                      const float* flows, float* rmax, float* ratio);
 int launch_push_ratio(const Layer& L, cudaStream_t s, int B, int ldb, const float* flow_scratch,
                       const float* values, float* flows, float* rmax_all);
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
-                        const float* theta, const float* scratch, float* values);
+                        const float* theta, const float* scratch, const float* pbase,
+                        float* values, float* vbase);
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
-                           const float* scratch, float* f_params);
+                           const float* scratch, const float* pbase, const float* vbase,
+                           float* f_params);
 int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
-                           const float* scratch, float* flow_scratch);
+                           const float* scratch, const float* pbase, const float* vbase,
+                           float* flow_scratch);
 int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows);
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, const float* theta, const float* flows,
                              const float* flow_scratch, float* f_params, bool inline_em,
                              bool* inline_done);
+// vbase_all: the whole vbase region (root_vb / root_cb are global rows)
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
-                    float* lroot);
+                    const float* vbase_all, float* lroot);
 int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,
                     float* prod_flows);
 int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params);
@@ -284,18 +310,11 @@ int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, 
 int launch_zero_ranges(cudaStream_t s, int64_t n, const int32_t* start, const int32_t* len,
                        int ldb, float* buf);
 
-// tensor-core kernels (pcb_tc.cu)
-int launch_sum_fwd_tc(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
-                      cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values);
+// tensor-core support (pcb_tc.cu)
 bool tc_supported(const Layer& L);
 bool tc_bwd_supported(const Layer& L);
 int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta);
-int launch_param_flow_tc(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
-                         int B, int ldb, const float* theta, const float* values,
-                         const float* flows, const float* scratch, const float* rmax,
-                         float* f_params);
-// warp-specialised persistent variants (pcb_tc_ws.cu), K block 16 / 32
+// warp-specialised persistent tensor-core kernels (pcb_tc_ws.cu), K block 16 / 32
 bool ws_supported(int kc, int nb);
 // long contractions (>= 32 K blocks, e.g. HMM's 4096-wide layers) use full
 // 256-wide stacks and split K across CTAs; short ones keep more, narrower
@@ -304,19 +323,18 @@ inline bool ws_long_k(int64_t cap) { return cap >= 32; }
 // split_ok: the group owns its layer's output rows, so K may be split
 // across CTAs (partial sums reduced in place, finished by the last arrival)
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
-                      cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values, float* gshift, int32_t* counters, bool split_ok);
+                      cudaStream_t s, int B, int ldb, const float* scratch, const float* pbase,
+                      float* values, float* vbase, float* gshift, int32_t* counters,
+                      bool split_ok);
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
-                         const float* rmax, float* flow_scratch, float* gshift,
-                         int32_t* counters, bool split_ok);
+                         const float* rmax, const float* vbase, const float* pbase,
+                         float* flow_scratch, float* gshift, int32_t* counters, bool split_ok);
 bool pf_ws_supported(const Layer& L);
 bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
-                         const float* scratch, float* f_params, const PfEm* em = nullptr);
-int launch_child_flow_tc(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
-                         cudaStream_t s, int B, int ldb, const float* values, const float* flows,
-                         const float* scratch, const float* rmax, float* flow_scratch);
+                         const float* scratch, const float* vbase, const float* pbase,
+                         float* f_params, const PfEm* em = nullptr);
 
 }  // namespace pcb

@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(IN_THREADS)
   if (r0 >= 0) {
     // leaf alias (lean step): the inputs' log values are the product rows of
     // the first layer's window (row r0 + dir * i); whole product blocks, so
-    // the block maxima the sum kernels shift by are formed here
+    // the block bases (floor of the block maximum) are formed here and the
+    // rows hold offsets from them
     const int64_t step = (int64_t)__ldg(adir + blk) * ldb;
     for (int b = threadIdx.x; b < B; b += IN_THREADS) {
       const int x = xT[(int64_t)var * ldb + b];
@@ -184,12 +185,13 @@ __global__ void __launch_bounds__(IN_THREADS)
       for (int i0 = 0; i0 < cnt; i0 += kn) {
         float mx = PCB_NEG_INF;
 #pragma unroll 8
-        for (int i = i0; i < i0 + kn; ++i) {
-          const float v = x < 0 ? 0.f : t[i * ncat];
-          dst[i * step] = v;
-          mx = fmaxf(mx, v);
-        }
-        abmax[(int64_t)((r0 + (step > 0 ? i0 : -i0)) / kn) * ldb + b] = mx;
+        for (int i = i0; i < i0 + kn; ++i) mx = fmaxf(mx, x < 0 ? 0.f : t[i * ncat]);
+        const float base = floorf(mx);  // -inf stays -inf
+        const bool dead = mx == PCB_NEG_INF;
+#pragma unroll 8
+        for (int i = i0; i < i0 + kn; ++i)
+          dst[i * step] = dead ? PCB_NEG_INF : (x < 0 ? 0.f : t[i * ncat]) - base;
+        abmax[(int64_t)((r0 + (step > 0 ? i0 : -i0)) / kn) * ldb + b] = base;
       }
     }
     return;
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(IN_THREADS)
 }
 
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
-                     const float* theta, float* values, float* scratch_all, float* bmax) {
+                     const float* theta, float* values, float* scratch_all, float* pbase_all) {
   ProfScope prof_(KC_INPUT_FWD, s);
   const InBlocks& ib = p->in_blocks;
   if (ib.n) {
@@ -224,7 +226,8 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
     k_input_fwd_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, values,
         alias ? ib.alias_row : nullptr, ib.alias_dir,
-        alias ? scratch_all + L0->scratch_off * (int64_t)ldb : nullptr, bmax,
+        alias ? scratch_all + L0->scratch_off * (int64_t)ldb : nullptr,
+        alias ? pbase_all + L0->pb_off * (int64_t)ldb : nullptr,
         alias ? (int)L0->k_n : 1);
     if (check_launch()) return PCB_CUDA;
   }
@@ -239,23 +242,6 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
 }
 
 // ---------------------------------------------------------------- K2 products
-// scratch[out_j, b] = sum_f values[child_jf, b]; fan-in 0 rows are the -inf
-// padding of the layer window (engine.py:68-71).
-__global__ void k_prod_eval(int64_t n, int f, int B, int ldb, const int32_t* __restrict__ out,
-                            const int32_t* __restrict__ ch, const float* __restrict__ values,
-                            float* __restrict__ scratch) {
-  int64_t total = n * (int64_t)B;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t j = t / B;
-    int b = (int)(t - j * B);
-    float acc = 0.f;
-    const int32_t* c = ch + j * f;
-    for (int q = 0; q < f; ++q) acc += values[(int64_t)c[q] * ldb + b];
-    scratch[(int64_t)out[j] * ldb + b] = acc;
-  }
-}
-
 __global__ void k_fill_rows(int64_t n, int B, int ldb, const int32_t* __restrict__ rows,
                             float* __restrict__ buf, float v) {
   int64_t total = n * (int64_t)B;
@@ -312,10 +298,12 @@ int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, f
 }
 
 // One CTA per (product block, 128-sample slab): 8 warps stride over the
-// block's scratch rows, lane = 4 consecutive samples (float4).  Every row is
-// the sum of its children's log values (-inf for window padding); the
-// per-sample block maximum goes to bmax (reduced across warps in shared
-// memory) so the sum contraction needs no max pre-pass.
+// block's scratch rows, lane = 4 consecutive samples (float4).  A product's
+// log value is the sum of its children's (engine.py:68-71): the integer
+// bases add exactly (beta), the offsets in fp32 (o).  The block base is
+// floor(max_j beta_j + o_j) (reduced across warps in shared memory; it is
+// also the shift the sum contraction needs, so no max pre-pass), and the
+// rows store (beta_j - base) + o_j.  -inf rows: window padding.
 constexpr int VB = 4;              // samples per lane (float4)
 constexpr int SLAB = 32 * VB;      // samples per CTA
 constexpr int RW = 8;              // warps per CTA (rows in flight)
@@ -325,56 +313,84 @@ __device__ __forceinline__ float4 f4max(float4 a, float4 b) {
   return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), fmaxf(a.w, b.w));
 }
 
-// max over the RW warps' float4 partials; warp 0 writes the result
-__device__ __forceinline__ void block_max_store(float4 mx, float* __restrict__ dst, bool live) {
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// max over the RW warps' float4 partials, broadcast to every warp
+__device__ __forceinline__ float4 block_max_all(float4 mx) {
   __shared__ float4 red[RW][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   red[warp][lane] = mx;
   __syncthreads();
-  if (warp == 0) {
 #pragma unroll
-    for (int w = 1; w < RW; ++w) mx = f4max(mx, red[w][lane]);
-    if (live) *reinterpret_cast<float4*>(dst) = mx;
-  }
+  for (int w = 0; w < RW; ++w) mx = f4max(mx, red[w][lane]);
+  return mx;
 }
 
+__device__ __forceinline__ float rebase(float beta, float o, float base) {
+  return base == PCB_NEG_INF ? PCB_NEG_INF : (beta - base) + o;
+}
+
+template <int PER>
 __global__ void __launch_bounds__(RW * 32)
     k_prod_block(int k_n, int B, int ldb, const int32_t* __restrict__ row_off,
-                 const int32_t* __restrict__ ch, const float* __restrict__ values,
-                 float* __restrict__ scratch, float* __restrict__ bmax) {
+                 const int32_t* __restrict__ ch, const int32_t* __restrict__ cb,
+                 const float* __restrict__ values, const float* __restrict__ vbase,
+                 float* __restrict__ scratch, float* __restrict__ pbase) {
   const int blk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.y * SLAB + lane * VB;
   const bool live = b < B;
   const float ninf = PCB_NEG_INF;
   float4 mx = make_float4(ninf, ninf, ninf, ninf);
-  for (int j = warp; j < k_n; j += RW) {
+  float4 be[PER], of[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int j = warp + u * RW;
+    be[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    of[u] = make_float4(ninf, ninf, ninf, ninf);
+    if (j >= k_n || !live) continue;
     const int r = blk * k_n + j;
     const int a = __ldg(row_off + r), z = __ldg(row_off + r + 1);
-    float4 acc = make_float4(ninf, ninf, ninf, ninf);
-    if (a < z && live) {
-      acc = *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + a) * ldb + b);
-      for (int q = a + 1; q < z; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + q) * ldb + b);
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
+    if (a < z) {
+      of[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = a; q < z; ++q) {
+        of[u] = f4add(of[u], *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + q) * ldb + b));
+        const int c = __ldg(cb + q);
+        if (c >= 0) be[u] = f4add(be[u], *reinterpret_cast<const float4*>(vbase + (int64_t)c * ldb + b));
       }
     }
-    if (live) *reinterpret_cast<float4*>(scratch + (int64_t)r * ldb + b) = acc;
-    mx = f4max(mx, acc);
+    mx = f4max(mx, f4add(be[u], of[u]));
   }
-  block_max_store(mx, bmax + (int64_t)blk * ldb + b, live);
+  mx = block_max_all(mx);
+  if (!live) return;
+  const float4 base = make_float4(floorf(mx.x), floorf(mx.y), floorf(mx.z), floorf(mx.w));
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int j = warp + u * RW;
+    if (j >= k_n) continue;
+    const float4 o = make_float4(rebase(be[u].x, of[u].x, base.x), rebase(be[u].y, of[u].y, base.y),
+                                 rebase(be[u].z, of[u].z, base.z), rebase(be[u].w, of[u].w, base.w));
+    *reinterpret_cast<float4*>(scratch + (int64_t)(blk * k_n + j) * ldb + b) = o;
+  }
+  if (warp == 0) *reinterpret_cast<float4*>(pbase + (int64_t)blk * ldb + b) = base;
 }
 
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
-                     float* scratch, float* bmax) {
+                     const float* vbase_all, float* scratch, float* pbase) {
   ProfScope prof_(KC_PROD_EVAL, s);
   if (!B || !L.n_pb) return PCB_OK;
   dim3 grid((unsigned)L.n_pb, (unsigned)((B + SLAB - 1) / SLAB));
-  k_prod_block<<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off, L.prow_ch, values,
-                                        scratch, bmax);
+#define PCB_PB(PER)                                                                          \
+  k_prod_block<PER><<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off, L.prow_ch,     \
+                                             L.prow_cb, values, vbase_all, scratch, pbase)
+  if (L.k_n <= RW) PCB_PB(1);
+  else if (L.k_n <= 2 * RW) PCB_PB(2);
+  else if (L.k_n <= 4 * RW) PCB_PB(4);
+  else if (L.k_n <= 8 * RW) PCB_PB(8);
+  else return PCB_USAGE;
+#undef PCB_PB
   return check_launch();
 }
 
@@ -547,15 +563,19 @@ int launch_push_ratio(const Layer& L, cudaStream_t s, int B, int ldb, const floa
 // ---------------------------------------------------------------- K3 (SIMT)
 // Alg. 1 for one sum-block row and a 32-sample tile (engine.py:74-102).
 // block (32, 8): tx = sample, ty strides over the k_m sums of the block.
+// The row's base G is the max of its real child blocks' bases; child values
+// enter as offset + (base - G) (an exact integer difference), the streaming
+// (lin, top) merge runs on those, and the outputs are offsets from G.
 constexpr int TB = 32;
 constexpr int TY = 8;
 constexpr int KMAX = 64;
 
 __global__ void __launch_bounds__(TB* TY)
-    k_sum_fwd_simt(int cap, int k_m, int k_n, int B, int ldb, const int32_t* __restrict__ sum_ids,
-                   const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
-                   const float* __restrict__ theta, const float* __restrict__ scratch,
-                   float* __restrict__ values) {
+    k_sum_fwd_simt(int cap, int k_m, int k_n, int B, int ldb, int64_t sb_base,
+                   const int32_t* __restrict__ sum_ids, const int32_t* __restrict__ prod_ids,
+                   const int32_t* __restrict__ param_ids, const float* __restrict__ theta,
+                   const float* __restrict__ scratch, const float* __restrict__ pbase,
+                   float* __restrict__ values, float* __restrict__ vbase) {
   __shared__ float ex[KMAX][TB];
   __shared__ float th[KMAX * KMAX];
   __shared__ float cm[TB];
@@ -564,6 +584,12 @@ __global__ void __launch_bounds__(TB* TY)
   const int tid = ty * TB + tx;
   const int b = blockIdx.x * TB + tx;
   const bool live_b = b < B;
+  float G = PCB_NEG_INF;
+  if (live_b)
+    for (int c = 0; c < cap; ++c)
+      if (param_ids[(int64_t)r * cap + c] != 0)
+        G = fmaxf(G, pbase[(int64_t)(prod_ids[(int64_t)r * cap + c] / k_n) * ldb + b]);
+  if (G == PCB_NEG_INF) G = 0.f;  // every child block -inf: the offsets say so
   float lin[KMAX / TY];
 #pragma unroll
   for (int i = 0; i < KMAX / TY; ++i) lin[i] = 0.f;
@@ -572,8 +598,9 @@ __global__ void __launch_bounds__(TB* TY)
     const int pid = prod_ids[(int64_t)r * cap + c];
     const int tid0 = param_ids[(int64_t)r * cap + c];
     if (tid0 == 0) continue;  // padded column: -inf child block, zero tile
+    const float d = live_b ? pbase[(int64_t)(pid / k_n) * ldb + b] - G : PCB_NEG_INF;
     for (int j = ty; j < k_n; j += TY)
-      ex[j][tx] = live_b ? scratch[(int64_t)(pid + j) * ldb + b] : PCB_NEG_INF;
+      ex[j][tx] = live_b ? scratch[(int64_t)(pid + j) * ldb + b] + d : PCB_NEG_INF;
     for (int q = tid; q < k_m * k_n; q += TB * TY) th[q] = __ldg(theta + tid0 + q);
     __syncthreads();
     if (ty == 0) {
@@ -609,16 +636,18 @@ __global__ void __launch_bounds__(TB* TY)
     const int m = ty + i * TY;
     if (m < k_m) values[(int64_t)(sid + m) * ldb + b] = logf(lin[i]) + top;
   }
+  if (ty == 0) vbase[(int64_t)((sid - sb_base) / k_m) * ldb + b] = G;
 }
 
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
-                        const float* theta, const float* scratch, float* values) {
+                        const float* theta, const float* scratch, const float* pbase,
+                        float* values, float* vbase) {
   ProfScope prof_(KC_SUM_FWD_SIMT, s);
   if (!g.rows) return PCB_OK;
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
   k_sum_fwd_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
-                                               g.sum_ids, g.prod_ids, g.param_ids, theta,
-                                               scratch, values);
+                                               L.sb_base, g.sum_ids, g.prod_ids, g.param_ids,
+                                               theta, scratch, pbase, values, vbase);
   return check_launch();
 }
 
@@ -630,15 +659,18 @@ __device__ __forceinline__ float log_ratio(float f, float l) {
 // ---------------------------------------------------------------- K4 (SIMT)
 // Alg. 3 for one (sum-block row, child column) tile (engine.py:105-126):
 // cum[m, n] = sum_b exp(lnf[m,b] - nmax[b]) * exp(child[n,b] + nmax[b]);
-// f_params[flow + m*k_n + n] += theta * cum.
+// f_params[flow + m*k_n + n] += theta * cum.  lnf uses the sums' offsets;
+// the child side adds the exact base difference (product block - sum block).
 constexpr int PF_THREADS = 256;
 
 __global__ void __launch_bounds__(PF_THREADS)
-    k_param_flow_simt(int cap, int k_m, int k_n, int B, int ldb, const int32_t* __restrict__ sum_ids,
-                      const int32_t* __restrict__ prod_ids, const int32_t* __restrict__ param_ids,
-                      const int32_t* __restrict__ flow_ids, const float* __restrict__ theta,
-                      const float* __restrict__ values, const float* __restrict__ flows,
-                      const float* __restrict__ scratch, float* __restrict__ f_params) {
+    k_param_flow_simt(int cap, int k_m, int k_n, int B, int ldb, int64_t sb_base,
+                      const int32_t* __restrict__ sum_ids, const int32_t* __restrict__ prod_ids,
+                      const int32_t* __restrict__ param_ids, const int32_t* __restrict__ flow_ids,
+                      const float* __restrict__ theta, const float* __restrict__ values,
+                      const float* __restrict__ flows, const float* __restrict__ scratch,
+                      const float* __restrict__ pbase, const float* __restrict__ vbase,
+                      float* __restrict__ f_params) {
   __shared__ float sc[KMAX][TB];
   __shared__ float em[KMAX][TB];
   __shared__ float nm[TB];
@@ -648,6 +680,8 @@ __global__ void __launch_bounds__(PF_THREADS)
   const int pid = prod_ids[(int64_t)r * cap + c];
   const int fid = flow_ids[(int64_t)r * cap + c];
   const int sid = sum_ids[r];
+  const float* pb = pbase + (int64_t)(pid / k_n) * ldb;
+  const float* vb = vbase + (int64_t)((sid - sb_base) / k_m) * ldb;
   const int tid = threadIdx.x;
   const int tx = tid % TB, ty = tid / TB;  // 32 x 8
   const int tile = k_m * k_n;
@@ -671,9 +705,10 @@ __global__ void __launch_bounds__(PF_THREADS)
     __syncthreads();
     const float nmax = nm[tx];
     const bool dead = (nmax == PCB_NEG_INF) || !live;
+    const float d = dead ? 0.f : pb[b] - vb[b];
     for (int m = ty; m < k_m; m += PF_THREADS / TB) sc[m][tx] = dead ? 0.f : expf(sc[m][tx] - nmax);
     for (int n = ty; n < k_n; n += PF_THREADS / TB)
-      em[n][tx] = dead ? 0.f : expf(scratch[(int64_t)(pid + n) * ldb + b] + nmax);
+      em[n][tx] = dead ? 0.f : expf((scratch[(int64_t)(pid + n) * ldb + b] + d) + nmax);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
@@ -699,24 +734,29 @@ __global__ void __launch_bounds__(PF_THREADS)
 
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
-                           const float* scratch, float* f_params) {
+                           const float* scratch, const float* pbase, const float* vbase,
+                           float* f_params) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!g.rows || !g.cap) return PCB_OK;
   dim3 grid((unsigned)g.cap, (unsigned)g.rows);
   k_param_flow_simt<<<grid, PF_THREADS, 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
-                                                g.sum_ids, g.prod_ids, g.param_ids, g.flow_ids,
-                                                theta, values, flows, scratch, f_params);
+                                                L.sb_base, g.sum_ids, g.prod_ids, g.param_ids,
+                                                g.flow_ids, theta, values, flows, scratch, pbase,
+                                                vbase, f_params);
   return check_launch();
 }
 
 // ---------------------------------------------------------------- K5 (SIMT)
 // Alg. 4 for one product-block row and a 32-sample tile (engine.py:129-165).
+// Parent ratios (offsets) are moved onto the product block's base: lnf +
+// (base_pb - base_sb), an exact integer difference per parent block.
 __global__ void __launch_bounds__(TB* TY)
-    k_child_flow_simt(int cap, int k_m, int k_n, int B, int ldb, const int32_t* __restrict__ ch_ids,
-                      const int32_t* __restrict__ par_ids, const int32_t* __restrict__ ppids,
-                      const float* __restrict__ theta, const float* __restrict__ values,
-                      const float* __restrict__ flows, const float* __restrict__ scratch,
-                      float* __restrict__ flow_scratch) {
+    k_child_flow_simt(int cap, int k_m, int k_n, int B, int ldb, int64_t sb_base,
+                      const int32_t* __restrict__ ch_ids, const int32_t* __restrict__ par_ids,
+                      const int32_t* __restrict__ ppids, const float* __restrict__ theta,
+                      const float* __restrict__ values, const float* __restrict__ flows,
+                      const float* __restrict__ scratch, const float* __restrict__ pbase,
+                      const float* __restrict__ vbase, float* __restrict__ flow_scratch) {
   __shared__ float sc[KMAX][TB];
   __shared__ float th[KMAX * KMAX];
   __shared__ float nm[TB];
@@ -725,6 +765,8 @@ __global__ void __launch_bounds__(TB* TY)
   const int tid = ty * TB + tx;
   const int b = blockIdx.x * TB + tx;
   const bool live_b = b < B;
+  const int ch = ch_ids[r];
+  const float bp = live_b ? pbase[(int64_t)(ch / k_n) * ldb + b] : PCB_NEG_INF;
   float lin[KMAX / TY];
 #pragma unroll
   for (int i = 0; i < KMAX / TY; ++i) lin[i] = 0.f;
@@ -733,9 +775,12 @@ __global__ void __launch_bounds__(TB* TY)
     const int tid0 = ppids[(int64_t)r * cap + p];
     if (tid0 == 0) continue;
     const int par = par_ids[(int64_t)r * cap + p];
+    const float d = (live_b && bp != PCB_NEG_INF)
+                        ? bp - vbase[(int64_t)((par - sb_base) / k_m) * ldb + b]
+                        : PCB_NEG_INF;
     for (int m = ty; m < k_m; m += TY) {
       const int64_t o = (int64_t)(par + m) * ldb + b;
-      sc[m][tx] = live_b ? log_ratio(flows[o], values[o]) : PCB_NEG_INF;
+      sc[m][tx] = live_b ? log_ratio(flows[o], values[o]) + d : PCB_NEG_INF;
     }
     for (int q = tid; q < k_m * k_n; q += TB * TY) th[q] = __ldg(theta + tid0 + q);
     __syncthreads();
@@ -766,14 +811,13 @@ __global__ void __launch_bounds__(TB* TY)
     __syncthreads();
   }
   if (!live_b) return;
-  const int ch = ch_ids[r];
 #pragma unroll
   for (int i = 0; i < KMAX / TY; ++i) {
     const int n = ty + i * TY;
     if (n < k_n) {
       const int64_t o = (int64_t)(ch + n) * ldb + b;
       const float lp = scratch[o];
-      // lin * exp(top + l_p) computed in log space to avoid overflow
+      // lin * exp(top + offset) computed in log space to avoid overflow
       flow_scratch[o] = (lin[i] > 0.f) ? expf(logf(lin[i]) + top + lp) : 0.f;
     }
   }
@@ -781,13 +825,15 @@ __global__ void __launch_bounds__(TB* TY)
 
 int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
-                           const float* scratch, float* flow_scratch) {
+                           const float* scratch, const float* pbase, const float* vbase,
+                           float* flow_scratch) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!g.rows) return PCB_OK;
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
   k_child_flow_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
-                                                  g.ch_ids, g.par_ids, g.par_param_ids, theta,
-                                                  values, flows, scratch, flow_scratch);
+                                                  L.sb_base, g.ch_ids, g.par_ids,
+                                                  g.par_param_ids, theta, values, flows, scratch,
+                                                  pbase, vbase, flow_scratch);
   return check_launch();
 }
 
@@ -1178,25 +1224,33 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
 }
 
 // ---------------------------------------------------------------- K10 root
-__global__ void k_root_fwd(int B, int ldb, int64_t root_slot, const int32_t* __restrict__ rc,
-                           int nrc, const float* __restrict__ values, float* __restrict__ lroot) {
+__global__ void k_root_fwd(int B, int ldb, int64_t root_slot, int64_t root_vb,
+                           const int32_t* __restrict__ rc, const int32_t* __restrict__ rcb,
+                           int nrc, const float* __restrict__ values,
+                           const float* __restrict__ vbase, float* __restrict__ lroot) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  float v;
+  // base + offset in double: |log p| may exceed the fp32 spacing of the parts
+  double v;
   if (root_slot >= 0) {
-    v = values[root_slot * ldb + b];
+    v = (double)values[root_slot * ldb + b];
+    if (root_vb >= 0) v += (double)vbase[root_vb * ldb + b];
   } else {
-    v = 0.f;
-    for (int q = 0; q < nrc; ++q) v += values[(int64_t)rc[q] * ldb + b];
+    v = 0.0;
+    for (int q = 0; q < nrc; ++q) {
+      v += (double)values[(int64_t)rc[q] * ldb + b];
+      if (rcb[q] >= 0) v += (double)vbase[(int64_t)rcb[q] * ldb + b];
+    }
   }
-  lroot[b] = v;
+  lroot[b] = (float)v;
 }
 
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
-                    float* lroot) {
+                    const float* vbase_all, float* lroot) {
   ProfScope prof_(KC_MISC, s);
-  k_root_fwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_children,
-                                              (int)p->n_root_children, values, lroot);
+  k_root_fwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_vb, p->root_children,
+                                              p->root_cb, (int)p->n_root_children, values,
+                                              vbase_all, lroot);
   return check_launch();
 }
 

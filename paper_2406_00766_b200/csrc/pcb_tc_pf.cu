@@ -10,7 +10,10 @@
 // per-sample max over the tile's sum blocks of the ratio shift R (k_ratio,
 // log2 units) and cancels between the two operands:
 //   A[m, b] = 2^{r[m,b] + R_blk(m)[b] - c_b},   E[j, b] = 2^{child[j,b] log2e + c_b}
-// (r = the shifted log2 ratio rows of k_ratio).  Both operands are split
+// (r = the shifted log2 ratio rows of k_ratio; child = the product
+// offsets moved onto the sums' base: offset + (base_pb - base_sum), an
+// exact integer difference — the sums of a super-row share one child row,
+// hence one base).  Both operands are split
 // into bf16 hi + lo and contracted as hi*hi + hi*lo + lo*hi (fp32 TMEM).
 //
 // Warp roles (14 warps):
@@ -77,13 +80,15 @@ struct PfCfg {
   static constexpr int kE = PF_N * PF_KS * 4;          // raw child rows
   static constexpr int kRP = 128;                      // R row pitch (TMA destinations are 128-B aligned)
   static constexpr int kR = PF_MAXMEM * kRP;            // raw R rows (one per sum block)
-  static constexpr int kRaw = (kA + kE + kR + 1023) / 1024 * 1024;  // swizzle-atom aligned stages
+  static constexpr int kCPG = PF_N / KN;                // child columns per item
+  static constexpr int kBs = kRP;                       // the sums' base row
+  static constexpr int kPb = kCPG * kRP;                // the child blocks' base rows
+  static constexpr int kRaw = (kA + kE + kR + kBs + kPb + 1023) / 1024 * 1024;  // swizzle-atom aligned
   static constexpr int kOpA = PF_M * PF_KS * 2;        // one bf16 A plane
   static constexpr int kOpB = PF_N * PF_KS * 2;        // one bf16 B plane
   static constexpr int kOp = 2 * kOpA + 2 * kOpB;
   static constexpr int kRS = (PF_KS == 16) ? 5 : RS, kOS = (PF_KS == 16) ? 3 : 4 - RS;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
-  static constexpr int kCPG = PF_N / KN;                // child columns per item
   static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need aligned bases");
 };
 
@@ -153,7 +158,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                     const __grid_constant__ CUtensorMap tm_R, const __grid_constant__ CUtensorMap tm_e,
                     const __grid_constant__ CUtensorMap tm_r128,
                     const __grid_constant__ CUtensorMap tm_Rt,
-                    const __grid_constant__ CUtensorMap tm_e256) {
+                    const __grid_constant__ CUtensorMap tm_e256,
+                    const __grid_constant__ CUtensorMap tm_vb,
+                    const __grid_constant__ CUtensorMap tm_pb,
+                    const __grid_constant__ CUtensorMap tm_pbn) {
   using C = PfCfg<KN, RS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOS], op_empty[C::kOS];
@@ -207,7 +215,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const int a_rows = (fl & 1) ? PF_M : it.nmem * a.k_m;
         const int r_rows = (fl & 1) ? PF_M / a.k_m : it.nmem;
         const int e_rows = (fl & 2) ? PF_N : ncol * KN;
-        const uint32_t bytes = (uint32_t)(a_rows + e_rows) * PF_KS * 4 + (uint32_t)r_rows * C::kRP;
+        const int pb_rows = (fl & 2) ? C::kCPG : ncol;
+        const uint32_t bytes = (uint32_t)(a_rows + e_rows) * PF_KS * 4 +
+                               (uint32_t)(r_rows + 1 + pb_rows) * C::kRP;
+        // the tile's sums share one base: that of its first sum block
+        const int vb_row =
+            (__ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo)) - (int)a.sb_base) / a.k_m;
         for (int kc = it.kc0; kc < it.kc1; ++kc) {
           const int b0 = kc * PF_KS;
           mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
@@ -225,11 +238,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
               tma_load_2d(st + C::kA + C::kE + s * C::kRP, &tm_R, b0, row / a.k_m, rf);
             }
           }
+          const uint32_t sb = st + C::kA + C::kE + C::kR;
+          tma_load_2d(sb, &tm_vb, b0, vb_row, rf);
           if (fl & 2) {
             tma_load_2d(st + C::kA, &tm_e256, b0, __ldg(prow + cols_p[0]), rf);
+            tma_load_2d(sb + C::kBs, &tm_pbn, b0, __ldg(prow + cols_p[0]) / KN, rf);
           } else {
-            for (int ci = 0; ci < ncol; ++ci)
+            for (int ci = 0; ci < ncol; ++ci) {
               tma_load_2d(st + C::kA + ci * KN * PF_KS * 4, &tm_e, b0, __ldg(prow + cols_p[ci]), rf);
+              tma_load_2d(sb + C::kBs + ci * C::kRP, &tm_pb, b0, __ldg(prow + cols_p[ci]) / KN, rf);
+            }
           }
           rr.next();
         }
@@ -291,6 +309,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const float* rA = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
         const float* rE = rA + C::kA / 4;
         const float* rR = rE + C::kE / 4;
+        const float* rB = rR + C::kR / 4;             // the sums' base (32 samples)
+        const float* rP = rB + C::kBs / 4;            // child block bases, kRP pitch
         float* c_s = cs[rr.slot()];
         if (t < PF_KS) {  // the chunk's per-sample shift: max of R over the tile's blocks
           float v = PCB_NEG_INF;
@@ -337,12 +357,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           *reinterpret_cast<uint4*>(oAl + off) = lo;
         }
         // E: npad rows x 4 octets
+        const float4* rB4 = reinterpret_cast<const float4*>(rB);
+        const float4* rP4 = reinterpret_cast<const float4*>(rP);
         for (int q = t; q < npad * (PF_KS / 8); q += PF_NCONV * 32) {
           const int n = q % npad, o = q / npad;
           const float4 x0 = rE4[n * PF_CH + swz_chunk(n, 2 * o)];
           const float4 x1 = rE4[n * PF_CH + swz_chunk(n, 2 * o + 1)];
           const float4 c0 = c4[2 * o], c1 = c4[2 * o + 1];
-          const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          const float4 p0 = rP4[(n / KN) * (C::kRP / 16) + 2 * o];
+          const float4 p1 = rP4[(n / KN) * (C::kRP / 16) + 2 * o + 1];
+          const float4 s0 = rB4[2 * o], s1 = rB4[2 * o + 1];
+          const float xs[8] = {x0.x + (p0.x - s0.x), x0.y + (p0.y - s0.y), x0.z + (p0.z - s0.z),
+                               x0.w + (p0.w - s0.w), x1.x + (p1.x - s1.x), x1.y + (p1.y - s1.y),
+                               x1.z + (p1.z - s1.z), x1.w + (p1.w - s1.w)};
           const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
           float v[8];
 #pragma unroll
@@ -563,7 +590,7 @@ namespace {
 
 template <int KN, int RS>
 int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float* rmax,
-              const float* scratch, cudaStream_t s) {
+              const float* scratch, const float* vbase, const float* pbase, cudaStream_t s) {
   using C = PfCfg<KN, RS>;
   static bool attr = false;
   if (!attr) {
@@ -581,16 +608,20 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   a.n_items = base * a.kslices;
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
   if (a.em && (a.kslices != 1 || a.cgroups != 1)) return PCB_USAGE;  // needs whole rows
-  CUtensorMap tr, tR, te, tr128, tRt, te256;
+  CUtensorMap tr, tR, te, tr128, tRt, te256, tvb, tpb, tpbn;
   if (make_rows_map(&tr, ratio, L.n_sb * L.k_m, a.ldb, (int)L.k_m, PF_KS, PF_SWZ) ||
       make_rows_map(&tR, rmax, L.n_sb, a.ldb, 1, C::kRP / 4, 0) ||
       make_rows_map(&te, scratch, L.window, a.ldb, KN, PF_KS, PF_SWZ) ||
       make_rows_map(&tr128, ratio, L.n_sb * L.k_m, a.ldb, PF_M, PF_KS, PF_SWZ) ||
       make_rows_map(&tRt, rmax, L.n_sb, a.ldb, PF_M / (int)L.k_m, C::kRP / 4, 0) ||
-      make_rows_map(&te256, scratch, L.window, a.ldb, PF_N, PF_KS, PF_SWZ))
+      make_rows_map(&te256, scratch, L.window, a.ldb, PF_N, PF_KS, PF_SWZ) ||
+      make_rows_map(&tvb, vbase, L.n_sb, a.ldb, 1, C::kRP / 4, 0) ||
+      make_rows_map(&tpb, pbase, L.n_pb, a.ldb, 1, C::kRP / 4, 0) ||
+      make_rows_map(&tpbn, pbase, L.n_pb, a.ldb, C::kCPG, C::kRP / 4, 0))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_param_flow_ws<KN, RS><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te, tr128, tRt, te256);
+  k_param_flow_ws<KN, RS><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te, tr128, tRt, te256,
+                                                              tvb, tpb, tpbn);
   return check_launch();
 }
 
@@ -615,7 +646,8 @@ bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B) {
 
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
-                         const float* scratch, float* f_params, const PfEm* em) {
+                         const float* scratch, const float* vbase, const float* pbase,
+                         float* f_params, const PfEm* em) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   PfArgs a{};
@@ -650,12 +682,12 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   // a deeper raw ring pays there
   const bool dense = g.cap * L.k_n > PF_N;
   switch (L.k_n) {
-    case 16: return dense ? launch_pf<16, 3>(a, L, ratio, rmax, scratch, s)
-                          : launch_pf<16, 2>(a, L, ratio, rmax, scratch, s);
-    case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, s)
-                          : launch_pf<32, 2>(a, L, ratio, rmax, scratch, s);
-    case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, s)
-                          : launch_pf<64, 2>(a, L, ratio, rmax, scratch, s);
+    case 16: return dense ? launch_pf<16, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
+                          : launch_pf<16, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+    case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
+                          : launch_pf<32, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+    case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
+                          : launch_pf<64, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     default: return PCB_USAGE;
   }
 }

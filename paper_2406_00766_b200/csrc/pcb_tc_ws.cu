@@ -4,6 +4,12 @@
 // Both are "transform + GEMM" over node-major fp32 rows:
 //   forward     D[b, n] = sum_j e^{child[j,b] - g_b} theta[n, j]      (A = children)
 //   child flow  D[b, j] = sum_m e^{lnf[m,b] - g_b} theta[m, j]         (A = parent ratios)
+// Log values are (integer block base, fp32 offset) pairs (pcb_internal.cuh):
+// the forward shift g_b is the max of the K blocks' bases G (the output
+// base; a K block enters as offset + (base - G)); the child flows move
+// every parent block's ratio onto a common base Gr (max of the parents'
+// bases) and every product block's offset back onto its own base in the
+// epilogue.  All base arithmetic is exact integer differences.
 // with M = 128 samples per work item, N = a stacked super-row (<= 256) and K
 // streamed one child (parent) block at a time.  A work item is one
 // (super-row, 128-sample tile); CTAs are persistent (one per SM, TMEM
@@ -77,11 +83,16 @@ struct WsArgs {
   int64_t plane;                   // elements per plane region of the bf16 theta copy
   const __nv_bfloat16* mma;
   const float* src0;               // scratch (fwd) / ratio rows r (cf, from sb_base)
-  const float* shift;              // bmax (fwd) / rmax R (cf)
+  const float* shift;              // pbase (fwd) / rmax R (cf), layer rows
   const float* aux;                // - / scratch (cf epilogue: child log values)
   float* out;                      // values (fwd) / flow_scratch (cf)
+  float* vbase;                    // fwd: the layer's sum-block base rows (written)
+  const float* vbase_in;           // cf: the layer's sum-block base rows
+  const float* pbase_in;           // cf: the layer's product-block base rows
+  int64_t out_base;                // fwd: first sum slot of the layer (vbase row of a slot)
   int32_t* counters;               // split-K arrivals per (super-row, tile)
   const float* gshift;             // precomputed per-(super-row, sample) shifts, or null
+  const float* gbase;              // cf: precomputed per-(super-row, sample) common bases Gr
   int64_t gshift_stride;           // ldb, or 0 when every super-row shares one shift row
 };
 
@@ -113,9 +124,10 @@ __device__ __forceinline__ int slice_first(const int32_t* __restrict__ real, int
 
 template <int MODE, int KC>
 struct WsCfg {
-  // raw rows per stage: the K block's rows (forward: child log values; child
-  // flow: shifted log2 flow ratios r) + (child flow) the block's shift row R
-  static constexpr int kRows = KC + (MODE == MODE_CF ? 1 : 0);
+  // raw rows per stage: the K block's rows (forward: child offsets; child
+  // flow: shifted log2 flow ratios r) + the block's base row (forward) / its
+  // shift row R and base row (child flow)
+  static constexpr int kRows = KC + (MODE == MODE_CF ? 2 : 1);
   static constexpr int kRaw = kRows * WS_M * 4;               // raw stage bytes
   static constexpr int kA = WS_M * KC * 2;                    // one bf16 A plane
   static constexpr int kBPlane = WS_NMAX * KC * 2;            // stacked theta hi (or lo) plane
@@ -135,7 +147,7 @@ struct WsCfg {
 template <int MODE, int KC>
 __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     k_sum_ws(const WsArgs a, const __grid_constant__ CUtensorMap tm0,
-             const __grid_constant__ CUtensorMap tm1) {
+             const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2) {
   using C = WsCfg<MODE, KC>;
   using W = WsWarps<C::kNConv>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -143,6 +155,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
   __shared__ uint64_t op_full[C::kOS], op_empty[C::kOS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
   __shared__ float g_s[2][WS_M];
+  __shared__ float gr_s[2][WS_M];        // child flow: the common parent base Gr
   __shared__ int g_nk[2];                // real K blocks of the item (0: dead)
   __shared__ int g_orow[2][WS_NMAX / 16];  // first output row of every 16 columns
   __shared__ bool g_last;
@@ -181,7 +194,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     // samples past ldb are zero-filled by the TMA unit
     if (lane == 0) {
       prefetch_tmap(&tm0);
-      if (MODE == MODE_CF) prefetch_tmap(&tm1);
+      prefetch_tmap(&tm1);
+      if (MODE == MODE_CF) prefetch_tmap(&tm2);
       Ring rr(C::kRS);
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         const WsItem it = ws_item(a, item);
@@ -196,7 +210,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
           mbar_arrive_expect_tx(rf, (uint32_t)C::kRaw);
           const uint32_t dst = smem_u32(raw + rr.slot() * C::kRaw);
           tma_load_2d(dst, &tm0, b0, row0, rf);
-          if (MODE == MODE_CF) tma_load_2d(dst + KC * WS_M * 4, &tm1, b0, row0 / KC, rf);
+          tma_load_2d(dst + KC * WS_M * 4, &tm1, b0, row0 / KC, rf);
+          if (MODE == MODE_CF) tma_load_2d(dst + (KC + 1) * WS_M * 4, &tm2, b0, row0 / KC, rf);
           rr.next();
         }
       }
@@ -298,23 +313,27 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       const int gs = g_u & 1;
       mbar_wait(smem_u32(&g_full[gs]), (uint32_t)((g_u >> 1) & 1));
       const float g = g_s[gs][t];
+      const float gr = gr_s[gs][t];
       const bool dead = !live || g == PCB_NEG_INF;
-      // forward: g is a natural-log max (folded into one FFMA per element);
-      // child flow: g is already in log2 units
-      const float gl2 = dead ? 0.f : (MODE == MODE_FWD ? g * kL2E : g);
+      // forward: g is the integer base G (natural log); child flow: g is in
+      // log2 units, gr the common base of the parent blocks
+      const float gl2 = dead ? 0.f : g;
       int c = slice_first(real, a.cap, it.ks * a.kper);
       for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
         mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
         const float* rs = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
         float x[KH];
         const float* rh = rs + kh * KH * WS_M;
+        float d;
         if (MODE == MODE_FWD) {
+          // (base_block - G) log2 e: an exact integer difference (-inf for an
+          // all -inf block), added to offset log2 e in one FFMA
+          d = (rs[KC * WS_M + t] - gl2) * kL2E;
 #pragma unroll
           for (int j = 0; j < KH; ++j) x[j] = rh[j * WS_M + t];
         } else {
-          // r + (R_block - g): both shifts are fp32 log2 values, their
-          // difference is small and (near-)exact
-          const float d = rs[KC * WS_M + t] - gl2;
+          // r + (R_block + (Gr - base_block) log2 e - g): small, (near-)exact
+          d = fmaf(gr - rs[(KC + 1) * WS_M + t], kL2E, rs[KC * WS_M + t]) - gl2;
 #pragma unroll
           for (int j = 0; j < KH; ++j) x[j] = rh[j * WS_M + t] + d;
         }
@@ -324,7 +343,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < KH; ++j) {
           if (MODE == MODE_FWD)
-            x[j] = dead ? 0.f : ex2(fmaf(x[j], kL2E, -gl2));
+            x[j] = dead ? 0.f : ex2(fmaf(x[j], kL2E, d));
           else
             x[j] = dead ? 0.f : ex2(x[j]);  // ex2(-inf) = 0: impossible sums, zero flow
         }
@@ -359,44 +378,65 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     // shifts of the lane's 4 samples: the K blocks' ids once (warp-uniform),
     // then the 4 x 8 side maxima of each round in flight together
     constexpr int SPL = WS_M / 32;  // samples per lane
-    auto shifts = [&](const WsItem& it, float* g, int& nk) {
+    // forward: g = max of the K blocks' bases; child flow: gr = max of the
+    // parent blocks' bases, then g = max of R + (gr - base) log2 e
+    auto shifts = [&](const WsItem& it, float* g, float* gr, int& nk) {
       const int64_t r0 = it.r0;
       const int32_t* src = a.src_ids + r0 * a.cap;
       const int32_t* real = a.real_ids + r0 * a.cap;
 #pragma unroll
-      for (int u = 0; u < SPL; ++u) g[u] = PCB_NEG_INF;
+      for (int u = 0; u < SPL; ++u) g[u] = gr[u] = PCB_NEG_INF;
       nk = 0;
       if (a.gshift) {  // long K: shifts precomputed by k_group_shift
         for (int c = 0; c < a.cap; ++c) nk += __ldg(real + c) != 0;
 #pragma unroll
         for (int u = 0; u < SPL; ++u) {
           const int b = it.b0 + lane + 32 * u;
-          if (b < a.B) g[u] = __ldg(a.gshift + (int64_t)it.sr * a.gshift_stride + b);
+          if (b < a.B) {
+            g[u] = __ldg(a.gshift + (int64_t)it.sr * a.gshift_stride + b);
+            if (MODE == MODE_CF) gr[u] = __ldg(a.gbase + (int64_t)it.sr * a.gshift_stride + b);
+          }
         }
         return;
       }
-      for (int c0 = 0; c0 < a.cap; c0 += 8) {
-        int sc[8];
+      const float* first = MODE == MODE_CF ? a.vbase_in : a.shift;
+      for (int pass = 0; pass < (MODE == MODE_CF ? 2 : 1); ++pass) {
+        for (int c0 = 0; c0 < a.cap; c0 += 8) {
+          int sc[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int c = c0 + e;
-          sc[e] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
-          nk += sc[e] >= 0;
+          for (int e = 0; e < 8; ++e) {
+            const int c = c0 + e;
+            sc[e] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
+            if (pass == 0) nk += sc[e] >= 0;
+          }
+          float v[SPL][8], w[SPL][8];
+#pragma unroll
+          for (int u = 0; u < SPL; ++u) {
+            const int b = it.b0 + lane + 32 * u;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const bool ok = sc[e] >= 0 && b < a.B;
+              const int64_t o = (int64_t)(sc[e] - a.sb_base) / KC * a.ldb + b;
+              v[u][e] = ok ? __ldg((pass == 0 ? first : a.shift) + o) : PCB_NEG_INF;
+              w[u][e] = (ok && pass == 1) ? __ldg(a.vbase_in + o) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < SPL; ++u)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if (pass == 0) g[u] = fmaxf(g[u], v[u][e]);
+              else gr[u] = fmaxf(gr[u], fmaf(g[u] - w[u][e], kL2E, v[u][e]));
+            }
         }
-        float v[SPL][8];
+      }
+      if (MODE == MODE_CF) {  // (g, gr) = (shift, base): pass 0 found the base
 #pragma unroll
         for (int u = 0; u < SPL; ++u) {
-          const int b = it.b0 + lane + 32 * u;
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            v[u][e] = (sc[e] >= 0 && b < a.B)
-                          ? __ldg(a.shift + (int64_t)(sc[e] - a.sb_base) / KC * a.ldb + b)
-                          : PCB_NEG_INF;
+          const float t = g[u];
+          g[u] = gr[u];
+          gr[u] = t;
         }
-#pragma unroll
-        for (int u = 0; u < SPL; ++u)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) g[u] = fmaxf(g[u], v[u][e]);
       }
     };
     int g_u = 0;
@@ -405,10 +445,13 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       const int gs = g_u & 1;
       mbar_wait(smem_u32(&g_empty[gs]), (uint32_t)(((g_u >> 1) & 1) ^ 1));
       int nk = 0;
-      float gv[SPL];
-      shifts(it, gv, nk);
+      float gv[SPL], gb[SPL];
+      shifts(it, gv, gb, nk);
 #pragma unroll
-      for (int u = 0; u < SPL; ++u) g_s[gs][lane + 32 * u] = gv[u];
+      for (int u = 0; u < SPL; ++u) {
+        g_s[gs][lane + 32 * u] = gv[u];
+        gr_s[gs][lane + 32 * u] = gb[u];
+      }
       const int N = it.S * a.nb;
       if (lane < N / 16) {
         const int c0 = lane * 16, sm = c0 / a.nb;
@@ -437,16 +480,23 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       // the slot is released at the end of the item (the shift warp runs
       // at most two items ahead, like the TMEM double buffer)
       const float g = g_s[gs][t];
+      const float gr = gr_s[gs][t];
       const int nk = g_nk[gs];
       const bool dead = g == PCB_NEG_INF || nk == 0;
       const int* orow_s = g_orow[gs];
       auto out_row = [&](int c0) -> int64_t { return orow_s[c0 >> 4]; };
       // finished result of 16 columns from their fp32 sums d (TMEM or reduced)
-      auto finish = [&](float* o, const float* d, const float* l) {
+      // finished result of 16 columns from their fp32 sums d (TMEM or
+      // reduced); forward: offsets ln D from the base G (stored with the
+      // first chunk of every sum block); child flow: l = product offsets
+      // already moved onto the common base (offset + base_pb - Gr)
+      auto finish = [&](int c0, float* o, const float* d, const float* l) {
         if (MODE == MODE_FWD) {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            o[(int64_t)i * a.ldb] = (dead || !(d[i] > 0.f)) ? PCB_NEG_INF : fmaf(lg2(d[i]), kLN2, g);
+            o[(int64_t)i * a.ldb] = (dead || !(d[i] > 0.f)) ? PCB_NEG_INF : lg2(d[i]) * kLN2;
+          if (c0 % a.nb == 0)
+            a.vbase[(out_row(c0) - a.out_base) / a.nb * a.ldb + b] = dead ? 0.f : g;
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i)  // flow = D * 2^g * exp(l) = 2^(log2 D + fma(l, log2 e, g))
@@ -454,9 +504,11 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         }
       };
       auto load_l = [&](int c0, float* l) {
-        const float* lp = a.aux + out_row(c0) * a.ldb + b;
+        const int64_t row = out_row(c0);
+        const float* lp = a.aux + row * a.ldb + b;
+        const float db = __ldg(a.pbase_in + row / a.nb * a.ldb + b) - gr;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) l[i] = lp[(int64_t)i * a.ldb];
+        for (int i = 0; i < 16; ++i) l[i] = lp[(int64_t)i * a.ldb] + db;
       };
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
@@ -479,7 +531,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
           }
-          finish(a.out + out_row(c0) * a.ldb + b, v, l);
+          finish(c0, a.out + out_row(c0) * a.ldb + b, v, l);
         }
         tc_fence_before();
         __syncwarp();
@@ -518,7 +570,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) d[i] = __ldcg(o + (int64_t)i * a.ldb);
             if (MODE == MODE_CF) load_l(c0, l);
-            finish(o, d, l);
+            finish(c0, o, d, l);
           }
         }
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // g_last reuse
@@ -545,25 +597,30 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
       return PCB_CUDA;
     attr = true;
   }
-  CUtensorMap tm0, tm1;
+  CUtensorMap tm0, tm1, tm2;
   if (make_rows_map(&tm0, a.src0, rows0, a.ldb, KC)) return PCB_CUDA;
-  // child flow: the per-block shift rows R, one row per box
-  if (make_rows_map(&tm1, MODE == MODE_CF ? a.shift : a.src0, MODE == MODE_CF ? rows1 : rows0,
-                    a.ldb, MODE == MODE_CF ? 1 : KC))
+  // per K block one row: the block base (forward) / the ratio shift R and the
+  // block base (child flow)
+  if (make_rows_map(&tm1, a.shift, rows1, a.ldb, 1)) return PCB_CUDA;
+  if (make_rows_map(&tm2, MODE == MODE_CF ? a.vbase_in : a.shift, rows1, a.ldb, 1))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_sum_ws<MODE, KC><<<grid, WsWarps<C::kNConv>::kThreads, C::kBytes, s>>>(a, tm0, tm1);
+  k_sum_ws<MODE, KC><<<grid, WsWarps<C::kNConv>::kThreads, C::kBytes, s>>>(a, tm0, tm1, tm2);
   return check_launch();
 }
 
-// per-(super-row, sample) shift of a long-K group: max over the super-row's
-// real K blocks of the side maxima (bmax / R).  CTA = super-row x 32
-// samples; its 8 warps split the K blocks (lane = sample), combined in smem.
+// per-(super-row, sample) shift of a long-K group over the super-row's real
+// K blocks: forward: the max of the blocks' bases; child flow: the common
+// base gr = max of the parent blocks' bases (to gbase) and the shift
+// max R + (gr - base) log2 e.  CTA = super-row x 32 samples; its 8 warps
+// split the K blocks (lane = sample), combined in smem.
+template <int MODE>
 __global__ void __launch_bounds__(256)
     k_group_shift(int cap, int kc, int B, int ldb, int64_t sb_base,
                   const int32_t* __restrict__ row_off, const int32_t* __restrict__ members,
                   const int32_t* __restrict__ src_ids, const int32_t* __restrict__ real_ids,
-                  const float* __restrict__ shift, float* __restrict__ gout) {
+                  const float* __restrict__ shift, const float* __restrict__ base,
+                  float* __restrict__ gout, float* __restrict__ gbase) {
   __shared__ float part[8][32];
   const int sr = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -571,33 +628,50 @@ __global__ void __launch_bounds__(256)
   const int64_t r0 = __ldg(members + __ldg(row_off + sr));
   const int32_t* src = src_ids + r0 * cap;
   const int32_t* real = real_ids + r0 * cap;
-  float g = PCB_NEG_INF;
-  if (b < B)
-    for (int c0 = warp; c0 < cap; c0 += 8 * 4) {
-      float v[4];
+  auto reduce = [&](const float* tab, float gr) {
+    float g = PCB_NEG_INF;
+    if (b < B)
+      for (int c0 = warp; c0 < cap; c0 += 8 * 4) {
+        float v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + 8 * u;
-        v[u] = (c < cap && __ldg(real + c) != 0)
-                   ? __ldg(shift + (int64_t)(__ldg(src + c) - sb_base) / kc * ldb + b)
-                   : PCB_NEG_INF;
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 8 * u;
+          const bool ok = c < cap && __ldg(real + c) != 0;
+          const int64_t o = ok ? (int64_t)(__ldg(src + c) - sb_base) / kc * ldb + b : 0;
+          v[u] = ok ? __ldg(tab + o) : PCB_NEG_INF;
+          if (ok && MODE == MODE_CF && gr != PCB_NEG_INF)
+            v[u] = fmaf(gr - __ldg(base + o), kL2E, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) g = fmaxf(g, v[u]);
       }
+    part[warp][lane] = g;
+    __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 4; ++u) g = fmaxf(g, v[u]);
+    for (int w = 0; w < 8; ++w) g = fmaxf(g, part[w][lane]);
+    __syncthreads();
+    return g;
+  };
+  if (MODE == MODE_FWD) {
+    const float g = reduce(shift, 0.f);
+    if (warp == 0 && b < B) gout[(int64_t)sr * ldb + b] = g;
+  } else {
+    const float gr = reduce(base, PCB_NEG_INF);
+    const float g = reduce(shift, gr);
+    if (warp == 0 && b < B) {
+      gout[(int64_t)sr * ldb + b] = g;
+      gbase[(int64_t)sr * ldb + b] = gr;
     }
-  part[warp][lane] = g;
-  __syncthreads();
-  if (warp == 0 && b < B) {
-#pragma unroll
-    for (int w = 1; w < 8; ++w) g = fmaxf(g, part[w][lane]);
-    gout[(int64_t)sr * ldb + b] = g;
   }
 }
 
-int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, cudaStream_t s) {
+template <int MODE>
+int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, float* gbase,
+                       cudaStream_t s) {
   dim3 grid((unsigned)count, (unsigned)((a.B + 31) / 32));
-  k_group_shift<<<grid, 256, 0, s>>>(a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off, a.members,
-                                     a.src_ids, a.real_ids, a.shift, gout);
+  k_group_shift<MODE><<<grid, 256, 0, s>>>(a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off,
+                                           a.members, a.src_ids, a.real_ids, a.shift,
+                                           a.vbase_in, gout, gbase);
   return check_launch();
 }
 
@@ -628,9 +702,16 @@ void plan_split(WsArgs& a, int64_t count, bool split_ok) {
 
 bool ws_supported(int kc, int nb) { return (kc == 16 || kc == 32) && (nb == 16 || nb == 32 || nb == 64); }
 
+namespace {
+inline bool tc_k(int64_t k) { return k == 16 || k == 32 || k == 64; }
+}  // namespace
+bool tc_supported(const Layer& L) { return tc_k(L.k_m) && tc_k(L.k_n); }
+bool tc_bwd_supported(const Layer& L) { return tc_k(L.k_m) && tc_k(L.k_n); }
+
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
-                      cudaStream_t s, int B, int ldb, const float* scratch, const float* bmax,
-                      float* values, float* gshift, int32_t* counters, bool split_ok) {
+                      cudaStream_t s, int B, int ldb, const float* scratch, const float* pbase,
+                      float* values, float* vbase, float* gshift, int32_t* counters,
+                      bool split_ok) {
   ProfScope prof_(KC_SUM_FWD_TC, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -651,13 +732,16 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.plane = P->mma_plane;
   a.mma = P->mma;
   a.src0 = scratch;
-  a.shift = bmax;
+  a.shift = pbase;
   a.aux = nullptr;
   a.out = values;
+  a.vbase = vbase;
+  a.out_base = L.sb_base;
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
   if (ws_long_k(a.cap)) {
-    if (launch_group_shift(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, s)) return PCB_CUDA;
+    if (launch_group_shift<MODE_FWD>(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, nullptr, s))
+      return PCB_CUDA;
     a.gshift = gshift;
     a.gshift_stride = g.uniform ? 0 : ldb;
   }
@@ -667,16 +751,16 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
                       sizeof(float) * L.n_sb * L.k_m * (int64_t)ldb, s) != cudaSuccess)
     return PCB_CUDA;
   switch (L.k_n) {
-    case 16: return launch_ws<MODE_FWD, 16>(a, L.window, 0, s);
-    case 32: return launch_ws<MODE_FWD, 32>(a, L.window, 0, s);
+    case 16: return launch_ws<MODE_FWD, 16>(a, L.window, L.n_pb, s);
+    case 32: return launch_ws<MODE_FWD, 32>(a, L.window, L.n_pb, s);
     default: return PCB_USAGE;
   }
 }
 
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
-                         const float* rmax, float* flow_scratch, float* gshift,
-                         int32_t* counters, bool split_ok) {
+                         const float* rmax, const float* vbase, const float* pbase,
+                         float* flow_scratch, float* gshift, int32_t* counters, bool split_ok) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -700,11 +784,16 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.shift = rmax;
   a.aux = scratch;
   a.out = flow_scratch;
+  a.vbase_in = vbase;
+  a.pbase_in = pbase;
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
   if (ws_long_k(a.cap)) {
-    if (launch_group_shift(a, (int)L.k_m, g.uniform ? 1 : tc.count, gshift, s)) return PCB_CUDA;
+    const int64_t n = g.uniform ? 1 : tc.count;
+    if (launch_group_shift<MODE_CF>(a, (int)L.k_m, n, gshift, gshift + n * ldb, s))
+      return PCB_CUDA;
     a.gshift = gshift;
+    a.gbase = gshift + n * ldb;
     a.gshift_stride = g.uniform ? 0 : ldb;
   }
   if (a.kslices > 1 &&

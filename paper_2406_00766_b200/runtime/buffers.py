@@ -4,6 +4,12 @@ Same arrays, same (rows x batch) node-major layout, on the GPU in fp32.
 Rows are padded to a stride ``ldb`` (multiple of 32 samples) so kernels
 can vectorise; the public attributes are ``[:, :B]`` views, so
 ``bufs.values[slot, col]`` indexes exactly like the reference.
+
+The device stores log values as (integer block base, fp32 offset) pairs
+(csrc/pcb_internal.cuh): ``values_full`` holds the offsets and the work
+buffer the per-(sum block, sample) bases.  ``bufs.values`` adds them back
+(fp32 log values, as the reference exposes); ``bufs.value_offsets`` is the
+raw device table.
 """
 from __future__ import annotations
 
@@ -36,8 +42,21 @@ class EvalBuffers:
     _extra: dict = field(default_factory=dict)
 
     @property
-    def values(self):
+    def value_offsets(self):
         return self.values_full[:, : self.batch_size]
+
+    @property
+    def values(self):
+        """Node log values [slots x B] (offset + block base, materialised)."""
+        import torch
+        raw = self.values_full[:, : self.batch_size]
+        vb = self._extra.get("slot_vb")
+        n_sb = int(self._extra.get("n_sb_tot", 0))
+        if vb is None or n_sb == 0:
+            return raw
+        base = self.work[: n_sb * self.ldb].view(n_sb, self.ldb)[:, : self.batch_size]
+        add = base[vb.clamp(min=0)]
+        return raw + torch.where((vb >= 0)[:, None], add, torch.zeros_like(add))
 
     @property
     def scratch(self):
@@ -71,7 +90,8 @@ def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None) -> Ev
     def z(rows):
         return torch.zeros((max(int(rows), 1), ldb), dtype=torch.float32, device=dev)
 
-    return EvalBuffers(
+    slot_vb = plan.info["slot_vb"][: max(compiled.num_value_slots, 1)]
+    bufs = EvalBuffers(
         batch_size=b, ldb=ldb,
         xT=torch.zeros((max(compiled.num_vars, 1), ldb), dtype=torch.int32, device=dev),
         values_full=z(compiled.num_value_slots),
@@ -84,3 +104,6 @@ def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None) -> Ev
         work=torch.zeros(max(n_work, 1), dtype=torch.float32, device=dev),
         device=dev,
     )
+    bufs._extra["slot_vb"] = torch.from_numpy(np.asarray(slot_vb, dtype=np.int64)).to(dev)
+    bufs._extra["n_sb_tot"] = int(slot_vb.max()) + 1 if slot_vb.size else 0
+    return bufs

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 22
+VERSION = 23
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -589,6 +589,27 @@ def _slab_of(ids, starts, slab):
     return out
 
 
+def slot_base_rows(compiled) -> np.ndarray:
+    """Per value slot: the row of its sum block's base in the device ``vbase``
+    region (sum blocks of all layers in layer order, each layer's blocks in
+    slot order), or -1 for slots with base 0 (reserved rows, inputs).  Log
+    values are stored as (base, offset) pairs; see csrc/pcb_internal.cuh."""
+    c = compiled
+    out = np.full(max(c.num_value_slots, 1), -1, dtype=np.int64)
+    off = 0
+    for L in c.layers:
+        sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
+            np.zeros(0, np.int64)
+        if not sids.size:
+            continue
+        base, n = int(sids.min()), int(sids.size)
+        if not np.array_equal(np.sort(sids), base + L.k_m * np.arange(n)):
+            raise RuntimeError("sum blocks of a layer must be contiguous value slots")
+        out[base:base + n * L.k_m] = off + np.arange(n * L.k_m) // L.k_m
+        off += n
+    return out
+
+
 def build_program(compiled, *, tensor_cores: bool = True):
     """Return (program int64 array, blob int32 array, info dict)."""
     blob = _Blob()
@@ -599,9 +620,13 @@ def build_program(compiled, *, tensor_cores: bool = True):
         prog.extend([off, n])
 
     c = compiled
+    slot_vb = slot_base_rows(c)
     prog += [c.num_vars, c.num_value_slots, c.scratch_size, c.num_prod_rows, c.theta_size,
              c.f_params_size, c.reserved, c.root_slot, c.root_row]
-    ref(c.root_children if c.root_children is not None else np.zeros(0, np.int64))
+    rc = np.asarray(c.root_children if c.root_children is not None else np.zeros(0), np.int64)
+    ref(rc)
+    ref(slot_vb[rc] if rc.size else np.zeros(0, np.int64))
+    prog.append(int(slot_vb[c.root_slot]) if c.root_slot >= 0 else -1)
     ref(np.asarray(c.var_categories, dtype=np.int64))
     prog.append(1 if tensor_cores else 0)
     t_start, t_slab_f, t_slab_c, t_km, t_kn, plane_t = mma_tiles(c, tensor_cores)
@@ -839,6 +864,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ch_flat[(row_off[ev.out][:, None] + np.arange(f)).ravel()] = ev.children.ravel()
         ref(row_off)
         ref(ch_flat)
+        ref(slot_vb[ch_flat] if ch_flat.size else np.zeros(0, np.int64))  # child base rows
         # derived: sum-block range of the layer (contiguous value slots)
         sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
             np.zeros(0, np.int64)
@@ -927,7 +953,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
             "pre_ratio_layers": int(sum(pre_ratio)), "em_fused_layers": int(sum(em_fusable)),
             "em_fused_layer_ids": [li for li, f in enumerate(em_fusable) if f], "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
-            "mma_elems": mma_elems, "scratch_rows": scratch_total}
+            "mma_elems": mma_elems, "scratch_rows": scratch_total, "slot_vb": slot_vb}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
 
 
