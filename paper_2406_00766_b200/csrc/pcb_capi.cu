@@ -194,6 +194,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.prow_off = r.ref();
     L.prow_ch = r.ref();
     L.prow_cb = r.ref();
+    L.prod_uniform = (int)r.get();
     L.sb_base = r.get();
     L.n_sb = r.get();
     L.push_flag = r.ref();

@@ -86,6 +86,7 @@ struct Layer {
   // derived tables (plan v3)
   const int32_t *prow_off, *prow_ch;  // per scratch row: product children CSR
   const int32_t* prow_cb;             // per CSR child: its value block's vbase row, -1 = base 0
+  int prod_uniform = 0;               // every block's rows share one child-base list (row 0's)
   int64_t sb_base, n_sb;              // sum blocks of the layer: slots [sb_base, +n_sb*k_m)
   int64_t n_pb;                       // product blocks in the window incl. pad block 0
   int64_t pb_off = 0, vb_off = 0;     // first pbase / vbase row of the layer

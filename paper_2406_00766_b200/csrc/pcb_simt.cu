@@ -332,8 +332,11 @@ __device__ __forceinline__ float rebase(float beta, float o, float base) {
   return base == PCB_NEG_INF ? PCB_NEG_INF : (beta - base) + o;
 }
 
-template <int PER>
-__global__ void __launch_bounds__(RW * 32)
+// UNI: every row of a block takes its children's bases from row 0's base
+// rows (plan.prod_blocks_uniform), so the summed base is formed once per
+// sample and only the offsets stay in registers.
+template <int PER, bool UNI>
+__global__ void __launch_bounds__(RW * 32, (UNI && PER == 4) ? 4 : 2)
     k_prod_block(int k_n, int B, int ldb, const int32_t* __restrict__ row_off,
                  const int32_t* __restrict__ ch, const int32_t* __restrict__ cb,
                  const float* __restrict__ values, const float* __restrict__ vbase,
@@ -344,34 +347,69 @@ __global__ void __launch_bounds__(RW * 32)
   const bool live = b < B;
   const float ninf = PCB_NEG_INF;
   float4 mx = make_float4(ninf, ninf, ninf, ninf);
-  float4 be[PER], of[PER];
+  float4 be[UNI ? 1 : PER], of[PER];
+  if (UNI) {
+    // rows share one fan-in (row 0's): slot by slot, every row's child index
+    // and value loads are issued together (PER independent gathers)
+    be[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int ra[PER];
+    bool rl[PER];
 #pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int j = warp + u * RW;
-    be[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    of[u] = make_float4(ninf, ninf, ninf, ninf);
-    if (j >= k_n || !live) continue;
-    const int r = blk * k_n + j;
-    const int a = __ldg(row_off + r), z = __ldg(row_off + r + 1);
-    if (a < z) {
-      of[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int q = a; q < z; ++q) {
-        of[u] = f4add(of[u], *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + q) * ldb + b));
-        const int c = __ldg(cb + q);
-        if (c >= 0) be[u] = f4add(be[u], *reinterpret_cast<const float4*>(vbase + (int64_t)c * ldb + b));
-      }
+    for (int u = 0; u < PER; ++u) {
+      const int j = warp + u * RW;
+      const int r = blk * k_n + j;
+      rl[u] = live && j < k_n && __ldg(row_off + r) < __ldg(row_off + r + 1);
+      ra[u] = (j < k_n) ? __ldg(row_off + r) : 0;
+      of[u] = rl[u] ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(ninf, ninf, ninf, ninf);
     }
-    mx = f4max(mx, f4add(be[u], of[u]));
+    const int a0 = __ldg(row_off + blk * k_n), f = __ldg(row_off + blk * k_n + 1) - a0;
+    for (int q = 0; q < f; ++q) {
+      int idx[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) idx[u] = rl[u] ? __ldg(ch + ra[u] + q) : 0;
+      const int c = live ? __ldg(cb + a0 + q) : -1;
+      float4 v[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+        if (rl[u]) v[u] = *reinterpret_cast<const float4*>(values + (int64_t)idx[u] * ldb + b);
+      if (c >= 0) be[0] = f4add(be[0], *reinterpret_cast<const float4*>(vbase + (int64_t)c * ldb + b));
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+        if (rl[u]) of[u] = f4add(of[u], v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) mx = f4max(mx, of[u]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int j = warp + u * RW;
+      be[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      of[u] = make_float4(ninf, ninf, ninf, ninf);
+      if (j >= k_n || !live) continue;
+      const int r = blk * k_n + j;
+      const int a = __ldg(row_off + r), z = __ldg(row_off + r + 1);
+      if (a < z) {
+        of[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = a; q < z; ++q) {
+          of[u] = f4add(of[u], *reinterpret_cast<const float4*>(values + (int64_t)__ldg(ch + q) * ldb + b));
+          const int c = __ldg(cb + q);
+          if (c >= 0) be[u] = f4add(be[u], *reinterpret_cast<const float4*>(vbase + (int64_t)c * ldb + b));
+        }
+      }
+      mx = f4max(mx, f4add(be[u], of[u]));
+    }
   }
   mx = block_max_all(mx);
   if (!live) return;
+  if (UNI) mx = f4add(mx, be[0]);
   const float4 base = make_float4(floorf(mx.x), floorf(mx.y), floorf(mx.z), floorf(mx.w));
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
     const int j = warp + u * RW;
     if (j >= k_n) continue;
-    const float4 o = make_float4(rebase(be[u].x, of[u].x, base.x), rebase(be[u].y, of[u].y, base.y),
-                                 rebase(be[u].z, of[u].z, base.z), rebase(be[u].w, of[u].w, base.w));
+    const float4 e = be[UNI ? 0 : u];
+    const float4 o = make_float4(rebase(e.x, of[u].x, base.x), rebase(e.y, of[u].y, base.y),
+                                 rebase(e.z, of[u].z, base.z), rebase(e.w, of[u].w, base.w));
     *reinterpret_cast<float4*>(scratch + (int64_t)(blk * k_n + j) * ldb + b) = o;
   }
   if (warp == 0) *reinterpret_cast<float4*>(pbase + (int64_t)blk * ldb + b) = base;
@@ -383,8 +421,13 @@ int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float
   if (!B || !L.n_pb) return PCB_OK;
   dim3 grid((unsigned)L.n_pb, (unsigned)((B + SLAB - 1) / SLAB));
 #define PCB_PB(PER)                                                                          \
-  k_prod_block<PER><<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off, L.prow_ch,     \
-                                             L.prow_cb, values, vbase_all, scratch, pbase)
+  (L.prod_uniform                                                                            \
+       ? k_prod_block<PER, true><<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off,    \
+                                                          L.prow_ch, L.prow_cb, values,     \
+                                                          vbase_all, scratch, pbase)        \
+       : k_prod_block<PER, false><<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off,   \
+                                                           L.prow_ch, L.prow_cb, values,    \
+                                                           vbase_all, scratch, pbase))
   if (L.k_n <= RW) PCB_PB(1);
   else if (L.k_n <= 2 * RW) PCB_PB(2);
   else if (L.k_n <= 4 * RW) PCB_PB(4);

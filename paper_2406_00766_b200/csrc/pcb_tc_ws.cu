@@ -399,44 +399,42 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         }
         return;
       }
-      const float* first = MODE == MODE_CF ? a.vbase_in : a.shift;
-      for (int pass = 0; pass < (MODE == MODE_CF ? 2 : 1); ++pass) {
-        for (int c0 = 0; c0 < a.cap; c0 += 8) {
-          int sc[8];
+      // one pass: child flow keeps (gr, g) online -- raising gr by d raises
+      // every earlier R + (gr - base) log2 e term, hence g, by d log2 e
+      for (int c0 = 0; c0 < a.cap; c0 += 8) {
+        int sc[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = c0 + e;
-            sc[e] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
-            if (pass == 0) nk += sc[e] >= 0;
-          }
-          float v[SPL][8], w[SPL][8];
-#pragma unroll
-          for (int u = 0; u < SPL; ++u) {
-            const int b = it.b0 + lane + 32 * u;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const bool ok = sc[e] >= 0 && b < a.B;
-              const int64_t o = (int64_t)(sc[e] - a.sb_base) / KC * a.ldb + b;
-              v[u][e] = ok ? __ldg((pass == 0 ? first : a.shift) + o) : PCB_NEG_INF;
-              w[u][e] = (ok && pass == 1) ? __ldg(a.vbase_in + o) : 0.f;
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < SPL; ++u)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              if (pass == 0) g[u] = fmaxf(g[u], v[u][e]);
-              else gr[u] = fmaxf(gr[u], fmaf(g[u] - w[u][e], kL2E, v[u][e]));
-            }
+        for (int e = 0; e < 8; ++e) {
+          const int c = c0 + e;
+          sc[e] = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
+          nk += sc[e] >= 0;
         }
-      }
-      if (MODE == MODE_CF) {  // (g, gr) = (shift, base): pass 0 found the base
+        float v[SPL][8], w[SPL][8];
 #pragma unroll
         for (int u = 0; u < SPL; ++u) {
-          const float t = g[u];
-          g[u] = gr[u];
-          gr[u] = t;
+          const int b = it.b0 + lane + 32 * u;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const bool ok = sc[e] >= 0 && b < a.B;
+            const int64_t o = (int64_t)(sc[e] - a.sb_base) / KC * a.ldb + b;
+            v[u][e] = ok ? __ldg(a.shift + o) : PCB_NEG_INF;
+            w[u][e] = (MODE == MODE_CF && ok) ? __ldg(a.vbase_in + o) : PCB_NEG_INF;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < SPL; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (MODE == MODE_FWD) {
+              g[u] = fmaxf(g[u], v[u][e]);
+            } else if (w[u][e] != PCB_NEG_INF) {
+              if (w[u][e] > gr[u]) {
+                if (g[u] != PCB_NEG_INF) g[u] += (w[u][e] - gr[u]) * kL2E;
+                gr[u] = w[u][e];
+              }
+              g[u] = fmaxf(g[u], fmaf(gr[u] - w[u][e], kL2E, v[u][e]));
+            }
+          }
       }
     };
     int g_u = 0;
@@ -490,7 +488,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       // reduced); forward: offsets ln D from the base G (stored with the
       // first chunk of every sum block); child flow: l = product offsets
       // already moved onto the common base (offset + base_pb - Gr)
-      auto finish = [&](int c0, float* o, const float* d, const float* l) {
+      auto finish = [&](int c0, float* o, const float* d, const float* l, float pb) {
         if (MODE == MODE_FWD) {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
@@ -498,17 +496,19 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
           if (c0 % a.nb == 0)
             a.vbase[(out_row(c0) - a.out_base) / a.nb * a.ldb + b] = dead ? 0.f : g;
         } else {
+          const float db = pb - gr;  // exact integer difference (-inf: dead block)
 #pragma unroll
           for (int i = 0; i < 16; ++i)  // flow = D * 2^g * exp(l) = 2^(log2 D + fma(l, log2 e, g))
-            o[(int64_t)i * a.ldb] = (dead || !(d[i] > 0.f)) ? 0.f : ex2(lg2(d[i]) + fmaf(l[i], kL2E, g));
+            o[(int64_t)i * a.ldb] =
+                (dead || !(d[i] > 0.f)) ? 0.f : ex2(lg2(d[i]) + fmaf(l[i] + db, kL2E, g));
         }
       };
-      auto load_l = [&](int c0, float* l) {
+      auto load_l = [&](int c0, float* l, float& pb) {
         const int64_t row = out_row(c0);
         const float* lp = a.aux + row * a.ldb + b;
-        const float db = __ldg(a.pbase_in + row / a.nb * a.ldb + b) - gr;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) l[i] = lp[(int64_t)i * a.ldb] + db;
+        for (int i = 0; i < 16; ++i) l[i] = lp[(int64_t)i * a.ldb];
+        pb = __ldg(a.pbase_in + row / a.nb * a.ldb + b);
       };
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
@@ -516,13 +516,14 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       if (a.kslices == 1) {
         // child flow: the epilogue also reads the children's log values; the
         // next chunk's are loaded before this chunk's TMEM load
-        float l[16], ln[16];
-        if (MODE == MODE_CF && live && h * 16 < N) load_l(h * 16, ln);
+        float l[16], ln[16], pb = 0.f, pbn = 0.f;
+        if (MODE == MODE_CF && live && h * 16 < N) load_l(h * 16, ln, pbn);
         for (int c0 = h * 16; c0 < N; c0 += 32) {
           if (MODE == MODE_CF) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) l[i] = ln[i];
-            if (live && c0 + 32 < N) load_l(c0 + 32, ln);
+            pb = pbn;
+            if (live && c0 + 32 < N) load_l(c0 + 32, ln, pbn);
           }
           float v[16];
           tmem_ld16(tbase + c0, v);
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
           }
-          finish(c0, a.out + out_row(c0) * a.ldb + b, v, l);
+          finish(c0, a.out + out_row(c0) * a.ldb + b, v, l, pb);
         }
         tc_fence_before();
         __syncwarp();
@@ -566,11 +567,11 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
           for (int c0 = h * 16; c0 < N; c0 += 32) {
             if (!live) continue;
             float* o = a.out + out_row(c0) * a.ldb + b;
-            float d[16], l[16];
+            float d[16], l[16], pb = 0.f;
 #pragma unroll
             for (int i = 0; i < 16; ++i) d[i] = __ldcg(o + (int64_t)i * a.ldb);
-            if (MODE == MODE_CF) load_l(c0, l);
-            finish(c0, o, d, l);
+            if (MODE == MODE_CF) load_l(c0, l, pb);
+            finish(c0, o, d, l, pb);
           }
         }
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // g_last reuse

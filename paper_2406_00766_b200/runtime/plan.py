@@ -610,6 +610,30 @@ def slot_base_rows(compiled) -> np.ndarray:
     return out
 
 
+def prod_blocks_uniform(fan, row_off, cb_flat, k_n: int) -> bool:
+    """Every product block of the window takes its children's bases from the
+    same base rows, slot by slot (its non-empty rows have one fan-in and one
+    child-base list; row 0 is non-empty unless the whole block is padding):
+    the product kernel then forms the block's summed base once per sample."""
+    nb = fan.size // k_n
+    if nb == 0:
+        return True
+    f = fan.reshape(nb, k_n)
+    f0 = f[:, :1]
+    if np.any((f != 0) & (f != f0)):
+        return False
+    fmax = int(fan.max()) if fan.size else 0
+    if fmax == 0:
+        return True
+    cb = np.full((fan.size, fmax), -3, dtype=np.int64)
+    r = np.repeat(np.arange(fan.size), fan)
+    q = np.arange(cb_flat.size) - np.repeat(row_off[:-1], fan)
+    cb[r, q] = cb_flat
+    cb = cb.reshape(nb, k_n, fmax)
+    live = (f != 0)[:, :, None]
+    return bool(np.all(~live | (cb == cb[:, :1, :])))
+
+
 def build_program(compiled, *, tensor_cores: bool = True):
     """Return (program int64 array, blob int32 array, info dict)."""
     blob = _Blob()
@@ -864,7 +888,9 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ch_flat[(row_off[ev.out][:, None] + np.arange(f)).ravel()] = ev.children.ravel()
         ref(row_off)
         ref(ch_flat)
-        ref(slot_vb[ch_flat] if ch_flat.size else np.zeros(0, np.int64))  # child base rows
+        cb_flat = slot_vb[ch_flat] if ch_flat.size else np.zeros(0, np.int64)
+        ref(cb_flat)  # child base rows
+        prog.append(int(prod_blocks_uniform(fan, row_off, cb_flat, L.k_n)))
         # derived: sum-block range of the layer (contiguous value slots)
         sids = np.concatenate([g.sum_ids for g in L.fwd_groups]) if L.fwd_groups else \
             np.zeros(0, np.int64)
