@@ -384,11 +384,11 @@ def run_ours(args, w):
     _lib.profile_read()
     # eager: the class timers are host-side event pairs; the side-stream
     # overlap is switched off so each class is timed on its own
-    ts.lean_mode = 2
+    ts.serial = True
     for i in range(prof_steps):
         ts._eager(dev_batches[i % n_pool])
     torch.cuda.synchronize()
-    ts.lean_mode = 1
+    ts.serial = False
     prof = _lib.profile_read()
     _lib.profile_enable(False)
 

@@ -27,6 +27,21 @@
  *   theta                [theta_size]
  *   xT                   [num_vars x ldb] int32, category or -1 (missing)
  * Sample columns b >= B are padding and never contribute to parameter flows.
+ *
+ * Log values are stored as (integer block base, fp32 offset) pairs: d_values
+ * and d_scratch hold offsets, d_work holds one integer-valued fp32 base per
+ * (sum block | product block, sample) (its first rows: the sum-block bases of
+ * all layers in layer order, see pcb_plan_workspace_floats).  A node's log
+ * value is offset + base; bases add exactly, so log-value differences (flow
+ * ratios) keep fp32 relative precision at any |log p|.
+ *
+ * Ownership and threading: the plan is immutable after pcb_plan_set_theta /
+ * pcb_plan_set_mma and may be shared by any number of streams; every call
+ * that runs on a stream takes its mutable state from its arguments (caller-
+ * owned buffers and, for pcb_train_step, a per-stream pcb_exec).  The
+ * tensor-core kernels read the bf16 planes of the plan's own theta, so
+ * passes over tensor-core layers require d_theta == the table bound with
+ * pcb_plan_set_theta (PCB_USAGE otherwise).
  */
 #ifndef PCIRC_B200_H
 #define PCIRC_B200_H
@@ -43,9 +58,15 @@ extern "C" {
 #define PCB_NUMERIC 3
 #define PCB_CUDA 4
 
-#define PCB_ABI_VERSION 2
+#define PCB_ABI_VERSION 3
 
 typedef struct pcb_plan pcb_plan;
+typedef struct pcb_exec pcb_exec;
+
+/* pcb_train_step flags */
+#define PCB_STEP_LEAN 1   /* lean launches (nothing downstream reads node values / flows) */
+#define PCB_STEP_SERIAL 2 /* no side-stream overlap (per-kernel-class profiling) */
+#define PCB_STEP_EM 4     /* apply the mini-batch EM update inside the call */
 
 /* ABI version of the loaded library. */
 int pcb_abi_version(void);
@@ -77,27 +98,6 @@ int pcb_theta_refresh(const pcb_plan* plan, void* stream, const float* d_theta);
  * rewrites the bf16 tensor-core planes (no separate pcb_theta_refresh). */
 int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta);
 
-/* Lean step mode (training steps that only consume the log-likelihood and
- * f_params): when the first layer's products are single-child aliases of
- * exclusively owned staged inputs (plan-detected), forward writes those
- * inputs' log values straight into the product rows of the scratch and
- * backward reads their flows straight from the product-flow rows, skipping
- * that layer's product evaluation and flow push.  The aliased inputs' rows of
- * d_values / d_flows and the aliased products' d_prod_flows rows are then not
- * written.  Host-side setting read at launch time (also while a CUDA graph
- * records); default 0. */
-int pcb_plan_set_lean(pcb_plan* plan, int lean);  /* 2: lean, side stream serialised (profiling) */
-
-/* Inline input EM for single-process lean steps (no flow all-reduce between
- * the backward pass and EM): while enabled, a lean pcb_backward on the plan's
- * own bound table applies the mini-batch EM update (pseudocount, step_size)
- * to every staged input's pmf in the input-flow pass itself (its flows are
- * then not written to d_f_params), zeroing and accumulating d_status; the
- * next pcb_em_update with the same parameters and d_status updates only the
- * remaining groups.  Same arithmetic as the separate pass. */
-int pcb_plan_set_inline_em(pcb_plan* plan, int enable, float pseudocount, float step_size,
-                           int32_t* d_status);
-
 /* Validate a device batch (xT, [num_vars x ldb]) against the category counts:
  * writes the number of bad entries to *d_bad (device int32).
  * Replaces: pcirc/runtime/engine.py:36-52 (_validate_batch) for device batches. */
@@ -111,9 +111,10 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
                             const int32_t* d_x, int32_t* d_xT);
 
 /* Floats of device workspace (d_work) the passes below need at row stride ldb:
- * per-(product block, sample) child maxima, per-(sum block, sample) flow-ratio
- * maxima and per-(sum, sample) shifted log2 flow ratios of one layer.  Derived
- * state, not part of the reference's buffers. */
+ * the sum-block bases of all layers [first n_sum_blocks x ldb floats], the
+ * product-block bases, per-(sum block, sample) flow-ratio maxima, per-(sum,
+ * sample) shifted log2 flow ratios of one layer, long-K shifts and split-K
+ * counters.  Derived state, not part of the reference's buffers. */
 int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb);
 
 /* Full forward pass: values, scratch, lroot[B].
@@ -140,6 +141,40 @@ int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int
                        const float* d_theta, const float* d_values, float* d_flows,
                        float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
                        float* d_f_params, float* d_work);
+
+/* Per-stream execution state of pcb_train_step: a side stream and two
+ * events (the parameter flows of pre-ratioed layers overlap the child-flow
+ * chain on the side stream).  One per stream that runs training steps. */
+int pcb_exec_create(const pcb_plan* plan, pcb_exec** out);
+int pcb_exec_destroy(pcb_exec* exec);
+
+/* One training step on a batch: forward + backward (+ EM with PCB_STEP_EM),
+ * the reference's _accumulate_batch + em_step_full + em_step_mini +
+ * apply_theta (pcirc/train.py:84-101, :133-142) in one call.
+ *   PCB_STEP_LEAN: lean launches.  When the first layer's products are
+ *     single-child aliases of exclusively owned staged inputs (plan-
+ *     detected), forward writes those inputs' log values straight into the
+ *     product rows and backward reads their flows from the product-flow rows
+ *     (that layer's product evaluation and push are skipped; those rows of
+ *     d_values / d_flows / d_prod_flows are not written); fused push + flow
+ *     ratio (the ratio rows of pre-ratioed layers overwrite their d_flows
+ *     rows); parameter flows of pre-ratioed layers on exec's side stream.
+ *   PCB_STEP_EM (requires d_theta == the plan's bound table): the update
+ *     theta <- (1 - step) theta + step normalise(F + pseudocount) of
+ *     pcb_em_update is applied in this call.  With PCB_STEP_LEAN, EM runs
+ *     inside the backward pass where the plan proves it exact (staged input
+ *     pmfs in the input-flow pass; tile blocks of eligible layers in the
+ *     parameter-flow epilogue): those parts of d_f_params are not written.
+ *     d_status (device int32[2]) is zeroed and receives [informative groups,
+ *     non-finite results].  Without PCB_STEP_EM d_theta is read-only and
+ *     d_f_params[:theta_size] holds the step's parameter flows (data-parallel
+ *     steps all-reduce them, then call pcb_em_update).
+ * d_prod_flows may be NULL as for pcb_backward; exec may be NULL (serial). */
+int pcb_train_step(const pcb_plan* plan, const pcb_exec* exec, void* stream, int B, int ldb,
+                   const int32_t* d_xT, float* d_theta, float* d_values, float* d_flows,
+                   float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
+                   float* d_f_params, float* d_lroot, float* d_work, int flags,
+                   float pseudocount, float step_size, int32_t* d_status);
 
 /* EM over the simplex groups, in place on d_theta:
  *   theta[g] <- (1 - step) * theta[g] + step * (F[g] + k) / sum(F[g] + k)

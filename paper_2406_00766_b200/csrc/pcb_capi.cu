@@ -272,10 +272,29 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   return PCB_OK;
 }
 
-pcb_plan::~pcb_plan() {
-  if (ev_fork) cudaEventDestroy(ev_fork);
-  if (ev_join) cudaEventDestroy(ev_join);
+pcb_exec::~pcb_exec() {
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
   if (side) cudaStreamDestroy(side);
+}
+
+int pcb_exec_create(const pcb_plan* plan, pcb_exec** out) {
+  if (!plan || !out) return PCB_USAGE;
+  pcb_exec* E = new (std::nothrow) pcb_exec();
+  if (!E) return PCB_USAGE;
+  if (cudaStreamCreateWithFlags(&E->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&E->fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&E->join, cudaEventDisableTiming) != cudaSuccess) {
+    delete E;
+    return PCB_CUDA;
+  }
+  *out = E;
+  return PCB_OK;
+}
+
+int pcb_exec_destroy(pcb_exec* exec) {
+  delete exec;
+  return PCB_OK;
 }
 
 int pcb_plan_destroy(pcb_plan* plan) {
@@ -294,24 +313,6 @@ int pcb_plan_set_mma(pcb_plan* plan, void* d_mma, int64_t elems) {
 int pcb_plan_set_theta(pcb_plan* plan, const float* d_theta) {
   if (!plan) return PCB_USAGE;
   plan->theta_bound = d_theta;
-  return PCB_OK;
-}
-
-int pcb_plan_set_inline_em(pcb_plan* plan, int enable, float pseudocount, float step_size,
-                           int32_t* d_status) {
-  if (!plan || (enable && (!(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f ||
-                           !d_status)))
-    return PCB_USAGE;
-  plan->inline_em = enable ? 1 : 0;
-  plan->inline_kappa = pseudocount;
-  plan->inline_step = step_size;
-  plan->inline_status = d_status;
-  return PCB_OK;
-}
-
-int pcb_plan_set_lean(pcb_plan* plan, int lean) {
-  if (!plan) return PCB_USAGE;
-  plan->lean = lean == 2 ? 2 : (lean ? 1 : 0);
   return PCB_OK;
 }
 
@@ -385,27 +386,21 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   return w;
 }
 
-// the input-flow pass applies EM to the staged inputs' pmfs (lean step, the
-// plan's own table, single process)
-bool inline_em_active(const pcb_plan* P, const float* theta) {
-  return P->inline_em && P->lean && theta == P->theta_bound;
-}
-
-// the layer's products alias their inputs in this (lean) step
-bool lean_alias(const pcb_plan* P, const Layer& L) {
-  return P->lean && P->leaf_alias && &L == &P->layers[0];
+// the layer's products alias their inputs in this (lean) pass
+bool lean_alias(const pcb_plan* P, const Step& st, const Layer& L) {
+  return st.lean && P->leaf_alias && &L == &P->layers[0];
 }
 
 // Products of every layer stay resident in their own window of the
 // all-layer scratch, so the backward pass reads them instead of recomputing
 // (the reference recomputes into one shared window, engine.py:242).
-int layer_forward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
-                  const float* theta, float* values, float* scratch_all, const Work& w) {
+int layer_forward(const pcb_plan* P, const Step& S, const Layer& L, cudaStream_t s, int B,
+                  int ldb, const float* theta, float* values, float* scratch_all, const Work& w) {
   float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
   float* pbase = w.pbase + L.pb_off * (int64_t)ldb;
   float* vbase = w.vbase + L.vb_off * (int64_t)ldb;
   int st;
-  if (lean_alias(P, L)) {
+  if (lean_alias(P, S, L)) {
     // the input pass wrote the product rows and block bases: only the
     // window's padding rows / blocks need -inf
     st = launch_fill(s, L.pad_rows, L.n_pad, B, ldb, scratch, PCB_NEG_INF);
@@ -455,16 +450,17 @@ int child_flows(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ld
   return PCB_OK;
 }
 
-int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ldb,
-                   const float* theta, const float* values, float* flows, float* scratch_all,
+int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B, int ldb,
+                   float* theta, const float* values, float* flows, float* scratch_all,
                    float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
+  const Layer& L = P->layers[li];
   float* scratch = scratch_all + L.scratch_off * (int64_t)ldb;
   int st = PCB_OK;
   // tensor-core flows: the persistent kernels (K blocks 16 / 32); other
   // block sizes take the SIMT kernels
   const bool tc = P->use_tc == 1 && tc_bwd_supported(L) && ws_supported((int)L.k_m, (int)L.k_n) &&
                   pf_ws_supported(L);
-  const bool fused = P->lean && P->push_ratio_ok;
+  const bool fused = S.lean && P->push_ratio_ok;
   // pre-ratioed layers (fused push): the flow rows already hold the ratios
   const float* ratio = w.ratio;
   const float* rmax = w.rmax;
@@ -477,28 +473,25 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
   }
   // parameter flows: on the side stream when their inputs (ratio rows in the
   // flows buffer, per-layer R rows, the layer's scratch window) stay valid
-  // for the rest of the pass, i.e. for pre-ratioed layers of a lean step
-  // EM fused into the parameter-flow epilogue (one-process lean step): the
-  // layer's θ tiles and planes are rewritten there, so its parameter flows
-  // run after its child flows (which read the planes)
-  L.em_done = 0;
-  const bool em_fuse = inline_em_active(P, theta) && L.em_fusable && fused && L.pre_ratio &&
-                       P->side && P->mma && tc && P->use_tc == 1 && pf_ws_supported(L) &&
-                       pf_layer_stores(P, L, B);
+  // for the rest of the pass, i.e. for pre-ratioed layers of a lean step.
+  // EM fused into the parameter-flow epilogue (one-process lean step with
+  // EM): the layer's theta tiles and planes are rewritten there, so its
+  // parameter flows run after its child flows (which read the planes)
+  const bool em_fuse = S.em && S.em_done && L.em_fusable && fused && L.pre_ratio && P->mma &&
+                       tc && pf_layer_stores(P, L, B);
   if (em_fuse) {
     st = child_flows(P, L, s, B, ldb, theta, values, flows, scratch, flow_scratch, ratio, rmax,
                      tc, w);
     if (st) return st;
   }
   cudaStream_t sp = s;
-  if (fused && L.pre_ratio && P->side && P->lean != 2) {
-    if (cudaEventRecord(P->ev_fork, s) != cudaSuccess ||
-        cudaStreamWaitEvent(P->side, P->ev_fork, 0) != cudaSuccess)
+  if (fused && L.pre_ratio && S.ex && S.lean != 2) {
+    if (cudaEventRecord(S.ex->fork, s) != cudaSuccess ||
+        cudaStreamWaitEvent(S.ex->side, S.ex->fork, 0) != cudaSuccess)
       return PCB_CUDA;
-    sp = P->side;
+    sp = S.ex->side;
   }
-  PfEm em{P->inline_kappa, P->inline_step, P->inline_status, P->mma, P->mma_plane,
-          const_cast<float*>(theta)};
+  PfEm em{S.kappa, S.step, S.status, P->mma, P->mma_plane, theta};
   // accumulating layers zero their own flow range first (fp_cover plans skip
   // the whole-buffer memset)
   if (P->fp_cover && L.flow_hi > L.flow_lo && !(tc && B > 0 && pf_layer_stores(P, L, B)) &&
@@ -518,17 +511,122 @@ int layer_backward(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int
     if (st) return st;
   }
   if (em_fuse) {
-    L.em_done = 1;
+    (*S.em_done)[li] = 1;
   } else {
     st = child_flows(P, L, s, B, ldb, theta, values, flows, scratch, flow_scratch, ratio, rmax,
                      tc, w);
     if (st) return st;
   }
   // aliased leaf products: the input pass reads their flow rows directly
-  if (lean_alias(P, L)) return PCB_OK;
+  if (lean_alias(P, S, L)) return PCB_OK;
   if (fused && L.n_pblk)
     return launch_push_ratio(L, s, B, ldb, flow_scratch, values, flows, w.rmax_all);
   return launch_prod_accum_push(L, s, B, ldb, flow_scratch, prod_flows, flows);
+}
+
+int run_forward(const pcb_plan* P, const Step& S, cudaStream_t s, int B, int ldb,
+                const int32_t* d_xT, const float* d_theta, float* d_values, float* d_scratch,
+                float* d_lroot, float* d_work) {
+  const Work w = carve(P, ldb, d_work);
+  // values.fill(-inf) (engine.py:204): every input and sum-block row (padding
+  // rows included) is written below, so only the reserved constant rows need it.
+  int st = launch_fill_range(s, 0, P->reserved, B, ldb, d_values, PCB_NEG_INF);
+  if (st) return st;
+  st = launch_input_fwd(P, s, B, ldb, d_xT, d_theta, d_values, d_scratch, w.pbase, S.lean != 0);
+  if (st) return st;
+  for (auto& L : P->layers) {
+    st = layer_forward(P, S, L, s, B, ldb, d_theta, d_values, d_scratch, w);
+    if (st) return st;
+  }
+  return launch_root_fwd(P, s, B, ldb, d_values, w.vbase, d_lroot);
+}
+
+int run_backward(const pcb_plan* P, Step& S, cudaStream_t s, int B, int ldb,
+                 const int32_t* d_xT, float* d_theta, const float* d_values, float* d_flows,
+                 float* d_scratch, float* d_flow_scratch, float* d_prod_flows, float* d_f_params,
+                 float* d_work) {
+  // prod_flows may be skipped only when no product row accumulates across layers
+  if (!d_prod_flows && P->num_prod_rows && !P->prod_flows_optional) return PCB_USAGE;
+  const Work w = carve(P, ldb, d_work);
+  {
+    ProfScope prof_(KC_MISC, s);
+    // replica ranges (past theta_size) are folded onto their master tiles and
+    // never written: a lean step, whose EM reads only [0, theta_size), leaves
+    // them alone
+    const int64_t fp_n = P->fp_cover ? zero_tile(P) : S.lean ? P->theta_size : P->f_params_size;
+    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * fp_n, s) != cudaSuccess) return PCB_CUDA;
+    if (!B) return PCB_OK;
+    // only rows that accumulate (several pushes) or receive none need zeros;
+    // single-push rows are stored by their push
+    if (launch_zero_ranges(s, P->n_zero, P->zero_start, P->zero_len, ldb, d_flows))
+      return PCB_CUDA;
+    // every product row's first accumulation stores (plan flag): no zeroing
+    if (d_prod_flows && P->num_prod_rows && !P->prod_rows_written &&
+        cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * P->num_prod_rows * ldb, s) !=
+            cudaSuccess)
+      return PCB_CUDA;
+  }
+  const bool side = S.lean && P->push_ratio_ok && S.ex && S.lean != 2;
+  int st = launch_root_bwd(P, s, B, ldb, d_flows, d_prod_flows);
+  if (st) return st;
+  for (size_t li = P->layers.size(); li-- > 0;) {
+    st = layer_backward(P, S, li, s, B, ldb, d_theta, d_values, d_flows, d_scratch,
+                        d_flow_scratch, d_prod_flows, d_f_params, w);
+    if (st) return st;
+  }
+  bool done = false;
+  st = launch_input_param_flows(P, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch, d_f_params,
+                                S.lean != 0, (S.em && P->in_inline_ok) ? &S : nullptr, &done);
+  if (st) return st;
+  S.inputs_done = done;
+  if (side && (cudaEventRecord(S.ex->join, S.ex->side) != cudaSuccess ||
+               cudaStreamWaitEvent(s, S.ex->join, 0) != cudaSuccess))
+    return PCB_CUDA;
+  return launch_replica_reduce(P, s, d_f_params);
+}
+
+// The EM pass over the groups the backward pass did not already update
+// (S.em_done layers' tile blocks, the staged inputs when S.inputs_done);
+// d_status accumulates (zeroed by the caller).
+int run_em(const pcb_plan* P, const Step* S, cudaStream_t s, const float* d_f_params,
+           float* d_theta, float kappa, float step, int32_t* d_status) {
+  // the plan's own table: the tile-block pass also rewrites the bf16 MMA
+  // planes; tensor-core tiles outside tile blocks get the separate refresh
+  const bool own = d_theta == P->theta_bound && P->mma;
+  int st = PCB_OK;
+  if (S && S->em_done) {
+    // tile blocks of layers whose EM ran in their parameter-flow epilogue are
+    // skipped (blocks are ordered: other layers first, then layer by layer)
+    int64_t lo = 0, hi = P->n_em_pre;
+    for (size_t li = 0; li < P->layers.size(); ++li) {
+      const Layer& L = P->layers[li];
+      if (!L.em_fusable || L.em_hi <= L.em_lo) continue;
+      const bool done = (*S->em_done)[li] != 0;
+      if (!done && L.em_lo == hi) {
+        hi = L.em_hi;
+        continue;
+      }
+      if (!done) {
+        st = launch_em_tiles(P, s, d_f_params, d_theta, kappa, step, d_status, own, lo, hi);
+        if (st) return st;
+        lo = L.em_lo;
+        hi = L.em_hi;
+      }
+    }
+    st = launch_em_tiles(P, s, d_f_params, d_theta, kappa, step, d_status, own, lo, hi);
+  } else {
+    st = launch_em_tiles(P, s, d_f_params, d_theta, kappa, step, d_status, own);
+  }
+  if (st) return st;
+  st = launch_em(P, s, d_f_params, d_theta, kappa, step, d_status, S && S->inputs_done);
+  if (st) return st;
+  if (own && P->n_em_tiles < P->n_mma_tiles) return launch_theta_to_mma(P, s, d_theta);
+  return PCB_OK;
+}
+
+// the tensor-core kernels read the bf16 planes of the plan's bound table
+bool theta_ok(const pcb_plan* P, const float* d_theta) {
+  return !P->use_tc || (P->mma && d_theta == P->theta_bound);
 }
 
 bool bad_dims(const pcb_plan* p, int B, int ldb) {
@@ -580,148 +678,90 @@ int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
 int pcb_forward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
                 const float* d_theta, float* d_values, float* d_scratch, float* d_lroot,
                 float* d_work) {
-  if (bad_dims(plan, B, ldb) || !d_work) return PCB_USAGE;
+  if (bad_dims(plan, B, ldb) || !d_work || !theta_ok(plan, d_theta)) return PCB_USAGE;
   if (!B) return PCB_OK;
-  cudaStream_t s = as_stream(stream);
-  const Work w = carve(plan, ldb, d_work);
-  // values.fill(-inf) (engine.py:204): every input and sum-block row (padding
-  // rows included) is written below, so only the reserved constant rows need it.
-  int st = launch_fill_range(s, 0, plan->reserved, B, ldb, d_values, PCB_NEG_INF);
-  if (st) return st;
-  st = launch_input_fwd(plan, s, B, ldb, d_xT, d_theta, d_values, d_scratch, w.pbase);
-  if (st) return st;
-  for (auto& L : plan->layers) {
-    st = layer_forward(plan, L, s, B, ldb, d_theta, d_values, d_scratch, w);
-    if (st) return st;
-  }
-  return launch_root_fwd(plan, s, B, ldb, d_values, w.vbase, d_lroot);
+  return run_forward(plan, Step{}, as_stream(stream), B, ldb, d_xT, d_theta, d_values, d_scratch,
+                     d_lroot, d_work);
 }
 
 int pcb_backward(const pcb_plan* plan, void* stream, int B, int ldb, const int32_t* d_xT,
                  const float* d_theta, const float* d_values, float* d_flows, float* d_scratch,
                  float* d_flow_scratch, float* d_prod_flows, float* d_f_params, float* d_work) {
-  if (bad_dims(plan, B, ldb) || !d_work) return PCB_USAGE;
-  // prod_flows may be skipped only when no product row accumulates across layers
-  if (!d_prod_flows && plan->num_prod_rows && !plan->prod_flows_optional) return PCB_USAGE;
+  if (bad_dims(plan, B, ldb) || !d_work || !theta_ok(plan, d_theta)) return PCB_USAGE;
+  Step S;  // no EM: theta is only read
+  return run_backward(plan, S, as_stream(stream), B, ldb, d_xT, const_cast<float*>(d_theta),
+                      d_values, d_flows, d_scratch, d_flow_scratch, d_prod_flows, d_f_params,
+                      d_work);
+}
+
+int pcb_train_step(const pcb_plan* plan, const pcb_exec* exec, void* stream, int B, int ldb,
+                   const int32_t* d_xT, float* d_theta, float* d_values, float* d_flows,
+                   float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
+                   float* d_f_params, float* d_lroot, float* d_work, int flags,
+                   float pseudocount, float step_size, int32_t* d_status) {
+  const bool em = (flags & PCB_STEP_EM) != 0;
+  if (bad_dims(plan, B, ldb) || !d_work || !theta_ok(plan, d_theta) ||
+      (flags & ~(PCB_STEP_LEAN | PCB_STEP_SERIAL | PCB_STEP_EM)))
+    return PCB_USAGE;
+  if (em && (!(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f || !d_status ||
+             d_theta != plan->theta_bound))
+    return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
-  const Work w = carve(plan, ldb, d_work);
-  {
-    ProfScope prof_(KC_MISC, s);
-    // replica ranges (past theta_size) are folded onto their master tiles and
-    // never written: a lean step, whose EM reads only [0, theta_size), leaves
-    // them alone
-    const int64_t fp_n = plan->fp_cover ? zero_tile(plan)
-                         : plan->lean  ? plan->theta_size
-                                       : plan->f_params_size;
-    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * fp_n, s) != cudaSuccess) return PCB_CUDA;
-    if (!B) return PCB_OK;
-    // only rows that accumulate (several pushes) or receive none need zeros;
-    // single-push rows are stored by their push
-    if (launch_zero_ranges(s, plan->n_zero, plan->zero_start, plan->zero_len, ldb, d_flows))
-      return PCB_CUDA;
-    // every product row's first accumulation stores (plan flag): no zeroing
-    if (d_prod_flows && plan->num_prod_rows && !plan->prod_rows_written &&
-        cudaMemsetAsync(d_prod_flows, 0, sizeof(float) * plan->num_prod_rows * ldb, s) !=
-            cudaSuccess)
-      return PCB_CUDA;
+  std::vector<char> em_done(plan->layers.size(), 0);
+  Step S;
+  S.lean = (flags & PCB_STEP_LEAN) ? ((flags & PCB_STEP_SERIAL) || !exec ? 2 : 1) : 0;
+  S.ex = exec;
+  if (em) {
+    S.em = S.lean != 0;  // EM inside the backward pass: lean launches only
+    S.kappa = pseudocount;
+    S.step = step_size;
+    S.status = d_status;
+    S.em_done = &em_done;
+    if (cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
   }
-  const bool side = plan->lean && plan->push_ratio_ok;
-  if (side && !plan->side &&
-      (cudaStreamCreateWithFlags(&plan->side, cudaStreamNonBlocking) != cudaSuccess ||
-       cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-       cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming) != cudaSuccess))
-    return PCB_CUDA;
-  const bool inl = inline_em_active(plan, d_theta);
-  plan->inline_done = inl ? 1 : 0;  // d_status zeroed here; inline updates may follow
-  plan->inline_inputs_done = 0;
-  if (inl && cudaMemsetAsync(plan->inline_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
-    return PCB_CUDA;
-  int st = launch_root_bwd(plan, s, B, ldb, d_flows, d_prod_flows);
-  if (st) return st;
-  for (auto it = plan->layers.rbegin(); it != plan->layers.rend(); ++it) {
-    st = layer_backward(plan, *it, s, B, ldb, d_theta, d_values, d_flows, d_scratch,
-                        d_flow_scratch, d_prod_flows, d_f_params, w);
+  int st = PCB_OK;
+  if (B) {
+    st = run_forward(plan, S, s, B, ldb, d_xT, d_theta, d_values, d_scratch, d_lroot, d_work);
     if (st) return st;
   }
-  bool done = false;
-  st = launch_input_param_flows(plan, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch,
-                                d_f_params, inl && plan->in_inline_ok, &done);
-  if (st) return st;
-  plan->inline_inputs_done = done ? 1 : 0;
-  if (side && (cudaEventRecord(plan->ev_join, plan->side) != cudaSuccess ||
-               cudaStreamWaitEvent(s, plan->ev_join, 0) != cudaSuccess))
-    return PCB_CUDA;
-  return launch_replica_reduce(plan, s, d_f_params);
+  st = run_backward(plan, S, s, B, ldb, d_xT, d_theta, d_values, d_flows, d_scratch,
+                    d_flow_scratch, d_prod_flows, d_f_params, d_work);
+  if (st || !em) return st;
+  return run_em(plan, &S, s, d_f_params, d_theta, pseudocount, step_size, d_status);
 }
 
 int pcb_layer_forward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
                       const float* d_theta, float* d_values, float* d_scratch, float* d_work) {
-  if (bad_dims(plan, B, ldb) || !d_work || layer < 0 || layer >= (int)plan->layers.size())
+  if (bad_dims(plan, B, ldb) || !d_work || layer < 0 || layer >= (int)plan->layers.size() ||
+      !theta_ok(plan, d_theta))
     return PCB_USAGE;
   if (!B) return PCB_OK;
-  return layer_forward(plan, plan->layers[layer], as_stream(stream), B, ldb, d_theta, d_values,
-                       d_scratch, carve(plan, ldb, d_work));
+  return layer_forward(plan, Step{}, plan->layers[layer], as_stream(stream), B, ldb, d_theta,
+                       d_values, d_scratch, carve(plan, ldb, d_work));
 }
 
 int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int ldb,
                        const float* d_theta, const float* d_values, float* d_flows,
                        float* d_scratch, float* d_flow_scratch, float* d_prod_flows,
                        float* d_f_params, float* d_work) {
-  if (bad_dims(plan, B, ldb) || !d_work || layer < 0 || layer >= (int)plan->layers.size())
+  if (bad_dims(plan, B, ldb) || !d_work || layer < 0 || layer >= (int)plan->layers.size() ||
+      !theta_ok(plan, d_theta) ||
+      (!d_prod_flows && plan->num_prod_rows && !plan->prod_flows_optional))
     return PCB_USAGE;
   if (!B) return PCB_OK;
-  return layer_backward(plan, plan->layers[layer], as_stream(stream), B, ldb, d_theta, d_values,
-                        d_flows, d_scratch, d_flow_scratch, d_prod_flows, d_f_params,
-                        carve(plan, ldb, d_work));
+  Step S;
+  return layer_backward(plan, S, (size_t)layer, as_stream(stream), B, ldb,
+                        const_cast<float*>(d_theta), d_values, d_flows, d_scratch,
+                        d_flow_scratch, d_prod_flows, d_f_params, carve(plan, ldb, d_work));
 }
 
 int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, float* d_theta,
                   float pseudocount, float step_size, int32_t* d_status) {
-  if (!plan || !(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f) return PCB_USAGE;
+  if (!plan || !d_status || !(pseudocount >= 0.f) || !(step_size > 0.f) || step_size > 1.f)
+    return PCB_USAGE;
   cudaStream_t s = as_stream(stream);
-  // inline input EM already updated the staged inputs' pmfs in the backward
-  // pass (same parameters; its counts are already in d_status)
-  const bool inl = inline_em_active(plan, d_theta) && plan->inline_done &&
-                   d_status == plan->inline_status && pseudocount == plan->inline_kappa &&
-                   step_size == plan->inline_step;
-  const bool inl_inputs = inl && plan->inline_inputs_done;
-  plan->inline_done = 0;
-  plan->inline_inputs_done = 0;
-  if (!inl && cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess)
-    return PCB_CUDA;
-  // the plan's own table: the tile-block pass also rewrites the bf16 MMA
-  // planes; tensor-core tiles outside tile blocks get the separate refresh
-  const bool own = d_theta == plan->theta_bound && plan->mma;
-  int st = PCB_OK;
-  if (inl) {
-    // tile blocks of layers whose EM ran in their parameter-flow epilogue are
-    // skipped (blocks are ordered: other layers first, then layer by layer)
-    int64_t lo = 0, hi = plan->n_em_pre;
-    for (const Layer& L : plan->layers) {
-      if (!L.em_fusable || L.em_hi <= L.em_lo) continue;
-      if (!L.em_done && L.em_lo == hi) {
-        hi = L.em_hi;
-        continue;
-      }
-      if (!L.em_done) {
-        st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own,
-                             lo, hi);
-        if (st) return st;
-        lo = L.em_lo;
-        hi = L.em_hi;
-      }
-    }
-    st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own, lo,
-                         hi);
-    for (const Layer& L : plan->layers) L.em_done = 0;
-  } else {
-    st = launch_em_tiles(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, own);
-  }
-  if (st) return st;
-  st = launch_em(plan, s, d_f_params, d_theta, pseudocount, step_size, d_status, inl_inputs);
-  if (st) return st;
-  if (own && plan->n_em_tiles < plan->n_mma_tiles) return launch_theta_to_mma(plan, s, d_theta);
-  return PCB_OK;
+  if (cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
+  return run_em(plan, nullptr, s, d_f_params, d_theta, pseudocount, step_size, d_status);
 }
 
 int pcb_axpy_accumulate(void* stream, int64_t n, const float* d_src, float* d_dst) {

@@ -102,10 +102,9 @@ struct Layer {
                 *q_base = nullptr, *q_kind = nullptr, *q_rrow = nullptr;
   int pre_ratio = 0;     // every sum block's ratio comes from a fused push
   // EM fused into this layer's parameter-flow epilogue (plan.em_fused_order):
-  // its tile blocks are [em_lo, em_hi); em_done: the last backward pass did it
+  // its tile blocks are [em_lo, em_hi)
   int em_fusable = 0;
   int64_t em_lo = 0, em_hi = 0;
-  mutable int em_done = 0;
   int64_t rmax_off = -1;  // its R rows in the all-layer rmax region
 };
 
@@ -143,7 +142,6 @@ struct Work {
 }  // namespace pcb
 
 struct pcb_plan {
-  ~pcb_plan();
   int64_t num_vars, num_value_slots, scratch_size, num_prod_rows, theta_size,
       f_params_size, reserved;
   int64_t root_slot, root_row;
@@ -196,30 +194,40 @@ struct pcb_plan {
   int64_t n_rmax = 0;
   int64_t n_alias_pad = 0;
   const int32_t* alias_pad = nullptr;  // pad blocks of the first layer's window
-  int lean = 0;
-  // lean steps: parameter flows of pre-ratioed layers run on a side stream
-  // (forked per layer, joined at the end of the backward pass), overlapping
-  // the child-flow / push chain; created on first use
-  mutable cudaStream_t side = nullptr;
-  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  // inline input EM (pcb_plan_set_inline_em): the input-flow pass of a lean
+  // inline input EM (pcb_train_step with EM): the input-flow pass of a lean
   // backward applies the EM update to the staged inputs' pmf groups (the
   // last small rest groups, [n_em_small_noninl, n_em_small)) directly
   int64_t n_em_small_noninl = 0;
   int in_inline_ok = 0;  // every staged input pmf is such a group (ncat <= 256)
-  int inline_em = 0;
-  float inline_kappa = 0.f, inline_step = 1.f;
-  int32_t* inline_status = nullptr;
-  mutable int inline_done = 0;         // the last backward pass zeroed d_status for inline EM
-  mutable int inline_inputs_done = 0;  // ... and updated the staged inputs' pmfs
   int64_t n_em_pre = 0;  // tile blocks of layers without fused EM (first in order)
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
 
+// Per-stream execution state of pcb_train_step (the plan itself is immutable):
+// lean steps run the parameter flows of pre-ratioed layers on a side stream,
+// forked per layer and joined at the end of the backward pass.
+struct pcb_exec {
+  ~pcb_exec();
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
 namespace pcb {
 
 extern unsigned long long g_launches;
+
+// Options of one pass (a plain forward / backward is Step{}); the per-call
+// state of a training step lives here, never in the plan.
+struct Step {
+  int lean = 0;              // 0 full, 1 lean, 2 lean without side-stream overlap
+  bool em = false;           // EM inside the backward pass where exact (one-process steps)
+  float kappa = 0.f, step = 1.f;
+  int32_t* status = nullptr;
+  const pcb_exec* ex = nullptr;
+  std::vector<char>* em_done = nullptr;  // per layer: EM fused into its parameter flows
+  bool inputs_done = false;              // the input-flow pass updated the staged pmfs
+};
 
 // kernel classes for the live per-class timing used by bench.py
 enum KClass {
@@ -248,6 +256,19 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: cache the
+// largest size set for each device ordinal (cache[kMaxDev] per kernel)
+constexpr int kMaxDev = 64;
+inline int ensure_smem(const void* fn, int bytes, int* cache) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return PCB_CUDA;
+  if (dev >= 0 && dev < kMaxDev && bytes <= cache[dev]) return PCB_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return PCB_CUDA;
+  if (dev >= 0 && dev < kMaxDev) cache[dev] = bytes;
+  return PCB_OK;
+}
+
 inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -261,7 +282,8 @@ int check_launch();
 // layer's first product / sum block row (Layer::pb_off / vb_off), except
 // where noted.
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
-                     const float* theta, float* values, float* scratch_all, float* pbase_all);
+                     const float* theta, float* values, float* scratch_all, float* pbase_all,
+                     bool alias);
 int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
                      const float* vbase_all, float* scratch, float* pbase);
 int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float* values,
@@ -281,10 +303,11 @@ int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, in
                            float* flow_scratch);
 int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
                            const float* flow_scratch, float* prod_flows, float* flows);
+// em: apply EM to the staged inputs' pmfs in this pass (theta updated in place)
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
-                             const int32_t* xT, const float* theta, const float* flows,
-                             const float* flow_scratch, float* f_params, bool inline_em,
-                             bool* inline_done);
+                             const int32_t* xT, float* theta, const float* flows,
+                             const float* flow_scratch, float* f_params, bool alias,
+                             const Step* em, bool* inline_done);
 // vbase_all: the whole vbase region (root_vb / root_cb are global rows)
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
                     const float* vbase_all, float* lroot);

@@ -209,19 +209,15 @@ __global__ void __launch_bounds__(IN_THREADS)
 }
 
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
-                     const float* theta, float* values, float* scratch_all, float* pbase_all) {
+                     const float* theta, float* values, float* scratch_all, float* pbase_all,
+                     bool alias) {
   ProfScope prof_(KC_INPUT_FWD, s);
   const InBlocks& ib = p->in_blocks;
   if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
-    static int attr = 0;
-    if (bytes > attr) {
-      if (cudaFuncSetAttribute(k_input_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               bytes) != cudaSuccess)
-        return PCB_CUDA;
-      attr = bytes;
-    }
-    const bool alias = p->lean && p->leaf_alias;
+    static int attr[kMaxDev] = {};
+    if (ensure_smem((const void*)k_input_fwd_block, bytes, attr)) return PCB_CUDA;
+    alias = alias && p->leaf_alias;
     const Layer* L0 = alias ? &p->layers[0] : nullptr;
     k_input_fwd_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, values,
@@ -1216,41 +1212,30 @@ __global__ void __launch_bounds__(IS_THREADS)
 }
 
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
-                             const int32_t* xT, const float* theta, const float* flows,
-                             const float* flow_scratch, float* f_params, bool inline_em,
-                             bool* inline_done) {
+                             const int32_t* xT, float* theta, const float* flows,
+                             const float* flow_scratch, float* f_params, bool alias,
+                             const Step* em, bool* inline_done) {
   ProfScope prof_(KC_INPUT_FLOW, s);
   *inline_done = false;
   const InBlocks& ib = p->in_blocks;
-  const int32_t* arow = (p->lean && p->leaf_alias) ? ib.alias_row : nullptr;
+  const int32_t* arow = (alias && p->leaf_alias) ? ib.alias_row : nullptr;
   // sorted (atomic-free) kernel when its shared-memory slots fit, else the
   // shared-memory histogram
   const int64_t sorted_bytes = ((int64_t)IS_WARPS * ldb + 2 * (ib.max_ncat + 1) + 1 + B) * 4;
   static const bool hist_only = getenv("PCB_INFLOW_HIST") != nullptr;
   if (ib.n && !hist_only && sorted_bytes <= 160 * 1024) {
-    static int attr_s = 0;
-    if (sorted_bytes > attr_s) {
-      if (cudaFuncSetAttribute(k_input_flow_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sorted_bytes) != cudaSuccess)
-        return PCB_CUDA;
-      attr_s = (int)sorted_bytes;
-    }
+    static int attr_s[kMaxDev] = {};
+    if (ensure_smem((const void*)k_input_flow_sorted, (int)sorted_bytes, attr_s)) return PCB_CUDA;
     k_input_flow_sorted<<<(unsigned)ib.n, IS_THREADS, (size_t)sorted_bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
-        arow, ib.alias_dir, flow_scratch, f_params,
-        inline_em ? const_cast<float*>(theta) : nullptr, p->inline_kappa, p->inline_step,
-        p->inline_status);
+        arow, ib.alias_dir, flow_scratch, f_params, em ? theta : nullptr,
+        em ? em->kappa : 0.f, em ? em->step : 1.f, em ? em->status : nullptr);
     if (check_launch()) return PCB_CUDA;
-    *inline_done = inline_em;
+    *inline_done = em != nullptr;
   } else if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
-    static int attr = 0;
-    if (bytes > attr) {
-      if (cudaFuncSetAttribute(k_input_flow_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               bytes) != cudaSuccess)
-        return PCB_CUDA;
-      attr = bytes;
-    }
+    static int attr[kMaxDev] = {};
+    if (ensure_smem((const void*)k_input_flow_block, bytes, attr)) return PCB_CUDA;
     k_input_flow_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
         arow, ib.alias_dir, flow_scratch, f_params);

@@ -592,13 +592,8 @@ template <int KN, int RS>
 int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float* rmax,
               const float* scratch, const float* vbase, const float* pbase, cudaStream_t s) {
   using C = PfCfg<KN, RS>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_param_flow_ws<KN, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kBytes) != cudaSuccess)
-      return PCB_CUDA;
-    attr = true;
-  }
+  static int attr[kMaxDev] = {};
+  if (ensure_smem((const void*)k_param_flow_ws<KN, RS>, C::kBytes, attr)) return PCB_CUDA;
   PfArgs a = a0;
   a.cgroups = (int)((a.cap * KN + PF_N - 1) / PF_N);
   a.mtiles = 2;  // super-rows hold <= 256 sums

@@ -591,13 +591,8 @@ namespace {
 template <int MODE, int KC>
 int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   using C = WsCfg<MODE, KC>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_sum_ws<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kBytes) != cudaSuccess)
-      return PCB_CUDA;
-    attr = true;
-  }
+  static int attr[kMaxDev] = {};
+  if (ensure_smem((const void*)k_sum_ws<MODE, KC>, C::kBytes, attr)) return PCB_CUDA;
   CUtensorMap tm0, tm1, tm2;
   if (make_rows_map(&tm0, a.src0, rows0, a.ldb, KC)) return PCB_CUDA;
   // per K block one row: the block base (forward) / the ratio shift R and the

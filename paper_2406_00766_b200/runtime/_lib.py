@@ -29,8 +29,10 @@ SIGNATURES = {
     "pcb_plan_set_mma": (_I, [_P, _P, _L]),
     "pcb_theta_refresh": (_I, [_P, _P, _P]),
     "pcb_plan_set_theta": (_I, [_P, _P]),
-    "pcb_plan_set_lean": (_I, [_P, _I]),
-    "pcb_plan_set_inline_em": (_I, [_P, _I, _F, _F, _P]),
+    "pcb_exec_create": (_I, [_P, C.POINTER(_P)]),
+    "pcb_exec_destroy": (_I, [_P]),
+    "pcb_train_step": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _F,
+                            _F, _P]),
     "pcb_tc_selftest_mn": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "pcb_check_batch": (_I, [_P, _P, _I, _I, _P, _P]),
     "pcb_transpose_batch_i64": (_I, [_P, _P, _I, _I, _P, _P]),
@@ -49,7 +51,10 @@ SIGNATURES = {
     "pcb_tc_selftest": (_I, [_P, _I, _I, _P, _P, _P]),
 }
 
-ABI_VERSION = 2
+ABI_VERSION = 3
+
+# pcb_train_step flags
+STEP_LEAN, STEP_SERIAL, STEP_EM = 1, 2, 4
 
 _lib = None
 

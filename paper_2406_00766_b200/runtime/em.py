@@ -18,7 +18,7 @@ from . import _lib
 from .plan import device_plan
 
 __all__ = ["EMAccumulator", "apply_theta", "em_accumulate", "em_step_full", "em_step_mini",
-           "em_update_", "write_back_params"]
+           "em_update_", "propagate_theta", "sync_theta_to_host", "write_back_params"]
 
 
 @dataclass
@@ -34,8 +34,8 @@ class EMAccumulator:
     def for_circuit(cls, compiled, device=None) -> "EMAccumulator":
         import torch
         plan = device_plan(compiled, device)
-        return cls(f_params=torch.zeros(compiled.f_params_size, dtype=torch.float64
-                                        if False else torch.float32, device=plan.device),
+        return cls(f_params=torch.zeros(compiled.f_params_size, dtype=torch.float32,
+                                        device=plan.device),
                    _ll=torch.zeros((), dtype=torch.float64, device=plan.device))
 
     @property
@@ -83,6 +83,8 @@ def em_update_(compiled, f_params, *, pseudocount: float, step_size: float, thet
     target = plan.theta if theta is None else theta
     _lib.call("pcb_em_update", plan.handle, _lib.stream_handle(), f_params.data_ptr(),
               target.data_ptr(), float(pseudocount), float(step_size), plan.status.data_ptr())
+    if target is plan.theta:
+        compiled.mark_theta_on_device(plan)
     # on plan.theta the EM pass rewrites the tensor-core planes itself
     if check:
         _status_check(plan, int(compiled.group_off.size - 1))
@@ -127,11 +129,23 @@ def apply_theta(compiled, new_theta):
         plan.upload_theta(new_theta if isinstance(new_theta, torch.Tensor) else compiled.theta)
 
 
-def sync_theta_to_host(compiled, device=None) -> np.ndarray:
-    """Copy the device theta (authoritative during training) back to ``compiled.theta``."""
-    plan = device_plan(compiled, device)
-    compiled.theta[:] = plan.theta.double().cpu().numpy()
+def sync_theta_to_host(compiled, device=None, *, plan=None) -> np.ndarray:
+    """Copy a plan's device theta (authoritative during training) back to
+    ``compiled.theta`` now (it is otherwise synced lazily on access)."""
+    plan = plan if plan is not None else device_plan(compiled, device)
+    compiled.mark_theta_on_device(plan)
     return compiled.theta
+
+
+def propagate_theta(compiled, plan) -> None:
+    """After training ``plan``: every other device plan of ``compiled`` (the
+    other tensor-core setting, other devices) takes its table, and the host
+    copy follows lazily."""
+    for other in (compiled._device_plans or {}).values():
+        if other is plan:
+            continue
+        other.upload_theta(plan.theta)
+    compiled.mark_theta_on_device(plan)
 
 
 def write_back_params(compiled, graph):

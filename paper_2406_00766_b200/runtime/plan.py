@@ -242,7 +242,7 @@ def leaf_alias(compiled, blocks, push_count):
     When every product of the first layer has a single child, that child is a
     staged input whose only parent is the product, and each staged input block
     maps onto whole product blocks of the layer window as one ascending or
-    descending run, a lean step (``pcb_plan_set_lean``) writes the inputs' log
+    descending run, a lean step (``pcb_train_step`` with PCB_STEP_LEAN) writes the inputs' log
     values straight into the product rows (plus the block maxima the sum
     kernels shift by) and reads the inputs' flows straight from the product
     flow rows: the product evaluation and the flow push of that layer vanish.

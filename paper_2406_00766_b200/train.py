@@ -99,99 +99,155 @@ def _dp():
     return 0, 1
 
 
-def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
-          tensor_cores: bool = True, group=None) -> TrainResult:
-    """Run EM; ``compiled.theta`` holds the trained table on return (``train.py:104-154``)."""
+def _device_data(compiled, data, dev):
+    """The dataset resident on the device as int32, validated there
+    (``engine.py:36-52``'s shape / category checks, FormatError)."""
     import torch
-    from .runtime import _lib
-    from .runtime.buffers import allocate_buffers
-    from .runtime.em import em_update_, sync_theta_to_host
-    from .runtime.engine import _validate_host_batch
+    from .errors import FormatError
+    if isinstance(data, torch.Tensor):
+        x = data
+    else:
+        arr = np.asarray(data)
+        if arr.dtype.kind not in "iu":
+            arr = arr.astype(np.int64)
+        x = torch.from_numpy(np.ascontiguousarray(arr))
+    if x.dim() != 2 or x.shape[1] != compiled.num_vars:
+        raise FormatError(f"batch must have shape (n, {compiled.num_vars}), got "
+                          f"{tuple(x.shape)}")
+    x = x.to(dev, non_blocking=False)
+    if x.numel():
+        cats = torch.as_tensor(np.asarray(compiled.var_categories), device=dev)
+        if bool((x < -1).any()):
+            raise FormatError("category values must be >= 0, or -1 for missing")
+        bad = (x >= cats[None, :]).any(dim=0)
+        if bool(bad.any()):
+            var = int(torch.nonzero(bad)[0, 0])
+            raise FormatError(
+                f"variable {var} has values outside [0, {compiled.var_categories[var]})")
+    return x.to(torch.int32).contiguous()
+
+
+def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
+          tensor_cores: bool = True, group=None, graph: bool = True) -> TrainResult:
+    """Run EM; ``compiled.theta`` holds the trained table on return (``train.py:104-154``).
+
+    Every step is one ``pcb_train_step`` (``runtime.step.TrainStep``): lean
+    launches, EM inside the backward pass where exact (one process), each
+    batch size's step captured once as a CUDA graph and replayed.  The data
+    stay on the device; the epoch log-likelihood and the EM status counters
+    accumulate there, and the host synchronises once per epoch.  If an epoch
+    reports a dead EM step or non-finite parameters, it is re-run from its
+    starting table eagerly with a check after every step, so the
+    ``NumericError`` is raised at the failing step with the parameters of the
+    step before it, as the reference does (``em.py:70-75``).
+    """
+    import torch
+    from .runtime.em import em_update_, propagate_theta
     from .runtime.plan import device_plan
+    from .runtime.step import TrainStep
 
     cfg = cfg or TrainConfig()
-    data = np.asarray(data, dtype=np.int64)
-    n = data.shape[0] if data.ndim == 2 else 0
+    plan = device_plan(compiled, device, tensor_cores=tensor_cores)
+    dev = plan.device
+    if not isinstance(data, torch.Tensor):
+        data = np.asarray(data)
+    n = int(data.shape[0]) if data.ndim == 2 else 0
     if n == 0:
         raise UsageError("training data is empty")
-    data = _validate_host_batch(compiled, data)
+    with torch.cuda.device(dev):
+        data_dev = _device_data(compiled, data, dev)
     result = TrainResult()
     batch_size = cfg.batch_size
     if batch_size > n:
         result.notes.append(f"batch size {batch_size} exceeds {n} samples; clipped to {n}")
         batch_size = n
-    plan = device_plan(compiled, device, tensor_cores=tensor_cores)
     if not plan.theta_finite:
         raise NumericError("parameter table contains non-finite values")
     rank, world = _dp()
-    dev = plan.device
-    data_dev = torch.from_numpy(data.astype(np.int32)).to(dev)
     shuffle_rng = np.random.default_rng(np.random.SeedSequence(cfg.seed).spawn(2)[1])
     theta_size = compiled.theta_size
     n_groups = int(compiled.group_off.size - 1)
-    bufs_cache: dict = {}
+    full = cfg.mode == "full"
+    # NCCL collectives can be captured in the step's graph; other backends replay eagerly
+    use_graph = graph
+    if world > 1:
+        import torch.distributed as dist
+        use_graph = graph and dist.get_backend(group) == "nccl"
+    ar = (lambda fp, ll: allreduce_accumulators(fp, ll, theta_size, group)) if world > 1 \
+        else None
+    steps: dict = {}
     with torch.cuda.device(dev):
-        stream = _lib.stream_handle()
-        dead_steps = torch.zeros((), dtype=torch.int32, device=dev)
-        bad_values = torch.zeros((), dtype=torch.int32, device=dev)
-        for _ in range(cfg.epochs):
-            t0 = time.perf_counter()
-            order = shuffle_rng.permutation(n) if cfg.mode == "mini" else np.arange(n)
-            order_dev = torch.from_numpy(order).to(dev)
+        ep_fp = torch.zeros(max(theta_size, 1), dtype=torch.float32, device=dev) if full \
+            else None
+
+        def step_for(B):
+            ts = steps.get(B)
+            if ts is None:
+                ts = steps[B] = TrainStep(
+                    compiled, B, pseudocount=cfg.pseudocount, step_size=cfg.step_size,
+                    device=dev, graph=use_graph and B > 0, tensor_cores=tensor_cores,
+                    allreduce=None if full else ar, accumulate=ep_fp)
+            return ts
+
+        def run_epoch(order_dev, eager_checks: bool, prev=None):
             ep_ll = torch.zeros((), dtype=torch.float64, device=dev)
-            ep_fp = (torch.zeros(compiled.f_params_size, dtype=torch.float32, device=dev)
-                     if cfg.mode == "full" else None)
-            samples = 0
+            dead = torch.zeros((), dtype=torch.int32, device=dev)
+            bad = torch.zeros((), dtype=torch.int32, device=dev)
+            if full:
+                ep_fp.zero_()
             for a in range(0, n, batch_size):
                 b_all = min(n, a + batch_size) - a
                 lo, hi = shard_span(b_all, rank, world)
-                B = hi - lo
-                bufs = bufs_cache.get(B)
-                if bufs is None:
-                    bufs = bufs_cache[B] = allocate_buffers(compiled, B, dev, plan=plan)
-                idx = order_dev[a + lo:a + hi]
-                xb = data_dev.index_select(0, idx)
-                step_ll = torch.zeros((), dtype=torch.float64, device=dev)
-                if B:
-                    _lib.call("pcb_transpose_batch_i32", plan.handle, stream, B, bufs.ldb,
-                              xb.data_ptr(), bufs.xT.data_ptr())
-                    _lib.call("pcb_forward", plan.handle, stream, B, bufs.ldb,
-                              bufs.xT.data_ptr(), plan.theta.data_ptr(),
-                              bufs.values_full.data_ptr(), bufs.scratch_full.data_ptr(),
-                              bufs.lroot.data_ptr(), bufs.work.data_ptr())
-                    step_ll += bufs.lroot.double().sum()
-                _lib.call("pcb_backward", plan.handle, stream, B, bufs.ldb, bufs.xT.data_ptr(),
-                          plan.theta.data_ptr(), bufs.values_full.data_ptr(),
-                          bufs.flows_full.data_ptr(), bufs.scratch_full.data_ptr(),
-                          bufs.flow_scratch_full.data_ptr(), bufs.prod_flows_full.data_ptr(),
-                          bufs.f_params.data_ptr(), bufs.work.data_ptr())
-                samples += b_all
-                if cfg.mode == "full":
-                    _lib.call("pcb_axpy_accumulate", stream, ep_fp.numel(),
-                              bufs.f_params.data_ptr(), ep_fp.data_ptr())
-                    ep_ll += step_ll
+                ts = step_for(hi - lo)
+                if hi > lo:
+                    torch.index_select(data_dev, 0, order_dev[a + lo:a + hi], out=ts.x)
+                if prev is not None and not full:
+                    prev.copy_(plan.theta)
+                ll = ts.run(ts.x)
+                ep_ll += ll
+                if full:
                     continue
-                allreduce_accumulators(bufs.f_params, step_ll, theta_size, group)
-                ep_ll += step_ll
-                em_update_(compiled, bufs.f_params, pseudocount=cfg.pseudocount,
-                           step_size=cfg.step_size, check=False, plan=plan)
                 if n_groups:
-                    dead_steps += (plan.status[0] == 0).int()
-                bad_values += plan.status[1]
-            if cfg.mode == "full":
+                    dead += (plan.status[0] == 0).int()
+                bad += plan.status[1]
+                if eager_checks and (int(dead.item()) or int(bad.item())):
+                    return ep_ll, dead, bad, True
+            if full:
                 allreduce_accumulators(ep_fp, ep_ll, theta_size, group)
                 em_update_(compiled, ep_fp, pseudocount=cfg.pseudocount, step_size=1.0,
                            check=False, plan=plan)
                 if n_groups:
-                    dead_steps += (plan.status[0] == 0).int()
-                bad_values += plan.status[1]
-            ll = float(ep_ll.item())
-            if int(dead_steps.item()):
-                raise NumericError("every normalization group accumulated zero flow; "
-                                   "use a positive pseudocount or check the data")
-            if int(bad_values.item()):
+                    dead += (plan.status[0] == 0).int()
+                bad += plan.status[1]
+            return ep_ll, dead, bad, False
+
+        for _ in range(cfg.epochs):
+            t0 = time.perf_counter()
+            order = shuffle_rng.permutation(n) if cfg.mode == "mini" else np.arange(n)
+            order_dev = torch.from_numpy(order).to(dev)
+            snapshot = plan.theta.clone()
+            ep_ll, dead, bad, _ = run_epoch(order_dev, eager_checks=False)
+            if int(dead.item()) or int(bad.item()):
+                # re-run the epoch from its starting table with per-step
+                # checks: raise at the failing step, parameters of the step
+                # before it (the failing step's update is rolled back)
+                plan.theta.copy_(snapshot)
+                plan.refresh_mma()
+                for ts in steps.values():
+                    ts.graph = None
+                prev = torch.empty_like(plan.theta)
+                ep_ll, dead, bad, stopped = run_epoch(order_dev, eager_checks=True, prev=prev)
+                if stopped and not full:
+                    plan.theta.copy_(prev)
+                    plan.refresh_mma()
+                plan.theta_finite = bool(torch.isfinite(plan.theta).all().item())
+                propagate_theta(compiled, plan)
+                if int(dead.item()):
+                    raise NumericError("every normalization group accumulated zero flow; "
+                                       "use a positive pseudocount or check the data")
                 raise NumericError("EM update produced non-finite parameters")
-            result.epoch_log_likelihood.append(ll / samples)
+            ll = float(ep_ll.item())
+            result.epoch_log_likelihood.append(ll / n)
             result.epoch_seconds.append(time.perf_counter() - t0)
-        sync_theta_to_host(compiled, dev)
+        propagate_theta(compiled, plan)
     return result

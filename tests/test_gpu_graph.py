@@ -9,11 +9,11 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def _steps(c, xs, graph):
+def _steps(c, xs, graph, theta0):
     import torch
     from paper_2406_00766_b200.runtime.step import TrainStep
     from paper_2406_00766_b200.runtime.em import apply_theta
-    apply_theta(c, c.theta)  # every run starts from the host table
+    apply_theta(c, theta0)  # every run starts from the same table
     ts = TrainStep(c, xs[0].shape[0], pseudocount=1e-6, step_size=0.05, graph=graph)
     lls = []
     for x in xs:
@@ -31,8 +31,8 @@ def test_graph_step_matches_eager_and_oracle():
     theta0 = c.theta.copy()
     rng = np.random.default_rng(11)
     xs = [rng.integers(0, 8, size=(160, 24)) for _ in range(3)]
-    th_e, ll_e, _ = _steps(c, xs, graph=False)
-    th_g, ll_g, ts = _steps(c, xs, graph=True)
+    th_e, ll_e, _ = _steps(c, xs, graph=False, theta0=theta0)
+    th_g, ll_g, ts = _steps(c, xs, graph=True, theta0=theta0)
     assert ts.graph is not None and ts.launches_per_step > 0
     np.testing.assert_allclose(ll_g, ll_e, rtol=1e-6)
     np.testing.assert_allclose(th_g, th_e, rtol=1e-5, atol=1e-9)
@@ -57,6 +57,8 @@ def test_lean_step_matches_full(tensor_cores, kind, k):
     push (no ratio pass).  Flows agree to float rounding: product flows with
     several parent blocks are accumulated atomically, so their summation order
     varies from run to run in either mode."""
+    import ctypes as C
+
     import torch
     from paper_2406_00766_b200 import structures as S
     from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
@@ -79,13 +81,20 @@ def test_lean_step_matches_full(tensor_cores, kind, k):
     lr0, b0 = forward(c, x, tensor_cores=tensor_cores)
     backward(c, b0, tensor_cores=tensor_cores)
     want_ll, want_f = lr0.clone(), b0.f_params.clone()
-    _lib.call("pcb_plan_set_lean", plan.handle, 1)
+    # the same batch through pcb_train_step with lean launches and no EM
+    lr1, b1 = forward(c, x, tensor_cores=tensor_cores)
+    ex = C.c_void_p()
+    _lib.call("pcb_exec_create", plan.handle, C.byref(ex))
     try:
-        lr1, b1 = forward(c, x, tensor_cores=tensor_cores)
-        backward(c, b1, tensor_cores=tensor_cores)
+        _lib.call("pcb_train_step", plan.handle, ex, _lib.stream_handle(), b1.batch_size,
+                  b1.ldb, b1.xT.data_ptr(), plan.theta.data_ptr(), b1.values_full.data_ptr(),
+                  b1.flows_full.data_ptr(), b1.scratch_full.data_ptr(),
+                  b1.flow_scratch_full.data_ptr(), b1.prod_flows_full.data_ptr(),
+                  b1.f_params.data_ptr(), b1.lroot.data_ptr(), b1.work.data_ptr(),
+                  _lib.STEP_LEAN, 0.0, 1.0, plan.status.data_ptr())
         torch.cuda.synchronize()
     finally:
-        _lib.call("pcb_plan_set_lean", plan.handle, 0)
+        _lib.load().pcb_exec_destroy(ex)
     assert torch.equal(lr1, want_ll)
     got, ref = b1.f_params.double(), want_f.double()
     assert torch.max(torch.abs(got - ref) / torch.clamp(ref.abs(), min=1e-30)).item() < 2e-6
@@ -115,14 +124,15 @@ def test_inline_em_matches_separate_pass(batch):
     xs = [rng.integers(0, 8, size=(batch, 30)) for _ in range(2)]
     for x in xs:
         x[rng.random(x.shape) < 0.1] = -1
-    apply_theta(c, c.theta)
+    theta0 = c.theta.copy()
+    apply_theta(c, theta0)
     ts = TrainStep(c, batch, pseudocount=1e-3, step_size=0.1, graph=False)
     lls, ths, sts = [], [], []
     for x in xs:
         lls.append(float(ts.run(torch.from_numpy(x.astype(np.int32)).cuda()).item()))
         ths.append(ts.plan.theta.double().cpu().numpy())
         sts.append(ts.plan.status[:2].cpu().numpy().copy())
-    apply_theta(c, c.theta)
+    apply_theta(c, theta0)
     plan = device_plan(c)
     for i, x in enumerate(xs):
         lr, bufs = forward(c, x)
@@ -142,7 +152,7 @@ def _lean_step_vs_oracle(c, x, pseudocount=1e-4, step=0.2):
     from paper_2406_00766_b200.runtime.em import apply_theta
     from paper_2406_00766_b200.runtime.step import TrainStep
     theta0 = c.theta.copy()
-    apply_theta(c, c.theta)
+    apply_theta(c, theta0)
     ts = TrainStep(c, x.shape[0], pseudocount=pseudocount, step_size=step, graph=True)
     ll = float(ts.run(torch.from_numpy(x.astype(np.int32)).cuda()).item())
     got = ts.plan.theta.double().cpu().numpy()
