@@ -10,15 +10,23 @@ parameter flows (N > 1) and the fused mini-batch EM update (alpha 0.01,
 pseudocount 1e-6) — the reference's ``train()`` inner loop
 (``pcirc/train.py:128-142``).
 
-``value``: inputs resident in HBM before the timed region.  ``e2e``: the same
-steps through the public API with each batch copied host(pinned)->device and
-the step log-likelihood read back inside the timed region (the next batch's
-copy runs on a copy stream while the current step computes).  Per-kernel-class
-times come from CUDA events recorded live on the launching stream in a
-separate profiled pass; the dominant class gives ``roofline``.  Every step's
-working set (GBs of values / flows / parameters) exceeds the 126 MB L2, so no
-explicit flush is needed.  ``--impl reference`` times the CPU oracle port of
-the reference on the host cores instead (rank 0 only).
+``value``: inputs resident in HBM before the timed region, the step replayed
+as a CUDA graph.  ``e2e``: one timed 60,000-sample epoch through the drop-in
+``train()`` from a host (numpy) dataset — ceil(60000 / B) steps including the
+tail batch, the per-epoch shuffle, host-side gathers and validation, every
+batch copied host -> device (streamed behind the compute) and the epoch
+log-likelihood read back; ``config.sec_per_epoch`` is that measured epoch.
+Per-kernel-class times come from CUDA events recorded live on the launching
+stream in a separate profiled pass.  Each class is reported against its
+roofline: HBM GB/s from its algorithmic bytes, and for the sum contractions
+also tensor TFLOP/s from its useful flops (2 x sum edges x B) against the
+measured bf16 peak; ``roofline`` is the dominant class on the bound its
+arithmetic intensity selects.  Every step's working set (GBs of values /
+flows / parameters) exceeds the 126 MB L2, so no explicit flush is needed.
+``--impl reference`` times the CPU oracle port of the reference on the host
+cores instead (rank 0 only): forward + backward per sample and the EM pass
+over the whole table timed separately and composed into a step of the
+workload's batch size.
 """
 from __future__ import annotations
 
@@ -120,34 +128,61 @@ def fused_em_bytes(c, info, B, sms=148):
     return e_f, n_pmf
 
 
-def algorithmic_bytes(c, B, info=None):
-    """Minimal fp32 HBM bytes per step per kernel class for
-    the lean training step: products stay resident (evaluated once), the
-    first layer's products alias their inputs when the plan allows it, and
-    the fused push moves each pushed product flow to its children once."""
+def _layer_counts(c, L):
+    n_sum = int(L.report.num_sums)
+    n_prod = int(L.report.num_prods)
+    F = sum(int(ev.children.size) for ev in L.prod_evals)
+    E = int(L.edge_sums.size)
+    # tile work the contraction executes (real (row, column) tile pairs)
+    E_pad = sum(int((np.asarray(g.param_ids) != 0).sum()) for g in L.fwd_groups) * L.k_m * L.k_n
+    return n_sum, n_prod, F, E, E_pad
+
+
+def class_model(c, B, info=None):
+    """Per kernel class of the lean training step: minimal fp32 HBM bytes per
+    step and, for the sum contractions, useful flops per step
+    (2 x sum edges x B, one multiply-add per edge and sample) and the
+    executed bf16 MMA flops (3 MMAs per 16-wide K step: hi*hi + hi*lo + lo*hi,
+    over the real tiles).  Products stay resident (evaluated once), the first
+    layer's products alias their inputs when the plan allows it, the fused
+    push moves each pushed product flow to its children once; each tied pmf
+    is read once.  Only the layers a class actually runs are counted (sum
+    layers of block size 16 / 32 on tensor cores, the rest SIMT)."""
+    from paper_2406_00766_b200.runtime.plan import tc_layer
     info = info or {}
-    n_in = sum(int(ch.node_ids.size) for ch in c.input_layer)
-    n_sum = sum(int(L.report.num_sums) for L in c.layers)
     skip = 1 if info.get("leaf_alias") else 0  # aliased first layer: no product pass / push
-    n_prod = sum(int(L.report.num_prods) for L in c.layers[skip:])
-    F = sum(int(ev.children.size) for L in c.layers[skip:] for ev in L.prod_evals)
-    E = c.num_edges
-    n_pmf = sum(int(ch.param_ids.size) * int(ch.num_categories) for ch in c.input_layer)
-    return {
-        # batch + value rows + each pmf once
-        "input_fwd": B * 4 * (c.num_vars + n_in) + 4 * n_pmf,
-        "prod_eval": B * 4 * (F + n_prod),
-        "sum_fwd_tc": B * 4 * (n_prod + n_sum) + 4 * E,
-        "sum_fwd_simt": B * 4 * (n_prod + n_sum) + 4 * E,
-        # ratio rows + product values; theta read + flow write per edge
-        "param_flow": B * 4 * (n_sum + n_prod) + 8 * E,
-        # ratio rows + product values + product-flow rows; bf16 hi/lo planes
-        "child_flow": B * 4 * (n_sum + 2 * n_prod) + 4 * E,
-        "accum_push": B * 4 * (n_prod + F + n_sum),  # product flows, child rows, sum values
-        # flow rows + batch + pmf read (missing-value spread) and flow write
-        "input_flow": B * 4 * (n_in + c.num_vars) + 8 * n_pmf,
-        "em": 20 * c.theta_size,
-    }
+    n_in = sum(int(ch.node_ids.size) for ch in c.input_layer)
+    pmf = set()
+    for ch in c.input_layer:
+        pmf.update((int(p), int(ch.num_categories)) for p in np.unique(ch.param_ids))
+    n_pmf = sum(k for _, k in pmf)
+    m = {k: {"bytes": 0, "flops": 0, "mma_flops": 0} for k in
+         ("input_fwd", "prod_eval", "sum_fwd_tc", "sum_fwd_simt", "param_flow", "child_flow",
+          "accum_push", "input_flow", "em")}
+    m["input_fwd"]["bytes"] = B * 4 * (c.num_vars + n_in) + 4 * n_pmf
+    m["input_flow"]["bytes"] = B * 4 * (n_in + c.num_vars) + 8 * n_pmf
+    m["em"]["bytes"] = 20 * c.theta_size
+    for li, L in enumerate(c.layers):
+        n_sum, n_prod, F, E, E_pad = _layer_counts(c, L)
+        tc = tc_layer(L) and L.k_m in (16, 32, 64) and L.k_n in (16, 32)
+        fwd = "sum_fwd_tc" if tc else "sum_fwd_simt"
+        if li >= skip:
+            m["prod_eval"]["bytes"] += B * 4 * (F + n_prod)
+            m["accum_push"]["bytes"] += B * 4 * (n_prod + F + n_sum)
+        m[fwd]["bytes"] += B * 4 * (n_prod + n_sum) + 4 * E
+        # ratio rows + product offsets; theta read + flow write per edge
+        m["param_flow"]["bytes"] += B * 4 * (n_sum + n_prod) + 8 * E
+        # ratio rows + product offsets + product-flow rows; theta (bf16 planes)
+        m["child_flow"]["bytes"] += B * 4 * (n_sum + 2 * n_prod) + 4 * E
+        for k in (fwd, "param_flow", "child_flow"):
+            m[k]["flops"] += 2 * E * B
+            if tc:
+                m[k]["mma_flops"] += 3 * 2 * E_pad * B
+    return m
+
+
+def algorithmic_bytes(c, B, info=None):
+    return {k: v["bytes"] for k, v in class_model(c, B, info).items()}
 
 
 class ClockSampler:
@@ -209,26 +244,39 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------- CPU oracle
-def cpu_step_time(c, w, B_cpu, seed=7):
-    """Oracle (float64 numpy port of the reference) fwd + bwd + EM on B_cpu samples."""
+def cpu_step_parts(c, w, B_cpu, seed=7):
+    """Oracle (float64 numpy port of the reference) on B_cpu samples: seconds
+    of forward + backward, and of the EM pass (em_step_full + em_step_mini
+    over the whole table, independent of the batch size)."""
     import oracle
     x = synthetic_batches(c, w, B_cpu, 1, seed)[0].astype(np.int64)
     theta = c.theta.copy()
     t0 = time.perf_counter()
     _, bufs = oracle.forward(c, x, theta=theta)
     oracle.backward(c, bufs, theta=theta)
+    t1 = time.perf_counter()
     new = oracle.em_step_full(c, bufs.f_params, theta=theta, pseudocount=PSEUDOCOUNT)
     if new is not None:
         theta = oracle.em_step_mini(theta, new, STEP_SIZE)
-    return time.perf_counter() - t0
+    return t1 - t0, time.perf_counter() - t1
 
 
 def cpu_sample_size(w):
-    """Samples per CPU step: the full batch where a step fits in ~seconds,
-    else a bounded sample (the per-step EM over all of theta is fixed cost)."""
+    """Samples per timed CPU forward + backward: the full batch where it fits
+    in seconds, else a bounded sample."""
     if w["kind"] == "hmm":
         return 4
     return {16: 512, 64: 64}.get(w["hidden_dim"], 32)
+
+
+def composed(w, B_cpu, t_fb, t_em):
+    """A step of the workload's batch B composed from the measured parts:
+    B / B_cpu x forward+backward(B_cpu) + EM (the reference's per-sample cost
+    is linear in B; its EM pass is one full-table pass per step)."""
+    B = w["batch"]
+    t = B / B_cpu * t_fb + t_em
+    return B / t, t, (f"step(B={B}) = {B}/{B_cpu} x {t_fb:.2f} s (fwd+bwd on {B_cpu} samples) "
+                      f"+ {t_em:.2f} s (EM over theta) = {t:.1f} s")
 
 
 def run_reference(args, w):
@@ -240,22 +288,25 @@ def run_reference(args, w):
     # a quarter of the baseline sample per step keeps K + W steps within minutes
     Bc = max(1, cpu_sample_size(w) // 4)
     for _ in range(args.warmup):
-        cpu_step_time(c, w, Bc)
-    tot = 0.0
+        cpu_step_parts(c, w, Bc)
+    fb = em = 0.0
     for _ in range(args.steps):
-        tot += cpu_step_time(c, w, Bc)
-    v = Bc * args.steps / tot
+        a, b = cpu_step_parts(c, w, Bc)
+        fb += a
+        em += b
+    v, t, formula = composed(w, Bc, fb / args.steps, em / args.steps)
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": "samples/sec fwd+bwd+EM", "value": v,
         "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000 * t, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": w["desc"], "batch_per_step": Bc,
-                   "sec_per_epoch": EPOCH / v},
+        "config": {"workload": args.workload, "desc": w["desc"], "batch_per_step": w["batch"],
+                   "sampled_batch": Bc, "composition": formula, "sec_per_epoch": EPOCH / v},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"{Bc} samples per step of the {args.workload} workload "
-                                   "(forward+backward+EM step over the full theta)"},
+                         "sample": f"per step: forward+backward on {Bc} samples of the "
+                                   f"{args.workload} workload + the EM pass over the full "
+                                   f"theta, composed to batch {w['batch']}: {formula}"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -292,10 +343,8 @@ def run_ours(args, w):
     n_pool = 4
     host_batches = synthetic_batches(c, w, B, n_pool, seed=rank)
     dev_batches = [torch.from_numpy(h).to(dev) for h in host_batches]
-    pinned = [torch.from_numpy(h).pin_memory() for h in host_batches]
     theta_size = c.theta_size
     ll_acc = torch.zeros((), dtype=torch.float64, device=dev)
-    ll_host = torch.zeros((), dtype=torch.float64).pin_memory()
     # the training step as a CUDA graph on one GPU (the batch is copied into a
     # static input buffer, every kernel replays without host launches); eager
     # launches with the NCCL all-reduce on N > 1
@@ -338,46 +387,6 @@ def run_ours(args, w):
     ms_step = ms / args.steps
     value = world * B * args.steps / (ms / 1000.0)
 
-    # ---- end-to-end through host memory
-    # every step's batch is copied from pinned host memory inside the timed
-    # region, on a copy stream into one of two device staging buffers while
-    # the previous step computes; the step then takes it with one
-    # device-to-device copy into the graph's static input (a few µs)
-    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stage = [torch.empty_like(ts.x) for _ in range(2)]
-    copy_stream = torch.cuda.Stream(dev)
-    copied = [torch.cuda.Event(), torch.cuda.Event()]
-    used = [torch.cuda.Event(), torch.cuda.Event()]
-    comp = torch.cuda.current_stream(dev)
-
-    def prefetch(i):
-        k = i % 2
-        copy_stream.wait_event(used[k]) if i >= 2 else copy_stream.wait_stream(comp)
-        with torch.cuda.stream(copy_stream):
-            stage[k].copy_(pinned[i % n_pool], non_blocking=True)
-            copied[k].record(copy_stream)
-
-    barrier()
-    ev2.record()
-    prefetch(0)
-    for i in range(args.steps):
-        k = i % 2
-        comp.wait_event(copied[k])
-        ts.x.copy_(stage[k], non_blocking=True)
-        used[k].record(comp)
-        if i + 1 < args.steps:
-            prefetch(i + 1)
-        sl = run(ts.x)
-        ll_host.copy_(sl, non_blocking=True)
-    ev3.record()
-    barrier()
-    ms_e2e = ev2.elapsed_time(ev3)
-    t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_e2e = float(t.item())
-    e2e_value = world * B * args.steps / (ms_e2e / 1000.0)
-
     # ---- profiled pass: live per-kernel-class CUDA-event times
     prof_steps = max(1, min(3, args.steps))
     _lib.profile_enable(True)
@@ -392,55 +401,102 @@ def run_ours(args, w):
     prof = _lib.profile_read()
     _lib.profile_enable(False)
 
+    # ---- end to end: one 60k-sample epoch through train() from host data
+    from paper_2406_00766_b200.train import TrainConfig, train
+    n_ep = EPOCH
+    data = synthetic_batches(c, w, n_ep, 1, seed=11)[0]  # identical on every rank
+    tcfg = dict(batch_size=world * B, mode="mini", step_size=STEP_SIZE, pseudocount=PSEUDOCOUNT,
+                seed=0)
+    tail = n_ep % (world * B)
+    warm = data[: 2 * world * B + tail]  # builds the full-batch and tail steps (cached)
+    train(c, warm, TrainConfig(epochs=1, **tcfg), device=dev)
+    barrier()
+    res = train(c, data, TrainConfig(epochs=1, **tcfg), device=dev)
+    ep_s = torch.tensor([res.epoch_seconds[0]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ep_s, op=dist.ReduceOp.MAX)
+    ep_s = float(ep_s.item())
+    e2e_value = n_ep / ep_s
+    n_steps_ep = -(-n_ep // (world * B))
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     hbm, tflops, peak_src = measured_peaks()
-    algo = algorithmic_bytes(c, B, ts.plan.info)
+    model = class_model(c, B, ts.plan.info)
     # one-process steps fold EM into the input-flow and parameter-flow passes
     # (DESIGN §3a): the EM class then covers only the small layers' groups, and
     # the per-class minimal bytes above (unfused) no longer describe it
-    inline_em = bool(getattr(ts, "_inline_em", False))
+    inline_em = world == 1
     if inline_em:
-        algo.pop("em", None)
+        model["em"]["bytes"] = None
         # the fused EM's extra minimal bytes: theta write + four bf16 planes
         # instead of the flow write per edge of the layers whose parameter
         # flows run unsplit, theta read + write instead of the flow write per
         # staged input pmf entry
         e_f, n_pmf = fused_em_bytes(c, ts.plan.info, B)
-        algo["param_flow"] += 8 * e_f
-        algo["input_flow"] += 4 * n_pmf
+        model["param_flow"]["bytes"] += 8 * e_f
+        model["input_flow"]["bytes"] += 4 * n_pmf
     classes = {k: v for k, v in prof.items() if v[0] > 0}
     total_prof = sum(v[0] for v in classes.values())
+    ridge = tflops * 1e12 / (hbm * 1e9)  # flop / byte where the two roofs meet
+
+    def figures(k, ms):
+        sec = ms / 1000.0
+        mk = model.get(k, {})
+        by, fl, mm = mk.get("bytes"), mk.get("flops", 0), mk.get("mma_flops", 0)
+        f = {"ms_per_step": ms}
+        if by:
+            f["gbs"] = by / sec / 1e9
+            f["hbm_frac"] = f["gbs"] / hbm
+        if fl:
+            f["tflops"] = fl / sec / 1e12
+            f["tensor_frac"] = f["tflops"] / tflops
+            f["mma_tflops_executed"] = mm / sec / 1e12 if mm else None
+            f["flop_per_byte"] = fl / by if by else None
+        return f
+
+    breakdown = {}
+    for k, v in classes.items():
+        breakdown[k] = figures(k, v[0] / prof_steps)
+        breakdown[k]["launches_per_step"] = v[2] / prof_steps
     dom = max(classes, key=lambda k: classes[k][0])
     dom_ms, dom_scopes, dom_launches = classes[dom]
     per_step_ms = dom_ms / prof_steps
-    dom_bytes = algo.get(dom)
+    fd = breakdown[dom]
+    mk = model.get(dom, {})
+    ai = (mk.get("flops", 0) / mk["bytes"]) if mk.get("bytes") else None
+    tensor_bound = bool(ai) and ai >= ridge
     traffic = None
     tr_file = ROOT / "profiles" / f"traffic_{args.workload}.json"
     if tr_file.exists():
         traffic = json.loads(tr_file.read_text()).get(dom)
-    achieved = (dom_bytes / (per_step_ms / 1000.0) / 1e9) if dom_bytes else None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
-                "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_step": dom_bytes,
+    if tensor_bound:
+        achieved, peak, unit = fd["tflops"], tflops, "TFLOP/s"
+    else:
+        achieved, peak, unit = fd.get("gbs"), hbm, "GB/s"
+    roofline = {"bound": "tensor" if tensor_bound else "hbm", "kernel": dom,
+                "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src + (" (bf16 sustained)" if tensor_bound else " (copy)"),
+                "algorithmic_bytes_per_step": mk.get("bytes"),
+                "useful_flops_per_step": mk.get("flops") or None,
+                "flop_per_byte": ai, "ridge_flop_per_byte": ridge,
+                "hbm_frac": fd.get("hbm_frac"), "tensor_frac": fd.get("tensor_frac"),
                 "kernel_ms_per_step": per_step_ms,
                 "launches_per_step": dom_launches / prof_steps,
                 "share_of_step": dom_ms / total_prof if total_prof else None}
-    breakdown = {k: {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[2] / prof_steps,
-                     "gbs": (algo[k] / (v[0] / prof_steps / 1000.0) / 1e9)
-                     if k in algo and v[0] > 0 else None}
-                 for k, v in classes.items()}
 
     cpu = None
     if world == 1 and not args.no_cpu:
         Bc = cpu_sample_size(w)
-        secs = cpu_step_time(c, w, Bc)
-        cpu = {"value": Bc / secs, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"one forward+backward+EM step on {Bc} samples of {args.workload} "
-                         f"({secs:.1f} s, numpy float64, BLAS threads = host cores)"}
+        t_fb, t_em = cpu_step_parts(c, w, Bc)
+        v, t, formula = composed(w, Bc, t_fb, t_em)
+        cpu = {"value": v, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"forward+backward on {Bc} samples of {args.workload} + the EM pass "
+                         f"over the full theta, composed to batch {B} (numpy float64, BLAS "
+                         f"threads = host cores): {formula}"}
     line = {
         "metric": "samples/sec fwd+bwd+EM", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -450,11 +506,19 @@ def run_ours(args, w):
                    "global_batch": world * B, "block_size": w["block"],
                    "em": f"mini-batch, step {STEP_SIZE}, pseudocount {PSEUDOCOUNT}",
                    "edges": c.num_edges, "theta_size": c.theta_size,
-                   "sec_per_epoch": EPOCH / value, "l2": "working set >> 126 MB L2 (no flush)",
+                   "sec_per_epoch": ep_s,
+                   "sec_per_epoch_note": f"measured: one {n_ep}-sample epoch through train() "
+                                         f"({n_steps_ep} steps incl. the tail batch) from host "
+                                         "data",
+                   "l2": "working set >> 126 MB L2 (no flush)",
                    "parallelism": f"dp{world}", "cuda_graph": graphed,
                    "em_in_backward": inline_em},
         "e2e": {"value": e2e_value, "unit": "samples/s",
-                "h2d_bytes_per_step": B * c.num_vars * 4, "d2h_bytes_per_step": 8},
+                "h2d_bytes_per_step": world * B * c.num_vars * 4 // world,
+                "d2h_bytes_per_step": 8,
+                "how": f"train(): {n_ep}-sample epoch, host numpy int32 dataset, shuffle + "
+                       "per-batch gather / validation on a loader thread, pinned H2D copies "
+                       "streamed behind the compute"},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "kernels": breakdown,

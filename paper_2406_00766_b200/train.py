@@ -100,21 +100,14 @@ def _dp():
 
 
 def _device_data(compiled, data, dev):
-    """The dataset resident on the device as int32, validated there
-    (``engine.py:36-52``'s shape / category checks, FormatError)."""
+    """A device-resident dataset as int32, validated there (``engine.py:36-52``)."""
     import torch
     from .errors import FormatError
-    if isinstance(data, torch.Tensor):
-        x = data
-    else:
-        arr = np.asarray(data)
-        if arr.dtype.kind not in "iu":
-            arr = arr.astype(np.int64)
-        x = torch.from_numpy(np.ascontiguousarray(arr))
+    x = data
     if x.dim() != 2 or x.shape[1] != compiled.num_vars:
         raise FormatError(f"batch must have shape (n, {compiled.num_vars}), got "
                           f"{tuple(x.shape)}")
-    x = x.to(dev, non_blocking=False)
+    x = x.to(dev)
     if x.numel():
         cats = torch.as_tensor(np.asarray(compiled.var_categories), device=dev)
         if bool((x < -1).any()):
@@ -133,29 +126,38 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
 
     Every step is one ``pcb_train_step`` (``runtime.step.TrainStep``): lean
     launches, EM inside the backward pass where exact (one process), each
-    batch size's step captured once as a CUDA graph and replayed.  The data
-    stay on the device; the epoch log-likelihood and the EM status counters
-    accumulate there, and the host synchronises once per epoch.  If an epoch
-    reports a dead EM step or non-finite parameters, it is re-run from its
-    starting table eagerly with a check after every step, so the
+    batch size's step captured once as a CUDA graph and replayed (steps are
+    cached on the device plan, so later calls reuse them).  Host data stream
+    to the device behind the compute (``runtime.loader.HostBatches``: rows
+    gathered in epoch order, validated per batch); device data are gathered
+    in place.  The epoch log-likelihood and the EM status counters
+    accumulate on the device; the host synchronises once per epoch.  If an
+    epoch reports a dead EM step or non-finite parameters, it is re-run from
+    its starting table eagerly with a check after every step, so the
     ``NumericError`` is raised at the failing step with the parameters of the
     step before it, as the reference does (``em.py:70-75``).
     """
     import torch
+    from .errors import FormatError
     from .runtime.em import em_update_, propagate_theta
+    from .runtime.loader import DeviceBatches, HostBatches
     from .runtime.plan import device_plan
     from .runtime.step import TrainStep
 
     cfg = cfg or TrainConfig()
     plan = device_plan(compiled, device, tensor_cores=tensor_cores)
     dev = plan.device
-    if not isinstance(data, torch.Tensor):
+    on_device = isinstance(data, torch.Tensor)
+    if not on_device:
         data = np.asarray(data)
+        if data.dtype.kind not in "iu":
+            data = data.astype(np.int64)
     n = int(data.shape[0]) if data.ndim == 2 else 0
     if n == 0:
         raise UsageError("training data is empty")
-    with torch.cuda.device(dev):
-        data_dev = _device_data(compiled, data, dev)
+    if data.shape[1] != compiled.num_vars:
+        raise FormatError(f"batch must have shape (n, {compiled.num_vars}), got "
+                          f"{tuple(data.shape)}")
     result = TrainResult()
     batch_size = cfg.batch_size
     if batch_size > n:
@@ -175,43 +177,61 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
         use_graph = graph and dist.get_backend(group) == "nccl"
     ar = (lambda fp, ll: allreduce_accumulators(fp, ll, theta_size, group)) if world > 1 \
         else None
-    steps: dict = {}
+    # this rank's row span of every batch (the reference's _chunk_ranges split)
+    spans = []
+    for a in range(0, n, batch_size):
+        lo, hi = shard_span(min(n, a + batch_size) - a, rank, world)
+        spans.append((a + lo, a + hi))
+    cache = plan.__dict__.setdefault("_train_steps", {})
     with torch.cuda.device(dev):
-        ep_fp = torch.zeros(max(theta_size, 1), dtype=torch.float32, device=dev) if full \
-            else None
+        data_dev = _device_data(compiled, data, dev) if on_device else None
+        acc_key = ("acc", world > 1, id(group))
+        ep_fp = None
+        if full:
+            ep_fp = cache.get(acc_key)
+            if ep_fp is None:
+                ep_fp = cache[acc_key] = torch.zeros(max(theta_size, 1), dtype=torch.float32,
+                                                     device=dev)
 
-        def step_for(B):
-            ts = steps.get(B)
+        def step_for(B, graphed):
+            key = (B, float(cfg.pseudocount), float(cfg.step_size), full,
+                   graphed and B > 0, world > 1, id(group))
+            ts = cache.get(key)
             if ts is None:
-                ts = steps[B] = TrainStep(
+                ts = cache[key] = TrainStep(
                     compiled, B, pseudocount=cfg.pseudocount, step_size=cfg.step_size,
-                    device=dev, graph=use_graph and B > 0, tensor_cores=tensor_cores,
+                    device=dev, graph=graphed and B > 0, tensor_cores=tensor_cores,
                     allreduce=None if full else ar, accumulate=ep_fp)
             return ts
 
-        def run_epoch(order_dev, eager_checks: bool, prev=None):
+        def run_epoch(order, graphed: bool, prev=None):
+            """prev: eager re-run with a check after every step (the table
+            before each step is kept in prev)."""
+            if on_device:
+                src = DeviceBatches(data_dev, torch.from_numpy(order).to(dev), spans)
+            else:
+                src = HostBatches(data, order, spans, compiled.var_categories, dev)
             ep_ll = torch.zeros((), dtype=torch.float64, device=dev)
             dead = torch.zeros((), dtype=torch.int32, device=dev)
             bad = torch.zeros((), dtype=torch.int32, device=dev)
             if full:
                 ep_fp.zero_()
-            for a in range(0, n, batch_size):
-                b_all = min(n, a + batch_size) - a
-                lo, hi = shard_span(b_all, rank, world)
-                ts = step_for(hi - lo)
-                if hi > lo:
-                    torch.index_select(data_dev, 0, order_dev[a + lo:a + hi], out=ts.x)
-                if prev is not None and not full:
-                    prev.copy_(plan.theta)
-                ll = ts.run(ts.x)
-                ep_ll += ll
-                if full:
-                    continue
-                if n_groups:
-                    dead += (plan.status[0] == 0).int()
-                bad += plan.status[1]
-                if eager_checks and (int(dead.item()) or int(bad.item())):
-                    return ep_ll, dead, bad, True
+            try:
+                for i, (a, b) in enumerate(spans):
+                    ts = step_for(b - a, graphed)
+                    src.fill(i, ts.x)
+                    if prev is not None and not full:
+                        prev.copy_(plan.theta)
+                    ep_ll += ts.run(ts.x)
+                    if full:
+                        continue
+                    if n_groups:
+                        dead += (plan.status[0] == 0).int()
+                    bad += plan.status[1]
+                    if prev is not None and (int(dead.item()) or int(bad.item())):
+                        return ep_ll, dead, bad, True
+            finally:
+                src.close()
             if full:
                 allreduce_accumulators(ep_fp, ep_ll, theta_size, group)
                 em_update_(compiled, ep_fp, pseudocount=cfg.pseudocount, step_size=1.0,
@@ -221,22 +241,27 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
                 bad += plan.status[1]
             return ep_ll, dead, bad, False
 
+        snapshot = None
         for _ in range(cfg.epochs):
             t0 = time.perf_counter()
             order = shuffle_rng.permutation(n) if cfg.mode == "mini" else np.arange(n)
-            order_dev = torch.from_numpy(order).to(dev)
-            snapshot = plan.theta.clone()
-            ep_ll, dead, bad, _ = run_epoch(order_dev, eager_checks=False)
+            if snapshot is None:
+                snapshot = plan.theta.clone()
+            else:
+                snapshot.copy_(plan.theta)
+            try:
+                ep_ll, dead, bad, _ = run_epoch(order, use_graph)
+            except FormatError:
+                propagate_theta(compiled, plan)
+                raise
             if int(dead.item()) or int(bad.item()):
                 # re-run the epoch from its starting table with per-step
                 # checks: raise at the failing step, parameters of the step
                 # before it (the failing step's update is rolled back)
                 plan.theta.copy_(snapshot)
                 plan.refresh_mma()
-                for ts in steps.values():
-                    ts.graph = None
                 prev = torch.empty_like(plan.theta)
-                ep_ll, dead, bad, stopped = run_epoch(order_dev, eager_checks=True, prev=prev)
+                ep_ll, dead, bad, stopped = run_epoch(order, False, prev=prev)
                 if stopped and not full:
                     plan.theta.copy_(prev)
                     plan.refresh_mma()
