@@ -244,10 +244,10 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------- CPU oracle
-def cpu_step_parts(c, w, B_cpu, seed=7):
+def cpu_step_parts(c, w, B_cpu, seed=7, em=True):
     """Oracle (float64 numpy port of the reference) on B_cpu samples: seconds
     of forward + backward, and of the EM pass (em_step_full + em_step_mini
-    over the whole table, independent of the batch size)."""
+    over the whole table, independent of the batch size; 0 when em=False)."""
     import oracle
     x = synthetic_batches(c, w, B_cpu, 1, seed)[0].astype(np.int64)
     theta = c.theta.copy()
@@ -255,6 +255,8 @@ def cpu_step_parts(c, w, B_cpu, seed=7):
     _, bufs = oracle.forward(c, x, theta=theta)
     oracle.backward(c, bufs, theta=theta)
     t1 = time.perf_counter()
+    if not em:
+        return t1 - t0, 0.0
     new = oracle.em_step_full(c, bufs.f_params, theta=theta, pseudocount=PSEUDOCOUNT)
     if new is not None:
         theta = oracle.em_step_mini(theta, new, STEP_SIZE)
@@ -285,16 +287,17 @@ def run_reference(args, w):
     if rank != 0:
         return
     c = build_circuit(w)
-    # a quarter of the baseline sample per step keeps K + W steps within minutes
-    Bc = max(1, cpu_sample_size(w) // 4)
-    for _ in range(args.warmup):
-        cpu_step_parts(c, w, Bc)
-    fb = em = 0.0
-    for _ in range(args.steps):
-        a, b = cpu_step_parts(c, w, Bc)
-        fb += a
-        em += b
-    v, t, formula = composed(w, Bc, fb / args.steps, em / args.steps)
+    # per step: forward + backward on a bounded sample (a sixteenth of the
+    # baseline sample keeps K + W steps within minutes); the batch-independent
+    # EM pass over the whole table is timed once after the steps
+    Bc = max(1, cpu_sample_size(w) // 16)
+    for i in range(args.warmup):
+        cpu_step_parts(c, w, Bc, seed=100 + i, em=False)
+    fb = 0.0
+    for i in range(args.steps):
+        fb += cpu_step_parts(c, w, Bc, seed=i, em=False)[0]
+    em = cpu_step_parts(c, w, Bc, seed=99)[1]
+    v, t, formula = composed(w, Bc, fb / args.steps, em)
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": "samples/sec fwd+bwd+EM", "value": v,
@@ -319,7 +322,7 @@ def run_ours(args, w):
     import torch.distributed as dist
     from paper_2406_00766_b200.runtime import _lib
     from paper_2406_00766_b200.runtime.step import TrainStep
-    from paper_2406_00766_b200.train import allreduce_accumulators
+    from paper_2406_00766_b200.train import shard_span
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -339,20 +342,27 @@ def run_ours(args, w):
     c = build_circuit(w)
     log(f"[bench] compiled {args.workload}: {c.num_edges} edges, theta {c.theta_size} "
         f"in {time.time() - t0:.1f}s")
-    B = w["batch"]
+    # strong scaling (north_star: the config's mini-batch is sharded across
+    # the GPUs): global batch = the config's, this rank's contiguous span of
+    # it (the reference's _chunk_ranges split); --scaling weak keeps the
+    # per-GPU batch fixed instead
+    G = w["batch"] * (world if args.scaling == "weak" else 1)
+    lo, hi = shard_span(G, rank, world)
+    B = hi - lo
     n_pool = 4
     host_batches = synthetic_batches(c, w, B, n_pool, seed=rank)
     dev_batches = [torch.from_numpy(h).to(dev) for h in host_batches]
-    theta_size = c.theta_size
     ll_acc = torch.zeros((), dtype=torch.float64, device=dev)
-    # the training step as a CUDA graph on one GPU (the batch is copied into a
-    # static input buffer, every kernel replays without host launches); eager
-    # launches with the NCCL all-reduce on N > 1
-    graphed = world == 1 and not args.no_graph
+
+    def reduce_(t):
+        dist.all_reduce(t)
+
+    # the training step as a CUDA graph (the batch is copied into a static
+    # input buffer, every kernel replays without host launches); on N > 1 the
+    # bucketed NCCL all-reduce of the parameter flows is captured with it
+    graphed = not args.no_graph and (world == 1 or backend == "nccl")
     ts = TrainStep(c, B, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, device=dev,
-                   graph=graphed,
-                   allreduce=None if world == 1 else
-                   (lambda fp, ll: allreduce_accumulators(fp, ll, theta_size)))
+                   graph=graphed, allreduce=None if world == 1 else reduce_)
     plan = ts.plan
     run = ts.run
 
@@ -385,7 +395,7 @@ def run_ours(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * B * args.steps / (ms / 1000.0)
+    value = G * args.steps / (ms / 1000.0)
 
     # ---- profiled pass: live per-kernel-class CUDA-event times
     prof_steps = max(1, min(3, args.steps))
@@ -405,19 +415,31 @@ def run_ours(args, w):
     from paper_2406_00766_b200.train import TrainConfig, train
     n_ep = EPOCH
     data = synthetic_batches(c, w, n_ep, 1, seed=11)[0]  # identical on every rank
-    tcfg = dict(batch_size=world * B, mode="mini", step_size=STEP_SIZE, pseudocount=PSEUDOCOUNT,
-                seed=0)
-    tail = n_ep % (world * B)
-    warm = data[: 2 * world * B + tail]  # builds the full-batch and tail steps (cached)
-    train(c, warm, TrainConfig(epochs=1, **tcfg), device=dev)
-    barrier()
-    res = train(c, data, TrainConfig(epochs=1, **tcfg), device=dev)
-    ep_s = torch.tensor([res.epoch_seconds[0]], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ep_s, op=dist.ReduceOp.MAX)
-    ep_s = float(ep_s.item())
+
+    def epoch(mode, gb):
+        """One timed epoch through train() (after a short untimed call that
+        builds its steps: full batches and the tail)."""
+        tcfg = dict(batch_size=gb, mode=mode, step_size=STEP_SIZE, pseudocount=PSEUDOCOUNT,
+                    seed=0)
+        train(c, data[: 2 * gb + n_ep % gb], TrainConfig(epochs=1, **tcfg), device=dev,
+              graph=graphed)
+        barrier()
+        res = train(c, data, TrainConfig(epochs=1, **tcfg), device=dev, graph=graphed)
+        t = torch.tensor([res.epoch_seconds[0]], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), -(-n_ep // gb)
+
+    ep_s, n_steps_ep = epoch("mini", G)
     e2e_value = n_ep / ep_s
-    n_steps_ep = -(-n_ep // (world * B))
+    # full-batch EM (train.py:130-146, the reference's default mode): one
+    # all-reduce and EM pass per epoch, so each GPU runs a full config batch
+    # per step at any N
+    fb_s, fb_steps = epoch("full", w["batch"] * world)
+    full_batch = {"value": n_ep / fb_s, "unit": "samples/s", "sec_per_epoch": fb_s,
+                  "steps": fb_steps, "batch_per_gpu": w["batch"], "global_batch":
+                  w["batch"] * world, "how": "one 60k-sample epoch through train(mode='full')"
+                                             " from host data, one EM per epoch"}
 
     if rank != 0:
         if world > 1:
@@ -500,10 +522,10 @@ def run_ours(args, w):
     line = {
         "metric": "samples/sec fwd+bwd+EM", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": args.workload, "desc": w["desc"], "batch_per_gpu": B,
-                   "global_batch": world * B, "block_size": w["block"],
+                   "global_batch": G, "block_size": w["block"],
                    "em": f"mini-batch, step {STEP_SIZE}, pseudocount {PSEUDOCOUNT}",
                    "edges": c.num_edges, "theta_size": c.theta_size,
                    "sec_per_epoch": ep_s,
@@ -514,7 +536,7 @@ def run_ours(args, w):
                    "parallelism": f"dp{world}", "cuda_graph": graphed,
                    "em_in_backward": inline_em},
         "e2e": {"value": e2e_value, "unit": "samples/s",
-                "h2d_bytes_per_step": world * B * c.num_vars * 4 // world,
+                "h2d_bytes_per_step": B * c.num_vars * 4,
                 "d2h_bytes_per_step": 8,
                 "how": f"train(): {n_ep}-sample epoch, host numpy int32 dataset, shuffle + "
                        "per-batch gather / validation on a loader thread, pinned H2D copies "
@@ -524,6 +546,7 @@ def run_ours(args, w):
         "kernels": breakdown,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
+        "full_batch_em": full_batch,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -539,6 +562,9 @@ def main():
     ap.add_argument("--workload", default="hclt256", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's batch sharded over the GPUs (north_star); "
+                         "weak: the config's batch per GPU")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -148,6 +148,14 @@ int pcb_layer_backward(const pcb_plan* plan, int layer, void* stream, int B, int
 int pcb_exec_create(const pcb_plan* plan, pcb_exec** out);
 int pcb_exec_destroy(pcb_exec* exec);
 
+/* Optional data-parallel overlap: n caller-owned cudaEvent_t handles.  A
+ * step's backward pass records events[l] once sum layer l's parameter flows
+ * are issued (on the stream that ran them) and events[num_layers] after the
+ * input flows, so the caller can start the all-reduce of each finished
+ * f_params range on another stream while the rest of the backward pass runs
+ * (the reference's fixed-order merge, pcirc/train.py:100-101, bucketed). */
+int pcb_exec_set_flow_events(pcb_exec* exec, void* const* events, int n);
+
 /* One training step on a batch: forward + backward (+ EM with PCB_STEP_EM),
  * the reference's _accumulate_batch + em_step_full + em_step_mini +
  * apply_theta (pcirc/train.py:84-101, :133-142) in one call.

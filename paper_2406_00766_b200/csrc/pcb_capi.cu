@@ -292,6 +292,13 @@ int pcb_exec_create(const pcb_plan* plan, pcb_exec** out) {
   return PCB_OK;
 }
 
+int pcb_exec_set_flow_events(pcb_exec* exec, void* const* events, int n) {
+  if (!exec || n < 0 || (n && !events)) return PCB_USAGE;
+  exec->flows_done.assign(n, nullptr);
+  for (int i = 0; i < n; ++i) exec->flows_done[i] = reinterpret_cast<cudaEvent_t>(events[i]);
+  return PCB_OK;
+}
+
 int pcb_exec_destroy(pcb_exec* exec) {
   delete exec;
   return PCB_OK;
@@ -510,6 +517,9 @@ int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B,
                                   vbase, f_params);
     if (st) return st;
   }
+  if (S.ex && li < S.ex->flows_done.size() && S.ex->flows_done[li] &&
+      cudaEventRecord(S.ex->flows_done[li], sp) != cudaSuccess)
+    return PCB_CUDA;
   if (em_fuse) {
     (*S.em_done)[li] = 1;
   } else {
@@ -579,6 +589,10 @@ int run_backward(const pcb_plan* P, Step& S, cudaStream_t s, int B, int ldb,
                                 S.lean != 0, (S.em && P->in_inline_ok) ? &S : nullptr, &done);
   if (st) return st;
   S.inputs_done = done;
+  const size_t nl = P->layers.size();
+  if (S.ex && nl < S.ex->flows_done.size() && S.ex->flows_done[nl] &&
+      cudaEventRecord(S.ex->flows_done[nl], s) != cudaSuccess)
+    return PCB_CUDA;
   if (side && (cudaEventRecord(S.ex->join, S.ex->side) != cudaSuccess ||
                cudaStreamWaitEvent(s, S.ex->join, 0) != cudaSuccess))
     return PCB_CUDA;

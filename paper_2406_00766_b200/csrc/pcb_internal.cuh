@@ -211,6 +211,11 @@ struct pcb_exec {
   ~pcb_exec();
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // optional, caller-owned: recorded when each layer's parameter flows are
+  // issued (index = layer) and after the input flows (index = num layers), so
+  // a data-parallel caller can all-reduce finished f_params ranges while the
+  // rest of the backward pass runs
+  std::vector<cudaEvent_t> flows_done;
 };
 
 namespace pcb {

@@ -31,6 +31,7 @@ SIGNATURES = {
     "pcb_plan_set_theta": (_I, [_P, _P]),
     "pcb_exec_create": (_I, [_P, C.POINTER(_P)]),
     "pcb_exec_destroy": (_I, [_P]),
+    "pcb_exec_set_flow_events": (_I, [_P, _P, _I]),
     "pcb_train_step": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _F,
                             _F, _P]),
     "pcb_tc_selftest_mn": (_I, [_P, _I, _I, _I, _P, _P, _P]),

@@ -979,7 +979,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             "pre_ratio_layers": int(sum(pre_ratio)), "em_fused_layers": int(sum(em_fusable)),
             "em_fused_layer_ids": [li for li, f in enumerate(em_fusable) if f], "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
-            "mma_elems": mma_elems, "scratch_rows": scratch_total, "slot_vb": slot_vb}
+            "mma_elems": mma_elems, "scratch_rows": scratch_total, "slot_vb": slot_vb,
+            "layer_flow_ranges": [tuple(int(v) for v in r) for r in layer_range]}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
 
 

@@ -14,9 +14,16 @@ parameters, caller-owned buffers, per-step state in the call's arguments
 and this step's ``pcb_exec``), so replay and eager launches run the same
 kernels on the same data.
 
-Data parallel (``allreduce`` given): the step runs forward + lean backward
-only, the caller's all-reduce sums ``f_params[:theta_size]`` and the
-log-likelihood, then ``pcb_em_update`` applies the (replicated) EM kernel.
+Data parallel (``allreduce`` given: a callable summing a device tensor in
+place over the ranks, e.g. an NCCL ``all_reduce``): the step runs forward +
+lean backward only, ``f_params[:theta_size]`` and the log-likelihood are
+summed, then ``pcb_em_update`` applies the (replicated) EM kernel.  The sum
+is bucketed by layer: the backward pass records an event as each sum
+layer's parameter flows are issued (``pcb_exec_set_flow_events``), and the
+all-reduce of that layer's f_params range starts on a communication stream
+at that event, overlapping the lower layers' backward; the input pmfs and
+the zero tile follow the input flows.  (Bucketing needs the plan's disjoint
+per-layer flow ranges, ``fp_cover``; otherwise one all-reduce at the end.)
 Full-batch EM (``accumulate`` given): forward + lean backward, the step's
 parameter flows added into the epoch accumulator (no EM).
 """
@@ -55,7 +62,10 @@ class TrainStep:
         h = C.c_void_p()
         with torch.cuda.device(self.dev):
             _lib.call("pcb_exec_create", self.plan.handle, C.byref(h))
-        self._exec = h
+            self._exec = h
+            self._buckets = None
+            if allreduce is not None and accumulate is None:
+                self._setup_buckets()
         self.serial = False  # True: no side-stream overlap (per-kernel-class profiling)
         self.graph = None
         self.ll = None
@@ -70,6 +80,44 @@ class TrainStep:
                 _lib.load().pcb_exec_destroy(h)
             except Exception:
                 pass
+
+    def _setup_buckets(self):
+        """Per-layer f_params ranges reduced as each layer finishes, then the
+        rest of [0, theta_size) (input pmfs, zero tile) after the input flows."""
+        import torch
+        info = self.plan.info
+        nl = len(self.c.layers)
+        theta = self.c.theta_size
+        ranges = info["layer_flow_ranges"] if info.get("fp_cover") else [(0, 0)] * nl
+        covered = sorted((lo, hi) for lo, hi in ranges if hi > lo)
+        rest, pos = [], 0
+        for lo, hi in covered:
+            if lo > pos:
+                rest.append((pos, lo))
+            pos = max(pos, hi)
+        if pos < theta:
+            rest.append((pos, theta))
+        self._events = [torch.cuda.Event() for _ in range(nl + 1)]
+        for e in self._events:  # materialise the CUDA events
+            e.record()
+        handles = (C.c_void_p * (nl + 1))(*[e.cuda_event for e in self._events])
+        _lib.call("pcb_exec_set_flow_events", self._exec, handles, nl + 1)
+        self._buckets = ([(li, lo, hi) for li, (lo, hi) in enumerate(ranges) if hi > lo][::-1]
+                         + [(nl, lo, hi) for lo, hi in rest])
+        self._comm = torch.cuda.Stream(self.dev)
+
+    def _reduce(self, ll):
+        """Bucketed all-reduce of f_params[:theta_size] and the step LL."""
+        import torch
+        b = self.bufs
+        comp = torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(self._comm):
+            for li, lo, hi in self._buckets:
+                self._comm.wait_event(self._events[li])
+                self.allreduce(b.f_params[lo:hi])
+            self._comm.wait_stream(comp)  # the LL sum is formed on the compute stream
+            self.allreduce(ll)
+        comp.wait_stream(self._comm)
 
     def _flags(self, em: bool) -> int:
         f = _lib.STEP_LEAN | (_lib.STEP_SERIAL if self.serial else 0)
@@ -92,7 +140,7 @@ class TrainStep:
             _lib.call("pcb_axpy_accumulate", s, self.c.theta_size, b.f_params.data_ptr(),
                       self.accumulate.data_ptr())
         elif not one:
-            self.allreduce(b.f_params, ll)
+            self._reduce(ll)
             em_update_(self.c, b.f_params, pseudocount=self.pseudocount,
                        step_size=self.step_size, check=False, plan=p)
         return ll

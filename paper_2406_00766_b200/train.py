@@ -175,8 +175,13 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
     if world > 1:
         import torch.distributed as dist
         use_graph = graph and dist.get_backend(group) == "nccl"
-    ar = (lambda fp, ll: allreduce_accumulators(fp, ll, theta_size, group)) if world > 1 \
-        else None
+    if world > 1:
+        import torch.distributed as dist
+
+        def ar(t):  # in-place sum over the data-parallel group
+            dist.all_reduce(t, group=group)
+    else:
+        ar = None
     # this rank's row span of every batch (the reference's _chunk_ranges split)
     spans = []
     for a in range(0, n, batch_size):
