@@ -53,6 +53,18 @@ WORKLOADS = {
                    batch=512, desc="HCLT latent=64, 3072 vars, 256 cats (dev proxy)"),
     "hmm4096": dict(kind="hmm", seq_len=32, hidden_dim=4096, vocab_size=50257, block=32,
                     batch=256, desc="HMM hidden=4096, vocab 50257, seq len 32"),
+    # PyJuice PD (elementwise products per cut) on ImageNet32 (32 x 32 x 3):
+    # cuts every 8 pixels, halving below; 213 M sum edges
+    "pd256": dict(kind="pd", shape=(32, 32, 3), split_interval=8, hidden_dim=256,
+                  num_categories=256, elementwise=True, block=32, batch=512,
+                  desc="PD (PyJuice, elementwise cuts every 8 px) latent=256, 32x32x3, "
+                       "256 cats"),
+    # RAT-SPN on MNIST (784 vars): depth 7, 32 repetitions, 32 sums per region,
+    # 32 factorised input components per leaf region; 137 M sum edges
+    "ratspn": dict(kind="ratspn", num_vars=784, depth=7, hidden_dim=32,
+                   num_input_components=32, num_repetitions=32, num_categories=256, block=32,
+                   batch=1024, desc="RAT-SPN depth 7, 32 repetitions, 32 sums / 32 inputs per "
+                                    "region, 784 vars, 256 cats"),
 }
 EPOCH = 60000
 STEP_SIZE = 0.01
@@ -85,12 +97,10 @@ def build_circuit(w):
 def _build_circuit(w):
     from paper_2406_00766_b200 import structures as S
     from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
-    if w["kind"] == "hclt":
-        cfg = S.StructureConfig(kind="hclt", num_vars=w["num_vars"], hidden_dim=w["hidden_dim"],
-                                num_categories=w["num_categories"], seed=0)
-    else:
-        cfg = S.StructureConfig(kind="hmm", seq_len=w["seq_len"], hidden_dim=w["hidden_dim"],
-                                vocab_size=w["vocab_size"], seed=0, tied=True)
+    keys = ("kind", "num_vars", "hidden_dim", "num_categories", "seq_len", "vocab_size",
+            "shape", "split_interval", "elementwise", "depth", "num_input_components",
+            "num_repetitions")
+    cfg = S.StructureConfig(seed=0, tied=True, **{k: w[k] for k in keys if k in w})
     g = S.build_structure(cfg)
     c = compile_circuit(g, CompileConfig(block_size=w["block"]), validate=False)
     return c

@@ -142,3 +142,61 @@ def test_hmm2048_vocab4096_big_groups():
     x = np.random.default_rng(6).integers(0, 4096, size=(96, 4))
     x[::7, 2] = -1
     _api_vs_oracle(c, x, step=1.0)
+
+
+def test_pd_elementwise_block32():
+    """configs[3] family: the PyJuice PD (elementwise products per cut,
+    dense h x (cuts h) sum blocks on tensor cores) at h = 64 on a 6 x 6 x 3
+    image with cuts every 2 pixels, through the API and the training step."""
+    import torch
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.runtime.em import apply_theta
+    from paper_2406_00766_b200.runtime.step import TrainStep
+    cfg = S.StructureConfig(kind="pd", shape=(6, 6, 3), split_interval=2, hidden_dim=64,
+                            num_categories=16, elementwise=True, seed=3)
+    g = S.build_pd(cfg)
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    assert c.num_edges == S.pd_edge_count((6, 6, 3), 64, 2)
+    assert max(L.k_m for L in c.layers) == 32
+    x = np.random.default_rng(8).integers(0, 16, size=(192, 108))
+    x[np.random.default_rng(9).random(x.shape) < 0.05] = -1
+    _api_vs_oracle(c, x, values=True, step=1.0)
+    theta0 = c.theta.copy()
+    ts = TrainStep(c, 192, pseudocount=1e-6, step_size=1.0, graph=True)
+    ts.run(torch.from_numpy(x.astype(np.int32)).cuda())
+    got = _np(ts.plan.theta)
+    apply_theta(c, theta0)
+    lr, rb = oracle.forward(c, x, theta=theta0)
+    oracle.backward(c, rb, theta=theta0)
+    want = oracle.em_step_full(c, rb.f_params, theta=theta0, pseudocount=1e-6)
+    assert rel_err(got, want) < RTOL
+
+
+def test_ratspn_depth7_repetitions():
+    """configs[4] family: RAT-SPN of depth 7 with repetitions (32 sums per
+    region: dense 32 x 1024 cross-product blocks, split-K contractions) over
+    140 variables at batch 256, through the API and the training step."""
+    import torch
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.runtime.em import apply_theta
+    from paper_2406_00766_b200.runtime.step import TrainStep
+    cfg = S.StructureConfig(kind="ratspn", num_vars=140, depth=7, hidden_dim=32,
+                            num_input_components=8, num_categories=16, num_repetitions=2,
+                            seed=4)
+    g = S.build_ratspn(cfg)
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    assert c.num_edges == S.ratspn_edge_count(140, 7, 32, 8, 2)
+    x = np.random.default_rng(10).integers(0, 16, size=(256, 140))
+    x[np.random.default_rng(11).random(x.shape) < 0.05] = -1
+    _api_vs_oracle(c, x, step=1.0)
+    theta0 = c.theta.copy()
+    ts = TrainStep(c, 256, pseudocount=1e-6, step_size=1.0, graph=True)
+    ts.run(torch.from_numpy(x.astype(np.int32)).cuda())
+    got = _np(ts.plan.theta)
+    apply_theta(c, theta0)
+    lr, rb = oracle.forward(c, x, theta=theta0)
+    oracle.backward(c, rb, theta=theta0)
+    want = oracle.em_step_full(c, rb.f_params, theta=theta0, pseudocount=1e-6)
+    assert rel_err(got, want) < RTOL
