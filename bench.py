@@ -331,8 +331,7 @@ def run_ours(args, w):
     import torch
     import torch.distributed as dist
     from paper_2406_00766_b200.runtime import _lib
-    from paper_2406_00766_b200.runtime.step import TrainStep
-    from paper_2406_00766_b200.train import shard_span
+    from paper_2406_00766_b200.train import cached_step, shard_span
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -364,15 +363,13 @@ def run_ours(args, w):
     dev_batches = [torch.from_numpy(h).to(dev) for h in host_batches]
     ll_acc = torch.zeros((), dtype=torch.float64, device=dev)
 
-    def reduce_(t):
-        dist.all_reduce(t)
-
     # the training step as a CUDA graph (the batch is copied into a static
     # input buffer, every kernel replays without host launches); on N > 1 the
-    # bucketed NCCL all-reduce of the parameter flows is captured with it
+    # bucketed NCCL all-reduce of the parameter flows is captured with it.
+    # The same cached step (buffers, graph) serves train() below.
     graphed = not args.no_graph and (world == 1 or backend == "nccl")
-    ts = TrainStep(c, B, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, device=dev,
-                   graph=graphed, allreduce=None if world == 1 else reduce_)
+    ts = cached_step(c, B, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, device=dev,
+                     graph=graphed)
     plan = ts.plan
     run = ts.run
 

@@ -75,8 +75,11 @@ class EvalBuffers:
         return self.prod_flows_full[:, : self.batch_size]
 
 
-def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None) -> EvalBuffers:
-    """Zeroed device workspace for ``batch_size`` samples."""
+def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None,
+                     prod_flows: bool = True) -> EvalBuffers:
+    """Zeroed device workspace for ``batch_size`` samples.  ``prod_flows=False``
+    (training steps on plans whose product rows are each accumulated and
+    pushed in one layer) leaves the product-flow table out: nothing reads it."""
     import torch
     from . import _lib
     from .plan import device_plan
@@ -98,7 +101,7 @@ def allocate_buffers(compiled, batch_size: int, device=None, *, plan=None) -> Ev
         scratch_full=z(plan.info["scratch_rows"]),  # every layer's window stays resident
         flows_full=z(compiled.num_value_slots),
         flow_scratch_full=z(compiled.scratch_size),
-        prod_flows_full=z(compiled.num_prod_rows),
+        prod_flows_full=z(compiled.num_prod_rows) if prod_flows else z(0),
         f_params=torch.zeros(max(compiled.f_params_size, 1), dtype=torch.float32, device=dev),
         lroot=torch.zeros(max(b, 1), dtype=torch.float32, device=dev)[:b],
         work=torch.zeros(max(n_work, 1), dtype=torch.float32, device=dev),

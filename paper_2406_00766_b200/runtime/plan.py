@@ -344,7 +344,8 @@ def push_ratio_tables(compiled, push_tabs):
         slots = np.asarray(L.prod_slots, dtype=np.int64)
         k = int(L.k_n)
         n = slots.size
-        ok = n > 0 and n % k == 0 and bool(np.all(flags == 3)) and \
+        # the fused kernel exists for product blocks of 16 / 32 / 64
+        ok = n > 0 and k in (16, 32, 64) and n % k == 0 and bool(np.all(flags == 3)) and \
             bool(np.all(pch & 1)) if n else False
         blocks = []
         if ok:

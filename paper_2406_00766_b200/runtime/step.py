@@ -52,13 +52,14 @@ class TrainStep:
         self.step_size = float(step_size)
         self.plan = device_plan(compiled, device, tensor_cores=tensor_cores)
         self.dev = self.plan.device
-        self.bufs = allocate_buffers(compiled, self.B, self.dev, plan=self.plan)
+        # the step never reads prod_flows: skip it when the layout allows
+        optional = bool(self.plan.info.get("prod_flows_optional"))
+        self.bufs = allocate_buffers(compiled, self.B, self.dev, plan=self.plan,
+                                     prod_flows=not optional)
         self.x = torch.zeros((self.B, compiled.num_vars), dtype=torch.int32, device=self.dev)
         self.allreduce = allreduce
         self.accumulate = accumulate
-        # the step never reads prod_flows: skip writing it when the layout allows
-        self._pf_ptr = (0 if self.plan.info.get("prod_flows_optional")
-                        else self.bufs.prod_flows_full.data_ptr())
+        self._pf_ptr = 0 if optional else self.bufs.prod_flows_full.data_ptr()
         h = C.c_void_p()
         with torch.cuda.device(self.dev):
             _lib.call("pcb_exec_create", self.plan.handle, C.byref(h))

@@ -120,6 +120,42 @@ def _device_data(compiled, data, dev):
     return x.to(torch.int32).contiguous()
 
 
+def cached_step(compiled, B: int, *, pseudocount: float, step_size: float, device=None,
+                graph: bool = True, tensor_cores: bool = True, group=None, full: bool = False):
+    """The training step of batch size B for these settings, built once per
+    device plan and reused by every later ``train()`` call (its buffers and
+    CUDA graph included).  Data parallel when torch.distributed is
+    initialised; ``full``: flows accumulated for full-batch EM."""
+    import torch
+    from .runtime.plan import device_plan
+    from .runtime.step import TrainStep
+    plan = device_plan(compiled, device, tensor_cores=tensor_cores)
+    cache = plan.__dict__.setdefault("_train_steps", {})
+    world = _dp()[1]
+    graph = graph and B > 0
+    key = (B, float(pseudocount), float(step_size), full, graph, world > 1, id(group))
+    ts = cache.get(key)
+    if ts is not None:
+        return ts
+    ar = None
+    if world > 1:
+        import torch.distributed as dist
+
+        def ar(t):  # in-place sum over the data-parallel group
+            dist.all_reduce(t, group=group)
+    acc = None
+    if full:
+        acc_key = ("acc", world > 1, id(group))
+        acc = cache.get(acc_key)
+        if acc is None:
+            acc = cache[acc_key] = torch.zeros(max(compiled.theta_size, 1),
+                                               dtype=torch.float32, device=plan.device)
+    ts = cache[key] = TrainStep(compiled, B, pseudocount=pseudocount, step_size=step_size,
+                                device=plan.device, graph=graph, tensor_cores=tensor_cores,
+                                allreduce=None if full else ar, accumulate=acc)
+    return ts
+
+
 def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
           tensor_cores: bool = True, group=None, graph: bool = True) -> TrainResult:
     """Run EM; ``compiled.theta`` holds the trained table on return (``train.py:104-154``).
@@ -142,8 +178,6 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
     from .runtime.em import em_update_, propagate_theta
     from .runtime.loader import DeviceBatches, HostBatches
     from .runtime.plan import device_plan
-    from .runtime.step import TrainStep
-
     cfg = cfg or TrainConfig()
     plan = device_plan(compiled, device, tensor_cores=tensor_cores)
     dev = plan.device
@@ -175,39 +209,21 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
     if world > 1:
         import torch.distributed as dist
         use_graph = graph and dist.get_backend(group) == "nccl"
-    if world > 1:
-        import torch.distributed as dist
-
-        def ar(t):  # in-place sum over the data-parallel group
-            dist.all_reduce(t, group=group)
-    else:
-        ar = None
     # this rank's row span of every batch (the reference's _chunk_ranges split)
     spans = []
     for a in range(0, n, batch_size):
         lo, hi = shard_span(min(n, a + batch_size) - a, rank, world)
         spans.append((a + lo, a + hi))
-    cache = plan.__dict__.setdefault("_train_steps", {})
     with torch.cuda.device(dev):
         data_dev = _device_data(compiled, data, dev) if on_device else None
-        acc_key = ("acc", world > 1, id(group))
-        ep_fp = None
-        if full:
-            ep_fp = cache.get(acc_key)
-            if ep_fp is None:
-                ep_fp = cache[acc_key] = torch.zeros(max(theta_size, 1), dtype=torch.float32,
-                                                     device=dev)
 
         def step_for(B, graphed):
-            key = (B, float(cfg.pseudocount), float(cfg.step_size), full,
-                   graphed and B > 0, world > 1, id(group))
-            ts = cache.get(key)
-            if ts is None:
-                ts = cache[key] = TrainStep(
-                    compiled, B, pseudocount=cfg.pseudocount, step_size=cfg.step_size,
-                    device=dev, graph=graphed and B > 0, tensor_cores=tensor_cores,
-                    allreduce=None if full else ar, accumulate=ep_fp)
-            return ts
+            return cached_step(compiled, B, pseudocount=cfg.pseudocount,
+                               step_size=cfg.step_size, device=dev, graph=graphed,
+                               tensor_cores=tensor_cores, group=group, full=full)
+
+        def acc():  # the full-batch accumulator shared by the cached steps
+            return step_for(spans[0][1] - spans[0][0], use_graph).accumulate
 
         def run_epoch(order, graphed: bool, prev=None):
             """prev: eager re-run with a check after every step (the table
@@ -220,7 +236,7 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
             dead = torch.zeros((), dtype=torch.int32, device=dev)
             bad = torch.zeros((), dtype=torch.int32, device=dev)
             if full:
-                ep_fp.zero_()
+                acc().zero_()
             try:
                 for i, (a, b) in enumerate(spans):
                     ts = step_for(b - a, graphed)
@@ -238,8 +254,8 @@ def train(compiled, data, cfg: TrainConfig | None = None, *, device=None,
             finally:
                 src.close()
             if full:
-                allreduce_accumulators(ep_fp, ep_ll, theta_size, group)
-                em_update_(compiled, ep_fp, pseudocount=cfg.pseudocount, step_size=1.0,
+                allreduce_accumulators(acc(), ep_ll, theta_size, group)
+                em_update_(compiled, acc(), pseudocount=cfg.pseudocount, step_size=1.0,
                            check=False, plan=plan)
                 if n_groups:
                     dead += (plan.status[0] == 0).int()
