@@ -41,7 +41,10 @@ namespace {
 
 constexpr int PF_M = 128;          // sums per tile
 constexpr int PF_N = 256;          // child columns per item
-constexpr int PF_KS = 32;          // samples per chunk (one 128-byte swizzled box row)
+#ifndef PCB_PF_KS
+#define PCB_PF_KS 32
+#endif
+constexpr int PF_KS = PCB_PF_KS;   // samples per chunk (one 128-byte swizzled box row)
 constexpr int PF_CH = PF_KS / 4;   // 16-byte chunks per box row
 constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
 #ifndef PCB_PF_NCONV
@@ -53,7 +56,7 @@ constexpr int PF_THREADS = (PF_EPI0 + 4) * 32;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
 
 struct PfArgs {
-  int cap, k_m, B, ldb;
+  int cap, k_m, lkm, B, ldb;  // lkm = log2(k_m)
   int store;  // 1: each flow entry has exactly one writer in the pass (plain stores)
   int n_items, mtiles, kslices, cgroups, nchunks;
   int64_t sb_base;
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       prefetch_tmap(&tm_r);
       prefetch_tmap(&tm_R);
       prefetch_tmap(&tm_e);
-      Ring rr(C::kRS);
+      Ring<C::kRS> rr;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         const PfItem it = pf_item(a, item);
         if (!pf_active(it)) continue;
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    Ring orr(C::kOS);
+    Ring<C::kOS> orr;
     int acc_u = 0;
     constexpr uint32_t SBO = (PF_KS / 8) * 128;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -296,7 +299,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   } else if (warp < PF_EPI0) {
     // ------------------------------------------------------------ converters
     const int t = tid - PF_CONV0 * 32;  // 0..PF_NCONV*32-1
-    Ring rr(C::kRS), orr(C::kOS);
+    Ring<C::kRS> rr;
+    Ring<C::kOS> orr;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const PfItem it = pf_item(a, item);
       if (!pf_active(it)) continue;
@@ -330,11 +334,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const float4* rR4 = reinterpret_cast<const float4*>(rR);
         const float4* c4 = reinterpret_cast<const float4*>(c_s);
         // A: 128 rows x 4 octets; thread -> (row = q % 128, octet = q / 128)
+#ifdef PCB_ABL_CONV
+        if (false)
+#endif
         for (int q = t; q < PF_M * (PF_KS / 8); q += PF_NCONV * 32) {
           const int m = q & (PF_M - 1), o = q >> 7;
           float v[8];
           if (m < it.rows) {
-            const int blk = m / a.k_m;
+            const int blk = m >> a.lkm;
             const float4 x0 = rA4[m * PF_CH + swz_chunk(m, 2 * o)];
             const float4 x1 = rA4[m * PF_CH + swz_chunk(m, 2 * o + 1)];
             const float4 R0 = rR4[blk * (C::kRP / 16) + 2 * o];
@@ -359,8 +366,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         // E: npad rows x 4 octets
         const float4* rB4 = reinterpret_cast<const float4*>(rB);
         const float4* rP4 = reinterpret_cast<const float4*>(rP);
-        for (int q = t; q < npad * (PF_KS / 8); q += PF_NCONV * 32) {
-          const int n = q % npad, o = q / npad;
+#ifdef PCB_ABL_CONV
+        if (false)
+#endif
+        for (int o = 0; o < PF_KS / 8; ++o)
+        for (int n = t; n < npad; n += PF_NCONV * 32) {
           const float4 x0 = rE4[n * PF_CH + swz_chunk(n, 2 * o)];
           const float4 x1 = rE4[n * PF_CH + swz_chunk(n, 2 * o + 1)];
           const float4 c0 = c4[2 * o], c1 = c4[2 * o + 1];
@@ -529,9 +539,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) th[i] = thn[i];
+#ifndef PCB_ABL_EPI
         if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
+#endif
         float v[16];
         tmem_ld16(tbase + c0, v);
+#ifdef PCB_ABL_EPI
+        if (v[0] != 12345.f) continue;
+#endif
         if (!live) continue;
         const int c = cols[c0 / KN];
         const int j0 = c0 % KN;
@@ -648,6 +663,7 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   PfArgs a{};
   a.cap = (int)g.cap;
   a.k_m = (int)L.k_m;
+  a.lkm = __builtin_ctz((unsigned)L.k_m);
   a.B = B;
   a.ldb = ldb;
   a.n_items = (int)tc.count;
@@ -679,8 +695,11 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
   switch (L.k_n) {
     case 16: return dense ? launch_pf<16, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
                           : launch_pf<16, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+#ifndef PCB_PF_RS32
+#define PCB_PF_RS32 2
+#endif
     case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
-                          : launch_pf<32, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+                          : launch_pf<32, PCB_PF_RS32>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
                           : launch_pf<64, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     default: return PCB_USAGE;

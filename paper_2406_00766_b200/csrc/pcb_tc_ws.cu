@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       prefetch_tmap(&tm0);
       prefetch_tmap(&tm1);
       if (MODE == MODE_CF) prefetch_tmap(&tm2);
-      Ring rr(C::kRS);
+      Ring<C::kRS> rr;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         const WsItem it = ws_item(a, item);
         const int b0 = it.b0;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     // ------------------------------------------------------------ theta producer
     // stacked theta tiles of each K block: hi planes back to back, then lo
     // planes, so the S tiles form one N = S * nb operand per plane
-    Ring orr(C::kOS);
+    Ring<C::kOS> orr;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const WsItem it = ws_item(a, item);
       const int m0 = it.m0, S = it.S;
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     }
   } else if (warp == WS_MMA) {
     // ------------------------------------------------------------ MMA issuer
-    Ring orr(C::kOS);
+    Ring<C::kOS> orr;
     int acc_u = 0;
     constexpr uint32_t SBO = (KC / 8) * 128;  // A and B both K-major, no swizzle
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -303,7 +303,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     const int t = (tid - WS_CONV0 * 32) & (WS_M - 1);  // sample within the item
     const int kh = (tid - WS_CONV0 * 32) / WS_M;        // which part of each K block
     constexpr int KH = KC * 4 / W::kConv;                // K columns per converter thread
-    Ring rr(C::kRS), orr(C::kOS);
+    Ring<C::kRS> rr;
+    Ring<C::kOS> orr;
     int g_u = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const WsItem it = ws_item(a, item);

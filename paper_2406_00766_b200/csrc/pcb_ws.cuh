@@ -17,13 +17,21 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 
 // ring position: slot and wait parities of use u of a ring with S stages
+// stage ring of S slots: slot index and mbarrier phase parity, kept
+// incrementally (no division per access)
+template <int S>
 struct Ring {
-  int S, u = 0;
-  __device__ explicit Ring(int s) : S(s) {}
-  __device__ int slot() const { return u % S; }
-  __device__ uint32_t full_par() const { return (uint32_t)((u / S) & 1); }
-  __device__ uint32_t empty_par() const { return full_par() ^ 1u; }
-  __device__ void next() { ++u; }
+  int s = 0;
+  uint32_t par = 0;
+  __device__ int slot() const { return s; }
+  __device__ uint32_t full_par() const { return par; }
+  __device__ uint32_t empty_par() const { return par ^ 1u; }
+  __device__ void next() {
+    if (++s == S) {
+      s = 0;
+      par ^= 1u;
+    }
+  }
 };
 
 __device__ __forceinline__ int next_real(const int32_t* __restrict__ ids, int cap, int c) {
