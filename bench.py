@@ -172,6 +172,10 @@ def class_model(c, B, info=None):
     m["input_fwd"]["bytes"] = B * 4 * (c.num_vars + n_in) + 4 * n_pmf
     m["input_flow"]["bytes"] = B * 4 * (n_in + c.num_vars) + 8 * n_pmf
     m["em"]["bytes"] = 20 * c.theta_size
+    # parameter tiles: a tile shared by several layers (tied HMM transitions)
+    # is read (and its flows accumulated) once per step at minimum — charge
+    # each unique tile to the first layer that uses it
+    seen = set()
     for li, L in enumerate(c.layers):
         n_sum, n_prod, F, E, E_pad = _layer_counts(c, L)
         tc = tc_layer(L) and L.k_m in (16, 32, 64) and L.k_n in (16, 32)
@@ -179,11 +183,18 @@ def class_model(c, B, info=None):
         if li >= skip:
             m["prod_eval"]["bytes"] += B * 4 * (F + n_prod)
             m["accum_push"]["bytes"] += B * 4 * (n_prod + F + n_sum)
-        m[fwd]["bytes"] += B * 4 * (n_prod + n_sum) + 4 * E
-        # ratio rows + product offsets; theta read + flow write per edge
-        m["param_flow"]["bytes"] += B * 4 * (n_sum + n_prod) + 8 * E
+        tiles = set()
+        for g in L.fwd_groups:
+            pid = np.asarray(g.param_ids)
+            tiles.update(np.unique(pid[pid != 0]).tolist())
+        new = tiles - seen
+        seen |= tiles
+        E_u = E * len(new) // max(len(tiles), 1)  # edges in tiles not yet charged
+        m[fwd]["bytes"] += B * 4 * (n_prod + n_sum) + 4 * E_u
+        # ratio rows + product offsets; theta read + flow write per unique edge
+        m["param_flow"]["bytes"] += B * 4 * (n_sum + n_prod) + 8 * E_u
         # ratio rows + product offsets + product-flow rows; theta (bf16 planes)
-        m["child_flow"]["bytes"] += B * 4 * (n_sum + 2 * n_prod) + 4 * E
+        m["child_flow"]["bytes"] += B * 4 * (n_sum + 2 * n_prod) + 4 * E_u
         for k in (fwd, "param_flow", "child_flow"):
             m[k]["flops"] += 2 * E * B
             if tc:
