@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 23;
+constexpr int64_t kVersion = 24;
 
 struct Reader {
   const int64_t* p;
@@ -142,6 +142,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
       G.param_slab_c = r.ref();
       G.exclusive = (int)r.get();
       G.uniform = (int)r.get();
+      G.pf_pre = (int)r.get();
       TcRows T, Tp;
       T.count = r.get();
       T.row_off = r.ref();
@@ -211,6 +212,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.pre_ratio = (int)r.get();
     L.rmax_off = r.get();
     L.n_pb = L.window / L.k_n;  // including the -inf pad block 0
+    for (const FwdGroup& G : L.fwd)
+      if (G.pf_pre) P->max_prep_rows = std::max(P->max_prep_rows, pf_prep_rows(L, G));
     L.pb_off = P->n_pb_tot;
     L.vb_off = P->n_sb_tot;
     P->n_pb_tot += L.n_pb;
@@ -389,7 +392,8 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.ratio = w.rmax + P->max_sb * (int64_t)ldb;
   w.gshift = w.ratio + P->max_sum_rows * (int64_t)ldb;
   w.rmax_all = w.gshift + 2 * P->max_tc_rows * (int64_t)ldb;
-  w.counters = reinterpret_cast<int32_t*>(w.rmax_all + P->n_rmax * (int64_t)ldb);
+  w.prep = w.rmax_all + P->n_rmax * (int64_t)ldb;
+  w.counters = reinterpret_cast<int32_t*>(w.prep + P->max_prep_rows * (int64_t)ldb);
   return w;
 }
 
@@ -511,7 +515,7 @@ int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B,
     const TcRows& T = L.pf_tc[g];
     if (tc && T.count > 0)
       st = launch_param_flow_ws(L, L.fwd[g], T, sp, B, ldb, theta, ratio, rmax, scratch, vbase,
-                                pbase, f_params, em_fuse ? &em : nullptr);
+                                pbase, f_params, em_fuse ? &em : nullptr, w.prep);
     else
       st = launch_param_flow_simt(L, L.fwd[g], sp, B, ldb, theta, values, flows, scratch, pbase,
                                   vbase, f_params);
@@ -684,7 +688,7 @@ int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
   // + one split-K arrival counter per (super-row, 128-sample tile)
   return (plan->n_sb_tot + plan->n_pb_tot + plan->max_sb + plan->max_sum_rows +
-          2 * plan->max_tc_rows + plan->n_rmax) *
+          2 * plan->max_tc_rows + plan->n_rmax + plan->max_prep_rows) *
              (int64_t)ldb +
          plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }

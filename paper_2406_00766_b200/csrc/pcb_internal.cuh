@@ -48,6 +48,7 @@ struct FwdGroup {
   const int32_t* param_slab_c;  // product-major plane offset per (row, col) (fused EM)
   int exclusive = 0;          // every flow tile of the group has no other writer in the pass
   int uniform = 0;            // every row has the same child blocks (dense layer)
+  int pf_pre = 0;             // parameter-flow operands converted once per layer (pf_pre_ok)
 };
 
 struct BwdGroup {
@@ -128,6 +129,8 @@ struct Layer {
 //                               its block's rmax (k_ratio)
 //   gshift [2 max_tc_rows x ldb] per-(super-row, sample) shifts of long-K
 //                               layers (child flows: g rows, then base rows)
+//   prep [max_prep_rows x ldb]  pre-converted bf16 hi/lo parameter-flow
+//                               operand images of one pf_pre layer (+ its shift row)
 //   counters [max_tc_rows x ldb/128] split-K arrivals (self-resetting, zeroed at allocation)
 struct Work {
   float* vbase;
@@ -136,6 +139,7 @@ struct Work {
   float* ratio;
   float* gshift;
   float* rmax_all;  // [n_rmax x ldb] R rows of the pre-ratioed layers
+  float* prep;
   int32_t* counters;
 };
 
@@ -171,6 +175,7 @@ struct pcb_plan {
   int use_tc;  // 0: SIMT; 1: tensor cores (warp-specialised where supported)
   int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1, max_tc_rows = 1;
   int64_t n_pb_tot = 0, n_sb_tot = 0;  // all layers' product / sum blocks (base rows)
+  int64_t max_prep_rows = 0;  // pre-converted parameter-flow operand rows (pf_pre groups)
   // bf16 tensor-core copies of theta tiles (plan v4)
   // bf16 planes: regions of mma_plane elements: [F hi][F lo][C hi][C lo];
   // tile t's sum-major planes at slab_f[t] (+ plane), its product-major
@@ -364,6 +369,8 @@ bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
                          const float* scratch, const float* vbase, const float* pbase,
-                         float* f_params, const PfEm* em = nullptr);
+                         float* f_params, const PfEm* em = nullptr, float* prep = nullptr);
+// pf_pre groups: image rows of the pre-converted operands
+int64_t pf_prep_rows(const Layer& L, const FwdGroup& g);
 
 }  // namespace pcb

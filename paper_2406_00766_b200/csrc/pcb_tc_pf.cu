@@ -52,7 +52,10 @@ constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
 #endif
 // warps: producer, MMA, converters, 4 epilogue
 constexpr int PF_CONV0 = 2, PF_NCONV = PCB_PF_NCONV, PF_EPI0 = PF_CONV0 + PF_NCONV;
-constexpr int PF_THREADS = (PF_EPI0 + 4) * 32;
+// 8 epilogue warps: two per TMEM lane quarter, alternate 16-column chunks
+// (the fused-EM path needs whole rows: only the first four work there)
+constexpr int PF_NEPI = 8;
+constexpr int PF_THREADS = (PF_EPI0 + PF_NEPI) * 32;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
 
 struct PfArgs {
@@ -73,6 +76,9 @@ struct PfArgs {
   int64_t plane;
   const int32_t *slab_f, *slab_c;
   float* theta_out;
+  // pre-converted operands (PRE kernels): per (128-sum tile, chunk) the A
+  // hi + lo plane images, per (256-child column group, chunk) the B images
+  const uint8_t *prep_a, *prep_e;
 };
 
 // RS raw stages and 4 - RS operand stages (32-sample chunks): 2 / 2 for
@@ -92,6 +98,9 @@ struct PfCfg {
   static constexpr int kOp = 2 * kOpA + 2 * kOpB;
   static constexpr int kRS = (PF_KS == 16) ? 5 : RS, kOS = (PF_KS == 16) ? 3 : 4 - RS;
   static constexpr int kBytes = kRS * kRaw + kOS * kOp;
+  // PRE: no raw ring, the whole buffer is operand stages
+  static constexpr int kOSP = kBytes / kOp;
+  static constexpr int kOSmax = kOSP > kOS ? kOSP : kOS;
   static_assert(kRaw % 1024 == 0 && kA % 1024 == 0, "swizzled boxes need aligned bases");
 };
 
@@ -124,8 +133,18 @@ __device__ __forceinline__ PfItem pf_item(const PfArgs& a, int item) {
   return it;
 }
 
+// every column of the item's row is real (flags bit 3): no scan
+__device__ __forceinline__ bool pf_dense_row(const PfArgs& a, const PfItem& it) {
+  return (__ldg(a.flags + it.sr) & 8) != 0;
+}
+
 // the item's real child columns (at most kCPG): writes cols[], returns count
 __device__ __forceinline__ int pf_cols(const PfArgs& a, const PfItem& it, int cpg, int* cols) {
+  if (pf_dense_row(a, it)) {
+    const int n = max(0, min(cpg, a.cap - it.cg * cpg));
+    for (int i = 0; i < n; ++i) cols[i] = it.cg * cpg + i;
+    return n;
+  }
   const int32_t* trow = a.param_ids + (int64_t)it.r0 * a.cap;
   int seen = 0, n = 0;
   for (int c = 0; c < a.cap && n < cpg; ++c) {
@@ -138,6 +157,7 @@ __device__ __forceinline__ int pf_cols(const PfArgs& a, const PfItem& it, int cp
 
 // number of real child columns of the item
 __device__ __forceinline__ int pf_ncols(const PfArgs& a, const PfItem& it, int cpg) {
+  if (pf_dense_row(a, it)) return max(0, min(cpg, a.cap - it.cg * cpg));
   const int32_t* trow = a.param_ids + (int64_t)it.r0 * a.cap;
   int seen = 0;
   for (int c = 0; c < a.cap; ++c) seen += __ldg(trow + c) != 0;
@@ -155,7 +175,11 @@ __device__ __forceinline__ int swz_chunk(int row, int c) {
 
 }  // namespace
 
-template <int KN, int RS>
+// PRE: the operands were converted once per layer (k_pf_prep, dense uniform
+// groups): the producer bulk-copies the bf16 plane images of the item's
+// 128-sum tile and 256-child column group straight into the operand ring;
+// the converter warps idle.
+template <int KN, int RS, bool PRE>
 __global__ void __launch_bounds__(PF_THREADS, 1)
     k_param_flow_ws(const PfArgs a, const __grid_constant__ CUtensorMap tm_r,
                     const __grid_constant__ CUtensorMap tm_R, const __grid_constant__ CUtensorMap tm_e,
@@ -167,28 +191,30 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                     const __grid_constant__ CUtensorMap tm_pbn) {
   using C = PfCfg<KN, RS>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOS], op_empty[C::kOS];
+  constexpr int OS = PRE ? C::kOSP : C::kOS;  // operand stages
+  __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS], op_full[C::kOSmax],
+      op_empty[C::kOSmax];
   __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ __align__(16) float cs[C::kRS][PF_KS];
   __shared__ int cols_p[C::kCPG];
-  __shared__ int cols_w[4][C::kCPG];  // epilogue warps' column lists
+  __shared__ int cols_w[PF_NEPI][C::kCPG];  // epilogue warps' column lists
   __shared__ float em_wt[4][32 * 33];  // fused EM: a warp's updated 32 x 32 tile
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
-  uint8_t* ops = smem + C::kRS * C::kRaw;
+  uint8_t* ops = PRE ? smem : smem + C::kRS * C::kRaw;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < C::kRS; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
       mbar_init(smem_u32(&raw_empty[i]), PF_NCONV);
     }
-    for (int i = 0; i < C::kOS; ++i) {
-      mbar_init(smem_u32(&op_full[i]), PF_NCONV);
+    for (int i = 0; i < OS; ++i) {
+      mbar_init(smem_u32(&op_full[i]), PRE ? 1 : PF_NCONV);  // PRE: the producer's tx
       mbar_init(smem_u32(&op_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), 4);
+      mbar_init(smem_u32(&acc_empty[i]), PF_NEPI);
     }
     fence_mbar_init();
   }
@@ -198,7 +224,31 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (warp == 0) {
+  if (PRE && warp == 0) {
+    // ------------------------------------------------------------ producer (PRE)
+    if (lane == 0) {
+      Ring<OS> orr;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        const PfItem it = pf_item(a, item);
+        if (!pf_active(it)) continue;
+        const int ncol = pf_cols(a, it, C::kCPG, cols_p);
+        if (!ncol) continue;
+        const int ta = (__ldg(a.sum_ids + __ldg(a.members + it.m0 + it.s_lo)) - (int)a.sb_base) /
+                       PF_M;
+        const uint8_t* ia = a.prep_a + ((int64_t)ta * a.nchunks) * (2 * C::kOpA);
+        const uint8_t* ie = a.prep_e + ((int64_t)it.cg * a.nchunks) * (2 * C::kOpB);
+        for (int kc = it.kc0; kc < it.kc1; ++kc) {
+          mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
+          const uint32_t of = smem_u32(&op_full[orr.slot()]);
+          mbar_arrive_expect_tx(of, (uint32_t)(2 * C::kOpA + 2 * C::kOpB));
+          const uint32_t st = smem_u32(ops + orr.slot() * C::kOp);
+          bulk_g2s(st, ia + (int64_t)kc * (2 * C::kOpA), (uint32_t)(2 * C::kOpA), of);
+          bulk_g2s(st + 2 * C::kOpA, ie + (int64_t)kc * (2 * C::kOpB), (uint32_t)(2 * C::kOpB), of);
+          orr.next();
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       prefetch_tmap(&tm_r);
@@ -258,7 +308,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    Ring<C::kOS> orr;
+    Ring<OS> orr;
     int acc_u = 0;
     constexpr uint32_t SBO = (PF_KS / 8) * 128;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -298,6 +348,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
   } else if (warp < PF_EPI0) {
     // ------------------------------------------------------------ converters
+    if constexpr (!PRE) {
     const int t = tid - PF_CONV0 * 32;  // 0..PF_NCONV*32-1
     Ring<C::kRS> rr;
     Ring<C::kOS> orr;
@@ -401,9 +452,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         orr.next();
       }
     }
+    }  // !PRE
   } else {
     // ------------------------------------------------------------ epilogue
     const int q4 = warp & 3;
+    const int h = (warp - PF_EPI0) >> 2;  // column half: chunks h*16, h*16 + 32, ...
     const int er = q4 * 32 + lane;  // sum row within the tile (TMEM lane)
     int* cols = cols_w[warp - PF_EPI0];
     int acc_u = 0;
@@ -440,10 +493,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         }
       };
       float th[16], thn[16];
-      if (live) load_th(tile_of(0), thn);
+      const bool em_idle = KN == 32 && a.em && h == 1;  // fused EM: rows on the first four warps
+      if (live && !em_idle && (a.em ? 0 : h * 16) < ncol * KN)
+        load_th(tile_of(a.em ? 0 : h * 16), thn);
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(as * PF_N) + ((uint32_t)(q4 * 32) << 16);
+      if (em_idle) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
+        ++acc_u;
+        continue;
+      }
       if constexpr (KN == 32) {
         if (a.em) {
           // pass 1: the row's group total sum(F + k) over all its columns
@@ -536,11 +598,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           continue;
         }
       }
-      for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+      for (int c0 = h * 16; c0 < ncol * KN; c0 += 32) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) th[i] = thn[i];
 #ifndef PCB_ABL_EPI
-        if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
+        if (live && c0 + 32 < ncol * KN) load_th(tile_of(c0 + 32), thn);
 #endif
         float v[16];
         tmem_ld16(tbase + c0, v);
@@ -603,12 +665,111 @@ int pf_kslices(int64_t count, int64_t cap, int kn, int B) {
 
 namespace {
 
+// ---------------------------------------------------------------- pre-conversion
+// Dense uniform groups (pf_pre_ok: every sum block over the same child row,
+// several 128-sum tiles and 256-child column groups per layer, e.g. HMM
+// transitions): each operand is converted once per layer instead of once per
+// item that uses it (the B operand 2 x (sum rows / 256) times, the A operand
+// (child columns / 256) times).  The shift is one per sample for the whole
+// layer, c_b = max over its sum blocks of R (it cancels between the
+// operands as the per-tile shift does).
+//   prep row 0          c_b
+//   A images            per (128-sum tile, 32-sample chunk): hi plane, lo
+//                       plane of 2^(r + R - c) in the MMA's K-major layout
+//   B images            per (256-child column group, chunk): hi, lo planes
+//                       of 2^((o + base_pb - base_sum) log2 e + c)
+__global__ void k_pf_shift(int n_sb, int B, int ldb, const float* __restrict__ rmax,
+                           float* __restrict__ c) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= ldb) return;
+  float m = PCB_NEG_INF;
+  if (b < B)
+    for (int k = 0; k < n_sb; ++k) m = fmaxf(m, __ldg(rmax + (int64_t)k * ldb + b));
+  c[b] = m;
+}
+
+__global__ void __launch_bounds__(256)
+    k_pf_prep(int n_a, int n_e, int k_m, int kn, int nchunks, int ldb, int cap,
+              const int32_t* __restrict__ prod_row0, const int32_t* __restrict__ param_row0,
+              const float* __restrict__ ratio, const float* __restrict__ rmax,
+              const float* __restrict__ scratch, const float* __restrict__ pbase,
+              const float* __restrict__ vbase, const float* __restrict__ c,
+              uint8_t* __restrict__ img_a, uint8_t* __restrict__ img_e) {
+  constexpr int kOpA = PF_M * PF_KS * 2, kOpB = PF_N * PF_KS * 2;
+  __shared__ int child0, n_real;
+  if (threadIdx.x == 0) {
+    int first = 0, cnt = 0;
+    while (first < cap && __ldg(param_row0 + first) == 0) ++first;
+    for (int q = 0; q < cap; ++q) cnt += __ldg(param_row0 + q) != 0;
+    child0 = first < cap ? __ldg(prod_row0 + first) : 0;
+    n_real = cnt * kn;  // contiguous real child rows (pf_pre_ok)
+  }
+  __syncthreads();
+  const int oct = ldb / 8;
+  const int64_t total = (int64_t)(n_a + n_e) * oct;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(t / oct), b0 = (int)(t % oct) * 8;
+    const int kc = b0 / PF_KS, k = b0 % PF_KS;
+    const float4 c0 = *reinterpret_cast<const float4*>(c + b0);
+    const float4 c1 = *reinterpret_cast<const float4*>(c + b0 + 4);
+    const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    float v[8];
+    uint8_t* dst;
+    uint32_t plane;
+    if (row < n_a) {
+      const float* rr = ratio + (int64_t)row * ldb + b0;
+      const float* RR = rmax + (int64_t)(row / k_m) * ldb + b0;
+      const float4 x0 = *reinterpret_cast<const float4*>(rr);
+      const float4 x1 = *reinterpret_cast<const float4*>(rr + 4);
+      const float4 R0 = *reinterpret_cast<const float4*>(RR);
+      const float4 R1 = *reinterpret_cast<const float4*>(RR + 4);
+      const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      const float Rs[8] = {R0.x, R0.y, R0.z, R0.w, R1.x, R1.y, R1.z, R1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = (cc[e] == PCB_NEG_INF) ? 0.f : ex2(xs[e] + (Rs[e] - cc[e]));
+      dst = img_a + ((int64_t)(row / PF_M) * nchunks + kc) * (2 * kOpA) +
+            kmajor_off(row % PF_M, k, PF_KS);
+      plane = kOpA;
+    } else {
+      const int n = row - n_a;
+      if (n >= n_real) continue;
+      const int srow = child0 + n;
+      const float* xr = scratch + (int64_t)srow * ldb + b0;
+      const float* pr = pbase + (int64_t)(srow / kn) * ldb + b0;
+      const float4 x0 = *reinterpret_cast<const float4*>(xr);
+      const float4 x1 = *reinterpret_cast<const float4*>(xr + 4);
+      const float4 p0 = *reinterpret_cast<const float4*>(pr);
+      const float4 p1 = *reinterpret_cast<const float4*>(pr + 4);
+      const float4 s0 = *reinterpret_cast<const float4*>(vbase + b0);
+      const float4 s1 = *reinterpret_cast<const float4*>(vbase + b0 + 4);
+      const float xs[8] = {x0.x + (p0.x - s0.x), x0.y + (p0.y - s0.y), x0.z + (p0.z - s0.z),
+                           x0.w + (p0.w - s0.w), x1.x + (p1.x - s1.x), x1.y + (p1.y - s1.y),
+                           x1.z + (p1.z - s1.z), x1.w + (p1.w - s1.w)};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        v[e] = (cc[e] == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(xs[e], kL2E, cc[e])), 1e37f);
+      dst = img_e + ((int64_t)(n / PF_N) * nchunks + kc) * (2 * kOpB) +
+            kmajor_off(n % PF_N, k, PF_KS);
+      plane = kOpB;
+    }
+    uint4 hi, lo;
+    split_pack8(v, hi, lo);
+    *reinterpret_cast<uint4*>(dst) = hi;
+    *reinterpret_cast<uint4*>(dst + plane) = lo;
+  }
+}
+
 template <int KN, int RS>
 int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float* rmax,
-              const float* scratch, const float* vbase, const float* pbase, cudaStream_t s) {
+              const float* scratch, const float* vbase, const float* pbase, cudaStream_t s,
+              float* prep = nullptr) {
   using C = PfCfg<KN, RS>;
-  static int attr[kMaxDev] = {};
-  if (ensure_smem((const void*)k_param_flow_ws<KN, RS>, C::kBytes, attr)) return PCB_CUDA;
+  const bool pre = prep != nullptr;
+  static int attr[kMaxDev] = {}, attr_p[kMaxDev] = {};
+  if (ensure_smem((const void*)k_param_flow_ws<KN, RS, false>, C::kBytes, attr) ||
+      (pre && ensure_smem((const void*)k_param_flow_ws<KN, RS, true>, C::kBytes, attr_p)))
+    return PCB_CUDA;
   PfArgs a = a0;
   a.cgroups = (int)((a.cap * KN + PF_N - 1) / PF_N);
   a.mtiles = 2;  // super-rows hold <= 256 sums
@@ -629,13 +790,40 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
       make_rows_map(&tpb, pbase, L.n_pb, a.ldb, 1, C::kRP / 4, 0) ||
       make_rows_map(&tpbn, pbase, L.n_pb, a.ldb, C::kCPG, C::kRP / 4, 0))
     return PCB_CUDA;
+  if (pre) {
+    // the layer's operands once: shift row, A images (all sum rows), B images
+    const int n_a = (int)(L.n_sb * L.k_m), n_e = a.cap * KN;
+    const int64_t a_rows = (n_a + PF_M - 1) / PF_M * PF_M;
+    float* c = prep;
+    uint8_t* img_a = reinterpret_cast<uint8_t*>(prep + a.ldb);
+    uint8_t* img_e = reinterpret_cast<uint8_t*>(prep + a.ldb + a_rows * a.ldb);
+    k_pf_shift<<<(a.ldb + 127) / 128, 128, 0, s>>>((int)L.n_sb, a.B, a.ldb, rmax, c);
+    if (check_launch()) return PCB_CUDA;
+    const int64_t tasks = (int64_t)(n_a + n_e) * (a.ldb / 8);
+    k_pf_prep<<<grid_for(tasks, 256), 256, 0, s>>>(n_a, n_e, (int)L.k_m, KN, a.nchunks, a.ldb,
+                                                   a.cap, a.prod_ids, a.param_ids, ratio, rmax,
+                                                   scratch, pbase, vbase, c, img_a, img_e);
+    if (check_launch()) return PCB_CUDA;
+    a.prep_a = img_a;
+    a.prep_e = img_e;
+  }
   const int grid = min(a.n_items, sm_count());
-  k_param_flow_ws<KN, RS><<<grid, PF_THREADS, C::kBytes, s>>>(a, tr, tR, te, tr128, tRt, te256,
-                                                              tvb, tpb, tpbn);
+  if (pre)
+    k_param_flow_ws<KN, RS, true><<<grid, PF_THREADS, C::kBytes, s>>>(
+        a, tr, tR, te, tr128, tRt, te256, tvb, tpb, tpbn);
+  else
+    k_param_flow_ws<KN, RS, false><<<grid, PF_THREADS, C::kBytes, s>>>(
+        a, tr, tR, te, tr128, tRt, te256, tvb, tpb, tpbn);
   return check_launch();
 }
 
 }  // namespace
+
+int64_t pf_prep_rows(const Layer& L, const FwdGroup& g) {
+  // the shift row, A images (sum rows to a 128 multiple), B images (child
+  // columns to a 256 multiple); one bf16 hi + lo pair per element = 1 float
+  return 1 + (L.n_sb * L.k_m + PF_M - 1) / PF_M * PF_M + (g.cap * L.k_n + PF_N - 1) / PF_N * PF_N;
+}
 
 bool pf_ws_supported(const Layer& L) {
   return (L.k_n == 16 || L.k_n == 32 || L.k_n == 64) && (L.k_m == 16 || L.k_m == 32 || L.k_m == 64);
@@ -657,7 +845,7 @@ bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B) {
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
                          const float* scratch, const float* vbase, const float* pbase,
-                         float* f_params, const PfEm* em) {
+                         float* f_params, const PfEm* em, float* prep) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   PfArgs a{};
@@ -698,7 +886,8 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
 #ifndef PCB_PF_RS32
 #define PCB_PF_RS32 2
 #endif
-    case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
+    case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s,
+                                             (g.pf_pre && !em) ? prep : nullptr)
                           : launch_pf<32, PCB_PF_RS32>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
                           : launch_pf<64, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 23
+VERSION = 24
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -562,6 +562,25 @@ def em_fused_order(compiled, tb, tensor_cores: bool):
     return out, n_pre, ranges, fus
 
 
+def pf_pre_ok(g, L) -> bool:
+    """Parameter flows of a dense uniform group (every sum block over the same
+    child row, several 256-child column groups or 128-sum tiles sharing it,
+    e.g. HMM transition layers) may convert their operands once per layer:
+    the sums are consecutive value slots from a 128-aligned start, the real
+    child blocks consecutive scratch rows (the pre-converted 128-sum and
+    256-child operand images are then addressed by row)."""
+    if L.k_n != 32 or L.k_m not in (16, 32) or len(L.fwd_groups) != 1:
+        return False
+    sid = np.sort(np.asarray(g.sum_ids, dtype=np.int64))
+    if sid.size < 4 or np.any(np.diff(sid) != L.k_m):
+        return False
+    real = np.asarray(g.param_ids[0]) != 0
+    p = np.asarray(g.prod_ids[0])[real]
+    if p.size < 8 or np.any(np.diff(p) != L.k_n):
+        return False
+    return int(real.sum()) * L.k_n > 256 or sid.size * L.k_m > 128
+
+
 def pf_contig_flags(g, offs, mem, k_m: int, k_n: int) -> np.ndarray:
     """Per (full-stack) super-row: bit 0 = its member sum blocks are
     consecutive sum rows, bit 1 = its real child blocks are consecutive
@@ -577,7 +596,8 @@ def pf_contig_flags(g, offs, mem, k_m: int, k_n: int) -> np.ndarray:
         real = g.param_ids[row] != 0
         p = g.prod_ids[row][real]
         e_ok = bool(np.all(np.diff(p) == k_n)) if p.size > 1 else True
-        flags[r] = int(a_ok) | (int(e_ok) << 1)
+        # bit 3: no padding column (the item's columns follow arithmetically)
+        flags[r] = int(a_ok) | (int(e_ok) << 1) | (int(bool(real.all())) << 3)
     return flags
 
 
@@ -824,7 +844,9 @@ def build_program(compiled, *, tensor_cores: bool = True):
             ref(_slab_of(g.param_ids, t_start, t_slab_c) if use_tc else np.zeros(0, np.int64))
             prog.append(exclusive(g))
             # every row has the same child blocks: one shift row serves them all
-            prog.append(int(rows > 0 and group_matrix_rows(g.prod_ids)[1].size == 1))
+            uniform = rows > 0 and group_matrix_rows(g.prod_ids)[1].size == 1
+            prog.append(int(uniform))
+            prog.append(int(use_tc and uniform and pf_pre_ok(g, L)))
             if use_tc and rows:
                 # forward: enough super-rows to fill the SMs; param flows: full
                 # stacks (their grid also spans column groups)
