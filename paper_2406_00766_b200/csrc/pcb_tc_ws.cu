@@ -122,6 +122,19 @@ __device__ __forceinline__ int slice_first(const int32_t* __restrict__ real, int
   return c;
 }
 
+// rows whose columns are all real (TcRows flags bit 3) step arithmetically
+__device__ __forceinline__ bool dense_row(const WsArgs& a, const WsItem& it) {
+  return a.flags && (__ldg(a.flags + it.sr) & 8);
+}
+__device__ __forceinline__ int col_first(const int32_t* __restrict__ real, int cap, int skip,
+                                         bool dense) {
+  return dense ? min(skip, cap) : slice_first(real, cap, skip);
+}
+__device__ __forceinline__ int col_next(const int32_t* __restrict__ real, int cap, int c,
+                                        bool dense) {
+  return dense ? c : next_real(real, cap, c);
+}
+
 template <int MODE, int KC>
 struct WsCfg {
   // raw rows per stage: the K block's rows (forward: child offsets; child
@@ -202,8 +215,9 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         const int b0 = it.b0;
         const int32_t* src = a.src_ids + (int64_t)it.r0 * a.cap;
         const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
-        int c = slice_first(real, a.cap, it.ks * a.kper);
-        for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
+        const bool dn = dense_row(a, it);
+      int c = col_first(real, a.cap, it.ks * a.kper, dn);
+        for (int k = 0; c < a.cap && k < a.kper; ++k, c = col_next(real, a.cap, c + 1, dn)) {
           const int row0 = __ldg(src + c) - (int)a.sb_base;
           mbar_wait(smem_u32(&raw_empty[rr.slot()]), rr.empty_par());
           const uint32_t rf = smem_u32(&raw_full[rr.slot()]);
@@ -226,8 +240,9 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       const int m0 = it.m0, S = it.S;
       const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
       const bool contig = a.flags && (__ldg(a.flags + it.sr) & 4);
-      int c = slice_first(real, a.cap, it.ks * a.kper);
-      for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
+      const bool dn = dense_row(a, it);
+      int c = col_first(real, a.cap, it.ks * a.kper, dn);
+      for (int k = 0; c < a.cap && k < a.kper; ++k, c = col_next(real, a.cap, c + 1, dn)) {
         mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
         const uint32_t of = smem_u32(&op_full[orr.slot()]);
         uint8_t* bdst = ops + orr.slot() * C::kOp + 2 * C::kA;
@@ -264,8 +279,9 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       tc_fence_after();
       const uint32_t d0 = tmem + (uint32_t)(as * WS_NMAX);
       bool first = true;
-      int c = slice_first(real, a.cap, it.ks * a.kper);
-      for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
+      const bool dn = dense_row(a, it);
+      int c = col_first(real, a.cap, it.ks * a.kper, dn);
+      for (int k = 0; c < a.cap && k < a.kper; ++k, c = col_next(real, a.cap, c + 1, dn)) {
         mbar_wait(smem_u32(&op_full[orr.slot()]), orr.full_par());
         tc_fence_after();
         if (lane == 0) {
@@ -319,8 +335,9 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       // forward: g is the integer base G (natural log); child flow: g is in
       // log2 units, gr the common base of the parent blocks
       const float gl2 = dead ? 0.f : g;
-      int c = slice_first(real, a.cap, it.ks * a.kper);
-      for (int k = 0; c < a.cap && k < a.kper; ++k, c = next_real(real, a.cap, c + 1)) {
+      const bool dn = dense_row(a, it);
+      int c = col_first(real, a.cap, it.ks * a.kper, dn);
+      for (int k = 0; c < a.cap && k < a.kper; ++k, c = col_next(real, a.cap, c + 1, dn)) {
         mbar_wait(smem_u32(&raw_full[rr.slot()]), rr.full_par());
         const float* rs = reinterpret_cast<const float*>(raw + rr.slot() * C::kRaw);
         float x[KH];
@@ -389,7 +406,10 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       for (int u = 0; u < SPL; ++u) g[u] = gr[u] = PCB_NEG_INF;
       nk = 0;
       if (a.gshift) {  // long K: shifts precomputed by k_group_shift
-        for (int c = 0; c < a.cap; ++c) nk += __ldg(real + c) != 0;
+        if (dense_row(a, it))
+          nk = a.cap;
+        else
+          for (int c = 0; c < a.cap; ++c) nk += __ldg(real + c) != 0;
 #pragma unroll
         for (int u = 0; u < SPL; ++u) {
           const int b = it.b0 + lane + 32 * u;

@@ -178,7 +178,8 @@ def theta_contig_flags(slab_ids, offs, mem, plane: int) -> np.ndarray:
         sl = slab_ids[m]                       # [S, cap]
         ok = np.all((sl[1:] - sl[:-1] == plane) | (sl[1:] < 0) & (sl[:-1] < 0)) \
             if m.size > 1 else True
-        flags[r] = 4 if ok else 0
+        # bit 3: every column of the row is real (no scan for real columns)
+        flags[r] = (4 if ok else 0) | (8 if bool(np.all(sl[0] >= 0)) else 0)
     return flags
 
 
