@@ -678,11 +678,83 @@ __global__ void __launch_bounds__(TB* TY)
   if (ty == 0) vbase[(int64_t)((sid - sb_base) / k_m) * ldb + b] = G;
 }
 
+// Single-sum rows (k_m = 1, e.g. an HMM or mixture root over thousands of
+// children): the eight thread rows split the child blocks (each its own
+// streaming (lin, top) pair, merged in shared memory at the end) instead of
+// one thread row walking all of them while seven idle.
+__global__ void __launch_bounds__(TB* TY)
+    k_sum_fwd_simt1(int cap, int k_n, int B, int ldb, int64_t sb_base,
+                    const int32_t* __restrict__ sum_ids, const int32_t* __restrict__ prod_ids,
+                    const int32_t* __restrict__ param_ids, const float* __restrict__ theta,
+                    const float* __restrict__ scratch, const float* __restrict__ pbase,
+                    float* __restrict__ values, float* __restrict__ vbase) {
+  __shared__ float lin_s[TY][TB], top_s[TY][TB], g_s[TY][TB];
+  const int r = blockIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int b = blockIdx.x * TB + tx;
+  const bool live = b < B;
+  const int32_t* prow = prod_ids + (int64_t)r * cap;
+  const int32_t* trow = param_ids + (int64_t)r * cap;
+  float G = PCB_NEG_INF;
+  if (live)
+    for (int c = ty; c < cap; c += TY)
+      if (trow[c] != 0) G = fmaxf(G, pbase[(int64_t)(prow[c] / k_n) * ldb + b]);
+  g_s[ty][tx] = G;
+  __syncthreads();
+  G = PCB_NEG_INF;
+#pragma unroll
+  for (int y = 0; y < TY; ++y) G = fmaxf(G, g_s[y][tx]);
+  if (G == PCB_NEG_INF) G = 0.f;
+  float lin = 0.f, top = PCB_NEG_INF;
+  if (live)
+    for (int c = ty; c < cap; c += TY) {
+      const int t0 = trow[c];
+      if (t0 == 0) continue;
+      const int pid = prow[c];
+      const float d = pbase[(int64_t)(pid / k_n) * ldb + b] - G;
+      float cmax = PCB_NEG_INF;
+      for (int j = 0; j < k_n; ++j) cmax = fmaxf(cmax, scratch[(int64_t)(pid + j) * ldb + b] + d);
+      if (cmax == PCB_NEG_INF) continue;
+      float part = 0.f;
+      for (int j = 0; j < k_n; ++j)
+        part = fmaf(__ldg(theta + t0 + j), expf(scratch[(int64_t)(pid + j) * ldb + b] + d - cmax),
+                    part);
+      if (cmax > top) {
+        lin = lin * expf(top - cmax) + part;
+        top = cmax;
+      } else {
+        lin += part * expf(cmax - top);
+      }
+    }
+  lin_s[ty][tx] = lin;
+  top_s[ty][tx] = top;
+  __syncthreads();
+  if (ty != 0 || !live) return;
+  float T = PCB_NEG_INF;
+#pragma unroll
+  for (int y = 0; y < TY; ++y) T = fmaxf(T, top_s[y][tx]);
+  float acc = 0.f;
+  if (T != PCB_NEG_INF)
+#pragma unroll
+    for (int y = 0; y < TY; ++y)
+      if (top_s[y][tx] != PCB_NEG_INF) acc += lin_s[y][tx] * expf(top_s[y][tx] - T);
+  const int sid = sum_ids[r];
+  values[(int64_t)sid * ldb + b] = logf(acc) + T;
+  vbase[(int64_t)(sid - sb_base) * ldb + b] = G;
+}
+
 int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                         const float* theta, const float* scratch, const float* pbase,
                         float* values, float* vbase) {
   ProfScope prof_(KC_SUM_FWD_SIMT, s);
   if (!g.rows) return PCB_OK;
+  if (L.k_m == 1 && g.cap >= 2 * TY) {
+    dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
+    k_sum_fwd_simt1<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_n, B, ldb, L.sb_base,
+                                                  g.sum_ids, g.prod_ids, g.param_ids, theta,
+                                                  scratch, pbase, values, vbase);
+    return check_launch();
+  }
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
   k_sum_fwd_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
                                                L.sb_base, g.sum_ids, g.prod_ids, g.param_ids,

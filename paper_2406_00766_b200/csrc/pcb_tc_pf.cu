@@ -27,6 +27,7 @@
 //                the group's flow tiles have a single writer and the batch
 //                is not sliced; else vector red.add).
 #include <math.h>
+#include <stdlib.h>
 
 #include "pcb_internal.cuh"
 #include "pcb_tc.cuh"
@@ -678,14 +679,22 @@ namespace {
 //                       plane of 2^(r + R - c) in the MMA's K-major layout
 //   B images            per (256-child column group, chunk): hi, lo planes
 //                       of 2^((o + base_pb - base_sum) log2 e + c)
-__global__ void k_pf_shift(int n_sb, int B, int ldb, const float* __restrict__ rmax,
-                           float* __restrict__ c) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= ldb) return;
+// CTA = 32 samples x 32 thread rows striding over the sum blocks
+__global__ void __launch_bounds__(1024)
+    k_pf_shift(int n_sb, int B, int ldb, const float* __restrict__ rmax, float* __restrict__ c) {
+  __shared__ float part[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + tx;
   float m = PCB_NEG_INF;
   if (b < B)
-    for (int k = 0; k < n_sb; ++k) m = fmaxf(m, __ldg(rmax + (int64_t)k * ldb + b));
-  c[b] = m;
+    for (int k = ty; k < n_sb; k += 32) m = fmaxf(m, __ldg(rmax + (int64_t)k * ldb + b));
+  part[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && b < ldb) {
+#pragma unroll 8
+    for (int y = 1; y < 32; ++y) m = fmaxf(m, part[y][tx]);
+    c[b] = m;
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -797,7 +806,7 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
     float* c = prep;
     uint8_t* img_a = reinterpret_cast<uint8_t*>(prep + a.ldb);
     uint8_t* img_e = reinterpret_cast<uint8_t*>(prep + a.ldb + a_rows * a.ldb);
-    k_pf_shift<<<(a.ldb + 127) / 128, 128, 0, s>>>((int)L.n_sb, a.B, a.ldb, rmax, c);
+    k_pf_shift<<<(a.ldb + 31) / 32, 1024, 0, s>>>((int)L.n_sb, a.B, a.ldb, rmax, c);
     if (check_launch()) return PCB_CUDA;
     const int64_t tasks = (int64_t)(n_a + n_e) * (a.ldb / 8);
     k_pf_prep<<<grid_for(tasks, 256), 256, 0, s>>>(n_a, n_e, (int)L.k_m, KN, a.nchunks, a.ldb,
@@ -818,6 +827,12 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
 }
 
 }  // namespace
+
+// PCB_PF_NO_PRE=1: convert per item as for every other group (A/B experiments)
+static bool pf_pre_off() {
+  static const bool off = getenv("PCB_PF_NO_PRE") != nullptr;
+  return off;
+}
 
 int64_t pf_prep_rows(const Layer& L, const FwdGroup& g) {
   // the shift row, A images (sum rows to a 128 multiple), B images (child
@@ -887,7 +902,7 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
 #define PCB_PF_RS32 2
 #endif
     case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s,
-                                             (g.pf_pre && !em) ? prep : nullptr)
+                                             (g.pf_pre && !em && !pf_pre_off()) ? prep : nullptr)
                           : launch_pf<32, PCB_PF_RS32>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
                           : launch_pf<64, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);

@@ -629,16 +629,18 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
 // per-(super-row, sample) shift of a long-K group over the super-row's real
 // K blocks: forward: the max of the blocks' bases; child flow: the common
 // base gr = max of the parent blocks' bases (to gbase) and the shift
-// max R + (gr - base) log2 e.  CTA = super-row x 32 samples; its 8 warps
-// split the K blocks (lane = sample), combined in smem.
+// max R + (gr - base) log2 e.  CTA = super-row x 32 samples; its 32 warps
+// split the K blocks (lane = sample), combined in smem: a 128-block row is
+// one round of loads per warp.
+constexpr int GS_WARPS = 32;
 template <int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(GS_WARPS * 32)
     k_group_shift(int cap, int kc, int B, int ldb, int64_t sb_base,
                   const int32_t* __restrict__ row_off, const int32_t* __restrict__ members,
                   const int32_t* __restrict__ src_ids, const int32_t* __restrict__ real_ids,
                   const float* __restrict__ shift, const float* __restrict__ base,
                   float* __restrict__ gout, float* __restrict__ gbase) {
-  __shared__ float part[8][32];
+  __shared__ float part[GS_WARPS][33];
   const int sr = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.y * 32 + lane;
@@ -648,11 +650,11 @@ __global__ void __launch_bounds__(256)
   auto reduce = [&](const float* tab, float gr) {
     float g = PCB_NEG_INF;
     if (b < B)
-      for (int c0 = warp; c0 < cap; c0 += 8 * 4) {
+      for (int c0 = warp; c0 < cap; c0 += GS_WARPS * 4) {
         float v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int c = c0 + 8 * u;
+          const int c = c0 + GS_WARPS * u;
           const bool ok = c < cap && __ldg(real + c) != 0;
           const int64_t o = ok ? (int64_t)(__ldg(src + c) - sb_base) / kc * ldb + b : 0;
           v[u] = ok ? __ldg(tab + o) : PCB_NEG_INF;
@@ -664,8 +666,8 @@ __global__ void __launch_bounds__(256)
       }
     part[warp][lane] = g;
     __syncthreads();
-#pragma unroll
-    for (int w = 0; w < 8; ++w) g = fmaxf(g, part[w][lane]);
+#pragma unroll 8
+    for (int w = 0; w < GS_WARPS; ++w) g = fmaxf(g, part[w][lane]);
     __syncthreads();
     return g;
   };
@@ -686,7 +688,7 @@ template <int MODE>
 int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, float* gbase,
                        cudaStream_t s) {
   dim3 grid((unsigned)count, (unsigned)((a.B + 31) / 32));
-  k_group_shift<MODE><<<grid, 256, 0, s>>>(a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off,
+  k_group_shift<MODE><<<grid, GS_WARPS * 32, 0, s>>>(a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off,
                                            a.members, a.src_ids, a.real_ids, a.shift,
                                            a.vbase_in, gout, gbase);
   return check_launch();
