@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 24;
+constexpr int64_t kVersion = 25;
 
 struct Reader {
   const int64_t* p;
@@ -89,6 +89,11 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     ch.slots = r.ref();
     ch.vars = r.ref();
     ch.pids = r.ref();
+    ch.n_u = r.get();
+    ch.u_pid = r.ref();
+    ch.u_off = r.ref();
+    ch.u_slot = r.ref();
+    ch.u_var = r.ref();
     P->inputs.push_back(ch);
   }
   P->in_blocks.n = r.get();
@@ -255,6 +260,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.em_hi = r.get();
     L.em_fusable = (int)r.get();
   }
+  P->n_shared_inline = r.get();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -588,11 +594,12 @@ int run_backward(const pcb_plan* P, Step& S, cudaStream_t s, int B, int ldb,
                         d_flow_scratch, d_prod_flows, d_f_params, w);
     if (st) return st;
   }
-  bool done = false;
+  bool done = false, sdone = false;
   st = launch_input_param_flows(P, s, B, ldb, d_xT, d_theta, d_flows, d_flow_scratch, d_f_params,
-                                S.lean != 0, (S.em && P->in_inline_ok) ? &S : nullptr, &done);
+                                S.lean != 0, S.em ? &S : nullptr, &done, &sdone);
   if (st) return st;
   S.inputs_done = done;
+  S.shared_done = sdone;
   const size_t nl = P->layers.size();
   if (S.ex && nl < S.ex->flows_done.size() && S.ex->flows_done[nl] &&
       cudaEventRecord(S.ex->flows_done[nl], s) != cudaSuccess)
@@ -636,7 +643,8 @@ int run_em(const pcb_plan* P, const Step* S, cudaStream_t s, const float* d_f_pa
     st = launch_em_tiles(P, s, d_f_params, d_theta, kappa, step, d_status, own);
   }
   if (st) return st;
-  st = launch_em(P, s, d_f_params, d_theta, kappa, step, d_status, S && S->inputs_done);
+  st = launch_em(P, s, d_f_params, d_theta, kappa, step, d_status, S && S->inputs_done,
+                 S && S->shared_done);
   if (st) return st;
   if (own && P->n_em_tiles < P->n_mma_tiles) return launch_theta_to_mma(P, s, d_theta);
   return PCB_OK;

@@ -21,6 +21,10 @@ struct Ref {
 struct InputChunk {
   int64_t ncat, n;
   const int32_t *slots, *vars, *pids;
+  // shared pmfs (plan.shared_pmf_table): per unique pmf (n_u) the CSR of its
+  // inputs' value slots and variables; 0 = none
+  int64_t n_u = 0;
+  const int32_t *u_pid = nullptr, *u_off = nullptr, *u_slot = nullptr, *u_var = nullptr;
 };
 
 // Inputs staged per variable in shared memory: block b covers `count`
@@ -205,6 +209,7 @@ struct pcb_plan {
   int64_t n_em_small_noninl = 0;
   int in_inline_ok = 0;  // every staged input pmf is such a group (ncat <= 256)
   int64_t n_em_pre = 0;  // tile blocks of layers without fused EM (first in order)
+  int64_t n_shared_inline = 0;  // shared-pmf groups (last rest groups) updated by the input pass
   int64_t n_zero = 0;            // flow-row ranges zeroed before the backward pass
   const int32_t *zero_start = nullptr, *zero_len = nullptr;
 };
@@ -237,6 +242,7 @@ struct Step {
   const pcb_exec* ex = nullptr;
   std::vector<char>* em_done = nullptr;  // per layer: EM fused into its parameter flows
   bool inputs_done = false;              // the input-flow pass updated the staged pmfs
+  bool shared_done = false;              // ... and the shared pmfs
 };
 
 // kernel classes for the live per-class timing used by bench.py
@@ -317,7 +323,7 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, float* theta, const float* flows,
                              const float* flow_scratch, float* f_params, bool alias,
-                             const Step* em, bool* inline_done);
+                             const Step* em, bool* inline_done, bool* shared_done);
 // vbase_all: the whole vbase region (root_vb / root_cb are global rows)
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
                     const float* vbase_all, float* lroot);
@@ -325,7 +331,8 @@ int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* fl
                     float* prod_flows);
 int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params);
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
-              float pseudocount, float step, int32_t* status, bool skip_inline);
+              float pseudocount, float step, int32_t* status, bool skip_inline,
+              bool skip_shared = false);
 int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
                     float pseudocount, float step, int32_t* status, bool planes,
                     int64_t blk0 = 0, int64_t blk1 = -1);

@@ -1283,12 +1283,88 @@ __global__ void __launch_bounds__(IS_THREADS)
   }
 }
 
+// Shared pmfs (plan.shared_pmf_table, e.g. tied HMM emissions): one CTA per
+// pmf builds the pmf's flow histogram over every input that uses it (all
+// positions x samples) in shared memory, spreads the missing-sample flow
+// over the pmf, and stores the whole row — or, with EM inline (one-process
+// lean steps), normalises, blends and stores theta directly (em.py:58-94
+// for that group; f_params is then not written).
+constexpr int SP_THREADS = 1024;
+__global__ void __launch_bounds__(SP_THREADS)
+    k_input_flow_shared(int ncat, int B, int ldb, const int32_t* __restrict__ u_pid,
+                        const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
+                        const int32_t* __restrict__ u_var, const int32_t* __restrict__ xT,
+                        const float* __restrict__ flows, float* __restrict__ theta,
+                        float* __restrict__ f_params, int em, float kappa, float step,
+                        int32_t* __restrict__ status) {
+  extern __shared__ float hist[];
+  __shared__ float red[SP_THREADS / 32];
+  const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t pid = __ldg(u_pid + u);
+  for (int c = tid; c < ncat; c += SP_THREADS) hist[c] = 0.f;
+  __syncthreads();
+  float miss = 0.f;
+  const int e0 = __ldg(u_off + u), e1 = __ldg(u_off + u + 1);
+  for (int e = e0; e < e1; ++e) {
+    const int32_t* xr = xT + (int64_t)__ldg(u_var + e) * ldb;
+    const float* fr = flows + (int64_t)__ldg(u_slot + e) * ldb;
+    for (int b = tid; b < B; b += SP_THREADS) {
+      const float f = fr[b];
+      if (f == 0.f) continue;
+      const int x = __ldg(xr + b);
+      if (x >= 0)
+        atomicAdd(hist + x, f);
+      else
+        miss += f;
+    }
+  }
+  auto block_sum = [&](float v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll 8
+    for (int w = 0; w < SP_THREADS / 32; ++w) t += red[w];
+    return t;
+  };
+  miss = block_sum(miss);
+  float* th = theta + pid;
+  if (!em) {
+    for (int c = tid; c < ncat; c += SP_THREADS)
+      f_params[pid + c] = hist[c] + (miss != 0.f ? miss * __ldg(th + c) : 0.f);
+    return;
+  }
+  // inline EM: F = flows (+ missing spread over theta), total sum(F + kappa)
+  float tot = 0.f;
+  for (int c = tid; c < ncat; c += SP_THREADS) {
+    const float F = hist[c] + (miss != 0.f ? miss * th[c] : 0.f);
+    hist[c] = F;
+    tot += F + kappa;
+  }
+  tot = block_sum(tot);
+  if (!(tot > 0.f)) return;  // uninformative group keeps theta (em.py:67-80)
+  const float inv = 1.f / tot;
+  int bad = 0;
+  for (int c = tid; c < ncat; c += SP_THREADS) {
+    const float nv = (hist[c] + kappa) * inv;
+    const float t = (step >= 1.f) ? nv : ((1.f - step) * th[c] + step * nv);
+    bad += !isfinite(t);
+    th[c] = t;
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if (tid == 0) atomicAdd(status, 1);
+  if (lane == 0 && bad) atomicAdd(status + 1, bad);
+}
+
 int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
                              const int32_t* xT, float* theta, const float* flows,
                              const float* flow_scratch, float* f_params, bool alias,
-                             const Step* em, bool* inline_done) {
+                             const Step* em, bool* inline_done, bool* shared_done) {
   ProfScope prof_(KC_INPUT_FLOW, s);
   *inline_done = false;
+  *shared_done = false;
+  const Step* em_staged = (em && p->in_inline_ok) ? em : nullptr;
   const InBlocks& ib = p->in_blocks;
   const int32_t* arow = (alias && p->leaf_alias) ? ib.alias_row : nullptr;
   // sorted (atomic-free) kernel when its shared-memory slots fit, else the
@@ -1300,10 +1376,11 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
     if (ensure_smem((const void*)k_input_flow_sorted, (int)sorted_bytes, attr_s)) return PCB_CUDA;
     k_input_flow_sorted<<<(unsigned)ib.n, IS_THREADS, (size_t)sorted_bytes, s>>>(
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
-        arow, ib.alias_dir, flow_scratch, f_params, em ? theta : nullptr,
-        em ? em->kappa : 0.f, em ? em->step : 1.f, em ? em->status : nullptr);
+        arow, ib.alias_dir, flow_scratch, f_params, em_staged ? theta : nullptr,
+        em_staged ? em_staged->kappa : 0.f, em_staged ? em_staged->step : 1.f,
+        em_staged ? em_staged->status : nullptr);
     if (check_launch()) return PCB_CUDA;
-    *inline_done = em != nullptr;
+    *inline_done = em_staged != nullptr;
   } else if (ib.n) {
     const int bytes = (int)ib.max_elems * 4;
     static int attr[kMaxDev] = {};
@@ -1313,13 +1390,26 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
         arow, ib.alias_dir, flow_scratch, f_params);
     if (check_launch()) return PCB_CUDA;
   }
+  const bool em_shared = em && p->n_shared_inline > 0;
   for (auto& c : p->inputs) {
     if (!c.n) continue;
+    if (c.n_u) {
+      const int bytes = (int)c.ncat * 4;
+      static int attr_sp[kMaxDev] = {};
+      if (ensure_smem((const void*)k_input_flow_shared, bytes, attr_sp)) return PCB_CUDA;
+      k_input_flow_shared<<<(unsigned)c.n_u, SP_THREADS, bytes, s>>>(
+          (int)c.ncat, B, ldb, c.u_pid, c.u_off, c.u_slot, c.u_var, xT, flows, theta, f_params,
+          em_shared ? 1 : 0, em ? em->kappa : 0.f, em ? em->step : 1.f,
+          em ? em->status : nullptr);
+      if (check_launch()) return PCB_CUDA;
+      continue;
+    }
     k_input_param_flow<<<grid_for(c.n * 32, 256), 256, 0, s>>>(c.n, (int)c.ncat, B, ldb, c.slots,
                                                                c.vars, c.pids, xT, theta, flows,
                                                                f_params);
     if (check_launch()) return PCB_CUDA;
   }
+  *shared_done = em_shared;
   return PCB_OK;
 }
 
@@ -1512,9 +1602,11 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
-              float pseudocount, float step, int32_t* status, bool skip_inline) {
+              float pseudocount, float step, int32_t* status, bool skip_inline,
+              bool skip_shared) {
   ProfScope prof_(KC_EM, s);
-  const int64_t nb = p->n_em_rest - p->n_em_small;
+  // shared-pmf groups (the last rest groups) were updated by the input pass
+  const int64_t nb = p->n_em_rest - p->n_em_small - (skip_shared ? p->n_shared_inline : 0);
   // the staged inputs' pmf groups (last among the small ones) were updated
   // by the input-flow pass (inline EM)
   const int64_t ns = skip_inline ? p->n_em_small_noninl : p->n_em_small;

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 24
+VERSION = 25
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -184,6 +184,27 @@ def theta_contig_flags(slab_ids, offs, mem, plane: int) -> np.ndarray:
 
 
 IN_BLOCK_ELEMS = 16384   # pmf entries staged in shared memory per input block (64 KB)
+SHARED_PMF_MAX = 56000   # categories of a shared pmf histogrammed in shared memory (224 KB)
+
+
+def shared_pmf_table(compiled, ncat, slots, vars_, pids):
+    """Generic input chunk whose pmfs are each used by several inputs (tied
+    HMM emissions: one pmf per hidden state, shared by every position) and by
+    no input outside the chunk: per unique pmf (ascending start) the CSR of
+    its inputs' value slots and variables — the input-flow pass then builds
+    each pmf's flow histogram in shared memory (one CTA per pmf) and stores
+    the whole row, instead of one global atomic per (input, sample).
+    Returns None when the chunk does not qualify."""
+    if ncat > SHARED_PMF_MAX or pids.size == 0:
+        return None
+    all_pids = np.concatenate([ch.param_ids for ch in compiled.input_layer])
+    uniq, counts = np.unique(all_pids, return_counts=True)
+    u, inv, cnt = np.unique(pids, return_inverse=True, return_counts=True)
+    if u.size == pids.size or not np.array_equal(counts[np.searchsorted(uniq, u)], cnt):
+        return None
+    order = np.argsort(inv, kind="stable")
+    off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+    return {"pid": u.astype(np.int64), "off": off, "slot": slots[order], "var": vars_[order]}
 
 
 def input_blocks(compiled):
@@ -699,11 +720,18 @@ def build_program(compiled, *, tensor_cores: bool = True):
     blocks, leftovers = input_blocks(c)
     alias_row, alias_dir, alias_pad = leaf_alias(c, blocks, push_count)
     prog.append(len(leftovers))
+    shared_pids = {}  # pmf start -> ncat of the shared-pmf chunks
     for ncat, slots, vars_, pids in leftovers:
         prog += [ncat, int(slots.size)]
         ref(slots)
         ref(vars_)
         ref(pids)
+        sp = shared_pmf_table(c, ncat, slots, vars_, pids)
+        prog.append(0 if sp is None else int(sp["pid"].size))
+        for key in ("pid", "off", "slot", "var"):
+            ref(sp[key] if sp is not None else np.zeros(0, np.int64))
+        if sp is not None:
+            shared_pids.update({int(q): int(ncat) for q in sp["pid"].tolist()})
     nb = int(blocks["var"].size)
     prog.append(nb)
     for key in ("var", "ncat", "slot0", "count", "pid_off", "pids"):
@@ -981,12 +1009,20 @@ def build_program(compiled, *, tensor_cores: bool = True):
     inl = np.array([bool(contig[g] >= 0 and in_pmf.get(int(contig[g])) == int(sz) and sz <= 256)
                     for g, sz in zip(rest.tolist(), gsize.tolist())], dtype=bool)
     small = gsize < EM_BIG
-    rest_o = np.concatenate([rest[small & ~inl], rest[small & inl], rest[~small]]).astype(np.int64)
-    n_small_noninl = int((small & ~inl).sum())
+    # groups that are exactly a shared pmf (shared_pmf_table) go last: the
+    # shared-pmf input-flow pass updates them inline
+    sinl = np.array([bool(contig[g] >= 0 and shared_pids.get(int(contig[g])) == int(sz))
+                     for g, sz in zip(rest.tolist(), gsize.tolist())], dtype=bool)
+    inl = inl & ~sinl
+    n_shared_inline = int(sinl.sum())
+    shared_inline_ok = bool(shared_pids) and n_shared_inline == len(shared_pids)
+    rest_o = np.concatenate([rest[small & ~inl & ~sinl], rest[small & inl],
+                             rest[~small & ~sinl], rest[sinl]]).astype(np.int64)
+    n_small_noninl = int((small & ~inl & ~sinl).sum())
     in_inline_ok = bool(nb) and int((small & inl).sum()) == int(blocks["pids"].size)
     rest = rest_o
     prog.append(int(rest.size))
-    prog.append(int(small.sum()))
+    prog.append(int((small & ~sinl).sum()))
     ref(rest)
     ref(contig[rest] if rest.size else np.zeros(0, np.int64))
     prog.append(int(pf_optional))
@@ -997,6 +1033,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
     prog.append(int(n_em_pre))
     for (lo, hi), fz in zip(em_ranges, em_fusable):
         prog += [int(lo), int(hi), int(fz)]
+    # shared-pmf groups (ordered last) updated inline by the input-flow pass
+    prog += [n_shared_inline if shared_inline_ok else 0]
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,
@@ -1004,7 +1042,8 @@ def build_program(compiled, *, tensor_cores: bool = True):
             "em_fused_layer_ids": [li for li, f in enumerate(em_fusable) if f], "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total, "slot_vb": slot_vb,
-            "layer_flow_ranges": [tuple(int(v) for v in r) for r in layer_range]}
+            "layer_flow_ranges": [tuple(int(v) for v in r) for r in layer_range],
+            "shared_pmfs": len(shared_pids), "shared_pmf_inline_em": shared_inline_ok}
     return np.asarray(prog, dtype=np.int64), blob.array(), info
 
 

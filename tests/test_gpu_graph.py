@@ -166,7 +166,7 @@ def _lean_step_vs_oracle(c, x, pseudocount=1e-4, step=0.2):
     apply_theta(c, theta0)
 
 
-@pytest.mark.parametrize("kind", ["pd", "ratspn", "hmm_untied", "hclt16"])
+@pytest.mark.parametrize("kind", ["pd", "ratspn", "hmm_untied", "hmm_tied", "hclt16"])
 def test_lean_train_step_other_structures(kind):
     """The lean / inline-EM training step on every generator family: each
     restructuring (leaf alias, fused push + ratio, side-stream parameter
@@ -185,6 +185,15 @@ def test_lean_train_step_other_structures(kind):
                                              num_categories=8, num_repetitions=6, seed=3))
         c = compile_circuit(g, CompileConfig(block_size=32))
         x = rng.integers(0, 8, size=(200, 16))
+    elif kind == "hmm_tied":
+        # emission pmfs shared by every position: the shared-pmf input-flow
+        # pass builds their histograms in shared memory and applies EM inline
+        g = S.build_structure(S.StructureConfig(kind="hmm", seq_len=6, hidden_dim=256,
+                                                vocab_size=300, seed=5, tied=True))
+        c = compile_circuit(g, CompileConfig(block_size=32))
+        from paper_2406_00766_b200.runtime.plan import device_plan
+        assert device_plan(c).info["shared_pmf_inline_em"]
+        x = rng.integers(0, 300, size=(96, 6))
     elif kind == "hmm_untied":
         g = S.build_structure(S.StructureConfig(kind="hmm", seq_len=6, hidden_dim=64,
                                                 vocab_size=30, seed=5, tied=False))
