@@ -116,6 +116,7 @@ __global__ void k_input_fwd(int64_t n, int B, int ldb, const int32_t* __restrict
 // rows are written coalesced along the batch.  Replaces 4-byte gathers that
 // each pull a 32-byte sector of a pmf table far larger than L2.
 constexpr int IN_THREADS = 512;
+constexpr int SP_THREADS = 1024;  // shared-pmf input kernels
 
 __global__ void __launch_bounds__(IN_THREADS)
     k_input_fwd_block(int B, int ldb, const int32_t* __restrict__ bvar,
@@ -208,6 +209,41 @@ __global__ void __launch_bounds__(IN_THREADS)
   }
 }
 
+// Shared pmfs (plan.shared_pmf_table): one CTA per pmf stages its log-pmf in
+// shared memory once (a coalesced row read) and serves every (input,
+// sample) of the inputs that use it from there — instead of one random
+// 32-byte-sector gather of the pmf table per (input, sample).
+__global__ void __launch_bounds__(SP_THREADS)
+    k_input_fwd_shared(int ncat, int B, int ldb, const int32_t* __restrict__ u_pid,
+                       const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
+                       const int32_t* __restrict__ u_var, const int32_t* __restrict__ xT,
+                       const float* __restrict__ theta, float* __restrict__ values) {
+  extern __shared__ float tbl[];
+  const int u = blockIdx.x, tid = threadIdx.x;
+  const float* th = theta + __ldg(u_pid + u);
+  for (int c = tid; c < ncat; c += SP_THREADS) tbl[c] = __logf(__ldg(th + c));
+  __syncthreads();
+  const int e0 = __ldg(u_off + u), e1 = __ldg(u_off + u + 1);
+  const int n_items = (e1 - e0) * B;
+  for (int t0 = tid; t0 < n_items; t0 += 4 * SP_THREADS) {
+    int x[4];
+    int64_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k * SP_THREADS;
+      o[k] = -1;
+      if (t < n_items) {
+        const int e = e0 + t / B, b = t - (t / B) * B;
+        x[k] = __ldg(xT + (int64_t)__ldg(u_var + e) * ldb + b);
+        o[k] = (int64_t)__ldg(u_slot + e) * ldb + b;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (o[k] >= 0) values[o[k]] = x[k] < 0 ? 0.f : tbl[x[k]];
+  }
+}
+
 int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const int32_t* xT,
                      const float* theta, float* values, float* scratch_all, float* pbase_all,
                      bool alias) {
@@ -230,6 +266,15 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
   for (auto& c : p->inputs) {
     int64_t total = c.n * B;
     if (!total) continue;
+    if (c.n_u) {
+      const int bytes = (int)c.ncat * 4;
+      static int attr_sp[kMaxDev] = {};
+      if (ensure_smem((const void*)k_input_fwd_shared, bytes, attr_sp)) return PCB_CUDA;
+      k_input_fwd_shared<<<(unsigned)c.n_u, SP_THREADS, bytes, s>>>(
+          (int)c.ncat, B, ldb, c.u_pid, c.u_off, c.u_slot, c.u_var, xT, theta, values);
+      if (check_launch()) return PCB_CUDA;
+      continue;
+    }
     k_input_fwd<<<grid_for(total, 256), 256, 0, s>>>(c.n, B, ldb, c.slots, c.vars, c.pids, xT,
                                                       theta, values);
     if (check_launch()) return PCB_CUDA;
@@ -1289,7 +1334,6 @@ __global__ void __launch_bounds__(IS_THREADS)
 // over the pmf, and stores the whole row — or, with EM inline (one-process
 // lean steps), normalises, blends and stores theta directly (em.py:58-94
 // for that group; f_params is then not written).
-constexpr int SP_THREADS = 1024;
 __global__ void __launch_bounds__(SP_THREADS)
     k_input_flow_shared(int ncat, int B, int ldb, const int32_t* __restrict__ u_pid,
                         const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
@@ -1305,17 +1349,30 @@ __global__ void __launch_bounds__(SP_THREADS)
   __syncthreads();
   float miss = 0.f;
   const int e0 = __ldg(u_off + u), e1 = __ldg(u_off + u + 1);
-  for (int e = e0; e < e1; ++e) {
-    const int32_t* xr = xT + (int64_t)__ldg(u_var + e) * ldb;
-    const float* fr = flows + (int64_t)__ldg(u_slot + e) * ldb;
-    for (int b = tid; b < B; b += SP_THREADS) {
-      const float f = fr[b];
-      if (f == 0.f) continue;
-      const int x = __ldg(xr + b);
-      if (x >= 0)
-        atomicAdd(hist + x, f);
+  // every (input, sample) pair of the pmf spread over the whole CTA, four
+  // pairs' loads in flight per thread before their shared-memory atomics
+  const int n_items = (e1 - e0) * B;
+  for (int t0 = tid; t0 < n_items; t0 += 4 * SP_THREADS) {
+    float f[4];
+    int x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k * SP_THREADS;
+      f[k] = 0.f;
+      x[k] = 0;
+      if (t < n_items) {
+        const int e = e0 + t / B, b = t - (t / B) * B;
+        f[k] = flows[(int64_t)__ldg(u_slot + e) * ldb + b];
+        x[k] = __ldg(xT + (int64_t)__ldg(u_var + e) * ldb + b);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (f[k] == 0.f) continue;
+      if (x[k] >= 0)
+        atomicAdd(hist + x[k], f[k]);
       else
-        miss += f;
+        miss += f[k];
     }
   }
   auto block_sum = [&](float v) {
