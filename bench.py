@@ -338,6 +338,58 @@ def run_reference(args, w):
 
 
 # ---------------------------------------------------------------- GPU arm
+def secondary(name, args, dev, world, rank, graphed):
+    """Another BASELINE config measured in the same run (device-resident
+    steps and a 60k-sample train() epoch from host data), reported under
+    ``secondary`` of the JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_00766_b200.train import TrainConfig, cached_step, shard_span, train
+    w = WORKLOADS[name]
+    t0 = time.time()
+    c = build_circuit(w)
+    compile_s = time.time() - t0
+    G = w["batch"]
+    lo, hi = shard_span(G, rank, world)
+    B = hi - lo
+    xs = [torch.from_numpy(h).to(dev) for h in synthetic_batches(c, w, B, 2, seed=rank)]
+    ts = cached_step(c, B, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, device=dev,
+                     graph=graphed)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        ts.run(xs[i % 2])
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        ts.run(xs[i % 2])
+    e1.record()
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    data = synthetic_batches(c, w, EPOCH, 1, seed=11)[0]
+    cfg = TrainConfig(epochs=1, batch_size=G, mode="mini", step_size=STEP_SIZE,
+                      pseudocount=PSEUDOCOUNT, seed=0)
+    train(c, data[: 2 * G + EPOCH % G], cfg, device=dev, graph=graphed)
+    barrier()
+    res = train(c, data, cfg, device=dev, graph=graphed)
+    t = torch.tensor([res.epoch_seconds[0]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ep = float(t.item())
+    return {"desc": w["desc"], "edges": c.num_edges, "theta_size": c.theta_size,
+            "global_batch": G, "value": G / (ms / 1000.0), "unit": "samples/s",
+            "ms_per_step": ms, "e2e": {"value": EPOCH / ep, "unit": "samples/s",
+                                       "sec_per_epoch": ep}, "compile_s": compile_s}
+
+
 def run_ours(args, w):
     import torch
     import torch.distributed as dist
@@ -459,6 +511,13 @@ def run_ours(args, w):
                   w["batch"] * world, "how": "one 60k-sample epoch through train(mode='full')"
                                              " from host data, one EM per epoch"}
 
+    # other BASELINE configs in the same run (every rank takes part)
+    sec = {}
+    for name in [n for n in args.secondary.split(",") if n and n != args.workload]:
+        try:
+            sec[name] = secondary(name, args, dev, world, rank, graphed)
+        except Exception as e:  # a secondary never sinks the headline line
+            sec[name] = {"error": f"{type(e).__name__}: {e}"}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -566,6 +625,8 @@ def run_ours(args, w):
         "cpu_baseline": cpu,
         "full_batch_em": full_batch,
     }
+    if sec:
+        line["secondary"] = sec
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -580,6 +641,9 @@ def main():
     ap.add_argument("--workload", default="hclt256", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly")
+    ap.add_argument("--secondary", default="hclt16",
+                    help="comma-separated other workloads measured in the same run "
+                         "(value + train() epoch) under 'secondary', e.g. hclt16,pd256,ratspn")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's batch sharded over the GPUs (north_star); "
                          "weak: the config's batch per GPU")

@@ -15,9 +15,11 @@ from pathlib import Path
 
 CLASSES = [
     ("k_input_fwd", "input_fwd"), ("k_prod_block", "prod_eval"),
-    ("k_sum_ws<0", "sum_fwd_tc"), ("k_sum_fwd_tc", "sum_fwd_tc"), ("k_sum_fwd_simt", "sum_fwd_simt"),
-    ("k_param_flow", "param_flow"), ("k_ratio", "param_flow"),
-    ("k_sum_ws<1", "child_flow"), ("k_child_flow", "child_flow"),
+    ("k_sum_ws<0", "sum_fwd_tc"), ("k_group_shift<0", "sum_fwd_tc"),
+    ("k_sum_fwd_simt", "sum_fwd_simt"),
+    ("k_param_flow", "param_flow"), ("k_ratio", "param_flow"), ("k_pf_", "param_flow"),
+    ("k_sum_ws<1", "child_flow"), ("k_group_shift<1", "child_flow"),
+    ("k_child_flow", "child_flow"),
     ("k_flow_push", "accum_push"), ("k_push_ratio", "accum_push"), ("k_input_flow", "input_flow"), ("k_input_param_flow", "input_flow"),
     ("k_replica", "replica"), ("k_em", "em"), ("k_theta_to_mma", "em"),
 ]
