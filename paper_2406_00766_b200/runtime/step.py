@@ -170,7 +170,34 @@ class TrainStep:
             self.accumulate.copy_(saved_acc)
         self.graph = g
 
-    def run(self, x):
+    def validate(self, x) -> None:
+        """Shape / dtype / device checks and the category check of
+        ``engine.py:36-52`` on the device (``pcb_check_batch``): FormatError.
+        ``run`` does not validate (the graph replays without host syncs;
+        ``train()`` validates every batch before its step)."""
+        import torch
+        from ..errors import FormatError
+        if not isinstance(x, torch.Tensor) or x.shape != (self.B, self.c.num_vars) or \
+                x.dtype != torch.int32:
+            raise FormatError(f"a step batch is an int32 tensor of shape ({self.B}, "
+                              f"{self.c.num_vars})")
+        xd = x.to(self.dev)
+        b = self.bufs
+        s = _lib.stream_handle()
+        _lib.call("pcb_transpose_batch_i32", self.plan.handle, s, self.B, b.ldb, xd.data_ptr(),
+                  b.xT.data_ptr())
+        bad = self.plan.status[3:4]
+        bad.zero_()
+        _lib.call("pcb_check_batch", self.plan.handle, s, self.B, b.ldb, b.xT.data_ptr(),
+                  bad.data_ptr())
+        if int(bad.item()):
+            raise FormatError("category values must lie in [0, ncat) or be -1 for missing")
+
+    def run(self, x, *, validate: bool = False):
+        """One step on batch ``x``; ``validate=True`` checks it first (a
+        host synchronisation)."""
+        if validate:
+            self.validate(x)
         self.c.mark_theta_on_device(self.plan)
         if self.graph is None:
             return self._eager(x)

@@ -215,3 +215,21 @@ def test_f_params_contract():
     fp = _np(b.f_params)
     assert rel_err(fp[:c.theta_size], rb.f_params[:c.theta_size]) < RTOL
     assert not fp[c.theta_size:].any()
+
+
+def test_train_step_validate():
+    """TrainStep.run(validate=True) raises FormatError on a bad batch before
+    any kernel reads it (ADVICE: out-of-range categories would index the
+    staged pmf tables out of bounds)."""
+    import torch
+    from paper_2406_00766_b200.errors import FormatError
+    from paper_2406_00766_b200.runtime.step import TrainStep
+    g, c = _hclt(nv=6, h=16, ncat=4, k=16)
+    ts = TrainStep(c, 8, pseudocount=1e-3, step_size=0.1, graph=True)
+    good = torch.zeros((8, 6), dtype=torch.int32, device="cuda")
+    ts.run(good, validate=True)
+    for bad in (torch.full((8, 6), 4, dtype=torch.int32, device="cuda"),
+                torch.zeros((8, 5), dtype=torch.int32, device="cuda"),
+                torch.zeros((8, 6), dtype=torch.int64, device="cuda")):
+        with pytest.raises(FormatError):
+            ts.run(bad, validate=True)
