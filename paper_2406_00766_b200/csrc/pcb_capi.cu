@@ -494,8 +494,9 @@ int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B,
   // EM fused into the parameter-flow epilogue (one-process lean step with
   // EM): the layer's theta tiles and planes are rewritten there, so its
   // parameter flows run after its child flows (which read the planes)
+  static const bool em_fuse_off = getenv("PCB_NO_EM_FUSE") != nullptr;  // A/B experiments
   const bool em_fuse = S.em && S.em_done && L.em_fusable && fused && L.pre_ratio && P->mma &&
-                       tc && pf_layer_stores(P, L, B);
+                       tc && pf_layer_stores(P, L, B) && !em_fuse_off;
   if (em_fuse) {
     st = child_flows(P, L, s, B, ldb, theta, values, flows, scratch, flow_scratch, ratio, rmax,
                      tc, w);

@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __shared__ __align__(16) float cs[C::kRS][PF_KS];
   __shared__ int cols_p[C::kCPG];
   __shared__ int cols_w[PF_NEPI][C::kCPG];  // epilogue warps' column lists
-  __shared__ float em_wt[4][32 * 33];  // fused EM: a warp's updated 32 x 32 tile
+  __shared__ float em_wt[4][32 * 33];  // fused EM: a warp pair's updated 32 x 32 tile
+  __shared__ float em_tot[4][2][32];   // fused EM: the pair's partial row totals
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
   uint8_t* ops = PRE ? smem : smem + C::kRS * C::kRaw;
@@ -494,44 +495,43 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         }
       };
       float th[16], thn[16];
-      const bool em_idle = KN == 32 && a.em && h == 1;  // fused EM: rows on the first four warps
-      if (live && !em_idle && (a.em ? 0 : h * 16) < ncol * KN)
-        load_th(tile_of(a.em ? 0 : h * 16), thn);
+      if (live && h * 16 < ncol * KN) load_th(tile_of(h * 16), thn);
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(as * PF_N) + ((uint32_t)(q4 * 32) << 16);
-      if (em_idle) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
-        ++acc_u;
-        continue;
-      }
       if constexpr (KN == 32) {
         if (a.em) {
+          // Fused EM, the two warps of a lane quarter (same 32 rows) split
+          // the columns in 16-wide chunks as in the plain epilogue and meet
+          // at a pair barrier (ids 2..5) for the row total and each 32 x 32
+          // product-major tile.
+          auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + q4) : "memory"); };
           // pass 1: the row's group total sum(F + k) over all its columns
           float tot = 0.f;
-          for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+          for (int c0 = h * 16; c0 < ncol * KN; c0 += 32) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) th[i] = thn[i];
-            if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
+            if (live && c0 + 32 < ncol * KN) load_th(tile_of(c0 + 32), thn);
             float v[16];
             tmem_ld16(tbase + c0, v);
             if (!live) continue;
 #pragma unroll
             for (int i = 0; i < 16; ++i) tot += ((th[i] != 0.f) ? th[i] * v[i] : 0.f) + a.kappa;
           }
+          em_tot[q4][h][lane] = tot;
+          pair_bar();
+          tot = em_tot[q4][0][lane] + em_tot[q4][1][lane];  // same order on both warps
           const bool inf_row = live && tot > 0.f;
           const float inv = inf_row ? 1.f / tot : 0.f;
-          em_inf += inf_row;
+          if (h == 0) em_inf += inf_row;
           // pass 2: blend, store theta, pack the sum-major planes; stage the
           // tile for the product-major planes
-          if (live) load_th(tile_of(0), thn);
-          float* wt = em_wt[warp - PF_EPI0];
-          for (int c0 = 0; c0 < ncol * KN; c0 += 16) {
+          if (live) load_th(tile_of(h * 16), thn);
+          float* wt = em_wt[q4];
+          for (int c0 = h * 16; c0 < ncol * KN; c0 += 32) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) th[i] = thn[i];
-            if (live && c0 + 16 < ncol * KN) load_th(tile_of(c0 + 16), thn);
+            if (live && c0 + 32 < ncol * KN) load_th(tile_of(c0 + 32), thn);
             float v[16];
             tmem_ld16(tbase + c0, v);
             const int c = cols[c0 / KN];
@@ -572,25 +572,23 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) wt[lane * 33 + j0 + i] = nt[i];
             }
-            if (j0 + 16 == KN) {  // the warp's 32 x 32 tile is complete
-              __syncwarp();
-              if (live) {
-                __nv_bfloat16* cpl = a.mma + 2 * a.plane + __ldg(a.slab_c + rowbase + c);
+            pair_bar();  // the pair's 32 x 32 tile is staged
+            if (live) {  // k_m == 32: a lane quarter is live or dead as a whole
+              __nv_bfloat16* cpl = a.mma + 2 * a.plane + __ldg(a.slab_c + rowbase + c);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const int q = lane + 32 * k, j = q >> 2, g8 = (q & 3) * 8;
-                  float e8[8];
+              for (int k = 2 * h; k < 2 * h + 2; ++k) {
+                const int q = lane + 32 * k, j = q >> 2, g8 = (q & 3) * 8;
+                float e8[8];
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) e8[e] = wt[(g8 + e) * 33 + j];
-                  uint4 hi, lo;
-                  split_pack8(e8, hi, lo);
-                  uint8_t* dst = reinterpret_cast<uint8_t*>(cpl) + (uint32_t)tile_off(j, g8, KN) * 2u;
-                  *reinterpret_cast<uint4*>(dst) = hi;
-                  *reinterpret_cast<uint4*>(dst + a.plane * 2) = lo;
-                }
+                for (int e = 0; e < 8; ++e) e8[e] = wt[(g8 + e) * 33 + j];
+                uint4 hi, lo;
+                split_pack8(e8, hi, lo);
+                uint8_t* dst = reinterpret_cast<uint8_t*>(cpl) + (uint32_t)tile_off(j, g8, KN) * 2u;
+                *reinterpret_cast<uint4*>(dst) = hi;
+                *reinterpret_cast<uint4*>(dst + a.plane * 2) = lo;
               }
-              __syncwarp();
             }
+            pair_bar();  // the tile is read before the next one is staged
           }
           tc_fence_before();
           __syncwarp();
