@@ -39,7 +39,29 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+HOST_SRC = CSRC / "host" / "pcc_compile.cpp"
+HOST_LIB = OUT_DIR / "libpcirc_host.so"
+
+
+def build_host(force: bool = False) -> Path:
+    """The native host-compiler core (plain C++17, std::thread)."""
+    if not force and HOST_LIB.exists() and HOST_LIB.stat().st_mtime >= HOST_SRC.stat().st_mtime:
+        return HOST_LIB
+    OUT_DIR.mkdir(exist_ok=True)
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    tmp = HOST_LIB.with_suffix(".so.tmp")
+    cmd = [cxx, "-O3", "-std=c++17", "-fPIC", "-shared", "-Wall", "-o", str(tmp), str(HOST_SRC),
+           "-lpthread"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("g++ failed on pcc_compile.cpp")
+    os.replace(tmp, HOST_LIB)
+    return HOST_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_host(force)
     if not force and not _stale():
         return LIB
     OUT_DIR.mkdir(exist_ok=True)

@@ -19,14 +19,16 @@ committed golden fixtures.
 from __future__ import annotations
 
 import hashlib
+import threading
 from dataclasses import dataclass
 
 import numpy as np
 
 from ..errors import CircuitValidationError, UsageError
 from ..graph import KIND_INPUT, KIND_PRODUCT, KIND_SUM, CircuitGraph
+from . import _native
 from ._rows import group_matrix_rows, group_rows, row_hashes
-from .blocks import PAD, detect_blocks_csr
+from .blocks import PAD, BlockLayout, detect_blocks_csr
 from .ir import (BackwardGroupIR, CompiledCircuit, FlowPushIR, ForwardGroupIR,
                  GraphLayer, InputLayerIR, LayerReport, ProductEvalIR, SumLayerIR)
 from .partition import partition_layer
@@ -114,7 +116,11 @@ class _Layer:
     """Per-layer working set (pass 1 -> pass 3)."""
 
     __slots__ = ("depth", "sids", "e_sum", "e_key", "e_slot", "off", "lo",
-                 "pair_codes", "pair_theta", "pair_sb", "pair_pb", "n_pb", "blk_slots")
+                 "pair_codes", "pair_theta", "pair_sb", "pair_pb", "n_pb", "blk_slots",
+                 "e_child", "nat")
+
+    def __init__(self):
+        self.e_sum = self.e_child = self.nat = None
 
 
 def _collect_layers(g: CircuitGraph, depth: np.ndarray, kinds: np.ndarray):
@@ -157,6 +163,61 @@ def _collect_layers(g: CircuitGraph, depth: np.ndarray, kinds: np.ndarray):
     return layers
 
 
+def _collect_layers_native(g: CircuitGraph, depth: np.ndarray, kinds: np.ndarray):
+    """``_collect_layers`` with the per-edge arrays written by one native pass
+    per layer (segments in id order, so sum ids ascend)."""
+    nat = _native.lib()
+    by_depth: dict[int, list] = {}
+    for s in g.segments:
+        if s.kind != KIND_SUM:
+            continue
+        d = depth[s.start:s.stop]
+        if s.count and d.min() == d.max():
+            by_depth.setdefault(int(d[0]), []).append((s, None))
+            continue
+        for dv in np.unique(d).tolist():
+            by_depth.setdefault(dv, []).append((s, np.flatnonzero(d == dv).astype(np.int64)))
+    kinds8 = np.ascontiguousarray(kinds, dtype=np.int8)
+    layers = []
+    for dv in sorted(by_depth):
+        parts = sorted(by_depth[dv], key=lambda t: t[0].start)
+        chs = [_native.i64(s.children) for s, _ in parts]
+        sls = [_native.i64(s.slots) for s, _ in parts]
+        fan = np.array([s.fan_in for s, _ in parts], dtype=np.int64)
+        nrows = np.array([s.count if r is None else r.size for s, r in parts], dtype=np.int64)
+        rows = [r for _, r in parts]
+        L = _Layer()
+        L.depth = dv
+        L.sids = np.concatenate([np.arange(s.start, s.stop, dtype=np.int64) if r is None
+                                 else s.start + r for s, r in parts])
+        counts = np.repeat(fan, nrows)
+        L.off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        E = int(L.off[-1])
+        starts = np.array([s.start for s, _ in parts], dtype=np.int64)
+        L.e_sum, L.e_child, L.e_key, L.e_slot = (np.empty(E, np.int64) for _ in range(4))
+        nat.pcc_gather_layer(len(parts), _native.ptr_array(chs), _native.ptr_array(sls),
+                             _native.ptr(fan), _native.ptr_array(rows), _native.ptr(nrows),
+                             _native.ptr(starts), _native.ptr(kinds8), KIND_PRODUCT, _VKEY_BASE,
+                             _native.ptr(L.e_sum), _native.ptr(L.e_child), _native.ptr(L.e_key),
+                             _native.ptr(L.e_slot))
+        layers.append(L)
+    return layers
+
+
+def _blocks_native(L, cfg) -> BlockLayout:
+    """``detect_blocks_csr`` through the native layer object (kept on ``L`` for
+    the tile pass)."""
+    z = np.zeros(0, dtype=np.int64)
+    if L.sids.size == 0:
+        return BlockLayout(1, 1, False, np.zeros((0, 1), np.int64), np.zeros((0, 1), np.int64),
+                           z, np.zeros(1, np.int64), z, z, z, z, z, z, 0.0, 0.0)
+    L.nat = _native.Layer(L.sids, L.e_key, L.off)
+    km, kn, dem, spad, ppad, a = L.nat.blocks(cfg.k_m, cfg.k_n, cfg.demote_threshold)
+    return BlockLayout(km, kn, dem, a["smat"], a["pmat"], a["cb_flat"], a["cb_off"],
+                       a["sum_keys"], a["sum_blk"], a["sum_off"], a["prod_keys"],
+                       a["prod_blk"], a["prod_off"], spad, ppad)
+
+
 def _lookup(keys_sorted, vals_a, vals_b, query):
     idx = np.searchsorted(keys_sorted, query)
     return vals_a[idx], vals_b[idx]
@@ -196,7 +257,16 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
     if validate:
         g.validate().raise_if_invalid()
     g.freeze()
+    if _native.lib() is not None:
+        try:
+            return _compile(g, cfg, True)
+        except _native.NativeError:
+            pass  # the numpy path raises the reference's exact error
+    return _compile(g, cfg, False)
 
+
+def _compile(g: CircuitGraph, cfg: CompileConfig, native: bool) -> CompiledCircuit:
+    ghash = _hash_async(g) if native else (lambda: graph_hash(g, False))
     params = g.params
     depth = g.depths()
     kinds = g.node_kinds()
@@ -205,10 +275,15 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
     n_nodes = g.num_nodes
 
     # -- pass 1: block layouts per sum layer -------------------------------
-    layers = _collect_layers(g, depth, kinds)
-    for L in layers:
-        L.lo = detect_blocks_csr(L.sids, L.e_key, L.off, cfg.k_m, cfg.k_n,
-                                 cfg.demote_threshold)
+    if native:
+        layers = _collect_layers_native(g, depth, kinds)
+        for L in layers:
+            L.lo = _blocks_native(L, cfg)
+    else:
+        layers = _collect_layers(g, depth, kinds)
+        for L in layers:
+            L.lo = detect_blocks_csr(L.sids, L.e_key, L.off, cfg.k_m, cfg.k_n,
+                                     cfg.demote_threshold)
     reserved = max([L.lo.k_m for L in layers] or [1])
 
     # -- value slots ---------------------------------------------------------
@@ -226,12 +301,16 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
     num_value_slots = int(next_slot)
 
     # -- physical parameter layout ------------------------------------------
-    rep = _tying_reps(g.num_param_slots, g.tying)
+    # native: no identity rep array for untied circuits, ranges instead of
+    # per-position input arrays (written into theta / slot_phys by the core)
+    rep = _tying_reps(g.num_param_slots, g.tying) if (g.tying or not native) else None
     zero_len = max([L.lo.k_m * L.lo.k_n for L in layers] or [1])
     theta_parts = [np.zeros(zero_len)]
     theta_size = zero_len
-    slot_phys = np.full(g.num_param_slots, -1, dtype=np.int64)
+    slot_phys = (_native.full_i64(g.num_param_slots, -1) if native
+                 else np.full(g.num_param_slots, -1, dtype=np.int64))
     assigned: list[tuple[np.ndarray, np.ndarray]] = []
+    in_copy = in_assign = None
 
     pmf_phys_of = np.full(n_nodes, -1, dtype=np.int64)
     if in_ids.size:
@@ -247,8 +326,11 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
             gid, first = group_matrix_rows(key)
         first_ncat = in_ncat[first]
         gstart = theta_size + np.concatenate([[0], np.cumsum(first_ncat)[:-1]])
-        for j, i in enumerate(first.tolist()):
-            theta_parts.append(params[in_slot[i]:in_slot[i] + in_ncat[i]].copy())
+        if native:
+            in_copy = (in_slot[first], first_ncat, gstart)
+        else:
+            for j, i in enumerate(first.tolist()):
+                theta_parts.append(params[in_slot[i]:in_slot[i] + in_ncat[i]].copy())
         theta_size += int(first_ncat.sum())
         starts = gstart[gid]
         pmf_phys_of[in_ids] = starts
@@ -259,15 +341,92 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
         ufirst = np.sort(ufirst)
         o = np.argsort(in_slot[ufirst], kind="stable")
         s_sorted, n_sorted = in_slot[ufirst][o], in_ncat[ufirst][o]
-        if np.any(s_sorted[1:] < s_sorted[:-1] + n_sorted[:-1]):
+        overlap = bool(np.any(s_sorted[1:] < s_sorted[:-1] + n_sorted[:-1]))
+        if overlap:
             ufirst = np.arange(in_ids.size)  # overlapping ranges: keep write order exact
         u_slot, u_ncat, u_start = in_slot[ufirst], in_ncat[ufirst], starts[ufirst]
-        rng_off = np.arange(int(u_ncat.sum())) - np.repeat(np.cumsum(u_ncat) - u_ncat, u_ncat)
-        rng_phys = np.repeat(u_start, u_ncat) + rng_off
-        rng_slots = np.repeat(u_slot, u_ncat) + rng_off
-        slot_phys[rng_slots] = rng_phys
-        assigned.append((rng_slots, rng_phys))
+        if native:
+            in_assign = (u_slot, u_ncat, u_start, overlap)
+        else:
+            rng_off = np.arange(int(u_ncat.sum())) - np.repeat(np.cumsum(u_ncat) - u_ncat, u_ncat)
+            rng_phys = np.repeat(u_start, u_ncat) + rng_off
+            rng_slots = np.repeat(u_slot, u_ncat) + rng_off
+            slot_phys[rng_slots] = rng_phys
+            assigned.append((rng_slots, rng_phys))
 
+    if native:
+        theta, theta_size, tile_starts, tile_writers = _tiles_native(
+            g, layers, rep, params, zero_len, theta_size, slot_phys, in_copy, in_assign)
+    else:
+        theta, theta_size, tile_starts, tile_writers = _tiles_numpy(
+            g, layers, rep, params, theta_parts, theta_size, slot_phys, assigned)
+    del assigned
+    return _finish(g, cfg, layers, kinds, depth, root, in_ids, in_var, in_ncat, n_nodes,
+                   reserved, node_value_slot, num_value_slots, zero_len, theta, theta_size,
+                   slot_phys, pmf_phys_of, tile_starts, tile_writers, native, ghash)
+
+
+def _tiles_native(g, layers, rep, params, zero_len, theta_size, slot_phys, in_copy, in_assign):
+    """build.py:251-339 through the native core: the input pmfs' theta ranges
+    and slot_phys, then per layer ``pcc_tiles`` (tile grids, the tied pattern
+    dedupe, theta fill, slot_phys) with the tying-alignment check."""
+    nat = _native.lib()
+    ptr = _native.ptr
+    tied = bool(g.tying)
+    share = tied or getattr(g, "shares_slots", True)
+    rep_arg = _native.i64(rep) if tied else None
+    nslots = int(g.num_param_slots)
+    params = np.ascontiguousarray(params, dtype=np.float64)
+    multi = ref = None
+    if share:
+        seen = np.zeros((nslots + 63) // 64 + 1, np.uint64)
+        multi = np.zeros_like(seen)
+        for L in layers:
+            nat.pcc_slot_uses(L.e_slot.size, ptr(L.e_slot), ptr(rep_arg), ptr(seen), ptr(multi))
+        del seen
+        ref = _native.full_i64(nslots, -1)
+    cap = theta_size + sum(int(L.lo.cb_flat.size) * L.lo.k_m * L.lo.k_n for L in layers)
+    buf = np.empty(max(cap, 1), dtype=np.float64)  # untouched pages stay unallocated
+    buf[:zero_len] = 0.0
+    if in_copy is not None:
+        src, ln, dst = (_native.i64(a) for a in in_copy)
+        nat.pcc_copy_ranges(src.size, ptr(src), ptr(ln), ptr(dst), ptr(params), ptr(buf))
+    if in_assign is not None:
+        us, un, ust = (_native.i64(a) for a in in_assign[:3])
+        if nat.pcc_assign_ranges(us.size, ptr(us), ptr(un), ptr(ust), int(in_assign[3]),
+                                 ptr(slot_phys), ptr(rep_arg), ptr(ref)):
+            raise _native.NativeError("tying")
+    ts = np.array([theta_size], dtype=np.int64)
+    table = nat.pcc_tiles_new()
+    try:
+        for L in layers:
+            lo = L.lo
+            n_sb, n_pb = lo.sum_block_mat.shape[0], lo.prod_block_mat.shape[0]
+            pair_theta = np.empty(lo.cb_flat.size, dtype=np.int64)
+            if L.nat is not None:
+                rc = nat.pcc_tiles(L.nat.h, table, ptr(L.e_slot), ptr(rep_arg), ptr(multi),
+                                   ptr(params), ptr(buf), cap, ptr(ts), ptr(slot_phys), ptr(ref),
+                                   ptr(pair_theta))
+                L.nat.free()
+                L.nat = None
+                if rc != 0:
+                    raise _native.NativeError(f"tiles rc={rc}")
+            L.pair_theta = pair_theta
+            L.pair_sb = np.repeat(np.arange(n_sb, dtype=np.int64), np.diff(lo.cb_off))
+            L.pair_pb = lo.cb_flat
+            L.pair_codes = L.pair_sb * n_pb + L.pair_pb
+            L.n_pb = n_pb
+        nt = int(nat.pcc_tiles_count(table))
+        tile_starts = np.empty(nt, dtype=np.int64)
+        tile_writers = np.empty(nt, dtype=np.int64)
+        nat.pcc_tiles_get(table, ptr(tile_starts), ptr(tile_writers))
+    finally:
+        nat.pcc_tiles_free(table)
+    theta_size = int(ts[0])
+    return buf[:theta_size], theta_size, tile_starts, tile_writers
+
+
+def _tiles_numpy(g, layers, rep, params, theta_parts, theta_size, slot_phys, assigned):
     tiles = _TileTable()
     writer_count: dict[int, int] = {}
     for L in layers:
@@ -325,8 +484,14 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
     theta = np.concatenate(theta_parts)
     if g.tying or getattr(g, "shares_slots", True):
         _check_tying_alignment(rep, assigned)
-    del assigned
+    tile_starts = np.array(sorted(writer_count), dtype=np.int64)
+    tile_writers = np.array([writer_count[t] for t in tile_starts.tolist()], dtype=np.int64)
+    return theta, theta_size, tile_starts, tile_writers
 
+
+def _finish(g, cfg, layers, kinds, depth, root, in_ids, in_var, in_ncat, n_nodes, reserved,
+            node_value_slot, num_value_slots, zero_len, theta, theta_size, slot_phys,
+            pmf_phys_of, tile_starts, tile_writers, native, ghash):
     # -- groups, product evaluation, flow bookkeeping ---------------------------
     prod_ch_off, prod_ch_flat = _product_children(g, n_nodes)
     node_prod_row = np.full(n_nodes, -1, dtype=np.int64)
@@ -416,7 +581,10 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
             if pm.any():
                 pushes.append(FlowPushIR(rows=rows_l[m[pm]], children=ch[pm]))
 
-        e_child = np.where(L.e_key >= 0, L.e_key, _VKEY_BASE - L.e_key)
+        e_child = L.e_child if L.e_child is not None else \
+            np.where(L.e_key >= 0, L.e_key, _VKEY_BASE - L.e_key)
+        if L.e_sum is None:
+            L.e_sum = np.repeat(L.sids, np.diff(L.off))
         report = LayerReport(
             depth=L.depth, num_sums=int(L.sids.size), num_prods=int(keys.size),
             k_m=km, k_n=kn, demoted=lo.demoted,
@@ -432,11 +600,9 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
             pushes=pushes, edge_sums=L.e_sum, edge_children=e_child,
             edge_slots=L.e_slot, report=report))
         # release pass-1 working arrays
-        L.e_sum = L.e_key = L.e_slot = None
+        L.e_sum = L.e_key = L.e_slot = L.e_child = None
 
     # -- contention replicas (build.py:516-533) -----------------------------
-    tile_starts = np.array(sorted(writer_count), dtype=np.int64)
-    tile_writers = np.array([writer_count[t] for t in tile_starts.tolist()], dtype=np.int64)
     f_params_size = theta_size
     reductions = []
     for layer in out_layers:
@@ -462,7 +628,7 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
                     f_params_size += tilesz * rep_rows.size
 
     # -- simplex groups (build.py:535-567) -------------------------------------
-    group_idx, group_off = _simplex_groups(g, pmf_phys_of, slot_phys, theta_size)
+    group_idx, group_off = _simplex_groups(g, pmf_phys_of, slot_phys, theta_size, native)
 
     # -- input chunks by category count ----------------------------------------
     input_layer = []
@@ -486,7 +652,7 @@ def compile_circuit(g, cfg: CompileConfig | None = None, *, validate: bool = Tru
         root_children = None
 
     return CompiledCircuit(
-        graph_hash=graph_hash(g), config=cfg, num_vars=g.num_vars, num_nodes=n_nodes,
+        graph_hash=ghash(), config=cfg, num_vars=g.num_vars, num_nodes=n_nodes,
         var_categories=g.var_categories(), reserved=int(reserved),
         num_value_slots=num_value_slots, scratch_size=int(scratch_size),
         num_prod_rows=int(num_prod_rows), theta_size=int(theta_size),
@@ -561,43 +727,57 @@ def _product_children(g: CircuitGraph, n_nodes: int):
     return off, flat
 
 
-def _simplex_groups(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
+def _simplex_groups(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size, native=False):
     """Normalisation groups over physical positions, first-occurrence order."""
-    fast = _simplex_groups_disjoint(g, pmf_phys_of, slot_phys, theta_size)
+    fast = _simplex_groups_disjoint(g, pmf_phys_of, slot_phys, theta_size, native)
     if fast is not None:
         return fast
+    if native:
+        return _simplex_groups_general_native(g, pmf_phys_of, slot_phys, theta_size)
     return _simplex_groups_general(g, pmf_phys_of, slot_phys, theta_size)
 
 
-def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
+def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size,
+                             native=False):
     """Fast path when no two sums share a physical position and no sum touches a
     pmf: every sum is its own group and inputs dedupe by their pmf range, so
-    the first-occurrence order is plain node-id order."""
+    the first-occurrence order is plain node-id order.  ``native``: position
+    claims in a bitset and the sorted sum rows written by ``pcc_sum_groups``."""
     sum_segs = [s for s in g.segments if s.kind == KIND_SUM]
     in_ids, _, in_ncat, _ = g.input_table()
     n_sum_pos = sum(s.count * s.fan_in for s in sum_segs)
-    claim = np.zeros(theta_size, dtype=np.int8)
+    nat = _native.lib() if native else None
+    if nat is not None:
+        bits = np.zeros((theta_size + 63) // 64 + 1, dtype=np.uint64)
+    else:
+        claim = np.zeros(theta_size, dtype=np.int8)
     if in_ids.size:
         starts = pmf_phys_of[in_ids]
         key = np.stack([starts, in_ncat], axis=1)
         _, first = np.unique(key, axis=0, return_index=True)
         first = np.sort(first)
         rs, rn = starts[first], in_ncat[first]
-        off = np.repeat(rs - np.concatenate([[0], np.cumsum(rn)[:-1]]), rn)
-        pmf_pos = np.arange(int(rn.sum()), dtype=np.int64) + off
-        claim[pmf_pos] = 1
-        if int(claim.sum()) != pmf_pos.size:
-            return None  # overlapping pmf ranges
+        if nat is not None:
+            rs, rn = _native.i64(rs), _native.i64(rn)
+            if nat.pcc_claim_ranges(rs.size, _native.ptr(rs), _native.ptr(rn), _native.ptr(bits)):
+                return None  # overlapping pmf ranges
+        else:
+            off = np.repeat(rs - np.concatenate([[0], np.cumsum(rn)[:-1]]), rn)
+            pmf_pos = np.arange(int(rn.sum()), dtype=np.int64) + off
+            claim[pmf_pos] = 1
+            if int(claim.sum()) != pmf_pos.size:
+                return None  # overlapping pmf ranges
     else:
         first = np.zeros(0, np.int64)
         rs = rn = np.zeros(0, np.int64)
-    for s in sum_segs:
-        pos = slot_phys[s.slots].ravel()
-        if np.any(claim[pos]):
-            return None
-        claim[pos] = 1
-    if int(claim.sum()) != int(rn.sum()) + n_sum_pos:
-        return None  # a position shared between sums (or within one sum)
+    if nat is None:
+        for s in sum_segs:
+            pos = slot_phys[s.slots].ravel()
+            if np.any(claim[pos]):
+                return None
+            claim[pos] = 1
+        if int(claim.sum()) != int(rn.sum()) + n_sum_pos:
+            return None  # a position shared between sums (or within one sum)
     # assemble in node-id order: input group starts and sum rows interleave
     items_id, items_kind, items_ref = [], [], []
     items_id.append(in_ids[first])
@@ -619,7 +799,11 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
     group_idx = np.empty(int(group_off[-1]), dtype=np.int64)
     # inputs: contiguous ranges
     ii = np.flatnonzero(kinds == 0)
-    if ii.size:
+    if ii.size and nat is not None:
+        dst0, st, n = (_native.i64(a) for a in (group_off[ii], rs[refs[ii]], rn[refs[ii]]))
+        nat.pcc_iota_ranges(dst0.size, _native.ptr(dst0), _native.ptr(st), _native.ptr(n),
+                            _native.ptr(group_idx))
+    elif ii.size:
         n = rn[refs[ii]]
         dst = np.repeat(group_off[ii], n) + (np.arange(int(n.sum())) -
                                               np.repeat(np.cumsum(n) - n, n))
@@ -632,9 +816,88 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
     for si, s in enumerate(sum_segs):
         rows = pos_of[base:base + s.count]
         base += s.count
+        if nat is not None:
+            dst = _native.i64(group_off[rows])
+            sl = _native.i64(s.slots)
+            if nat.pcc_sum_groups(s.count, s.fan_in, _native.ptr(sl), _native.ptr(slot_phys),
+                                  _native.ptr(bits), _native.ptr(dst), _native.ptr(group_idx)):
+                return None  # a position shared between sums (or within one sum)
+            continue
         phys = np.sort(slot_phys[s.slots], axis=1)
         dst = group_off[rows][:, None] + np.arange(s.fan_in)
         group_idx[dst] = phys
+    return group_idx, group_off
+
+
+def _ranges_index(starts, lens):
+    """Concatenated ranges start[i] + [0, lens[i])."""
+    lens = np.asarray(lens, dtype=np.int64)
+    tot = int(lens.sum())
+    return np.repeat(np.asarray(starts, dtype=np.int64) - (np.cumsum(lens) - lens), lens) + \
+        np.arange(tot, dtype=np.int64)
+
+
+def _simplex_groups_general_native(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size):
+    """``_simplex_groups_general`` with the sorted sum rows grouped by the
+    native core (``pcc_rows_*``) and the overlap claims in ``pcc_claim_groups``."""
+    nat = _native.lib()
+    ptr = _native.ptr
+    r_start, r_n, r_id = [], [], []
+    in_ids, _, in_ncat, _ = g.input_table()
+    if in_ids.size:
+        r_start.append(pmf_phys_of[in_ids])
+        r_n.append(in_ncat)
+        r_id.append(in_ids)
+    rg = nat.pcc_rows_new()
+    try:
+        for s in g.segments:
+            if s.kind != KIND_SUM or s.count == 0:
+                continue
+            f = s.fan_in
+            cs = np.empty(s.count, dtype=np.int64)
+            nat.pcc_rows_add(rg, s.count, f, ptr(_native.i64(s.slots)), ptr(slot_phys), s.start,
+                             ptr(cs))
+            contig = cs >= 0
+            if contig.any():
+                r_start.append(cs[contig])
+                r_n.append(np.full(int(contig.sum()), f, np.int64))
+                r_id.append(np.arange(s.start, s.stop, dtype=np.int64)[contig])
+        nm = np.zeros(1, np.int64)
+        ng = int(nat.pcc_rows_count(rg, ptr(nm)))
+        row_first = np.empty(ng, np.int64)
+        row_off = np.empty(ng + 1, np.int64)
+        row_mem = np.empty(int(nm[0]), np.int64)
+        nat.pcc_rows_get(rg, ptr(row_first), ptr(row_off), ptr(row_mem))
+    finally:
+        nat.pcc_rows_free(rg)
+    if r_start:
+        rs, rn, rid = (np.concatenate(a) for a in (r_start, r_n, r_id))
+        order = np.argsort(rid, kind="stable")
+        key = np.stack([rs[order], rn[order]], axis=1)
+        _, first = np.unique(key, axis=0, return_index=True)
+        rng_id, rng_start, rng_n = rid[order][first], key[first, 0], key[first, 1]
+    else:
+        rng_id = rng_start = rng_n = np.zeros(0, np.int64)
+    ids = np.concatenate([rng_id, row_first])
+    if ids.size == 0:
+        return np.zeros(0, dtype=np.int64), np.zeros(1, dtype=np.int64)
+    sizes = np.concatenate([rng_n, np.diff(row_off)])
+    order = np.argsort(ids, kind="stable")
+    group_off = np.concatenate([[0], np.cumsum(sizes[order])]).astype(np.int64)
+    pos = np.empty(ids.size, np.int64)
+    pos[order] = np.arange(ids.size)
+    group_idx = np.empty(int(group_off[-1]), dtype=np.int64)
+    nr = rng_id.size
+    if nr:
+        dst, st, ln = (_native.i64(a) for a in (group_off[pos[:nr]], rng_start, rng_n))
+        nat.pcc_iota_ranges(nr, ptr(dst), ptr(st), ptr(ln), ptr(group_idx))
+    if ng:
+        group_idx[_ranges_index(group_off[pos[nr:]], np.diff(row_off))] = row_mem
+    claim = _native.full_i64(max(theta_size, 1), -1)
+    if nat.pcc_claim_groups(ids.size, ptr(group_off), ptr(group_idx), ptr(claim)):
+        raise CircuitValidationError(
+            "normalization groups overlap after parameter tying; tie whole "
+            "sum nodes (or whole pmfs), not parts of them")
     return group_idx, group_off
 
 
@@ -702,15 +965,62 @@ def _simplex_groups_general(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size)
     return group_idx, group_off
 
 
-def graph_hash(g) -> str:
-    """Structural hash (``build.py:634-657``): same byte stream, built per segment."""
+def _hash_async(g):
+    """graph_hash on a worker thread (sha256 and the native record writer
+    release the GIL), overlapping the compile; returns the joiner."""
+    box: dict = {}
+
+    def run():
+        try:
+            box["h"] = graph_hash(g, True)
+        except BaseException as e:  # re-raised by the joiner
+            box["e"] = e
+
+    th = threading.Thread(target=run, name="pcirc-graph-hash", daemon=True)
+    th.start()
+
+    def join() -> str:
+        th.join()
+        if "e" in box:
+            raise box["e"]
+        return box["h"]
+    return join
+
+
+def graph_hash(g, native: bool | None = None) -> str:
+    """Structural hash (``build.py:634-657``): same byte stream, built per segment
+    (records written by ``pcc_hash_records`` when the native core is loaded)."""
     g = _as_graph(g)
+    nat = _native.lib() if native in (None, True) else None
     h = hashlib.sha256()
     h.update(b"pcirc-graph-1")
     h.update(np.array([g.num_vars, g.num_nodes, g.root], dtype=np.int64).tobytes())
     for s in g.segments:
         f = max(s.fan_in, 1)
         step = max(1, (64 << 20) // (16 * f + 25))  # bound the record buffer
+        if nat is not None and (s.kind == KIND_INPUT or s.fan_in > 0):
+            rec_sz = 25 if s.kind == KIND_INPUT else (1 + 8 * f if s.kind == KIND_PRODUCT
+                                                      else 1 + 16 * f)
+            arrs = ((_native.i64(s.var), _native.i64(s.ncat), _native.i64(s.slot))
+                    if s.kind == KIND_INPUT else
+                    (_native.i64(s.children), _native.i64(s.slots) if s.kind == KIND_SUM else None))
+            buf = np.empty(min(step, s.count) * rec_sz, dtype=np.uint8)
+            for a in range(0, s.count, step):
+                b = min(s.count, a + step)
+                out = buf[:(b - a) * rec_sz]
+                if s.kind == KIND_INPUT:
+                    v, n, sl = arrs
+                    nat.pcc_hash_records(0, b - a, 0, None, None, _native.ptr(v[a:b]),
+                                         _native.ptr(n[a:b]), _native.ptr(sl[a:b]),
+                                         _native.ptr(out))
+                else:
+                    ch, sl = arrs
+                    nat.pcc_hash_records(1 if s.kind == KIND_PRODUCT else 2, b - a, f,
+                                         _native.ptr(ch[a:b]),
+                                         None if sl is None else _native.ptr(sl[a:b]),
+                                         None, None, None, _native.ptr(out))
+                h.update(out)
+            continue
         for a in range(0, s.count, step):
             b = min(s.count, a + step)
             if s.kind == KIND_INPUT:
@@ -727,7 +1037,7 @@ def graph_hash(g) -> str:
                 rec["c"] = s.children[a:b]
                 rec["s"] = s.slots[a:b]
             h.update(rec.tobytes())
-    h.update(g.params.tobytes())
+    h.update(memoryview(np.ascontiguousarray(g.params, dtype=np.float64)).cast("B"))
     if g.tying:
         h.update(np.array(sorted(g.tying.items()), dtype=np.int64).tobytes())
     return h.hexdigest()
