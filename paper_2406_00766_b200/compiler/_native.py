@@ -27,8 +27,8 @@ _SIGS = {
     "pcc_version": (C.c_int, []),
     "pcc_set_threads": (None, [C.c_int]),
     "pcc_threads": (C.c_int, []),
-    "pcc_gather_layer": (None, [C.c_int, _P, _P, _P, _P, _P, _P, _P, C.c_int8, _I64, _P, _P, _P,
-                                _P]),
+    "pcc_gather_layer": (None, [C.c_int, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int8, _I64, _P, _P,
+                                _P, _P]),
     "pcc_fill_i64": (None, [_P, _I64, _I64]),
     "pcc_copy_ranges": (None, [_I64, _P, _P, _P, _P, _P]),
     "pcc_iota_ranges": (None, [_I64, _P, _P, _P, _P]),
@@ -51,7 +51,14 @@ _SIGS = {
     "pcc_hash_records": (None, [C.c_int, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "pcc_rows_new": (_P, []),
     "pcc_rows_free": (None, [_P]),
-    "pcc_rows_add": (None, [_P, _I64, _I64, _P, _P, _I64, _P]),
+    "pcc_rows_add_multi": (None, [_P, _I64, _P, _I64, _P, _P, _P, _P]),
+    "pcc_sum_groups_multi": (C.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P]),
+    "pcc_depths": (None, [_I64, _P, _P, _P, _P, _P, _P, _P]),
+    "pcc_hash_records_multi": (None, [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "pcc_release": (None, []),
+    "pcc_group_runs": (None, [_I64, _P, _P, _P, _P, _P]),
+    "pcc_minmax": (None, [_P, _I64, _P]),
+    "pcc_narrow_i32": (None, [_P, _I64, _P]),
     "pcc_rows_count": (_I64, [_P, _P]),
     "pcc_rows_get": (None, [_P, _P, _P, _P]),
     "pcc_claim_groups": (C.c_int, [_I64, _P, _P, _P]),
@@ -93,8 +100,30 @@ def full_i64(n: int, value: int) -> np.ndarray:
     return a
 
 
+def rows(a) -> tuple[np.ndarray, int]:
+    """(array, row stride in elements) of a 2-D int64 matrix whose rows are
+    contiguous -- broadcast views (stride 0, one row shared by a segment)
+    are passed as they are instead of being materialised."""
+    a = np.asarray(a)
+    if a.ndim == 2 and a.dtype == np.int64 and (a.strides[1] == 8 or a.shape[1] <= 1) \
+            and a.strides[0] >= 0 and a.strides[0] % 8 == 0:
+        return a, a.strides[0] // 8
+    c = np.ascontiguousarray(a, dtype=np.int64).reshape(a.shape[0], -1)
+    return c, c.shape[1]
+
+
 def ptr_array(arrs) -> C.Array:
     return (C.c_void_p * len(arrs))(*[ptr(a) for a in arrs])
+
+
+def addr(a: np.ndarray) -> int:
+    """Data address of a C-contiguous array (cheaper than ``a.ctypes``)."""
+    return a.__array_interface__["data"][0]
+
+
+def addr_array(addrs) -> np.ndarray:
+    """A pointer table (uint64) from data addresses (0 = null)."""
+    return np.array(addrs, dtype=np.uint64)
 
 
 class NativeError(Exception):

@@ -168,20 +168,28 @@ def _collect_layers_native(g: CircuitGraph, depth: np.ndarray, kinds: np.ndarray
     per layer (segments in id order, so sum ids ascend)."""
     nat = _native.lib()
     by_depth: dict[int, list] = {}
-    for s in g.segments:
-        if s.kind != KIND_SUM:
-            continue
-        d = depth[s.start:s.stop]
-        if s.count and d.min() == d.max():
-            by_depth.setdefault(int(d[0]), []).append((s, None))
-            continue
-        for dv in np.unique(d).tolist():
-            by_depth.setdefault(dv, []).append((s, np.flatnonzero(d == dv).astype(np.int64)))
+    segs = [s for s in g.segments if s.kind == KIND_SUM and s.count]
+    if segs:
+        st = np.array([s.start for s in segs], dtype=np.int64)
+        cn = np.array([s.count for s in segs], dtype=np.int64)
+        idx = _ranges_index(st, cn)
+        firsts = np.concatenate([[0], np.cumsum(cn)[:-1]])
+        dmin = np.minimum.reduceat(depth[idx], firsts)
+        dmax = np.maximum.reduceat(depth[idx], firsts)
+        for i, s in enumerate(segs):
+            if dmin[i] == dmax[i]:
+                by_depth.setdefault(int(dmin[i]), []).append((s, None))
+                continue
+            d = depth[s.start:s.stop]
+            for dv in np.unique(d).tolist():
+                by_depth.setdefault(dv, []).append((s, np.flatnonzero(d == dv).astype(np.int64)))
     kinds8 = np.ascontiguousarray(kinds, dtype=np.int8)
     layers = []
     for dv in sorted(by_depth):
         parts = sorted(by_depth[dv], key=lambda t: t[0].start)
-        chs = [_native.i64(s.children) for s, _ in parts]
+        chv = [_native.rows(s.children) for s, _ in parts]
+        chs = [c for c, _ in chv]
+        ch_stride = np.array([st for _, st in chv], dtype=np.int64)
         sls = [_native.i64(s.slots) for s, _ in parts]
         fan = np.array([s.fan_in for s, _ in parts], dtype=np.int64)
         nrows = np.array([s.count if r is None else r.size for s, r in parts], dtype=np.int64)
@@ -195,7 +203,9 @@ def _collect_layers_native(g: CircuitGraph, depth: np.ndarray, kinds: np.ndarray
         E = int(L.off[-1])
         starts = np.array([s.start for s, _ in parts], dtype=np.int64)
         L.e_sum, L.e_child, L.e_key, L.e_slot = (np.empty(E, np.int64) for _ in range(4))
-        nat.pcc_gather_layer(len(parts), _native.ptr_array(chs), _native.ptr_array(sls),
+        ch_tab = _native.addr_array([_native.addr(c) for c in chs])
+        nat.pcc_gather_layer(len(parts), _native.ptr(ch_tab), _native.ptr(ch_stride),
+                             _native.ptr_array(sls),
                              _native.ptr(fan), _native.ptr_array(rows), _native.ptr(nrows),
                              _native.ptr(starts), _native.ptr(kinds8), KIND_PRODUCT, _VKEY_BASE,
                              _native.ptr(L.e_sum), _native.ptr(L.e_child), _native.ptr(L.e_key),
@@ -778,6 +788,9 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
             claim[pos] = 1
         if int(claim.sum()) != int(rn.sum()) + n_sum_pos:
             return None  # a position shared between sums (or within one sum)
+    if nat is not None:
+        return _simplex_disjoint_assemble_native(nat, sum_segs, in_ids, first, rs, rn, slot_phys,
+                                                 bits)
     # assemble in node-id order: input group starts and sum rows interleave
     items_id, items_kind, items_ref = [], [], []
     items_id.append(in_ids[first])
@@ -829,6 +842,37 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
     return group_idx, group_off
 
 
+def _simplex_disjoint_assemble_native(nat, sum_segs, in_ids, first, rs, rn, slot_phys, bits):
+    """The node-id-ordered assembly of ``_simplex_groups_disjoint`` with
+    whole-circuit arrays (no per-segment work) and the sorted sum rows written
+    by one ``pcc_sum_groups_multi`` call."""
+    ptr = _native.ptr
+    st = np.array([s.start for s in sum_segs], dtype=np.int64)
+    cn = np.array([s.count for s in sum_segs], dtype=np.int64)
+    fn = np.array([s.fan_in for s in sum_segs], dtype=np.int64)
+    sum_ids = _ranges_index(st, cn)
+    n_in = first.size
+    ids = np.concatenate([in_ids[first], sum_ids])
+    sizes = np.concatenate([rn, np.repeat(fn, cn)])
+    order = np.argsort(ids, kind="stable")
+    group_off = np.concatenate([[0], np.cumsum(sizes[order])]).astype(np.int64)
+    pos_of = np.empty(ids.size, dtype=np.int64)
+    pos_of[order] = np.arange(ids.size)
+    group_idx = np.empty(int(group_off[-1]), dtype=np.int64)
+    if n_in:
+        dst0 = _native.i64(group_off[pos_of[:n_in]])
+        rs_, rn_ = _native.i64(rs), _native.i64(rn)
+        nat.pcc_iota_ranges(n_in, ptr(dst0), ptr(rs_), ptr(rn_), ptr(group_idx))
+    if sum_segs:
+        slots = [_native.i64(s.slots) for s in sum_segs]
+        tab = _native.addr_array([_native.addr(a) for a in slots])
+        dst = _native.i64(group_off[pos_of[n_in:]])
+        if nat.pcc_sum_groups_multi(len(sum_segs), ptr(cn), ptr(fn), ptr(tab), ptr(slot_phys),
+                                    ptr(bits), ptr(dst), ptr(group_idx)):
+            return None  # a position shared between sums (or within one sum)
+    return group_idx, group_off
+
+
 def _ranges_index(starts, lens):
     """Concatenated ranges start[i] + [0, lens[i])."""
     lens = np.asarray(lens, dtype=np.int64)
@@ -848,20 +892,25 @@ def _simplex_groups_general_native(g: CircuitGraph, pmf_phys_of, slot_phys, thet
         r_start.append(pmf_phys_of[in_ids])
         r_n.append(in_ncat)
         r_id.append(in_ids)
+    by_fan: dict[int, list] = {}
+    for s in g.segments:
+        if s.kind == KIND_SUM and s.count:
+            by_fan.setdefault(s.fan_in, []).append(s)
     rg = nat.pcc_rows_new()
     try:
-        for s in g.segments:
-            if s.kind != KIND_SUM or s.count == 0:
-                continue
-            f = s.fan_in
-            cs = np.empty(s.count, dtype=np.int64)
-            nat.pcc_rows_add(rg, s.count, f, ptr(_native.i64(s.slots)), ptr(slot_phys), s.start,
-                             ptr(cs))
+        for f, segs in by_fan.items():
+            st = np.array([s.start for s in segs], dtype=np.int64)
+            cn = np.array([s.count for s in segs], dtype=np.int64)
+            slots = [_native.i64(s.slots) for s in segs]
+            tab = _native.addr_array([_native.addr(a) for a in slots])
+            cs = np.empty(int(cn.sum()), dtype=np.int64)
+            nat.pcc_rows_add_multi(rg, len(segs), ptr(cn), f, ptr(tab), ptr(st), ptr(slot_phys),
+                                   ptr(cs))
             contig = cs >= 0
             if contig.any():
                 r_start.append(cs[contig])
                 r_n.append(np.full(int(contig.sum()), f, np.int64))
-                r_id.append(np.arange(s.start, s.stop, dtype=np.int64)[contig])
+                r_id.append(_ranges_index(st, cn)[contig])
         nm = np.zeros(1, np.int64)
         ng = int(nat.pcc_rows_count(rg, ptr(nm)))
         row_first = np.empty(ng, np.int64)
@@ -987,40 +1036,74 @@ def _hash_async(g):
     return join
 
 
+def _hash_segments_native(nat, g, h, limit: int = 64 << 20):
+    """Records of runs of segments written by ``pcc_hash_records_multi`` into
+    <= ``limit``-byte buffers (one segment larger than that is cut into row
+    ranges)."""
+    ptr, i64, addr = _native.ptr, _native.i64, _native.addr
+    batch: list = []
+    keep: list = []
+    size = 0
+
+    def flush():
+        nonlocal batch, keep, size
+        if not batch:
+            return
+        kinds = np.array([b[0] for b in batch], dtype=np.int8)
+        counts = np.array([b[1] for b in batch], dtype=np.int64)
+        fans = np.array([b[2] for b in batch], dtype=np.int64)
+        tabs = [_native.addr_array([b[3 + j] for b in batch]) for j in range(3)]
+        a_st = np.array([b[6] for b in batch], dtype=np.int64)
+        b_st = np.array([b[7] for b in batch], dtype=np.int64)
+        out = np.empty(size, dtype=np.uint8)
+        nat.pcc_hash_records_multi(len(batch), ptr(kinds), ptr(counts), ptr(fans),
+                                   ptr(tabs[0]), ptr(a_st), ptr(tabs[1]), ptr(b_st),
+                                   ptr(tabs[2]), ptr(out))
+        h.update(out)
+        batch, keep, size = [], [], 0
+
+    for s in g.segments:
+        f = max(s.fan_in, 1)
+        rec = 25 if s.kind == KIND_INPUT else (1 + 8 * f if s.kind == KIND_PRODUCT else 1 + 16 * f)
+        strides = (0, 0)
+        if s.kind == KIND_INPUT:
+            arrs = (i64(s.var), i64(s.ncat), i64(s.slot))
+        elif s.kind == KIND_PRODUCT:
+            ch, cs = _native.rows(s.children)
+            arrs, strides = (ch,), (cs, 0)
+        else:
+            (ch, cs), (sl, ss) = _native.rows(s.children), _native.rows(s.slots)
+            arrs, strides = (ch, sl), (cs, ss)
+        step = max(1, limit // rec)
+        for a in range(0, s.count, step):
+            b = min(s.count, a + step)
+            if size + (b - a) * rec > limit:
+                flush()
+            parts = [x[a:b] for x in arrs]
+            keep.extend(parts)
+            ads = [addr(x) for x in parts] + [0] * (3 - len(parts))
+            batch.append((s.kind, b - a, f, *ads, *strides))
+            size += (b - a) * rec
+    flush()
+
+
 def graph_hash(g, native: bool | None = None) -> str:
     """Structural hash (``build.py:634-657``): same byte stream, built per segment
-    (records written by ``pcc_hash_records`` when the native core is loaded)."""
+    (records written by ``pcc_hash_records_multi`` when the native core is loaded)."""
     g = _as_graph(g)
     nat = _native.lib() if native in (None, True) else None
     h = hashlib.sha256()
     h.update(b"pcirc-graph-1")
     h.update(np.array([g.num_vars, g.num_nodes, g.root], dtype=np.int64).tobytes())
+    if nat is not None and all(s.kind == KIND_INPUT or s.fan_in > 0 for s in g.segments):
+        _hash_segments_native(nat, g, h)
+        h.update(memoryview(np.ascontiguousarray(g.params, dtype=np.float64)).cast("B"))
+        if g.tying:
+            h.update(np.array(sorted(g.tying.items()), dtype=np.int64).tobytes())
+        return h.hexdigest()
     for s in g.segments:
         f = max(s.fan_in, 1)
         step = max(1, (64 << 20) // (16 * f + 25))  # bound the record buffer
-        if nat is not None and (s.kind == KIND_INPUT or s.fan_in > 0):
-            rec_sz = 25 if s.kind == KIND_INPUT else (1 + 8 * f if s.kind == KIND_PRODUCT
-                                                      else 1 + 16 * f)
-            arrs = ((_native.i64(s.var), _native.i64(s.ncat), _native.i64(s.slot))
-                    if s.kind == KIND_INPUT else
-                    (_native.i64(s.children), _native.i64(s.slots) if s.kind == KIND_SUM else None))
-            buf = np.empty(min(step, s.count) * rec_sz, dtype=np.uint8)
-            for a in range(0, s.count, step):
-                b = min(s.count, a + step)
-                out = buf[:(b - a) * rec_sz]
-                if s.kind == KIND_INPUT:
-                    v, n, sl = arrs
-                    nat.pcc_hash_records(0, b - a, 0, None, None, _native.ptr(v[a:b]),
-                                         _native.ptr(n[a:b]), _native.ptr(sl[a:b]),
-                                         _native.ptr(out))
-                else:
-                    ch, sl = arrs
-                    nat.pcc_hash_records(1 if s.kind == KIND_PRODUCT else 2, b - a, f,
-                                         _native.ptr(ch[a:b]),
-                                         None if sl is None else _native.ptr(sl[a:b]),
-                                         None, None, None, _native.ptr(out))
-                h.update(out)
-            continue
         for a in range(0, s.count, step):
             b = min(s.count, a + step)
             if s.kind == KIND_INPUT:

@@ -28,6 +28,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <thread>
 #include <unordered_map>
 #include <vector>
@@ -173,6 +174,25 @@ i64 pow2_floor(i64 n) {
   return p;
 }
 
+// Uninitialised scratch reused across layers: no zero fill, and pages
+// first-touched once by the parallel writers (released by pcc_release).
+struct Scratch {
+  std::unique_ptr<i64[]> p;
+  size_t n = 0;
+  i64* get(size_t m) {
+    if (m > n) {
+      p.reset(new i64[m]);
+      n = m;
+    }
+    return p.get();
+  }
+  void release() {
+    p.reset();
+    n = 0;
+  }
+};
+Scratch g_tmp, g_par, g_grid, g_pat, g_rows;
+
 struct Layer {
   // caller-owned inputs (kept alive by the Python layer object)
   i64 n = 0, E = 0;
@@ -202,7 +222,8 @@ inline int32_t pidx(const Layer& L, i64 k) { return L.kix[(size_t)(k - L.kmin)];
 
 void sum_sets(Layer& L) {
   const i64 n = L.n;
-  std::vector<i64> tmp(L.E), ulen(n);
+  i64* tmp = g_tmp.get((size_t)L.E);
+  std::vector<i64> ulen(n);
   pfor(n, [&](i64 lo, i64 hi, int) {
     for (i64 r = lo; r < hi; ++r) {
       const i64 a = L.off[r], b = L.off[r + 1];
@@ -212,8 +233,8 @@ void sum_sets(Layer& L) {
         if (c == 0 || bl != last) tmp[a + c++] = bl;
         last = bl;
       }
-      std::sort(tmp.begin() + a, tmp.begin() + a + c);
-      ulen[r] = std::unique(tmp.begin() + a, tmp.begin() + a + c) - (tmp.begin() + a);
+      std::sort(tmp + a, tmp + a + c);
+      ulen[r] = std::unique(tmp + a, tmp + a + c) - (tmp + a);
     }
   }, 1 << 8);
   L.b2_off.assign(n + 1, 0);
@@ -221,7 +242,7 @@ void sum_sets(Layer& L) {
   L.b2.resize(L.b2_off[n]);
   pfor(n, [&](i64 lo, i64 hi, int) {
     for (i64 r = lo; r < hi; ++r)
-      std::copy(tmp.begin() + L.off[r], tmp.begin() + L.off[r] + ulen[r], L.b2.begin() + L.b2_off[r]);
+      std::copy(tmp + L.off[r], tmp + L.off[r] + ulen[r], L.b2.begin() + L.b2_off[r]);
   }, 1 << 10);
 }
 
@@ -299,7 +320,7 @@ int blocks(Layer& L, i64 k, i64 k_n, double demote) {
     }
     poff_par[p + 1] = s;
   }
-  std::vector<i64> par(E);
+  i64* par = g_par.get((size_t)E);
   {
     std::vector<std::thread> th;
     for (int t = 0; t < T; ++t)
@@ -314,9 +335,8 @@ int blocks(Layer& L, i64 k, i64 k_n, double demote) {
   }
   cnt = std::vector<i64>();
   L.pcls = group_rows(P, [&](i64 p) {
-    return std::pair<const i64*, i64>(par.data() + poff_par[p], poff_par[p + 1] - poff_par[p]);
+    return std::pair<const i64*, i64>(par + poff_par[p], poff_par[p + 1] - poff_par[p]);
   });
-  par = std::vector<i64>();
   const i64 kn0 = std::min(k_n, pow2_floor(std::max<i64>(P, 1)));
   const i64 km0 = std::min(k, pow2_floor(std::max<i64>(n, 1)));
   block_pass(L, km0, kn0);
@@ -350,7 +370,6 @@ struct TileTable {
   std::vector<i64> starts, writers;                          // per tile, creation order
 };
 
-std::vector<i64> g_grid;  // tile grids of the layer being compiled
 
 inline u64 table_key(i64 tilesz, u64 h) { return h ^ mix((u64)tilesz * 0x9E3779B97F4A7C15ull); }
 
@@ -367,9 +386,11 @@ int pcc_threads() { return nthreads(); }
 // One sum layer's per-edge sum ids / child ids / child keys / slots from its
 // segments: segment s contributes rows rows[s][0..nrows[s]) (or 0..nrows[s]
 // when rows[s] is null) of its (count, fan) children / slots matrices, in the
-// given order; starts[s] is its first node id.
-void pcc_gather_layer(int nseg, const i64* const* children, const i64* const* slots,
-                      const i64* fan, const i64* const* rows, const i64* nrows, const i64* starts,
+// given order; starts[s] is its first node id.  Children rows are
+// ch_stride[s] elements apart (0: one row broadcast to every sum).
+void pcc_gather_layer(int nseg, const i64* const* children, const i64* ch_stride,
+                      const i64* const* slots, const i64* fan, const i64* const* rows,
+                      const i64* nrows, const i64* starts,
                       const int8_t* kinds, int8_t product_kind, i64 vkey_base, i64* e_sum,
                       i64* e_child, i64* e_key, i64* e_slot) {
   std::vector<i64> rbase(nseg + 1, 0), ebase(nseg + 1, 0);
@@ -386,7 +407,7 @@ void pcc_gather_layer(int nseg, const i64* const* children, const i64* const* sl
       while (g >= rbase[s + 1]) ++s;
       const i64 q = g - rbase[s], f = fan[s];
       const i64 r = rows[s] ? rows[s][q] : q;
-      const i64* c = children[s] + r * f;
+      const i64* c = children[s] + r * ch_stride[s];
       const i64* sl = slots[s] + r * f;
       const i64 o = ebase[s] + q * f, sid = starts[s] + r;
       for (i64 j = 0; j < f; ++j) {
@@ -518,9 +539,11 @@ void pcc_slot_uses(i64 E, const i64* slots, const i64* rep, u64* seen, u64* mult
 
 void* pcc_tiles_new() { return new TileTable; }
 
-void pcc_tiles_free(void* t) {
-  delete static_cast<TileTable*>(t);
-  std::vector<i64>().swap(g_grid);  // the compile's tile-grid scratch
+void pcc_tiles_free(void* t) { delete static_cast<TileTable*>(t); }
+
+// frees the scratch buffers kept across the layers of one compile
+void pcc_release() {
+  for (Scratch* b : {&g_tmp, &g_par, &g_grid, &g_pat, &g_rows}) b->release();
 }
 
 i64 pcc_tiles_count(void* t) { return (i64)static_cast<TileTable*>(t)->starts.size(); }
@@ -546,10 +569,8 @@ int pcc_tiles(void* h, void* table, const i64* slots, const i64* rep, const u64*
   TileTable& T = *static_cast<TileTable*>(table);
   const i64 km = L.km, kn = L.kn, tsz = km * kn;
   const i64 npair = (i64)L.cb_flat.size();
-  std::vector<i64>& grid = g_grid;  // reused across layers (no fresh page faults)
-  if (grid.size() < (size_t)(npair * tsz)) grid.resize((size_t)(npair * tsz));
-  pfor(npair * tsz, [&](i64 lo, i64 hi, int) { std::fill(grid.begin() + lo, grid.begin() + hi, -1); },
-       1 << 20);
+  i64* grid = g_grid.get((size_t)(npair * tsz));
+  pfor(npair * tsz, [&](i64 lo, i64 hi, int) { std::fill(grid + lo, grid + hi, (i64)-1); }, 1 << 20);
   std::atomic<int> dup{0};
   pfor(L.n, [&](i64 lo, i64 hi, int) {
     for (i64 r = lo; r < hi; ++r) {
@@ -594,7 +615,7 @@ int pcc_tiles(void* h, void* table, const i64* slots, const i64* rep, const u64*
   for (i64 q = 0; q < npair; ++q)
     if (!uniq[q]) shared_rows.push_back(q);
   const i64 ns = (i64)shared_rows.size();
-  std::vector<i64> pat((size_t)(ns * tsz));
+  i64* pat = g_pat.get((size_t)(ns * tsz));
   std::vector<u64> hsh(ns);
   pfor(ns, [&](i64 lo, i64 hi, int) {
     for (i64 i = lo; i < hi; ++i) {
@@ -767,57 +788,73 @@ void* pcc_rows_new() { return new RowGroups; }
 
 void pcc_rows_free(void* h) { delete static_cast<RowGroups*>(h); }
 
-// rows [0, count) of a (count, fan) slot matrix, node ids id0 + i.
-// contig_start[i] = first position of a contiguous row, else -1.
-void pcc_rows_add(void* h, i64 count, i64 fan, const i64* slots, const i64* slot_phys, i64 id0,
-                  i64* contig_start) {
+// Rows of several segments of one fan-in (segment s: counts[s] rows of its
+// (count, fan) slot matrix, node ids id0s[s] + i), in the order given (node-id
+// order).  contig_start (one per row, concatenated): first position of a
+// contiguous row, else -1.  Rows are sorted and hashed in parallel chunks;
+// grouping is sequential in row order (first occurrence).
+void pcc_rows_add_multi(void* h, i64 nseg, const i64* counts, i64 fan,
+                        const i64* const* slot_ptrs, const i64* id0s, const i64* slot_phys,
+                        i64* contig_start) {
   RowGroups& G = *static_cast<RowGroups*>(h);
-  std::vector<i64> rows((size_t)(count * fan));
-  std::vector<u64> hs(count);
-  pfor(count, [&](i64 lo, i64 hi, int) {
-    for (i64 i = lo; i < hi; ++i) {
-      i64* r = rows.data() + i * fan;
-      const i64* sl = slots + i * fan;
-      for (i64 j = 0; j < fan; ++j) r[j] = slot_phys[sl[j]];
-      std::sort(r, r + fan);
-      const bool contig = r[fan - 1] - r[0] == fan - 1 &&
-                          std::adjacent_find(r, r + fan, [](i64 a, i64 b) { return b != a + 1; }) ==
-                              r + fan;
-      contig_start[i] = contig ? r[0] : -1;
-      if (!contig) hs[i] = row_hash(r, fan);
-    }
-  }, std::max<i64>(1, (1 << 14) / std::max<i64>(fan, 1)));
-  i64 ncontig = 0;
-  for (i64 i = 0; i < count; ++i) ncontig += contig_start[i] >= 0;
-  const i64 need = (i64)G.first_id.size() + count - ncontig;
-  if (need > G.cap) {  // rehash into a larger table
-    G.cap = std::max<i64>(2 * G.cap, need);
-    G.heads.init(G.cap);
-    std::fill(G.next.begin(), G.next.end(), -1);
-    for (i64 gi = 0; gi < (i64)G.first_id.size(); ++gi) {
-      i64& hd = G.heads.at(G.hash[gi]);
-      G.next[gi] = hd;
-      hd = gi;
-    }
-  }
-  for (i64 i = 0; i < count; ++i) {
-    if (contig_start[i] >= 0) continue;
-    const i64* r = rows.data() + i * fan;
-    i64& hd = G.heads.at(hs[i]);
-    bool found = false;
-    for (i64 c = hd; c >= 0; c = G.next[c])
-      if (G.off[c + 1] - G.off[c] == fan &&
-          std::memcmp(G.members.data() + G.off[c], r, sizeof(i64) * fan) == 0) {
-        found = true;
-        break;
+  std::vector<i64> rbase(nseg + 1, 0);
+  for (i64 s = 0; s < nseg; ++s) rbase[s + 1] = rbase[s] + counts[s];
+  const i64 N = rbase[nseg];
+  if (!N || fan <= 0) return;
+  const i64 step = std::max<i64>(1, ((i64)1 << 25) / fan);
+  std::vector<u64> hs;
+  for (i64 q0 = 0; q0 < N; q0 += step) {
+    const i64 q1 = std::min(N, q0 + step), nq = q1 - q0;
+    i64* rows = g_rows.get((size_t)(nq * fan));
+    hs.resize(nq);
+    pfor(nq, [&](i64 lo, i64 hi, int) {
+      i64 s = (i64)(std::upper_bound(rbase.begin(), rbase.end(), q0 + lo) - rbase.begin()) - 1;
+      for (i64 i = lo; i < hi; ++i) {
+        while (q0 + i >= rbase[s + 1]) ++s;
+        i64* r = rows + i * fan;
+        const i64* sl = slot_ptrs[s] + (q0 + i - rbase[s]) * fan;
+        for (i64 j = 0; j < fan; ++j) r[j] = slot_phys[sl[j]];
+        std::sort(r, r + fan);
+        const bool contig = r[fan - 1] - r[0] == fan - 1 &&
+                            std::adjacent_find(r, r + fan, [](i64 a, i64 b) { return b != a + 1; }) ==
+                                r + fan;
+        contig_start[q0 + i] = contig ? r[0] : -1;
+        if (!contig) hs[i] = row_hash(r, fan);
       }
-    if (found) continue;
-    G.first_id.push_back(id0 + i);
-    G.hash.push_back(hs[i]);
-    G.members.insert(G.members.end(), r, r + fan);
-    G.off.push_back((i64)G.members.size());
-    G.next.push_back(hd);
-    hd = (i64)G.first_id.size() - 1;
+    }, std::max<i64>(1, (1 << 14) / fan));
+    i64 ncontig = 0;
+    for (i64 i = 0; i < nq; ++i) ncontig += contig_start[q0 + i] >= 0;
+    const i64 need = (i64)G.first_id.size() + nq - ncontig;
+    if (need > G.cap) {  // rehash into a larger table
+      G.cap = std::max<i64>(2 * G.cap, need);
+      G.heads.init(G.cap);
+      for (i64 gi = 0; gi < (i64)G.first_id.size(); ++gi) {
+        i64& hd = G.heads.at(G.hash[gi]);
+        G.next[gi] = hd;
+        hd = gi;
+      }
+    }
+    i64 s = (i64)(std::upper_bound(rbase.begin(), rbase.end(), q0) - rbase.begin()) - 1;
+    for (i64 i = 0; i < nq; ++i) {
+      while (q0 + i >= rbase[s + 1]) ++s;
+      if (contig_start[q0 + i] >= 0) continue;
+      const i64* r = rows + i * fan;
+      i64& hd = G.heads.at(hs[i]);
+      bool found = false;
+      for (i64 c = hd; c >= 0; c = G.next[c])
+        if (G.off[c + 1] - G.off[c] == fan &&
+            std::memcmp(G.members.data() + G.off[c], r, sizeof(i64) * fan) == 0) {
+          found = true;
+          break;
+        }
+      if (found) continue;
+      G.first_id.push_back(id0s[s] + (q0 + i - rbase[s]));
+      G.hash.push_back(hs[i]);
+      G.members.insert(G.members.end(), r, r + fan);
+      G.off.push_back((i64)G.members.size());
+      G.next.push_back(hd);
+      hd = (i64)G.first_id.size() - 1;
+    }
   }
 }
 
@@ -848,6 +885,154 @@ int pcc_claim_groups(i64 ngroups, const i64* group_off, const i64* group_idx, i6
       }
   }, 1 << 6);
   return bad.load();
+}
+
+// pcc_sum_groups over several segments (segment s: counts[s] rows of fan
+// fans[s]); dst: one group_idx offset per row, concatenated.
+int pcc_sum_groups_multi(i64 nseg, const i64* counts, const i64* fans, const i64* const* slot_ptrs,
+                         const i64* slot_phys, u64* bits, const i64* dst, i64* group_idx) {
+  std::vector<i64> rbase(nseg + 1, 0);
+  i64 E = 0;
+  for (i64 s = 0; s < nseg; ++s) rbase[s + 1] = rbase[s] + counts[s], E += counts[s] * fans[s];
+  const i64 N = rbase[nseg];
+  std::atomic<int> bad{0};
+  pfor(N, [&](i64 lo, i64 hi, int) {
+    i64 s = (i64)(std::upper_bound(rbase.begin(), rbase.end(), lo) - rbase.begin()) - 1;
+    for (i64 q = lo; q < hi; ++q) {
+      if (bad.load(std::memory_order_relaxed)) return;  // the general path takes over
+      while (q >= rbase[s + 1]) ++s;
+      const i64 fan = fans[s];
+      i64* out = group_idx + dst[q];
+      const i64* sl = slot_ptrs[s] + (q - rbase[s]) * fan;
+      bool sorted = true;
+      for (i64 j = 0; j < fan; ++j) {
+        const i64 p = slot_phys[sl[j]];
+        out[j] = p;
+        if (j && p < out[j - 1]) sorted = false;
+        const u64 bit = 1ull << ((u64)p & 63);
+        if (__atomic_fetch_or(&bits[(u64)p >> 6], bit, __ATOMIC_RELAXED) & bit)
+          bad.store(1, std::memory_order_relaxed);
+      }
+      if (!sorted) std::sort(out, out + fan);
+    }
+  }, std::max<i64>(1, (1 << 14) / std::max<i64>(1, N ? E / N : 1)));
+  return bad.load();
+}
+
+// Depths (build.py:103-110) of segments given in dependency order: inputs 0,
+// else 1 + the max child depth.  kinds[s] = 0 marks an input segment.
+void pcc_depths(i64 nseg, const i64* starts, const i64* counts, const i64* fans,
+                const int8_t* kinds, const i64* const* child_ptrs, const i64* strides,
+                i64* depth) {
+  for (i64 s = 0; s < nseg; ++s) {
+    if (kinds[s] == 0) {
+      std::fill(depth + starts[s], depth + starts[s] + counts[s], (i64)0);
+      continue;
+    }
+    const i64 f = fans[s], st = strides[s];
+    if (st == 0) {  // broadcast rows: one child list for the whole segment
+      i64 m = -1;
+      for (i64 j = 0; j < f; ++j) m = std::max(m, depth[child_ptrs[s][j]]);
+      std::fill(depth + starts[s], depth + starts[s] + counts[s], m + 1);
+      continue;
+    }
+    auto body = [&](i64 lo, i64 hi, int) {
+      for (i64 i = lo; i < hi; ++i) {
+        const i64* c = child_ptrs[s] + i * st;
+        i64 m = -1;
+        for (i64 j = 0; j < f; ++j) m = std::max(m, depth[c[j]]);
+        depth[starts[s] + i] = m + 1;
+      }
+    };
+    if (counts[s] * f >= (1 << 16))
+      pfor(counts[s], body, std::max<i64>(1, (1 << 14) / std::max<i64>(f, 1)));
+    else
+      body(0, counts[s], 0);
+  }
+}
+
+// graph_hash records of several segments, concatenated in order (see
+// pcc_hash_records; a / b / c are var / ncat / slot for inputs, children /
+// slots for sums, children for products; a_stride / b_stride: row strides in
+// elements, 0 for broadcast rows).
+void pcc_hash_records_multi(i64 nseg, const int8_t* kinds, const i64* counts, const i64* fans,
+                            const i64* const* a, const i64* a_stride, const i64* const* b,
+                            const i64* b_stride, const i64* const* c, uint8_t* out) {
+  std::vector<i64> obase(nseg + 1, 0);
+  for (i64 s = 0; s < nseg; ++s) {
+    const i64 f = std::max<i64>(fans[s], 1);
+    const i64 rec = kinds[s] == 0 ? 25 : (kinds[s] == 1 ? 1 + 8 * f : 1 + 16 * f);
+    obase[s + 1] = obase[s] + rec * counts[s];
+  }
+  pfor(nseg, [&](i64 lo, i64 hi, int) {
+    for (i64 s = lo; s < hi; ++s) {
+      const i64 f = std::max<i64>(fans[s], 1);
+      uint8_t* o = out + obase[s];
+      for (i64 i = 0; i < counts[s]; ++i) {
+        if (kinds[s] == 0) {
+          *o++ = 'I';
+          const i64 v[3] = {a[s][i], b[s][i], c[s][i]};
+          std::memcpy(o, v, 24);
+          o += 24;
+        } else if (kinds[s] == 1) {
+          *o++ = 'P';
+          std::memcpy(o, a[s] + i * a_stride[s], 8 * f);
+          o += 8 * f;
+        } else {
+          *o++ = 'S';
+          std::memcpy(o, a[s] + i * a_stride[s], 8 * f);
+          std::memcpy(o + 8 * f, b[s] + i * b_stride[s], 8 * f);
+          o += 16 * f;
+        }
+      }
+    }
+  }, 64);
+}
+
+// Run-length encoding of the simplex-group table (runtime/plan.py
+// group_runs): maximal runs of consecutive theta indices inside each group.
+// Pass 1 (rs == null): runs per group into run_off[g + 1]; pass 2: run
+// starts / lengths at the exclusive prefix run_off.
+void pcc_group_runs(i64 ngroups, const i64* go, const i64* gi, i64* run_off, i64* rs, i64* rl) {
+  pfor(ngroups, [&](i64 lo, i64 hi, int) {
+    for (i64 g = lo; g < hi; ++g) {
+      const i64 a = go[g], b = go[g + 1];
+      if (!rs) {
+        i64 n = a < b;
+        for (i64 i = a + 1; i < b; ++i) n += gi[i] != gi[i - 1] + 1;
+        run_off[g + 1] = n;
+        continue;
+      }
+      i64 r = run_off[g];
+      for (i64 i = a; i < b; ++i) {
+        if (i == a || gi[i] != gi[i - 1] + 1) {
+          rs[r] = gi[i];
+          rl[r++] = 1;
+        } else {
+          ++rl[r - 1];
+        }
+      }
+    }
+  }, 1 << 10);
+}
+
+// min / max of an int64 array (the plan's int32 range check)
+void pcc_minmax(const i64* a, i64 n, i64* out) {
+  std::vector<i64> mn(nthreads(), INT64_MAX), mx(nthreads(), INT64_MIN);
+  pfor(n, [&](i64 lo, i64 hi, int t) {
+    i64 x = INT64_MAX, y = INT64_MIN;
+    for (i64 i = lo; i < hi; ++i) x = std::min(x, a[i]), y = std::max(y, a[i]);
+    mn[t] = std::min(mn[t], x), mx[t] = std::max(mx[t], y);
+  }, 1 << 20);
+  out[0] = *std::min_element(mn.begin(), mn.end());
+  out[1] = *std::max_element(mx.begin(), mx.end());
+}
+
+// dst = int32(src), checked beforehand
+void pcc_narrow_i32(const i64* src, i64 n, int32_t* dst) {
+  pfor(n, [&](i64 lo, i64 hi, int) {
+    for (i64 i = lo; i < hi; ++i) dst[i] = (int32_t)src[i];
+  }, 1 << 20);
 }
 
 // graph_hash records (build.py:634-657) of rows [0, count) of one segment:

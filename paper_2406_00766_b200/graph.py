@@ -492,6 +492,21 @@ class CircuitGraph:
         """Topological depth: inputs 0, else 1 + max child depth (``build.py:103-110``)."""
         depth = np.zeros(self._num_nodes, dtype=np.int64)
         if self._ordered():
+            from .compiler import _native
+            nat = _native.lib()
+            if nat is not None and self.segments:
+                segs = self.segments
+                ch = [None if s.kind == KIND_INPUT else _native.rows(s.children) for s in segs]
+                rs = np.array([0 if c is None else c[1] for c in ch], np.int64)
+                st = np.array([s.start for s in segs], np.int64)
+                cn = np.array([s.count for s in segs], np.int64)
+                fn = np.array([s.fan_in for s in segs], np.int64)
+                kd = np.array([s.kind for s in segs], np.int8)
+                tab = _native.addr_array([0 if c is None else _native.addr(c[0]) for c in ch])
+                nat.pcc_depths(len(segs), _native.ptr(st), _native.ptr(cn), _native.ptr(fn),
+                               _native.ptr(kd), _native.ptr(tab), _native.ptr(rs),
+                               _native.ptr(depth))
+                return depth
             for s in self.segments:
                 if s.kind != KIND_INPUT:
                     depth[s.start:s.stop] = 1 + depth[s.children].max(axis=1)

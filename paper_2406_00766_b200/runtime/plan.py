@@ -28,25 +28,50 @@ INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
 
 
+def _host_lib():
+    """The native host library (compiler/_native.py), or None."""
+    from ..compiler import _native
+    return _native.lib()
+
+
 class _Blob:
     def __init__(self):
         self.parts: list[np.ndarray] = []
         self.size = 0
 
     def add(self, arr) -> tuple[int, int]:
-        a = np.ascontiguousarray(np.asarray(arr, dtype=np.int64).ravel())
-        if a.size and (a.max() > INT32_MAX or a.min() < -INT32_MAX):
-            raise UsageError("index table exceeds int32 range")
+        a = np.asarray(arr).ravel()
+        if a.size:
+            nat = _host_lib() if a.size >= (1 << 20) else None
+            if nat is not None and a.dtype == np.int64 and a.flags.c_contiguous:
+                mm = np.empty(2, np.int64)
+                nat.pcc_minmax(a.ctypes.data, a.size, mm.ctypes.data)
+                lo, hi = int(mm[0]), int(mm[1])
+            else:
+                lo, hi = int(a.min()), int(a.max())
+            if hi > INT32_MAX or lo < -INT32_MAX:
+                raise UsageError("index table exceeds int32 range")
         off = self.size
         if a.size:
-            self.parts.append(a.astype(np.int32))
+            self.parts.append(a)  # narrowed once, into the final table
             self.size += a.size
         return off, int(a.size)
 
     def array(self) -> np.ndarray:
         if not self.parts:
             return np.zeros(1, dtype=np.int32)
-        return np.concatenate(self.parts)
+        out = np.empty(self.size, dtype=np.int32)
+        nat = _host_lib()
+        pos = 0
+        for a in self.parts:
+            if nat is not None and a.size >= (1 << 20) and a.dtype == np.int64 \
+                    and a.flags.c_contiguous:
+                nat.pcc_narrow_i32(a.ctypes.data, a.size, out[pos:].ctypes.data)
+            else:
+                np.copyto(out[pos:pos + a.size], a, casting="unsafe")
+            pos += a.size
+        self.parts = []
+        return out
 
 
 SMS = 148  # B200 streaming multiprocessors
@@ -435,6 +460,19 @@ def group_runs(group_idx, group_off):
     n = gi.size
     if n == 0:
         return np.zeros(go.size, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64)
+    from ..compiler import _native
+    nat = _native.lib()
+    if nat is not None:  # native two-pass encoding (no whole-table temporaries)
+        gi, go = _native.i64(gi), _native.i64(go)
+        ng = go.size - 1
+        run_off = np.zeros(ng + 1, np.int64)
+        nat.pcc_group_runs(ng, _native.ptr(go), _native.ptr(gi), _native.ptr(run_off), None, None)
+        np.cumsum(run_off, out=run_off)
+        rs = np.empty(int(run_off[-1]), np.int64)
+        rl = np.empty_like(rs)
+        nat.pcc_group_runs(ng, _native.ptr(go), _native.ptr(gi), _native.ptr(run_off),
+                           _native.ptr(rs), _native.ptr(rl))
+        return run_off, rs, rl
     brk = np.ones(n, dtype=bool)
     brk[1:] = gi[1:] != gi[:-1] + 1
     brk[go[:-1][go[:-1] < n]] = True          # every group starts a run
@@ -487,10 +525,13 @@ def em_tile_blocks(compiled, t_start, t_slab_f, t_slab_c, t_km, t_kn):
         cnt = np.bincount(inv, minlength=key.shape[0])
         torder = np.argsort(inv, kind="stable")
         offs = np.concatenate([[0], np.cumsum(cnt)])
-        for b in range(key.shape[0]):
+        # every group of a block lives exactly in its tiles, and is distinct
+        ks = np.sort(key, axis=1)
+        distinct = (ks[:, 1:] != ks[:, :-1]).all(axis=1) if km > 1 else np.ones(key.shape[0], bool)
+        exact = (n_runs_of[key] == cnt[:, None]).all(axis=1)
+        for b in np.flatnonzero(distinct & exact).tolist():
             grp = key[b]
-            # every group of the block lives exactly in these tiles (and is distinct)
-            if np.unique(grp).size != km or np.any(n_runs_of[grp] != cnt[b]) or covered[grp].any():
+            if covered[grp].any():
                 continue
             blocks.append((km, kn, grp, tiles[torder[offs[b]:offs[b + 1]]]))
             covered[grp] = True
@@ -1002,17 +1043,27 @@ def build_program(compiled, *, tensor_cores: bool = True):
     contig[one] = gi[np.minimum(go[:-1][one], max(gi.size - 1, 0))]
     # small groups that are exactly a staged input's pmf (ncat <= 256) go
     # last among the small ones: the inline input EM updates them
-    in_pmf = {}
+    def map_eq(keys, vals, q, want):
+        """q in keys and (last value of q) == want, vectorised dict lookup."""
+        keys, vals = np.asarray(keys, np.int64), np.asarray(vals, np.int64)
+        if keys.size == 0 or q.size == 0:
+            return np.zeros(q.size, dtype=bool)
+        ks, idx = np.unique(keys[::-1], return_index=True)  # last occurrence wins
+        vs = vals[::-1][idx]
+        pos = np.minimum(np.searchsorted(ks, q), ks.size - 1)
+        return (ks[pos] == q) & (vs[pos] == want)
+
+    crest = contig[rest] if rest.size else np.zeros(0, np.int64)
     if nb:
         ncat_of = np.repeat(blocks["ncat"], blocks["count"])
-        in_pmf = dict(zip(blocks["pids"].tolist(), ncat_of.tolist()))
-    inl = np.array([bool(contig[g] >= 0 and in_pmf.get(int(contig[g])) == int(sz) and sz <= 256)
-                    for g, sz in zip(rest.tolist(), gsize.tolist())], dtype=bool)
+        inl = (crest >= 0) & map_eq(blocks["pids"], ncat_of, crest, gsize) & (gsize <= 256)
+    else:
+        inl = np.zeros(rest.size, dtype=bool)
     small = gsize < EM_BIG
     # groups that are exactly a shared pmf (shared_pmf_table) go last: the
     # shared-pmf input-flow pass updates them inline
-    sinl = np.array([bool(contig[g] >= 0 and shared_pids.get(int(contig[g])) == int(sz))
-                     for g, sz in zip(rest.tolist(), gsize.tolist())], dtype=bool)
+    sinl = (crest >= 0) & map_eq(list(shared_pids.keys()), list(shared_pids.values()), crest,
+                                 gsize)
     inl = inl & ~sinl
     n_shared_inline = int(sinl.sum())
     shared_inline_ok = bool(shared_pids) and n_shared_inline == len(shared_pids)

@@ -179,3 +179,20 @@ def test_numpy_selector(nat, monkeypatch):
     assert _native.lib() is None
     monkeypatch.delenv("PCB_COMPILER")
     assert _native.lib() is not None
+
+
+def test_group_runs_native_equals_numpy(nat, monkeypatch):
+    """runtime/plan.py group_runs: the native two-pass encoding against the
+    numpy one on ragged groups (empty groups, repeats, gaps)."""
+    from paper_2406_00766_b200.runtime.plan import group_runs
+    rng = np.random.default_rng(0)
+    for _ in range(100):
+        sizes = rng.integers(0, 12, int(rng.integers(1, 30)))
+        go = np.concatenate([[0], np.cumsum(sizes)])
+        gi = np.cumsum(rng.integers(0, 3, int(go[-1]))) + int(rng.integers(0, 5))
+        got = group_runs(gi, go)
+        monkeypatch.setenv("PCB_COMPILER", "numpy")
+        want = group_runs(gi, go)
+        monkeypatch.delenv("PCB_COMPILER")
+        for a, b in zip(got, want):
+            np.testing.assert_array_equal(a, b)
