@@ -94,15 +94,25 @@ def build_circuit(w):
     return _build_circuit(w)
 
 
+HOST_BUILD: dict = {}  # last _build_circuit's host timings (bench line: config.host_build)
+
+
 def _build_circuit(w):
     from paper_2406_00766_b200 import structures as S
-    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.compiler import CompileConfig, _native, compile_circuit
     keys = ("kind", "num_vars", "hidden_dim", "num_categories", "seq_len", "vocab_size",
             "shape", "split_interval", "elementwise", "depth", "num_input_components",
             "num_repetitions")
     cfg = S.StructureConfig(seed=0, tied=True, **{k: w[k] for k in keys if k in w})
+    t0 = time.perf_counter()
     g = S.build_structure(cfg)
+    t1 = time.perf_counter()
     c = compile_circuit(g, CompileConfig(block_size=w["block"]), validate=False)
+    t2 = time.perf_counter()
+    HOST_BUILD.clear()
+    HOST_BUILD.update(structure_s=round(t1 - t0, 2), compile_s=round(t2 - t1, 2),
+                      compiler="native" if _native.lib() is not None else "numpy",
+                      host_threads=os.cpu_count())
     return c
 
 
@@ -412,8 +422,9 @@ def run_ours(args, w):
             dist.init_process_group(backend)
     t0 = time.time()
     c = build_circuit(w)
+    host_build = dict(HOST_BUILD)
     log(f"[bench] compiled {args.workload}: {c.num_edges} edges, theta {c.theta_size} "
-        f"in {time.time() - t0:.1f}s")
+        f"in {time.time() - t0:.1f}s {host_build}")
     # strong scaling (north_star: the config's mini-batch is sharded across
     # the GPUs): global batch = the config's, this rank's contiguous span of
     # it (the reference's _chunk_ranges split); --scaling weak keeps the
@@ -431,8 +442,10 @@ def run_ours(args, w):
     # bucketed NCCL all-reduce of the parameter flows is captured with it.
     # The same cached step (buffers, graph) serves train() below.
     graphed = not args.no_graph and (world == 1 or backend == "nccl")
+    t0 = time.perf_counter()
     ts = cached_step(c, B, pseudocount=PSEUDOCOUNT, step_size=STEP_SIZE, device=dev,
                      graph=graphed)
+    host_build["plan_and_upload_s"] = round(time.perf_counter() - t0, 2)
     plan = ts.plan
     run = ts.run
 
@@ -611,7 +624,8 @@ def run_ours(args, w):
                                          "data",
                    "l2": "working set >> 126 MB L2 (no flush)",
                    "parallelism": f"dp{world}", "cuda_graph": graphed,
-                   "em_in_backward": inline_em},
+                   "em_in_backward": inline_em,
+                   "host_build": host_build or "loaded from PCB_CIRCUIT_CACHE"},
         "e2e": {"value": e2e_value, "unit": "samples/s",
                 "h2d_bytes_per_step": B * c.num_vars * 4,
                 "d2h_bytes_per_step": 8,
