@@ -345,6 +345,7 @@ namespace {
 
 __global__ void k_check_batch(int64_t nv, int B, int ldb, const int32_t* __restrict__ ncat,
                               const int32_t* __restrict__ xT, int32_t* bad) {
+  pdl_enter();
   int64_t total = nv * (int64_t)B;
   int cnt = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -360,6 +361,7 @@ __global__ void k_check_batch(int64_t nv, int B, int ldb, const int32_t* __restr
 template <typename T>
 __global__ void k_transpose(int64_t nv, int B, int ldb, const T* __restrict__ x,
                             int32_t* __restrict__ xT) {
+  pdl_enter();
   __shared__ int32_t tile[32][33];
   const int64_t v0 = (int64_t)blockIdx.x * 32;
   const int b0 = blockIdx.y * 32;
@@ -377,12 +379,14 @@ __global__ void k_transpose(int64_t nv, int B, int ldb, const T* __restrict__ x,
 }
 
 __global__ void k_axpy(int64_t n, const float* __restrict__ a, float* __restrict__ y) {
+  pdl_enter();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x)
     y[t] += a[t];
 }
 
 __global__ void k_nonfinite(int64_t n, const float* __restrict__ x, int32_t* cnt) {
+  pdl_enter();
   int c = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x)
@@ -668,7 +672,7 @@ int pcb_check_batch(const pcb_plan* plan, void* stream, int B, int ldb, const in
                     int32_t* d_bad) {
   if (bad_dims(plan, B, ldb)) return PCB_USAGE;
   if (!B) return PCB_OK;
-  k_check_batch<<<grid_for(plan->num_vars * B, 256), 256, 0, as_stream(stream)>>>(
+  launch_k(k_check_batch, dim3(grid_for(plan->num_vars * B, 256)), dim3(256), 0, as_stream(stream), 
       plan->num_vars, B, ldb, plan->var_ncat, d_xT, d_bad);
   return check_launch();
 }
@@ -678,7 +682,7 @@ int pcb_transpose_batch_i64(const pcb_plan* plan, void* stream, int B, int ldb,
   if (bad_dims(plan, B, ldb)) return PCB_USAGE;
   if (!B) return PCB_OK;
   dim3 grid((unsigned)((plan->num_vars + 31) / 32), (unsigned)((B + 31) / 32));
-  k_transpose<int64_t><<<grid, dim3(32, 8), 0, as_stream(stream)>>>(plan->num_vars, B, ldb, d_x,
+  launch_k((k_transpose<int64_t>), dim3(grid), dim3(dim3(32, 8)), 0, as_stream(stream), plan->num_vars, B, ldb, d_x,
                                                                      d_xT);
   return check_launch();
 }
@@ -688,7 +692,7 @@ int pcb_transpose_batch_i32(const pcb_plan* plan, void* stream, int B, int ldb,
   if (bad_dims(plan, B, ldb)) return PCB_USAGE;
   if (!B) return PCB_OK;
   dim3 grid((unsigned)((plan->num_vars + 31) / 32), (unsigned)((B + 31) / 32));
-  k_transpose<int32_t><<<grid, dim3(32, 8), 0, as_stream(stream)>>>(plan->num_vars, B, ldb, d_x,
+  launch_k((k_transpose<int32_t>), dim3(grid), dim3(dim3(32, 8)), 0, as_stream(stream), plan->num_vars, B, ldb, d_x,
                                                                      d_xT);
   return check_launch();
 }
@@ -793,7 +797,7 @@ int pcb_em_update(const pcb_plan* plan, void* stream, const float* d_f_params, f
 
 int pcb_axpy_accumulate(void* stream, int64_t n, const float* d_src, float* d_dst) {
   if (n <= 0) return PCB_OK;
-  k_axpy<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, d_src, d_dst);
+  launch_k(k_axpy, dim3(grid_for(n, 256)), dim3(256), 0, as_stream(stream), n, d_src, d_dst);
   return check_launch();
 }
 
@@ -801,7 +805,7 @@ int pcb_count_nonfinite(void* stream, int64_t n, const float* d_x, int32_t* d_co
   cudaStream_t s = as_stream(stream);
   if (cudaMemsetAsync(d_count, 0, sizeof(int32_t), s) != cudaSuccess) return PCB_CUDA;
   if (n <= 0) return PCB_OK;
-  k_nonfinite<<<grid_for(n, 256), 256, 0, s>>>(n, d_x, d_count);
+  launch_k(k_nonfinite, dim3(grid_for(n, 256)), dim3(256), 0, s, n, d_x, d_count);
   return check_launch();
 }
 

@@ -294,6 +294,39 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
 
 int check_launch();
 
+// Programmatic dependent launch (PDL).  Every kernel of the library is
+// launched through launch_k with cudaLaunchAttributeProgrammaticStream-
+// Serialization, and begins with pdl_enter(): griddepcontrol.wait (the
+// previous kernel in the stream has completed and its writes are visible --
+// no global access happens before it).  No kernel triggers its dependents
+// early (the implicit trigger is each CTA's exit): the launch of the next
+// kernel is processed ahead and released as this one drains, instead of
+// after it (inside CUDA graphs: a programmatic edge).  An early
+// griddepcontrol.launch_dependents at kernel entry was measured slower
+// (HCLT-256 61.8k vs 62.9k samples/s, HMM-4096 34.4k vs 37.5k): dependent
+// CTAs parked on the SMs beside the running kernel cost it issue slots.
+// PCB_NO_PDL=1 launches without the attribute (plain stream order; the
+// wait is then a no-op).
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 // SIMT kernels (pcb_simt.cu).  Base rows: `pbase` / `vbase` point at the
 // layer's first product / sum block row (Layer::pb_off / vb_off), except
 // where noted.

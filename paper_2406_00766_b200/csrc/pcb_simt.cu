@@ -14,6 +14,11 @@ namespace pcb {
 
 unsigned long long g_launches = 0;
 
+bool pdl_enabled() {
+  static const bool on = getenv("PCB_NO_PDL") == nullptr;
+  return on;
+}
+
 int check_launch() {
   ++g_launches;
   cudaError_t e = cudaGetLastError();
@@ -98,6 +103,7 @@ __global__ void k_input_fwd(int64_t n, int B, int ldb, const int32_t* __restrict
                             const int32_t* __restrict__ vars, const int32_t* __restrict__ pids,
                             const int32_t* __restrict__ xT, const float* __restrict__ theta,
                             float* __restrict__ values) {
+  pdl_enter();
   int64_t total = n * (int64_t)B;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -126,6 +132,7 @@ __global__ void __launch_bounds__(IN_THREADS)
                       const float* __restrict__ theta, float* __restrict__ values,
                       const int32_t* __restrict__ arow, const int32_t* __restrict__ adir,
                       float* __restrict__ ascratch, float* __restrict__ abmax, int kn) {
+  pdl_enter();
   extern __shared__ float tbl[];
   const int blk = blockIdx.x;
   const int ncat = bncat[blk], cnt = bcount[blk], var = bvar[blk];
@@ -218,6 +225,7 @@ __global__ void __launch_bounds__(SP_THREADS)
                        const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
                        const int32_t* __restrict__ u_var, const int32_t* __restrict__ xT,
                        const float* __restrict__ theta, float* __restrict__ values) {
+  pdl_enter();
   extern __shared__ float tbl[];
   const int u = blockIdx.x, tid = threadIdx.x;
   const float* th = theta + __ldg(u_pid + u);
@@ -255,7 +263,7 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
     if (ensure_smem((const void*)k_input_fwd_block, bytes, attr)) return PCB_CUDA;
     alias = alias && p->leaf_alias;
     const Layer* L0 = alias ? &p->layers[0] : nullptr;
-    k_input_fwd_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
+    launch_k(k_input_fwd_block, dim3((unsigned)ib.n), dim3(IN_THREADS), bytes, s, 
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, values,
         alias ? ib.alias_row : nullptr, ib.alias_dir,
         alias ? scratch_all + L0->scratch_off * (int64_t)ldb : nullptr,
@@ -270,12 +278,12 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
       const int bytes = (int)c.ncat * 4;
       static int attr_sp[kMaxDev] = {};
       if (ensure_smem((const void*)k_input_fwd_shared, bytes, attr_sp)) return PCB_CUDA;
-      k_input_fwd_shared<<<(unsigned)c.n_u, SP_THREADS, bytes, s>>>(
+      launch_k(k_input_fwd_shared, dim3((unsigned)c.n_u), dim3(SP_THREADS), bytes, s, 
           (int)c.ncat, B, ldb, c.u_pid, c.u_off, c.u_slot, c.u_var, xT, theta, values);
       if (check_launch()) return PCB_CUDA;
       continue;
     }
-    k_input_fwd<<<grid_for(total, 256), 256, 0, s>>>(c.n, B, ldb, c.slots, c.vars, c.pids, xT,
+    launch_k(k_input_fwd, dim3(grid_for(total, 256)), dim3(256), 0, s, c.n, B, ldb, c.slots, c.vars, c.pids, xT,
                                                       theta, values);
     if (check_launch()) return PCB_CUDA;
   }
@@ -285,6 +293,7 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
 // ---------------------------------------------------------------- K2 products
 __global__ void k_fill_rows(int64_t n, int B, int ldb, const int32_t* __restrict__ rows,
                             float* __restrict__ buf, float v) {
+  pdl_enter();
   int64_t total = n * (int64_t)B;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -297,12 +306,13 @@ __global__ void k_fill_rows(int64_t n, int B, int ldb, const int32_t* __restrict
 int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, float* buf,
                 float v) {
   if (!n) return PCB_OK;
-  k_fill_rows<<<grid_for(n * B, 256), 256, 0, s>>>(n, B, ldb, rows, buf, v);
+  launch_k(k_fill_rows, dim3(grid_for(n * B, 256)), dim3(256), 0, s, n, B, ldb, rows, buf, v);
   return check_launch();
 }
 
 __global__ void k_fill_range(int64_t row0, int64_t n, int B, int ldb, float* __restrict__ buf,
                              float v) {
+  pdl_enter();
   int64_t total = n * (int64_t)B;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -315,6 +325,7 @@ __global__ void k_fill_range(int64_t row0, int64_t n, int B, int ldb, float* __r
 // zero rows [start_r, start_r + len_r) of a [rows x ldb] buffer for every range r
 __global__ void k_zero_ranges(int64_t n, const int32_t* __restrict__ start,
                               const int32_t* __restrict__ len, int ldb, float* __restrict__ buf) {
+  pdl_enter();
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
     float4* p = reinterpret_cast<float4*>(buf + (int64_t)__ldg(start + r) * ldb);
@@ -326,7 +337,7 @@ __global__ void k_zero_ranges(int64_t n, const int32_t* __restrict__ start,
 int launch_zero_ranges(cudaStream_t s, int64_t n, const int32_t* start, const int32_t* len,
                        int ldb, float* buf) {
   if (!n) return PCB_OK;
-  k_zero_ranges<<<grid_for(n, 1, 148 * 16), 256, 0, s>>>(n, start, len, ldb, buf);
+  launch_k(k_zero_ranges, dim3(grid_for(n, 1, 148 * 16)), dim3(256), 0, s, n, start, len, ldb, buf);
   return check_launch();
 }
 
@@ -334,7 +345,7 @@ int launch_fill_range(cudaStream_t s, int64_t row0, int64_t n, int B, int ldb, f
                       float v) {
   ProfScope prof_(KC_MISC, s);
   if (!n || !B) return PCB_OK;
-  k_fill_range<<<grid_for(n * B, 256), 256, 0, s>>>(row0, n, B, ldb, buf, v);
+  launch_k(k_fill_range, dim3(grid_for(n * B, 256)), dim3(256), 0, s, row0, n, B, ldb, buf, v);
   return check_launch();
 }
 
@@ -382,6 +393,7 @@ __global__ void __launch_bounds__(RW * 32, (UNI && PER == 4) ? 4 : 2)
                  const int32_t* __restrict__ ch, const int32_t* __restrict__ cb,
                  const float* __restrict__ values, const float* __restrict__ vbase,
                  float* __restrict__ scratch, float* __restrict__ pbase) {
+  pdl_enter();
   const int blk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.y * SLAB + lane * VB;
@@ -463,10 +475,10 @@ int launch_prod_eval(const Layer& L, cudaStream_t s, int B, int ldb, const float
   dim3 grid((unsigned)L.n_pb, (unsigned)((B + SLAB - 1) / SLAB));
 #define PCB_PB(PER)                                                                          \
   (L.prod_uniform                                                                            \
-       ? k_prod_block<PER, true><<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off,    \
+       ? launch_k((k_prod_block<PER, true>), dim3(grid), dim3(RW * 32), 0, s, (int)L.k_n, B, ldb, L.prow_off,    \
                                                           L.prow_ch, L.prow_cb, values,     \
                                                           vbase_all, scratch, pbase)        \
-       : k_prod_block<PER, false><<<grid, RW * 32, 0, s>>>((int)L.k_n, B, ldb, L.prow_off,   \
+       : launch_k((k_prod_block<PER, false>), dim3(grid), dim3(RW * 32), 0, s, (int)L.k_n, B, ldb, L.prow_off,   \
                                                            L.prow_ch, L.prow_cb, values,    \
                                                            vbase_all, scratch, pbase))
   if (L.k_n <= RW) PCB_PB(1);
@@ -491,6 +503,7 @@ constexpr int KM_MAX = 64;
 __global__ void __launch_bounds__(RW * 32, 5)
     k_ratio(int k_m, int B, int ldb, int64_t sb_base, const float* __restrict__ values,
             const float* __restrict__ flows, float* __restrict__ rmax, float* __restrict__ ratio) {
+  pdl_enter();
   constexpr int PER = KM_MAX / RW;
   const int blk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -547,7 +560,7 @@ int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float
   if (!B || !L.n_sb) return PCB_OK;
   if (L.k_m > KM_MAX) return PCB_USAGE;
   dim3 grid((unsigned)L.n_sb, (unsigned)((B + SLAB - 1) / SLAB));
-  k_ratio<<<grid, RW * 32, 0, s>>>((int)L.k_m, B, ldb, L.sb_base, values, flows, rmax, ratio);
+  launch_k(k_ratio, dim3(grid), dim3(RW * 32), 0, s, (int)L.k_m, B, ldb, L.sb_base, values, flows, rmax, ratio);
   return check_launch();
 }
 
@@ -566,6 +579,7 @@ __global__ void __launch_bounds__(RW * 32)
                  const int32_t* __restrict__ qkind, const int32_t* __restrict__ qrrow,
                  const float* __restrict__ fs, const float* __restrict__ values,
                  float* __restrict__ flows, float* __restrict__ rmax_all) {
+  pdl_enter();
   constexpr int PER = (K + RW - 1) / RW;
   const int q = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -632,7 +646,7 @@ int launch_push_ratio(const Layer& L, cudaStream_t s, int B, int ldb, const floa
   if (!B || !L.n_pq) return PCB_OK;
   dim3 grid((unsigned)L.n_pq, (unsigned)((B + SLAB - 1) / SLAB));
 #define PCB_PR(K)                                                                              \
-  k_push_ratio<K><<<grid, RW * 32, 0, s>>>(B, ldb, L.q_blk, L.pb_row, L.q_base, L.q_kind,      \
+  launch_k((k_push_ratio<K>), dim3(grid), dim3(RW * 32), 0, s, B, ldb, L.q_blk, L.pb_row, L.q_base, L.q_kind,      \
                                            L.q_rrow, flow_scratch, values, flows, rmax_all)
   switch (L.k_n) {
     case 16: PCB_PR(16); break;
@@ -660,6 +674,7 @@ __global__ void __launch_bounds__(TB* TY)
                    const int32_t* __restrict__ param_ids, const float* __restrict__ theta,
                    const float* __restrict__ scratch, const float* __restrict__ pbase,
                    float* __restrict__ values, float* __restrict__ vbase) {
+  pdl_enter();
   __shared__ float ex[KMAX][TB];
   __shared__ float th[KMAX * KMAX];
   __shared__ float cm[TB];
@@ -733,6 +748,7 @@ __global__ void __launch_bounds__(TB* TY)
                     const int32_t* __restrict__ param_ids, const float* __restrict__ theta,
                     const float* __restrict__ scratch, const float* __restrict__ pbase,
                     float* __restrict__ values, float* __restrict__ vbase) {
+  pdl_enter();
   __shared__ float lin_s[TY][TB], top_s[TY][TB], g_s[TY][TB];
   const int r = blockIdx.y;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -793,15 +809,15 @@ int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B
                         float* values, float* vbase) {
   ProfScope prof_(KC_SUM_FWD_SIMT, s);
   if (!g.rows) return PCB_OK;
-  if (L.k_m == 1 && g.cap >= 2 * TY) {
+  if (L.k_m == 1 && g.cap >= 2) {  // thread rows split the child blocks
     dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
-    k_sum_fwd_simt1<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_n, B, ldb, L.sb_base,
+    launch_k(k_sum_fwd_simt1, dim3(grid), dim3(dim3(TB, TY)), 0, s, (int)g.cap, (int)L.k_n, B, ldb, L.sb_base,
                                                   g.sum_ids, g.prod_ids, g.param_ids, theta,
                                                   scratch, pbase, values, vbase);
     return check_launch();
   }
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
-  k_sum_fwd_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
+  launch_k(k_sum_fwd_simt, dim3(grid), dim3(dim3(TB, TY)), 0, s, (int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
                                                L.sb_base, g.sum_ids, g.prod_ids, g.param_ids,
                                                theta, scratch, pbase, values, vbase);
   return check_launch();
@@ -827,6 +843,7 @@ __global__ void __launch_bounds__(PF_THREADS)
                       const float* __restrict__ flows, const float* __restrict__ scratch,
                       const float* __restrict__ pbase, const float* __restrict__ vbase,
                       float* __restrict__ f_params) {
+  pdl_enter();
   __shared__ float sc[KMAX][TB];
   __shared__ float em[KMAX][TB];
   __shared__ float nm[TB];
@@ -888,6 +905,62 @@ __global__ void __launch_bounds__(PF_THREADS)
   }
 }
 
+// Single-sum rows (k_m = 1, e.g. an HCLT / HMM root): the ratio shift is the
+// row's own log ratio, so cum[n] = sum_b exp(child[n,b] + d_b + lr_b).  The
+// eight warps take interleaved 32-sample chunks (lane = sample, coalesced
+// child rows), keep k_n partial sums each, and meet in a fixed-order
+// reduction (warp shuffles, then warp 0..7 in order): deterministic.
+__global__ void __launch_bounds__(PF_THREADS)
+    k_param_flow_simt1(int cap, int k_n, int B, int ldb, int64_t sb_base,
+                       const int32_t* __restrict__ sum_ids, const int32_t* __restrict__ prod_ids,
+                       const int32_t* __restrict__ param_ids, const int32_t* __restrict__ flow_ids,
+                       const float* __restrict__ theta, const float* __restrict__ values,
+                       const float* __restrict__ flows, const float* __restrict__ scratch,
+                       const float* __restrict__ pbase, const float* __restrict__ vbase,
+                       float* __restrict__ f_params) {
+  pdl_enter();
+  constexpr int NW = PF_THREADS / 32;
+  __shared__ float red[NW][KMAX];
+  const int r = blockIdx.y, c = blockIdx.x;
+  const int tid0 = param_ids[(int64_t)r * cap + c];
+  if (tid0 == 0) return;
+  const int pid = prod_ids[(int64_t)r * cap + c];
+  const int fid = flow_ids[(int64_t)r * cap + c];
+  const int sid = sum_ids[r];
+  const float* pb = pbase + (int64_t)(pid / k_n) * ldb;
+  const float* vb = vbase + (int64_t)(sid - sb_base) * ldb;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float acc[KMAX];
+#pragma unroll
+  for (int n = 0; n < KMAX; ++n) acc[n] = 0.f;
+  for (int b = w * 32 + lane; b < B; b += NW * 32) {
+    const int64_t o = (int64_t)sid * ldb + b;
+    const float lr = log_ratio(flows[o], values[o]);
+    if (lr == PCB_NEG_INF) continue;
+    const float e = lr + (pb[b] - vb[b]);
+#pragma unroll
+    for (int n = 0; n < KMAX; ++n)
+      if (n < k_n) acc[n] += expf(scratch[(int64_t)(pid + n) * ldb + b] + e);
+  }
+#pragma unroll
+  for (int n = 0; n < KMAX; ++n) {
+    if (n >= k_n) break;
+    float v = acc[n];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[w][n] = v;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < k_n) {
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) sum += red[q][t];
+    const float th = __ldg(theta + tid0 + t);
+    if (th != 0.f) atomicAdd(f_params + fid + t, th * sum);
+  }
+}
+
 int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B, int ldb,
                            const float* theta, const float* values, const float* flows,
                            const float* scratch, const float* pbase, const float* vbase,
@@ -895,7 +968,14 @@ int launch_param_flow_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, in
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!g.rows || !g.cap) return PCB_OK;
   dim3 grid((unsigned)g.cap, (unsigned)g.rows);
-  k_param_flow_simt<<<grid, PF_THREADS, 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
+  if (L.k_m == 1) {
+    launch_k(k_param_flow_simt1, dim3(grid), dim3(PF_THREADS), 0, s, (int)g.cap, (int)L.k_n, B, ldb, L.sb_base,
+                                                   g.sum_ids, g.prod_ids, g.param_ids, g.flow_ids,
+                                                   theta, values, flows, scratch, pbase, vbase,
+                                                   f_params);
+    return check_launch();
+  }
+  launch_k(k_param_flow_simt, dim3(grid), dim3(PF_THREADS), 0, s, (int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
                                                 L.sb_base, g.sum_ids, g.prod_ids, g.param_ids,
                                                 g.flow_ids, theta, values, flows, scratch, pbase,
                                                 vbase, f_params);
@@ -913,6 +993,7 @@ __global__ void __launch_bounds__(TB* TY)
                       const float* __restrict__ values, const float* __restrict__ flows,
                       const float* __restrict__ scratch, const float* __restrict__ pbase,
                       const float* __restrict__ vbase, float* __restrict__ flow_scratch) {
+  pdl_enter();
   __shared__ float sc[KMAX][TB];
   __shared__ float th[KMAX * KMAX];
   __shared__ float nm[TB];
@@ -986,7 +1067,7 @@ int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, in
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!g.rows) return PCB_OK;
   dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
-  k_child_flow_simt<<<grid, dim3(TB, TY), 0, s>>>((int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
+  launch_k(k_child_flow_simt, dim3(grid), dim3(dim3(TB, TY)), 0, s, (int)g.cap, (int)L.k_m, (int)L.k_n, B, ldb,
                                                   L.sb_base, g.ch_ids, g.par_ids,
                                                   g.par_param_ids, theta, values, flows, scratch,
                                                   pbase, vbase, flow_scratch);
@@ -998,6 +1079,7 @@ int launch_child_flow_simt(const Layer& L, const BwdGroup& g, cudaStream_t s, in
 __global__ void k_prod_accum(int64_t n, int B, int ldb, const int32_t* __restrict__ slots,
                              const int32_t* __restrict__ rows, const float* __restrict__ fs,
                              float* __restrict__ pf) {
+  pdl_enter();
   int64_t total = n * (int64_t)B;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1011,6 +1093,7 @@ __global__ void k_prod_accum(int64_t n, int B, int ldb, const int32_t* __restric
 __global__ void k_push(int64_t n, int f, int B, int ldb, const int32_t* __restrict__ rows,
                        const int32_t* __restrict__ ch, const float* __restrict__ pf,
                        float* __restrict__ flows) {
+  pdl_enter();
   int64_t total = n * (int64_t)B;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1034,6 +1117,7 @@ __global__ void __launch_bounds__(RW * 32)
                 const int32_t* __restrict__ rows, const int32_t* __restrict__ flag,
                 const int32_t* __restrict__ poff, const int32_t* __restrict__ pch,
                 const float* __restrict__ fs, float* __restrict__ pf, float* __restrict__ flows) {
+  pdl_enter();
   // each warp takes PU consecutive product rows; their index loads, then
   // their flow loads, are issued together before any store
   constexpr int PU = 4;
@@ -1090,7 +1174,7 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
   ProfScope prof_(KC_ACCUM_PUSH, s);
   if (!B || !L.n_prod) return PCB_OK;
   dim3 grid((unsigned)((L.n_prod + RW * 4 - 1) / (RW * 4)), (unsigned)((B + SLAB - 1) / SLAB));
-  k_flow_push<<<grid, RW * 32, 0, s>>>(L.n_prod, B, ldb, L.prod_slots, L.prod_rows, L.push_flag,
+  launch_k(k_flow_push, dim3(grid), dim3(RW * 32), 0, s, L.n_prod, B, ldb, L.prod_slots, L.prod_rows, L.push_flag,
                                        L.push_off, L.push_ch, flow_scratch, prod_flows, flows);
   return check_launch();
 }
@@ -1098,13 +1182,13 @@ int launch_prod_accum_push(const Layer& L, cudaStream_t s, int B, int ldb,
 int launch_prod_accum_push_buckets(const Layer& L, cudaStream_t s, int B, int ldb,
                                    const float* flow_scratch, float* prod_flows, float* flows) {
   if (L.n_prod) {
-    k_prod_accum<<<grid_for(L.n_prod * B, 256), 256, 0, s>>>(L.n_prod, B, ldb, L.prod_slots,
+    launch_k(k_prod_accum, dim3(grid_for(L.n_prod * B, 256)), dim3(256), 0, s, L.n_prod, B, ldb, L.prod_slots,
                                                               L.prod_rows, flow_scratch, prod_flows);
     if (check_launch()) return PCB_CUDA;
   }
   for (auto& p : L.pushes) {
     if (!p.n) continue;
-    k_push<<<grid_for(p.n * B, 256), 256, 0, s>>>(p.n, (int)p.f, B, ldb, p.idx, p.children,
+    launch_k(k_push, dim3(grid_for(p.n * B, 256)), dim3(256), 0, s, p.n, (int)p.f, B, ldb, p.idx, p.children,
                                                    prod_flows, flows);
     if (check_launch()) return PCB_CUDA;
   }
@@ -1119,6 +1203,7 @@ __global__ void k_input_param_flow(int64_t n, int ncat, int B, int ldb,
                                    const int32_t* __restrict__ vars, const int32_t* __restrict__ pids,
                                    const int32_t* __restrict__ xT, const float* __restrict__ theta,
                                    const float* __restrict__ flows, float* __restrict__ f_params) {
+  pdl_enter();
   // one warp per input node: lanes run along the batch (coalesced flows / x)
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1152,6 +1237,7 @@ __global__ void __launch_bounds__(IN_THREADS)
                        const float* __restrict__ theta, const float* __restrict__ flows,
                        const int32_t* __restrict__ arow, const int32_t* __restrict__ adir,
                        const float* __restrict__ aflows, float* __restrict__ f_params) {
+  pdl_enter();
   extern __shared__ float hist[];
   __shared__ float miss[128];
   const int blk = blockIdx.x;
@@ -1207,6 +1293,7 @@ __global__ void __launch_bounds__(IS_THREADS)
                         const float* __restrict__ aflows, float* __restrict__ f_params,
                         float* __restrict__ em_theta, float kappa, float step,
                         int32_t* __restrict__ status) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t sm_raw[];
   const int blk = blockIdx.x;
   int informative = 0, bad = 0;
@@ -1341,6 +1428,7 @@ __global__ void __launch_bounds__(SP_THREADS)
                         const float* __restrict__ flows, float* __restrict__ theta,
                         float* __restrict__ f_params, int em, float kappa, float step,
                         int32_t* __restrict__ status) {
+  pdl_enter();
   extern __shared__ float hist[];
   __shared__ float red[SP_THREADS / 32];
   const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1431,7 +1519,7 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
   if (ib.n && !hist_only && sorted_bytes <= 160 * 1024) {
     static int attr_s[kMaxDev] = {};
     if (ensure_smem((const void*)k_input_flow_sorted, (int)sorted_bytes, attr_s)) return PCB_CUDA;
-    k_input_flow_sorted<<<(unsigned)ib.n, IS_THREADS, (size_t)sorted_bytes, s>>>(
+    launch_k(k_input_flow_sorted, dim3((unsigned)ib.n), dim3(IS_THREADS), (size_t)sorted_bytes, s, 
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
         arow, ib.alias_dir, flow_scratch, f_params, em_staged ? theta : nullptr,
         em_staged ? em_staged->kappa : 0.f, em_staged ? em_staged->step : 1.f,
@@ -1442,7 +1530,7 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
     const int bytes = (int)ib.max_elems * 4;
     static int attr[kMaxDev] = {};
     if (ensure_smem((const void*)k_input_flow_block, bytes, attr)) return PCB_CUDA;
-    k_input_flow_block<<<(unsigned)ib.n, IN_THREADS, bytes, s>>>(
+    launch_k(k_input_flow_block, dim3((unsigned)ib.n), dim3(IN_THREADS), bytes, s, 
         B, ldb, ib.var, ib.ncat, ib.slot0, ib.count, ib.pid_off, ib.pids, xT, theta, flows,
         arow, ib.alias_dir, flow_scratch, f_params);
     if (check_launch()) return PCB_CUDA;
@@ -1454,14 +1542,14 @@ int launch_input_param_flows(const pcb_plan* p, cudaStream_t s, int B, int ldb,
       const int bytes = (int)c.ncat * 4;
       static int attr_sp[kMaxDev] = {};
       if (ensure_smem((const void*)k_input_flow_shared, bytes, attr_sp)) return PCB_CUDA;
-      k_input_flow_shared<<<(unsigned)c.n_u, SP_THREADS, bytes, s>>>(
+      launch_k(k_input_flow_shared, dim3((unsigned)c.n_u), dim3(SP_THREADS), bytes, s, 
           (int)c.ncat, B, ldb, c.u_pid, c.u_off, c.u_slot, c.u_var, xT, flows, theta, f_params,
           em_shared ? 1 : 0, em ? em->kappa : 0.f, em ? em->step : 1.f,
           em ? em->status : nullptr);
       if (check_launch()) return PCB_CUDA;
       continue;
     }
-    k_input_param_flow<<<grid_for(c.n * 32, 256), 256, 0, s>>>(c.n, (int)c.ncat, B, ldb, c.slots,
+    launch_k(k_input_param_flow, dim3(grid_for(c.n * 32, 256)), dim3(256), 0, s, c.n, (int)c.ncat, B, ldb, c.slots,
                                                                c.vars, c.pids, xT, theta, flows,
                                                                f_params);
     if (check_launch()) return PCB_CUDA;
@@ -1475,6 +1563,7 @@ __global__ void k_root_fwd(int B, int ldb, int64_t root_slot, int64_t root_vb,
                            const int32_t* __restrict__ rc, const int32_t* __restrict__ rcb,
                            int nrc, const float* __restrict__ values,
                            const float* __restrict__ vbase, float* __restrict__ lroot) {
+  pdl_enter();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   // base + offset in double: |log p| may exceed the fp32 spacing of the parts
@@ -1495,7 +1584,7 @@ __global__ void k_root_fwd(int B, int ldb, int64_t root_slot, int64_t root_vb,
 int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const float* values,
                     const float* vbase_all, float* lroot) {
   ProfScope prof_(KC_MISC, s);
-  k_root_fwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_vb, p->root_children,
+  launch_k(k_root_fwd, dim3((B + 255) / 256), dim3(256), 0, s, B, ldb, p->root_slot, p->root_vb, p->root_children,
                                               p->root_cb, (int)p->n_root_children, values,
                                               vbase_all, lroot);
   return check_launch();
@@ -1504,6 +1593,7 @@ int launch_root_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const flo
 __global__ void k_root_bwd(int B, int ldb, int64_t root_slot, int64_t root_row,
                            const int32_t* __restrict__ rc, int nrc, float* __restrict__ flows,
                            float* __restrict__ pf) {
+  pdl_enter();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   if (root_slot >= 0) {
@@ -1517,7 +1607,7 @@ __global__ void k_root_bwd(int B, int ldb, int64_t root_slot, int64_t root_row,
 int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* flows,
                     float* prod_flows) {
   ProfScope prof_(KC_MISC, s);
-  k_root_bwd<<<(B + 255) / 256, 256, 0, s>>>(B, ldb, p->root_slot, p->root_row,
+  launch_k(k_root_bwd, dim3((B + 255) / 256), dim3(256), 0, s, B, ldb, p->root_slot, p->root_row,
                                               p->root_children, (int)p->n_root_children, flows,
                                               prod_flows);
   return check_launch();
@@ -1529,6 +1619,7 @@ int launch_root_bwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, float* fl
 __global__ void k_replica_reduce(int64_t n_dst, const int32_t* __restrict__ dst,
                                  const int32_t* __restrict__ len, const int32_t* __restrict__ soff,
                                  const int32_t* __restrict__ src, float* __restrict__ f) {
+  pdl_enter();
   for (int64_t d = blockIdx.x; d < n_dst; d += gridDim.x) {
     const int L = len[d];
     const int a = soff[d], z = soff[d + 1];
@@ -1543,7 +1634,7 @@ __global__ void k_replica_reduce(int64_t n_dst, const int32_t* __restrict__ dst,
 int launch_replica_reduce(const pcb_plan* p, cudaStream_t s, float* f_params) {
   ProfScope prof_(KC_REPLICA, s);
   if (!p->red_n) return PCB_OK;
-  k_replica_reduce<<<grid_for(p->red_n, 1, 148 * 16), 256, 0, s>>>(
+  launch_k(k_replica_reduce, dim3(grid_for(p->red_n, 1, 148 * 16)), dim3(256), 0, s, 
       p->red_n, p->red_dst, p->red_len, p->red_src_off, p->red_src, f_params);
   return check_launch();
 }
@@ -1556,6 +1647,7 @@ __global__ void k_em(int64_t n_list, const int32_t* __restrict__ glist,
                      const int32_t* __restrict__ gstart, const int32_t* __restrict__ gidx,
                      const int32_t* __restrict__ goff, const float* __restrict__ F,
                      float* __restrict__ theta, float kappa, float step, int32_t* status) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1622,6 +1714,7 @@ __global__ void __launch_bounds__(256)
              const int32_t* __restrict__ gstart, const int32_t* __restrict__ gidx,
              const int32_t* __restrict__ goff, const float* __restrict__ F,
              float* __restrict__ theta, float kappa, float step, int32_t* status) {
+  pdl_enter();
   __shared__ float red[8];
   __shared__ float tot_s;
   int informative = 0, bad = 0;
@@ -1669,13 +1762,13 @@ int launch_em(const pcb_plan* p, cudaStream_t s, const float* f_params, float* t
   const int64_t ns = skip_inline ? p->n_em_small_noninl : p->n_em_small;
   if (ns) {
     int blocks = grid_for(ns * 32, 256, 148 * 16);
-    k_em<<<blocks, 256, 0, s>>>(ns, p->em_rest, p->em_rest_start, p->group_idx, p->group_off,
+    launch_k(k_em, dim3(blocks), dim3(256), 0, s, ns, p->em_rest, p->em_rest_start, p->group_idx, p->group_off,
                                 f_params, theta, pseudocount, step, status);
     if (check_launch()) return PCB_CUDA;
   }
   if (nb) {
     const int64_t s0 = p->n_em_small;
-    k_em_big<<<grid_for(nb, 1, 148 * 8), 256, 0, s>>>(nb, p->em_rest + s0, p->em_rest_start + s0,
+    launch_k(k_em_big, dim3(grid_for(nb, 1, 148 * 8)), dim3(256), 0, s, nb, p->em_rest + s0, p->em_rest_start + s0,
                                                       p->group_idx, p->group_off, f_params,
                                                       theta, pseudocount, step, status);
     if (check_launch()) return PCB_CUDA;

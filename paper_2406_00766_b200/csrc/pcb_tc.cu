@@ -16,6 +16,7 @@ using namespace tc;
 __global__ void __launch_bounds__(128, 1)
     k_tc_selftest(int n, int k, const uint16_t* __restrict__ A, const uint16_t* __restrict__ Bm,
                   float* __restrict__ D) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + 128 * k * 2;
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(128, 1)
 __global__ void __launch_bounds__(128, 1)
     k_tc_selftest_mn(int n, int k, int variant, const uint16_t* __restrict__ A,
                      const uint16_t* __restrict__ Bkn, float* __restrict__ D) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint16_t* sB = reinterpret_cast<uint16_t*>(smem + 128 * k * 2);
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(TM_THREADS)
                    const int32_t* __restrict__ t_km, const int32_t* __restrict__ t_kn,
                    const float* __restrict__ theta, __nv_bfloat16* __restrict__ mma,
                    int64_t plane) {
+  pdl_enter();
   __shared__ float tile[TM_MAX * (TM_MAX + 1)];
   // the next tile's elements are loaded (float4, row-major) while this one is packed
   float4 nx[TM_V4];
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(EM_THREADS)
                const float* __restrict__ F, float* __restrict__ theta,
                __nv_bfloat16* __restrict__ mma, int64_t plane_n, float kappa, float step,
                int planes, int32_t* status) {
+  pdl_enter();
   __shared__ float tile[EM_SMEM];
   const int tid = threadIdx.x;
   int informative = 0, bad = 0;
@@ -473,7 +477,7 @@ int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, fl
   ProfScope prof_(KC_EM, s);
   if (blk1 < 0) blk1 = p->n_em_blk;
   if (blk1 <= blk0) return PCB_OK;
-  k_em_tiles<<<grid_for(blk1 - blk0, 1, 148 * 8), EM_THREADS, 0, s>>>(
+  launch_k(k_em_tiles, dim3(grid_for(blk1 - blk0, 1, 148 * 8)), dim3(EM_THREADS), 0, s, 
       blk0, blk1, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab_f,
       p->em_tile_slab_c, f_params, theta, p->mma, p->mma_plane, pseudocount, step,
       planes ? 1 : 0, status);
@@ -483,7 +487,7 @@ int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, fl
 int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta) {
   ProfScope prof_(KC_EM, s);
   if (!p->n_mma_tiles || !p->mma) return PCB_OK;
-  k_theta_to_mma<<<grid_for(p->n_mma_tiles, 1, 148 * 8), TM_THREADS, 0, s>>>(
+  launch_k(k_theta_to_mma, dim3(grid_for(p->n_mma_tiles, 1, 148 * 8)), dim3(TM_THREADS), 0, s, 
       p->n_mma_tiles, p->mma_theta, p->mma_slab_f, p->mma_slab_c, p->mma_km, p->mma_kn, theta,
       p->mma, p->mma_plane);
   return check_launch();
@@ -498,7 +502,7 @@ extern "C" int pcb_tc_selftest_mn(void* stream, int n, int k, int variant, const
   if (cudaFuncSetAttribute(pcb::k_tc_selftest_mn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            bytes) != cudaSuccess)
     return PCB_CUDA;
-  pcb::k_tc_selftest_mn<<<1, 128, bytes, reinterpret_cast<cudaStream_t>(stream)>>>(
+  pcb::launch_k(pcb::k_tc_selftest_mn, dim3(1), dim3(128), bytes, reinterpret_cast<cudaStream_t>(stream), 
       n, k, variant, d_a, d_b, d_d);
   return pcb::check_launch();
 }
@@ -510,7 +514,7 @@ extern "C" int pcb_tc_selftest(void* stream, int n, int k, const uint16_t* d_a,
   if (cudaFuncSetAttribute(pcb::k_tc_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            bytes) != cudaSuccess)
     return PCB_CUDA;
-  pcb::k_tc_selftest<<<1, 128, bytes, reinterpret_cast<cudaStream_t>(stream)>>>(n, k, d_a, d_b,
+  pcb::launch_k(pcb::k_tc_selftest, dim3(1), dim3(128), bytes, reinterpret_cast<cudaStream_t>(stream), n, k, d_a, d_b,
                                                                                  d_d);
   return pcb::check_launch();
 }

@@ -16,14 +16,14 @@
 // hence one base).  Both operands are split
 // into bf16 hi + lo and contracted as hi*hi + hi*lo + lo*hi (fp32 TMEM).
 //
-// Warp roles (14 warps):
+// Warp roles (18 warps):
 //   warp 0       producer: per 32-sample chunk, 2-D TMA boxes (128-byte
 //                swizzled) of the tile's r rows, its R rows and the child
 //                log-value rows into the raw ring;
 //   warp 1       MMA issuer (double-buffered TMEM accumulators, 2 x 256 cols);
 //   warps 2-9    converters: the chunk's shifts c_b, then raw -> exponentials
 //                -> packed bf16 planes in the K-major core-matrix layout;
-//   warps 10-13  epilogue: TMEM -> theta (.) cum -> f_params (plain stores when
+//   warps 10-17  epilogue: TMEM -> theta (.) cum -> f_params (plain stores when
 //                the group's flow tiles have a single writer and the batch
 //                is not sliced; else vector red.add).
 #include <math.h>
@@ -54,7 +54,8 @@ constexpr int PF_SWZ = PF_KS * 4;  // TMA swizzle span in bytes (64 or 128)
 // warps: producer, MMA, converters, 4 epilogue
 constexpr int PF_CONV0 = 2, PF_NCONV = PCB_PF_NCONV, PF_EPI0 = PF_CONV0 + PF_NCONV;
 // 8 epilogue warps: two per TMEM lane quarter, alternate 16-column chunks
-// (the fused-EM path needs whole rows: only the first four work there)
+// (the fused-EM path too: the pair meets at a named barrier for the row
+// totals and each staged 32 x 32 product-major tile)
 constexpr int PF_NEPI = 8;
 constexpr int PF_THREADS = (PF_EPI0 + PF_NEPI) * 32;
 constexpr int PF_MAXMEM = PF_M / 16;  // sum blocks per tile (k_m >= 16)
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                     const __grid_constant__ CUtensorMap tm_vb,
                     const __grid_constant__ CUtensorMap tm_pb,
                     const __grid_constant__ CUtensorMap tm_pbn) {
+  pdl_enter();
   using C = PfCfg<KN, RS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int OS = PRE ? C::kOSP : C::kOS;  // operand stages
@@ -680,6 +682,7 @@ namespace {
 // CTA = 32 samples x 32 thread rows striding over the sum blocks
 __global__ void __launch_bounds__(1024)
     k_pf_shift(int n_sb, int B, int ldb, const float* __restrict__ rmax, float* __restrict__ c) {
+  pdl_enter();
   __shared__ float part[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int b = blockIdx.x * 32 + tx;
@@ -702,6 +705,7 @@ __global__ void __launch_bounds__(256)
               const float* __restrict__ scratch, const float* __restrict__ pbase,
               const float* __restrict__ vbase, const float* __restrict__ c,
               uint8_t* __restrict__ img_a, uint8_t* __restrict__ img_e) {
+  pdl_enter();
   constexpr int kOpA = PF_M * PF_KS * 2, kOpB = PF_N * PF_KS * 2;
   __shared__ int child0, n_real;
   if (threadIdx.x == 0) {
@@ -804,10 +808,10 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
     float* c = prep;
     uint8_t* img_a = reinterpret_cast<uint8_t*>(prep + a.ldb);
     uint8_t* img_e = reinterpret_cast<uint8_t*>(prep + a.ldb + a_rows * a.ldb);
-    k_pf_shift<<<(a.ldb + 31) / 32, 1024, 0, s>>>((int)L.n_sb, a.B, a.ldb, rmax, c);
+    launch_k(k_pf_shift, dim3((a.ldb + 31) / 32), dim3(1024), 0, s, (int)L.n_sb, a.B, a.ldb, rmax, c);
     if (check_launch()) return PCB_CUDA;
     const int64_t tasks = (int64_t)(n_a + n_e) * (a.ldb / 8);
-    k_pf_prep<<<grid_for(tasks, 256), 256, 0, s>>>(n_a, n_e, (int)L.k_m, KN, a.nchunks, a.ldb,
+    launch_k(k_pf_prep, dim3(grid_for(tasks, 256)), dim3(256), 0, s, n_a, n_e, (int)L.k_m, KN, a.nchunks, a.ldb,
                                                    a.cap, a.prod_ids, a.param_ids, ratio, rmax,
                                                    scratch, pbase, vbase, c, img_a, img_e);
     if (check_launch()) return PCB_CUDA;
@@ -816,10 +820,10 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   }
   const int grid = min(a.n_items, sm_count());
   if (pre)
-    k_param_flow_ws<KN, RS, true><<<grid, PF_THREADS, C::kBytes, s>>>(
+    launch_k((k_param_flow_ws<KN, RS, true>), dim3(grid), dim3(PF_THREADS), C::kBytes, s, 
         a, tr, tR, te, tr128, tRt, te256, tvb, tpb, tpbn);
   else
-    k_param_flow_ws<KN, RS, false><<<grid, PF_THREADS, C::kBytes, s>>>(
+    launch_k((k_param_flow_ws<KN, RS, false>), dim3(grid), dim3(PF_THREADS), C::kBytes, s, 
         a, tr, tR, te, tr128, tRt, te256, tvb, tpb, tpbn);
   return check_launch();
 }

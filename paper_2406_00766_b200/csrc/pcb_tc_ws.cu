@@ -161,6 +161,7 @@ template <int MODE, int KC>
 __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     k_sum_ws(const WsArgs a, const __grid_constant__ CUtensorMap tm0,
              const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2) {
+  pdl_enter();
   using C = WsCfg<MODE, KC>;
   using W = WsWarps<C::kNConv>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -567,8 +568,13 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
           tmem_ld16(tbase + c0, v);
           if (!live || !nks) continue;
           float* o = a.out + out_row(c0) * a.ldb + b;
+#ifdef PCB_ABL_NOATOMIC  // timing ablation only: wrong results
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[(int64_t)i * a.ldb] = v[i];
+#else
 #pragma unroll
           for (int i = 0; i < 16; ++i) atomicAdd(o + (int64_t)i * a.ldb, v[i]);
+#endif
         }
         tc_fence_before();
         __syncwarp();
@@ -622,7 +628,7 @@ int launch_ws(const WsArgs& a, int64_t rows0, int64_t rows1, cudaStream_t s) {
   if (make_rows_map(&tm2, MODE == MODE_CF ? a.vbase_in : a.shift, rows1, a.ldb, 1))
     return PCB_CUDA;
   const int grid = min(a.n_items, sm_count());
-  k_sum_ws<MODE, KC><<<grid, WsWarps<C::kNConv>::kThreads, C::kBytes, s>>>(a, tm0, tm1, tm2);
+  launch_k((k_sum_ws<MODE, KC>), dim3(grid), dim3(WsWarps<C::kNConv>::kThreads), C::kBytes, s, a, tm0, tm1, tm2);
   return check_launch();
 }
 
@@ -640,6 +646,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32)
                   const int32_t* __restrict__ src_ids, const int32_t* __restrict__ real_ids,
                   const float* __restrict__ shift, const float* __restrict__ base,
                   float* __restrict__ gout, float* __restrict__ gbase) {
+  pdl_enter();
   __shared__ float part[GS_WARPS][33];
   const int sr = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -688,7 +695,7 @@ template <int MODE>
 int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, float* gbase,
                        cudaStream_t s) {
   dim3 grid((unsigned)count, (unsigned)((a.B + 31) / 32));
-  k_group_shift<MODE><<<grid, GS_WARPS * 32, 0, s>>>(a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off,
+  launch_k((k_group_shift<MODE>), dim3(grid), dim3(GS_WARPS * 32), 0, s, a.cap, kc, a.B, a.ldb, a.sb_base, a.row_off,
                                            a.members, a.src_ids, a.real_ids, a.shift,
                                            a.vbase_in, gout, gbase);
   return check_launch();
