@@ -56,6 +56,33 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// The same MMA keeping A in the tensor core's operand collector for the next
+// MMA (collector::a::fill), then consuming it from there without a shared-
+// memory read (collector::a::lastuse): the hi*hi, hi*lo pair shares A_hi.
+#ifndef PCB_NO_COLLECTOR
+#define PCB_COLL_FILL ".collector::a::fill"
+#define PCB_COLL_LAST ".collector::a::lastuse"
+#else
+#define PCB_COLL_FILL ""
+#define PCB_COLL_LAST ""
+#endif
+__device__ __forceinline__ void mma_bf16_keep_a(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16" PCB_COLL_FILL " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_bf16_reuse_a(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16" PCB_COLL_LAST " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t mbar_saddr) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             const uint64_t al = make_desc(aL + k * 256, 128, SBO);
             const uint64_t bh = make_desc(bH + k * 256, 128, SBO);
             const uint64_t bl = make_desc(bL + k * 256, 128, SBO);
-            mma_bf16(d, ah, bh, idesc, (kc > it.kc0 || k > 0) ? 1u : 0u);
-            mma_bf16(d, ah, bl, idesc, 1u);
+            mma_bf16_keep_a(d, ah, bh, idesc, (kc > it.kc0 || k > 0) ? 1u : 0u);
+            mma_bf16_reuse_a(d, ah, bl, idesc, 1u);
             mma_bf16(d, al, bh, idesc, 1u);
           }
           mma_commit(smem_u32(&op_empty[orr.slot()]));

@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
             const uint64_t al = make_desc(aL + ks * 256, 128, SBO);
             const uint64_t bh = make_desc(bH + ks * 256, 128, SBO);
             const uint64_t bl = make_desc(bL + ks * 256, 128, SBO);
-            mma_bf16(d0, ah, bh, idesc, (first && ks == 0) ? 0u : 1u);
-            mma_bf16(d0, ah, bl, idesc, 1u);
+            mma_bf16_keep_a(d0, ah, bh, idesc, (first && ks == 0) ? 0u : 1u);
+            mma_bf16_reuse_a(d0, ah, bl, idesc, 1u);
             mma_bf16(d0, al, bh, idesc, 1u);
           }
           mma_commit(smem_u32(&op_empty[orr.slot()]));
