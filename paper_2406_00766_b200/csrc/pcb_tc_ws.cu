@@ -579,18 +579,20 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[as]));
-        __threadfence();
+        // arrival protocol (release / acquire by one thread, cumulative over
+        // the epilogue barrier -- no per-thread GPU-scope fence)
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
         if (warp == W::kEpi0 && lane == 0) {
           int32_t* cnt = a.counters + it.sr * a.ntiles + it.tile;
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");  // this CTA's partial sums first
           const int old = atomicAdd(cnt, 1);
           const bool last = old == a.kslices - 1;
           if (last) *cnt = 0;  // self-resetting for the next launch
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");  // then every slice's partial sums
           g_last = last;
         }
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
         if (g_last) {
-          __threadfence();
           for (int c0 = h * 16; c0 < N; c0 += 32) {
             if (!live) continue;
             float* o = a.out + out_row(c0) * a.ldb + b;
