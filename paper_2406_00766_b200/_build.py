@@ -45,7 +45,9 @@ HOST_LIB = OUT_DIR / "libpcirc_host.so"
 
 def build_host(force: bool = False) -> Path:
     """The native host-compiler core (plain C++17, std::thread)."""
-    if not force and HOST_LIB.exists() and HOST_LIB.stat().st_mtime >= HOST_SRC.stat().st_mtime:
+    deps = [HOST_SRC, PKG.parent / "include" / "pcirc_host.h"]
+    if not force and HOST_LIB.exists() and all(HOST_LIB.stat().st_mtime >= d.stat().st_mtime
+                                               for d in deps):
         return HOST_LIB
     OUT_DIR.mkdir(exist_ok=True)
     cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"

@@ -45,10 +45,6 @@ _SIGS = {
     "pcc_tiles_count": (_I64, [_P]),
     "pcc_tiles_get": (None, [_P, _P, _P]),
     "pcc_tiles": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
-    "pcc_tying_assign": (C.c_int, [_I64, _P, _P, _P, _P]),
-    "pcc_claim": (C.c_int, [_I64, _P, _P]),
-    "pcc_sum_groups": (C.c_int, [_I64, _I64, _P, _P, _P, _P, _P]),
-    "pcc_hash_records": (None, [C.c_int, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "pcc_rows_new": (_P, []),
     "pcc_rows_free": (None, [_P]),
     "pcc_rows_add_multi": (None, [_P, _I64, _P, _I64, _P, _P, _P, _P]),

@@ -432,6 +432,7 @@ def _tiles_native(g, layers, rep, params, zero_len, theta_size, slot_phys, in_co
         nat.pcc_tiles_get(table, ptr(tile_starts), ptr(tile_writers))
     finally:
         nat.pcc_tiles_free(table)
+        nat.pcc_release()
     theta_size = int(ts[0])
     return buf[:theta_size], theta_size, tile_starts, tile_writers
 
@@ -752,7 +753,7 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
     """Fast path when no two sums share a physical position and no sum touches a
     pmf: every sum is its own group and inputs dedupe by their pmf range, so
     the first-occurrence order is plain node-id order.  ``native``: position
-    claims in a bitset and the sorted sum rows written by ``pcc_sum_groups``."""
+    claims in a bitset and the sorted sum rows written by ``pcc_sum_groups_multi``."""
     sum_segs = [s for s in g.segments if s.kind == KIND_SUM]
     in_ids, _, in_ncat, _ = g.input_table()
     n_sum_pos = sum(s.count * s.fan_in for s in sum_segs)
@@ -812,11 +813,7 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
     group_idx = np.empty(int(group_off[-1]), dtype=np.int64)
     # inputs: contiguous ranges
     ii = np.flatnonzero(kinds == 0)
-    if ii.size and nat is not None:
-        dst0, st, n = (_native.i64(a) for a in (group_off[ii], rs[refs[ii]], rn[refs[ii]]))
-        nat.pcc_iota_ranges(dst0.size, _native.ptr(dst0), _native.ptr(st), _native.ptr(n),
-                            _native.ptr(group_idx))
-    elif ii.size:
+    if ii.size:
         n = rn[refs[ii]]
         dst = np.repeat(group_off[ii], n) + (np.arange(int(n.sum())) -
                                               np.repeat(np.cumsum(n) - n, n))
@@ -829,13 +826,6 @@ def _simplex_groups_disjoint(g: CircuitGraph, pmf_phys_of, slot_phys, theta_size
     for si, s in enumerate(sum_segs):
         rows = pos_of[base:base + s.count]
         base += s.count
-        if nat is not None:
-            dst = _native.i64(group_off[rows])
-            sl = _native.i64(s.slots)
-            if nat.pcc_sum_groups(s.count, s.fan_in, _native.ptr(sl), _native.ptr(slot_phys),
-                                  _native.ptr(bits), _native.ptr(dst), _native.ptr(group_idx)):
-                return None  # a position shared between sums (or within one sum)
-            continue
         phys = np.sort(slot_phys[s.slots], axis=1)
         dst = group_off[rows][:, None] + np.arange(s.fan_in)
         group_idx[dst] = phys

@@ -15,9 +15,12 @@
 //                         rep-slot pattern dedupe (within the layer and against
 //                         every earlier layer), theta fill, slot_phys, the
 //                         parallel-edge and tying-alignment checks;
-//   * pcc_sum_groups    - the sorted physical positions of every sum row for the
-//                         simplex groups (build.py:535-567), with overlap claims;
-//   * pcc_hash_records  - the graph_hash byte records (build.py:634-657).
+//   * pcc_sum_groups_multi / pcc_rows_* - the sorted physical positions of
+//                         every sum row for the simplex groups (build.py:535-567),
+//                         with overlap claims;
+//   * pcc_hash_records_multi - the graph_hash byte records (build.py:634-657);
+//   * pcc_depths, pcc_group_runs, pcc_minmax, pcc_narrow_i32 - graph depths and
+//                         the device-plan table helpers.
 // Orderings are the reference's (dict insertion = first occurrence, np.unique
 // = ascending); grouping is exact (64-bit row hashes, then element-wise
 // comparison with the group representative).  Parallel loops are plain
@@ -32,6 +35,8 @@
 #include <thread>
 #include <unordered_map>
 #include <vector>
+
+#include "../../../include/pcirc_host.h"
 
 namespace {
 using i64 = int64_t;
@@ -718,61 +723,6 @@ int pcc_tiles(void* h, void* table, const i64* slots, const i64* rep, const u64*
   return bad.load() ? 2 : 0;
 }
 
-// Tying check for ranges assigned outside the layers (input pmfs): ref[rep[s]]
-// must agree with phys for every (slot, phys).  Returns 1 if misaligned.
-int pcc_tying_assign(i64 n, const i64* slots, const i64* phys, const i64* rep, i64* ref) {
-  std::atomic<int> bad{0};
-  pfor(n, [&](i64 lo, i64 hi, int) {
-    for (i64 i = lo; i < hi; ++i) {
-      const i64 r = rep ? rep[slots[i]] : slots[i];
-      i64 expect = -1;
-      if (!__atomic_compare_exchange_n(&ref[r], &expect, phys[i], false, __ATOMIC_RELAXED,
-                                       __ATOMIC_RELAXED) &&
-          expect != phys[i])
-        bad.store(1, std::memory_order_relaxed);
-    }
-  });
-  return bad.load();
-}
-
-// Claims positions in a bitset; returns 1 if any was claimed before.
-int pcc_claim(i64 n, const i64* pos, u64* bits) {
-  std::atomic<int> bad{0};
-  pfor(n, [&](i64 lo, i64 hi, int) {
-    for (i64 i = lo; i < hi; ++i) {
-      const u64 p = (u64)pos[i], bit = 1ull << (p & 63);
-      if (__atomic_fetch_or(&bits[p >> 6], bit, __ATOMIC_RELAXED) & bit)
-        bad.store(1, std::memory_order_relaxed);
-    }
-  });
-  return bad.load();
-}
-
-// Simplex rows of one sum segment: row i's positions slot_phys[slots[i, :]]
-// sorted into group_idx[dst[i] ...]; every position claimed.  Returns 1 on
-// a position claimed twice.
-int pcc_sum_groups(i64 count, i64 fan, const i64* slots, const i64* slot_phys, u64* bits,
-                   const i64* dst, i64* group_idx) {
-  std::atomic<int> bad{0};
-  pfor(count, [&](i64 lo, i64 hi, int) {
-    for (i64 i = lo; i < hi; ++i) {
-      i64* out = group_idx + dst[i];
-      const i64* s = slots + i * fan;
-      bool sorted = true;
-      for (i64 j = 0; j < fan; ++j) {
-        const i64 p = slot_phys[s[j]];
-        out[j] = p;
-        if (j && p < out[j - 1]) sorted = false;
-        const u64 bit = 1ull << ((u64)p & 63);
-        if (__atomic_fetch_or(&bits[(u64)p >> 6], bit, __ATOMIC_RELAXED) & bit)
-          bad.store(1, std::memory_order_relaxed);
-      }
-      if (!sorted) std::sort(out, out + fan);
-    }
-  }, std::max<i64>(1, (1 << 14) / std::max<i64>(fan, 1)));
-  return bad.load();
-}
-
 // ---------------------------------------------------------------- simplex
 // Exact grouping of the sorted physical rows of non-contiguous sums
 // (build.py:535-567, the general path): rows are added segment by segment in
@@ -1033,31 +983,6 @@ void pcc_narrow_i32(const i64* src, i64 n, int32_t* dst) {
   pfor(n, [&](i64 lo, i64 hi, int) {
     for (i64 i = lo; i < hi; ++i) dst[i] = (int32_t)src[i];
   }, 1 << 20);
-}
-
-// graph_hash records (build.py:634-657) of rows [0, count) of one segment:
-// inputs 'I' + (var, ncat, slot); products 'P' + children; sums 'S' +
-// children + slots; little-endian int64.
-void pcc_hash_records(int kind, i64 count, i64 fan, const i64* children, const i64* slots,
-                      const i64* var, const i64* ncat, const i64* slot, uint8_t* out) {
-  const i64 rec = kind == 0 ? 1 + 24 : (kind == 1 ? 1 + 8 * fan : 1 + 16 * fan);
-  pfor(count, [&](i64 lo, i64 hi, int) {
-    for (i64 i = lo; i < hi; ++i) {
-      uint8_t* o = out + i * rec;
-      if (kind == 0) {
-        o[0] = 'I';
-        const i64 v[3] = {var[i], ncat[i], slot[i]};
-        std::memcpy(o + 1, v, 24);
-      } else if (kind == 1) {
-        o[0] = 'P';
-        std::memcpy(o + 1, children + i * fan, 8 * fan);
-      } else {
-        o[0] = 'S';
-        std::memcpy(o + 1, children + i * fan, 8 * fan);
-        std::memcpy(o + 1 + 8 * fan, slots + i * fan, 8 * fan);
-      }
-    }
-  }, std::max<i64>(1, (1 << 16) / rec));
 }
 
 }  // extern "C"
