@@ -145,12 +145,26 @@ struct WsCfg {
   static constexpr int kA = WS_M * KC * 2;                    // one bf16 A plane
   static constexpr int kBPlane = WS_NMAX * KC * 2;            // stacked theta hi (or lo) plane
   static constexpr int kB = 2 * kBPlane;
-  static constexpr int kOp = 2 * kA + kB;
-  static constexpr int kBudget = 210 * 1024;
-  static constexpr int kOS = (KC <= 16) ? 4 : 2;
-  static constexpr int kRSmax = (kBudget - kOS * kOp) / kRaw;
+#ifndef PCB_WS_BUDGET
+#define PCB_WS_BUDGET 220
+#endif
+  static constexpr int kBudget = PCB_WS_BUDGET * 1024;
+  // separate rings for the converted A planes (converters -> MMA) and the
+  // theta planes (bulk copies -> MMA): the theta stream gets the depth to
+  // cover its L2 / HBM latency (4 stages of 32 KB at KC = 32, was 2 shared
+  // stages: HMM-4096 sum forward 1.75 -> 1.63 ms, child flows 2.24 -> 2.03),
+  // the converters' A ring stays shallow (its input is the raw ring)
+#ifndef PCB_WS_AS
+#define PCB_WS_AS 2
+#endif
+#ifndef PCB_WS_BS
+#define PCB_WS_BS 4
+#endif
+  static constexpr int kAS = (KC <= 16) ? 4 : PCB_WS_AS;
+  static constexpr int kBS = (KC <= 16) ? 4 : PCB_WS_BS;
+  static constexpr int kRSmax = (kBudget - kAS * 2 * kA - kBS * kB) / kRaw;
   static constexpr int kRS = kRSmax > 8 ? 8 : kRSmax;
-  static constexpr int kBytes = kRS * kRaw + kOS * kOp;
+  static constexpr int kBytes = kRS * kRaw + kAS * 2 * kA + kBS * kB;
   static_assert(kRS >= 2, "raw ring too small");
   static constexpr int kNConv = 8;  // converter warps: two threads per sample
 };
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
   using W = WsWarps<C::kNConv>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t raw_full[C::kRS], raw_empty[C::kRS];
-  __shared__ uint64_t op_full[C::kOS], op_empty[C::kOS];
+  __shared__ uint64_t a_full[C::kAS], a_empty[C::kAS], b_full[C::kBS], b_empty[C::kBS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
   __shared__ float g_s[2][WS_M];
   __shared__ float gr_s[2][WS_M];        // child flow: the common parent base Gr
@@ -175,7 +189,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
   __shared__ bool g_last;
   __shared__ uint32_t tmem_base;
   uint8_t* raw = smem;
-  uint8_t* ops = smem + C::kRS * C::kRaw;
+  uint8_t* aops = smem + C::kRS * C::kRaw;       // A ring: hi plane, lo plane per stage
+  uint8_t* bops = aops + C::kAS * 2 * C::kA;       // theta ring: hi planes, lo planes
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -183,9 +198,13 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       mbar_init(smem_u32(&raw_full[i]), 1);
       mbar_init(smem_u32(&raw_empty[i]), W::kConv);
     }
-    for (int i = 0; i < C::kOS; ++i) {
-      mbar_init(smem_u32(&op_full[i]), W::kConv + 1);  // converter warps + theta tx
-      mbar_init(smem_u32(&op_empty[i]), 1);
+    for (int i = 0; i < C::kAS; ++i) {
+      mbar_init(smem_u32(&a_full[i]), W::kConv);  // converter warps
+      mbar_init(smem_u32(&a_empty[i]), 1);
+    }
+    for (int i = 0; i < C::kBS; ++i) {
+      mbar_init(smem_u32(&b_full[i]), 1);  // theta producer (+ tx)
+      mbar_init(smem_u32(&b_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
@@ -235,7 +254,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     // ------------------------------------------------------------ theta producer
     // stacked theta tiles of each K block: hi planes back to back, then lo
     // planes, so the S tiles form one N = S * nb operand per plane
-    Ring<C::kOS> orr;
+    Ring<C::kBS> brr;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const WsItem it = ws_item(a, item);
       const int m0 = it.m0, S = it.S;
@@ -244,9 +263,9 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       const bool dn = dense_row(a, it);
       int c = col_first(real, a.cap, it.ks * a.kper, dn);
       for (int k = 0; c < a.cap && k < a.kper; ++k, c = col_next(real, a.cap, c + 1, dn)) {
-        mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
-        const uint32_t of = smem_u32(&op_full[orr.slot()]);
-        uint8_t* bdst = ops + orr.slot() * C::kOp + 2 * C::kA;
+        mbar_wait(smem_u32(&b_empty[brr.slot()]), brr.empty_par());
+        const uint32_t of = smem_u32(&b_full[brr.slot()]);
+        uint8_t* bdst = bops + brr.slot() * C::kB;
         if (lane == 0) mbar_arrive_expect_tx(of, (uint32_t)(2 * S * plane_bytes));
         __syncwarp();
         if (contig) {  // the S tiles of this column are one run per plane
@@ -263,12 +282,13 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
                      (uint32_t)plane_bytes, of);
           }
         }
-        orr.next();
+        brr.next();
       }
     }
   } else if (warp == WS_MMA) {
     // ------------------------------------------------------------ MMA issuer
-    Ring<C::kOS> orr;
+    Ring<C::kAS> arr;
+    Ring<C::kBS> brr;
     int acc_u = 0;
     constexpr uint32_t SBO = (KC / 8) * 128;  // A and B both K-major, no swizzle
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -283,12 +303,12 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       const bool dn = dense_row(a, it);
       int c = col_first(real, a.cap, it.ks * a.kper, dn);
       for (int k = 0; c < a.cap && k < a.kper; ++k, c = col_next(real, a.cap, c + 1, dn)) {
-        mbar_wait(smem_u32(&op_full[orr.slot()]), orr.full_par());
+        mbar_wait(smem_u32(&b_full[brr.slot()]), brr.full_par());
+        mbar_wait(smem_u32(&a_full[arr.slot()]), arr.full_par());
         tc_fence_after();
         if (lane == 0) {
-          uint8_t* st = ops + orr.slot() * C::kOp;
-          const uint32_t aH = smem_u32(st), aL = aH + C::kA;
-          const uint32_t bH = aH + 2 * C::kA, bL = bH + C::kBPlane;
+          const uint32_t aH = smem_u32(aops + arr.slot() * 2 * C::kA), aL = aH + C::kA;
+          const uint32_t bH = smem_u32(bops + brr.slot() * C::kB), bL = bH + C::kBPlane;
           const uint32_t idesc = idesc_bf16(WS_M, S * a.nb);
 #pragma unroll
           for (int ks = 0; ks < KC / 16; ++ks) {
@@ -300,11 +320,13 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
             mma_bf16_reuse_a(d0, ah, bl, idesc, 1u);
             mma_bf16(d0, al, bh, idesc, 1u);
           }
-          mma_commit(smem_u32(&op_empty[orr.slot()]));
+          mma_commit(smem_u32(&a_empty[arr.slot()]));
+          mma_commit(smem_u32(&b_empty[brr.slot()]));
         }
         __syncwarp();
         first = false;
-        orr.next();
+        arr.next();
+        brr.next();
       }
       if (lane == 0) {
         if (first)
@@ -321,7 +343,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
     const int kh = (tid - WS_CONV0 * 32) / WS_M;        // which part of each K block
     constexpr int KH = KC * 4 / W::kConv;                // K columns per converter thread
     Ring<C::kRS> rr;
-    Ring<C::kOS> orr;
+    Ring<C::kAS> arr;
     int g_u = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       const WsItem it = ws_item(a, item);
@@ -366,8 +388,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
           else
             x[j] = dead ? 0.f : ex2(x[j]);  // ex2(-inf) = 0: impossible sums, zero flow
         }
-        mbar_wait(smem_u32(&op_empty[orr.slot()]), orr.empty_par());
-        uint8_t* sAh = ops + orr.slot() * C::kOp;
+        mbar_wait(smem_u32(&a_empty[arr.slot()]), arr.empty_par());
+        uint8_t* sAh = aops + arr.slot() * 2 * C::kA;
         uint8_t* sAl = sAh + C::kA;
 #pragma unroll
         for (int q = 0; q < KH / 8; ++q) {
@@ -382,8 +404,8 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&op_full[orr.slot()]));
-        orr.next();
+        if (lane == 0) mbar_arrive(smem_u32(&a_full[arr.slot()]));
+        arr.next();
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&g_empty[gs]));
