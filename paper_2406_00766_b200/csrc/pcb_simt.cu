@@ -739,17 +739,19 @@ __global__ void __launch_bounds__(TB* TY)
 }
 
 // Single-sum rows (k_m = 1, e.g. an HMM or mixture root over thousands of
-// children): the eight thread rows split the child blocks (each its own
+// children): TY1 thread rows split the child blocks (each its own
 // streaming (lin, top) pair, merged in shared memory at the end) instead of
-// one thread row walking all of them while seven idle.
-__global__ void __launch_bounds__(TB* TY)
+// one thread row walking all of them; 32 rows: a 128-block root (HMM-4096)
+// is 4 blocks per thread.
+constexpr int TY1 = 32;
+__global__ void __launch_bounds__(TB* TY1)
     k_sum_fwd_simt1(int cap, int k_n, int B, int ldb, int64_t sb_base,
                     const int32_t* __restrict__ sum_ids, const int32_t* __restrict__ prod_ids,
                     const int32_t* __restrict__ param_ids, const float* __restrict__ theta,
                     const float* __restrict__ scratch, const float* __restrict__ pbase,
                     float* __restrict__ values, float* __restrict__ vbase) {
   pdl_enter();
-  __shared__ float lin_s[TY][TB], top_s[TY][TB], g_s[TY][TB];
+  __shared__ float lin_s[TY1][TB], top_s[TY1][TB], g_s[TY1][TB];
   const int r = blockIdx.y;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int b = blockIdx.x * TB + tx;
@@ -758,17 +760,17 @@ __global__ void __launch_bounds__(TB* TY)
   const int32_t* trow = param_ids + (int64_t)r * cap;
   float G = PCB_NEG_INF;
   if (live)
-    for (int c = ty; c < cap; c += TY)
+    for (int c = ty; c < cap; c += TY1)
       if (trow[c] != 0) G = fmaxf(G, pbase[(int64_t)(prow[c] / k_n) * ldb + b]);
   g_s[ty][tx] = G;
   __syncthreads();
   G = PCB_NEG_INF;
 #pragma unroll
-  for (int y = 0; y < TY; ++y) G = fmaxf(G, g_s[y][tx]);
+  for (int y = 0; y < TY1; ++y) G = fmaxf(G, g_s[y][tx]);
   if (G == PCB_NEG_INF) G = 0.f;
   float lin = 0.f, top = PCB_NEG_INF;
   if (live)
-    for (int c = ty; c < cap; c += TY) {
+    for (int c = ty; c < cap; c += TY1) {
       const int t0 = trow[c];
       if (t0 == 0) continue;
       const int pid = prow[c];
@@ -793,11 +795,11 @@ __global__ void __launch_bounds__(TB* TY)
   if (ty != 0 || !live) return;
   float T = PCB_NEG_INF;
 #pragma unroll
-  for (int y = 0; y < TY; ++y) T = fmaxf(T, top_s[y][tx]);
+  for (int y = 0; y < TY1; ++y) T = fmaxf(T, top_s[y][tx]);
   float acc = 0.f;
   if (T != PCB_NEG_INF)
 #pragma unroll
-    for (int y = 0; y < TY; ++y)
+    for (int y = 0; y < TY1; ++y)
       if (top_s[y][tx] != PCB_NEG_INF) acc += lin_s[y][tx] * expf(top_s[y][tx] - T);
   const int sid = sum_ids[r];
   values[(int64_t)sid * ldb + b] = logf(acc) + T;
@@ -811,7 +813,7 @@ int launch_sum_fwd_simt(const Layer& L, const FwdGroup& g, cudaStream_t s, int B
   if (!g.rows) return PCB_OK;
   if (L.k_m == 1 && g.cap >= 2) {  // thread rows split the child blocks
     dim3 grid((B + TB - 1) / TB, (unsigned)g.rows);
-    launch_k(k_sum_fwd_simt1, dim3(grid), dim3(dim3(TB, TY)), 0, s, (int)g.cap, (int)L.k_n, B, ldb, L.sb_base,
+    launch_k(k_sum_fwd_simt1, dim3(grid), dim3(dim3(TB, TY1)), 0, s, (int)g.cap, (int)L.k_n, B, ldb, L.sb_base,
                                                   g.sum_ids, g.prod_ids, g.param_ids, theta,
                                                   scratch, pbase, values, vbase);
     return check_launch();

@@ -36,6 +36,7 @@
 // Every hand-off is an mbarrier: raw full/empty, operand full/empty,
 // accumulator full/empty, shift full/empty.
 #include <math.h>
+#include <stdlib.h>
 
 #include "pcb_internal.cuh"
 #include "pcb_tc.cuh"
@@ -94,6 +95,7 @@ struct WsArgs {
   const float* gshift;             // precomputed per-(super-row, sample) shifts, or null
   const float* gbase;              // cf: precomputed per-(super-row, sample) common bases Gr
   int64_t gshift_stride;           // ldb, or 0 when every super-row shares one shift row
+  int coop;                        // long K, one item per CTA: shifts computed in-kernel
 };
 
 struct WsItem {
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
   __shared__ int g_orow[2][WS_NMAX / 16];  // first output row of every 16 columns
   __shared__ bool g_last;
   __shared__ uint32_t tmem_base;
+  __shared__ int cs_g[WS_M], cs_gr[WS_M];  // coop shifts: order-preserving ints
   uint8_t* raw = smem;
   uint8_t* aops = smem + C::kRS * C::kRaw;       // A ring: hi plane, lo plane per stage
   uint8_t* bops = aops + C::kAS * 2 * C::kA;       // theta ring: hi planes, lo planes
@@ -220,6 +223,84 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base;
   const int plane_bytes = a.nb * KC * 2;  // one bf16 plane of one theta tile
+
+  // Long K with one item per CTA: the item's per-sample shifts (what
+  // k_group_shift would precompute) come from the 17 converter, epilogue and
+  // shift warps together while the producers start streaming -- one round of
+  // loads per warp (lane = sample, 8 K blocks per warp), then order-preserving
+  // integer max reductions in shared memory.  Child flow: each thread keeps
+  // (gr, g) online; the partial g are moved onto the common gr before the
+  // second reduction.
+  const bool coop = a.coop && warp >= WS_CONV0 && warp != W::kTheta;
+  if (coop) {
+    constexpr int NW = W::kShift - WS_CONV0;  // converters + epilogue + shift (theta excluded)
+    const int wr = (warp == W::kShift) ? NW - 1 : warp - WS_CONV0;
+    const int ct = wr * 32 + lane;
+    auto ord = [](float f) {
+      const int i = __float_as_int(f);
+      return i >= 0 ? i : i ^ 0x7fffffff;
+    };
+    auto unord = [](int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); };
+    for (int q = ct; q < WS_M; q += NW * 32) cs_g[q] = cs_gr[q] = ord(PCB_NEG_INF);
+    asm volatile("bar.sync 3, %0;" ::"n"(NW * 32) : "memory");
+    const WsItem it = ws_item(a, blockIdx.x);
+    const int32_t* src = a.src_ids + (int64_t)it.r0 * a.cap;
+    const int32_t* real = a.real_ids + (int64_t)it.r0 * a.cap;
+    constexpr int SPL = WS_M / 32;
+    float g[SPL], gr[SPL];
+#pragma unroll
+    for (int u = 0; u < SPL; ++u) g[u] = gr[u] = PCB_NEG_INF;
+    for (int c0 = wr; c0 < a.cap; c0 += NW * 4) {
+      float v[4][SPL], w[4][SPL];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = c0 + NW * e;
+        const int sc = (c < a.cap && __ldg(real + c) != 0) ? __ldg(src + c) : -1;
+#pragma unroll
+        for (int u = 0; u < SPL; ++u) {
+          const int b = it.b0 + lane + 32 * u;
+          const bool ok = sc >= 0 && b < a.B;
+          const int64_t o = (int64_t)(sc - a.sb_base) / KC * a.ldb + b;
+          v[e][u] = ok ? __ldg(a.shift + o) : PCB_NEG_INF;
+          w[e][u] = (MODE == MODE_CF && ok) ? __ldg(a.vbase_in + o) : PCB_NEG_INF;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int u = 0; u < SPL; ++u) {
+          if (MODE == MODE_FWD) {
+            g[u] = fmaxf(g[u], v[e][u]);
+          } else if (w[e][u] != PCB_NEG_INF) {
+            if (w[e][u] > gr[u]) {
+              if (g[u] != PCB_NEG_INF) g[u] += (w[e][u] - gr[u]) * kL2E;
+              gr[u] = w[e][u];
+            }
+            g[u] = fmaxf(g[u], fmaf(gr[u] - w[e][u], kL2E, v[e][u]));
+          }
+        }
+    }
+    if (MODE == MODE_CF) {
+#pragma unroll
+      for (int u = 0; u < SPL; ++u)
+        if (gr[u] != PCB_NEG_INF) atomicMax(&cs_gr[lane + 32 * u], ord(gr[u]));
+      asm volatile("bar.sync 3, %0;" ::"n"(NW * 32) : "memory");
+#pragma unroll
+      for (int u = 0; u < SPL; ++u) {
+        const float G = unord(cs_gr[lane + 32 * u]);
+        if (g[u] != PCB_NEG_INF) g[u] += (G - gr[u]) * kL2E;  // onto the common base
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SPL; ++u)
+      if (g[u] != PCB_NEG_INF) atomicMax(&cs_g[lane + 32 * u], ord(g[u]));
+    asm volatile("bar.sync 3, %0;" ::"n"(NW * 32) : "memory");
+    for (int q = ct; q < WS_M; q += NW * 32) {
+      g_s[0][q] = unord(cs_g[q]);
+      gr_s[0][q] = unord(cs_gr[q]);
+    }
+    asm volatile("bar.sync 3, %0;" ::"n"(NW * 32) : "memory");
+  }
 
   if (warp == WS_PRODUCER) {
     // ------------------------------------------------------------ raw producer
@@ -487,12 +568,19 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
       const int gs = g_u & 1;
       mbar_wait(smem_u32(&g_empty[gs]), (uint32_t)(((g_u >> 1) & 1) ^ 1));
       int nk = 0;
-      float gv[SPL], gb[SPL];
-      shifts(it, gv, gb, nk);
+      if (a.coop && g_u == 0) {  // shifts already in g_s[0] / gr_s[0]
+        if (dense_row(a, it))
+          nk = a.cap;
+        else
+          for (int c = 0; c < a.cap; ++c) nk += __ldg(a.real_ids + (int64_t)it.r0 * a.cap + c) != 0;
+      } else {
+        float gv[SPL], gb[SPL];
+        shifts(it, gv, gb, nk);
 #pragma unroll
-      for (int u = 0; u < SPL; ++u) {
-        g_s[gs][lane + 32 * u] = gv[u];
-        gr_s[gs][lane + 32 * u] = gb[u];
+        for (int u = 0; u < SPL; ++u) {
+          g_s[gs][lane + 32 * u] = gv[u];
+          gr_s[gs][lane + 32 * u] = gb[u];
+        }
       }
       const int N = it.S * a.nb;
       if (lane < N / 16) {
@@ -725,6 +813,13 @@ int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, floa
   return check_launch();
 }
 
+// In-kernel long-K shifts when every CTA runs exactly one item (the persistent
+// grid is min(items, SMs)); PCB_NO_COOP_SHIFT=1 keeps the separate shift kernel.
+bool coop_ok(const WsArgs& a) {
+  static const bool off = getenv("PCB_NO_COOP_SHIFT") != nullptr;
+  return !off && a.n_items <= sm_count();
+}
+
 // K split so a layer with few (super-row, tile) items still covers the SMs:
 // >= 2 K blocks per slice; only when the group owns all output rows it zeroes
 // The slice count minimises a wave model: waves(items) x (K blocks per item +
@@ -790,10 +885,14 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
   if (ws_long_k(a.cap)) {
-    if (launch_group_shift<MODE_FWD>(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, nullptr, s))
-      return PCB_CUDA;
-    a.gshift = gshift;
-    a.gshift_stride = g.uniform ? 0 : ldb;
+    if (coop_ok(a)) {
+      a.coop = 1;
+    } else {
+      if (launch_group_shift<MODE_FWD>(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, nullptr, s))
+        return PCB_CUDA;
+      a.gshift = gshift;
+      a.gshift_stride = g.uniform ? 0 : ldb;
+    }
   }
   // split K reduces partial sums in place: zero the layer's sum rows first
   if (a.kslices > 1 &&
@@ -839,12 +938,16 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
   if (ws_long_k(a.cap)) {
-    const int64_t n = g.uniform ? 1 : tc.count;
-    if (launch_group_shift<MODE_CF>(a, (int)L.k_m, n, gshift, gshift + n * ldb, s))
-      return PCB_CUDA;
-    a.gshift = gshift;
-    a.gbase = gshift + n * ldb;
-    a.gshift_stride = g.uniform ? 0 : ldb;
+    if (coop_ok(a)) {
+      a.coop = 1;
+    } else {
+      const int64_t n = g.uniform ? 1 : tc.count;
+      if (launch_group_shift<MODE_CF>(a, (int)L.k_m, n, gshift, gshift + n * ldb, s))
+        return PCB_CUDA;
+      a.gshift = gshift;
+      a.gbase = gshift + n * ldb;
+      a.gshift_stride = g.uniform ? 0 : ldb;
+    }
   }
   if (a.kslices > 1 &&
       cudaMemsetAsync(flow_scratch, 0, sizeof(float) * L.window * (int64_t)ldb, s) != cudaSuccess)
