@@ -903,9 +903,19 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
 #ifndef PCB_PF_RS32
 #define PCB_PF_RS32 2
 #endif
-    case 32: return dense ? launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s,
-                                             (g.pf_pre && !em && !pf_pre_off()) ? prep : nullptr)
-                          : launch_pf<32, PCB_PF_RS32>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+#ifndef PCB_PF_DENSE_RS
+#define PCB_PF_DENSE_RS 2
+#endif
+    case 32: {
+      // PRE (operands converted once per layer): every stage is an operand
+      // stage.  Dense without PRE (RAT-SPN's 1024-child rows): keep two
+      // operand stages -- three raw stages leave one, which serialises the
+      // converters and the MMAs
+      const bool pre = g.pf_pre && !em && !pf_pre_off();
+      if (dense && pre) return launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s, prep);
+      if (dense) return launch_pf<32, PCB_PF_DENSE_RS>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+      return launch_pf<32, PCB_PF_RS32>(a, L, ratio, rmax, scratch, vbase, pbase, s);
+    }
     case 64: return dense ? launch_pf<64, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s)
                           : launch_pf<64, 2>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     default: return PCB_USAGE;

@@ -820,6 +820,14 @@ bool coop_ok(const WsArgs& a) {
   return !off && a.n_items <= sm_count();
 }
 
+// Many items per CTA and a moderate K (RAT-SPN: 32 blocks, ~100 items per
+// CTA): the shift warp computes each item's shifts while the previous item
+// runs (four rounds of loads), so no precompute launch is needed either.
+bool shift_warp_ok(const WsArgs& a) {
+  static const bool off = getenv("PCB_FORCE_GROUP_SHIFT") != nullptr;
+  return !off && a.cap <= 64 && a.n_items >= 4 * sm_count();
+}
+
 // K split so a layer with few (super-row, tile) items still covers the SMs:
 // >= 2 K blocks per slice; only when the group owns all output rows it zeroes
 // The slice count minimises a wave model: waves(items) x (K blocks per item +
@@ -884,7 +892,7 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   a.out_base = L.sb_base;
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
-  if (ws_long_k(a.cap)) {
+  if (ws_long_k(a.cap) && !shift_warp_ok(a)) {
     if (coop_ok(a)) {
       a.coop = 1;
     } else {
@@ -937,7 +945,7 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   a.pbase_in = pbase;
   a.counters = counters;
   plan_split(a, tc.count, split_ok);
-  if (ws_long_k(a.cap)) {
+  if (ws_long_k(a.cap) && !shift_warp_ok(a)) {
     if (coop_ok(a)) {
       a.coop = 1;
     } else {
