@@ -200,7 +200,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ __align__(16) float cs[C::kRS][PF_KS];
   __shared__ int cols_p[C::kCPG];
-  __shared__ int cols_w[PF_NEPI][C::kCPG];  // epilogue warps' column lists
+  // PRE: the converter warps have nothing to convert and join the epilogue
+  constexpr int NEW = PRE ? PF_NEPI + PF_NCONV : PF_NEPI;  // epilogue warps
+  constexpr int CSTEP = 16 * (NEW / 4);                      // column stride per warp
+  __shared__ int cols_w[NEW][C::kCPG];  // epilogue warps' column lists
   __shared__ float em_wt[4][32 * 33];  // fused EM: a warp pair's updated 32 x 32 tile
   __shared__ float em_tot[4][2][32];   // fused EM: the pair's partial row totals
   __shared__ uint32_t tmem_base;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), PF_NEPI);
+      mbar_init(smem_u32(&acc_empty[i]), NEW);
     }
     fence_mbar_init();
   }
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       __syncwarp();
       ++acc_u;
     }
-  } else if (warp < PF_EPI0) {
+  } else if (!PRE && warp < PF_EPI0) {
     // ------------------------------------------------------------ converters
     if constexpr (!PRE) {
     const int t = tid - PF_CONV0 * 32;  // 0..PF_NCONV*32-1
@@ -459,10 +462,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }  // !PRE
   } else {
     // ------------------------------------------------------------ epilogue
+    // NEW / 4 warps per TMEM lane quarter (q4 = warp % 4), each taking every
+    // (NEW / 4)-th 16-column chunk
+    const int ew = warp - (PRE ? PF_CONV0 : PF_EPI0);
     const int q4 = warp & 3;
-    const int h = (warp - PF_EPI0) >> 2;  // column half: chunks h*16, h*16 + 32, ...
+    const int h = ew >> 2;          // column phase: chunks h*16, h*16 + CSTEP, ...
     const int er = q4 * 32 + lane;  // sum row within the tile (TMEM lane)
-    int* cols = cols_w[warp - PF_EPI0];
+    int* cols = cols_w[ew];
     int acc_u = 0;
     int em_inf = 0, em_bad = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       mbar_wait(smem_u32(&acc_full[as]), (uint32_t)((acc_u >> 1) & 1));
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(as * PF_N) + ((uint32_t)(q4 * 32) << 16);
-      if constexpr (KN == 32) {
+      if constexpr (KN == 32 && !PRE) {
         if (a.em) {
           // Fused EM, the two warps of a lane quarter (same 32 rows) split
           // the columns in 16-wide chunks as in the plain epilogue and meet
@@ -599,11 +605,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           continue;
         }
       }
-      for (int c0 = h * 16; c0 < ncol * KN; c0 += 32) {
+      for (int c0 = h * 16; c0 < ncol * KN; c0 += CSTEP) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) th[i] = thn[i];
 #ifndef PCB_ABL_EPI
-        if (live && c0 + 32 < ncol * KN) load_th(tile_of(c0 + 32), thn);
+        if (live && c0 + CSTEP < ncol * KN) load_th(tile_of(c0 + CSTEP), thn);
 #endif
         float v[16];
         tmem_ld16(tbase + c0, v);
