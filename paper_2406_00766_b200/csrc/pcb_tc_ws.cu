@@ -814,18 +814,22 @@ int launch_group_shift(const WsArgs& a, int kc, int64_t count, float* gout, floa
 }
 
 // In-kernel long-K shifts when every CTA runs exactly one item (the persistent
-// grid is min(items, SMs)); PCB_NO_COOP_SHIFT=1 keeps the separate shift kernel.
+// grid is min(items, SMs)).  The environment is read per launch so tests can
+// drive every shift path: PCB_NO_COOP_SHIFT=1 keeps the separate shift kernel.
 bool coop_ok(const WsArgs& a) {
-  static const bool off = getenv("PCB_NO_COOP_SHIFT") != nullptr;
-  return !off && a.n_items <= sm_count();
+  return getenv("PCB_NO_COOP_SHIFT") == nullptr && a.n_items <= sm_count();
 }
 
 // Many items per CTA and a moderate K (RAT-SPN: 32 blocks, ~100 items per
 // CTA): the shift warp computes each item's shifts while the previous item
 // runs (four rounds of loads), so no precompute launch is needed either.
+// PCB_FORCE_GROUP_SHIFT=1 disables it; PCB_SHIFT_WARP_MIN_ITEMS overrides the
+// item threshold (default 4 x SMs).
 bool shift_warp_ok(const WsArgs& a) {
-  static const bool off = getenv("PCB_FORCE_GROUP_SHIFT") != nullptr;
-  return !off && a.cap <= 64 && a.n_items >= 4 * sm_count();
+  if (getenv("PCB_FORCE_GROUP_SHIFT")) return false;
+  const char* m = getenv("PCB_SHIFT_WARP_MIN_ITEMS");
+  const int64_t min_items = m ? atoll(m) : 4 * (int64_t)sm_count();
+  return a.cap <= 64 && a.n_items >= min_items;
 }
 
 // K split so a layer with few (super-row, tile) items still covers the SMs:
