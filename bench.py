@@ -333,7 +333,7 @@ def run_reference(args, w):
     line = {
         "impl": "reference", "metric": "samples/sec fwd+bwd+EM", "value": v,
         "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * t, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000 * t, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "desc": w["desc"], "batch_per_step": w["batch"],
                    "sampled_batch": Bc, "composition": formula, "sec_per_epoch": EPOCH / v},
