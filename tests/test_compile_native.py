@@ -87,7 +87,7 @@ def test_random_circuits_native_equals_numpy(nat):
     for trial in range(25):
         g = _random_circuit(rng)
         g.freeze()
-        for k in (1, 2, 4, 8):
+        for k in (1, 2, 4, 8, 16, 32):
             try:
                 b = dumps_compiled(B._compile(g, CompileConfig(block_size=k), False))
             except CircuitValidationError:  # the native pass must defer too
@@ -204,3 +204,27 @@ def test_group_runs_native_equals_numpy(nat, monkeypatch):
         monkeypatch.delenv("PCB_COMPILER")
         for a, b in zip(got, want):
             np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.reference
+def test_reference_random_circuits_native_equals_numpy(nat, ref_pcirc):
+    """The reference test suite's own random-circuit generator (multi-parent
+    nodes, zero pmf entries, input children of sums): native == numpy at
+    every block size."""
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from circuitgen import random_circuit
+    rng = np.random.default_rng(21)
+    for trial in range(20):
+        rg = random_circuit(rng, max_vars=8, max_nodes=300)
+        g = CircuitGraph.from_reference(rg)
+        g.freeze()
+        for k in (1, 2, 4, 8, 16):
+            try:
+                b = dumps_compiled(B._compile(g, CompileConfig(block_size=k), False))
+            except CircuitValidationError:
+                with pytest.raises(_native.NativeError):
+                    B._compile(g, CompileConfig(block_size=k), True)
+                continue
+            a = dumps_compiled(B._compile(g, CompileConfig(block_size=k), True))
+            assert a == b, (trial, k)
