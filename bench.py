@@ -229,17 +229,42 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        """In-process NVML reads (every 10 ms), else None."""
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+            def read():
+                r = get_reasons(h)
+                act = lambda bit: "Active" if r & bit else "Not Active"  # noqa: E731
+                return [str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), str(mx), hex(r),
+                        act(0x8), act(0x40), act(0x20), act(0x4)]
+            read()
+            return read
+        except Exception:
+            return None
+
     def _run(self):
+        read = self._nvml()
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([s.strip() for s in out.split(",")])
+                if read is not None:
+                    self.rows.append(read())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if read is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -463,11 +488,13 @@ def run_ours(args, w):
     launches0 = _lib.load().pcb_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
         barrier()
         ev0.record()
         for i in range(args.steps):
             ll_acc += run(dev_batches[i % n_pool])
         ev1.record()
+        torch.cuda.synchronize()  # the sampler covers the device work, not just the enqueue
         barrier()
     launches = _lib.load().pcb_launch_count() - launches0
     if graphed:  # replays launch the captured kernels without host calls
