@@ -196,7 +196,9 @@ struct Scratch {
     n = 0;
   }
 };
-Scratch g_tmp, g_par, g_grid, g_pat, g_rows;
+// per calling thread: concurrent compiles from several Python threads (ctypes
+// releases the GIL) never share a buffer
+thread_local Scratch g_tmp, g_par, g_grid, g_pat, g_rows;
 
 struct Layer {
   // caller-owned inputs (kept alive by the Python layer object)

@@ -228,3 +228,24 @@ def test_reference_random_circuits_native_equals_numpy(nat, ref_pcirc):
                 continue
             a = dumps_compiled(B._compile(g, CompileConfig(block_size=k), True))
             assert a == b, (trial, k)
+
+
+def test_concurrent_compiles_thread_safe(nat):
+    """Two Python threads compiling at once (ctypes releases the GIL; the
+    native scratch is per thread) give the serial layouts."""
+    import threading
+    graphs = [S.build_structure(S.StructureConfig(kind=k, seed=3, **kw))
+              for k, kw, _ in (STRUCTS[0], STRUCTS[2])]
+    ks = (STRUCTS[0][2], STRUCTS[2][2])
+    want = [dumps_compiled(compile_circuit(g, CompileConfig(block_size=k)))
+            for g, k in zip(graphs, ks)]
+    got = [None, None]
+
+    def run(i):
+        got[i] = dumps_compiled(compile_circuit(graphs[i], CompileConfig(block_size=ks[i])))
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert got == want
