@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 25;
+constexpr int64_t kVersion = 26;
 
 struct Reader {
   const int64_t* p;
@@ -216,6 +216,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.q_rrow = r.ref();
     L.pre_ratio = (int)r.get();
     L.rmax_off = r.get();
+    L.pf_fuse = (int)r.get();
     L.n_pb = L.window / L.k_n;  // including the -inf pad block 0
     for (const FwdGroup& G : L.fwd)
       if (G.pf_pre) P->max_prep_rows = std::max(P->max_prep_rows, pf_prep_rows(L, G));
@@ -227,6 +228,21 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     if (L.n_sb > P->max_sb) P->max_sb = L.n_sb;
     if (L.n_sb * L.k_m > P->max_sum_rows) P->max_sum_rows = L.n_sb * L.k_m;
     P->layers.push_back(std::move(L));
+  }
+  // tied-layer parameter-flow fusion groups: rank members by layer index
+  for (size_t li = 0; li < P->layers.size(); ++li) {
+    Layer& L = P->layers[li];
+    if (L.pf_fuse < 0) continue;
+    int rank = 0, n = 0;
+    for (size_t lj = 0; lj < P->layers.size(); ++lj)
+      if (P->layers[lj].pf_fuse == L.pf_fuse) {
+        ++n;
+        if (lj < li) ++rank;
+      }
+    L.pf_fuse_rank = rank;
+    L.pf_fuse_n = n;
+    if (L.fwd.size() == 1)
+      P->fuse_prep_rows = std::max(P->fuse_prep_rows, (int64_t)n * pf_prep_rows(L, L.fwd[0]));
   }
   P->red_n = r.get();
   P->red_dst = r.ref();
@@ -403,7 +419,8 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.gshift = w.ratio + P->max_sum_rows * (int64_t)ldb;
   w.rmax_all = w.gshift + 2 * P->max_tc_rows * (int64_t)ldb;
   w.prep = w.rmax_all + P->n_rmax * (int64_t)ldb;
-  w.counters = reinterpret_cast<int32_t*>(w.prep + P->max_prep_rows * (int64_t)ldb);
+  w.fprep = w.prep + P->max_prep_rows * (int64_t)ldb;
+  w.counters = reinterpret_cast<int32_t*>(w.fprep + P->fuse_prep_rows * (int64_t)ldb);
   return w;
 }
 
@@ -471,6 +488,28 @@ int child_flows(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ld
   return PCB_OK;
 }
 
+// the layer's parameter flows run on the exec's side stream in this step
+static bool pf_side(const pcb_plan* P, const Step& S, const Layer& L) {
+  return S.lean && P->push_ratio_ok && L.pre_ratio && S.ex && S.lean != 2;
+}
+
+// Tied-layer parameter-flow fusion in this pass: a whole backward pass, no
+// per-layer flow hooks (data parallel), and the rank-0 member (launched last)
+// on the side stream whenever any member is, so every member's operand
+// staging precedes the fused contraction in stream order.
+static bool pf_fuse_ok(const pcb_plan* P, const Step& S, const Layer& L, bool tc) {
+  if (!tc || !S.pass || !pf_fusable(L) || (S.ex && !S.ex->flows_done.empty())) return false;
+  bool any_side = false, zero_side = false;
+  for (const Layer& M : P->layers) {
+    if (M.pf_fuse != L.pf_fuse) continue;
+    if (!pf_fusable(M)) return false;
+    const bool sd = pf_side(P, S, M);
+    any_side |= sd;
+    if (M.pf_fuse_rank == 0) zero_side = sd;
+  }
+  return zero_side || !any_side;
+}
+
 int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B, int ldb,
                    float* theta, const float* values, float* flows, float* scratch_all,
                    float* flow_scratch, float* prod_flows, float* f_params, const Work& w) {
@@ -524,12 +563,16 @@ int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B,
   const float* vbase = w.vbase + L.vb_off * (int64_t)ldb;
   for (size_t g = 0; g < L.fwd.size(); ++g) {
     const TcRows& T = L.pf_tc[g];
-    if (tc && T.count > 0)
+    if (tc && T.count > 0) {
+      const PfFuse fz{L.pf_fuse_rank, L.pf_fuse_n, w.fprep};
+      const bool fuse = !em_fuse && pf_fuse_ok(P, S, L, tc);
       st = launch_param_flow_ws(L, L.fwd[g], T, sp, B, ldb, theta, ratio, rmax, scratch, vbase,
-                                pbase, f_params, em_fuse ? &em : nullptr, w.prep);
-    else
+                                pbase, f_params, em_fuse ? &em : nullptr, w.prep,
+                                fuse ? &fz : nullptr);
+    } else {
       st = launch_param_flow_simt(L, L.fwd[g], sp, B, ldb, theta, values, flows, scratch, pbase,
                                   vbase, f_params);
+    }
     if (st) return st;
   }
   if (S.ex && li < S.ex->flows_done.size() && S.ex->flows_done[li] &&
@@ -592,6 +635,7 @@ int run_backward(const pcb_plan* P, Step& S, cudaStream_t s, int B, int ldb,
       return PCB_CUDA;
   }
   const bool side = S.lean && P->push_ratio_ok && S.ex && S.lean != 2;
+  S.pass = true;  // every layer's stream placement is this pass's (pf_fuse_ok)
   int st = launch_root_bwd(P, s, B, ldb, d_flows, d_prod_flows);
   if (st) return st;
   for (size_t li = P->layers.size(); li-- > 0;) {
@@ -701,7 +745,7 @@ int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   if (!plan || ldb <= 0) return -1;
   // + one split-K arrival counter per (super-row, 128-sample tile)
   return (plan->n_sb_tot + plan->n_pb_tot + plan->max_sb + plan->max_sum_rows +
-          2 * plan->max_tc_rows + plan->n_rmax + plan->max_prep_rows) *
+          2 * plan->max_tc_rows + plan->n_rmax + plan->max_prep_rows + plan->fuse_prep_rows) *
              (int64_t)ldb +
          plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }

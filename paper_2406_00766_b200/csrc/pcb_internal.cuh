@@ -75,6 +75,10 @@ struct TcRows {
 
 struct Layer {
   int64_t k_m, k_n, window, n_prod;
+  // parameter-flow fusion over tied layers (plan pf fusion id >= 0): this
+  // layer's rank among the n members (rank 0 = lowest index = last in the
+  // backward pass, which launches the one fused contraction)
+  int pf_fuse = -1, pf_fuse_rank = 0, pf_fuse_n = 0;
   int64_t flow_lo = 0, flow_hi = 0;  // the layer's f_params flow range (disjoint when fp_cover)
   int64_t scratch_off;  // first row of this layer's window in the all-layer scratch
   const int32_t* pad_rows;
@@ -135,6 +139,8 @@ struct Layer {
 //                               layers (child flows: g rows, then base rows)
 //   prep [max_prep_rows x ldb]  pre-converted bf16 hi/lo parameter-flow
 //                               operand images of one pf_pre layer (+ its shift row)
+//   fprep [fuse_prep_rows x ldb] the same for every member of a tied-layer
+//                               fusion group, laid end to end along K
 //   counters [max_tc_rows x ldb/128] split-K arrivals (self-resetting, zeroed at allocation)
 struct Work {
   float* vbase;
@@ -144,6 +150,7 @@ struct Work {
   float* gshift;
   float* rmax_all;  // [n_rmax x ldb] R rows of the pre-ratioed layers
   float* prep;
+  float* fprep;
   int32_t* counters;
 };
 
@@ -180,6 +187,7 @@ struct pcb_plan {
   int64_t max_pb = 1, max_sb = 1, max_sum_rows = 1, max_tc_rows = 1;
   int64_t n_pb_tot = 0, n_sb_tot = 0;  // all layers' product / sum blocks (base rows)
   int64_t max_prep_rows = 0;  // pre-converted parameter-flow operand rows (pf_pre groups)
+  int64_t fuse_prep_rows = 0;  // ... of the largest tied-layer fusion group
   // bf16 tensor-core copies of theta tiles (plan v4)
   // bf16 planes: regions of mma_plane elements: [F hi][F lo][C hi][C lo];
   // tile t's sum-major planes at slab_f[t] (+ plane), its product-major
@@ -243,6 +251,7 @@ struct Step {
   std::vector<char>* em_done = nullptr;  // per layer: EM fused into its parameter flows
   bool inputs_done = false;              // the input-flow pass updated the staged pmfs
   bool shared_done = false;              // ... and the shared pmfs
+  bool pass = false;                     // a whole backward pass (stream placement known)
 };
 
 // kernel classes for the live per-class timing used by bench.py
@@ -370,6 +379,12 @@ int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, fl
                     float pseudocount, float step, int32_t* status, bool planes,
                     int64_t blk0 = 0, int64_t blk1 = -1);
 // EM fused into the parameter-flow epilogue (one-process lean steps)
+// a tied-layer parameter-flow fusion member (launch_param_flow_ws)
+struct PfFuse {
+  int rank, n;   // segment of this layer, members
+  float* prep;   // the group's operand images (n shift rows, n x A, n x B)
+};
+
 struct PfEm {
   float kappa, step;
   int32_t* status;
@@ -409,7 +424,10 @@ bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
                          const float* scratch, const float* vbase, const float* pbase,
-                         float* f_params, const PfEm* em = nullptr, float* prep = nullptr);
+                         float* f_params, const PfEm* em = nullptr, float* prep = nullptr,
+                         const PfFuse* fuse = nullptr);
+// the layer may join its tied-layer parameter-flow fusion group
+bool pf_fusable(const Layer& L);
 // pf_pre groups: image rows of the pre-converted operands
 int64_t pf_prep_rows(const Layer& L, const FwdGroup& g);
 

@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(1024)
 }
 
 __global__ void __launch_bounds__(256)
-    k_pf_prep(int n_a, int n_e, int k_m, int kn, int nchunks, int ldb, int cap,
+    k_pf_prep(int n_a, int n_e, int k_m, int kn, int nstride, int kc_off, int ldb, int cap,
               const int32_t* __restrict__ prod_row0, const int32_t* __restrict__ param_row0,
               const float* __restrict__ ratio, const float* __restrict__ rmax,
               const float* __restrict__ scratch, const float* __restrict__ pbase,
@@ -747,7 +747,7 @@ __global__ void __launch_bounds__(256)
       const float Rs[8] = {R0.x, R0.y, R0.z, R0.w, R1.x, R1.y, R1.z, R1.w};
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[e] = (cc[e] == PCB_NEG_INF) ? 0.f : ex2(xs[e] + (Rs[e] - cc[e]));
-      dst = img_a + ((int64_t)(row / PF_M) * nchunks + kc) * (2 * kOpA) +
+      dst = img_a + ((int64_t)(row / PF_M) * nstride + kc_off + kc) * (2 * kOpA) +
             kmajor_off(row % PF_M, k, PF_KS);
       plane = kOpA;
     } else {
@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         v[e] = (cc[e] == PCB_NEG_INF) ? 0.f : fminf(ex2(fmaf(xs[e], kL2E, cc[e])), 1e37f);
-      dst = img_e + ((int64_t)(n / PF_N) * nchunks + kc) * (2 * kOpB) +
+      dst = img_e + ((int64_t)(n / PF_N) * nstride + kc_off + kc) * (2 * kOpB) +
             kmajor_off(n % PF_N, k, PF_KS);
       plane = kOpB;
     }
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(256)
 template <int KN, int RS>
 int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float* rmax,
               const float* scratch, const float* vbase, const float* pbase, cudaStream_t s,
-              float* prep = nullptr) {
+              float* prep = nullptr, const PfFuse* fuse = nullptr) {
   using C = PfCfg<KN, RS>;
   const bool pre = prep != nullptr;
   static int attr[kMaxDev] = {}, attr_p[kMaxDev] = {};
@@ -796,6 +796,7 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
   a.kslices = pf_kslices(a.n_items, a.cap, KN, a.B);  // n_items holds the super-row count here
   const int base = a.n_items * a.cgroups * a.mtiles;
   a.n_items = base * a.kslices;
+  auto base_items = [base](const PfArgs&) { return base; };
   a.store = a.store && a.kslices == 1;  // batch slices add partial sums
   if (a.em && (a.kslices != 1 || a.cgroups != 1)) return PCB_USAGE;  // needs whole rows
   CUtensorMap tr, tR, te, tr128, tRt, te256, tvb, tpb, tpbn;
@@ -810,21 +811,33 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
       make_rows_map(&tpbn, pbase, L.n_pb, a.ldb, C::kCPG, C::kRP / 4, 0))
     return PCB_CUDA;
   if (pre) {
-    // the layer's operands once: shift row, A images (all sum rows), B images
+    // the layer's operands once: shift row, A images (all sum rows), B images.
+    // A fusion member writes its segment (chunks rank * nchunks ...) of the
+    // group's images; the rank-0 member (last in the backward pass) then runs
+    // one contraction over all n segments, storing every flow once
     const int n_a = (int)(L.n_sb * L.k_m), n_e = a.cap * KN;
     const int64_t a_rows = (n_a + PF_M - 1) / PF_M * PF_M;
-    float* c = prep;
-    uint8_t* img_a = reinterpret_cast<uint8_t*>(prep + a.ldb);
-    uint8_t* img_e = reinterpret_cast<uint8_t*>(prep + a.ldb + a_rows * a.ldb);
+    const int nseg = fuse ? fuse->n : 1, rank = fuse ? fuse->rank : 0;
+    float* base = fuse ? fuse->prep : prep;
+    float* c = base + (int64_t)rank * a.ldb;
+    uint8_t* img_a = reinterpret_cast<uint8_t*>(base + (int64_t)nseg * a.ldb);
+    uint8_t* img_e = reinterpret_cast<uint8_t*>(base + (int64_t)nseg * (1 + a_rows) * a.ldb);
     launch_k(k_pf_shift, dim3((a.ldb + 31) / 32), dim3(1024), 0, s, (int)L.n_sb, a.B, a.ldb, rmax, c);
     if (check_launch()) return PCB_CUDA;
     const int64_t tasks = (int64_t)(n_a + n_e) * (a.ldb / 8);
-    launch_k(k_pf_prep, dim3(grid_for(tasks, 256)), dim3(256), 0, s, n_a, n_e, (int)L.k_m, KN, a.nchunks, a.ldb,
-                                                   a.cap, a.prod_ids, a.param_ids, ratio, rmax,
-                                                   scratch, pbase, vbase, c, img_a, img_e);
+    launch_k(k_pf_prep, dim3(grid_for(tasks, 256)), dim3(256), 0, s, n_a, n_e, (int)L.k_m, KN,
+             nseg * a.nchunks, rank * a.nchunks, a.ldb, a.cap, a.prod_ids, a.param_ids, ratio,
+             rmax, scratch, pbase, vbase, c, img_a, img_e);
     if (check_launch()) return PCB_CUDA;
     a.prep_a = img_a;
     a.prep_e = img_e;
+    if (fuse) {
+      if (rank != 0) return PCB_OK;  // operands staged; the rank-0 member contracts
+      a.nchunks *= nseg;
+      a.kslices = 1;
+      a.n_items = base_items(a);
+      a.store = 1;  // the group's tiles have no writer outside this launch
+    }
   }
   const int grid = min(a.n_items, sm_count());
   if (pre)
@@ -842,6 +855,11 @@ int launch_pf(const PfArgs& a0, const Layer& L, const float* ratio, const float*
 static bool pf_pre_off() {
   static const bool off = getenv("PCB_PF_NO_PRE") != nullptr;
   return off;
+}
+
+bool pf_fusable(const Layer& L) {
+  return L.pf_fuse >= 0 && L.fwd.size() == 1 && L.fwd[0].pf_pre && L.k_n == 32 && !pf_pre_off() &&
+         getenv("PCB_NO_PF_FUSE") == nullptr;
 }
 
 int64_t pf_prep_rows(const Layer& L, const FwdGroup& g) {
@@ -870,7 +888,7 @@ bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B) {
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,
                          int B, int ldb, const float* theta, const float* ratio, const float* rmax,
                          const float* scratch, const float* vbase, const float* pbase,
-                         float* f_params, const PfEm* em, float* prep) {
+                         float* f_params, const PfEm* em, float* prep, const PfFuse* fuse) {
   ProfScope prof_(KC_PARAM_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   PfArgs a{};
@@ -920,7 +938,8 @@ int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cu
       // operand stages -- three raw stages leave one, which serialises the
       // converters and the MMAs
       const bool pre = g.pf_pre && !em && !pf_pre_off();
-      if (dense && pre) return launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s, prep);
+      if (dense && pre)
+        return launch_pf<32, 3>(a, L, ratio, rmax, scratch, vbase, pbase, s, prep, fuse);
       if (dense) return launch_pf<32, PCB_PF_DENSE_RS>(a, L, ratio, rmax, scratch, vbase, pbase, s);
       return launch_pf<32, PCB_PF_RS32>(a, L, ratio, rmax, scratch, vbase, pbase, s);
     }

@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 25
+VERSION = 26
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -844,6 +844,43 @@ def build_program(compiled, *, tensor_cores: bool = True):
         f = folded(g.flow_ids)[g.param_ids != 0]
         return int(bool(np.all(fcnt[np.searchsorted(fu, f)] == 1))) if f.size else 1
 
+    # parameter-flow fusion (tied layers, e.g. HMM transitions): layers whose
+    # single pre-converted dense group is the same table (same tied tiles,
+    # same relative sum / child structure) and whose flow tiles no other layer
+    # writes run ONE parameter-flow contraction over the concatenated batches
+    # of all of them (the layers' pre-converted operand images laid end to
+    # end along K): one epilogue of plain stores instead of one reduction
+    # pass per layer
+    fuse_id = [-1] * len(c.layers)
+    if tensor_cores:
+        cand: dict = {}
+        for li, L in enumerate(c.layers):
+            if not tc_layer(L) or len(L.fwd_groups) != 1:
+                continue
+            g = L.fwd_groups[0]
+            rows = g.prod_ids.shape[0]
+            if not (rows > 0 and group_matrix_rows(g.prod_ids)[1].size == 1 and pf_pre_ok(g, L)):
+                continue
+            f = folded(g.flow_ids)[g.param_ids != 0]
+            if np.unique(f).size != f.size:
+                continue
+            sid = np.asarray(g.sum_ids, np.int64)
+            pid = np.asarray(g.prod_ids, np.int64)
+            key = (L.k_m, L.k_n, g.param_ids.shape, np.asarray(g.param_ids, np.int64).tobytes(),
+                   np.asarray(folded(g.flow_ids), np.int64).tobytes(), (sid - sid.min()).tobytes(),
+                   (pid - pid.min()).tobytes())
+            cand.setdefault(key, []).append((li, f))
+        nid = 0
+        for members in cand.values():
+            if len(members) < 2:
+                continue
+            f = members[0][1]
+            if not np.all(fcnt[np.searchsorted(fu, f)] == len(members)):
+                continue  # another layer writes these tiles too
+            for li, _ in members:
+                fuse_id[li] = nid
+            nid += 1
+
     # per-layer flow ranges and whether f_params[:theta_size] is covered by
     # them, the staged (stored) input pmfs and the zero tile, all disjoint
     layer_range, fp_cover = [], True
@@ -999,7 +1036,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
         prog.append(int(pr["row"].size))
         for key in ("row", "f", "qoff", "qblk", "qbase", "qkind", "qrrow"):
             ref(pr[key])
-        prog += [int(pre_ratio[li]), int(rmax_off[li])]
+        prog += [int(pre_ratio[li]), int(rmax_off[li]), int(fuse_id[li])]
 
     red = red[:0]  # folded above: no replica reduction pass
     if red.shape[0]:
@@ -1090,6 +1127,7 @@ def build_program(compiled, *, tensor_cores: bool = True):
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,
             "pre_ratio_layers": int(sum(pre_ratio)), "em_fused_layers": int(sum(em_fusable)),
+            "pf_fused_layers": int(sum(1 for f in fuse_id if f >= 0)),
             "em_fused_layer_ids": [li for li, f in enumerate(em_fusable) if f], "input_inline_em": in_inline_ok, "blob_elems": blob.size, "tc_super_rows": n_tc_rows, "mma_tiles": int(t_start.size),
             "em_tile_blocks": int(tb["blk_km"].size), "em_rest_groups": int(rest.size),
             "mma_elems": mma_elems, "scratch_rows": scratch_total, "slot_vb": slot_vb,
