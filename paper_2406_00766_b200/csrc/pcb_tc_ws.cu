@@ -96,6 +96,7 @@ struct WsArgs {
   const float* gbase;              // cf: precomputed per-(super-row, sample) common bases Gr
   int64_t gshift_stride;           // ldb, or 0 when every super-row shares one shift row
   int coop;                        // long K, one item per CTA: shifts computed in-kernel
+  int split_finish;                // coop split K: every slice finishes a share of the columns
 };
 
 struct WsItem {
@@ -692,18 +693,39 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         // arrival protocol (release / acquire by one thread, cumulative over
         // the epilogue barrier -- no per-thread GPU-scope fence)
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
+        // Co-resident slices (coop: one item per CTA, all CTAs resident):
+        // every slice waits for all partial sums, then finishes its own
+        // share of the columns -- the finish is spread over the k slices
+        // instead of serialised on the last one.  Otherwise the last slice
+        // to arrive finishes the whole item.
+        const bool spread = a.coop && a.split_finish;
         if (warp == W::kEpi0 && lane == 0) {
           int32_t* cnt = a.counters + it.sr * a.ntiles + it.tile;
           asm volatile("fence.acq_rel.gpu;" ::: "memory");  // this CTA's partial sums first
           const int old = atomicAdd(cnt, 1);
-          const bool last = old == a.kslices - 1;
-          if (last) *cnt = 0;  // self-resetting for the next launch
+          bool last = old == a.kslices - 1;
+          if (spread) {
+            int v = old + 1;
+            while (v < a.kslices) {
+              __nanosleep(64);
+              v = atomicAdd(cnt, 0);
+            }
+            last = true;
+          } else if (last) {
+            *cnt = 0;  // self-resetting for the next launch
+          }
           asm volatile("fence.acq_rel.gpu;" ::: "memory");  // then every slice's partial sums
           g_last = last;
         }
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");
         if (g_last) {
-          for (int c0 = h * 16; c0 < N; c0 += 32) {
+          int cq0 = 0, cq1 = N;
+          if (spread) {  // this slice's columns (16-column aligned)
+            const int per = ((N / 16 + a.kslices - 1) / a.kslices) * 16;
+            cq0 = min(N, it.ks * per);
+            cq1 = min(N, cq0 + per);
+          }
+          for (int c0 = cq0 + h * 16; c0 < cq1; c0 += 32) {
             if (!live) continue;
             float* o = a.out + out_row(c0) * a.ldb + b;
             float d[16], l[16], pb = 0.f;
@@ -714,6 +736,10 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
           }
         }
         asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // g_last reuse
+        if (spread && warp == W::kEpi0 && lane == 0) {  // second arrival; the last resets
+          int32_t* cnt = a.counters + it.sr * a.ntiles + it.tile;
+          if (atomicAdd(cnt, 1) == 2 * a.kslices - 1) atomicExch(cnt, 0);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&g_empty[gs]));
@@ -899,6 +925,7 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   if (ws_long_k(a.cap) && !shift_warp_ok(a)) {
     if (coop_ok(a)) {
       a.coop = 1;
+      a.split_finish = getenv("PCB_NO_SPLIT_FINISH") == nullptr;
     } else {
       if (launch_group_shift<MODE_FWD>(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, nullptr, s))
         return PCB_CUDA;
@@ -952,6 +979,7 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   if (ws_long_k(a.cap) && !shift_warp_ok(a)) {
     if (coop_ok(a)) {
       a.coop = 1;
+      a.split_finish = getenv("PCB_NO_SPLIT_FINISH") == nullptr;
     } else {
       const int64_t n = g.uniform ? 1 : tc.count;
       if (launch_group_shift<MODE_CF>(a, (int)L.k_m, n, gshift, gshift + n * ldb, s))
