@@ -249,8 +249,15 @@ class ClockSampler:
         except Exception:
             return None
 
+    def _sample(self):
+        try:
+            if self._read is not None:
+                self.rows.append(self._read())
+        except Exception:
+            pass
+
     def _run(self):
-        read = self._nvml()
+        read = self._read
         while not self._stop.is_set():
             try:
                 if read is not None:
@@ -267,11 +274,14 @@ class ClockSampler:
             self._stop.wait(0.01 if read is not None else 0.2)
 
     def __enter__(self):
+        self._read = self._nvml()  # initialised before the timed region starts
+        self._sample()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        self._sample()  # the state at the end of the device work
         self._stop.set()
         self._t.join(timeout=6)
 
