@@ -51,6 +51,16 @@ WORKLOADS = {
                    batch=512, desc="HCLT latent=16, 784 vars (MNIST-shaped), 256 cats"),
     "hclt64": dict(kind="hclt", num_vars=3072, hidden_dim=64, num_categories=256, block=32,
                    batch=512, desc="HCLT latent=64, 3072 vars, 256 cats (dev proxy)"),
+    # deep trees: the same HCLT-256 on a breadth-first
+    # spanning tree of the 32 x 32 x 3 pixel grid (a Chow-Liu-like tree of
+    # neighbouring pixels: 64 levels) and on a path (3072 levels, the
+    # latency-bound worst case)
+    "hclt256_grid": dict(kind="hclt", num_vars=3072, hidden_dim=256, num_categories=256,
+                         shape=(32, 32, 3), tree="grid", block=32, batch=512,
+                         desc="HCLT latent=256 on a pixel-grid BFS tree (depth 64), 3072 vars"),
+    "hclt256_chain": dict(kind="hclt", num_vars=3072, hidden_dim=256, num_categories=256,
+                          tree="chain", block=32, batch=512,
+                          desc="HCLT latent=256 on a path (depth 3072), 3072 vars"),
     "hmm4096": dict(kind="hmm", seq_len=32, hidden_dim=4096, vocab_size=50257, block=32,
                     batch=256, desc="HMM hidden=4096, vocab 50257, seq len 32"),
     # PyJuice PD (elementwise products per cut) on ImageNet32 (32 x 32 x 3):
@@ -102,7 +112,7 @@ def _build_circuit(w):
     from paper_2406_00766_b200.compiler import CompileConfig, _native, compile_circuit
     keys = ("kind", "num_vars", "hidden_dim", "num_categories", "seq_len", "vocab_size",
             "shape", "split_interval", "elementwise", "depth", "num_input_components",
-            "num_repetitions")
+            "num_repetitions", "tree")
     cfg = S.StructureConfig(seed=0, tied=True, **{k: w[k] for k in keys if k in w})
     t0 = time.perf_counter()
     g = S.build_structure(cfg)

@@ -23,7 +23,7 @@ def main():
     w = bench.WORKLOADS[name]
     keys = ("kind", "num_vars", "hidden_dim", "num_categories", "seq_len", "vocab_size",
             "shape", "split_interval", "elementwise", "depth", "num_input_components",
-            "num_repetitions")
+            "num_repetitions", "tree")
     cfg = S.StructureConfig(seed=0, tied=True, **{k: w[k] for k in keys if k in w})
     t0 = time.perf_counter()
     g = S.build_structure(cfg)
