@@ -200,3 +200,31 @@ def test_ratspn_depth7_repetitions():
     oracle.backward(c, rb, theta=theta0)
     want = oracle.em_step_full(c, rb.f_params, theta=theta0, pseudocount=1e-6)
     assert rel_err(got, want) < RTOL
+
+
+@pytest.mark.parametrize("tree,kw", [("chain", dict(num_vars=48)),
+                                     ("grid", dict(num_vars=48, shape=(4, 4, 3)))])
+def test_hclt_deep_trees(tree, kw):
+    """The deep-tree workloads' generators (hclt256_chain / hclt256_grid) at
+    reduced size: one TC layer per tree level, through the API and the
+    graphed lean training step."""
+    import torch
+    from paper_2406_00766_b200 import structures as S
+    from paper_2406_00766_b200.compiler import CompileConfig, compile_circuit
+    from paper_2406_00766_b200.runtime.em import apply_theta
+    from paper_2406_00766_b200.runtime.step import TrainStep
+    g = S.build_hclt(S.StructureConfig(kind="hclt", hidden_dim=64, num_categories=8, seed=2,
+                                       tree=tree, **kw))
+    c = compile_circuit(g, CompileConfig(block_size=32))
+    x = np.random.default_rng(15).integers(0, 8, size=(128, c.num_vars))
+    x[np.random.default_rng(16).random(x.shape) < 0.05] = -1
+    _api_vs_oracle(c, x, step=1.0)
+    theta0 = c.theta.copy()
+    ts = TrainStep(c, 128, pseudocount=1e-6, step_size=1.0, graph=True)
+    ts.run(torch.from_numpy(x.astype(np.int32)).cuda())
+    got = _np(ts.plan.theta)
+    apply_theta(c, theta0)
+    lr, rb = oracle.forward(c, x, theta=theta0)
+    oracle.backward(c, rb, theta=theta0)
+    want = oracle.em_step_full(c, rb.f_params, theta=theta0, pseudocount=1e-6)
+    assert rel_err(got, want) < RTOL
