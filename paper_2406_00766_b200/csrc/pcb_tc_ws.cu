@@ -17,24 +17,30 @@
 // so the batch tiles of one super-row run side by side and share its theta
 // tiles through L2.
 //
-// Warp roles (19 warps):
+// Warp roles (20 warps):
 //   warp 0      raw producer: one 2-D TMA box (cp.async.bulk.tensor) of the
 //               K block's fp32 rows x 128 samples per source array into the
 //               raw ring;
 //   warp 18     theta producer: 1-D bulk copies of the stacked pre-split bf16
-//               theta planes into the operand ring;
+//               theta planes into the theta ring (4 stages at block 32);
 //   warp 1      MMA issuer: three kind::f16 MMAs per 16-wide K step
-//               (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM), commits
-//               free operand stages and publish finished accumulators;
+//               (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM; A_hi kept
+//               in the operand collector for the second), commits free A and
+//               theta stages and publishes finished accumulators;
 //   warps 2-9   converters: thread = (sample, K half); raw row values -> shifted
 //               exponential (MUFU ex2, shift folded into one FFMA) -> packed
-//               bf16 hi/lo planes in the K-major core-matrix layout;
-//   warps 10-17 shift + epilogue: per-sample shift g_b of the next item (max
-//               of the side maxima bmax / rmax over its K blocks), then TMEM ->
-//               registers -> log-domain result -> coalesced fp32 row stores
-//               (two warps per TMEM lane quarter, alternate 16-column chunks).
-// Every hand-off is an mbarrier: raw full/empty, operand full/empty,
-// accumulator full/empty, shift full/empty.
+//               bf16 hi/lo planes in the K-major core-matrix layout (A ring);
+//   warp 19     shift warp: per-sample shift g_b of the next item (max of the
+//               block bases / ratio shifts over its K blocks), live-K count,
+//               output rows -- for long K with one item per CTA computed at
+//               kernel start by warps 2-17 and 19 together;
+//   warps 10-17 epilogue: TMEM -> registers -> log-domain result -> coalesced
+//               fp32 row stores (two warps per TMEM lane quarter, alternate
+//               16-column chunks); split K: partial sums reduced in L2, then
+//               the co-resident slices each finish a share of the columns (or
+//               the last arrival finishes the item).
+// Every hand-off is an mbarrier: raw full/empty, A full/empty, theta
+// full/empty, accumulator full/empty, shift full/empty.
 #include <math.h>
 #include <stdlib.h>
 
