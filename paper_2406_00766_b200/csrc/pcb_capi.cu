@@ -420,7 +420,8 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.rmax_all = w.gshift + 2 * P->max_tc_rows * (int64_t)ldb;
   w.prep = w.rmax_all + P->n_rmax * (int64_t)ldb;
   w.fprep = w.prep + P->max_prep_rows * (int64_t)ldb;
-  w.counters = reinterpret_cast<int32_t*>(w.fprep + P->fuse_prep_rows * (int64_t)ldb);
+  w.part = w.fprep + P->fuse_prep_rows * (int64_t)ldb;
+  w.counters = reinterpret_cast<int32_t*>(w.part + ws_part_floats());
   return w;
 }
 
@@ -452,7 +453,7 @@ int layer_forward(const pcb_plan* P, const Step& S, const Layer& L, cudaStream_t
     if (P->use_tc && T.count > 0 && tc_supported(L) && ws_supported((int)L.k_n, (int)L.k_m))
       st = launch_sum_fwd_ws(P, L, L.fwd[g], ws_long_k(L.fwd[g].cap) ? L.pf_tc[g] : T, s, B, ldb,
                              scratch, pbase, values, vbase, w.gshift, w.counters,
-                             L.fwd.size() == 1);
+                             L.fwd.size() == 1, w.part);
     else
       st = launch_sum_fwd_simt(L, L.fwd[g], s, B, ldb, theta, scratch, pbase, values, vbase);
     if (st) return st;
@@ -479,7 +480,7 @@ int child_flows(const pcb_plan* P, const Layer& L, cudaStream_t s, int B, int ld
     if (tc && T.count > 0 && P->use_tc == 1 && ws_supported((int)L.k_m, (int)L.k_n))
       st = launch_child_flow_ws(P, L, L.bwd[g], ws_long_k(L.bwd[g].cap) ? L.bwd_tc_full[g] : T,
                                 s, B, ldb, ratio, scratch, rmax, vbase, pbase, flow_scratch,
-                                w.gshift, w.counters, L.bwd.size() == 1);
+                                w.gshift, w.counters, L.bwd.size() == 1, w.part);
     else
       st = launch_child_flow_simt(L, L.bwd[g], s, B, ldb, theta, values, flows, scratch, pbase,
                                   vbase, flow_scratch);
@@ -747,6 +748,7 @@ int64_t pcb_plan_workspace_floats(const pcb_plan* plan, int ldb) {
   return (plan->n_sb_tot + plan->n_pb_tot + plan->max_sb + plan->max_sum_rows +
           2 * plan->max_tc_rows + plan->n_rmax + plan->max_prep_rows + plan->fuse_prep_rows) *
              (int64_t)ldb +
+         ws_part_floats() +
          plan->max_tc_rows * (int64_t)((ldb + 127) / 128);
 }
 

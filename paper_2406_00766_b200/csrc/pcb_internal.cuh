@@ -151,6 +151,7 @@ struct Work {
   float* rmax_all;  // [n_rmax x ldb] R rows of the pre-ratioed layers
   float* prep;
   float* fprep;
+  float* part;  // split-K partial sums of co-resident slices (one tile per CTA)
   int32_t* counters;
 };
 
@@ -414,11 +415,14 @@ inline bool ws_long_k(int64_t cap) { return cap >= 32; }
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* pbase,
                       float* values, float* vbase, float* gshift, int32_t* counters,
-                      bool split_ok);
+                      bool split_ok, float* part = nullptr);
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
                          const float* rmax, const float* vbase, const float* pbase,
-                         float* flow_scratch, float* gshift, int32_t* counters, bool split_ok);
+                         float* flow_scratch, float* gshift, int32_t* counters, bool split_ok,
+                         float* part = nullptr);
+// floats of the split-K partial-sum slab (one 128 x 256 tile per SM)
+int64_t ws_part_floats();
 bool pf_ws_supported(const Layer& L);
 bool pf_layer_stores(const pcb_plan* P, const Layer& L, int B);
 int launch_param_flow_ws(const Layer& L, const FwdGroup& g, const TcRows& tc, cudaStream_t s,

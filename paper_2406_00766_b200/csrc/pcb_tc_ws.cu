@@ -103,6 +103,7 @@ struct WsArgs {
   int64_t gshift_stride;           // ldb, or 0 when every super-row shares one shift row
   int coop;                        // long K, one item per CTA: shifts computed in-kernel
   int split_finish;                // coop split K: every slice finishes a share of the columns
+  float* part;                     // coop split K: this launch's partial-sum slab (or null)
 };
 
 struct WsItem {
@@ -683,7 +684,15 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
         for (int c0 = h * 16; c0 < N; c0 += 32) {
           float v[16];
           tmem_ld16(tbase + c0, v);
-          if (!live || !nks) continue;
+          if (!live) continue;
+          if (a.part) {  // this slice's partial sums: plain coalesced stores (zeros
+                         // for a slice without real K blocks: the finish reads every slice)
+            float* pp = a.part + ((int64_t)blockIdx.x * WS_NMAX + c0) * WS_M + t;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pp[(int64_t)i * WS_M] = nks ? v[i] : 0.f;
+            continue;
+          }
+          if (!nks) continue;
           float* o = a.out + out_row(c0) * a.ldb + b;
 #ifdef PCB_ABL_NOATOMIC  // timing ablation only: wrong results
 #pragma unroll
@@ -735,8 +744,20 @@ __global__ void __launch_bounds__(WsWarps<WsCfg<MODE, KC>::kNConv>::kThreads, 1)
             if (!live) continue;
             float* o = a.out + out_row(c0) * a.ldb + b;
             float d[16], l[16], pb = 0.f;
+            if (a.part) {  // the k slices' partial sums (one CTA per slice)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) d[i] = __ldcg(o + (int64_t)i * a.ldb);
+              for (int i = 0; i < 16; ++i) d[i] = 0.f;
+              for (int q = 0; q < a.kslices; ++q) {
+                const float* pp =
+                    a.part + ((int64_t)(it.tile + a.ntiles * (q + a.kslices * it.sr)) * WS_NMAX + c0) *
+                                 WS_M + t;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) d[i] += __ldcg(pp + (int64_t)i * WS_M);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) d[i] = __ldcg(o + (int64_t)i * a.ldb);
+            }
             if (MODE == MODE_CF) load_l(c0, l, pb);
             finish(c0, o, d, l, pb);
           }
@@ -889,6 +910,8 @@ void plan_split(WsArgs& a, int64_t count, bool split_ok) {
 
 }  // namespace
 
+int64_t ws_part_floats() { return (int64_t)sm_count() * WS_M * WS_NMAX; }
+
 bool ws_supported(int kc, int nb) { return (kc == 16 || kc == 32) && (nb == 16 || nb == 32 || nb == 64); }
 
 namespace {
@@ -900,7 +923,7 @@ bool tc_bwd_supported(const Layer& L) { return tc_k(L.k_m) && tc_k(L.k_n); }
 int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, const TcRows& tc,
                       cudaStream_t s, int B, int ldb, const float* scratch, const float* pbase,
                       float* values, float* vbase, float* gshift, int32_t* counters,
-                      bool split_ok) {
+                      bool split_ok, float* part) {
   ProfScope prof_(KC_SUM_FWD_TC, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -932,6 +955,9 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
     if (coop_ok(a)) {
       a.coop = 1;
       a.split_finish = getenv("PCB_NO_SPLIT_FINISH") == nullptr;
+      // partial sums through a slab instead of L2 reductions into the output
+      if (a.split_finish && a.kslices > 1 && part && getenv("PCB_NO_SPLIT_SLAB") == nullptr)
+        a.part = part;
     } else {
       if (launch_group_shift<MODE_FWD>(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, nullptr, s))
         return PCB_CUDA;
@@ -954,7 +980,8 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
 int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, const TcRows& tc,
                          cudaStream_t s, int B, int ldb, const float* ratio, const float* scratch,
                          const float* rmax, const float* vbase, const float* pbase,
-                         float* flow_scratch, float* gshift, int32_t* counters, bool split_ok) {
+                         float* flow_scratch, float* gshift, int32_t* counters, bool split_ok,
+                         float* part) {
   ProfScope prof_(KC_CHILD_FLOW, s);
   if (!tc.count || !B) return PCB_OK;
   WsArgs a{};
@@ -986,6 +1013,9 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
     if (coop_ok(a)) {
       a.coop = 1;
       a.split_finish = getenv("PCB_NO_SPLIT_FINISH") == nullptr;
+      // partial sums through a slab instead of L2 reductions into the output
+      if (a.split_finish && a.kslices > 1 && part && getenv("PCB_NO_SPLIT_SLAB") == nullptr)
+        a.part = part;
     } else {
       const int64_t n = g.uniform ? 1 : tc.count;
       if (launch_group_shift<MODE_CF>(a, (int)L.k_m, n, gshift, gshift + n * ldb, s))
