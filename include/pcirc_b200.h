@@ -177,7 +177,12 @@ int pcb_exec_set_flow_events(pcb_exec* exec, void* const* events, int n);
  *     non-finite results].  Without PCB_STEP_EM d_theta is read-only and
  *     d_f_params[:theta_size] holds the step's parameter flows (data-parallel
  *     steps all-reduce them, then call pcb_em_update).
- * d_prod_flows may be NULL as for pcb_backward; exec may be NULL (serial). */
+ * d_prod_flows may be NULL as for pcb_backward; exec may be NULL (serial).
+ * Concurrency: unlike the pure passes, at most one training step may be in
+ * flight per device at a time (a second one on another stream or under MPS
+ * must be ordered after it): the split-K slices of its long contractions
+ * wait for each other on the device and assume their launch owns the SMs it
+ * was granted.  Steps of different processes are time-sliced and safe. */
 int pcb_train_step(const pcb_plan* plan, const pcb_exec* exec, void* stream, int B, int ldb,
                    const int32_t* d_xT, float* d_theta, float* d_values, float* d_flows,
                    float* d_scratch, float* d_flow_scratch, float* d_prod_flows,

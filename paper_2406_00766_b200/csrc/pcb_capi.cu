@@ -410,7 +410,12 @@ __global__ void k_nonfinite(int64_t n, const float* __restrict__ x, int32_t* cnt
   if (c) atomicAdd(cnt, c);
 }
 
-Work carve(const pcb_plan* P, int ldb, float* d_work) {
+// spread: split-K slices of the long-K sum kernels may wait for each other
+// on the device (spread finish, partial-sum slab), which needs all of a
+// launch's CTAs co-resident: only training steps, whose contract is one step
+// in flight per device (pcirc_b200.h), enable it; the pure passes, which may
+// run on any number of concurrent streams, keep the last-arrival finish.
+Work carve(const pcb_plan* P, int ldb, float* d_work, bool spread = false) {
   Work w;
   w.vbase = d_work;
   w.pbase = w.vbase + P->n_sb_tot * (int64_t)ldb;
@@ -422,6 +427,7 @@ Work carve(const pcb_plan* P, int ldb, float* d_work) {
   w.fprep = w.prep + P->max_prep_rows * (int64_t)ldb;
   w.part = w.fprep + P->fuse_prep_rows * (int64_t)ldb;
   w.counters = reinterpret_cast<int32_t*>(w.part + ws_part_floats());
+  if (!spread) w.part = nullptr;
   return w;
 }
 
@@ -596,7 +602,7 @@ int layer_backward(const pcb_plan* P, Step& S, size_t li, cudaStream_t s, int B,
 int run_forward(const pcb_plan* P, const Step& S, cudaStream_t s, int B, int ldb,
                 const int32_t* d_xT, const float* d_theta, float* d_values, float* d_scratch,
                 float* d_lroot, float* d_work) {
-  const Work w = carve(P, ldb, d_work);
+  const Work w = carve(P, ldb, d_work, S.exclusive);
   // values.fill(-inf) (engine.py:204): every input and sum-block row (padding
   // rows included) is written below, so only the reserved constant rows need it.
   int st = launch_fill_range(s, 0, P->reserved, B, ldb, d_values, PCB_NEG_INF);
@@ -616,7 +622,7 @@ int run_backward(const pcb_plan* P, Step& S, cudaStream_t s, int B, int ldb,
                  float* d_work) {
   // prod_flows may be skipped only when no product row accumulates across layers
   if (!d_prod_flows && P->num_prod_rows && !P->prod_flows_optional) return PCB_USAGE;
-  const Work w = carve(P, ldb, d_work);
+  const Work w = carve(P, ldb, d_work, S.exclusive);
   {
     ProfScope prof_(KC_MISC, s);
     // replica ranges (past theta_size) are folded onto their master tiles and
@@ -788,6 +794,7 @@ int pcb_train_step(const pcb_plan* plan, const pcb_exec* exec, void* stream, int
   Step S;
   S.lean = (flags & PCB_STEP_LEAN) ? ((flags & PCB_STEP_SERIAL) || !exec ? 2 : 1) : 0;
   S.ex = exec;
+  S.exclusive = true;
   if (em) {
     S.em = S.lean != 0;  // EM inside the backward pass: lean launches only
     S.kappa = pseudocount;

@@ -253,6 +253,7 @@ struct Step {
   bool inputs_done = false;              // the input-flow pass updated the staged pmfs
   bool shared_done = false;              // ... and the shared pmfs
   bool pass = false;                     // a whole backward pass (stream placement known)
+  bool exclusive = false;                // pcb_train_step: one step in flight per device
 };
 
 // kernel classes for the live per-class timing used by bench.py

@@ -954,9 +954,11 @@ int launch_sum_fwd_ws(const pcb_plan* P, const Layer& L, const FwdGroup& g, cons
   if (ws_long_k(a.cap) && !shift_warp_ok(a)) {
     if (coop_ok(a)) {
       a.coop = 1;
-      a.split_finish = getenv("PCB_NO_SPLIT_FINISH") == nullptr;
+      // part != nullptr: the caller guarantees no other spread launch runs
+      // concurrently (pcb_capi.cu carve), so the slices may wait for each other
+      a.split_finish = part && getenv("PCB_NO_SPLIT_FINISH") == nullptr;
       // partial sums through a slab instead of L2 reductions into the output
-      if (a.split_finish && a.kslices > 1 && part && getenv("PCB_NO_SPLIT_SLAB") == nullptr)
+      if (a.split_finish && a.kslices > 1 && getenv("PCB_NO_SPLIT_SLAB") == nullptr)
         a.part = part;
     } else {
       if (launch_group_shift<MODE_FWD>(a, (int)L.k_n, g.uniform ? 1 : tc.count, gshift, nullptr, s))
@@ -1012,9 +1014,11 @@ int launch_child_flow_ws(const pcb_plan* P, const Layer& L, const BwdGroup& g, c
   if (ws_long_k(a.cap) && !shift_warp_ok(a)) {
     if (coop_ok(a)) {
       a.coop = 1;
-      a.split_finish = getenv("PCB_NO_SPLIT_FINISH") == nullptr;
+      // part != nullptr: the caller guarantees no other spread launch runs
+      // concurrently (pcb_capi.cu carve), so the slices may wait for each other
+      a.split_finish = part && getenv("PCB_NO_SPLIT_FINISH") == nullptr;
       // partial sums through a slab instead of L2 reductions into the output
-      if (a.split_finish && a.kslices > 1 && part && getenv("PCB_NO_SPLIT_SLAB") == nullptr)
+      if (a.split_finish && a.kslices > 1 && getenv("PCB_NO_SPLIT_SLAB") == nullptr)
         a.part = part;
     } else {
       const int64_t n = g.uniform ? 1 : tc.count;
