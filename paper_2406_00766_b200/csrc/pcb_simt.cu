@@ -9,6 +9,7 @@
 #include <stdlib.h>
 
 #include "pcb_internal.cuh"
+#include "pcb_tc.cuh"
 
 namespace pcb {
 
@@ -123,6 +124,14 @@ __global__ void k_input_fwd(int64_t n, int B, int ldb, const int32_t* __restrict
 // each pull a 32-byte sector of a pmf table far larger than L2.
 constexpr int IN_THREADS = 512;
 constexpr int SP_THREADS = 1024;  // shared-pmf input kernels
+#ifndef PCB_SP_UNROLL
+#define PCB_SP_UNROLL 16
+#endif
+#ifndef PCB_SP_ITEMS
+#define PCB_SP_ITEMS 8
+#endif
+constexpr int SP_UNROLL = PCB_SP_UNROLL;  // row loads in flight per thread
+constexpr int SP_ITEMS = PCB_SP_ITEMS;    // (input, sample) loads in flight per thread
 
 __global__ void __launch_bounds__(IN_THREADS)
     k_input_fwd_block(int B, int ldb, const int32_t* __restrict__ bvar,
@@ -217,38 +226,69 @@ __global__ void __launch_bounds__(IN_THREADS)
 }
 
 // Shared pmfs (plan.shared_pmf_table): one CTA per pmf stages its log-pmf in
-// shared memory once (a coalesced row read) and serves every (input,
-// sample) of the inputs that use it from there — instead of one random
-// 32-byte-sector gather of the pmf table per (input, sample).
+// shared memory once and serves every (input, sample) of the inputs that use
+// it from there -- instead of one random 32-byte-sector gather of the pmf
+// table per (input, sample).  The row (up to 201 KB for HMM emissions) comes
+// in by 1-D TMA bulk copies from its 16-byte-aligned start (the ragged tail
+// by plain loads), so the whole row is in flight at once rather than a few
+// loads per thread; the logs are then taken in place.
+#ifndef PCB_SP_FWD_BULK
+#define PCB_SP_FWD_BULK 1
+#endif
+constexpr int SP_BULK_CHUNK = 16384;  // bytes per bulk copy
 __global__ void __launch_bounds__(SP_THREADS)
     k_input_fwd_shared(int ncat, int B, int ldb, const int32_t* __restrict__ u_pid,
                        const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
                        const int32_t* __restrict__ u_var, const int32_t* __restrict__ xT,
                        const float* __restrict__ theta, float* __restrict__ values) {
   pdl_enter();
-  extern __shared__ float tbl[];
+  extern __shared__ __align__(16) float tbl_raw[];
   const int u = blockIdx.x, tid = threadIdx.x;
-  const float* th = theta + __ldg(u_pid + u);
+  const int64_t pid = __ldg(u_pid + u);
+#if PCB_SP_FWD_BULK
+  __shared__ __align__(8) uint64_t mbar;
+  const int64_t a0 = pid & ~(int64_t)3, end = pid + ncat;
+  const int64_t a1 = end & ~(int64_t)3;  // the body [a0, a1) by TMA
+  const int lead = (int)(pid - a0);
+  float* tbl = tbl_raw + lead;           // tbl[c] = pmf entry c
+  const uint32_t mb = tc::smem_u32(&mbar);
+  if (tid == 0) {
+    tc::mbar_init(mb, 1);
+    tc::fence_mbar_init();
+    const uint32_t body = (uint32_t)((a1 - a0) * 4);
+    tc::mbar_arrive_expect_tx(mb, body);
+    for (uint32_t off = 0; off < body; off += SP_BULK_CHUNK)
+      tc::bulk_g2s(tc::smem_u32(tbl_raw) + off, theta + a0 + off / 4, min(SP_BULK_CHUNK, (int)(body - off)),
+               mb);
+  }
+  for (int64_t c = (a1 > pid ? a1 : pid) + tid; c < end; c += SP_THREADS)
+    tbl_raw[c - a0] = __ldg(theta + c);
+  __syncthreads();  // mbarrier initialised, tail stored
+  tc::mbar_wait(mb, 0);
+  for (int c = tid; c < ncat; c += SP_THREADS) tbl[c] = __logf(tbl[c]);
+#else
+  float* tbl = tbl_raw;
+  const float* th = theta + pid;
   for (int c = tid; c < ncat; c += SP_THREADS) tbl[c] = __logf(__ldg(th + c));
+#endif
   __syncthreads();
   const int e0 = __ldg(u_off + u), e1 = __ldg(u_off + u + 1);
   const int n_items = (e1 - e0) * B;
-  for (int t0 = tid; t0 < n_items; t0 += 4 * SP_THREADS) {
-    int x[4];
-    int64_t o[4];
+  // branch-free batches (indices clamped to the last item) so every item's
+  // loads issue before the first one is used
+  for (int t0 = tid; t0 < n_items; t0 += SP_ITEMS * SP_THREADS) {
+    int x[SP_ITEMS];
+    int64_t o[SP_ITEMS];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int t = t0 + k * SP_THREADS;
-      o[k] = -1;
-      if (t < n_items) {
-        const int e = e0 + t / B, b = t - (t / B) * B;
-        x[k] = __ldg(xT + (int64_t)__ldg(u_var + e) * ldb + b);
-        o[k] = (int64_t)__ldg(u_slot + e) * ldb + b;
-      }
+    for (int k = 0; k < SP_ITEMS; ++k) {
+      const int t = min(t0 + k * SP_THREADS, n_items - 1);
+      const int e = e0 + t / B, b = t - (t / B) * B;
+      o[k] = (int64_t)__ldg(u_slot + e) * ldb + b;
+      x[k] = __ldg(xT + (int64_t)__ldg(u_var + e) * ldb + b);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (o[k] >= 0) values[o[k]] = x[k] < 0 ? 0.f : tbl[x[k]];
+    for (int k = 0; k < SP_ITEMS; ++k)
+      if (t0 + k * SP_THREADS < n_items) values[o[k]] = x[k] < 0 ? 0.f : tbl[x[k]];
   }
 }
 
@@ -275,7 +315,7 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
     int64_t total = c.n * B;
     if (!total) continue;
     if (c.n_u) {
-      const int bytes = (int)c.ncat * 4;
+      const int bytes = (int)(c.ncat + 4) * 4;  // + the aligned row start's lead
       static int attr_sp[kMaxDev] = {};
       if (ensure_smem((const void*)k_input_fwd_shared, bytes, attr_sp)) return PCB_CUDA;
       launch_k(k_input_fwd_shared, dim3((unsigned)c.n_u), dim3(SP_THREADS), bytes, s, 
@@ -1439,26 +1479,24 @@ __global__ void __launch_bounds__(SP_THREADS)
   __syncthreads();
   float miss = 0.f;
   const int e0 = __ldg(u_off + u), e1 = __ldg(u_off + u + 1);
-  // every (input, sample) pair of the pmf spread over the whole CTA, four
+  // every (input, sample) pair of the pmf spread over the whole CTA, SP_ITEMS
   // pairs' loads in flight per thread before their shared-memory atomics
   const int n_items = (e1 - e0) * B;
-  for (int t0 = tid; t0 < n_items; t0 += 4 * SP_THREADS) {
-    float f[4];
-    int x[4];
+  for (int t0 = tid; t0 < n_items; t0 += SP_ITEMS * SP_THREADS) {
+    float f[SP_ITEMS];
+    int x[SP_ITEMS];
+    // branch-free batch (indices clamped to the last item): every item's
+    // loads issue before the first atomic
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int t = t0 + k * SP_THREADS;
-      f[k] = 0.f;
-      x[k] = 0;
-      if (t < n_items) {
-        const int e = e0 + t / B, b = t - (t / B) * B;
-        f[k] = flows[(int64_t)__ldg(u_slot + e) * ldb + b];
-        x[k] = __ldg(xT + (int64_t)__ldg(u_var + e) * ldb + b);
-      }
+    for (int k = 0; k < SP_ITEMS; ++k) {
+      const int t = min(t0 + k * SP_THREADS, n_items - 1);
+      const int e = e0 + t / B, b = t - (t / B) * B;
+      f[k] = flows[(int64_t)__ldg(u_slot + e) * ldb + b];
+      x[k] = __ldg(xT + (int64_t)__ldg(u_var + e) * ldb + b);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (f[k] == 0.f) continue;
+    for (int k = 0; k < SP_ITEMS; ++k) {
+      if (t0 + k * SP_THREADS >= n_items || f[k] == 0.f) continue;
       if (x[k] >= 0)
         atomicAdd(hist + x[k], f[k]);
       else
@@ -1484,20 +1522,50 @@ __global__ void __launch_bounds__(SP_THREADS)
   }
   // inline EM: F = flows (+ missing spread over theta), total sum(F + kappa)
   float tot = 0.f;
-  for (int c = tid; c < ncat; c += SP_THREADS) {
-    const float F = hist[c] + (miss != 0.f ? miss * th[c] : 0.f);
-    hist[c] = F;
-    tot += F + kappa;
+  if (miss != 0.f) {
+    for (int c0 = tid; c0 < ncat; c0 += SP_UNROLL * SP_THREADS) {
+      float v[SP_UNROLL];
+#pragma unroll
+      for (int k = 0; k < SP_UNROLL; ++k) {
+        const int c = c0 + k * SP_THREADS;
+        v[k] = c < ncat ? th[c] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < SP_UNROLL; ++k) {
+        const int c = c0 + k * SP_THREADS;
+        if (c < ncat) {
+          const float F = hist[c] + miss * v[k];
+          hist[c] = F;
+          tot += F + kappa;
+        }
+      }
+    }
+  } else {
+    for (int c = tid; c < ncat; c += SP_THREADS) tot += hist[c] + kappa;
   }
   tot = block_sum(tot);
   if (!(tot > 0.f)) return;  // uninformative group keeps theta (em.py:67-80)
   const float inv = 1.f / tot;
   int bad = 0;
-  for (int c = tid; c < ncat; c += SP_THREADS) {
-    const float nv = (hist[c] + kappa) * inv;
-    const float t = (step >= 1.f) ? nv : ((1.f - step) * th[c] + step * nv);
-    bad += !isfinite(t);
-    th[c] = t;
+  // the blend's theta read and write are the pass's traffic: SP_UNROLL
+  // loads in flight per thread
+  for (int c0 = tid; c0 < ncat; c0 += SP_UNROLL * SP_THREADS) {
+    float v[SP_UNROLL];
+#pragma unroll
+    for (int k = 0; k < SP_UNROLL; ++k) {
+      const int c = c0 + k * SP_THREADS;
+      v[k] = (c < ncat && step < 1.f) ? th[c] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < SP_UNROLL; ++k) {
+      const int c = c0 + k * SP_THREADS;
+      if (c < ncat) {
+        const float nv = (hist[c] + kappa) * inv;
+        const float t = (step >= 1.f) ? nv : ((1.f - step) * v[k] + step * nv);
+        bad += !isfinite(t);
+        th[c] = t;
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
   if (tid == 0) atomicAdd(status, 1);
