@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(IN_THREADS)
 #ifndef PCB_SP_FWD_BULK
 #define PCB_SP_FWD_BULK 1
 #endif
-constexpr int SP_BULK_CHUNK = 16384;  // bytes per bulk copy
+constexpr int SP_BULK_CHUNK = 16384;  // bytes per bulk copy / L2 prefetch
+#ifndef PCB_SP_FLOW_PREFETCH
+#define PCB_SP_FLOW_PREFETCH 1
+#endif
 __global__ void __launch_bounds__(SP_THREADS)
     k_input_fwd_shared(int ncat, int B, int ldb, const int32_t* __restrict__ u_pid,
                        const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
@@ -1475,6 +1478,18 @@ __global__ void __launch_bounds__(SP_THREADS)
   __shared__ float red[SP_THREADS / 32];
   const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t pid = __ldg(u_pid + u);
+#if PCB_SP_FLOW_PREFETCH
+  // the inline-EM blend reads the whole theta row after the histogram: have
+  // TMA pull its aligned body into L2 now, under the histogram phase
+  if (em && tid == 0) {
+    const int64_t a0 = (pid + 3) & ~(int64_t)3, a1 = (pid + ncat) & ~(int64_t)3;
+    for (int64_t o = a0; o < a1; o += SP_BULK_CHUNK / 4) {
+      const uint32_t bytes = (uint32_t)(min((int64_t)SP_BULK_CHUNK / 4, a1 - o) * 4);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(theta + o), "r"(bytes)
+                   : "memory");
+    }
+  }
+#endif
   for (int c = tid; c < ncat; c += SP_THREADS) hist[c] = 0.f;
   __syncthreads();
   float miss = 0.f;
