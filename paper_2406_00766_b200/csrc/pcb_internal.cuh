@@ -401,6 +401,18 @@ int launch_fill(cudaStream_t s, const int32_t* rows, int64_t n, int B, int ldb, 
 int launch_zero_ranges(cudaStream_t s, int64_t n, const int32_t* start, const int32_t* len,
                        int ldb, float* buf);
 
+// streaming multiprocessors of the current device (grid sizing)
+inline int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 // tensor-core support (pcb_tc.cu)
 bool tc_supported(const Layer& L);
 bool tc_bwd_supported(const Layer& L);

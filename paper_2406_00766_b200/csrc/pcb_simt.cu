@@ -239,11 +239,25 @@ constexpr int SP_BULK_CHUNK = 16384;  // bytes per bulk copy / L2 prefetch
 #ifndef PCB_SP_FLOW_PREFETCH
 #define PCB_SP_FLOW_PREFETCH 1
 #endif
+#ifndef PCB_SP_NEXT
+#define PCB_SP_NEXT 1
+#endif
+// L2 prefetch (TMA) of the 16-byte-aligned body of floats [p0, p1)
+__device__ __forceinline__ void l2_prefetch_row(const float* base, int64_t p0, int64_t p1) {
+  const int64_t a0 = (p0 + 3) & ~(int64_t)3, a1 = p1 & ~(int64_t)3;
+  for (int64_t o = a0; o < a1; o += SP_BULK_CHUNK / 4) {
+    const uint32_t bytes = (uint32_t)(min((int64_t)SP_BULK_CHUNK / 4, a1 - o) * 4);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(bytes)
+                 : "memory");
+  }
+}
+
 __global__ void __launch_bounds__(SP_THREADS)
     k_input_fwd_shared(int ncat, int B, int ldb, const int32_t* __restrict__ u_pid,
                        const int32_t* __restrict__ u_off, const int32_t* __restrict__ u_slot,
                        const int32_t* __restrict__ u_var, const int32_t* __restrict__ xT,
-                       const float* __restrict__ theta, float* __restrict__ values) {
+                       const float* __restrict__ theta, float* __restrict__ values,
+                       int n_u, int nsm) {
   pdl_enter();
   extern __shared__ __align__(16) float tbl_raw[];
   const int u = blockIdx.x, tid = threadIdx.x;
@@ -263,6 +277,13 @@ __global__ void __launch_bounds__(SP_THREADS)
     for (uint32_t off = 0; off < body; off += SP_BULK_CHUNK)
       tc::bulk_g2s(tc::smem_u32(tbl_raw) + off, theta + a0 + off / 4, min(SP_BULK_CHUNK, (int)(body - off)),
                mb);
+#if PCB_SP_NEXT
+    // the row of the CTA that takes this SM next, into L2 under this one's work
+    if (u + nsm < n_u) {
+      const int64_t nx = __ldg(u_pid + u + nsm);
+      l2_prefetch_row(theta, nx, nx + ncat);
+    }
+#endif
   }
   for (int64_t c = (a1 > pid ? a1 : pid) + tid; c < end; c += SP_THREADS)
     tbl_raw[c - a0] = __ldg(theta + c);
@@ -322,7 +343,8 @@ int launch_input_fwd(const pcb_plan* p, cudaStream_t s, int B, int ldb, const in
       static int attr_sp[kMaxDev] = {};
       if (ensure_smem((const void*)k_input_fwd_shared, bytes, attr_sp)) return PCB_CUDA;
       launch_k(k_input_fwd_shared, dim3((unsigned)c.n_u), dim3(SP_THREADS), bytes, s, 
-          (int)c.ncat, B, ldb, c.u_pid, c.u_off, c.u_slot, c.u_var, xT, theta, values);
+          (int)c.ncat, B, ldb, c.u_pid, c.u_off, c.u_slot, c.u_var, xT, theta, values,
+          (int)c.n_u, sm_count());
       if (check_launch()) return PCB_CUDA;
       continue;
     }
@@ -1480,15 +1502,9 @@ __global__ void __launch_bounds__(SP_THREADS)
   const int64_t pid = __ldg(u_pid + u);
 #if PCB_SP_FLOW_PREFETCH
   // the inline-EM blend reads the whole theta row after the histogram: have
-  // TMA pull its aligned body into L2 now, under the histogram phase
-  if (em && tid == 0) {
-    const int64_t a0 = (pid + 3) & ~(int64_t)3, a1 = (pid + ncat) & ~(int64_t)3;
-    for (int64_t o = a0; o < a1; o += SP_BULK_CHUNK / 4) {
-      const uint32_t bytes = (uint32_t)(min((int64_t)SP_BULK_CHUNK / 4, a1 - o) * 4);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(theta + o), "r"(bytes)
-                   : "memory");
-    }
-  }
+  // TMA pull its aligned body into L2 now, under the histogram phase (the
+  // next CTA's row as well measured slower: the blend already streams)
+  if (em && tid == 0) l2_prefetch_row(theta, pid, pid + ncat);
 #endif
   for (int c = tid; c < ncat; c += SP_THREADS) hist[c] = 0.f;
   __syncthreads();
