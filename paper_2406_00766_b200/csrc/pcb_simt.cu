@@ -133,6 +133,19 @@ constexpr int SP_THREADS = 1024;  // shared-pmf input kernels
 constexpr int SP_UNROLL = PCB_SP_UNROLL;  // row loads in flight per thread
 constexpr int SP_ITEMS = PCB_SP_ITEMS;    // (input, sample) loads in flight per thread
 
+#ifndef PCB_IN_PREFETCH
+#define PCB_IN_PREFETCH 1
+#endif
+// TMA L2 prefetch of floats [p, p + n) (16-byte-aligned body only)
+__device__ __forceinline__ void l2_prefetch(const float* p, int64_t n) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 15) & ~(uintptr_t)15;
+  const uintptr_t e = reinterpret_cast<uintptr_t>(p + n) & ~(uintptr_t)15;
+  for (uintptr_t o = a; o < e; o += 16384) {
+    const uint32_t bytes = (uint32_t)(e - o < 16384 ? e - o : 16384);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(o), "r"(bytes) : "memory");
+  }
+}
+
 __global__ void __launch_bounds__(IN_THREADS)
     k_input_fwd_block(int B, int ldb, const int32_t* __restrict__ bvar,
                       const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
@@ -148,6 +161,11 @@ __global__ void __launch_bounds__(IN_THREADS)
   const int64_t slot0 = bslot0[blk];
   const int32_t* pid = pids + bpoff[blk];
   const int total = cnt * ncat;
+#if PCB_IN_PREFETCH
+  // every pmf row of the block into L2 at once (TMA), ahead of the staging
+  // loads below, which then hit L2
+  for (int i = threadIdx.x; i < cnt; i += IN_THREADS) l2_prefetch(theta + __ldg(pid + i), ncat);
+#endif
   // stage log-pmfs: a warp per input row, float4 loads when the pmf is
   // 16-byte aligned (4 rows in flight per warp), else scalar loads
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
