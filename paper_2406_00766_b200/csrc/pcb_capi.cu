@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 26;
+constexpr int64_t kVersion = 27;
 
 struct Reader {
   const int64_t* p;
@@ -277,6 +277,7 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
     L.em_fusable = (int)r.get();
   }
   P->n_shared_inline = r.get();
+  P->em_split32 = (int)r.get();  // some tile block takes k_em_tiles32
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;

@@ -179,6 +179,7 @@ struct pcb_plan {
   // (updated tile by tile, bf16 planes written in the same pass); the other
   // groups (em_rest) take the generic per-group pass
   int64_t n_em_blk = 0, n_em_tiles = 0, n_em_rest = 0, n_em_small = 0;  // rest: small first
+  int em_split32 = 0;  // some tile block takes k_em_tiles32 (pcb_tc.cu)
   const int32_t *em_km = nullptr, *em_kn = nullptr, *em_tile_off = nullptr, *em_goff = nullptr,
                 *em_tile_start = nullptr, *em_tile_slab_f = nullptr, *em_tile_slab_c = nullptr,
                 *em_rest = nullptr,
@@ -417,6 +418,8 @@ inline int sm_count() {
 bool tc_supported(const Layer& L);
 bool tc_bwd_supported(const Layer& L);
 int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta);
+// EM tile block handled by the split kernel k_em_tiles32
+bool em_split32_block(int km, int kn, int ntiles);
 // warp-specialised persistent tensor-core kernels (pcb_tc_ws.cu), K block 16 / 32
 bool ws_supported(int kc, int nb);
 // long contractions (>= 32 K blocks, e.g. HMM's 4096-wide layers) use full

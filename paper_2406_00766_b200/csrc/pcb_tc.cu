@@ -242,6 +242,10 @@ constexpr int EM_NP = 4;  // row passes per thread (k_m x k_n <= 64 x 64)
 // memory for one plane-packing pass
 constexpr int EM_RT = 8;
 constexpr int EM_SMEM = (8 * 32 * 33 > TM_MAX * (TM_MAX + 1)) ? 8 * 32 * 33 : TM_MAX * (TM_MAX + 1);
+// tile blocks of k_em_tiles32: 32 x 32 tiles, more than one register round
+__host__ __device__ __forceinline__ bool split32_blk(int km, int kn, int nt) {
+  return km == 32 && kn == 32 && nt > EM_RT;
+}
 __global__ void __launch_bounds__(EM_THREADS)
     k_em_tiles(int64_t blk0, int64_t n_blk, const int32_t* __restrict__ bkm,
                const int32_t* __restrict__ bkn,
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(EM_THREADS)
                const int32_t* __restrict__ tslab_f, const int32_t* __restrict__ tslab_c,
                const float* __restrict__ F, float* __restrict__ theta,
                __nv_bfloat16* __restrict__ mma, int64_t plane_n, float kappa, float step,
-               int planes, int32_t* status) {
+               int planes, int32_t* status, int skip32) {
   pdl_enter();
   __shared__ float tile[EM_SMEM];
   const int tid = threadIdx.x;
@@ -257,85 +261,106 @@ __global__ void __launch_bounds__(EM_THREADS)
   for (int64_t b = blk0 + blockIdx.x; b < n_blk; b += gridDim.x) {
     const int km = __ldg(bkm + b), kn = __ldg(bkn + b);
     const int t0 = __ldg(toff + b), t1 = __ldg(toff + b + 1);
-    if (km * kn == 4 * EM_THREADS && km == 32 && t1 - t0 <= EM_RT) {
+    if (skip32 && split32_blk(km, kn, t1 - t0)) continue;  // k_em_tiles32
+    if (km == 32 && kn == 32) {
+      // 32 x 32 tiles, any number per block (HMM-4096: 128): the row totals
+      // with EM_RT tiles' flows in flight per round, then blend / store /
+      // pack EM_RT tiles per round (their flows and theta loaded together;
+      // one barrier pair per round instead of per tile)
       const int r = tid >> 3, c4 = (tid & 7) * 4;  // row, column quad (k_n = 32)
+      const int nt = t1 - t0;
       float4 fv[EM_RT], ov[EM_RT];
-#pragma unroll
-      for (int u = 0; u < EM_RT; ++u) {
-        if (t0 + u < t1) {
-          const int64_t o = __ldg(tstart + t0 + u) + r * 32 + c4;
-          fv[u] = ld4(F + o);
-          ov[u] = ld4(theta + o);
-        }
-      }
       float acc = 0.f;
+      for (int c0 = 0; c0 < nt; c0 += EM_RT) {
 #pragma unroll
-      for (int u = 0; u < EM_RT; ++u)
-        if (t0 + u < t1)
-          acc += (fv[u].x + kappa) + (fv[u].y + kappa) + (fv[u].z + kappa) + (fv[u].w + kappa);
+        for (int u = 0; u < EM_RT; ++u) {
+          if (c0 + u < nt) {
+            const int64_t o = __ldg(tstart + t0 + c0 + u) + r * 32 + c4;
+            fv[u] = ld4(F + o);
+            if (nt <= EM_RT) ov[u] = ld4(theta + o);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < EM_RT; ++u)
+          if (c0 + u < nt)
+            acc += (fv[u].x + kappa) + (fv[u].y + kappa) + (fv[u].z + kappa) + (fv[u].w + kappa);
+      }
 #pragma unroll
       for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       const float inv = acc > 0.f ? 1.f / acc : 0.f;
       if (acc > 0.f && (tid & 7) == 0) ++informative;
+      for (int c0 = 0; c0 < nt; c0 += EM_RT) {
+        const int nc = min(EM_RT, nt - c0);
+        if (nt > EM_RT) {
 #pragma unroll
-      for (int u = 0; u < EM_RT; ++u) {
-        if (t0 + u >= t1) continue;
-        float4 o = ov[u];
-        if (inv > 0.f) {
-          const float4 f = fv[u];
-          const float n[4] = {(f.x + kappa) * inv, (f.y + kappa) * inv, (f.z + kappa) * inv,
-                              (f.w + kappa) * inv};
-          float* op = &o.x;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            op[e] = (step >= 1.f) ? n[e] : ((1.f - step) * op[e] + step * n[e]);
-            if (!isfinite(op[e])) ++bad;
-          }
-          float* tp = theta + __ldg(tstart + t0 + u) + r * 32 + c4;
-          if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
-            *reinterpret_cast<float4*>(tp) = o;
-          } else {
-            tp[0] = o.x, tp[1] = o.y, tp[2] = o.z, tp[3] = o.w;
+          for (int u = 0; u < EM_RT; ++u) {
+            if (u < nc) {
+              const int64_t o = __ldg(tstart + t0 + c0 + u) + r * 32 + c4;
+              fv[u] = ld4(F + o);
+              ov[u] = ld4(theta + o);
+            }
           }
         }
-        if (planes) {
-          float* d = tile + u * (32 * 33) + r * 33 + c4;
-          d[0] = o.x, d[1] = o.y, d[2] = o.z, d[3] = o.w;
-        }
-      }
-      if (!planes) continue;
-      __syncthreads();
-      const int nt = t1 - t0, n8 = 32 * 32 / 8;
-      for (int q = tid; q < nt * 2 * n8; q += EM_THREADS) {
-        const int u = q / (2 * n8), qq = q - u * 2 * n8;
-        const float* tl = tile + u * (32 * 33);
-        float v[8];
-        uint32_t off;
-        int pl;
-        if (qq < n8) {  // sum-major core row (m, j..j+7)
-          const int m = qq >> 2, j = (qq & 3) * 8;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = tl[m * 33 + j + e];
-          off = (uint32_t)tile_off(m, j, 32) * 2u;
-          pl = 0;
-        } else {  // product-major core row (j, m..m+7)
-          const int rr = qq - n8;
-          const int j = rr >> 2, m = (rr & 3) * 8;
+        for (int u = 0; u < EM_RT; ++u) {
+          if (u >= nc) continue;
+          float4 o = ov[u];
+          if (inv > 0.f) {
+            const float4 f = fv[u];
+            const float n[4] = {(f.x + kappa) * inv, (f.y + kappa) * inv, (f.z + kappa) * inv,
+                                (f.w + kappa) * inv};
+            float* op = &o.x;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = tl[(m + e) * 33 + j];
-          off = (uint32_t)tile_off(j, m, 32) * 2u;
-          pl = 2;
+            for (int e = 0; e < 4; ++e) {
+              op[e] = (step >= 1.f) ? n[e] : ((1.f - step) * op[e] + step * n[e]);
+              if (!isfinite(op[e])) ++bad;
+            }
+            float* tp = theta + __ldg(tstart + t0 + c0 + u) + r * 32 + c4;
+            if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
+              *reinterpret_cast<float4*>(tp) = o;
+            } else {
+              tp[0] = o.x, tp[1] = o.y, tp[2] = o.z, tp[3] = o.w;
+            }
+          }
+          if (planes) {
+            float* d = tile + u * (32 * 33) + r * 33 + c4;
+            d[0] = o.x, d[1] = o.y, d[2] = o.z, d[3] = o.w;
+          }
         }
-        uint4 hi, lo;
-        split_pack8(v, hi, lo);
-        uint8_t* dst = reinterpret_cast<uint8_t*>(
-                           pl == 0 ? mma + __ldg(tslab_f + t0 + u)
-                                   : mma + 2 * plane_n + __ldg(tslab_c + t0 + u)) +
-                       off;
-        *reinterpret_cast<uint4*>(dst) = hi;
-        *reinterpret_cast<uint4*>(dst + plane_n * 2) = lo;
+        if (!planes) continue;
+        __syncthreads();
+        const int n8 = 32 * 32 / 8;
+        for (int q = tid; q < nc * 2 * n8; q += EM_THREADS) {
+          const int u = q / (2 * n8), qq = q - u * 2 * n8;
+          const float* tl = tile + u * (32 * 33);
+          float v[8];
+          uint32_t off;
+          int pl;
+          if (qq < n8) {  // sum-major core row (m, j..j+7)
+            const int m = qq >> 2, j = (qq & 3) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = tl[m * 33 + j + e];
+            off = (uint32_t)tile_off(m, j, 32) * 2u;
+            pl = 0;
+          } else {  // product-major core row (j, m..m+7)
+            const int rr = qq - n8;
+            const int j = rr >> 2, m = (rr & 3) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = tl[(m + e) * 33 + j];
+            off = (uint32_t)tile_off(j, m, 32) * 2u;
+            pl = 2;
+          }
+          uint4 hi, lo;
+          split_pack8(v, hi, lo);
+          uint8_t* dst = reinterpret_cast<uint8_t*>(
+                             pl == 0 ? mma + __ldg(tslab_f + t0 + c0 + u)
+                                     : mma + 2 * plane_n + __ldg(tslab_c + t0 + c0 + u)) +
+                         off;
+          *reinterpret_cast<uint4*>(dst) = hi;
+          *reinterpret_cast<uint4*>(dst + plane_n * 2) = lo;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       continue;
     }
 
@@ -471,18 +496,159 @@ __global__ void __launch_bounds__(EM_THREADS)
   }
 }
 
+// Blocks of more than EM_RT 32 x 32 tiles (HMM-4096: 128 per block, only
+// 128 blocks): four 256-thread tile groups per CTA split the block's tiles
+// (rounds of E32_RT tiles, interleaved), combine their row partials in
+// shared memory in a fixed order, then blend / store / pack their own tiles
+// under per-group named barriers -- four times the loads in flight of one
+// group per block.
+constexpr int E32_G = 4, E32_RT = 4;
+constexpr int E32_SMEM = E32_G * E32_RT * 32 * 33 * 4;
+__global__ void __launch_bounds__(E32_G * 256, 1)
+    k_em_tiles32(int64_t blk0, int64_t n_blk, const int32_t* __restrict__ bkm,
+                 const int32_t* __restrict__ bkn, const int32_t* __restrict__ toff,
+                 const int32_t* __restrict__ tstart, const int32_t* __restrict__ tslab_f,
+                 const int32_t* __restrict__ tslab_c, const float* __restrict__ F,
+                 float* __restrict__ theta, __nv_bfloat16* __restrict__ mma, int64_t plane_n,
+                 float kappa, float step, int planes, int32_t* status) {
+  pdl_enter();
+  extern __shared__ __align__(16) float e32_tiles[];
+  __shared__ float part[E32_G][32];
+  const int tid = threadIdx.x, g = tid >> 8, lt = tid & 255;
+  const int r = lt >> 3, c4 = (lt & 7) * 4;  // row, column quad
+  float* tile = e32_tiles + g * (E32_RT * 32 * 33);
+  int informative = 0, bad = 0;
+  for (int64_t b = blk0 + blockIdx.x; b < n_blk; b += gridDim.x) {
+    const int km = __ldg(bkm + b), kn = __ldg(bkn + b);
+    const int t0 = __ldg(toff + b), t1 = __ldg(toff + b + 1);
+    if (!split32_blk(km, kn, t1 - t0)) continue;
+    const int nt = t1 - t0;
+    float4 fv[E32_RT], ov[E32_RT];
+    float acc = 0.f;
+    for (int c0 = g * E32_RT; c0 < nt; c0 += E32_G * E32_RT) {
+#pragma unroll
+      for (int u = 0; u < E32_RT; ++u)
+        if (c0 + u < nt) fv[u] = ld4(F + __ldg(tstart + t0 + c0 + u) + r * 32 + c4);
+#pragma unroll
+      for (int u = 0; u < E32_RT; ++u)
+        if (c0 + u < nt)
+          acc += (fv[u].x + kappa) + (fv[u].y + kappa) + (fv[u].z + kappa) + (fv[u].w + kappa);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((lt & 7) == 0) part[g][r] = acc;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int q = 0; q < E32_G; ++q) tot += part[q][r];
+    const float inv = tot > 0.f ? 1.f / tot : 0.f;
+    if (tot > 0.f && g == 0 && (lt & 7) == 0) ++informative;
+    for (int c0 = g * E32_RT; c0 < nt; c0 += E32_G * E32_RT) {
+      const int nc = min(E32_RT, nt - c0);
+#pragma unroll
+      for (int u = 0; u < E32_RT; ++u) {
+        if (u < nc) {
+          const int64_t o = __ldg(tstart + t0 + c0 + u) + r * 32 + c4;
+          fv[u] = ld4(F + o);
+          ov[u] = ld4(theta + o);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < E32_RT; ++u) {
+        if (u >= nc) continue;
+        float4 o = ov[u];
+        if (inv > 0.f) {
+          const float4 f = fv[u];
+          const float n[4] = {(f.x + kappa) * inv, (f.y + kappa) * inv, (f.z + kappa) * inv,
+                              (f.w + kappa) * inv};
+          float* op = &o.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            op[e] = (step >= 1.f) ? n[e] : ((1.f - step) * op[e] + step * n[e]);
+            if (!isfinite(op[e])) ++bad;
+          }
+          float* tp = theta + __ldg(tstart + t0 + c0 + u) + r * 32 + c4;
+          if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
+            *reinterpret_cast<float4*>(tp) = o;
+          } else {
+            tp[0] = o.x, tp[1] = o.y, tp[2] = o.z, tp[3] = o.w;
+          }
+        }
+        if (planes) {
+          float* d = tile + u * (32 * 33) + r * 33 + c4;
+          d[0] = o.x, d[1] = o.y, d[2] = o.z, d[3] = o.w;
+        }
+      }
+      if (!planes) continue;
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+      const int n8 = 32 * 32 / 8;
+      for (int q = lt; q < nc * 2 * n8; q += 256) {
+        const int u = q / (2 * n8), qq = q - u * 2 * n8;
+        const float* tl = tile + u * (32 * 33);
+        float v[8];
+        uint32_t off;
+        int pl;
+        if (qq < n8) {  // sum-major core row (m, j..j+7)
+          const int m = qq >> 2, j = (qq & 3) * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = tl[m * 33 + j + e];
+          off = (uint32_t)tile_off(m, j, 32) * 2u;
+          pl = 0;
+        } else {  // product-major core row (j, m..m+7)
+          const int rr = qq - n8;
+          const int j = rr >> 2, m = (rr & 3) * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = tl[(m + e) * 33 + j];
+          off = (uint32_t)tile_off(j, m, 32) * 2u;
+          pl = 2;
+        }
+        uint4 hi, lo;
+        split_pack8(v, hi, lo);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(
+                           pl == 0 ? mma + __ldg(tslab_f + t0 + c0 + u)
+                                   : mma + 2 * plane_n + __ldg(tslab_c + t0 + c0 + u)) +
+                       off;
+        *reinterpret_cast<uint4*>(dst) = hi;
+        *reinterpret_cast<uint4*>(dst + plane_n * 2) = lo;
+      }
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+    }
+    __syncthreads();  // part[] reused by the next block
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    informative += __shfl_xor_sync(0xffffffffu, informative, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((tid & 31) == 0) {
+    if (informative) atomicAdd(status, informative);
+    if (bad) atomicAdd(status + 1, bad);
+  }
+}
+
 int launch_em_tiles(const pcb_plan* p, cudaStream_t s, const float* f_params, float* theta,
                     float pseudocount, float step, int32_t* status, bool planes, int64_t blk0,
                     int64_t blk1) {
   ProfScope prof_(KC_EM, s);
   if (blk1 < 0) blk1 = p->n_em_blk;
   if (blk1 <= blk0) return PCB_OK;
+  // read per launch (tests toggle it)
+  const bool split32 = p->em_split32 && getenv("PCB_NO_EM_SPLIT32") == nullptr;
   launch_k(k_em_tiles, dim3(grid_for(blk1 - blk0, 1, 148 * 8)), dim3(EM_THREADS), 0, s, 
       blk0, blk1, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start, p->em_tile_slab_f,
       p->em_tile_slab_c, f_params, theta, p->mma, p->mma_plane, pseudocount, step,
-      planes ? 1 : 0, status);
+      planes ? 1 : 0, status, split32 ? 1 : 0);
+  if (check_launch()) return PCB_CUDA;
+  if (!split32) return PCB_OK;
+  static int attr[kMaxDev] = {};
+  if (ensure_smem((const void*)k_em_tiles32, E32_SMEM, attr)) return PCB_CUDA;
+  launch_k(k_em_tiles32, dim3(grid_for(blk1 - blk0, 1, 148)), dim3(E32_G * 256), (size_t)E32_SMEM,
+           s, blk0, blk1, p->em_km, p->em_kn, p->em_tile_off, p->em_tile_start,
+           p->em_tile_slab_f, p->em_tile_slab_c, f_params, theta, p->mma, p->mma_plane,
+           pseudocount, step, planes ? 1 : 0, status);
   return check_launch();
 }
+
+bool em_split32_block(int km, int kn, int ntiles) { return split32_blk(km, kn, ntiles); }
 
 int launch_theta_to_mma(const pcb_plan* p, cudaStream_t s, const float* theta) {
   ProfScope prof_(KC_EM, s);

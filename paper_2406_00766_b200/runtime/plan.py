@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 26
+VERSION = 27
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -1123,6 +1123,10 @@ def build_program(compiled, *, tensor_cores: bool = True):
         prog += [int(lo), int(hi), int(fz)]
     # shared-pmf groups (ordered last) updated inline by the input-flow pass
     prog += [n_shared_inline if shared_inline_ok else 0]
+    # tile blocks of more than EM_RT 32 x 32 tiles take the split EM kernel
+    # (pcb_tc.cu k_em_tiles32, EM_RT = 8)
+    ntl = np.diff(tb["blk_tile_off"])
+    prog.append(int(bool(np.any((tb["blk_km"] == 32) & (tb["blk_kn"] == 32) & (ntl > 8)))))
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,

@@ -66,3 +66,33 @@ def test_fused_parameter_flows_lean_train_step():
     want = oracle.em_step_full(c, rb.f_params, theta=theta0, pseudocount=1e-6)
     assert abs(ll - lr.sum()) <= 1e-6 * abs(lr.sum())
     assert rel_err(got, want) < RTOL
+
+
+def test_em_tile_blocks_split_kernel(monkeypatch):
+    """Tile blocks of more than 8 32 x 32 tiles (1024 hidden: 32 per block)
+    take k_em_tiles32 (four tile groups per CTA); PCB_NO_EM_SPLIT32=1 (read
+    per launch) runs them through k_em_tiles.  Both against the float64
+    oracle's EM step."""
+    import torch
+    from paper_2406_00766_b200.runtime import backward, em_update_, forward
+    from paper_2406_00766_b200.runtime.plan import device_plan
+    c = _hmm()
+    x = np.random.default_rng(3).integers(0, 50, size=(128, 6))
+    _, rb = oracle.forward(c, x)
+    oracle.backward(c, rb)
+    want = oracle.em_step_mini(c.theta, oracle.em_step_full(c, rb.f_params, pseudocount=1e-6), 0.25)
+    plan = device_plan(c)
+    saved = plan.theta.clone()
+    got = {}
+    for mode in ("split", "single"):
+        if mode == "single":
+            monkeypatch.setenv("PCB_NO_EM_SPLIT32", "1")
+        _, bufs = forward(c, x)
+        backward(c, bufs)
+        em_update_(c, bufs.f_params, pseudocount=1e-6, step_size=0.25, plan=plan)
+        torch.cuda.synchronize()
+        got[mode] = _np(plan.theta)
+        plan.theta.copy_(saved)
+        plan.refresh_mma()
+        assert rel_err(got[mode], want) < RTOL, mode
+    assert rel_err(got["split"], got["single"]) < 1e-6
