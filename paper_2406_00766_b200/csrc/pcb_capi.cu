@@ -13,7 +13,7 @@ using namespace pcb;
 namespace {
 
 constexpr int64_t kMagic = 0x50434232;  // "PCB2"
-constexpr int64_t kVersion = 27;
+constexpr int64_t kVersion = 28;
 
 struct Reader {
   const int64_t* p;
@@ -278,6 +278,8 @@ int pcb_plan_create(const int64_t* prog, int64_t prog_len, const int32_t* d_blob
   }
   P->n_shared_inline = r.get();
   P->em_split32 = (int)r.get();  // some tile block takes k_em_tiles32
+  P->sp_lo = r.get();            // f_params range stored whole by k_input_flow_shared
+  P->sp_hi = r.get();
   if (!r.ok || r.get() != kMagic) {
     delete P;
     return PCB_USAGE;
@@ -630,7 +632,17 @@ int run_backward(const pcb_plan* P, Step& S, cudaStream_t s, int B, int ldb,
     // never written: a lean step, whose EM reads only [0, theta_size), leaves
     // them alone
     const int64_t fp_n = P->fp_cover ? zero_tile(P) : S.lean ? P->theta_size : P->f_params_size;
-    if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * fp_n, s) != cudaSuccess) return PCB_CUDA;
+    // the shared-pmf rows are stored whole by their input-flow kernel (or,
+    // with EM inline, not written at all): no zero fill there
+    const int64_t sk_lo = std::max(P->sp_lo, zero_tile(P)), sk_hi = std::min(P->sp_hi, fp_n);
+    if (B > 0 && sk_lo < sk_hi && getenv("PCB_NO_FP_SKIP") == nullptr) {
+      if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * sk_lo, s) != cudaSuccess ||
+          cudaMemsetAsync(d_f_params + sk_hi, 0, sizeof(float) * (fp_n - sk_hi), s) !=
+              cudaSuccess)
+        return PCB_CUDA;
+    } else if (cudaMemsetAsync(d_f_params, 0, sizeof(float) * fp_n, s) != cudaSuccess) {
+      return PCB_CUDA;
+    }
     if (!B) return PCB_OK;
     // only rows that accumulate (several pushes) or receive none need zeros;
     // single-push rows are stored by their push

@@ -180,6 +180,7 @@ struct pcb_plan {
   // groups (em_rest) take the generic per-group pass
   int64_t n_em_blk = 0, n_em_tiles = 0, n_em_rest = 0, n_em_small = 0;  // rest: small first
   int em_split32 = 0;  // some tile block takes k_em_tiles32 (pcb_tc.cu)
+  int64_t sp_lo = 0, sp_hi = 0;  // f_params range of the shared pmfs (contiguous) or empty
   const int32_t *em_km = nullptr, *em_kn = nullptr, *em_tile_off = nullptr, *em_goff = nullptr,
                 *em_tile_start = nullptr, *em_tile_slab_f = nullptr, *em_tile_slab_c = nullptr,
                 *em_rest = nullptr,

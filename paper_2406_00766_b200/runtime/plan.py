@@ -22,7 +22,7 @@ from ..errors import UsageError
 from . import _lib
 
 MAGIC = 0x50434232
-VERSION = 27
+VERSION = 28
 TC_NMAX = 256
 INT32_MAX = np.iinfo(np.int32).max
 EM_BIG = 2048  # simplex groups at least this large get a whole CTA in the EM pass
@@ -1127,6 +1127,16 @@ def build_program(compiled, *, tensor_cores: bool = True):
     # (pcb_tc.cu k_em_tiles32, EM_RT = 8)
     ntl = np.diff(tb["blk_tile_off"])
     prog.append(int(bool(np.any((tb["blk_km"] == 32) & (tb["blk_kn"] == 32) & (ntl > 8)))))
+    # f_params range the shared-pmf input-flow kernel stores whole rows into
+    # (one CTA per pmf, plain stores): when contiguous, the backward pass's
+    # zero fill skips it
+    sp_lo = sp_hi = 0
+    if shared_pids:
+        st = np.array(sorted(shared_pids), dtype=np.int64)
+        ln = np.array([shared_pids[int(k)] for k in st], dtype=np.int64)
+        if np.all(st[1:] == st[:-1] + ln[:-1]):
+            sp_lo, sp_hi = int(st[0]), int(st[-1] + ln[-1])
+    prog += [sp_lo, sp_hi]
     prog.append(MAGIC)
     info = {"prod_flows_optional": pf_optional, "fp_cover": fp_cover,
             "leaf_alias": alias_pad is not None,
