@@ -655,8 +655,14 @@ int launch_ratio_max(const Layer& L, cudaStream_t s, int B, int ldb, const float
 // whose shift R goes to its rmax_all row.  Replaces the push's flow stores
 // plus the ratio pass's re-read of flows and values.  The block's product
 // flows are read once per slot (the slots of a block are adjacent CTAs: L2).
+// 6 resident CTAs per SM (40 registers, a small spill): each CTA's life is
+// ~3 dependent latency rounds for 48 KB, so residency sets the bandwidth
+// (HCLT-256: 1.31 ms at 4 CTAs / SM -> 1.05 ms; 5: 1.23, 7 / 8: 1.53)
+#ifndef PCB_PR_MINB
+#define PCB_PR_MINB 6
+#endif
 template <int K>
-__global__ void __launch_bounds__(RW * 32)
+__global__ void __launch_bounds__(RW * 32, PCB_PR_MINB)
     k_push_ratio(int B, int ldb, const int32_t* __restrict__ qblk,
                  const int32_t* __restrict__ prow, const int32_t* __restrict__ qbase,
                  const int32_t* __restrict__ qkind, const int32_t* __restrict__ qrrow,
