@@ -470,8 +470,13 @@ __device__ __forceinline__ float rebase(float beta, float o, float base) {
 // UNI: every row of a block takes its children's bases from row 0's base
 // rows (plan.prod_blocks_uniform), so the summed base is formed once per
 // sample and only the offsets stay in registers.
+// 4 resident CTAs per SM (64 registers): 5 / 6 spill the gathered rows
+// (HCLT-256 products 0.87 -> 0.97 / 1.25 ms)
+#ifndef PCB_PB_MINB
+#define PCB_PB_MINB 4
+#endif
 template <int PER, bool UNI>
-__global__ void __launch_bounds__(RW * 32, (UNI && PER == 4) ? 4 : 2)
+__global__ void __launch_bounds__(RW * 32, (UNI && PER == 4) ? PCB_PB_MINB : 2)
     k_prod_block(int k_n, int B, int ldb, const int32_t* __restrict__ row_off,
                  const int32_t* __restrict__ ch, const int32_t* __restrict__ cb,
                  const float* __restrict__ values, const float* __restrict__ vbase,
