@@ -1379,7 +1379,11 @@ __global__ void __launch_bounds__(IN_THREADS)
 // categories, adding the missing-flow spread, with one coalesced store per
 // pmf entry (the block owns its pmf ranges exclusively).
 constexpr int IS_THREADS = 256, IS_WARPS = IS_THREADS / 32;
+#ifdef PCB_IS_MINB
+__global__ void __launch_bounds__(IS_THREADS, PCB_IS_MINB)
+#else
 __global__ void __launch_bounds__(IS_THREADS)
+#endif
     k_input_flow_sorted(int B, int ldb, const int32_t* __restrict__ bvar,
                         const int32_t* __restrict__ bncat, const int32_t* __restrict__ bslot0,
                         const int32_t* __restrict__ bcount, const int32_t* __restrict__ bpoff,
